@@ -1,0 +1,277 @@
+/*
+ * distgrid_b200.h — the C ABI of the B200-native DistGrid per-ray train/render path.
+ *
+ * This is the drop-in boundary for the hot path of the reference C++ library
+ * (/root/reference/proj, namespace distgrid).  The reference has no FFI; its public
+ * boundary is the C++ API in proj/include/distgrid/<module>.hpp.  Each entry point below names
+ * the reference interface it replaces (file:line, paths relative to proj/).  The C++
+ * facade in include/distgrid_b200/distgrid.hpp re-exposes these under the reference
+ * names; Python tests/bench bind them with ctypes (paper_2405_04416_b200/dg.py).
+ *
+ * Conventions (mirroring the reference):
+ *  - every call returns an int status (dg_status); dg_last_error() gives a thread-local
+ *    message.  DG_EINVAL <-> std::invalid_argument, DG_ERANGE <-> std::out_of_range,
+ *    DG_EPROTO <-> std::runtime_error (protocol / missing partial), DG_ETIMEOUT <->
+ *    TransportTimeout, DG_ECUDA / DG_ENCCL for device / collective failures.
+ *  - one context per GPU; a context owns every partition p with part_rank[p] == rank.
+ *    A context is used from one host thread at a time (mirrors Worker ownership,
+ *    worker.hpp:60-63).
+ *  - gradients accumulate (+=) into context-owned sinks that dg_adam_step zeroes,
+ *    exactly as FieldGrads / AdamState in the reference (worker.cpp:524-547).
+ *  - buffers flagged DG_MEM_HOST are staged through the context; DG_MEM_DEVICE pointers
+ *    are used in place on the context's stream.
+ *
+ * No torch types cross this boundary: plain pointers, sizes and PODs only.
+ */
+#ifndef DISTGRID_B200_H
+#define DISTGRID_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_ABI_VERSION 1
+#define DG_MAX_SEGMENTS 16   /* kx + ky - 1 <= 16  (partition.cpp:254-296) */
+#define DG_MAX_PARTITIONS 64 /* kx * ky <= 64 */
+#define DG_MAX_LEVELS 16     /* grid_levels; F must be 2 on the device path */
+
+typedef enum dg_status {
+  DG_OK = 0,
+  DG_EINVAL = 1,
+  DG_ERANGE = 2,
+  DG_EPROTO = 3,
+  DG_ETIMEOUT = 4,
+  DG_ECUDA = 5,
+  DG_ENCCL = 6,
+  DG_ENOMEM = 7
+} dg_status;
+
+typedef enum dg_mem { DG_MEM_HOST = 0, DG_MEM_DEVICE = 1 } dg_mem;
+
+/*
+ * Run configuration: the RunConfig fields that define the path (config.hpp:13-78)
+ * plus the two boxes handed to split_regions (partition.hpp:83-88).
+ */
+typedef struct dg_run_config {
+  /* partition: split_regions(inner, outer, kx, ky, ground_altitude) */
+  double inner_lo[3], inner_hi[3];
+  double outer_lo[3], outer_hi[3];
+  double ground_altitude;
+  uint32_t kx, ky;
+  /* hash grids (config.hpp:24-30) */
+  uint32_t grid_levels;
+  uint32_t grid_features;
+  uint32_t base_resolution;
+  uint32_t max_resolution;
+  uint32_t fine_table_log2;
+  uint32_t coarse_table_log2;
+  uint32_t appearance_dim;
+  /* ray marching (config.hpp:33): step = longest outer axis / divisor */
+  double march_step_divisor;
+  /* occupancy (config.hpp:36-43) */
+  uint32_t occ_resolution;
+  double occ_decay;
+  uint64_t occ_warmup_steps;
+  uint64_t occ_update_interval;
+  double occ_threshold_early;
+  double occ_threshold_late;
+  uint64_t occ_threshold_switch_step;
+  double occ_threshold_scale;
+  /* training (config.hpp:46-58, train.hpp:14-18, 50-54) */
+  uint64_t seed;
+  uint64_t total_steps;
+  double lr_start, lr_end;
+  double lambda_transmittance;
+  double lambda_distortion;
+  double transmittance_clamp;
+  double adam_beta1, adam_beta2, adam_eps;
+  uint32_t wire_f32;                    /* config.hpp:21 (partials are f32 on this path) */
+  uint32_t distortion_cross_correction; /* config.hpp:56; must be 0 */
+  uint32_t occupancy_updates;           /* 1: run Worker::update_occupancy cadence */
+  uint32_t reserved;
+} dg_run_config;
+
+/* RunConfig defaults (config.hpp:13-78) with inner = outer = [0,1]^3. */
+void dg_default_config(dg_run_config* cfg);
+
+/* A batch of supervised rays (dataset.hpp:79-83: SupervisedRay), structure of arrays.
+ * Ray ids are batch indices (worker.cpp:153): ray i of this shard has global id
+ * first_ray_id + i, which keys the per-ray jitter (worker.cpp:258-262). */
+typedef struct dg_ray_batch {
+  const double* origin;     /* n x 3 */
+  const double* dir;        /* n x 3, unit */
+  const float* color_gt;    /* n x 3 (train only; may be NULL for render) */
+  const uint32_t* image_id; /* n (may be NULL: image 0) */
+  uint64_t n;
+  uint64_t first_ray_id;
+  int32_t mem;              /* dg_mem of all four arrays */
+  int32_t reserved;
+} dg_ray_batch;
+
+/* worker.hpp:153-162 StepStats (losses are sums over rays, unweighted by lambda). */
+typedef struct dg_step_stats {
+  uint64_t step;
+  double loss_rgb;
+  double loss_transmittance;
+  double loss_distortion;
+  double lr;
+  uint64_t rays;
+  uint64_t dropped_rays;
+  uint64_t bytes_sent;   /* exchange bytes (both exchanges), this rank */
+  uint64_t samples;      /* march samples shaded on this rank */
+  uint64_t items;        /* (ray, partition) segments owned by this rank */
+} dg_step_stats;
+
+/* render.hpp:38-43 MergedRender, structure of arrays. */
+typedef struct dg_merged {
+  float* rgb;           /* n x 3 */
+  float* transmittance; /* n */
+  float* depth;         /* n */
+  int32_t mem;
+  int32_t reserved;
+} dg_merged;
+
+/* One parameter array of a partition's flat state, in the order of
+ * FieldParams::parameter_arrays (field.cpp:203-208) for fine then coarse, which is the
+ * order AdamState sees in Worker::apply_updates (worker.cpp:524-547). */
+typedef struct dg_array_desc {
+  uint64_t offset; /* in floats, into the partition's flat parameter vector */
+  uint64_t size;
+  uint32_t cascade; /* 0 fine, 1 coarse */
+  uint32_t kind;    /* 0 grid level, 1 density W, 2 density b, 3 color W, 4 color b */
+  uint32_t index;   /* level or layer index */
+  uint32_t reserved;
+} dg_array_desc;
+
+typedef struct dg_ctx dg_ctx;
+
+const char* dg_last_error(void);
+int dg_abi_version(void);
+
+/* ---- context (replaces Worker construction, worker.cpp:178-206; DistributedRun ctor
+ * worker.cpp:630-690).  Partition p lives on rank p % world.  device < 0: use the
+ * current device.  Parameters start zeroed: call dg_init_params_reference or
+ * dg_set_params.  Occupancy starts fill_occupied (worker.cpp:199-200). ---- */
+int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_ctx** out);
+int dg_ctx_destroy(dg_ctx* ctx);
+int dg_partition_count(const dg_ctx* ctx, uint32_t* n_total, uint32_t* n_local);
+int dg_partition_rank(const dg_ctx* ctx, uint32_t partition, int* rank);
+int dg_march_step(const dg_ctx* ctx, double* step); /* worker.cpp:923-925 */
+/* region boxes after split_regions (partition.cpp:206-252) */
+int dg_region_boxes(const dg_ctx* ctx, uint32_t partition, double fine_lo[3], double fine_hi[3],
+                    double coarse_lo[3], double coarse_hi[3]);
+/* level shapes (grid.cpp:65-73), mapping modes and rows (grid.cpp:90-105) */
+int dg_grid_levels(const dg_ctx* ctx, uint32_t partition, uint32_t cascade, uint32_t* shapes /*L x 3*/,
+                   uint32_t* modes /*L*/, uint64_t* rows /*L*/);
+
+/* ---- state: injection for parity, extraction for checkpoints ---- */
+int dg_param_count(const dg_ctx* ctx, uint32_t partition, uint64_t* n_floats);
+int dg_param_layout(const dg_ctx* ctx, uint32_t partition, dg_array_desc* arrays,
+                    uint32_t capacity, uint32_t* n_arrays);
+int dg_set_params(dg_ctx* ctx, uint32_t partition, const float* host_params);
+int dg_get_params(dg_ctx* ctx, uint32_t partition, float* host_params);
+int dg_get_grads(dg_ctx* ctx, uint32_t partition, float* host_grads);
+int dg_zero_grads(dg_ctx* ctx);
+int dg_set_adam(dg_ctx* ctx, uint32_t partition, const float* m, const float* v, uint64_t step_count);
+int dg_get_adam(dg_ctx* ctx, uint32_t partition, float* m, float* v, uint64_t* step_count);
+/* Worker::step_ (worker.hpp:144): the lr schedule index of the next step. */
+int dg_set_step(dg_ctx* ctx, uint64_t step);
+int dg_get_step(const dg_ctx* ctx, uint64_t* step);
+/* Reference-exact initialisation (worker.cpp:186-190, grid.cpp:90-105, mlp.cpp:38-53):
+ * mt19937_64 streams seeded with counter_hash(seed, 0xf1e1d|0xc0a45e, region), rounded
+ * to fp32.  Host-side, once per partition (not on the per-step path). */
+int dg_init_params_reference(dg_ctx* ctx, uint32_t partition);
+/* Fast device-side random init for throughput runs: tables U[-1e-4,1e-4], Xavier MLPs,
+ * counter-hash stream (not the reference's mt19937 stream). */
+int dg_init_params_fast(dg_ctx* ctx, uint32_t partition, uint64_t seed);
+/* Occupancy bitfields (grid.hpp:99-141), one u8 per cell, row-major ix-fastest. */
+int dg_occupancy_shape(const dg_ctx* ctx, uint32_t partition, uint32_t cascade, uint32_t shape[3]);
+int dg_set_occupancy(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const uint8_t* bits);
+int dg_get_occupancy(dg_ctx* ctx, uint32_t partition, uint32_t cascade, uint8_t* bits);
+/* Appearance rows (field.hpp:21-29 AppearanceTable); image ids must be < 2^20. */
+int dg_set_appearance(dg_ctx* ctx, const uint32_t* image_ids, const float* rows, uint32_t n_images);
+
+/* ---- composed path ---- */
+/* DistributedRun::training_step (worker.cpp:730-755) + Worker::handle_training_batch
+ * (worker.cpp:251-401) for this rank's partitions.  With world > 1 every rank passes its
+ * home shard (contiguous global ray ids) and the exchanges run over the communicator. */
+int dg_train_step(dg_ctx* ctx, const dg_ray_batch* batch, uint64_t step, dg_step_stats* stats);
+/* DistributedRun::evaluate_rays (worker.cpp:757-834): jitter off, partials merged at the
+ * home rank in schedule order, depth carried.  appearance: appearance_dim floats (host). */
+int dg_render(dg_ctx* ctx, const dg_ray_batch* batch, const float* appearance, dg_merged* out);
+
+/* ---- communicator (replaces transport.hpp:30-98) ---- */
+#define DG_NCCL_UNIQUE_ID_BYTES 128
+int dg_comm_unique_id(uint8_t id[DG_NCCL_UNIQUE_ID_BYTES]);
+int dg_comm_init_nccl(dg_ctx* ctx, const uint8_t id[DG_NCCL_UNIQUE_ID_BYTES]);
+/* Host-staged exchange: the context copies send blocks to host and calls back
+ * (used for multi-process tests over gloo; never the production path). */
+typedef int (*dg_alltoallv_fn)(void* user, const void* send, const uint64_t* send_bytes,
+                                void* recv, const uint64_t* recv_bytes);
+int dg_comm_init_host(dg_ctx* ctx, dg_alltoallv_fn fn, void* user);
+
+/* ---- stage entry points (per-stage parity + the facade's batched overloads) ---- */
+/* segment_ray over a batch (partition.cpp:254-296, geometry.cpp:7-28): nseg per ray,
+ * region/t_enter/t_exit in n x DG_MAX_SEGMENTS slots.  Bit-exact fp64. */
+int dg_segment_rays(dg_ctx* ctx, const double* origin, const double* dir, uint64_t n,
+                    uint8_t* nseg, uint16_t* region, double* t_enter, double* t_exit, int32_t mem);
+/* cascade_march (worker.cpp:79-110) for n (ray, segment) pairs owned by `partition`.
+ * Pass t/delta/cascade == NULL to get counts only; otherwise offsets (exclusive scan of
+ * counts) place each ray's samples.  Bit-exact fp64. */
+int dg_cascade_march(dg_ctx* ctx, uint32_t partition, const double* origin, const double* dir,
+                     const double* t0, const double* t1, const uint64_t* ray_id, uint64_t n,
+                     int32_t jitter, uint64_t batch_id, uint32_t* counts, const uint64_t* offsets,
+                     double* t, double* delta, uint8_t* cascade, int32_t mem);
+/* HashGrid::encode over n normalised points (grid.cpp:107-130).  rows (optional):
+ * n x L x 8 table rows (UINT32_MAX for skipped zero-weight corners), bit-exact. */
+int dg_encode(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const double* points, uint64_t n,
+              float* features, uint32_t* rows, int32_t mem);
+/* HashGrid::encode_backward (grid.cpp:132-157): accumulates into the grad sink. */
+int dg_encode_backward(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const double* points,
+                       const float* upstream, uint64_t n, int32_t mem);
+/* query_density + query_color (field.cpp:230-288) on normalised points. */
+int dg_field_forward(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const double* points,
+                     const float* dirs, const float* appearance, uint64_t n, float* sigma,
+                     float* rgb, int32_t mem);
+/* field_backward (field.cpp:290-327): accumulates into the grad sink. */
+int dg_field_backward(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const double* points,
+                      const float* dirs, const float* appearance, const float* sigma_grad,
+                      const float* rgb_grad, uint64_t n, int32_t mem);
+/* Worker::apply_updates (worker.cpp:524-547): dense Adam over every local parameter with
+ * lr = LrSchedule::at(step_) (train.cpp:77-80, 91-115), then zero the grads. */
+int dg_adam_step(dg_ctx* ctx, double lr);
+double dg_lr_at(const dg_run_config* cfg, uint64_t step);
+
+/* ---- introspection of the last dg_train_step / dg_render on this rank ---- */
+typedef struct dg_item_view {
+  uint64_t n_items;       /* (ray, partition) segments of this partition */
+  uint64_t n_fine;        /* fine samples */
+  uint64_t n_coarse;      /* coarse samples */
+} dg_item_view;
+int dg_last_items(dg_ctx* ctx, uint32_t partition, dg_item_view* view);
+/* per item: global ray id, my schedule order, t_enter/t_exit, sample count */
+int dg_last_item_data(dg_ctx* ctx, uint32_t partition, uint64_t* ray_id, uint8_t* order,
+                      double* t_enter, double* t_exit, uint32_t* n_samples);
+/* per item samples in t order (concatenated in item order): t, delta, cascade */
+int dg_last_samples(dg_ctx* ctx, uint32_t partition, double* t, double* delta, uint8_t* cascade);
+/* per item own partial (rgb, T) as computed by the composite kernel */
+int dg_last_partials(dg_ctx* ctx, uint32_t partition, float* rgb, float* transmittance);
+/* launches of this library's kernels since the context was created */
+int dg_kernel_launches(const dg_ctx* ctx, uint64_t* n);
+/* per-stage device time of the last step (ms), measured with events on the ctx stream */
+typedef struct dg_stage_times {
+  float segment, march, encode_fwd, mlp_fwd, composite, exchange, merge_bwd, mlp_bwd, encode_bwd,
+      adam, total;
+  float reserved[5];
+} dg_stage_times;
+int dg_enable_stage_timing(dg_ctx* ctx, int enable);
+int dg_last_stage_times(dg_ctx* ctx, dg_stage_times* t);
+int dg_synchronize(dg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DISTGRID_B200_H */

@@ -1,0 +1,371 @@
+"""TEST INFRASTRUCTURE: ctypes bindings of the oracle libraries.
+
+  Oracle      — oracle/build/liboracle.so, the C restatement (dg_oracle.c).
+  Reference   — oracle/_ref/libdistgrid_ref.so, the unmodified reference library built from
+                /root/reference sources + ref_harness.cpp.  Present only where it was built.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference legs import
+this module.  The product path (paper_2405_04416_b200) never does.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+from paper_2405_04416_b200.abi import DG_MAX_SEGMENTS, RunConfig
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "build", "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libdistgrid_ref.so")
+
+P = C.c_void_p
+U8 = np.uint8
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def build_oracle():
+    import subprocess
+    subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+
+
+_oracle = None
+_ref = None
+
+
+def oracle_lib():
+    global _oracle
+    if _oracle is None:
+        if not os.path.exists(ORACLE_SO):
+            build_oracle()
+        lib = C.CDLL(ORACLE_SO)
+        lib.or_run_create.restype = P
+        lib.or_run_create.argtypes = [C.POINTER(RunConfig), C.c_uint32, P]
+        lib.or_run_destroy.argtypes = [P]
+        for name in ("or_run_params", "or_run_grads", "or_run_adam_m", "or_run_adam_v",
+                     "or_run_occ_density"):
+            getattr(lib, name).restype = C.POINTER(C.c_double)
+        lib.or_run_params.argtypes = [P, C.c_uint32]
+        lib.or_run_grads.argtypes = [P, C.c_uint32]
+        lib.or_run_adam_m.argtypes = [P, C.c_uint32]
+        lib.or_run_adam_v.argtypes = [P, C.c_uint32]
+        lib.or_run_occ_density.argtypes = [P, C.c_uint32, C.c_uint32]
+        lib.or_run_adam_t.restype = C.POINTER(C.c_uint64)
+        lib.or_run_adam_t.argtypes = [P, C.c_uint32]
+        lib.or_run_worker_step.restype = C.POINTER(C.c_uint64)
+        lib.or_run_worker_step.argtypes = [P, C.c_uint32]
+        lib.or_run_occ_bits.restype = C.POINTER(C.c_uint8)
+        lib.or_run_occ_bits.argtypes = [P, C.c_uint32, C.c_uint32]
+        lib.or_run_set_occupancy.argtypes = [P, C.c_uint32, C.c_uint32, P]
+        lib.or_run_train_step.argtypes = [P, P, P, P, P, C.c_uint64, C.c_uint64, P]
+        lib.or_run_eval_rays.argtypes = [P, P, P, C.c_uint64, P, P, P, P]
+        lib.or_last_error.restype = C.c_char_p
+        lib.or_run_model.restype = P
+        lib.or_segment_ray.argtypes = [P, P, P, P, P, P]
+        lib.or_counter_uniform.restype = C.c_double
+        lib.or_counter_uniform.argtypes = [C.c_uint64] * 4
+        lib.or_counter_hash.restype = C.c_uint64
+        lib.or_counter_hash.argtypes = [C.c_uint64] * 4
+        lib.or_lr_at.restype = C.c_double
+        lib.or_lr_at.argtypes = [C.POINTER(RunConfig), C.c_uint64]
+        lib.or_level_resolution.restype = C.c_uint32
+        lib.or_level_resolution.argtypes = [C.c_uint32] * 4
+        _oracle = lib
+    return _oracle
+
+
+def ref_available():
+    return os.path.exists(REF_SO)
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError("reference build missing: " + REF_SO)
+        lib = C.CDLL(REF_SO)
+        lib.refh_create.restype = P
+        lib.refh_create.argtypes = [C.POINTER(RunConfig), C.c_uint32, P]
+        lib.refh_destroy.argtypes = [P]
+        lib.refh_param_count.restype = C.c_uint64
+        lib.refh_param_count.argtypes = [P, C.c_uint32]
+        lib.refh_get_params.argtypes = [P, C.c_uint32, P]
+        lib.refh_set_params.argtypes = [P, C.c_uint32, P]
+        lib.refh_get_adam.argtypes = [P, C.c_uint32, P, P, P, P]
+        lib.refh_set_adam.argtypes = [P, C.c_uint32, P, P, C.c_uint64, C.c_uint64]
+        lib.refh_set_occupancy.argtypes = [P, C.c_uint32, C.c_uint32, P]
+        lib.refh_get_occupancy.argtypes = [P, C.c_uint32, C.c_uint32, P, P]
+        lib.refh_train_step.argtypes = [P, P, P, P, P, C.c_uint64, C.c_uint64, P]
+        lib.refh_eval_rays.argtypes = [P, P, P, C.c_uint64, P, P, P, P]
+        lib.refh_segment_rays.argtypes = [C.POINTER(RunConfig), P, P, C.c_uint64, P, P, P, P]
+        lib.refh_cascade_march.argtypes = [P, C.c_uint32, P, P, P, P, P, C.c_uint64, C.c_int,
+                                           C.c_uint64, P, P, P, P, C.c_uint64]
+        lib.refh_encode.argtypes = [P, C.c_uint32, C.c_uint32, P, C.c_uint64, P, P]
+        lib.refh_field_forward.argtypes = [P, C.c_uint32, C.c_uint32, P, P, P, C.c_uint64, P, P]
+        lib.refh_field_backward.argtypes = [P, C.c_uint32, C.c_uint32, P, P, P, P, P, C.c_uint64]
+        lib.refh_stage_grads.argtypes = [P, C.c_uint32, P, C.c_int]
+        lib.refh_march_step.restype = C.c_double
+        lib.refh_march_step.argtypes = [P]
+        lib.refh_default_config.argtypes = [C.POINTER(RunConfig)]
+        lib.refh_last_error.restype = C.c_char_p
+        lib.refh_time_replicas.restype = C.c_double
+        lib.refh_time_replicas.argtypes = [P, C.c_uint32, P, P, P, C.c_uint64, C.c_uint64,
+                                           C.c_uint64]
+        _ref = lib
+    return _ref
+
+
+class _RunBase:
+    """Common numpy-facing API of the oracle run and the reference run."""
+
+    def __init__(self, cfg, app_rows):
+        self.cfg = cfg.copy()
+        self.app = np.ascontiguousarray(np.asarray(app_rows, dtype=np.float64))
+        self.n_images = self.app.shape[0]
+
+
+class OracleRun(_RunBase):
+    """or_run: single-threaded C restatement of DistributedRun (worker.cpp:630-834)."""
+
+    def __init__(self, cfg, app_rows):
+        super().__init__(cfg, app_rows)
+        self.lib = oracle_lib()
+        self.h = self.lib.or_run_create(C.byref(self.cfg), self.n_images, _ptr(self.app))
+        if not self.h:
+            raise RuntimeError(self.lib.or_last_error().decode())
+        self.P = self.cfg.kx * self.cfg.ky
+        self._nparams = [self._count(g) for g in range(self.P)]
+
+    def _count(self, g):
+        # parameter count from the reference layout formula (shared with the GPU layout)
+        from paper_2405_04416_b200.layout import partition_param_count
+        return partition_param_count(self.cfg, g)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.or_run_destroy(self.h)
+            self.h = None
+
+    def _arr(self, ptr, n):
+        return np.ctypeslib.as_array(ptr, shape=(n,))
+
+    def params(self, g):
+        return self._arr(self.lib.or_run_params(self.h, g), self._nparams[g])
+
+    def grads(self, g):
+        return self._arr(self.lib.or_run_grads(self.h, g), self._nparams[g])
+
+    def adam(self, g):
+        m = self._arr(self.lib.or_run_adam_m(self.h, g), self._nparams[g])
+        v = self._arr(self.lib.or_run_adam_v(self.h, g), self._nparams[g])
+        return m, v, self.lib.or_run_adam_t(self.h, g)[0], self.lib.or_run_worker_step(self.h, g)[0]
+
+    def set_params(self, g, p):
+        self.params(g)[:] = p
+
+    def set_adam(self, g, m, v, t, wstep):
+        mm, vv, _, _ = self.adam(g)
+        mm[:] = m
+        vv[:] = v
+        self.lib.or_run_adam_t(self.h, g)[0] = t
+        self.lib.or_run_worker_step(self.h, g)[0] = wstep
+
+    def set_occupancy(self, g, cascade, bits):
+        bits = np.ascontiguousarray(bits, dtype=U8)
+        self.lib.or_run_set_occupancy(self.h, g, cascade, _ptr(bits))
+
+    def occupancy(self, g, cascade, ncells):
+        return self._arr(self.lib.or_run_occ_bits(self.h, g, cascade), ncells).copy()
+
+    def train_step(self, o, d, gt, img, step):
+        stats = np.zeros(8)
+        gt64 = np.ascontiguousarray(gt, dtype=np.float64)
+        img = np.ascontiguousarray(img, dtype=np.uint32)
+        rc = self.lib.or_run_train_step(self.h, _ptr(o), _ptr(d), _ptr(gt64), _ptr(img), len(o),
+                                        step, _ptr(stats))
+        if rc != 0:
+            raise RuntimeError(self.lib.or_last_error().decode())
+        return dict(loss_rgb=stats[0], loss_transmittance=stats[1], loss_distortion=stats[2],
+                    lr=stats[3], rays=int(stats[4]), dropped_rays=int(stats[5]))
+
+    def eval_rays(self, o, d, app_vec):
+        n = len(o)
+        rgb = np.zeros((n, 3))
+        T = np.zeros(n)
+        depth = np.zeros(n)
+        app_vec = np.ascontiguousarray(app_vec, dtype=np.float64)
+        rc = self.lib.or_run_eval_rays(self.h, _ptr(o), _ptr(d), n, _ptr(app_vec), _ptr(rgb),
+                                       _ptr(T), _ptr(depth))
+        if rc != 0:
+            raise RuntimeError(self.lib.or_last_error().decode())
+        return rgb, T, depth
+
+
+class RefRun(_RunBase):
+    """The reference DistributedRun itself, through oracle/ref_harness.cpp."""
+
+    def __init__(self, cfg, app_rows):
+        super().__init__(cfg, app_rows)
+        self.lib = ref_lib()
+        self.h = self.lib.refh_create(C.byref(self.cfg), self.n_images, _ptr(self.app))
+        if not self.h:
+            raise RuntimeError(self.lib.refh_last_error().decode())
+        self.P = self.cfg.kx * self.cfg.ky
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.refh_destroy(self.h)
+            self.h = None
+
+    def _check(self, rc):
+        if rc != 0:
+            raise RuntimeError(self.lib.refh_last_error().decode())
+
+    def nparams(self, g):
+        return int(self.lib.refh_param_count(self.h, g))
+
+    def params(self, g):
+        out = np.zeros(self.nparams(g))
+        self.lib.refh_get_params(self.h, g, _ptr(out))
+        return out
+
+    def set_params(self, g, p):
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        self.lib.refh_set_params(self.h, g, _ptr(p))
+
+    def adam(self, g):
+        n = self.nparams(g)
+        m = np.zeros(n)
+        v = np.zeros(n)
+        t = C.c_uint64()
+        ws = C.c_uint64()
+        self.lib.refh_get_adam(self.h, g, _ptr(m), _ptr(v), C.byref(t), C.byref(ws))
+        return m, v, t.value, ws.value
+
+    def set_adam(self, g, m, v, t, wstep):
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        self._check(self.lib.refh_set_adam(self.h, g, _ptr(m), _ptr(v), t, wstep))
+
+    def set_occupancy(self, g, cascade, bits):
+        bits = np.ascontiguousarray(bits, dtype=U8)
+        self.lib.refh_set_occupancy(self.h, g, cascade, _ptr(bits))
+
+    def occupancy(self, g, cascade, ncells):
+        bits = np.zeros(ncells, dtype=U8)
+        self.lib.refh_get_occupancy(self.h, g, cascade, _ptr(bits), None)
+        return bits
+
+    def train_step(self, o, d, gt, img, step):
+        stats = np.zeros(8)
+        gt64 = np.ascontiguousarray(gt, dtype=np.float64)
+        img = np.ascontiguousarray(img, dtype=np.uint32)
+        self._check(self.lib.refh_train_step(self.h, _ptr(o), _ptr(d), _ptr(gt64), _ptr(img),
+                                             len(o), step, _ptr(stats)))
+        return dict(loss_rgb=stats[0], loss_transmittance=stats[1], loss_distortion=stats[2],
+                    lr=stats[3], rays=int(stats[4]), dropped_rays=int(stats[5]))
+
+    def eval_rays(self, o, d, app_vec):
+        n = len(o)
+        rgb = np.zeros((n, 3))
+        T = np.zeros(n)
+        depth = np.zeros(n)
+        app_vec = np.ascontiguousarray(app_vec, dtype=np.float64)
+        self._check(self.lib.refh_eval_rays(self.h, _ptr(o), _ptr(d), n, _ptr(app_vec), _ptr(rgb),
+                                            _ptr(T), _ptr(depth)))
+        return rgb, T, depth
+
+    # ---- stage functions ----
+    def cascade_march(self, g, o, d, t0, t1, ray_id, jitter, batch_id, capacity=None):
+        n = len(o)
+        cap = capacity or int(n * 4096)
+        counts = np.zeros(n, dtype=np.uint32)
+        t = np.zeros(cap)
+        delta = np.zeros(cap)
+        casc = np.zeros(cap, dtype=U8)
+        ray_id = np.ascontiguousarray(ray_id, dtype=np.uint64)
+        self._check(self.lib.refh_cascade_march(self.h, g, _ptr(o), _ptr(d), _ptr(t0), _ptr(t1),
+                                                _ptr(ray_id), n, int(jitter), batch_id,
+                                                _ptr(counts), _ptr(t), _ptr(delta), _ptr(casc),
+                                                cap))
+        tot = int(counts.sum())
+        return counts, t[:tot], delta[:tot], casc[:tot]
+
+    def encode(self, g, cascade, pts):
+        n = len(pts)
+        L, F = self.cfg.grid_levels, self.cfg.grid_features
+        out = np.zeros((n, L * F))
+        rows = np.zeros((n, L, 8), dtype=np.uint32)
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        self._check(self.lib.refh_encode(self.h, g, cascade, _ptr(pts), n, _ptr(out), _ptr(rows)))
+        return out, rows
+
+    def field_forward(self, g, cascade, pts, dirs, app):
+        n = len(pts)
+        sigma = np.zeros(n)
+        rgb = np.zeros((n, 3))
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        dirs = np.ascontiguousarray(dirs, dtype=np.float64)
+        app = np.ascontiguousarray(app, dtype=np.float64)
+        self._check(self.lib.refh_field_forward(self.h, g, cascade, _ptr(pts), _ptr(dirs),
+                                                _ptr(app), n, _ptr(sigma), _ptr(rgb)))
+        return sigma, rgb
+
+    def field_backward(self, g, cascade, pts, dirs, app, dsig, drgb):
+        n = len(pts)
+        args = [np.ascontiguousarray(x, dtype=np.float64) for x in (pts, dirs, app, dsig, drgb)]
+        self._check(self.lib.refh_field_backward(self.h, g, cascade, *[_ptr(a) for a in args], n))
+
+    def stage_grads(self, g, zero=True):
+        out = np.zeros(self.nparams(g))
+        self.lib.refh_stage_grads(self.h, g, _ptr(out), int(zero))
+        return out
+
+
+def ref_segment_rays(cfg, o, d):
+    lib = ref_lib()
+    n = len(o)
+    nseg = np.zeros(n, dtype=U8)
+    region = np.zeros((n, DG_MAX_SEGMENTS), dtype=np.uint16)
+    te = np.zeros((n, DG_MAX_SEGMENTS))
+    tx = np.zeros((n, DG_MAX_SEGMENTS))
+    rc = lib.refh_segment_rays(C.byref(cfg), _ptr(o), _ptr(d), n, _ptr(nseg), _ptr(region),
+                               _ptr(te), _ptr(tx))
+    if rc != 0:
+        raise RuntimeError(lib.refh_last_error().decode())
+    return nseg, region, te, tx
+
+
+def oracle_segment_rays(cfg, o, d):
+    """or_segment_ray over a batch (partition.cpp:254-296 restated)."""
+    lib = oracle_lib()
+    model = ModelBuffer(cfg)
+    n = len(o)
+    nseg = np.zeros(n, dtype=U8)
+    region = np.zeros((n, DG_MAX_SEGMENTS), dtype=np.uint32)
+    te = np.zeros((n, DG_MAX_SEGMENTS))
+    tx = np.zeros((n, DG_MAX_SEGMENTS))
+    for i in range(n):
+        k = lib.or_segment_ray(model.ptr, _ptr(o[i]), _ptr(d[i]),
+                               region[i].ctypes.data_as(P), te[i].ctypes.data_as(P),
+                               tx[i].ctypes.data_as(P))
+        nseg[i] = k
+    return nseg, region.astype(np.uint16), te, tx
+
+
+class ModelBuffer:
+    """An or_model initialised for cfg (opaque, sized generously)."""
+
+    SIZE = 1 << 20
+
+    def __init__(self, cfg):
+        lib = oracle_lib()
+        self.buf = C.create_string_buffer(self.SIZE)
+        self.cfg = cfg.copy()
+        lib.or_model_init.argtypes = [P, C.POINTER(RunConfig)]
+        rc = lib.or_model_init(C.cast(self.buf, P), C.byref(self.cfg))
+        if rc != 0:
+            raise RuntimeError(lib.or_last_error().decode())
+        self.ptr = C.cast(self.buf, P)
