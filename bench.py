@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py — training rays/s (and render rays/s, encode GB/s) of the B200 DistGrid path.
+
+Contract (see the task statement): `python bench.py --gpus N --steps K --warmup W` runs the
+training step on N GPUs of one node (torchrun for N > 1, one rank per GPU, one partition per
+GPU), times exactly K steps after W warm-up steps with CUDA events on the step stream,
+bracketed by barrier + synchronize, max over ranks, and rank 0 prints ONE JSON line.
+
+Workload (SURVEY §8d weak-scaling point of C4): G = N partitions in a kx x ky tiling of unit
+tiles (1x1, 2x1, 2x2, 4x2), hash grid L=16 F=2 T=2^24 per partition, N0=16, Nmax=2048,
+131,072 rays per GPU from the balanced reflected-drift generator, march step 4/416
+(~128 samples/ray), inner == outer box, occupancy all occupied, random-init parameters.
+A step = DistributedRun::training_step over the whole batch: segmentation, dispatch,
+march, encode, MLP, composite, partial exchange, merge + losses + backward, dense Adam.
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref, the
+unmodified reference library) on this host, rank 0 only.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training rays/sec and render rays/sec at 1/2/4/8 B200; encode GB/s vs HBM/L2 peak"
+ENCODE_BYTES_PER_SAMPLE = 16 * 8 * 2 * 4      # L x 8 corners x F x fp32
+MLP_FLOP_TRAIN = 62208                          # fwd + bwd per sample
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops_sustained"]), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_reference(cfg, o, d, gt, rays, steps, warmup):
+    """The unmodified reference DistributedRun (oracle/_ref) on this host: each step is a
+    bounded sample of `rays` rays of the same workload (its K=1 worker thread + driver)."""
+    from oracle.bindings import RefRun, ref_available
+    from paper_2405_04416_b200 import workloads
+    if not ref_available():
+        return None, "oracle/_ref not built"
+    app = workloads.appearance_rows(cfg.appearance_dim, 1)
+    t0 = time.perf_counter()
+    run = RefRun(cfg, app)
+    init_s = time.perf_counter() - t0
+    img = np.zeros(rays, dtype=np.uint32)
+    times = []
+    for s in range(warmup + steps):
+        lo = (s * rays) % max(1, len(o) - rays)
+        a = time.perf_counter()
+        run.train_step(o[lo:lo + rays], d[lo:lo + rays], gt[lo:lo + rays].astype(np.float64), img, s)
+        if s >= warmup:
+            times.append(time.perf_counter() - a)
+    del run
+    sec = float(np.sum(times))
+    return {"value": rays * len(times) / sec, "unit": "rays/s", "cores": 1, "kind": "reference",
+            "sample": f"{len(times)} x DistributedRun::training_step on {rays} rays of the bench "
+                      f"workload (K=1 worker thread; reference init {init_s:.1f}s excluded)",
+            "ms_per_step": 1000 * sec / len(times)}, None
+
+
+def run_reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    from paper_2405_04416_b200 import workloads
+    wl = workloads.weak(1, rays_per_gpu=args.rays_per_gpu, table_log2=args.table_log2)
+    o, d, gt, _ = workloads.make_rays(wl.cfg, 4096, wl.generator, seed=1)
+    res, why = cpu_reference(wl.cfg, o, d, gt, args.ref_rays, args.steps, min(args.warmup, 1))
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": why}))
+        return 0
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "rays/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name + " (CPU sample)", "rays_per_step": args.ref_rays,
+                       "table_log2": args.table_log2, "partitions": 1},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": "rays/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rays-per-gpu", type=int, default=131072)
+    ap.add_argument("--table-log2", type=int, default=24)
+    ap.add_argument("--render-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-rays", type=int, default=512)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_04416_b200 import abi, dg, workloads
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
+    wl = workloads.weak(world, rays_per_gpu=args.rays_per_gpu, table_log2=args.table_log2)
+    cfg = wl.cfg
+    B = wl.n_rays
+    shard = B // world
+    lo, hi = rank * shard, (rank + 1) * shard
+    NB = 1 if args.profile else 3  # distinct batches cycled over the steps
+    batches_host = []
+    for k in range(NB):
+        o, d, gt, img = workloads.make_rays(cfg, B, wl.generator, seed=1 + k)
+        batches_host.append((o[lo:hi], d[lo:hi], gt[lo:hi], img[lo:hi]))
+
+    ctx = dg.Context(cfg, device=local, rank=rank, world=world)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.tensor(list(dg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ctx.comm_init_nccl(bytes(uid.cpu().tolist()))
+    for g in ctx.local:
+        ctx.init_fast(g, seed=1)
+    ctx.set_appearance(workloads.appearance_rows(cfg.appearance_dim, 1))
+
+    # device-resident inputs (value) ---------------------------------------------
+    dev = []
+    for (o, d, gt, img) in batches_host:
+        t = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (o, d, gt, img.astype(np.int32))]
+        b = abi.RayBatch()
+        b.origin, b.dir, b.color_gt, b.image_id = (t[0].data_ptr(), t[1].data_ptr(),
+                                                   t[2].data_ptr(), t[3].data_ptr())
+        b.n, b.first_ray_id, b.mem = len(o), lo, abi.DG_MEM_DEVICE
+        dev.append((b, t))
+    sptr = C.c_void_p()
+    dg.lib().dg_get_stream(ctx.h, C.byref(sptr))
+    stream = torch.cuda.ExternalStream(sptr.value)
+    stats = abi.StepStats()
+
+    def step(i, batches):
+        rc = ctx.train_step_raw(batches[i % len(batches)][0], i, stats)
+        if rc != 0:
+            raise dg.DGError(rc, dg.lib().dg_last_error().decode())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, n, first):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(n):
+            fn(first + i)
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for i in range(args.warmup):
+        step(i, dev)
+    launches0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        ms = timed(lambda i: step(i, dev), args.steps, args.warmup)
+    launches = ctx.kernel_launches() - launches0
+    ms_per_step = ms / args.steps
+    value = B / (ms_per_step / 1000.0)
+    samples_rank = int(stats.samples)
+    items_rank = int(stats.items)
+    bytes_sent = int(stats.bytes_sent)
+
+    # per-stage device times of one more step (events on the step stream)
+    ctx.enable_stage_timing(True)
+    step(args.warmup + args.steps, dev)
+    st = ctx.stage_times()
+    ctx.enable_stage_timing(False)
+
+    line = None
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "ms_per_step": ms_per_step, "stages_ms": st}))
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # render throughput (evaluate_rays through the same kernels) ------------------
+    m = abi.Merged()
+    out = [torch.empty(x, device="cuda") for x in ((shard, 3), (shard,), (shard,))]
+    m.rgb, m.transmittance, m.depth, m.mem = (out[0].data_ptr(), out[1].data_ptr(),
+                                               out[2].data_ptr(), abi.DG_MEM_DEVICE)
+    app = np.ascontiguousarray(workloads.appearance_rows(cfg.appearance_dim, 1)[0], dtype=np.float32)
+
+    def render(i):
+        rc = ctx.render_raw(dev[i % len(dev)][0], app, m)
+        if rc != 0:
+            raise dg.DGError(rc, dg.lib().dg_last_error().decode())
+
+    render(0)
+    rms = timed(render, args.render_steps, 0) / args.render_steps
+    render_value = B / (rms / 1000.0)
+
+    # end-to-end through the C ABI with pinned host buffers -------------------------
+    e2e = None
+    if not args.no_e2e:
+        pinned = []
+        for (o, d, gt, img) in batches_host:
+            t = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (o, d, gt, img.astype(np.int32))]
+            b = abi.RayBatch()
+            b.origin, b.dir, b.color_gt, b.image_id = (t[0].data_ptr(), t[1].data_ptr(),
+                                                       t[2].data_ptr(), t[3].data_ptr())
+            b.n, b.first_ray_id, b.mem = len(o), lo, abi.DG_MEM_HOST
+            pinned.append((b, t))
+        step(0, pinned)
+        ems = timed(lambda i: step(i, pinned), args.steps, args.warmup + args.steps + 1)
+        e2e = {"value": B / (ems / args.steps / 1000.0), "unit": "rays/s",
+               "h2d_bytes_per_step": int(stats.h2d_bytes), "d2h_bytes_per_step": int(stats.d2h_bytes),
+               "ms_per_step": ems / args.steps}
+
+    # roofline of the dominant kernel + the encode kernels ----------------------------
+    hbm, tensor_peak, peak_kind = peaks()
+    enc_bytes = samples_rank * ENCODE_BYTES_PER_SAMPLE
+    stage_ms = {k: v for k, v in st.items() if k != "total"}
+    dominant = max(stage_ms, key=stage_ms.get)
+    enc_fwd_gbs = enc_bytes / (st["encode_fwd"] / 1e3) / 1e9 if st["encode_fwd"] > 0 else 0.0
+    enc_bwd_gbs = 2 * enc_bytes / (st["encode_bwd"] / 1e3) / 1e9 if st["encode_bwd"] > 0 else 0.0
+    mlp_tflops = samples_rank * MLP_FLOP_TRAIN / ((st["mlp_fwd"] + st["mlp_bwd"]) / 1e3) / 1e12
+    if dominant in ("mlp_fwd", "mlp_bwd"):
+        roof = {"kernel": "mlp_fwd+mlp_bwd (FFMA fp32)", "bound": "tensor", "achieved": mlp_tflops,
+                "peak": tensor_peak, "unit": "TFLOP/s", "frac": mlp_tflops / tensor_peak,
+                "traffic": None,
+                "note": f"{MLP_FLOP_TRAIN} FLOP/sample x {samples_rank} samples; peak = {peak_kind} "
+                        f"sustained bf16 (the kernel runs on the fp32 FMA pipe)"}
+    else:
+        ach = {"encode_fwd": enc_fwd_gbs, "encode_bwd": enc_bwd_gbs}.get(dominant, enc_fwd_gbs)
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": None}
+    roof["stage_ms"] = st
+    roofline_encode = {"encode_fwd": {"achieved": enc_fwd_gbs, "peak": hbm, "unit": "GB/s",
+                                      "frac": enc_fwd_gbs / hbm,
+                                      "bytes": f"{ENCODE_BYTES_PER_SAMPLE} B/sample x {samples_rank}"},
+                       "encode_bwd": {"achieved": enc_bwd_gbs, "peak": hbm, "unit": "GB/s",
+                                      "frac": enc_bwd_gbs / hbm,
+                                      "bytes": f"{2 * ENCODE_BYTES_PER_SAMPLE} B/sample (atomic RMW)"},
+                       "peak_kind": peak_kind}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        o, d, gt, _ = batches_host[0]
+        cpu, why = cpu_reference(cfg, o, d, gt, args.ref_rays, 1, 0)
+        if cpu is None:
+            cpu = {"value": None, "unit": "rays/s", "cores": 0, "kind": "reference", "sample": why}
+        else:
+            cpu.pop("ms_per_step", None)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+                "data": "synthetic (random-init grids, drift-generator rays)",
+                "config": {"workload": wl.name, "note": wl.note, "global_batch_rays": B,
+                           "partitions": cfg.kx * cfg.ky, "tiling": [cfg.kx, cfg.ky],
+                           "grid": {"L": 16, "F": 2, "T_log2": args.table_log2, "N0": 16, "Nmax": 2048},
+                           "samples_per_step_rank0": samples_rank, "items_rank0": items_rank,
+                           "l2": "working set > L2 (hash tables 1 GiB+/partition, sample buffers); "
+                                 "3 distinct ray batches cycled",
+                           "parallelism": f"partition-parallel x{world}"},
+                "render_rays_per_s": render_value, "render_ms": rms,
+                "encode_gbs": enc_fwd_gbs, "exchange_bytes_rank0": bytes_sent,
+                "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+                "roofline": roof, "roofline_encode": roofline_encode, "cpu_baseline": cpu}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -123,6 +123,8 @@ typedef struct dg_step_stats {
   uint64_t bytes_sent;   /* exchange bytes (both exchanges), this rank */
   uint64_t samples;      /* march samples shaded on this rank */
   uint64_t items;        /* (ray, partition) segments owned by this rank */
+  uint64_t h2d_bytes;    /* host->device bytes this call moved (batch staging + tables) */
+  uint64_t d2h_bytes;    /* device->host bytes this call moved (counts, losses) */
 } dg_step_stats;
 
 /* render.hpp:38-43 MergedRender, structure of arrays. */
@@ -270,6 +272,8 @@ typedef struct dg_stage_times {
 int dg_enable_stage_timing(dg_ctx* ctx, int enable);
 int dg_last_stage_times(dg_ctx* ctx, dg_stage_times* t);
 int dg_synchronize(dg_ctx* ctx);
+/* the context's CUDA stream (cudaStream_t) so callers can record events on it */
+int dg_get_stream(dg_ctx* ctx, void** stream);
 
 #ifdef __cplusplus
 }

@@ -369,3 +369,87 @@ class ModelBuffer:
         if rc != 0:
             raise RuntimeError(lib.or_last_error().decode())
         self.ptr = C.cast(self.buf, P)
+
+
+class OracleModel:
+    """or_model for cfg + the per-stage restatements on flat partition arrays."""
+
+    def __init__(self, cfg):
+        lib = oracle_lib()
+        lib.or_model_size.restype = C.c_uint64
+        lib.or_model_init.argtypes = [P, C.POINTER(RunConfig)]
+        self.cfg = cfg.copy()
+        self.buf = C.create_string_buffer(int(lib.or_model_size()))
+        self.ptr = C.cast(self.buf, P)
+        if lib.or_model_init(self.ptr, C.byref(self.cfg)) != 0:
+            raise RuntimeError(lib.or_last_error().decode())
+        self.lib = lib
+        lib.or_stage_cascade_march.argtypes = [P, C.c_uint32, P, P, P, P, P, P, P, C.c_uint64,
+                                               C.c_int, C.c_uint64, P, P, P, P, C.c_uint64]
+        lib.or_stage_encode.argtypes = [P, C.c_uint32, C.c_uint32, P, P, C.c_uint64, P, P]
+        lib.or_stage_field_forward.argtypes = [P, C.c_uint32, C.c_uint32, P, P, P, P, C.c_uint64,
+                                               P, P]
+        lib.or_stage_field_backward.argtypes = [P, C.c_uint32, C.c_uint32, P, P, P, P, P, P, P,
+                                                C.c_uint64]
+        lib.or_segment_ray.argtypes = [P, P, P, P, P, P]
+
+    def segment_rays(self, o, d):
+        n = len(o)
+        nseg = np.zeros(n, dtype=U8)
+        region = np.zeros((n, DG_MAX_SEGMENTS), dtype=np.uint32)
+        te = np.zeros((n, DG_MAX_SEGMENTS))
+        tx = np.zeros((n, DG_MAX_SEGMENTS))
+        o = np.ascontiguousarray(o, dtype=np.float64)
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        for i in range(n):
+            nseg[i] = self.lib.or_segment_ray(self.ptr, _ptr(o[i]), _ptr(d[i]), _ptr(region[i]),
+                                              _ptr(te[i]), _ptr(tx[i]))
+        return nseg, region.astype(np.uint16), te, tx
+
+    def cascade_march(self, g, occ_fine, occ_coarse, o, d, t0, t1, ray_id, jitter, batch_id):
+        n = len(o)
+        cap = max(16, int(n) * 8192)
+        counts = np.zeros(n, dtype=np.uint32)
+        t = np.zeros(cap)
+        delta = np.zeros(cap)
+        casc = np.zeros(cap, dtype=U8)
+        args = [np.ascontiguousarray(x, dtype=np.float64) for x in (o, d, t0, t1)]
+        rid = np.ascontiguousarray(ray_id, dtype=np.uint64)
+        of = np.ascontiguousarray(occ_fine, dtype=U8)
+        oc = np.ascontiguousarray(occ_coarse, dtype=U8)
+        rc = self.lib.or_stage_cascade_march(self.ptr, g, _ptr(of), _ptr(oc), *[_ptr(a) for a in args],
+                                             _ptr(rid), n, int(jitter), batch_id, _ptr(counts),
+                                             _ptr(t), _ptr(delta), _ptr(casc), cap)
+        if rc != 0:
+            raise RuntimeError(self.lib.or_last_error().decode())
+        tot = int(counts.sum())
+        return counts, t[:tot], delta[:tot], casc[:tot]
+
+    def encode(self, g, cascade, params, pts):
+        n = len(pts)
+        L, F = self.cfg.grid_levels, self.cfg.grid_features
+        out = np.zeros((n, L * F))
+        rows = np.zeros((n, L, 8), dtype=np.uint32)
+        params = np.ascontiguousarray(params, dtype=np.float64)
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        self.lib.or_stage_encode(self.ptr, g, cascade, _ptr(params), _ptr(pts), n, _ptr(out),
+                                 _ptr(rows))
+        return out, rows
+
+    def field_forward(self, g, cascade, params, pts, dirs, app):
+        n = len(pts)
+        sigma = np.zeros(n)
+        rgb = np.zeros((n, 3))
+        a = [np.ascontiguousarray(x, dtype=np.float64) for x in (params, pts, dirs, app)]
+        self.lib.or_stage_field_forward(self.ptr, g, cascade, *[_ptr(x) for x in a], n,
+                                        _ptr(sigma), _ptr(rgb))
+        return sigma, rgb
+
+    def field_backward(self, g, cascade, params, pts, dirs, app, dsig, drgb):
+        n = len(pts)
+        params = np.ascontiguousarray(params, dtype=np.float64)
+        grads = np.zeros_like(params)
+        a = [np.ascontiguousarray(x, dtype=np.float64) for x in (pts, dirs, app, dsig, drgb)]
+        self.lib.or_stage_field_backward(self.ptr, g, cascade, _ptr(params), _ptr(grads),
+                                         *[_ptr(x) for x in a], n)
+        return grads

@@ -1228,3 +1228,58 @@ int or_run_eval_rays(or_run* r, const double* origin, const double* dir, uint64_
   }
   return 0;
 }
+
+/* ---- stage wrappers for the per-stage parity tests (flat partition arrays) ---- */
+uint64_t or_model_size(void) { return sizeof(or_model); }
+
+int or_stage_cascade_march(const or_model* m, uint32_t region, const uint8_t* occ_fine,
+                           const uint8_t* occ_coarse, const double* o, const double* d,
+                           const double* t0, const double* t1, const uint64_t* ray_id, uint64_t n,
+                           int jitter, uint64_t batch_id, uint32_t* counts, double* t,
+                           double* delta, uint8_t* cascade, uint64_t cap) {
+  uint64_t off = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const int k = or_cascade_march(m, region, occ_fine, occ_coarse, o + 3 * i, d + 3 * i, t0[i],
+                                   t1[i], jitter, ray_id[i], batch_id, t + off, delta + off,
+                                   cascade + off, (int)(cap - off));
+    if (k < 0) return -1;
+    counts[i] = (uint32_t)k;
+    off += (uint64_t)k;
+  }
+  return 0;
+}
+
+void or_stage_encode(const or_model* m, uint32_t region, uint32_t cascade, const double* params,
+                     const double* pts, uint64_t n, double* out, uint32_t* rows) {
+  const or_field_layout* f = &m->field[region][cascade];
+  const double* base = params + (cascade == 0 ? 0 : m->field[region][0].size);
+  for (uint64_t i = 0; i < n; ++i)
+    or_encode(&f->grid, base, pts + 3 * i, out + i * f->enc_width,
+              rows ? rows + i * f->grid.L * 8 : NULL);
+}
+
+void or_stage_field_forward(const or_model* m, uint32_t region, uint32_t cascade,
+                            const double* params, const double* pts, const double* dirs,
+                            const double* app, uint64_t n, double* sigma, double* rgb) {
+  const or_field_layout* f = &m->field[region][cascade];
+  const double* base = params + (cascade == 0 ? 0 : m->field[region][0].size);
+  or_field_cache c;
+  for (uint64_t i = 0; i < n; ++i) {
+    or_field_forward(f, base, pts + 3 * i, dirs + 3 * i, app + i * m->cfg.appearance_dim, &c);
+    sigma[i] = c.sigma;
+    for (int k = 0; k < 3; ++k) rgb[3 * i + k] = c.rgb[k];
+  }
+}
+
+void or_stage_field_backward(const or_model* m, uint32_t region, uint32_t cascade,
+                             const double* params, double* grads, const double* pts,
+                             const double* dirs, const double* app, const double* dsigma,
+                             const double* drgb, uint64_t n) {
+  const or_field_layout* f = &m->field[region][cascade];
+  const uint64_t off = cascade == 0 ? 0 : m->field[region][0].size;
+  or_field_cache c;
+  for (uint64_t i = 0; i < n; ++i) {
+    or_field_forward(f, params + off, pts + 3 * i, dirs + 3 * i, app + i * m->cfg.appearance_dim, &c);
+    or_field_backward(f, params + off, grads + off, &c, dsigma[i], drgb + 3 * i);
+  }
+}

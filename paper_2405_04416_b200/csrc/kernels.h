@@ -1,0 +1,148 @@
+// kernels.h — launch wrappers for the sm_100a kernels (one translation unit each).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "dg_common.cuh"
+
+namespace dg {
+
+// Per-item state after setup (structure of arrays, capacity NI).
+struct ItemArrays {
+  RayRec* rec;        // dispatch record (origin/dir rounded in place when wire_f32)
+  double* te;         // my segment t_enter / t_exit
+  double* tx;
+  double* t0;         // schedule.front().t_enter / schedule.back().t_exit
+  double* t1;
+  uint8_t* nseg;
+  uint8_t* order;     // my index in the schedule
+  uint8_t* part;      // local partition index
+  uint8_t* sched;     // NI x 16 global partition ids
+  uint32_t* cnt;      // [2][NI]: fine, coarse sample counts (scanned in place -> offsets)
+  uint32_t* off;      // [2][NI] exclusive offsets (fine region, coarse region)
+  uint32_t* ncb;      // coarse samples before the fine box
+  uint32_t* contains; // [P][NI] 1 when partition q is in the schedule and q != mine
+  uint32_t* cscan;    // exclusive scan of contains
+  float4* partial;    // rgb, T of my segment
+  float* depth;       // depth_sum of my segment
+};
+
+struct SampleArrays {
+  double* t;
+  double* delta;
+  uint32_t* item;
+  float* X;        // n x 32 encoded features
+  float4* out;     // sigma, r, g, b
+  float4* grad;    // dsigma, dr, dg, db
+  float* dX;       // n x 32
+};
+
+struct LossAccum {
+  double rgb[kMaxPart];
+  double trans[kMaxPart];
+  double dist[kMaxPart];
+  uint32_t error;     // bit 0: unknown image id, bit 1: partial protocol mismatch
+  uint32_t pad;
+};
+
+// ---- ray-side kernels (kernels_ray.cu) ----
+void launch_segment_home(const Geo* geo, const double* o, const double* d, uint64_t n,
+                         const uint8_t* slot_of_part, uint8_t* nseg, uint8_t* sched,
+                         uint32_t* flags, unsigned long long* dropped, cudaStream_t s);
+void launch_pack_dispatch(uint64_t n, uint32_t P, const uint8_t* nseg, const uint8_t* sched,
+                          const uint8_t* slot_of_part, const uint32_t* pos, const double* o,
+                          const double* d, const float* gt, const uint32_t* img,
+                          uint64_t first_ray_id, RayRec* out, cudaStream_t s);
+void launch_item_setup(const Geo* geo, const PartDesc* parts, const uint8_t* occ,
+                       const uint32_t* part_item_off, uint32_t n_local, uint32_t n_items,
+                       ItemArrays it, uint32_t P, double step, uint64_t seed, uint64_t batch_id,
+                       int jitter, int wire_f32, uint32_t n_images, uint32_t* error,
+                       cudaStream_t s);
+void launch_march_fill(const PartDesc* parts, const uint8_t* occ, uint32_t n_items,
+                       ItemArrays it, SampleArrays sm, uint32_t fine_total, double step,
+                       uint64_t seed, uint64_t batch_id, int jitter, cudaStream_t s);
+void launch_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, uint32_t fine_total,
+                      int with_depth, cudaStream_t s);
+void launch_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
+                          const uint8_t* local_of_global, const uint64_t* stream_off,
+                          uint32_t P, PartialRec* send, cudaStream_t s);
+void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
+                           const PartDesc* parts, const uint64_t* stream_off, uint32_t P,
+                           const PartialRec* recv, SampleArrays sm, uint32_t fine_total,
+                           double lambda_t, double lambda_d, double t_clamp, LossAccum* loss,
+                           cudaStream_t s);
+void launch_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P, const uint32_t* part_item_off,
+                        const uint32_t* contains, const uint32_t* cscan, uint32_t* out,
+                        cudaStream_t s);
+// eval: home merge in schedule order from item partials (world == 1) or reply records
+void launch_home_merge(uint64_t n, uint32_t P, const uint8_t* nseg, const uint8_t* sched,
+                       const uint8_t* slot_of_part, const uint32_t* pos, const float4* partial,
+                       const float* depth, const PartialRec* reply, int wire_f32, float* rgb,
+                       float* trans, float* depth_out, cudaStream_t s);
+
+// stage-entry helpers
+void launch_segment_full(const Geo* geo, const double* o, const double* d, uint64_t n, uint8_t* nseg,
+                         uint8_t* sched, double* te, double* tx, cudaStream_t s);
+void launch_u8_to_u16(const uint8_t* in, uint16_t* out, uint64_t n, cudaStream_t s);
+void launch_march_points(const PartDesc* part, const uint8_t* occ, const double* o, const double* d,
+                         const double* t0, const double* t1, const uint64_t* ray_id, uint64_t n,
+                         double step, uint64_t seed, uint64_t batch_id, int jitter, uint32_t* counts,
+                         const uint64_t* offsets, double* t, double* delta, uint8_t* cascade,
+                         cudaStream_t s);
+void launch_items_to_records(uint32_t n, const float4* partial, const float* depth, const RayRec* rec,
+                             PartialRec* out, cudaStream_t s);
+
+// ---- field kernels ----
+struct FieldLaunch {
+  const FieldDesc* fields;     // [2][n_local] (cascade-major)
+  const PartDesc* parts;
+  const ItemArrays* it_dummy;  // unused
+  const RayRec* rec;           // items
+  const uint8_t* item_part;
+  const double* s_t;
+  const uint32_t* s_item;
+  uint32_t fine_total;
+  uint32_t n_total;
+  uint32_t n_local;
+  const float* params;
+  float* grads;
+};
+void launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s);
+void launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s);
+// stand-alone points variant (stage entry points): all points belong to one field
+void launch_encode_points(const FieldDesc* field, const float* params, const double* pts,
+                          uint64_t n, float* X, uint32_t* rows, cudaStream_t s);
+void launch_encode_points_bwd(const FieldDesc* field, float* grads, const double* pts,
+                              const float* dX, uint64_t n, cudaStream_t s);
+
+// MLP: tiles never straddle fields.  field_off: n_fields+1 sample offsets.
+struct MlpLaunch {
+  const FieldDesc* fields;
+  uint32_t n_fields;
+  const uint32_t* field_off;   // device, n_fields + 1
+  const uint32_t* tile_off;    // device, n_fields + 1 (prefix of tiles)
+  uint32_t n_tiles;
+  const float* X;
+  const float* dirs_f;         // optional per-sample dirs (stage entry) else from items
+  const RayRec* rec;
+  const uint32_t* s_item;
+  const float* app_table;      // [n_images][app_dim]
+  const float* app_override;   // eval: one vector for all samples (or per-sample when app_per_sample)
+  int app_per_sample;
+  const float* params;
+  float* grads;
+  float4* out;                 // fwd: sigma, rgb
+  const float4* grad_in;       // bwd: dsigma, drgb
+  float* dX;                   // bwd
+};
+void launch_mlp_fwd(const MlpLaunch& m, cudaStream_t s);
+void launch_mlp_bwd(const MlpLaunch& m, int num_sms, cudaStream_t s);
+
+// ---- optimizer / init (kernels_adam.cu) ----
+void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, float b1, float b2,
+                 float eps, float inv_bias1, float inv_sqrt_bias2, cudaStream_t s);
+void launch_fill_uniform(float* p, uint64_t n, float lo, float hi, uint64_t seed, cudaStream_t s);
+
+}  // namespace dg

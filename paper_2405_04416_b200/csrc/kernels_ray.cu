@@ -1,0 +1,620 @@
+// kernels_ray.cu — per-ray / per-item kernels of stages 1, 2 and 5.
+//
+//   k_segment_home    plan_batch (worker.cpp:141-165) + segment_ray (partition.cpp:254-296)
+//   k_pack_dispatch   exchange-1 send layout (RayDispatch, wire.cpp:29-46)
+//   k_item_setup      Worker::handle_training_batch phase-1 head (worker.cpp:268-284)
+//                     + cascade_march sample count (worker.cpp:79-110)
+//   k_march_fill      cascade_march sample emission into field-major sample arrays
+//   k_composite       local_render (render.cpp:46-78) per (ray, partition) item
+//   k_pack_partials   exchange-2 send layout (PartialScatter, worker.cpp:314-334)
+//   k_merge_backward  backward_ray (worker.cpp:403-522): merge_forward, losses, merge_backward,
+//                     distortion, local_render_backward (render.cpp:101-179, train.cpp:8-75)
+//   k_home_merge      dispatch_eval driver merge (worker.cpp:801-826)
+#include <cub/cub.cuh>
+
+#include "geometry.cuh"
+#include "kernels.h"
+
+namespace dg {
+
+namespace {
+
+__device__ __forceinline__ void load_geo(Geo& sg, const Geo* g) {
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(g);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(&sg);
+  for (int i = threadIdx.x; i < (int)(sizeof(Geo) / 4); i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+}
+
+__global__ void k_segment_home(const Geo* __restrict__ geo, const double* __restrict__ o,
+                               const double* __restrict__ d, uint64_t n,
+                               const uint8_t* __restrict__ slot_of_part, uint8_t* __restrict__ nseg,
+                               uint8_t* __restrict__ sched, uint32_t* __restrict__ flags,
+                               unsigned long long* __restrict__ dropped) {
+  __shared__ Geo sg;
+  load_geo(sg, geo);
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool miss = false;
+  if (i < n) {
+    double oo[3] = {o[3 * i], o[3 * i + 1], o[3 * i + 2]};
+    double dd[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+    uint8_t reg[kMaxSeg];
+    double te[kMaxSeg], tx[kMaxSeg];
+    const int ns = segment_ray(sg, oo, dd, reg, te, tx);
+    nseg[i] = (uint8_t)ns;
+    uint8_t* sc = sched + i * kMaxSeg;
+    for (int s = 0; s < kMaxSeg; ++s) sc[s] = s < ns ? reg[s] : 0xff;
+    for (int s = 0; s < ns; ++s) flags[(uint64_t)slot_of_part[reg[s]] * n + i] = 1u;
+    miss = ns == 0;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, miss);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(dropped, (unsigned long long)__popc(m));
+}
+
+__global__ void k_pack_dispatch(uint64_t n, const uint8_t* __restrict__ nseg,
+                                const uint8_t* __restrict__ sched,
+                                const uint8_t* __restrict__ slot_of_part,
+                                const uint32_t* __restrict__ pos, const double* __restrict__ o,
+                                const double* __restrict__ d, const float* __restrict__ gt,
+                                const uint32_t* __restrict__ img, uint64_t first_ray_id,
+                                RayRec* __restrict__ out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ns = nseg[i];
+  if (ns == 0) return;
+  RayRec r;
+  for (int a = 0; a < 3; ++a) {
+    r.o[a] = o[3 * i + a];
+    r.d[a] = d[3 * i + a];
+    r.gt[a] = gt ? gt[3 * i + a] : 0.0f;
+  }
+  r.img = img ? img[i] : 0u;
+  r.ray_id = (uint32_t)(first_ray_id + i);
+  r.pad = 0;
+  for (int s = 0; s < ns; ++s) {
+    const uint32_t p = sched[i * kMaxSeg + s];
+    out[pos[(uint64_t)slot_of_part[p] * n + i]] = r;
+  }
+}
+
+__device__ __forceinline__ uint32_t part_of_item(const uint32_t* off, uint32_t n_local, uint32_t i) {
+  uint32_t p = 0;
+  while (p + 1 < n_local && i >= off[p + 1]) ++p;
+  return p;
+}
+
+__device__ __forceinline__ double round_f32(double v) { return (double)(float)v; }
+
+__global__ void k_item_setup(const Geo* __restrict__ geo, const PartDesc* __restrict__ parts,
+                             const uint8_t* __restrict__ occ,
+                             const uint32_t* __restrict__ part_item_off, uint32_t n_local,
+                             uint32_t n_items, ItemArrays it, uint32_t P, double step,
+                             uint64_t seed, uint64_t batch_id, int jitter, int wire_f32,
+                             uint32_t n_images, uint32_t* __restrict__ error) {
+  __shared__ Geo sg;
+  load_geo(sg, geo);
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const uint32_t lp = part_of_item(part_item_off, n_local, i);
+  const PartDesc& pd = parts[lp];
+  RayRec r = it.rec[i];
+  uint8_t reg[kMaxSeg];
+  double te[kMaxSeg], tx[kMaxSeg];
+  const int ns = segment_ray(sg, r.o, r.d, reg, te, tx);
+  int mo = -1;
+  for (int s = 0; s < ns; ++s)
+    if (reg[s] == pd.global_id) mo = s;
+  if (mo < 0) {  // "dispatched ray does not intersect this region" (worker.cpp:274-276)
+    atomicOr(error, 2u);
+    it.nseg[i] = 0;
+    it.order[i] = 0;
+    it.part[i] = (uint8_t)lp;
+    it.cnt[i] = it.cnt[n_items + i] = it.ncb[i] = 0u;
+    for (uint32_t q = 0; q < P; ++q) it.contains[(uint64_t)q * n_items + i] = 0u;
+    return;
+  }
+  if (r.img >= n_images) atomicOr(error, 1u);  // AppearanceTable::row (field.cpp:125-130)
+  if (wire_f32) {  // WireWriter::real rounding of the RayDispatch payload (wire.hpp:55-62)
+    for (int a = 0; a < 3; ++a) {
+      r.o[a] = round_f32(r.o[a]);
+      r.d[a] = round_f32(r.d[a]);
+    }
+    for (int s = 0; s < ns; ++s) {
+      te[s] = round_f32(te[s]);
+      tx[s] = round_f32(tx[s]);
+    }
+    it.rec[i] = r;
+  }
+  const double t0 = te[mo], t1 = tx[mo];
+  it.te[i] = t0;
+  it.tx[i] = t1;
+  it.t0[i] = ns > 0 ? te[0] : 0.0;
+  it.t1[i] = ns > 0 ? tx[ns - 1] : 0.0;
+  it.nseg[i] = (uint8_t)ns;
+  it.order[i] = (uint8_t)mo;
+  it.part[i] = (uint8_t)lp;
+  uint8_t* sc = it.sched + (uint64_t)i * kMaxSeg;
+  for (int s = 0; s < kMaxSeg; ++s) sc[s] = s < ns ? reg[s] : 0xff;
+  for (uint32_t q = 0; q < P; ++q) it.contains[(uint64_t)q * n_items + i] = 0u;
+  for (int s = 0; s < ns; ++s)
+    if (reg[s] != pd.global_id) it.contains[(uint64_t)reg[s] * n_items + i] = 1u;
+  // sample counts of cascade_march
+  const double offset = jitter ? dmul(step, counter_uniform(seed, (uint64_t)r.ray_id, batch_id))
+                               : dmul(0.5, step);
+  uint32_t nf = 0, nc = 0, ncb = 0;
+  double fa, fb;
+  auto count = [&](double, double, int casc) {
+    if (casc == 0) {
+      ++nf;
+    } else {
+      ++nc;
+      if (nf == 0) ++ncb;
+    }
+  };
+  const bool has_fine = cascade_march(pd, occ, r.o, r.d, t0, t1, step, offset, fa, fb, count);
+  if (!has_fine) ncb = nc;
+  it.cnt[i] = nf;
+  it.cnt[n_items + i] = nc;
+  it.ncb[i] = ncb;
+}
+
+__global__ void k_march_fill(const PartDesc* __restrict__ parts, const uint8_t* __restrict__ occ,
+                             uint32_t n_items, ItemArrays it, SampleArrays sm, double step,
+                             uint64_t seed, uint64_t batch_id, int jitter) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const PartDesc& pd = parts[it.part[i]];
+  const RayRec& r = it.rec[i];
+  const double offset = jitter ? dmul(step, counter_uniform(seed, (uint64_t)r.ray_id, batch_id))
+                               : dmul(0.5, step);
+  uint32_t pf = it.off[i], pc = it.off[n_items + i];
+  double fa, fb;
+  auto emit = [&](double t, double delta, int casc) {
+    const uint32_t s = casc == 0 ? pf++ : pc++;
+    sm.t[s] = t;
+    sm.delta[s] = delta;
+    sm.item[s] = i;
+  };
+  cascade_march(pd, occ, r.o, r.d, it.te[i], it.tx[i], step, offset, fa, fb, emit);
+}
+
+// Visit an item's samples in t order: coarse-before, fine, coarse-after.
+template <class F>
+__device__ __forceinline__ void for_item_samples(const ItemArrays& it, uint32_t n_items, uint32_t i,
+                                                 F&& f) {
+  const uint32_t fo = it.off[i], nf = it.cnt[i];
+  const uint32_t co = it.off[n_items + i], nc = it.cnt[n_items + i], ncb = it.ncb[i];
+  for (uint32_t k = 0; k < ncb; ++k) f(co + k);
+  for (uint32_t k = 0; k < nf; ++k) f(fo + k);
+  for (uint32_t k = ncb; k < nc; ++k) f(co + k);
+}
+
+template <class F>
+__device__ __forceinline__ void for_item_samples_rev(const ItemArrays& it, uint32_t n_items,
+                                                     uint32_t i, F&& f) {
+  const uint32_t fo = it.off[i], nf = it.cnt[i];
+  const uint32_t co = it.off[n_items + i], nc = it.cnt[n_items + i], ncb = it.ncb[i];
+  for (uint32_t k = nc; k-- > ncb;) f(co + k);
+  for (uint32_t k = nf; k-- > 0;) f(fo + k);
+  for (uint32_t k = ncb; k-- > 0;) f(co + k);
+}
+
+__global__ void k_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, int with_depth) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  float T = 1.0f, r = 0.0f, g = 0.0f, b = 0.0f, dep = 0.0f;
+  for_item_samples(it, n_items, i, [&](uint32_t s) {
+    const float4 o = sm.out[s];
+    const float x = o.x * (float)sm.delta[s];
+    const float alpha = -expm1f(-x);
+    const float w = T * alpha;
+    r = fmaf(o.y, w, r);
+    g = fmaf(o.z, w, g);
+    b = fmaf(o.w, w, b);
+    if (with_depth) dep = fmaf(w, (float)sm.t[s], dep);
+    T *= expf(-x);
+  });
+  it.partial[i] = make_float4(r, g, b, T);
+  it.depth[i] = dep;
+}
+
+__device__ __forceinline__ uint32_t ordinal(const ItemArrays& it, uint32_t n_items,
+                                            const uint32_t* part_item_off, uint32_t lp, uint32_t q,
+                                            uint32_t i) {
+  const uint64_t row = (uint64_t)q * n_items;
+  return it.cscan[row + i] - it.cscan[row + part_item_off[lp]];
+}
+
+__global__ void k_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* __restrict__ part_item_off,
+                                const uint8_t* __restrict__ global_of_local,
+                                const uint64_t* __restrict__ stream_off, uint32_t P,
+                                PartialRec* __restrict__ send) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const uint32_t lp = it.part[i];
+  const uint32_t gid = global_of_local[lp];
+  const int ns = it.nseg[i];
+  if (ns <= 1) return;
+  const float4 pr = it.partial[i];
+  PartialRec rec;
+  rec.rgb[0] = pr.x;
+  rec.rgb[1] = pr.y;
+  rec.rgb[2] = pr.z;
+  rec.T = pr.w;
+  rec.depth = it.depth[i];
+  rec.ray_id = it.rec[i].ray_id;
+  const uint8_t* sc = it.sched + (uint64_t)i * kMaxSeg;
+  for (int s = 0; s < ns; ++s) {
+    const uint32_t q = sc[s];
+    if (q == gid) continue;
+    send[stream_off[gid * P + q] + ordinal(it, n_items, part_item_off, lp, q, i)] = rec;
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
+                                 const uint32_t* __restrict__ part_item_off,
+                                 const PartDesc* __restrict__ parts,
+                                 const uint64_t* __restrict__ stream_off, uint32_t P,
+                                 const PartialRec* __restrict__ recv, SampleArrays sm,
+                                 double lambda_t, double lambda_d, double t_clamp,
+                                 LossAccum* __restrict__ loss) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  double l_rgb = 0.0, l_t = 0.0, l_d = 0.0;
+  uint32_t lp = 0;
+  if (i < n_items) {
+    lp = it.part[i];
+    const uint32_t gid = parts[lp].global_id;
+    const int ns = it.nseg[i];
+    const int mo = it.order[i];
+    const RayRec& rr = it.rec[i];
+    const uint8_t* sc = it.sched + (uint64_t)i * kMaxSeg;
+    double pc[kMaxSeg][3], pT[kMaxSeg];
+    bool bad = false;
+    for (int s = 0; s < ns; ++s) {
+      float4 v;
+      if (s == mo) {
+        v = it.partial[i];
+      } else {
+        const uint32_t q = sc[s];
+        const PartialRec rec =
+            recv[stream_off[q * P + gid] + ordinal(it, n_items, part_item_off, lp, q, i)];
+        if (rec.ray_id != rr.ray_id) bad = true;
+        v = make_float4(rec.rgb[0], rec.rgb[1], rec.rgb[2], rec.T);
+      }
+      pc[s][0] = v.x;
+      pc[s][1] = v.y;
+      pc[s][2] = v.z;
+      pT[s] = v.w;
+    }
+    if (bad) atomicOr(&loss->error, 2u);  // "missing partial" (worker.cpp:371-376)
+    // merge_forward (render.cpp:101-116)
+    double C[3] = {0.0, 0.0, 0.0}, prefix = 1.0;
+    double pre[kMaxSeg + 1];
+    for (int s = 0; s < ns; ++s) {
+      pre[s] = prefix;
+      for (int a = 0; a < 3; ++a) C[a] += pc[s][a] * prefix;
+      prefix *= pT[s];
+    }
+    pre[ns] = prefix;
+    const double T = prefix;
+    const double gt[3] = {rr.gt[0], rr.gt[1], rr.gt[2]};
+    const double Tc = smin(T, 1.0 - t_clamp);
+    if (sc[0] == gid) {  // first owner reports (worker.cpp:409-416)
+      for (int a = 0; a < 3; ++a) l_rgb += (C[a] - gt[a]) * (C[a] - gt[a]);
+      l_t = -log(1.0 - Tc);
+    }
+    double up_c[3];
+    for (int a = 0; a < 3; ++a) up_c[a] = (C[a] - gt[a]) * 2.0;
+    const double up_t = lambda_t * (1.0 / (1.0 - Tc));
+    // merge_backward for my segment (render.cpp:118-143)
+    double suffix = 1.0;
+    for (int s = ns - 1; s > mo; --s) suffix *= pT[s];
+    double g_c[3];
+    for (int a = 0; a < 3; ++a) g_c[a] = up_c[a] * pre[mo];
+    double running = 1.0, color_term = 0.0;
+    for (int k = mo + 1; k < ns; ++k) {
+      color_term += running * (up_c[0] * pc[k][0] + up_c[1] * pc[k][1] + up_c[2] * pc[k][2]);
+      running *= pT[k];
+    }
+    const double g_t = up_t * pre[mo] * suffix + pre[mo] * color_term;
+    // local forward recompute: prefix per sample, distortion totals (worker.cpp:435-451)
+    const double ray_t0 = it.t0[i];
+    const float inv_span = (float)(1.0 / (it.t1[i] - ray_t0));
+    float Tl = 1.0f, Wt = 0.0f, Mt = 0.0f, Wp = 0.0f, Mp = 0.0f, pair = 0.0f, interval = 0.0f;
+    uint32_t n = 0;
+    for_item_samples(it, n_items, i, [&](uint32_t s) {
+      const float x = sm.out[s].x * (float)sm.delta[s];
+      const float alpha = -expm1f(-x);
+      const float w = Tl * alpha;
+      const float ss = (float)((sm.t[s] - ray_t0)) * inv_span;
+      const float ds = (float)sm.delta[s] * inv_span;
+      pair += 2.0f * w * (ss * Wp - Mp);
+      interval += w * w * ds;
+      Wp += w;
+      Mp += w * ss;
+      sm.grad[s] = make_float4(Tl, 0.f, 0.f, 0.f);  // stash prefix for the reverse sweep
+      Tl *= expf(-x);
+      ++n;
+    });
+    Wt = Wp;
+    Mt = Mp;
+    if (n > 0) l_d = (double)(pair + interval / 3.0f);
+    // reverse sweep: local_render_backward with the distortion weight channel
+    const float ucx = (float)g_c[0], ucy = (float)g_c[1], ucz = (float)g_c[2];
+    const float ut = (float)g_t;
+    const float ld = (float)lambda_d;
+    float tail_c = 0.0f, tail_t = 1.0f, Ws = 0.0f, Ms = 0.0f;
+    for_item_samples_rev(it, n_items, i, [&](uint32_t s) {
+      const float4 o = sm.out[s];
+      const float delta = (float)sm.delta[s];
+      const float x = o.x * delta;
+      const float alpha = -expm1f(-x);
+      const float om = expf(-x);
+      const float pf = sm.grad[s].x;
+      const float w = pf * alpha;
+      const float ss = (float)((sm.t[s] - ray_t0)) * inv_span;
+      const float ds = delta * inv_span;
+      float wup = 0.0f;
+      if (ld > 0.0f) {
+        const float Wl = Wt - Ws - w, Ml = Mt - Ms - w * ss;
+        const float gd = 2.0f * (ss * Wl - Ml) + 2.0f * (Ms - ss * Ws) + (2.0f / 3.0f) * w * ds;
+        wup = ld * gd;
+      }
+      const float u = ucx * o.y + ucy * o.z + ucz * o.w + wup;
+      const float alpha_grad = pf * (u - tail_c) - ut * pf * tail_t;
+      const float dsig = alpha_grad * delta * om;
+      const float cw = pf * alpha;
+      sm.grad[s] = make_float4(dsig, ucx * cw, ucy * cw, ucz * cw);
+      tail_c = alpha * u + om * tail_c;
+      tail_t *= om;
+      Ws += w;
+      Ms += w * ss;
+    });
+  }
+  // per-partition loss sums: warp-reduce when the warp is uniform, else per-lane atomics
+  const unsigned active = __ballot_sync(0xffffffffu, i < n_items);
+  const uint32_t lp0 = __shfl_sync(0xffffffffu, lp, 0);
+  const bool uniform = __all_sync(0xffffffffu, lp == lp0 || i >= n_items);
+  if (uniform) {
+    const double a = warp_sum(l_rgb), b = warp_sum(l_t), c = warp_sum(l_d);
+    if ((threadIdx.x & 31) == 0 && active) {
+      atomicAdd(&loss->rgb[lp0], a);
+      atomicAdd(&loss->trans[lp0], b);
+      atomicAdd(&loss->dist[lp0], c);
+    }
+  } else if (i < n_items) {
+    atomicAdd(&loss->rgb[lp], l_rgb);
+    atomicAdd(&loss->trans[lp], l_t);
+    atomicAdd(&loss->dist[lp], l_d);
+  }
+}
+
+__global__ void k_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P,
+                              const uint32_t* __restrict__ part_item_off,
+                              const uint32_t* __restrict__ cscan, uint32_t* __restrict__ out) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_local * P) return;
+  const uint32_t lp = t / P, q = t % P;
+  const uint64_t row = (uint64_t)q * n_items;
+  out[t] = cscan[row + part_item_off[lp + 1]] - cscan[row + part_item_off[lp]];
+}
+
+__global__ void k_home_merge(uint64_t n, const uint8_t* __restrict__ nseg,
+                             const uint8_t* __restrict__ sched, const uint8_t* __restrict__ slot_of_part,
+                             const uint32_t* __restrict__ pos, const float4* __restrict__ partial,
+                             const float* __restrict__ depth, const PartialRec* __restrict__ reply,
+                             float* __restrict__ rgb, float* __restrict__ trans,
+                             float* __restrict__ depth_out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ns = nseg[i];
+  double C[3] = {0.0, 0.0, 0.0}, prefix = 1.0, dep = 0.0;
+  for (int s = 0; s < ns; ++s) {
+    const uint32_t p = sched[i * kMaxSeg + s];
+    const uint32_t idx = pos[(uint64_t)slot_of_part[p] * n + i];
+    float4 v;
+    float dp;
+    if (reply) {
+      const PartialRec r = reply[idx];
+      v = make_float4(r.rgb[0], r.rgb[1], r.rgb[2], r.T);
+      dp = r.depth;
+    } else {
+      v = partial[idx];
+      dp = depth[idx];
+    }
+    C[0] += v.x * prefix;
+    C[1] += v.y * prefix;
+    C[2] += v.z * prefix;
+    dep += dp * prefix;
+    prefix *= v.w;
+  }
+  rgb[3 * i] = (float)C[0];
+  rgb[3 * i + 1] = (float)C[1];
+  rgb[3 * i + 2] = (float)C[2];
+  trans[i] = (float)prefix;
+  depth_out[i] = (float)dep;
+}
+
+__global__ void k_segment_full(const Geo* __restrict__ geo, const double* __restrict__ o,
+                               const double* __restrict__ d, uint64_t n, uint8_t* __restrict__ nseg,
+                               uint8_t* __restrict__ sched, double* __restrict__ te,
+                               double* __restrict__ tx) {
+  __shared__ Geo sg;
+  load_geo(sg, geo);
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double oo[3] = {o[3 * i], o[3 * i + 1], o[3 * i + 2]};
+  double dd[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+  uint8_t reg[kMaxSeg];
+  double a[kMaxSeg], b[kMaxSeg];
+  const int ns = segment_ray(sg, oo, dd, reg, a, b);
+  nseg[i] = (uint8_t)ns;
+  for (int s = 0; s < kMaxSeg; ++s) {
+    sched[i * kMaxSeg + s] = s < ns ? reg[s] : 0xff;
+    te[i * kMaxSeg + s] = s < ns ? a[s] : 0.0;
+    tx[i * kMaxSeg + s] = s < ns ? b[s] : 0.0;
+  }
+}
+
+__global__ void k_u8_to_u16(const uint8_t* in, uint16_t* out, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i] == 0xff ? 0 : in[i];
+}
+
+__global__ void k_march_points(const PartDesc* __restrict__ part, const uint8_t* __restrict__ occ,
+                               const double* __restrict__ o, const double* __restrict__ d,
+                               const double* __restrict__ t0, const double* __restrict__ t1,
+                               const uint64_t* __restrict__ ray_id, uint64_t n, double step,
+                               uint64_t seed, uint64_t batch_id, int jitter,
+                               uint32_t* __restrict__ counts, const uint64_t* __restrict__ offsets,
+                               double* __restrict__ t, double* __restrict__ delta,
+                               uint8_t* __restrict__ cascade) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double oo[3] = {o[3 * i], o[3 * i + 1], o[3 * i + 2]};
+  const double dd[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+  const double offset = jitter ? dmul(step, counter_uniform(seed, ray_id[i], batch_id)) : dmul(0.5, step);
+  double fa, fb;
+  uint32_t k = 0;
+  const uint64_t base = offsets ? offsets[i] : 0;
+  auto emit = [&](double tt, double dl, int casc) {
+    if (t) {
+      t[base + k] = tt;
+      delta[base + k] = dl;
+      cascade[base + k] = (uint8_t)casc;
+    }
+    ++k;
+  };
+  cascade_march(*part, occ, oo, dd, t0[i], t1[i], step, offset, fa, fb, emit);
+  if (!t) counts[i] = k;
+}
+
+__global__ void k_items_to_records(uint32_t n, const float4* __restrict__ partial,
+                                   const float* __restrict__ depth, const RayRec* __restrict__ rec,
+                                   PartialRec* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 v = partial[i];
+  PartialRec r;
+  r.rgb[0] = v.x;
+  r.rgb[1] = v.y;
+  r.rgb[2] = v.z;
+  r.T = v.w;
+  r.depth = depth[i];
+  r.ray_id = rec[i].ray_id;
+  out[i] = r;
+}
+
+inline unsigned blocks(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void launch_segment_home(const Geo* geo, const double* o, const double* d, uint64_t n,
+                         const uint8_t* slot_of_part, uint8_t* nseg, uint8_t* sched,
+                         uint32_t* flags, unsigned long long* dropped, cudaStream_t s) {
+  if (!n) return;
+  k_segment_home<<<blocks(n, 128), 128, 0, s>>>(geo, o, d, n, slot_of_part, nseg, sched, flags,
+                                                 dropped);
+}
+
+void launch_pack_dispatch(uint64_t n, uint32_t, const uint8_t* nseg, const uint8_t* sched,
+                          const uint8_t* slot_of_part, const uint32_t* pos, const double* o,
+                          const double* d, const float* gt, const uint32_t* img,
+                          uint64_t first_ray_id, RayRec* out, cudaStream_t s) {
+  if (!n) return;
+  k_pack_dispatch<<<blocks(n, 256), 256, 0, s>>>(n, nseg, sched, slot_of_part, pos, o, d, gt, img,
+                                                 first_ray_id, out);
+}
+
+void launch_item_setup(const Geo* geo, const PartDesc* parts, const uint8_t* occ,
+                       const uint32_t* part_item_off, uint32_t n_local, uint32_t n_items,
+                       ItemArrays it, uint32_t P, double step, uint64_t seed, uint64_t batch_id,
+                       int jitter, int wire_f32, uint32_t n_images, uint32_t* error,
+                       cudaStream_t s) {
+  if (!n_items) return;
+  k_item_setup<<<blocks(n_items, 128), 128, 0, s>>>(geo, parts, occ, part_item_off, n_local,
+                                                    n_items, it, P, step, seed, batch_id, jitter,
+                                                    wire_f32, n_images, error);
+}
+
+void launch_march_fill(const PartDesc* parts, const uint8_t* occ, uint32_t n_items,
+                       ItemArrays it, SampleArrays sm, uint32_t, double step, uint64_t seed,
+                       uint64_t batch_id, int jitter, cudaStream_t s) {
+  if (!n_items) return;
+  k_march_fill<<<blocks(n_items, 128), 128, 0, s>>>(parts, occ, n_items, it, sm, step, seed,
+                                                    batch_id, jitter);
+}
+
+void launch_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, uint32_t,
+                      int with_depth, cudaStream_t s) {
+  if (!n_items) return;
+  k_composite<<<blocks(n_items, 128), 128, 0, s>>>(n_items, it, sm, with_depth);
+}
+
+void launch_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
+                          const uint8_t* global_of_local, const uint64_t* stream_off, uint32_t P,
+                          PartialRec* send, cudaStream_t s) {
+  if (!n_items) return;
+  k_pack_partials<<<blocks(n_items, 256), 256, 0, s>>>(n_items, it, part_item_off, global_of_local,
+                                                       stream_off, P, send);
+}
+
+void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
+                           const PartDesc* parts, const uint64_t* stream_off, uint32_t P,
+                           const PartialRec* recv, SampleArrays sm, uint32_t, double lambda_t,
+                           double lambda_d, double t_clamp, LossAccum* loss, cudaStream_t s) {
+  if (!n_items) return;
+  k_merge_backward<<<blocks(n_items, 128), 128, 0, s>>>(n_items, it, part_item_off, parts,
+                                                        stream_off, P, recv, sm, lambda_t,
+                                                        lambda_d, t_clamp, loss);
+}
+
+void launch_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P, const uint32_t* part_item_off,
+                        const uint32_t*, const uint32_t* cscan, uint32_t* out, cudaStream_t s) {
+  k_pair_counts<<<blocks((uint64_t)n_local * P, 128), 128, 0, s>>>(n_items, n_local, P,
+                                                                   part_item_off, cscan, out);
+}
+
+void launch_home_merge(uint64_t n, uint32_t, const uint8_t* nseg, const uint8_t* sched,
+                       const uint8_t* slot_of_part, const uint32_t* pos, const float4* partial,
+                       const float* depth, const PartialRec* reply, int, float* rgb, float* trans,
+                       float* depth_out, cudaStream_t s) {
+  if (!n) return;
+  k_home_merge<<<blocks(n, 256), 256, 0, s>>>(n, nseg, sched, slot_of_part, pos, partial, depth,
+                                              reply, rgb, trans, depth_out);
+}
+
+void launch_segment_full(const Geo* geo, const double* o, const double* d, uint64_t n, uint8_t* nseg,
+                         uint8_t* sched, double* te, double* tx, cudaStream_t s) {
+  if (!n) return;
+  k_segment_full<<<blocks(n, 128), 128, 0, s>>>(geo, o, d, n, nseg, sched, te, tx);
+}
+
+void launch_u8_to_u16(const uint8_t* in, uint16_t* out, uint64_t n, cudaStream_t s) {
+  if (!n) return;
+  k_u8_to_u16<<<blocks(n, 256), 256, 0, s>>>(in, out, n);
+}
+
+void launch_march_points(const PartDesc* part, const uint8_t* occ, const double* o, const double* d,
+                         const double* t0, const double* t1, const uint64_t* ray_id, uint64_t n,
+                         double step, uint64_t seed, uint64_t batch_id, int jitter, uint32_t* counts,
+                         const uint64_t* offsets, double* t, double* delta, uint8_t* cascade,
+                         cudaStream_t s) {
+  if (!n) return;
+  k_march_points<<<blocks(n, 128), 128, 0, s>>>(part, occ, o, d, t0, t1, ray_id, n, step, seed,
+                                                batch_id, jitter, counts, offsets, t, delta, cascade);
+}
+
+void launch_items_to_records(uint32_t n, const float4* partial, const float* depth, const RayRec* rec,
+                             PartialRec* out, cudaStream_t s) {
+  if (!n) return;
+  k_items_to_records<<<blocks(n, 256), 256, 0, s>>>(n, partial, depth, rec, out);
+}
+
+}  // namespace dg

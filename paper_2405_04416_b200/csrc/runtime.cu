@@ -1,0 +1,1668 @@
+// runtime.cu — the C ABI (include/distgrid_b200.h): context, state, and the composed
+// per-step pipeline that replaces DistributedRun::training_step / evaluate_rays
+// (worker.cpp:730-834) and Worker::handle_training_batch (worker.cpp:251-401).
+//
+// Per step, on each rank (one GPU), for the partitions it owns:
+//   K1  segment home rays, count per destination partition, scan, pack dispatch records
+//   X1  exchange 1 (rays -> owners): all-to-all-v, then a block transpose into items
+//   K2  item setup (owner recomputes the schedule bit-exactly) + sample count, scan, fill
+//   K3  hash-grid encode (fwd)            K4  fused MLP (fwd)
+//   K5a composite -> own partial          X2  exchange 2 (partials -> every other owner)
+//   K5b merge + losses + merge/composite backward per item
+//   K4b MLP backward (weight grads, d encoding)   K3b hash-grid backward (atomics)
+//   K6  dense Adam + grad zeroing (every rank, every step, even with no rays)
+// Single-rank runs skip the all-to-all copies: the exchange buffers alias.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "geometry.cuh"
+#include "kernels.h"
+
+using namespace dg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(DG_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                     __FILE__, __LINE__);                                                 \
+  } while (0)
+
+#define TRY(call)                 \
+  do {                            \
+    int rc_ = (call);             \
+    if (rc_ != DG_OK) return rc_; \
+  } while (0)
+
+// ---------------------------------------------------------------- host layout math
+uint32_t level_resolution(uint32_t levels, uint32_t base, uint32_t maxr, uint32_t level) {
+  if (levels == 1) return base;  // grid.cpp:56-63
+  const double growth = std::exp((std::log(double(maxr)) - std::log(double(base))) / double(levels - 1));
+  return uint32_t(std::llround(double(base) * std::pow(growth, double(level))));
+}
+
+void grid_shape(const double aspect[3], uint32_t nres, uint32_t out[3]) {  // grid.cpp:65-73
+  const double n = double(nres);
+  const double s = smax(aspect[0], smax(aspect[1], aspect[2]));
+  for (int a = 0; a < 3; ++a) out[a] = uint32_t(std::ceil(aspect[a] / s * n));
+}
+
+// A device buffer that only grows.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  int ensure(size_t want) {
+    if (want <= bytes) return DG_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t n = std::max<size_t>(want + want / 4, 256);
+    if (cudaMalloc(&p, n) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(DG_ENOMEM, "cudaMalloc(%zu) failed", n);
+    }
+    bytes = n;
+    return DG_OK;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct dg_ctx {
+  dg_run_config cfg{};
+  int device = 0, rank = 0, world = 1;
+  uint32_t P = 1;
+  std::vector<uint32_t> local;          // global ids of local partitions (ascending)
+  std::vector<int> part_rank;           // rank of each global partition
+  std::vector<uint8_t> slot_of_part;    // rank-major slot of each partition
+  std::vector<uint32_t> part_of_slot;
+  std::vector<uint8_t> local_of_global; // 0xff when remote
+  Geo geo{};
+  std::vector<PartDesc> parts;
+  std::vector<FieldDesc> fields;        // [2][n_local] cascade-major
+  std::vector<uint64_t> part_param_off; // per local partition (floats, device layout)
+  std::vector<uint64_t> part_param_cnt; // flat (reference-order) count
+  std::vector<uint64_t> field_dev_off;  // [2][n_local] device offset of each field
+  std::vector<uint64_t> field_size;     // [2][n_local]
+  std::vector<std::vector<dg_array_desc>> layouts;
+  uint64_t n_params = 0;
+  uint64_t occ_bytes = 0;
+  double step = 0.0;
+  uint64_t adam_t = 0;
+  uint64_t worker_step = 0;
+  uint32_t n_images = 0, app_rows = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::unique_ptr<Comm> comm;
+  uint64_t launches = 0;
+  bool timing = false;
+  cudaEvent_t ev[12] = {};
+  dg_stage_times times{};
+
+  // persistent device state
+  DBuf d_geo, d_parts, d_fields, params, grads, adam_m, adam_v, occ, app, slot_of_part_d,
+      local_of_global_d, global_of_local_d;
+  // per-step scratch
+  DBuf h_o, h_d, h_gt, h_img, h_nseg, h_sched, h_flags, h_pos, cub_tmp, small, dropped, loss,
+      error, rec, it_te, it_tx, it_t0, it_t1, it_nseg, it_order, it_part, it_sched, it_cnt,
+      it_off, it_ncb, it_contains, it_cscan, it_partial, it_depth, part_item_off_d, s_t, s_delta,
+      s_item, s_X, s_out, s_grad, s_dX, field_off_d, tile_off_f, tile_off_b, stream_send_d,
+      stream_recv_d, send_buf, recv_buf, x_send, x_recv, out_rgb, out_T, out_depth, eval_app,
+      perm_tab;
+  // last step (introspection)
+  std::vector<uint32_t> part_item_off;   // n_local + 1
+  std::vector<uint32_t> field_off;       // 2 n_local + 1
+  uint32_t n_items = 0, n_fine = 0, n_coarse = 0;
+  bool have_last = false;
+  uint64_t h2d = 0, d2h = 0;  // bytes moved by the current call
+};
+
+namespace {
+
+int ctx_setup(dg_ctx* c) {
+  const dg_run_config& cfg = c->cfg;
+  if (cfg.kx < 1 || cfg.ky < 1) return set_err(DG_EINVAL, "split_regions: kx, ky must be >= 1");
+  if (cfg.kx * cfg.ky > DG_MAX_PARTITIONS) return set_err(DG_EINVAL, "too many partitions (max 64)");
+  if (cfg.kx + cfg.ky - 1 > DG_MAX_SEGMENTS) return set_err(DG_EINVAL, "kx + ky - 1 must be <= 16");
+  if (cfg.grid_features != 2) return set_err(DG_EINVAL, "device path requires grid_features == 2");
+  if (cfg.grid_levels < 1 || cfg.grid_levels > DG_MAX_LEVELS)
+    return set_err(DG_EINVAL, "grid_levels must be in [1, 16]");
+  if (cfg.appearance_dim > 17) return set_err(DG_EINVAL, "appearance_dim must be <= 17");
+  if (cfg.fine_table_log2 > 30 || cfg.coarse_table_log2 > 30)
+    return set_err(DG_EINVAL, "table_log2 must be <= 30");
+  if (cfg.base_resolution > cfg.max_resolution)
+    return set_err(DG_EINVAL, "grid: base_resolution must be <= max_resolution");
+  if (!(cfg.march_step_divisor > 0.0)) return set_err(DG_EINVAL, "march_step_divisor must be positive");
+  if (cfg.distortion_cross_correction)
+    return set_err(DG_EINVAL, "distortion_cross_correction is not supported on the device path");
+  if (!(cfg.transmittance_clamp > 0.0 && cfg.transmittance_clamp < 1.0))
+    return set_err(DG_EINVAL, "config: transmittance clamp must be in (0,1)");
+  c->P = cfg.kx * cfg.ky;
+  // split_regions (partition.cpp:206-252): planes computed once, shared bitwise
+  Geo& g = c->geo;
+  std::memset(&g, 0, sizeof g);
+  for (int a = 0; a < 3; ++a) {
+    g.outer_lo[a] = cfg.outer_lo[a];
+    g.outer_hi[a] = cfg.outer_hi[a];
+  }
+  for (uint32_t i = 0; i <= cfg.kx; ++i)
+    g.xp[i] = i == 0 ? cfg.inner_lo[0]
+              : i == cfg.kx ? cfg.inner_hi[0]
+                            : cfg.inner_lo[0] + (cfg.inner_hi[0] - cfg.inner_lo[0]) * double(i) / double(cfg.kx);
+  for (uint32_t i = 0; i <= cfg.ky; ++i)
+    g.yp[i] = i == 0 ? cfg.inner_lo[1]
+              : i == cfg.ky ? cfg.inner_hi[1]
+                            : cfg.inner_lo[1] + (cfg.inner_hi[1] - cfg.inner_lo[1]) * double(i) / double(cfg.ky);
+  g.kx = cfg.kx;
+  g.ky = cfg.ky;
+  g.P = c->P;
+  for (int a = 0; a < 3; ++a)
+    if (!(cfg.inner_lo[a] <= cfg.inner_hi[a]) || !(cfg.outer_lo[a] <= cfg.inner_lo[a]) ||
+        !(cfg.inner_hi[a] <= cfg.outer_hi[a]))
+      return set_err(DG_EINVAL, "manifest: fine not inside coarse");
+  // march step (worker.cpp:923-925)
+  const double ext[3] = {cfg.outer_hi[0] - cfg.outer_lo[0], cfg.outer_hi[1] - cfg.outer_lo[1],
+                         cfg.outer_hi[2] - cfg.outer_lo[2]};
+  c->step = smax(ext[0], smax(ext[1], ext[2])) / cfg.march_step_divisor;
+  // placement: partition p on rank p % world; rank-major slot order
+  c->part_rank.resize(c->P);
+  c->local_of_global.assign(c->P, 0xff);
+  for (uint32_t p = 0; p < c->P; ++p) {
+    c->part_rank[p] = int(p % uint32_t(c->world));
+    if (c->part_rank[p] == c->rank) {
+      c->local_of_global[p] = uint8_t(c->local.size());
+      c->local.push_back(p);
+    }
+  }
+  c->slot_of_part.assign(c->P, 0);
+  for (int r = 0; r < c->world; ++r)
+    for (uint32_t p = 0; p < c->P; ++p)
+      if (c->part_rank[p] == r) {
+        c->slot_of_part[p] = uint8_t(c->part_of_slot.size());
+        c->part_of_slot.push_back(p);
+      }
+  // per local partition: boxes, occupancy shapes, field layouts
+  const uint32_t nl = uint32_t(c->local.size());
+  c->parts.resize(nl);
+  c->fields.resize(2 * nl);
+  c->layouts.resize(nl);
+  c->field_dev_off.assign(2 * nl, 0);
+  c->field_size.assign(2 * nl, 0);
+  uint64_t poff = 0, ooff = 0;
+  for (uint32_t lp = 0; lp < nl; ++lp) {
+    const uint32_t gid = c->local[lp];
+    const uint32_t ix = gid % cfg.kx, iy = gid / cfg.kx;
+    PartDesc& pd = c->parts[lp];
+    std::memset(&pd, 0, sizeof pd);
+    pd.global_id = gid;
+    pd.fine_lo[0] = g.xp[ix];
+    pd.fine_lo[1] = g.yp[iy];
+    pd.fine_lo[2] = cfg.inner_lo[2];
+    pd.fine_hi[0] = g.xp[ix + 1];
+    pd.fine_hi[1] = g.yp[iy + 1];
+    pd.fine_hi[2] = cfg.inner_hi[2];
+    pd.coarse_lo[0] = ix == 0 ? cfg.outer_lo[0] : g.xp[ix];
+    pd.coarse_lo[1] = iy == 0 ? cfg.outer_lo[1] : g.yp[iy];
+    pd.coarse_lo[2] = cfg.outer_lo[2];
+    pd.coarse_hi[0] = ix == cfg.kx - 1 ? cfg.outer_hi[0] : g.xp[ix + 1];
+    pd.coarse_hi[1] = iy == cfg.ky - 1 ? cfg.outer_hi[1] : g.yp[iy + 1];
+    pd.coarse_hi[2] = cfg.outer_hi[2];
+    c->part_param_off.push_back(poff);
+    uint64_t flat = 0;  // reference-order offset within the partition
+    for (int casc = 0; casc < 2; ++casc) {
+      const double* lo = casc == 0 ? pd.fine_lo : pd.coarse_lo;
+      const double* hi = casc == 0 ? pd.fine_hi : pd.coarse_hi;
+      const double aspect[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+      // occupancy grid (grid.cpp:161-172)
+      grid_shape(aspect, cfg.occ_resolution, pd.occ_n[casc]);
+      pd.occ_off[casc] = ooff;
+      ooff += uint64_t(pd.occ_n[casc][0]) * pd.occ_n[casc][1] * pd.occ_n[casc][2];
+      ooff = (ooff + 15) & ~uint64_t(15);
+      // hash grid (grid.cpp:90-105) + MLPs (field.cpp:189-201)
+      FieldDesc& fd = c->fields[casc * nl + lp];
+      std::memset(&fd, 0, sizeof fd);
+      for (int a = 0; a < 3; ++a) {
+        fd.box_lo[a] = lo[a];
+        fd.box_hi[a] = hi[a];
+      }
+      fd.L = cfg.grid_levels;
+      fd.coarse = uint32_t(casc);
+      fd.app_dim = cfg.appearance_dim;
+      fd.part = lp;
+      fd.base = poff;
+      const uint32_t T = 1u << (casc == 0 ? cfg.fine_table_log2 : cfg.coarse_table_log2);
+      uint64_t o = 0;
+      for (uint32_t l = 0; l < cfg.grid_levels; ++l) {
+        LevelDesc& lv = fd.lv[l];
+        const uint32_t n = level_resolution(cfg.grid_levels, cfg.base_resolution, cfg.max_resolution, l);
+        grid_shape(aspect, n, lv.n);
+        const uint64_t vox = uint64_t(lv.n[0]) * lv.n[1] * lv.n[2];
+        lv.hashed = vox <= T ? 0u : 1u;
+        const uint64_t rows = lv.hashed ? T : vox;
+        lv.mask = lv.hashed ? T - 1 : 0u;
+        lv.offset = o;
+        c->layouts[lp].push_back({flat + o, rows * 2, uint32_t(casc), 0u, l, 0u});
+        o += rows * 2;
+      }
+      const uint32_t enc = cfg.grid_levels * 2, cin = 31 + cfg.appearance_dim;
+      auto add = [&](uint64_t& field_off, uint64_t size, uint32_t kind, uint32_t idx) {
+        field_off = o;
+        c->layouts[lp].push_back({flat + o, size, uint32_t(casc), kind, idx, 0u});
+        o += size;
+      };
+      add(fd.dw0, 64ull * enc, 1, 0);
+      add(fd.db0, 64, 2, 0);
+      add(fd.dw1, 16ull * 64, 1, 1);
+      add(fd.db1, 16, 2, 1);
+      add(fd.cw0, 64ull * cin, 3, 0);
+      add(fd.cb0, 64, 4, 0);
+      add(fd.cw1, 64ull * 64, 3, 1);
+      add(fd.cb1, 64, 4, 1);
+      add(fd.cw2, 3ull * 64, 3, 2);
+      add(fd.cb2, 3, 4, 2);
+      fd.size = o;
+      c->field_dev_off[casc * nl + lp] = poff;
+      c->field_size[casc * nl + lp] = o;
+      flat += o;
+      poff += o;
+      poff = (poff + 3) & ~uint64_t(3);  // 16-byte alignment of every field (float2/float4 access)
+    }
+    c->part_param_cnt.push_back(flat);
+  }
+  c->n_params = poff;
+  c->occ_bytes = std::max<uint64_t>(ooff, 16);
+  return DG_OK;
+}
+
+int upload(DBuf& b, const void* src, size_t bytes, cudaStream_t s) {
+  TRY(b.ensure(bytes ? bytes : 16));
+  if (bytes) CU(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, s));
+  return DG_OK;
+}
+
+int ctx_alloc(dg_ctx* c) {
+  cudaStream_t s = c->stream;
+  TRY(upload(c->d_geo, &c->geo, sizeof(Geo), s));
+  TRY(upload(c->d_parts, c->parts.data(), sizeof(PartDesc) * c->parts.size(), s));
+  TRY(upload(c->d_fields, c->fields.data(), sizeof(FieldDesc) * c->fields.size(), s));
+  TRY(upload(c->slot_of_part_d, c->slot_of_part.data(), c->slot_of_part.size(), s));
+  std::vector<uint8_t> gol(c->local.begin(), c->local.end());
+  TRY(upload(c->global_of_local_d, gol.data(), gol.size(), s));
+  TRY(upload(c->local_of_global_d, c->local_of_global.data(), c->local_of_global.size(), s));
+  const size_t pb = std::max<uint64_t>(c->n_params, 4) * sizeof(float);
+  for (DBuf* b : {&c->params, &c->grads, &c->adam_m, &c->adam_v}) {
+    TRY(b->ensure(pb));
+    CU(cudaMemsetAsync(b->p, 0, pb, s));
+  }
+  TRY(c->occ.ensure(c->occ_bytes));
+  CU(cudaMemsetAsync(c->occ.p, 1, c->occ_bytes, s));  // fill_occupied (worker.cpp:199-200)
+  // default appearance: one zero row for image 0
+  c->app_rows = 1;
+  c->n_images = 1;
+  TRY(c->app.ensure(64 * sizeof(float)));
+  CU(cudaMemsetAsync(c->app.p, 0, 64 * sizeof(float), s));
+  TRY(c->dropped.ensure(sizeof(unsigned long long)));
+  TRY(c->loss.ensure(sizeof(LossAccum)));
+  TRY(c->error.ensure(sizeof(uint32_t)));
+  CU(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
+template <class T>
+int exclusive_scan(dg_ctx* c, const T* in, T* out, uint64_t n) {
+  size_t tmp = 0;
+  CU(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, c->stream));
+  TRY(c->cub_tmp.ensure(tmp + 16));
+  CU(cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, in, out, n, c->stream));
+  return DG_OK;
+}
+
+void mark(dg_ctx* c, int i) {
+  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+}
+
+ItemArrays item_arrays(dg_ctx* c) {
+  ItemArrays it;
+  it.rec = c->rec.as<RayRec>();
+  it.te = c->it_te.as<double>();
+  it.tx = c->it_tx.as<double>();
+  it.t0 = c->it_t0.as<double>();
+  it.t1 = c->it_t1.as<double>();
+  it.nseg = c->it_nseg.as<uint8_t>();
+  it.order = c->it_order.as<uint8_t>();
+  it.part = c->it_part.as<uint8_t>();
+  it.sched = c->it_sched.as<uint8_t>();
+  it.cnt = c->it_cnt.as<uint32_t>();
+  it.off = c->it_off.as<uint32_t>();
+  it.ncb = c->it_ncb.as<uint32_t>();
+  it.contains = c->it_contains.as<uint32_t>();
+  it.cscan = c->it_cscan.as<uint32_t>();
+  it.partial = c->it_partial.as<float4>();
+  it.depth = c->it_depth.as<float>();
+  return it;
+}
+
+SampleArrays sample_arrays(dg_ctx* c) {
+  SampleArrays sm;
+  sm.t = c->s_t.as<double>();
+  sm.delta = c->s_delta.as<double>();
+  sm.item = c->s_item.as<uint32_t>();
+  sm.X = c->s_X.as<float>();
+  sm.out = c->s_out.as<float4>();
+  sm.grad = c->s_grad.as<float4>();
+  sm.dX = c->s_dX.as<float>();
+  return sm;
+}
+
+// Stage the batch into device buffers (host -> device when mem == HOST).
+int stage_batch(dg_ctx* c, const dg_ray_batch* b, const double*& o, const double*& d,
+                const float*& gt, const uint32_t*& img) {
+  const uint64_t n = b->n;
+  if (b->mem == DG_MEM_DEVICE) {
+    o = b->origin;
+    d = b->dir;
+    gt = b->color_gt;
+    img = b->image_id;
+    return DG_OK;
+  }
+  cudaStream_t s = c->stream;
+  c->h2d += n * 48 + (b->color_gt ? n * 12 : 0) + (b->image_id ? n * 4 : 0);
+  TRY(c->h_o.ensure(n * 24 + 16));
+  TRY(c->h_d.ensure(n * 24 + 16));
+  if (n) CU(cudaMemcpyAsync(c->h_o.p, b->origin, n * 24, cudaMemcpyHostToDevice, s));
+  if (n) CU(cudaMemcpyAsync(c->h_d.p, b->dir, n * 24, cudaMemcpyHostToDevice, s));
+  o = c->h_o.as<double>();
+  d = c->h_d.as<double>();
+  gt = nullptr;
+  img = nullptr;
+  if (b->color_gt) {
+    TRY(c->h_gt.ensure(n * 12 + 16));
+    if (n) CU(cudaMemcpyAsync(c->h_gt.p, b->color_gt, n * 12, cudaMemcpyHostToDevice, s));
+    gt = c->h_gt.as<float>();
+  }
+  if (b->image_id) {
+    TRY(c->h_img.ensure(n * 4 + 16));
+    if (n) CU(cudaMemcpyAsync(c->h_img.p, b->image_id, n * 4, cudaMemcpyHostToDevice, s));
+    img = c->h_img.as<uint32_t>();
+  }
+  return DG_OK;
+}
+
+// Block transpose between [a][b] and [b][a] layouts of fixed-size records (8-byte words).
+__global__ void k_block_permute(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst,
+                                uint32_t words, const uint64_t* __restrict__ tab, uint32_t nblk,
+                                uint64_t total) {
+  // tab: [nblk] src start, [nblk] dst start, [nblk] count (records)
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= total) return;
+  uint32_t b = 0;
+  while (b + 1 < nblk && r >= tab[b + 1]) ++b;
+  const uint64_t k = r - tab[b];
+  const uint64_t so = tab[b] + k, dof = tab[nblk + b] + k;
+  for (uint32_t w = 0; w < words; ++w) dst[dof * words + w] = src[so * words + w];
+}
+
+// Runs the K1/X1/K2 front half shared by train and render.  On return the items and
+// sample arrays are filled (march done) and c->part_item_off / c->field_off describe them.
+int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, uint64_t* dropped_out,
+               uint64_t* bytes_sent) {
+  cudaStream_t s = c->stream;
+  const uint64_t n = b->n;
+  const uint32_t P = c->P, nl = uint32_t(c->local.size());
+  const double* o;
+  const double* d;
+  const float* gt;
+  const uint32_t* img;
+  TRY(stage_batch(c, b, o, d, gt, img));
+  mark(c, 0);
+  // ---- K1: segment home rays ----
+  const uint64_t nf = uint64_t(P) * n + 1;
+  TRY(c->h_nseg.ensure(n + 16));
+  TRY(c->h_sched.ensure(n * kMaxSeg + 16));
+  TRY(c->h_flags.ensure(nf * 4));
+  TRY(c->h_pos.ensure(nf * 4));
+  CU(cudaMemsetAsync(c->h_flags.p, 0, nf * 4, s));
+  CU(cudaMemsetAsync(c->dropped.p, 0, 8, s));
+  CU(cudaMemsetAsync(c->error.p, 0, 4, s));
+  launch_segment_home(c->d_geo.as<Geo>(), o, d, n, c->slot_of_part_d.as<uint8_t>(),
+                      c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(), c->h_flags.as<uint32_t>(),
+                      c->dropped.as<unsigned long long>(), s);
+  ++c->launches;
+  TRY(exclusive_scan(c, c->h_flags.as<uint32_t>(), c->h_pos.as<uint32_t>(), nf));
+  // per-slot dispatch counts: pos[slot * n] for slot = 0..P
+  TRY(c->small.ensure(4096 * 4));
+  std::vector<uint32_t> slot_start(P + 1);
+  CU(cudaMemcpy2DAsync(slot_start.data(), 4, c->h_pos.as<uint32_t>(), n ? n * 4 : 4, 4, P + 1,
+                       cudaMemcpyDeviceToHost, s));
+  unsigned long long dropped = 0;
+  CU(cudaMemcpyAsync(&dropped, c->dropped.p, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  c->d2h += (P + 1) * 4 + 8;
+  if (n == 0)
+    for (auto& v : slot_start) v = 0;
+  *dropped_out = dropped;
+  std::vector<uint64_t> send_cnt(P);  // records to each partition (by global id)
+  for (uint32_t p = 0; p < P; ++p)
+    send_cnt[p] = slot_start[c->slot_of_part[p] + 1] - slot_start[c->slot_of_part[p]];
+  const uint64_t total_send = slot_start[P];
+  // ---- X1: dispatch ----
+  std::vector<uint32_t> pio(nl + 1, 0);
+  uint64_t n_items = 0;
+  if (c->world == 1) {
+    for (uint32_t lp = 0; lp < nl; ++lp) pio[lp + 1] = pio[lp] + uint32_t(send_cnt[c->local[lp]]);
+    n_items = total_send;
+    TRY(c->rec.ensure(n_items * sizeof(RayRec) + 16));
+    launch_pack_dispatch(n, P, c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(),
+                         c->slot_of_part_d.as<uint8_t>(), c->h_pos.as<uint32_t>(), o, d, gt, img,
+                         b->first_ray_id, c->rec.as<RayRec>(), s);
+    ++c->launches;
+  } else {
+    const int W = c->world;
+    TRY(c->x_send.ensure(total_send * sizeof(RayRec) + 16));
+    launch_pack_dispatch(n, P, c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(),
+                         c->slot_of_part_d.as<uint8_t>(), c->h_pos.as<uint32_t>(), o, d, gt, img,
+                         b->first_ray_id, c->x_send.as<RayRec>(), s);
+    ++c->launches;
+    // counts exchange: every rank sends its full per-partition count vector to every peer
+    std::vector<uint64_t> cnt_send(uint64_t(W) * P), cnt_recv(uint64_t(W) * P);
+    for (int r = 0; r < W; ++r)
+      for (uint32_t p = 0; p < P; ++p) cnt_send[uint64_t(r) * P + p] = send_cnt[p];
+    TRY(c->send_buf.ensure(cnt_send.size() * 8));
+    TRY(c->recv_buf.ensure(cnt_recv.size() * 8));
+    CU(cudaMemcpyAsync(c->send_buf.p, cnt_send.data(), cnt_send.size() * 8, cudaMemcpyHostToDevice, s));
+    std::vector<uint64_t> sb(W, uint64_t(P) * 8), rb(W, uint64_t(P) * 8);
+    std::string err;
+    int rc = c->comm->alltoallv(c->send_buf.p, sb, c->recv_buf.p, rb, s, err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    CU(cudaMemcpyAsync(cnt_recv.data(), c->recv_buf.p, cnt_recv.size() * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    c->h2d += cnt_send.size() * 8;
+    c->d2h += cnt_recv.size() * 8;
+    // cnt_recv[src][p]: records src sends to partition p
+    std::vector<uint64_t> sbytes(W, 0), rbytes(W, 0);
+    for (uint32_t p = 0; p < P; ++p) sbytes[c->part_rank[p]] += send_cnt[p] * sizeof(RayRec);
+    for (int r = 0; r < W; ++r)
+      for (uint32_t lp = 0; lp < nl; ++lp) rbytes[r] += cnt_recv[uint64_t(r) * P + c->local[lp]] * sizeof(RayRec);
+    uint64_t rtotal = 0;
+    for (int r = 0; r < W; ++r) rtotal += rbytes[r];
+    n_items = rtotal / sizeof(RayRec);
+    TRY(c->x_recv.ensure(rtotal + 16));
+    rc = c->comm->alltoallv(c->x_send.p, sbytes, c->x_recv.p, rbytes, s, err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    for (int r = 0; r < W; ++r)
+      if (r != c->rank) *bytes_sent += sbytes[r];
+    // transpose [src][lp] -> [lp][src]
+    for (uint32_t lp = 0; lp < nl; ++lp) {
+      uint64_t t = 0;
+      for (int r = 0; r < W; ++r) t += cnt_recv[uint64_t(r) * P + c->local[lp]];
+      pio[lp + 1] = pio[lp] + uint32_t(t);
+    }
+    std::vector<uint64_t> tab;
+    const uint32_t nblk = nl * uint32_t(W);
+    std::vector<uint64_t> src_start(nblk), dst_start(nblk);
+    uint64_t acc = 0;
+    for (int r = 0; r < W; ++r)  // recv layout [src][lp]
+      for (uint32_t lp = 0; lp < nl; ++lp) {
+        src_start[uint64_t(r) * nl + lp] = acc;
+        acc += cnt_recv[uint64_t(r) * P + c->local[lp]];
+      }
+    // blocks enumerated in recv order; dst offsets in [lp][src]
+    std::vector<uint64_t> dst_off_lp(nl, 0);
+    for (uint32_t lp = 0; lp < nl; ++lp) dst_off_lp[lp] = pio[lp];
+    std::vector<uint64_t> run(nl, 0);
+    for (int r = 0; r < W; ++r)
+      for (uint32_t lp = 0; lp < nl; ++lp) {
+        dst_start[uint64_t(r) * nl + lp] = dst_off_lp[lp] + run[lp];
+        run[lp] += cnt_recv[uint64_t(r) * P + c->local[lp]];
+      }
+    tab.insert(tab.end(), src_start.begin(), src_start.end());
+    tab.insert(tab.end(), dst_start.begin(), dst_start.end());
+    TRY(upload(c->perm_tab, tab.data(), tab.size() * 8, s));
+    TRY(c->rec.ensure(n_items * sizeof(RayRec) + 16));
+    if (n_items) {
+      k_block_permute<<<unsigned((n_items + 255) / 256), 256, 0, s>>>(
+          c->x_recv.as<uint64_t>(), c->rec.as<uint64_t>(), sizeof(RayRec) / 8,
+          c->perm_tab.as<uint64_t>(), nblk, n_items);
+      ++c->launches;
+    }
+  }
+  mark(c, 1);
+  // ---- K2: item setup + counts ----
+  const uint32_t NI = uint32_t(n_items);
+  c->n_items = NI;
+  c->part_item_off = pio;
+  TRY(upload(c->part_item_off_d, pio.data(), pio.size() * 4, s));
+  c->h2d += pio.size() * 4;
+  TRY(c->it_te.ensure(uint64_t(NI) * 8 + 16));
+  TRY(c->it_tx.ensure(uint64_t(NI) * 8 + 16));
+  TRY(c->it_t0.ensure(uint64_t(NI) * 8 + 16));
+  TRY(c->it_t1.ensure(uint64_t(NI) * 8 + 16));
+  TRY(c->it_nseg.ensure(NI + 16));
+  TRY(c->it_order.ensure(NI + 16));
+  TRY(c->it_part.ensure(NI + 16));
+  TRY(c->it_sched.ensure(uint64_t(NI) * kMaxSeg + 16));
+  TRY(c->it_cnt.ensure((2ull * NI + 1) * 4));
+  TRY(c->it_off.ensure((2ull * NI + 1) * 4));
+  TRY(c->it_ncb.ensure(uint64_t(NI) * 4 + 16));
+  TRY(c->it_contains.ensure((uint64_t(P) * NI + 1) * 4));
+  TRY(c->it_cscan.ensure((uint64_t(P) * NI + 1) * 4));
+  TRY(c->it_partial.ensure(uint64_t(NI) * 16 + 16));
+  TRY(c->it_depth.ensure(uint64_t(NI) * 4 + 16));
+  CU(cudaMemsetAsync(c->it_cnt.as<uint32_t>() + 2ull * NI, 0, 4, s));
+  CU(cudaMemsetAsync(c->it_contains.as<uint32_t>() + uint64_t(P) * NI, 0, 4, s));
+  ItemArrays it = item_arrays(c);
+  launch_item_setup(c->d_geo.as<Geo>(), c->d_parts.as<PartDesc>(), c->occ.as<uint8_t>(),
+                    c->part_item_off_d.as<uint32_t>(), nl, NI, it, P, c->step, c->cfg.seed,
+                    batch_id, train, int(c->cfg.wire_f32), c->app_rows, c->error.as<uint32_t>(), s);
+  ++c->launches;
+  TRY(exclusive_scan(c, c->it_cnt.as<uint32_t>(), c->it_off.as<uint32_t>(), 2ull * NI + 1));
+  if (train && P > 1)
+    TRY(exclusive_scan(c, c->it_contains.as<uint32_t>(), c->it_cscan.as<uint32_t>(),
+                       uint64_t(P) * NI + 1));
+  // field sample ranges: off[pio[lp]] (fine) and off[NI + pio[lp]] (coarse), lp = 0..nl
+  std::vector<uint32_t> fo(2 * (nl + 1));
+  for (uint32_t k = 0; k <= nl; ++k) {
+    CU(cudaMemcpyAsync(&fo[k], c->it_off.as<uint32_t>() + pio[k], 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&fo[nl + 1 + k], c->it_off.as<uint32_t>() + NI + pio[k], 4,
+                       cudaMemcpyDeviceToHost, s));
+  }
+  uint32_t err_flag = 0;
+  CU(cudaMemcpyAsync(&err_flag, c->error.p, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  c->d2h += fo.size() * 4 + 4;
+  if (err_flag & 1u) return set_err(DG_ERANGE, "appearance: unknown image id");
+  if (err_flag & 2u) return set_err(DG_EPROTO, "worker: dispatched ray does not intersect this region");
+  // fields: [fine lp 0..nl-1][coarse lp 0..nl-1]
+  c->field_off.assign(2 * nl + 1, 0);
+  for (uint32_t lp = 0; lp < nl; ++lp) c->field_off[lp] = fo[lp];
+  for (uint32_t lp = 0; lp < nl; ++lp) c->field_off[nl + lp] = fo[nl + 1 + lp];
+  c->field_off[2 * nl] = fo[2 * nl + 1];
+  c->n_fine = fo[nl];
+  c->n_coarse = fo[2 * nl + 1] - fo[nl];
+  const uint64_t NS = uint64_t(c->n_fine) + c->n_coarse;
+  TRY(c->s_t.ensure(NS * 8 + 16));
+  TRY(c->s_delta.ensure(NS * 8 + 16));
+  TRY(c->s_item.ensure(NS * 4 + 16));
+  TRY(c->s_X.ensure(NS * kEnc * 4 + 16));
+  TRY(c->s_out.ensure(NS * 16 + 16));
+  TRY(c->s_grad.ensure(NS * 16 + 16));
+  TRY(c->s_dX.ensure(NS * kEnc * 4 + 16));
+  SampleArrays sm = sample_arrays(c);
+  launch_march_fill(c->d_parts.as<PartDesc>(), c->occ.as<uint8_t>(), NI, it, sm, c->n_fine,
+                    c->step, c->cfg.seed, batch_id, train, s);
+  ++c->launches;
+  // tile tables
+  std::vector<uint32_t> tf(2 * nl + 1, 0), tb(2 * nl + 1, 0);
+  for (uint32_t f = 0; f < 2 * nl; ++f) {
+    const uint32_t cnt = c->field_off[f + 1] - c->field_off[f];
+    tf[f + 1] = tf[f] + (cnt + 127) / 128;
+    tb[f + 1] = tb[f] + (cnt + 63) / 64;
+  }
+  TRY(upload(c->field_off_d, c->field_off.data(), c->field_off.size() * 4, s));
+  TRY(upload(c->tile_off_f, tf.data(), tf.size() * 4, s));
+  TRY(upload(c->tile_off_b, tb.data(), tb.size() * 4, s));
+  c->h2d += (c->field_off.size() + tf.size() + tb.size()) * 4;
+  mark(c, 2);
+  c->have_last = true;
+  return DG_OK;
+}
+
+FieldLaunch field_launch(dg_ctx* c) {
+  FieldLaunch f{};
+  f.fields = c->d_fields.as<FieldDesc>();
+  f.parts = c->d_parts.as<PartDesc>();
+  f.rec = c->rec.as<RayRec>();
+  f.item_part = c->it_part.as<uint8_t>();
+  f.s_t = c->s_t.as<double>();
+  f.s_item = c->s_item.as<uint32_t>();
+  f.fine_total = c->n_fine;
+  f.n_total = c->n_fine + c->n_coarse;
+  f.n_local = uint32_t(c->local.size());
+  f.params = c->params.as<float>();
+  f.grads = c->grads.as<float>();
+  return f;
+}
+
+MlpLaunch mlp_launch(dg_ctx* c, bool bwd) {
+  MlpLaunch m{};
+  m.fields = c->d_fields.as<FieldDesc>();
+  m.n_fields = uint32_t(2 * c->local.size());
+  m.field_off = c->field_off_d.as<uint32_t>();
+  std::vector<uint32_t> dummy;
+  const uint32_t nl = uint32_t(c->local.size());
+  uint32_t tiles = 0;
+  for (uint32_t f = 0; f < 2 * nl; ++f) {
+    const uint32_t cnt = c->field_off[f + 1] - c->field_off[f];
+    tiles += bwd ? (cnt + 63) / 64 : (cnt + 127) / 128;
+  }
+  m.tile_off = bwd ? c->tile_off_b.as<uint32_t>() : c->tile_off_f.as<uint32_t>();
+  m.n_tiles = tiles;
+  m.X = c->s_X.as<float>();
+  m.rec = c->rec.as<RayRec>();
+  m.s_item = c->s_item.as<uint32_t>();
+  m.app_table = c->app.as<float>();
+  m.params = c->params.as<float>();
+  m.grads = c->grads.as<float>();
+  m.out = c->s_out.as<float4>();
+  m.grad_in = c->s_grad.as<float4>();
+  m.dX = c->s_dX.as<float>();
+  return m;
+}
+
+// Exchange-2 stream tables.  Stream (q -> p) carries the partials of q's items whose
+// schedule contains p, in ray order; pair_cnt[lq][p] is known locally and is symmetric.
+int exchange_partials(dg_ctx* c, const std::vector<uint32_t>& pair_cnt, uint64_t* bytes_sent,
+                      const PartialRec** recv_out) {
+  cudaStream_t s = c->stream;
+  const uint32_t P = c->P, nl = uint32_t(c->local.size());
+  const int W = c->world;
+  auto cnt = [&](uint32_t q, uint32_t p) -> uint64_t {  // records in stream q -> p
+    if (c->local_of_global[q] != 0xff) return pair_cnt[uint64_t(c->local_of_global[q]) * P + p];
+    return pair_cnt[uint64_t(c->local_of_global[p]) * P + q];  // symmetric
+  };
+  std::vector<uint64_t> send_off(uint64_t(P) * P, 0), recv_off(uint64_t(P) * P, 0);
+  std::vector<uint64_t> sbytes(W, 0), rbytes(W, 0);
+  uint64_t so = 0, ro = 0;
+  for (int r = 0; r < W; ++r) {  // send layout: [dest r][q local][p on r]
+    const uint64_t start = so;
+    for (uint32_t lq = 0; lq < nl; ++lq)
+      for (uint32_t p = 0; p < P; ++p)
+        if (c->part_rank[p] == r && p != c->local[lq]) {
+          send_off[uint64_t(c->local[lq]) * P + p] = so;
+          so += cnt(c->local[lq], p);
+        }
+    sbytes[r] = (so - start) * sizeof(PartialRec);
+  }
+  for (int r = 0; r < W; ++r) {  // recv layout: [src r][q on r][p local]
+    const uint64_t start = ro;
+    for (uint32_t q = 0; q < P; ++q)
+      if (c->part_rank[q] == r)
+        for (uint32_t lp = 0; lp < nl; ++lp)
+          if (q != c->local[lp]) {
+            recv_off[uint64_t(q) * P + c->local[lp]] = ro;
+            ro += cnt(q, c->local[lp]);
+          }
+    rbytes[r] = (ro - start) * sizeof(PartialRec);
+  }
+  TRY(upload(c->stream_send_d, send_off.data(), send_off.size() * 8, s));
+  TRY(upload(c->stream_recv_d, recv_off.data(), recv_off.size() * 8, s));
+  c->h2d += (send_off.size() + recv_off.size()) * 8;
+  TRY(c->send_buf.ensure(so * sizeof(PartialRec) + 16));
+  launch_pack_partials(c->n_items, item_arrays(c), c->part_item_off_d.as<uint32_t>(),
+                       c->global_of_local_d.as<uint8_t>(), c->stream_send_d.as<uint64_t>(), P,
+                       c->send_buf.as<PartialRec>(), s);
+  ++c->launches;
+  if (W == 1) {
+    *recv_out = c->send_buf.as<PartialRec>();  // single rank: the streams alias
+    return DG_OK;
+  }
+  TRY(c->recv_buf.ensure(ro * sizeof(PartialRec) + 16));
+  std::string err;
+  const int rc = c->comm->alltoallv(c->send_buf.p, sbytes, c->recv_buf.p, rbytes, s, err);
+  if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+  for (int r = 0; r < W; ++r)
+    if (r != c->rank) *bytes_sent += sbytes[r];
+  *recv_out = c->recv_buf.as<PartialRec>();
+  return DG_OK;
+}
+
+template <class T>
+int d2h(std::vector<T>& v, const void* src, uint64_t n, cudaStream_t s) {
+  v.resize(n);
+  if (n) CU(cudaMemcpyAsync(v.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  return DG_OK;
+}
+
+int check_ctx(const dg_ctx* c) {
+  if (!c) return set_err(DG_EINVAL, "null context");
+  return DG_OK;
+}
+
+int check_part(const dg_ctx* c, uint32_t partition, uint32_t* lp) {
+  TRY(check_ctx(c));
+  if (partition >= c->P) return set_err(DG_ERANGE, "partition %u out of range", partition);
+  if (c->local_of_global[partition] == 0xff)
+    return set_err(DG_EINVAL, "partition %u is not owned by rank %d", partition, c->rank);
+  *lp = c->local_of_global[partition];
+  return DG_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+int dg_abi_version(void) { return DG_ABI_VERSION; }
+
+void dg_default_config(dg_run_config* c) {
+  std::memset(c, 0, sizeof *c);
+  for (int a = 0; a < 3; ++a) {
+    c->inner_lo[a] = c->outer_lo[a] = 0.0;
+    c->inner_hi[a] = c->outer_hi[a] = 1.0;
+  }
+  c->kx = c->ky = 1;
+  c->grid_levels = 8;
+  c->grid_features = 2;
+  c->base_resolution = 16;
+  c->max_resolution = 512;
+  c->fine_table_log2 = 15;
+  c->coarse_table_log2 = 12;
+  c->appearance_dim = 16;
+  c->march_step_divisor = 1024.0;
+  c->occ_resolution = 128;
+  c->occ_decay = 0.99;
+  c->occ_warmup_steps = 4096;
+  c->occ_update_interval = 16;
+  c->occ_threshold_early = 0.6;
+  c->occ_threshold_late = 60.0;
+  c->occ_threshold_switch_step = 10000;
+  c->occ_threshold_scale = 1.0;
+  c->seed = 1;
+  c->total_steps = 20000;
+  c->lr_start = 0.05;
+  c->lr_end = 0.005;
+  c->lambda_transmittance = 1e-3;
+  c->lambda_distortion = 1e-3;
+  c->transmittance_clamp = 1e-6;
+  c->adam_beta1 = 0.9;
+  c->adam_beta2 = 0.99;
+  c->adam_eps = 1e-15;
+  c->occupancy_updates = 1;
+}
+
+double dg_lr_at(const dg_run_config* cfg, uint64_t step) {  // train.cpp:77-80
+  const double progress = cfg->total_steps == 0 ? 1.0 : double(step) / double(cfg->total_steps);
+  return cfg->lr_end + 0.5 * (cfg->lr_start - cfg->lr_end) * (1.0 + std::cos(M_PI * progress));
+}
+
+int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_ctx** out) {
+  if (!cfg || !out) return set_err(DG_EINVAL, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return set_err(DG_EINVAL, "bad rank/world");
+  auto c = std::make_unique<dg_ctx>();
+  c->cfg = *cfg;
+  c->rank = rank;
+  c->world = world;
+  if (device < 0) CU(cudaGetDevice(&device));
+  c->device = device;
+  CU(cudaSetDevice(device));
+  CU(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  TRY(ctx_setup(c.get()));
+  CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  for (auto& e : c->ev) CU(cudaEventCreate(&e));
+  TRY(ctx_alloc(c.get()));
+  *out = c.release();
+  return DG_OK;
+}
+
+int dg_ctx_destroy(dg_ctx* c) {
+  if (!c) return DG_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  cudaStream_t s = c->stream;
+  delete c;
+  if (s) cudaStreamDestroy(s);
+  return DG_OK;
+}
+
+int dg_partition_count(const dg_ctx* c, uint32_t* n_total, uint32_t* n_local) {
+  TRY(check_ctx(c));
+  if (n_total) *n_total = c->P;
+  if (n_local) *n_local = uint32_t(c->local.size());
+  return DG_OK;
+}
+
+int dg_partition_rank(const dg_ctx* c, uint32_t p, int* rank) {
+  TRY(check_ctx(c));
+  if (p >= c->P) return set_err(DG_ERANGE, "partition out of range");
+  *rank = c->part_rank[p];
+  return DG_OK;
+}
+
+int dg_march_step(const dg_ctx* c, double* step) {
+  TRY(check_ctx(c));
+  *step = c->step;
+  return DG_OK;
+}
+
+int dg_region_boxes(const dg_ctx* c, uint32_t p, double fl[3], double fh[3], double cl[3], double ch[3]) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  const PartDesc& pd = c->parts[lp];
+  for (int a = 0; a < 3; ++a) {
+    fl[a] = pd.fine_lo[a];
+    fh[a] = pd.fine_hi[a];
+    cl[a] = pd.coarse_lo[a];
+    ch[a] = pd.coarse_hi[a];
+  }
+  return DG_OK;
+}
+
+int dg_grid_levels(const dg_ctx* c, uint32_t p, uint32_t cascade, uint32_t* shapes, uint32_t* modes,
+                   uint64_t* rows) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  const FieldDesc& fd = c->fields[cascade * c->local.size() + lp];
+  for (uint32_t l = 0; l < fd.L; ++l) {
+    for (int a = 0; a < 3; ++a) shapes[3 * l + a] = fd.lv[l].n[a];
+    if (modes) modes[l] = fd.lv[l].hashed;
+    if (rows) rows[l] = fd.lv[l].hashed ? uint64_t(fd.lv[l].mask) + 1
+                                        : uint64_t(fd.lv[l].n[0]) * fd.lv[l].n[1] * fd.lv[l].n[2];
+  }
+  return DG_OK;
+}
+
+int dg_param_count(const dg_ctx* c, uint32_t p, uint64_t* n) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  *n = c->part_param_cnt[lp];
+  return DG_OK;
+}
+
+int dg_param_layout(const dg_ctx* c, uint32_t p, dg_array_desc* arrays, uint32_t capacity, uint32_t* n) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  const auto& L = c->layouts[lp];
+  *n = uint32_t(L.size());
+  for (uint32_t i = 0; i < L.size() && i < capacity; ++i) arrays[i] = L[i];
+  return DG_OK;
+}
+
+// Flat (reference-order, fine then coarse) <-> device layout (each field 16-byte aligned).
+static int copy_part(dg_ctx* c, uint32_t p, DBuf& buf, float* host, const float* in) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  const size_t nl = c->local.size();
+  uint64_t flat = 0;
+  for (int casc = 0; casc < 2; ++casc) {
+    float* dev = buf.as<float>() + c->field_dev_off[casc * nl + lp];
+    const size_t bytes = c->field_size[casc * nl + lp] * sizeof(float);
+    if (in) CU(cudaMemcpyAsync(dev, in + flat, bytes, cudaMemcpyHostToDevice, c->stream));
+    else CU(cudaMemcpyAsync(host + flat, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    flat += c->field_size[casc * nl + lp];
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+int dg_set_params(dg_ctx* c, uint32_t p, const float* in) { return copy_part(c, p, c->params, nullptr, in); }
+int dg_get_params(dg_ctx* c, uint32_t p, float* out) { return copy_part(c, p, c->params, out, nullptr); }
+int dg_get_grads(dg_ctx* c, uint32_t p, float* out) { return copy_part(c, p, c->grads, out, nullptr); }
+
+int dg_zero_grads(dg_ctx* c) {
+  TRY(check_ctx(c));
+  CU(cudaMemsetAsync(c->grads.p, 0, c->n_params * sizeof(float), c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+int dg_set_adam(dg_ctx* c, uint32_t p, const float* m, const float* v, uint64_t t) {
+  TRY(copy_part(c, p, c->adam_m, nullptr, m));
+  TRY(copy_part(c, p, c->adam_v, nullptr, v));
+  c->adam_t = t;
+  return DG_OK;
+}
+
+int dg_get_adam(dg_ctx* c, uint32_t p, float* m, float* v, uint64_t* t) {
+  TRY(copy_part(c, p, c->adam_m, m, nullptr));
+  TRY(copy_part(c, p, c->adam_v, v, nullptr));
+  if (t) *t = c->adam_t;
+  return DG_OK;
+}
+
+int dg_set_step(dg_ctx* c, uint64_t step) {
+  TRY(check_ctx(c));
+  c->worker_step = step;
+  return DG_OK;
+}
+
+int dg_get_step(const dg_ctx* c, uint64_t* step) {
+  TRY(check_ctx(c));
+  *step = c->worker_step;
+  return DG_OK;
+}
+
+// worker.cpp:186-190: Rng(counter_hash(seed, 0xf1e1d|0xc0a45e, region)); grid levels in order
+// (uniform[-1e-4,1e-4]), then each MLP layer's weights (Xavier bound), biases zero.
+int dg_init_params_reference(dg_ctx* c, uint32_t p) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  std::vector<float> host(c->part_param_cnt[lp], 0.0f);
+  for (int casc = 0; casc < 2; ++casc) {
+    const uint64_t salt = casc == 0 ? 0xf1e1dull : 0xc0a45eull;
+    std::mt19937_64 eng(splitmix64(counter_hash(c->cfg.seed, salt, p, 0)));
+    auto uni = [&](double lo, double hi) {
+      return lo + (hi - lo) * (double(eng() >> 11) * 0x1.0p-53);
+    };
+    const FieldDesc& fd = c->fields[casc * c->local.size() + lp];
+    const uint64_t fb = casc == 0 ? 0 : c->field_size[lp];
+    for (uint32_t l = 0; l < fd.L; ++l) {
+      const LevelDesc& lv = fd.lv[l];
+      const uint64_t rows = lv.hashed ? uint64_t(lv.mask) + 1 : uint64_t(lv.n[0]) * lv.n[1] * lv.n[2];
+      for (uint64_t k = 0; k < rows * 2; ++k) host[fb + lv.offset + k] = float(uni(-1e-4, 1e-4));
+    }
+    const uint32_t enc = fd.L * 2, cin = 31 + fd.app_dim;
+    struct L3 {
+      uint64_t off;
+      uint32_t in, out;
+    } layers[] = {{fd.dw0, enc, 64}, {fd.dw1, 64, 16}, {fd.cw0, cin, 64}, {fd.cw1, 64, 64}, {fd.cw2, 64, 3}};
+    for (const L3& L : layers) {
+      const double bound = std::sqrt(6.0 / double(L.in + L.out));
+      for (uint64_t k = 0; k < uint64_t(L.in) * L.out; ++k) host[fb + L.off + k] = float(uni(-bound, bound));
+    }
+  }
+  return dg_set_params(c, p, host.data());
+}
+
+int dg_init_params_fast(dg_ctx* c, uint32_t p, uint64_t seed) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  float* base = c->params.as<float>();
+  for (int casc = 0; casc < 2; ++casc) {
+    const FieldDesc& fd = c->fields[casc * c->local.size() + lp];
+    const uint64_t grid_floats = fd.dw0;
+    launch_fill_uniform(base + fd.base, grid_floats, -1e-4f, 1e-4f, counter_hash(seed, p, casc, 1), c->stream);
+    const uint32_t enc = fd.L * 2, cin = 31 + fd.app_dim;
+    struct L3 {
+      uint64_t w, b;
+      uint32_t in, out;
+    } layers[] = {{fd.dw0, fd.db0, enc, 64}, {fd.dw1, fd.db1, 64, 16}, {fd.cw0, fd.cb0, cin, 64},
+                  {fd.cw1, fd.cb1, 64, 64}, {fd.cw2, fd.cb2, 64, 3}};
+    int li = 0;
+    for (const L3& L : layers) {
+      const float bound = float(std::sqrt(6.0 / double(L.in + L.out)));
+      launch_fill_uniform(base + fd.base + L.w, uint64_t(L.in) * L.out, -bound, bound,
+                          counter_hash(seed, p, casc, 100 + li++), c->stream);
+      CU(cudaMemsetAsync(base + fd.base + L.b, 0, L.out * sizeof(float), c->stream));
+    }
+  }
+  c->launches += 12;
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+int dg_occupancy_shape(const dg_ctx* c, uint32_t p, uint32_t cascade, uint32_t shape[3]) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  for (int a = 0; a < 3; ++a) shape[a] = c->parts[lp].occ_n[cascade][a];
+  return DG_OK;
+}
+
+static int occ_copy(dg_ctx* c, uint32_t p, uint32_t cascade, uint8_t* out, const uint8_t* in) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  const PartDesc& pd = c->parts[lp];
+  const uint64_t n = uint64_t(pd.occ_n[cascade][0]) * pd.occ_n[cascade][1] * pd.occ_n[cascade][2];
+  uint8_t* dev = c->occ.as<uint8_t>() + pd.occ_off[cascade];
+  if (in) CU(cudaMemcpyAsync(dev, in, n, cudaMemcpyHostToDevice, c->stream));
+  else CU(cudaMemcpyAsync(out, dev, n, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+int dg_set_occupancy(dg_ctx* c, uint32_t p, uint32_t cascade, const uint8_t* bits) {
+  return occ_copy(c, p, cascade, nullptr, bits);
+}
+int dg_get_occupancy(dg_ctx* c, uint32_t p, uint32_t cascade, uint8_t* bits) {
+  return occ_copy(c, p, cascade, bits, nullptr);
+}
+
+int dg_set_appearance(dg_ctx* c, const uint32_t* ids, const float* rows, uint32_t n) {
+  TRY(check_ctx(c));
+  uint32_t max_id = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (ids[i] >= (1u << 20)) return set_err(DG_ERANGE, "appearance: image id >= 2^20");
+    max_id = std::max(max_id, ids[i]);
+  }
+  const uint32_t d = c->cfg.appearance_dim;
+  const uint32_t nrows = n ? max_id + 1 : 1;
+  std::vector<float> table(uint64_t(nrows) * d + 16, 0.0f);
+  for (uint32_t i = 0; i < n; ++i)
+    std::memcpy(&table[uint64_t(ids[i]) * d], rows + uint64_t(i) * d, d * sizeof(float));
+  TRY(upload(c->app, table.data(), table.size() * sizeof(float), c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  c->app_rows = n ? nrows : 0;  // ids with no row are rejected in the step (DG_ERANGE)
+  c->n_images = n;
+  return DG_OK;
+}
+
+int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats* stats) {
+  TRY(check_ctx(c));
+  if (!b) return set_err(DG_EINVAL, "null batch");
+  if (b->n && (!b->origin || !b->dir || !b->color_gt)) return set_err(DG_EINVAL, "batch: missing arrays");
+  if (b->n >= (1ull << 32) || b->first_ray_id + b->n > (1ull << 32))
+    return set_err(DG_EINVAL, "batch: ray ids must fit in 32 bits");
+  if (c->world > 1 && !c->comm) return set_err(DG_EINVAL, "world > 1 needs dg_comm_init_*");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const uint32_t P = c->P, nl = uint32_t(c->local.size());
+  uint64_t dropped = 0, bytes = 0;
+  c->h2d = c->d2h = 0;
+  TRY(front_half(c, b, 1, step, &dropped, &bytes));
+  const uint32_t NI = c->n_items;
+  ItemArrays it = item_arrays(c);
+  SampleArrays sm = sample_arrays(c);
+  // pair counts for exchange 2 (P > 1)
+  std::vector<uint32_t> pair_cnt(uint64_t(nl) * P, 0);
+  if (P > 1 && NI) {
+    TRY(c->small.ensure(uint64_t(nl) * P * 4 + 16));
+    launch_pair_counts(NI, nl, P, c->part_item_off_d.as<uint32_t>(), nullptr,
+                       c->it_cscan.as<uint32_t>(), c->small.as<uint32_t>(), s);
+    ++c->launches;
+    CU(cudaMemcpyAsync(pair_cnt.data(), c->small.p, pair_cnt.size() * 4, cudaMemcpyDeviceToHost, s));
+    c->d2h += pair_cnt.size() * 4;
+  }
+  CU(cudaMemsetAsync(c->loss.p, 0, sizeof(LossAccum), s));
+  // K3 / K4 forward
+  const FieldLaunch fl = field_launch(c);
+  launch_encode_fwd(fl, sm.X, s);
+  mark(c, 3);
+  const MlpLaunch mf = mlp_launch(c, false);
+  launch_mlp_fwd(mf, s);
+  mark(c, 4);
+  launch_composite(NI, it, sm, c->n_fine, 0, s);
+  mark(c, 5);
+  c->launches += 3;
+  // X2: partial exchange (alias on a single rank)
+  CU(cudaStreamSynchronize(s));  // pair counts on the host
+  const PartialRec* recv = c->send_buf.as<PartialRec>();
+  if (P > 1) {
+    TRY(exchange_partials(c, pair_cnt, &bytes, &recv));
+  } else {
+    TRY(c->stream_recv_d.ensure(16));
+  }
+  mark(c, 6);
+  // K5b merge / losses / composite backward
+  launch_merge_backward(NI, it, c->part_item_off_d.as<uint32_t>(), c->d_parts.as<PartDesc>(),
+                        P > 1 ? c->stream_recv_d.as<uint64_t>() : nullptr, P, recv, sm,
+                        c->n_fine, c->cfg.lambda_transmittance, c->cfg.lambda_distortion,
+                        c->cfg.transmittance_clamp, c->loss.as<LossAccum>(), s);
+  mark(c, 7);
+  // K4b / K3b backward
+  const MlpLaunch mb = mlp_launch(c, true);
+  launch_mlp_bwd(mb, c->num_sms, s);
+  mark(c, 8);
+  launch_encode_bwd(fl, sm.dX, s);
+  mark(c, 9);
+  c->launches += 3;
+  // K6 Adam over every local parameter, lr at the pre-increment step (worker.cpp:544)
+  const double lr = dg_lr_at(&c->cfg, c->worker_step);
+  c->adam_t += 1;
+  const double bias1 = 1.0 - std::pow(c->cfg.adam_beta1, double(c->adam_t));
+  const double bias2 = 1.0 - std::pow(c->cfg.adam_beta2, double(c->adam_t));
+  launch_adam(c->params.as<float>(), c->grads.as<float>(), c->adam_m.as<float>(), c->adam_v.as<float>(),
+              c->n_params, float(lr), float(c->cfg.adam_beta1), float(c->cfg.adam_beta2),
+              float(c->cfg.adam_eps), float(1.0 / bias1), float(1.0 / bias2), s);
+  ++c->launches;
+  mark(c, 10);
+  c->worker_step = step + 1;
+  LossAccum la;
+  CU(cudaMemcpyAsync(&la, c->loss.p, sizeof la, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  c->d2h += sizeof la;
+  if (la.error & 2u) return set_err(DG_EPROTO, "worker: missing partial in batch %llu", (unsigned long long)step);
+  if (c->timing) {
+    float* t = &c->times.segment;
+    for (int k = 0; k < 10; ++k) cudaEventElapsedTime(&t[k], c->ev[k], c->ev[k + 1]);
+    cudaEventElapsedTime(&c->times.total, c->ev[0], c->ev[10]);
+  }
+  if (stats) {
+    std::memset(stats, 0, sizeof *stats);
+    stats->step = step;
+    for (uint32_t lp = 0; lp < nl; ++lp) {  // ControlSync per worker (wire.cpp:117-128)
+      const bool f32 = c->cfg.wire_f32 != 0;
+      stats->loss_rgb += f32 ? double(float(la.rgb[lp])) : la.rgb[lp];
+      stats->loss_transmittance += f32 ? double(float(la.trans[lp])) : la.trans[lp];
+      stats->loss_distortion += f32 ? double(float(la.dist[lp])) : la.dist[lp];
+    }
+    stats->lr = dg_lr_at(&c->cfg, step);
+    stats->rays = b->n - dropped;
+    stats->dropped_rays = dropped;
+    stats->bytes_sent = bytes;
+    stats->samples = uint64_t(c->n_fine) + c->n_coarse;
+    stats->items = NI;
+    stats->h2d_bytes = c->h2d;
+    stats->d2h_bytes = c->d2h;
+  }
+  return DG_OK;
+}
+
+int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merged* out) {
+  TRY(check_ctx(c));
+  if (!b || !out) return set_err(DG_EINVAL, "null argument");
+  if (b->n && (!b->origin || !b->dir)) return set_err(DG_EINVAL, "batch: missing arrays");
+  if (c->world > 1 && !c->comm) return set_err(DG_EINVAL, "world > 1 needs dg_comm_init_*");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  uint64_t dropped = 0, bytes = 0;
+  dg_ray_batch bb = *b;
+  bb.color_gt = nullptr;
+  bb.image_id = nullptr;
+  // eval appearance vector through the wire (EvalRequest reals, wire.cpp:170-176)
+  std::vector<float> app(c->cfg.appearance_dim + 1, 0.0f);
+  for (uint32_t k = 0; k < c->cfg.appearance_dim; ++k) app[k] = appearance ? appearance[k] : 0.0f;
+  TRY(upload(c->eval_app, app.data(), app.size() * sizeof(float), s));
+  const uint32_t saved_rows = c->app_rows;
+  c->app_rows = std::max<uint32_t>(c->app_rows, 1);
+  const int rc = front_half(c, &bb, 0, 0, &dropped, &bytes);
+  c->app_rows = saved_rows;
+  TRY(rc);
+  const uint32_t NI = c->n_items;
+  ItemArrays it = item_arrays(c);
+  SampleArrays sm = sample_arrays(c);
+  const FieldLaunch fl = field_launch(c);
+  launch_encode_fwd(fl, sm.X, s);
+  MlpLaunch mf = mlp_launch(c, false);
+  mf.app_override = c->eval_app.as<float>();
+  launch_mlp_fwd(mf, s);
+  launch_composite(NI, it, sm, c->n_fine, 1, s);
+  c->launches += 3;
+  const uint64_t n = b->n;
+  float* rgb = out->rgb;
+  float* tr = out->transmittance;
+  float* dep = out->depth;
+  if (out->mem != DG_MEM_DEVICE) {
+    TRY(c->out_rgb.ensure(n * 12 + 16));
+    TRY(c->out_T.ensure(n * 4 + 16));
+    TRY(c->out_depth.ensure(n * 4 + 16));
+    rgb = c->out_rgb.as<float>();
+    tr = c->out_T.as<float>();
+    dep = c->out_depth.as<float>();
+  }
+  const PartialRec* reply = nullptr;
+  if (c->world > 1) {
+    // reply: items [lp][src] -> send [src][lp] (the home rank's dispatch layout)
+    const int W = c->world;
+    const uint32_t nl = uint32_t(c->local.size());
+    // per (lp, src) counts from part_item_off and the gather table of front_half
+    std::vector<uint64_t> tab(2 * uint64_t(nl) * W);
+    // re-derive counts from the perm table (src_start, dst_start) uploaded in front_half
+    std::vector<uint64_t> perm(2 * uint64_t(nl) * W);
+    CU(cudaMemcpyAsync(perm.data(), c->perm_tab.p, perm.size() * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const uint32_t nblk = nl * uint32_t(W);
+    std::vector<uint64_t> cnt(nblk);
+    for (uint32_t k = 0; k < nblk; ++k)
+      cnt[k] = (k + 1 < nblk ? perm[k + 1] : NI) - perm[k];
+    // blocks in [src][lp] order: src_start = perm[k], dst(items) start = perm[nblk + k]
+    std::vector<PartialRec> dummy;
+    TRY(c->send_buf.ensure(uint64_t(NI) * sizeof(PartialRec) + 16));
+    // pack partial records in item order first
+    {
+      std::vector<uint64_t> t2(2 * nblk);
+      for (uint32_t k = 0; k < nblk; ++k) {
+        t2[k] = perm[nblk + k];  // source (items) start for block k
+        t2[nblk + k] = perm[k];  // destination (reply send) start
+      }
+      // k_block_permute walks blocks by source start, which must be ascending: items are
+      // [lp][src] so sort the blocks by item start.
+      std::vector<uint32_t> order(nblk);
+      for (uint32_t k = 0; k < nblk; ++k) order[k] = k;
+      std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b2) { return t2[a] < t2[b2]; });
+      std::vector<uint64_t> t3(2 * nblk);
+      for (uint32_t k = 0; k < nblk; ++k) {
+        t3[k] = t2[order[k]];
+        t3[nblk + k] = t2[nblk + order[k]];
+      }
+      TRY(upload(c->perm_tab, t3.data(), t3.size() * 8, s));
+    }
+    // item partials -> PartialRec (in item order) in recv_buf, then permute into send_buf
+    TRY(c->recv_buf.ensure(uint64_t(NI) * sizeof(PartialRec) + 16));
+    {
+      launch_items_to_records(NI, it.partial, it.depth, it.rec, c->recv_buf.as<PartialRec>(), s);
+    }
+    if (NI) {
+      k_block_permute<<<unsigned((NI + 255) / 256), 256, 0, s>>>(
+          c->recv_buf.as<uint64_t>(), c->send_buf.as<uint64_t>(), sizeof(PartialRec) / 8,
+          c->perm_tab.as<uint64_t>(), nblk, NI);
+      c->launches += 2;
+    }
+    std::vector<uint64_t> sbytes(W, 0), rbytes(W, 0);
+    for (int r = 0; r < W; ++r)
+      for (uint32_t lp = 0; lp < nl; ++lp) sbytes[r] += cnt[uint64_t(r) * nl + lp] * sizeof(PartialRec);
+    // home side: what I dispatched to each rank comes back
+    std::vector<uint32_t> slot_start(c->P + 1);
+    CU(cudaMemcpy2DAsync(slot_start.data(), 4, c->h_pos.as<uint32_t>(), n ? n * 4 : 4, 4, c->P + 1,
+                         cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (uint32_t p = 0; p < c->P; ++p)
+      rbytes[c->part_rank[p]] +=
+          uint64_t(slot_start[c->slot_of_part[p] + 1] - slot_start[c->slot_of_part[p]]) * sizeof(PartialRec);
+    uint64_t rtot = 0;
+    for (auto v : rbytes) rtot += v;
+    TRY(c->x_recv.ensure(rtot + 16));
+    std::string err;
+    const int rc2 = c->comm->alltoallv(c->send_buf.p, sbytes, c->x_recv.p, rbytes, s, err);
+    if (rc2 != DG_OK) return set_err(rc2, "%s", err.c_str());
+    reply = c->x_recv.as<PartialRec>();
+  }
+  launch_home_merge(n, c->P, c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(),
+                    c->slot_of_part_d.as<uint8_t>(), c->h_pos.as<uint32_t>(), it.partial, it.depth,
+                    reply, int(c->cfg.wire_f32), rgb, tr, dep, s);
+  ++c->launches;
+  if (out->mem != DG_MEM_DEVICE && n) {
+    CU(cudaMemcpyAsync(out->rgb, rgb, n * 12, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(out->transmittance, tr, n * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(out->depth, dep, n * 4, cudaMemcpyDeviceToHost, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
+int dg_comm_unique_id(uint8_t id[DG_NCCL_UNIQUE_ID_BYTES]) {
+  std::string err;
+  const int rc = nccl_unique_id(id, err);
+  if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+  return DG_OK;
+}
+
+int dg_comm_init_nccl(dg_ctx* c, const uint8_t id[DG_NCCL_UNIQUE_ID_BYTES]) {
+  TRY(check_ctx(c));
+  std::string err;
+  Comm* comm = make_nccl_comm(id, c->rank, c->world, c->device, err);
+  if (!comm) return set_err(DG_ENCCL, "%s", err.c_str());
+  c->comm.reset(comm);
+  return DG_OK;
+}
+
+int dg_comm_init_host(dg_ctx* c, dg_alltoallv_fn fn, void* user) {
+  TRY(check_ctx(c));
+  if (!fn) return set_err(DG_EINVAL, "null callback");
+  c->comm.reset(make_host_comm(fn, user, c->rank, c->world));
+  return DG_OK;
+}
+
+// ---------------------------------------------------------------- stage entry points
+int dg_segment_rays(dg_ctx* c, const double* origin, const double* dir, uint64_t n, uint8_t* nseg,
+                    uint16_t* region, double* t_enter, double* t_exit, int32_t mem) {
+  TRY(check_ctx(c));
+  cudaStream_t s = c->stream;
+  DBuf o, d, ns, sc, te, tx;
+  const double* od = origin;
+  const double* dd = dir;
+  if (mem != DG_MEM_DEVICE) {
+    TRY(upload(o, origin, n * 24, s));
+    TRY(upload(d, dir, n * 24, s));
+    od = o.as<double>();
+    dd = d.as<double>();
+  }
+  TRY(ns.ensure(n + 16));
+  TRY(sc.ensure(n * kMaxSeg + 16));
+  TRY(te.ensure(n * kMaxSeg * 8 + 16));
+  TRY(tx.ensure(n * kMaxSeg * 8 + 16));
+  launch_segment_full(c->d_geo.as<Geo>(), od, dd, n, ns.as<uint8_t>(), sc.as<uint8_t>(),
+                      te.as<double>(), tx.as<double>(), s);
+  ++c->launches;
+  std::vector<uint8_t> hs(n * kMaxSeg);
+  if (mem != DG_MEM_DEVICE) {
+    CU(cudaMemcpyAsync(nseg, ns.p, n, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hs.data(), sc.p, n * kMaxSeg, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(t_enter, te.p, n * kMaxSeg * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(t_exit, tx.p, n * kMaxSeg * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < n * kMaxSeg; ++i) region[i] = hs[i] == 0xff ? 0 : hs[i];
+  } else {
+    CU(cudaMemcpyAsync(nseg, ns.p, n, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(t_enter, te.p, n * kMaxSeg * 8, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(t_exit, tx.p, n * kMaxSeg * 8, cudaMemcpyDeviceToDevice, s));
+    launch_u8_to_u16(sc.as<uint8_t>(), region, n * kMaxSeg, s);
+    CU(cudaStreamSynchronize(s));
+  }
+  return DG_OK;
+}
+
+int dg_cascade_march(dg_ctx* c, uint32_t p, const double* origin, const double* dir, const double* t0,
+                     const double* t1, const uint64_t* ray_id, uint64_t n, int32_t jitter,
+                     uint64_t batch_id, uint32_t* counts, const uint64_t* offsets, double* t,
+                     double* delta, uint8_t* cascade, int32_t mem) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (mem == DG_MEM_DEVICE) return set_err(DG_EINVAL, "dg_cascade_march: host buffers only");
+  cudaStream_t s = c->stream;
+  DBuf o, d, a, b, rid, cnt, off, tt, dl, cs;
+  TRY(upload(o, origin, n * 24, s));
+  TRY(upload(d, dir, n * 24, s));
+  TRY(upload(a, t0, n * 8, s));
+  TRY(upload(b, t1, n * 8, s));
+  TRY(upload(rid, ray_id, n * 8, s));
+  TRY(cnt.ensure(n * 4 + 16));
+  uint64_t total = 0;
+  if (t) {
+    if (!offsets || !counts) return set_err(DG_EINVAL, "fill mode needs counts and offsets");
+    for (uint64_t i = 0; i < n; ++i) total = std::max(total, offsets[i] + counts[i]);
+    TRY(upload(off, offsets, n * 8, s));
+    TRY(tt.ensure(total * 8 + 16));
+    TRY(dl.ensure(total * 8 + 16));
+    TRY(cs.ensure(total + 16));
+  }
+  launch_march_points(c->d_parts.as<PartDesc>() + lp, c->occ.as<uint8_t>(), o.as<double>(), d.as<double>(),
+                      a.as<double>(), b.as<double>(), rid.as<uint64_t>(), n, c->step, c->cfg.seed,
+                      batch_id, jitter, cnt.as<uint32_t>(), t ? off.as<uint64_t>() : nullptr,
+                      t ? tt.as<double>() : nullptr, t ? dl.as<double>() : nullptr,
+                      t ? cs.as<uint8_t>() : nullptr, s);
+  ++c->launches;
+  if (!t) {
+    CU(cudaMemcpyAsync(counts, cnt.p, n * 4, cudaMemcpyDeviceToHost, s));
+  } else {
+    CU(cudaMemcpyAsync(t, tt.p, total * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(delta, dl.p, total * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(cascade, cs.p, total, cudaMemcpyDeviceToHost, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
+int dg_encode(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points, uint64_t n,
+              float* features, uint32_t* rows, int32_t mem) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  cudaStream_t s = c->stream;
+  const FieldDesc* fd = c->d_fields.as<FieldDesc>() + cascade * c->local.size() + lp;
+  const uint32_t L = c->cfg.grid_levels;
+  DBuf pts, X, R;
+  const double* pd = points;
+  if (mem != DG_MEM_DEVICE) {
+    TRY(upload(pts, points, n * 24, s));
+    pd = pts.as<double>();
+  }
+  TRY(X.ensure(n * kEnc * 4 + 16));
+  if (rows) TRY(R.ensure(n * L * 8 * 4 + 16));
+  launch_encode_points(fd, c->params.as<float>(), pd, n, X.as<float>(), rows ? R.as<uint32_t>() : nullptr, s);
+  ++c->launches;
+  // features: n x (L*2) compacted from the padded n x 32 rows
+  std::vector<float> hx(n * kEnc);
+  CU(cudaMemcpyAsync(hx.data(), X.p, n * kEnc * 4, cudaMemcpyDeviceToHost, s));
+  if (rows) {
+    if (mem == DG_MEM_DEVICE) CU(cudaMemcpyAsync(rows, R.p, n * L * 8 * 4, cudaMemcpyDeviceToDevice, s));
+    else CU(cudaMemcpyAsync(rows, R.p, n * L * 8 * 4, cudaMemcpyDeviceToHost, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  std::vector<float> packed(n * L * 2);
+  for (uint64_t i = 0; i < n; ++i)
+    std::memcpy(&packed[i * L * 2], &hx[i * kEnc], L * 2 * sizeof(float));
+  if (mem == DG_MEM_DEVICE) CU(cudaMemcpy(features, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice));
+  else std::memcpy(features, packed.data(), packed.size() * 4);
+  return DG_OK;
+}
+
+int dg_encode_backward(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points,
+                       const float* upstream, uint64_t n, int32_t mem) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  if (mem == DG_MEM_DEVICE) return set_err(DG_EINVAL, "dg_encode_backward: host buffers only");
+  cudaStream_t s = c->stream;
+  const uint32_t L = c->cfg.grid_levels;
+  std::vector<float> up(n * kEnc, 0.0f);
+  for (uint64_t i = 0; i < n; ++i) std::memcpy(&up[i * kEnc], upstream + i * L * 2, L * 2 * 4);
+  DBuf pts, dX;
+  TRY(upload(pts, points, n * 24, s));
+  TRY(upload(dX, up.data(), up.size() * 4, s));
+  launch_encode_points_bwd(c->d_fields.as<FieldDesc>() + cascade * c->local.size() + lp, c->grads.as<float>(),
+                           pts.as<double>(), dX.as<float>(), n, s);
+  ++c->launches;
+  CU(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
+// Field stage entries: build one-sample "items" so the production MLP kernels run unchanged.
+static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points, const float* dirs,
+                       const float* app, uint64_t n, const float* sig_grad, const float* rgb_grad,
+                       float* sigma, float* rgb) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  cudaStream_t s = c->stream;
+  const uint32_t nl = uint32_t(c->local.size());
+  const uint32_t f = cascade * nl + lp;
+  const FieldDesc* fd = c->d_fields.as<FieldDesc>() + f;
+  DBuf pts, X, recs, items, appb, out, gin, dX, foff, toff;
+  TRY(upload(pts, points, n * 24, s));
+  TRY(X.ensure(n * kEnc * 4 + 16));
+  launch_encode_points(fd, c->params.as<float>(), pts.as<double>(), n, X.as<float>(), nullptr, s);
+  std::vector<RayRec> rr(n);
+  std::vector<uint32_t> ids(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    std::memset(&rr[i], 0, sizeof(RayRec));
+    for (int a = 0; a < 3; ++a) rr[i].d[a] = dirs[3 * i + a];
+    ids[i] = uint32_t(i);
+  }
+  TRY(upload(recs, rr.data(), n * sizeof(RayRec), s));
+  TRY(upload(items, ids.data(), n * 4, s));
+  TRY(upload(appb, app, n * c->cfg.appearance_dim * 4, s));
+  // fields 0..2nl-1 with only field f non-empty
+  std::vector<uint32_t> fo(2 * nl + 1, 0), tf(2 * nl + 1, 0), tb(2 * nl + 1, 0);
+  for (uint32_t k = f + 1; k <= 2 * nl; ++k) {
+    fo[k] = uint32_t(n);
+    tf[k] = uint32_t((n + 127) / 128);
+    tb[k] = uint32_t((n + 63) / 64);
+  }
+  TRY(upload(foff, fo.data(), fo.size() * 4, s));
+  MlpLaunch m{};
+  m.fields = c->d_fields.as<FieldDesc>();
+  m.n_fields = 2 * nl;
+  m.field_off = foff.as<uint32_t>();
+  m.X = X.as<float>();
+  m.rec = recs.as<RayRec>();
+  m.s_item = items.as<uint32_t>();
+  m.app_override = appb.as<float>();
+  m.app_per_sample = 1;
+  m.params = c->params.as<float>();
+  m.grads = c->grads.as<float>();
+  TRY(out.ensure(n * 16 + 16));
+  m.out = out.as<float4>();
+  if (!sig_grad) {
+    TRY(upload(toff, tf.data(), tf.size() * 4, s));
+    m.tile_off = toff.as<uint32_t>();
+    m.n_tiles = tf[2 * nl];
+    launch_mlp_fwd(m, s);
+    std::vector<float4> h(n);
+    CU(cudaMemcpyAsync(h.data(), out.p, n * 16, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < n; ++i) {
+      sigma[i] = h[i].x;
+      rgb[3 * i] = h[i].y;
+      rgb[3 * i + 1] = h[i].z;
+      rgb[3 * i + 2] = h[i].w;
+    }
+    c->launches += 2;
+    return DG_OK;
+  }
+  std::vector<float4> g(n);
+  for (uint64_t i = 0; i < n; ++i)
+    g[i] = make_float4(sig_grad[i], rgb_grad[3 * i], rgb_grad[3 * i + 1], rgb_grad[3 * i + 2]);
+  TRY(upload(gin, g.data(), n * 16, s));
+  TRY(dX.ensure(n * kEnc * 4 + 16));
+  TRY(upload(toff, tb.data(), tb.size() * 4, s));
+  m.tile_off = toff.as<uint32_t>();
+  m.n_tiles = tb[2 * nl];
+  m.grad_in = gin.as<float4>();
+  m.dX = dX.as<float>();
+  launch_mlp_bwd(m, c->num_sms, s);
+  launch_encode_points_bwd(fd, c->grads.as<float>(), pts.as<double>(), dX.as<float>(), n, s);
+  c->launches += 3;
+  CU(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
+int dg_field_forward(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points, const float* dirs,
+                     const float* app, uint64_t n, float* sigma, float* rgb, int32_t mem) {
+  if (mem == DG_MEM_DEVICE) return set_err(DG_EINVAL, "dg_field_forward: host buffers only");
+  return field_stage(c, p, cascade, points, dirs, app, n, nullptr, nullptr, sigma, rgb);
+}
+
+int dg_field_backward(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points, const float* dirs,
+                      const float* app, const float* sigma_grad, const float* rgb_grad, uint64_t n,
+                      int32_t mem) {
+  if (mem == DG_MEM_DEVICE) return set_err(DG_EINVAL, "dg_field_backward: host buffers only");
+  if (!sigma_grad || !rgb_grad) return set_err(DG_EINVAL, "null gradients");
+  return field_stage(c, p, cascade, points, dirs, app, n, sigma_grad, rgb_grad, nullptr, nullptr);
+}
+
+int dg_adam_step(dg_ctx* c, double lr) {
+  TRY(check_ctx(c));
+  c->adam_t += 1;
+  const double bias1 = 1.0 - std::pow(c->cfg.adam_beta1, double(c->adam_t));
+  const double bias2 = 1.0 - std::pow(c->cfg.adam_beta2, double(c->adam_t));
+  launch_adam(c->params.as<float>(), c->grads.as<float>(), c->adam_m.as<float>(), c->adam_v.as<float>(),
+              c->n_params, float(lr), float(c->cfg.adam_beta1), float(c->cfg.adam_beta2),
+              float(c->cfg.adam_eps), float(1.0 / bias1), float(1.0 / bias2), c->stream);
+  ++c->launches;
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+// ---------------------------------------------------------------- introspection
+int dg_last_items(dg_ctx* c, uint32_t p, dg_item_view* v) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (!c->have_last) return set_err(DG_EINVAL, "no step has run");
+  const uint32_t nl = uint32_t(c->local.size());
+  v->n_items = c->part_item_off[lp + 1] - c->part_item_off[lp];
+  v->n_fine = c->field_off[lp + 1] - c->field_off[lp];
+  v->n_coarse = c->field_off[nl + lp + 1] - c->field_off[nl + lp];
+  return DG_OK;
+}
+
+int dg_last_item_data(dg_ctx* c, uint32_t p, uint64_t* ray_id, uint8_t* order, double* te, double* tx,
+                      uint32_t* n_samples) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (!c->have_last) return set_err(DG_EINVAL, "no step has run");
+  cudaStream_t s = c->stream;
+  const uint32_t a = c->part_item_off[lp], n = c->part_item_off[lp + 1] - a, NI = c->n_items;
+  std::vector<RayRec> rec;
+  std::vector<uint8_t> ord;
+  std::vector<double> vte, vtx;
+  std::vector<uint32_t> cnt;
+  TRY(d2h(rec, c->rec.as<RayRec>() + a, n, s));
+  TRY(d2h(ord, c->it_order.as<uint8_t>() + a, n, s));
+  TRY(d2h(vte, c->it_te.as<double>() + a, n, s));
+  TRY(d2h(vtx, c->it_tx.as<double>() + a, n, s));
+  TRY(d2h(cnt, c->it_cnt.p, 2ull * NI, s));
+  CU(cudaStreamSynchronize(s));
+  for (uint32_t i = 0; i < n; ++i) {
+    if (ray_id) ray_id[i] = rec[i].ray_id;
+    if (order) order[i] = ord[i];
+    if (te) te[i] = vte[i];
+    if (tx) tx[i] = vtx[i];
+    if (n_samples) n_samples[i] = cnt[a + i] + cnt[NI + a + i];
+  }
+  return DG_OK;
+}
+
+int dg_last_samples(dg_ctx* c, uint32_t p, double* t, double* delta, uint8_t* cascade) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (!c->have_last) return set_err(DG_EINVAL, "no step has run");
+  cudaStream_t s = c->stream;
+  const uint32_t NI = c->n_items;
+  const uint64_t NS = uint64_t(c->n_fine) + c->n_coarse;
+  std::vector<uint32_t> cnt, off, ncb;
+  std::vector<double> st, sd;
+  TRY(d2h(cnt, c->it_cnt.p, 2ull * NI, s));
+  TRY(d2h(off, c->it_off.p, 2ull * NI, s));
+  TRY(d2h(ncb, c->it_ncb.p, NI, s));
+  TRY(d2h(st, c->s_t.p, NS, s));
+  TRY(d2h(sd, c->s_delta.p, NS, s));
+  CU(cudaStreamSynchronize(s));
+  uint64_t k = 0;
+  auto put = [&](uint32_t idx, uint8_t casc) {
+    t[k] = st[idx];
+    delta[k] = sd[idx];
+    if (cascade) cascade[k] = casc;
+    ++k;
+  };
+  for (uint32_t i = c->part_item_off[lp]; i < c->part_item_off[lp + 1]; ++i) {
+    for (uint32_t j = 0; j < ncb[i]; ++j) put(off[NI + i] + j, 1);
+    for (uint32_t j = 0; j < cnt[i]; ++j) put(off[i] + j, 0);
+    for (uint32_t j = ncb[i]; j < cnt[NI + i]; ++j) put(off[NI + i] + j, 1);
+  }
+  return DG_OK;
+}
+
+int dg_last_partials(dg_ctx* c, uint32_t p, float* rgb, float* transmittance) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (!c->have_last) return set_err(DG_EINVAL, "no step has run");
+  const uint32_t a = c->part_item_off[lp], n = c->part_item_off[lp + 1] - a;
+  std::vector<float4> v;
+  TRY(d2h(v, c->it_partial.as<float4>() + a, n, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (uint32_t i = 0; i < n; ++i) {
+    rgb[3 * i] = v[i].x;
+    rgb[3 * i + 1] = v[i].y;
+    rgb[3 * i + 2] = v[i].z;
+    transmittance[i] = v[i].w;
+  }
+  return DG_OK;
+}
+
+int dg_kernel_launches(const dg_ctx* c, uint64_t* n) {
+  TRY(check_ctx(c));
+  *n = c->launches;
+  return DG_OK;
+}
+
+int dg_enable_stage_timing(dg_ctx* c, int enable) {
+  TRY(check_ctx(c));
+  c->timing = enable != 0;
+  return DG_OK;
+}
+
+int dg_last_stage_times(dg_ctx* c, dg_stage_times* t) {
+  TRY(check_ctx(c));
+  *t = c->times;
+  return DG_OK;
+}
+
+int dg_get_stream(dg_ctx* c, void** stream) {
+  TRY(check_ctx(c));
+  *stream = (void*)c->stream;
+  return DG_OK;
+}
+
+int dg_synchronize(dg_ctx* c) {
+  TRY(check_ctx(c));
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,395 @@
+"""ctypes binding of libdg_b200.so (include/distgrid_b200.h) — the Python face of the
+drop-in boundary, used by tests/, bench.py and __graft_entry__.
+
+Mirrors the reference's DistributedRun surface (worker.hpp:182-226):
+    ctx.train_step(origin, dir, color_gt, image_id, step) -> StepStats   (training_step)
+    ctx.render(origin, dir, appearance)                     -> (rgb, T, depth) (evaluate_rays)
+plus state injection/extraction (params, Adam moments, occupancy) for parity.
+
+There is no fallback: if the CUDA library is missing this module raises on load.
+"""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+from . import abi
+from .abi import (DG_MAX_SEGMENTS, DG_MEM_DEVICE, DG_MEM_HOST, ArrayDesc, ItemView, Merged,
+                  RayBatch, RunConfig, StageTimes, StepStats)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdg_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "distgrid_b200.h")
+
+P = C.c_void_p
+
+
+class DGError(RuntimeError):
+    """Maps dg_status codes onto the reference's exception classes by name."""
+
+    def __init__(self, code, msg):
+        self.code = code
+        self.status = abi.STATUS_NAMES.get(code, str(code))
+        super().__init__(f"{self.status}: {msg}")
+
+
+_lib = None
+
+
+def header_functions():
+    """Names of every dg_* function declared in include/distgrid_b200.h."""
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(dg_[a-z0-9_]+)\s*\(", text)) - {"dg_alltoallv_fn"})
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.dg_last_error.restype = C.c_char_p
+        L.dg_lr_at.restype = C.c_double
+        L.dg_lr_at.argtypes = [C.POINTER(RunConfig), C.c_uint64]
+        L.dg_default_config.argtypes = [C.POINTER(RunConfig)]
+        L.dg_ctx_create.argtypes = [C.POINTER(RunConfig), C.c_int, C.c_int, C.c_int, C.POINTER(P)]
+        L.dg_ctx_destroy.argtypes = [P]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise DGError(rc, lib().dg_last_error().decode())
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(P)
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _c32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class Context:
+    """One dg_ctx: the partitions of `rank` on `device` (partition p lives on rank p % world)."""
+
+    def __init__(self, cfg, device=-1, rank=0, world=1):
+        L = lib()
+        self.cfg = cfg.copy()
+        self.h = P()
+        _check(L.dg_ctx_create(C.byref(self.cfg), device, rank, world, C.byref(self.h)))
+        self.rank, self.world = rank, world
+        nt, nl = C.c_uint32(), C.c_uint32()
+        _check(L.dg_partition_count(self.h, C.byref(nt), C.byref(nl)))
+        self.P = nt.value
+        self.local = [p for p in range(self.P) if p % world == rank]
+        self._cb = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().dg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- geometry / layout ----
+    @property
+    def march_step(self):
+        v = C.c_double()
+        _check(lib().dg_march_step(self.h, C.byref(v)))
+        return v.value
+
+    def param_count(self, g):
+        n = C.c_uint64()
+        _check(lib().dg_param_count(self.h, C.c_uint32(g), C.byref(n)))
+        return n.value
+
+    def param_layout(self, g):
+        arr = (ArrayDesc * 64)()
+        n = C.c_uint32()
+        _check(lib().dg_param_layout(self.h, C.c_uint32(g), arr, 64, C.byref(n)))
+        return [dict(offset=a.offset, size=a.size, cascade=a.cascade, kind=a.kind, index=a.index)
+                for a in arr[:n.value]]
+
+    def grid_levels(self, g, cascade):
+        L = self.cfg.grid_levels
+        shapes = np.zeros((L, 3), dtype=np.uint32)
+        modes = np.zeros(L, dtype=np.uint32)
+        rows = np.zeros(L, dtype=np.uint64)
+        _check(lib().dg_grid_levels(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(shapes),
+                                    _p(modes), _p(rows)))
+        return shapes, modes, rows
+
+    def occupancy_shape(self, g, cascade):
+        s = (C.c_uint32 * 3)()
+        _check(lib().dg_occupancy_shape(self.h, C.c_uint32(g), C.c_uint32(cascade), s))
+        return tuple(s)
+
+    # ---- state ----
+    def set_params(self, g, p):
+        p = _c32(p)
+        assert p.size == self.param_count(g)
+        _check(lib().dg_set_params(self.h, C.c_uint32(g), _p(p)))
+
+    def get_params(self, g):
+        out = np.zeros(self.param_count(g), dtype=np.float32)
+        _check(lib().dg_get_params(self.h, C.c_uint32(g), _p(out)))
+        return out
+
+    def get_grads(self, g):
+        out = np.zeros(self.param_count(g), dtype=np.float32)
+        _check(lib().dg_get_grads(self.h, C.c_uint32(g), _p(out)))
+        return out
+
+    def zero_grads(self):
+        _check(lib().dg_zero_grads(self.h))
+
+    def set_adam(self, g, m, v, t):
+        m, v = _c32(m), _c32(v)
+        _check(lib().dg_set_adam(self.h, C.c_uint32(g), _p(m), _p(v), C.c_uint64(t)))
+
+    def get_adam(self, g):
+        n = self.param_count(g)
+        m = np.zeros(n, dtype=np.float32)
+        v = np.zeros(n, dtype=np.float32)
+        t = C.c_uint64()
+        _check(lib().dg_get_adam(self.h, C.c_uint32(g), _p(m), _p(v), C.byref(t)))
+        return m, v, t.value
+
+    def set_step(self, s):
+        _check(lib().dg_set_step(self.h, C.c_uint64(s)))
+
+    def get_step(self):
+        v = C.c_uint64()
+        _check(lib().dg_get_step(self.h, C.byref(v)))
+        return v.value
+
+    def init_reference(self, g):
+        _check(lib().dg_init_params_reference(self.h, C.c_uint32(g)))
+
+    def init_fast(self, g, seed=1):
+        _check(lib().dg_init_params_fast(self.h, C.c_uint32(g), C.c_uint64(seed)))
+
+    def set_occupancy(self, g, cascade, bits):
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        _check(lib().dg_set_occupancy(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(bits)))
+
+    def get_occupancy(self, g, cascade):
+        s = self.occupancy_shape(g, cascade)
+        bits = np.zeros(s[0] * s[1] * s[2], dtype=np.uint8)
+        _check(lib().dg_get_occupancy(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(bits)))
+        return bits
+
+    def set_appearance(self, rows, ids=None):
+        rows = _c32(np.atleast_2d(rows))
+        ids = np.arange(rows.shape[0], dtype=np.uint32) if ids is None else \
+            np.ascontiguousarray(ids, dtype=np.uint32)
+        _check(lib().dg_set_appearance(self.h, _p(ids), _p(rows), C.c_uint32(rows.shape[0])))
+
+    # ---- composed path ----
+    def _batch(self, origin, dir, color_gt=None, image_id=None, first_ray_id=0):
+        b = RayBatch()
+        self._keep = [_c64(origin), _c64(dir),
+                      None if color_gt is None else _c32(color_gt),
+                      None if image_id is None else np.ascontiguousarray(image_id, dtype=np.uint32)]
+        o, d, gt, img = self._keep
+        b.origin, b.dir, b.color_gt, b.image_id = _p(o), _p(d), _p(gt), _p(img)
+        b.n = len(o)
+        b.first_ray_id = first_ray_id
+        b.mem = DG_MEM_HOST
+        return b
+
+    def train_step(self, origin, dir, color_gt, image_id=None, step=0, first_ray_id=0):
+        b = self._batch(origin, dir, color_gt, image_id, first_ray_id)
+        st = StepStats()
+        _check(lib().dg_train_step(self.h, C.byref(b), C.c_uint64(step), C.byref(st)))
+        return {k: getattr(st, k) for k, _ in StepStats._fields_}
+
+    def train_step_raw(self, batch, step, stats):
+        """Zero-copy variant for pre-built RayBatch structs (device or pinned host)."""
+        return lib().dg_train_step(self.h, C.byref(batch), C.c_uint64(step), C.byref(stats))
+
+    def render(self, origin, dir, appearance, first_ray_id=0):
+        b = self._batch(origin, dir, None, None, first_ray_id)
+        n = b.n
+        rgb = np.zeros((n, 3), dtype=np.float32)
+        T = np.zeros(n, dtype=np.float32)
+        depth = np.zeros(n, dtype=np.float32)
+        m = Merged()
+        m.rgb, m.transmittance, m.depth, m.mem = _p(rgb), _p(T), _p(depth), DG_MEM_HOST
+        app = _c32(appearance)
+        _check(lib().dg_render(self.h, C.byref(b), _p(app), C.byref(m)))
+        return rgb, T, depth
+
+    def render_raw(self, batch, app, merged):
+        return lib().dg_render(self.h, C.byref(batch), _p(app), C.byref(merged))
+
+    # ---- comms ----
+    def comm_init_nccl(self, uid_bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid_bytes))
+        _check(lib().dg_comm_init_nccl(self.h, buf))
+
+    def comm_init_host(self, fn):
+        """fn(send: bytes-like per peer list, recv_sizes) -> list of received bytes (rank order)."""
+        proto = C.CFUNCTYPE(C.c_int, P, P, C.POINTER(C.c_uint64), P, C.POINTER(C.c_uint64))
+
+        def cb(user, send, send_bytes, recv, recv_bytes):
+            try:
+                W = self.world
+                sb = [send_bytes[i] for i in range(W)]
+                rb = [recv_bytes[i] for i in range(W)]
+                total = sum(sb)
+                blob = C.string_at(send, total) if total else b""
+                blocks, off = [], 0
+                for s in sb:
+                    blocks.append(blob[off:off + s])
+                    off += s
+                got = fn(blocks, rb)
+                off = 0
+                for r in range(W):
+                    assert len(got[r]) == rb[r], (r, len(got[r]), rb[r])
+                    if rb[r]:
+                        C.memmove(recv + off, got[r], rb[r])
+                    off += rb[r]
+                return 0
+            except Exception as e:  # surfaces as DG_ETIMEOUT
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._cb = proto(cb)
+        _check(lib().dg_comm_init_host(self.h, self._cb, None))
+
+    # ---- stage entry points ----
+    def segment_rays(self, origin, dir):
+        o, d = _c64(origin), _c64(dir)
+        n = len(o)
+        nseg = np.zeros(n, dtype=np.uint8)
+        region = np.zeros((n, DG_MAX_SEGMENTS), dtype=np.uint16)
+        te = np.zeros((n, DG_MAX_SEGMENTS))
+        tx = np.zeros((n, DG_MAX_SEGMENTS))
+        _check(lib().dg_segment_rays(self.h, _p(o), _p(d), C.c_uint64(n), _p(nseg), _p(region),
+                                     _p(te), _p(tx), DG_MEM_HOST))
+        return nseg, region, te, tx
+
+    def cascade_march(self, g, origin, dir, t0, t1, ray_id, jitter, batch_id):
+        o, d, a, b = _c64(origin), _c64(dir), _c64(t0), _c64(t1)
+        rid = np.ascontiguousarray(ray_id, dtype=np.uint64)
+        n = len(o)
+        counts = np.zeros(n, dtype=np.uint32)
+        args = (self.h, C.c_uint32(g), _p(o), _p(d), _p(a), _p(b), _p(rid), C.c_uint64(n),
+                C.c_int32(int(jitter)), C.c_uint64(batch_id))
+        _check(lib().dg_cascade_march(*args, _p(counts), None, None, None, None, DG_MEM_HOST))
+        off = np.zeros(n, dtype=np.uint64)
+        off[1:] = np.cumsum(counts.astype(np.uint64))[:-1]
+        tot = int(counts.sum())
+        t = np.zeros(max(tot, 1))
+        delta = np.zeros(max(tot, 1))
+        casc = np.zeros(max(tot, 1), dtype=np.uint8)
+        _check(lib().dg_cascade_march(*args, _p(counts), _p(off), _p(t), _p(delta), _p(casc),
+                                      DG_MEM_HOST))
+        return counts, t[:tot], delta[:tot], casc[:tot]
+
+    def encode(self, g, cascade, points, with_rows=True):
+        pts = _c64(points)
+        n = len(pts)
+        Lf = self.cfg.grid_levels * 2
+        feats = np.zeros((n, Lf), dtype=np.float32)
+        rows = np.zeros((n, self.cfg.grid_levels, 8), dtype=np.uint32) if with_rows else None
+        _check(lib().dg_encode(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(pts), C.c_uint64(n),
+                               _p(feats), _p(rows), DG_MEM_HOST))
+        return feats, rows
+
+    def encode_backward(self, g, cascade, points, upstream):
+        pts, up = _c64(points), _c32(upstream)
+        _check(lib().dg_encode_backward(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(pts),
+                                        _p(up), C.c_uint64(len(pts)), DG_MEM_HOST))
+
+    def field_forward(self, g, cascade, points, dirs, app):
+        pts, dd, aa = _c64(points), _c32(dirs), _c32(app)
+        n = len(pts)
+        sigma = np.zeros(n, dtype=np.float32)
+        rgb = np.zeros((n, 3), dtype=np.float32)
+        _check(lib().dg_field_forward(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(pts), _p(dd),
+                                      _p(aa), C.c_uint64(n), _p(sigma), _p(rgb), DG_MEM_HOST))
+        return sigma, rgb
+
+    def field_backward(self, g, cascade, points, dirs, app, dsigma, drgb):
+        pts, dd, aa, ds, dr = _c64(points), _c32(dirs), _c32(app), _c32(dsigma), _c32(drgb)
+        _check(lib().dg_field_backward(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(pts), _p(dd),
+                                       _p(aa), _p(ds), _p(dr), C.c_uint64(len(pts)), DG_MEM_HOST))
+
+    def adam_step(self, lr):
+        _check(lib().dg_adam_step(self.h, C.c_double(lr)))
+
+    # ---- introspection ----
+    def last_items(self, g):
+        v = ItemView()
+        _check(lib().dg_last_items(self.h, C.c_uint32(g), C.byref(v)))
+        return v.n_items, v.n_fine, v.n_coarse
+
+    def last_item_data(self, g):
+        n, _, _ = self.last_items(g)
+        rid = np.zeros(n, dtype=np.uint64)
+        order = np.zeros(n, dtype=np.uint8)
+        te = np.zeros(n)
+        tx = np.zeros(n)
+        ns = np.zeros(n, dtype=np.uint32)
+        _check(lib().dg_last_item_data(self.h, C.c_uint32(g), _p(rid), _p(order), _p(te), _p(tx),
+                                       _p(ns)))
+        return rid, order, te, tx, ns
+
+    def last_samples(self, g):
+        _, nf, nc = self.last_items(g)
+        tot = nf + nc
+        t = np.zeros(max(tot, 1))
+        d = np.zeros(max(tot, 1))
+        c = np.zeros(max(tot, 1), dtype=np.uint8)
+        _check(lib().dg_last_samples(self.h, C.c_uint32(g), _p(t), _p(d), _p(c)))
+        return t[:tot], d[:tot], c[:tot]
+
+    def last_partials(self, g):
+        n, _, _ = self.last_items(g)
+        rgb = np.zeros((n, 3), dtype=np.float32)
+        T = np.zeros(n, dtype=np.float32)
+        _check(lib().dg_last_partials(self.h, C.c_uint32(g), _p(rgb), _p(T)))
+        return rgb, T
+
+    def kernel_launches(self):
+        v = C.c_uint64()
+        _check(lib().dg_kernel_launches(self.h, C.byref(v)))
+        return v.value
+
+    def enable_stage_timing(self, on=True):
+        _check(lib().dg_enable_stage_timing(self.h, int(on)))
+
+    def stage_times(self):
+        t = StageTimes()
+        _check(lib().dg_last_stage_times(self.h, C.byref(t)))
+        return t.as_dict()
+
+    def synchronize(self):
+        _check(lib().dg_synchronize(self.h))
+
+
+def lr_at(cfg, step):
+    return lib().dg_lr_at(C.byref(cfg), C.c_uint64(step))
+
+
+def nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    _check(lib().dg_comm_unique_id(buf))
+    return bytes(buf)
