@@ -272,6 +272,11 @@ typedef struct dg_stage_times {
 int dg_enable_stage_timing(dg_ctx* ctx, int enable);
 int dg_last_stage_times(dg_ctx* ctx, dg_stage_times* t);
 int dg_synchronize(dg_ctx* ctx);
+/* Diagnostics: runs the tcgen05 operand-layout self-test on the current device.
+ * Host fp32 inputs A[128x64], B[64x64], X[128x32]; outputs Y0 = A B^T, Y1 = A B (128x64) and
+ * Y2 = A^T X (64x32), each a split-bf16 (3-term) tcgen05.mma product accumulated in TMEM. */
+int dg_selftest_tcgen05(const float* A, const float* B, const float* X, float* Y0, float* Y1,
+                        float* Y2);
 /* the context's CUDA stream (cudaStream_t) so callers can record events on it */
 int dg_get_stream(dg_ctx* ctx, void** stream);
 

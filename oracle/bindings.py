@@ -45,10 +45,11 @@ def oracle_lib():
         lib.or_run_create.argtypes = [C.POINTER(RunConfig), C.c_uint32, P]
         lib.or_run_destroy.argtypes = [P]
         for name in ("or_run_params", "or_run_grads", "or_run_adam_m", "or_run_adam_v",
-                     "or_run_occ_density"):
+                     "or_run_occ_density", "or_run_abs_grads"):
             getattr(lib, name).restype = C.POINTER(C.c_double)
         lib.or_run_params.argtypes = [P, C.c_uint32]
         lib.or_run_grads.argtypes = [P, C.c_uint32]
+        lib.or_run_abs_grads.argtypes = [P, C.c_uint32]
         lib.or_run_adam_m.argtypes = [P, C.c_uint32]
         lib.or_run_adam_v.argtypes = [P, C.c_uint32]
         lib.or_run_occ_density.argtypes = [P, C.c_uint32, C.c_uint32]
@@ -156,6 +157,10 @@ class OracleRun(_RunBase):
 
     def grads(self, g):
         return self._arr(self.lib.or_run_grads(self.h, g), self._nparams[g])
+
+    def abs_grads(self, g):
+        """sum over contributions of |contribution| for every gradient entry (last step)"""
+        return self._arr(self.lib.or_run_abs_grads(self.h, g), self._nparams[g])
 
     def adam(self, g):
         m = self._arr(self.lib.or_run_adam_m(self.h, g), self._nparams[g])

@@ -33,6 +33,16 @@ static inline double sclamp(double v, double lo, double hi) {
 }
 static inline int iclamp(int v, int lo, int hi) { return (v < lo) ? lo : ((hi < v) ? hi : v); }
 
+/* Test-only: when set, every gradient contribution t is also accumulated as |t| into the
+ * parallel array g_abs (same offsets as the grads base g_gbase).  Used to state the gradient
+ * tolerance relative to sum |contributions| (the standard bound for reordered fp sums). */
+static double* g_abs = NULL;
+static const double* g_gbase = NULL;
+#define OR_ABS(ptr, val)                                     \
+  do {                                                       \
+    if (g_abs) g_abs[(ptr) - g_gbase] += fabs(val);          \
+  } while (0)
+
 /* ------------------------------------------------------------------ rng.hpp:8-62 */
 uint64_t or_splitmix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ull;
@@ -534,7 +544,10 @@ void or_encode_backward(const or_grid* g, double* grads, const double p[3], cons
       if (w == 0.0) continue;
       const uint32_t row = corner_row(g, l, &cw, c);
       double* dst = grads + g->offset[l] + (size_t)row * F;
-      for (uint32_t k = 0; k < F; ++k) dst[k] += w * u[k];
+      for (uint32_t k = 0; k < F; ++k) {
+        dst[k] += w * u[k];
+        OR_ABS(dst + k, w * u[k]);
+      }
     }
   }
 }
@@ -637,8 +650,12 @@ static void dense_backward(const double* W, double* gW, double* gb, const double
     const double dv = delta[r];
     if (dv == 0.0) continue;
     double* wg = gW + (size_t)r * n_in;
-    for (uint32_t c = 0; c < n_in; ++c) wg[c] += dv * in[c];
+    for (uint32_t c = 0; c < n_in; ++c) {
+      wg[c] += dv * in[c];
+      OR_ABS(wg + c, dv * in[c]);
+    }
     gb[r] += dv;
+    OR_ABS(gb + r, dv);
   }
   if (in_grad) {
     for (uint32_t c = 0; c < n_in; ++c) in_grad[c] = 0.0;
@@ -832,6 +849,7 @@ struct or_run {
   double* params[DG_MAX_PARTITIONS];
   double* grads[DG_MAX_PARTITIONS];
   double* last_grads[DG_MAX_PARTITIONS];
+  double* abs_grads[DG_MAX_PARTITIONS];
   double* am[DG_MAX_PARTITIONS];
   double* av[DG_MAX_PARTITIONS];
   uint64_t at[DG_MAX_PARTITIONS];
@@ -847,6 +865,7 @@ struct or_run {
 const or_model* or_run_model(const or_run* r) { return &r->m; }
 double* or_run_params(or_run* r, uint32_t g) { return r->params[g]; }
 double* or_run_grads(or_run* r, uint32_t g) { return r->last_grads[g]; }
+double* or_run_abs_grads(or_run* r, uint32_t g) { return r->abs_grads[g]; }
 double* or_run_adam_m(or_run* r, uint32_t g) { return r->am[g]; }
 double* or_run_adam_v(or_run* r, uint32_t g) { return r->av[g]; }
 uint64_t* or_run_adam_t(or_run* r, uint32_t g) { return &r->at[g]; }
@@ -880,6 +899,7 @@ or_run* or_run_create(const dg_run_config* cfg, uint32_t n_images, const double*
     r->params[g] = (double*)calloc(n, sizeof(double));
     r->grads[g] = (double*)calloc(n, sizeof(double));
     r->last_grads[g] = (double*)calloc(n, sizeof(double));
+    r->abs_grads[g] = (double*)calloc(n, sizeof(double));
     r->am[g] = (double*)calloc(n, sizeof(double));
     r->av[g] = (double*)calloc(n, sizeof(double));
     for (int c = 0; c < 2; ++c) {
@@ -907,6 +927,7 @@ void or_run_destroy(or_run* r) {
     free(r->params[g]);
     free(r->grads[g]);
     free(r->last_grads[g]);
+    free(r->abs_grads[g]);
     free(r->am[g]);
     free(r->av[g]);
     for (int c = 0; c < 2; ++c) {
@@ -1089,6 +1110,9 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
   /* Phase 3 per worker: merge, losses, backward (worker.cpp:362-385, 403-522). */
   for (uint32_t g = 0; g < m->P && rc == 0; ++g) {
     loss_rgb[g] = loss_t[g] = loss_d[g] = 0.0;
+    memset(r->abs_grads[g], 0, sizeof(double) * m->nparams[g]);
+    g_abs = r->abs_grads[g];
+    g_gbase = r->grads[g];
     for (uint64_t i = 0; i < n; ++i) {
       const or_dray* d = &rays[i];
       int mo = -1;
@@ -1150,6 +1174,8 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
         or_field_backward(f, r->params[g] + off, r->grads[g] + off, &fcache[k], sgs[k], sgc + 3 * k);
       }
     }
+    g_abs = NULL;
+    g_gbase = NULL;
     if (rc) break;
     /* apply_updates (worker.cpp:524-547): Adam with lr at the pre-increment step_ */
     const double lr = or_lr_at(cfg, r->wstep[g]);

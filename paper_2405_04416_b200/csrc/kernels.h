@@ -106,6 +106,7 @@ struct FieldLaunch {
   uint32_t fine_total;
   uint32_t n_total;
   uint32_t n_local;
+  uint32_t levels;
   const float* params;
   float* grads;
 };
@@ -113,9 +114,9 @@ void launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s);
 void launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s);
 // stand-alone points variant (stage entry points): all points belong to one field
 void launch_encode_points(const FieldDesc* field, const float* params, const double* pts,
-                          uint64_t n, float* X, uint32_t* rows, cudaStream_t s);
+                          uint64_t n, uint32_t levels, float* X, uint32_t* rows, cudaStream_t s);
 void launch_encode_points_bwd(const FieldDesc* field, float* grads, const double* pts,
-                              const float* dX, uint64_t n, cudaStream_t s);
+                              const float* dX, uint64_t n, uint32_t levels, cudaStream_t s);
 
 // MLP: tiles never straddle fields.  field_off: n_fields+1 sample offsets.
 struct MlpLaunch {
@@ -124,7 +125,9 @@ struct MlpLaunch {
   const uint32_t* field_off;   // device, n_fields + 1
   const uint32_t* tile_off;    // device, n_fields + 1 (prefix of tiles)
   uint32_t n_tiles;
-  const float* X;
+  const float* X;              // level-major [levels][x_stride] float2
+  uint64_t x_stride;           // samples per level row of X / dX
+  uint32_t levels;
   const float* dirs_f;         // optional per-sample dirs (stage entry) else from items
   const RayRec* rec;
   const uint32_t* s_item;
@@ -135,7 +138,7 @@ struct MlpLaunch {
   float* grads;
   float4* out;                 // fwd: sigma, rgb
   const float4* grad_in;       // bwd: dsigma, drgb
-  float* dX;                   // bwd
+  float* dX;                   // bwd, level-major like X
 };
 void launch_mlp_fwd(const MlpLaunch& m, cudaStream_t s);
 void launch_mlp_bwd(const MlpLaunch& m, int num_sms, cudaStream_t s);
@@ -144,5 +147,9 @@ void launch_mlp_bwd(const MlpLaunch& m, int num_sms, cudaStream_t s);
 void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, float b1, float b2,
                  float eps, float inv_bias1, float inv_sqrt_bias2, cudaStream_t s);
 void launch_fill_uniform(float* p, uint64_t n, float lo, float hi, uint64_t seed, cudaStream_t s);
+
+// ---- tcgen05 self-test (kernels_tc.cu) ----
+int tc_selftest(const float* A, const float* B, const float* X, float* Y0, float* Y1, float* Y2,
+                cudaStream_t s);
 
 }  // namespace dg

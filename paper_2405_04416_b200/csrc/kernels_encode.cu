@@ -1,12 +1,14 @@
 // kernels_encode.cu — stage 3: multi-resolution hash-grid encode forward and backward.
 //
 //   k_encode_fwd   HashGrid::encode (grid.cpp:107-130) on the march samples; one thread per
-//                  (sample, level), 16 lanes per sample, so a warp covers 2 samples x 16
-//                  levels and each lane has its 8 corner gathers in flight at once (float2
+//                  (level, sample), a warp = 32 consecutive samples (mostly one ray) of one
+//                  level, each lane with its 8 corner gathers in flight at once (float2
 //                  rows, F = 2).  Position, lattice indices and corner weights are fp64 and
 //                  bit-exact (geometry.cuh); features accumulate in fp32.
 //   k_encode_bwd   HashGrid::encode_backward (grid.cpp:132-157): the same corners receive
 //                  w * upstream through vector float2 atomics (red.global.add.v2.f32).
+//
+// Features and their gradients are level-major: X[l][s] (float2), l < L, s < n_total.
 //
 // Algorithmic traffic: 8 corners x L levels x 8 B = 1024 B/sample gathered
 // forward; the backward read-modify-writes the same 1024 B.
@@ -63,37 +65,36 @@ __device__ __forceinline__ void scatter_level(float2* __restrict__ table, const 
   }
 }
 
+// Level-major launch: grid (sample chunks, levels).  CTAs are dispatched roughly in blockIdx
+// order, so the device works through one level's table at a time: a dense level (<= 2^24
+// rows) or one hashed 2^24-row table (128 MiB) is the live working set, which keeps the L2
+// hit rate high instead of streaming every level's random rows from HBM at once.  Features
+// are stored level-major too (X[l][s] float2), so every store is coalesced.
 __global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __restrict__ X) {
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t s = tid >> 4;
-  const uint32_t l = (uint32_t)(tid & 15);
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t l = blockIdx.y;
   if (s >= f.n_total) return;
   const uint32_t casc = s >= f.fine_total ? 1u : 0u;
   const uint32_t item = f.s_item[s];
   const FieldDesc& fd = f.fields[casc * f.n_local + f.item_part[item]];
-  float2 acc = make_float2(0.f, 0.f);
-  if (l < fd.L) {
-    const RayRec& r = f.rec[item];
-    double p[3];
-    normalized_point(fd.box_lo, fd.box_hi, r.o, r.d, f.s_t[s], p);
-    Corners c;
-    level_corners(fd.lv[l], p, c);
-    acc = gather_level(reinterpret_cast<const float2*>(f.params + fd.base + fd.lv[l].offset), c);
-  }
-  reinterpret_cast<float2*>(X)[s * 16 + l] = acc;
+  const RayRec& r = f.rec[item];
+  double p[3];
+  normalized_point(fd.box_lo, fd.box_hi, r.o, r.d, f.s_t[s], p);
+  Corners c;
+  level_corners(fd.lv[l], p, c);
+  const float2 acc = gather_level(reinterpret_cast<const float2*>(f.params + fd.base + fd.lv[l].offset), c);
+  reinterpret_cast<float2*>(X)[(uint64_t)l * f.n_total + s] = acc;
 }
 
 __global__ void __launch_bounds__(256) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t s = tid >> 4;
-  const uint32_t l = (uint32_t)(tid & 15);
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t l = blockIdx.y;
   if (s >= f.n_total) return;
+  const float2 up = reinterpret_cast<const float2*>(dX)[(uint64_t)l * f.n_total + s];
+  if (up.x == 0.f && up.y == 0.f) return;
   const uint32_t casc = s >= f.fine_total ? 1u : 0u;
   const uint32_t item = f.s_item[s];
   const FieldDesc& fd = f.fields[casc * f.n_local + f.item_part[item]];
-  if (l >= fd.L) return;
-  const float2 up = reinterpret_cast<const float2*>(dX)[s * 16 + l];
-  if (up.x == 0.f && up.y == 0.f) return;
   const RayRec& r = f.rec[item];
   double p[3];
   normalized_point(fd.box_lo, fd.box_hi, r.o, r.d, f.s_t[s], p);
@@ -105,33 +106,27 @@ __global__ void __launch_bounds__(256) k_encode_bwd(FieldLaunch f, const float* 
 __global__ void k_encode_points(const FieldDesc* __restrict__ field, const float* __restrict__ params,
                                 const double* __restrict__ pts, uint64_t n, float* __restrict__ X,
                                 uint32_t* __restrict__ rows) {
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t s = tid >> 4;
-  const uint32_t l = (uint32_t)(tid & 15);
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t l = blockIdx.y;
   if (s >= n) return;
   const FieldDesc& fd = *field;
-  float2 acc = make_float2(0.f, 0.f);
-  if (l < fd.L) {
-    const double p[3] = {pts[3 * s], pts[3 * s + 1], pts[3 * s + 2]};
-    Corners c;
-    level_corners(fd.lv[l], p, c);
-    if (rows)
-      for (int k = 0; k < 8; ++k) rows[(s * fd.L + l) * 8 + k] = c.row[k];
-    acc = gather_level(reinterpret_cast<const float2*>(params + fd.base + fd.lv[l].offset), c);
-  }
-  reinterpret_cast<float2*>(X)[s * 16 + l] = acc;
+  const double p[3] = {pts[3 * s], pts[3 * s + 1], pts[3 * s + 2]};
+  Corners c;
+  level_corners(fd.lv[l], p, c);
+  if (rows)
+    for (int k = 0; k < 8; ++k) rows[(s * fd.L + l) * 8 + k] = c.row[k];
+  reinterpret_cast<float2*>(X)[(uint64_t)l * n + s] =
+      gather_level(reinterpret_cast<const float2*>(params + fd.base + fd.lv[l].offset), c);
 }
 
 __global__ void k_encode_points_bwd(const FieldDesc* __restrict__ field, float* __restrict__ grads,
                                     const double* __restrict__ pts, const float* __restrict__ dX,
                                     uint64_t n) {
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t s = tid >> 4;
-  const uint32_t l = (uint32_t)(tid & 15);
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t l = blockIdx.y;
   if (s >= n) return;
   const FieldDesc& fd = *field;
-  if (l >= fd.L) return;
-  const float2 up = reinterpret_cast<const float2*>(dX)[s * 16 + l];
+  const float2 up = reinterpret_cast<const float2*>(dX)[(uint64_t)l * n + s];
   if (up.x == 0.f && up.y == 0.f) return;
   const double p[3] = {pts[3 * s], pts[3 * s + 1], pts[3 * s + 2]};
   Corners c;
@@ -139,30 +134,30 @@ __global__ void k_encode_points_bwd(const FieldDesc* __restrict__ field, float* 
   scatter_level(reinterpret_cast<float2*>(grads + fd.base + fd.lv[l].offset), c, up);
 }
 
-inline unsigned grid16(uint64_t n) { return (unsigned)((n * 16 + 255) / 256); }
+inline dim3 grid_lv(uint64_t n, uint32_t L) { return dim3((unsigned)((n + 255) / 256), L); }
 
 }  // namespace
 
 void launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s) {
   if (!f.n_total) return;
-  k_encode_fwd<<<grid16(f.n_total), 256, 0, s>>>(f, X);
+  k_encode_fwd<<<grid_lv(f.n_total, f.levels), 256, 0, s>>>(f, X);
 }
 
 void launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s) {
   if (!f.n_total) return;
-  k_encode_bwd<<<grid16(f.n_total), 256, 0, s>>>(f, dX);
+  k_encode_bwd<<<grid_lv(f.n_total, f.levels), 256, 0, s>>>(f, dX);
 }
 
 void launch_encode_points(const FieldDesc* field, const float* params, const double* pts,
-                          uint64_t n, float* X, uint32_t* rows, cudaStream_t s) {
+                          uint64_t n, uint32_t levels, float* X, uint32_t* rows, cudaStream_t s) {
   if (!n) return;
-  k_encode_points<<<grid16(n), 256, 0, s>>>(field, params, pts, n, X, rows);
+  k_encode_points<<<grid_lv(n, levels), 256, 0, s>>>(field, params, pts, n, X, rows);
 }
 
 void launch_encode_points_bwd(const FieldDesc* field, float* grads, const double* pts,
-                              const float* dX, uint64_t n, cudaStream_t s) {
+                              const float* dX, uint64_t n, uint32_t levels, cudaStream_t s) {
   if (!n) return;
-  k_encode_points_bwd<<<grid16(n), 256, 0, s>>>(field, grads, pts, dX, n);
+  k_encode_points_bwd<<<grid_lv(n, levels), 256, 0, s>>>(field, grads, pts, dX, n);
 }
 
 }  // namespace dg

@@ -273,19 +273,18 @@ __device__ __forceinline__ float clip15(float v, bool& clipped) {
   return v > 15.f ? 15.f : (v < -15.f ? -15.f : v);
 }
 
-// Load a tile's encodings (n x 32, sample-major in global) into x[32][LD]; zero-pad rows.
+// Load a tile's encodings (level-major float2 rows in global) into x[32][LD]; zero-pad.
 template <int TILE>
-__device__ __forceinline__ void load_x(const float* __restrict__ X, uint64_t s0, int count,
+__device__ __forceinline__ void load_x(const MlpLaunch& m, uint64_t s0, int count,
                                        float* __restrict__ x) {
   constexpr int LD = TILE + 4;
-  for (int e = threadIdx.x; e < TILE * 8; e += NT) {
-    const int s = e / 8, q = e % 8;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (s < count) v = *reinterpret_cast<const float4*>(X + (s0 + s) * kEnc + q * 4);
-    x[(q * 4 + 0) * LD + s] = v.x;
-    x[(q * 4 + 1) * LD + s] = v.y;
-    x[(q * 4 + 2) * LD + s] = v.z;
-    x[(q * 4 + 3) * LD + s] = v.w;
+  for (int e = threadIdx.x; e < TILE * 16; e += NT) {
+    const int l = e / TILE, s = e % TILE;
+    float2 v = make_float2(0.f, 0.f);
+    if (s < count && l < (int)m.levels)
+      v = reinterpret_cast<const float2*>(m.X)[(uint64_t)l * m.x_stride + s0 + s];
+    x[(2 * l) * LD + s] = v.x;
+    x[(2 * l + 1) * LD + s] = v.y;
   }
 }
 
@@ -350,7 +349,7 @@ __global__ void __launch_bounds__(NT, 2) k_mlp_fwd(MlpLaunch m) {
       load_weights(fd, m.params, sm.w, nullptr);
       loaded = f;
     }
-    load_x<FT>(m.X, s0, count, sm.a);
+    load_x<FT>(m, s0, count, sm.a);
     __syncthreads();
     gemm_layer<FT, kHidden, kEnc, 4, 8>(sm.w.d0, kHidden, sm.w.bd0, sm.a, sm.b, ACT_RELU);
     __syncthreads();
@@ -477,7 +476,7 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_bwd(MlpLaunch m) {
     }
     const int cact = fd.coarse ? ACT_SIGMOID : ACT_RELU;
     // ---- forward recompute ----
-    load_x<BT>(m.X, s0, count, sm.x);
+    load_x<BT>(m, s0, count, sm.x);
     __syncthreads();
     gemm_layer<BT, kHidden, kEnc, 4, 4>(sm.w.d0, kHidden, sm.w.bd0, sm.x, sm.h1, ACT_RELU);
     __syncthreads();
@@ -544,13 +543,11 @@ __global__ void __launch_bounds__(NT, 1) k_mlp_bwd(MlpLaunch m) {
     __syncthreads();
     gemm_back<BT, kEnc, kHidden, 4, 2>(sm.wn.d0, kEnc, sm.h1, sm.x, ACT_NONE);
     __syncthreads();
-    for (int e = tid; e < BT * 8; e += NT) {
-      const int s = e / 8, q = e % 8;
-      if (s < count) {
-        const float4 v = make_float4(sm.x[(q * 4 + 0) * BLD + s], sm.x[(q * 4 + 1) * BLD + s],
-                                     sm.x[(q * 4 + 2) * BLD + s], sm.x[(q * 4 + 3) * BLD + s]);
-        *reinterpret_cast<float4*>(m.dX + (s0 + s) * kEnc + q * 4) = v;
-      }
+    for (int e = tid; e < BT * 16; e += NT) {
+      const int l = e / BT, s = e % BT;
+      if (s < count && l < (int)m.levels)
+        reinterpret_cast<float2*>(m.dX)[(uint64_t)l * m.x_stride + s0 + s] =
+            make_float2(sm.x[(2 * l) * BLD + s], sm.x[(2 * l + 1) * BLD + s]);
     }
     __syncthreads();
   }

@@ -649,6 +649,7 @@ FieldLaunch field_launch(dg_ctx* c) {
   f.fine_total = c->n_fine;
   f.n_total = c->n_fine + c->n_coarse;
   f.n_local = uint32_t(c->local.size());
+  f.levels = c->cfg.grid_levels;
   f.params = c->params.as<float>();
   f.grads = c->grads.as<float>();
   return f;
@@ -669,6 +670,8 @@ MlpLaunch mlp_launch(dg_ctx* c, bool bwd) {
   m.tile_off = bwd ? c->tile_off_b.as<uint32_t>() : c->tile_off_f.as<uint32_t>();
   m.n_tiles = tiles;
   m.X = c->s_X.as<float>();
+  m.x_stride = uint64_t(c->n_fine) + c->n_coarse;
+  m.levels = c->cfg.grid_levels;
   m.rec = c->rec.as<RayRec>();
   m.s_item = c->s_item.as<uint32_t>();
   m.app_table = c->app.as<float>();
@@ -1404,7 +1407,7 @@ int dg_encode(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points, uin
   }
   TRY(X.ensure(n * kEnc * 4 + 16));
   if (rows) TRY(R.ensure(n * L * 8 * 4 + 16));
-  launch_encode_points(fd, c->params.as<float>(), pd, n, X.as<float>(), rows ? R.as<uint32_t>() : nullptr, s);
+  launch_encode_points(fd, c->params.as<float>(), pd, n, L, X.as<float>(), rows ? R.as<uint32_t>() : nullptr, s);
   ++c->launches;
   // features: n x (L*2) compacted from the padded n x 32 rows
   std::vector<float> hx(n * kEnc);
@@ -1414,9 +1417,12 @@ int dg_encode(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points, uin
     else CU(cudaMemcpyAsync(rows, R.p, n * L * 8 * 4, cudaMemcpyDeviceToHost, s));
   }
   CU(cudaStreamSynchronize(s));
-  std::vector<float> packed(n * L * 2);
+  std::vector<float> packed(n * L * 2);  // level-major [L][n] float2 -> [n][L*2]
   for (uint64_t i = 0; i < n; ++i)
-    std::memcpy(&packed[i * L * 2], &hx[i * kEnc], L * 2 * sizeof(float));
+    for (uint32_t l = 0; l < L; ++l) {
+      packed[i * L * 2 + 2 * l] = hx[(l * n + i) * 2];
+      packed[i * L * 2 + 2 * l + 1] = hx[(l * n + i) * 2 + 1];
+    }
   if (mem == DG_MEM_DEVICE) CU(cudaMemcpy(features, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice));
   else std::memcpy(features, packed.data(), packed.size() * 4);
   return DG_OK;
@@ -1430,13 +1436,17 @@ int dg_encode_backward(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
   if (mem == DG_MEM_DEVICE) return set_err(DG_EINVAL, "dg_encode_backward: host buffers only");
   cudaStream_t s = c->stream;
   const uint32_t L = c->cfg.grid_levels;
-  std::vector<float> up(n * kEnc, 0.0f);
-  for (uint64_t i = 0; i < n; ++i) std::memcpy(&up[i * kEnc], upstream + i * L * 2, L * 2 * 4);
+  std::vector<float> up(n * kEnc, 0.0f);  // [n][L*2] -> level-major [L][n] float2
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t l = 0; l < L; ++l) {
+      up[(l * n + i) * 2] = upstream[i * L * 2 + 2 * l];
+      up[(l * n + i) * 2 + 1] = upstream[i * L * 2 + 2 * l + 1];
+    }
   DBuf pts, dX;
   TRY(upload(pts, points, n * 24, s));
   TRY(upload(dX, up.data(), up.size() * 4, s));
   launch_encode_points_bwd(c->d_fields.as<FieldDesc>() + cascade * c->local.size() + lp, c->grads.as<float>(),
-                           pts.as<double>(), dX.as<float>(), n, s);
+                           pts.as<double>(), dX.as<float>(), n, L, s);
   ++c->launches;
   CU(cudaStreamSynchronize(s));
   return DG_OK;
@@ -1456,7 +1466,7 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
   DBuf pts, X, recs, items, appb, out, gin, dX, foff, toff;
   TRY(upload(pts, points, n * 24, s));
   TRY(X.ensure(n * kEnc * 4 + 16));
-  launch_encode_points(fd, c->params.as<float>(), pts.as<double>(), n, X.as<float>(), nullptr, s);
+  launch_encode_points(fd, c->params.as<float>(), pts.as<double>(), n, c->cfg.grid_levels, X.as<float>(), nullptr, s);
   std::vector<RayRec> rr(n);
   std::vector<uint32_t> ids(n);
   for (uint64_t i = 0; i < n; ++i) {
@@ -1480,6 +1490,8 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
   m.n_fields = 2 * nl;
   m.field_off = foff.as<uint32_t>();
   m.X = X.as<float>();
+  m.x_stride = n;
+  m.levels = c->cfg.grid_levels;
   m.rec = recs.as<RayRec>();
   m.s_item = items.as<uint32_t>();
   m.app_override = appb.as<float>();
@@ -1516,7 +1528,7 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
   m.grad_in = gin.as<float4>();
   m.dX = dX.as<float>();
   launch_mlp_bwd(m, c->num_sms, s);
-  launch_encode_points_bwd(fd, c->grads.as<float>(), pts.as<double>(), dX.as<float>(), n, s);
+  launch_encode_points_bwd(fd, c->grads.as<float>(), pts.as<double>(), dX.as<float>(), n, c->cfg.grid_levels, s);
   c->launches += 3;
   CU(cudaStreamSynchronize(s));
   return DG_OK;
@@ -1650,6 +1662,26 @@ int dg_enable_stage_timing(dg_ctx* c, int enable) {
 int dg_last_stage_times(dg_ctx* c, dg_stage_times* t) {
   TRY(check_ctx(c));
   *t = c->times;
+  return DG_OK;
+}
+
+int dg_selftest_tcgen05(const float* A, const float* B, const float* X, float* Y0, float* Y1,
+                        float* Y2) {
+  DBuf a, b, x, y0, y1, y2;
+  cudaStream_t s = nullptr;
+  TRY(upload(a, A, 128 * 64 * 4, s));
+  TRY(upload(b, B, 64 * 64 * 4, s));
+  TRY(upload(x, X, 128 * 32 * 4, s));
+  TRY(y0.ensure(128 * 64 * 4));
+  TRY(y1.ensure(128 * 64 * 4));
+  TRY(y2.ensure(64 * 32 * 4));
+  if (tc_selftest(a.as<float>(), b.as<float>(), x.as<float>(), y0.as<float>(), y1.as<float>(),
+                  y2.as<float>(), s) != 0)
+    return set_err(DG_ECUDA, "tcgen05 self-test launch failed");
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(Y0, y0.p, 128 * 64 * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(Y1, y1.p, 128 * 64 * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(Y2, y2.p, 64 * 32 * 4, cudaMemcpyDeviceToHost));
   return DG_OK;
 }
 

@@ -203,48 +203,17 @@ def _check_losses(sg, so):
     assert abs(sg["lr"] - so["lr"]) < 1e-15
 
 
-# Stated gradient tolerance.  Gradients are compared per parameter array by relative L2.
-# The hash-table gradients are sums of thousands of per-sample terms of both signs; at the
-# reference's init state (tables +-1e-4) every sample shades to nearly the same colour, so
-# the density gradient is a difference of near-equal colours (render.cpp:163, u - tail_color)
-# and the sums are ill-conditioned.  The bar is therefore relative to the problem's own
-# conditioning: GRAD_TOL, or 20x the rel-L2 by which the fp64 oracle itself moves when its
-# parameters are perturbed by fp32 rounding noise (2^-24 relative) — the error any
-# fp32-parameter implementation cannot avoid.
+# Stated gradient tolerance.  Gradients are sums of many per-sample contributions of both
+# signs, accumulated by fp32 atomics in a nondeterministic order from fp32 per-sample terms.
+# The standard error bound of such a sum scales with sum |contributions|, not with |sum|, so
+# the bar is stated against the oracle's exact fp64 sum of |contributions| (or_run_abs_grads):
+#     ||g_gpu - g_ref||_2 <= ABS_TOL * || sum_i |t_i| ||_2      per parameter array,
+# or the plain relative L2 GRAD_TOL when that is already met.
 GRAD_TOL = 1e-4
-NOISE_FACTOR = 20.0
+ABS_TOL = 1e-5
 
 
-def _noise_floor(cfg, p0, o, d, gt, img, step, src=None):
-    """rel-L2 per (partition, array) between two oracle runs whose parameters differ by
-    fp32-rounding-level relative noise."""
-    rng = np.random.default_rng(12345)
-    app = app_rows(1)
-    runs = []
-    for k in range(2):
-        orc = OracleRun(cfg, app)
-        for g in range(cfg.kx * cfg.ky):
-            p = p0[g].copy()
-            if k:
-                p *= 1.0 + rng.uniform(-1, 1, p.size) * 2.0 ** -24
-            orc.set_params(g, p)
-            if src is not None:
-                for c, box in enumerate(layout.region_boxes(cfg, g)):
-                    sh = layout.occupancy_shape(cfg, box)
-                    orc.set_occupancy(g, c, src.occupancy(g, c, sh[0] * sh[1] * sh[2]))
-        orc.train_step(o, d, gt, img, step)
-        runs.append(orc)
-    floor = {}
-    for g in range(cfg.kx * cfg.ky):
-        a, b = runs[0].grads(g), runs[1].grads(g)
-        from .helpers import layout_arrays
-        for arr in layout_arrays(cfg, g):
-            sl = slice(arr["offset"], arr["offset"] + arr["size"])
-            floor[(g, arr["offset"])] = rel_l2(b[sl], a[sl]) if np.abs(a[sl]).max() > 0 else 0.0
-    return floor
-
-
-def _check_update(cfg, ctx, orc, p0, lr, floor=None):
+def _check_update(cfg, ctx, orc, p0, lr):
     worst = {}
     for g in range(cfg.kx * cfg.ky):
         m_g, _, t_g = ctx.get_adam(g)
@@ -259,17 +228,16 @@ def _check_update(cfg, ctx, orc, p0, lr, floor=None):
                 assert np.abs(grad_g[a]).max() < 1e-20
                 continue
             e = rel_l2(grad_g[a], ref)
-            nf = floor.get((g, arr["offset"]), 0.0) if floor else 0.0
-            tol = max(GRAD_TOL, NOISE_FACTOR * nf)
-            worst[arr["kind"]] = max(worst.get(arr["kind"], 0.0), e)
-            assert e < tol, (g, arr, e, nf)
+            e_abs = np.linalg.norm(grad_g[a] - ref) / np.linalg.norm(orc.abs_grads(g)[a])
+            worst[arr["kind"]] = max(worst.get(arr["kind"], 0.0), min(e / GRAD_TOL, e_abs / ABS_TOL))
+            assert e < GRAD_TOL or e_abs < ABS_TOL, (g, arr, e, e_abs)
         dp_g = ctx.get_params(g).astype(np.float64) - p0[g]
         dp_o = orc.params(g) - p0[g]
         big = np.abs(grad_o) > 1e-6 * np.abs(grad_o).max()
         err = np.abs(dp_g - dp_o)[big]
         # sign flips of near-cancelling gradients are allowed on a tiny fraction
         assert np.mean(err <= 1e-3 * lr) > 0.999, (g, np.mean(err <= 1e-3 * lr), err.max())
-    print("grad rel-L2 by kind", worst)
+    print("grad error / bar by kind", worst)
 
 
 @pytest.mark.parametrize("state", ["init", "trained"])
@@ -299,7 +267,7 @@ def test_train_step_parity(kx, ky, gen, n, state):
         assert np.array_equal(cnt, co)
         assert np.array_equal(t_g.view(np.uint64), to.view(np.uint64))
         assert np.array_equal(d_g.view(np.uint64), do.view(np.uint64))
-    _check_update(cfg, ctx, orc, p0, sg["lr"], _noise_floor(cfg, p0, o, d, gt, img, 0))
+    _check_update(cfg, ctx, orc, p0, sg["lr"])
 
 
 def test_train_step_coarse_cascade_and_partial_occupancy():
@@ -312,7 +280,7 @@ def test_train_step_coarse_cascade_and_partial_occupancy():
     so = orc.train_step(o, d, gt, img, 0)
     _check_losses(sg, so)
     assert any(ctx.last_items(g)[2] > 0 for g in range(4))  # coarse samples exist
-    _check_update(cfg, ctx, orc, p0, sg["lr"], _noise_floor(cfg, p0, o, d, gt, img, 0, src=orc))
+    _check_update(cfg, ctx, orc, p0, sg["lr"])
 
 
 def test_train_step_wire_f32():
