@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -124,6 +125,7 @@ struct dg_ctx {
   uint32_t n_images = 0, app_rows = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
+  int mlp_impl = 1;  // 1: tcgen05 split-bf16 forward (default), 0: FFMA fp32 (DG_MLP=ffma)
   std::unique_ptr<Comm> comm;
   uint64_t launches = 0;
   bool timing = false;
@@ -822,6 +824,7 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   CU(cudaSetDevice(device));
   CU(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   TRY(ctx_setup(c.get()));
+  if (const char* e = std::getenv("DG_MLP")) c->mlp_impl = std::strcmp(e, "ffma") == 0 ? 0 : 1;
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) CU(cudaEventCreate(&e));
   TRY(ctx_alloc(c.get()));
@@ -1097,7 +1100,8 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   launch_encode_fwd(fl, sm.X, s);
   mark(c, 3);
   const MlpLaunch mf = mlp_launch(c, false);
-  launch_mlp_fwd(mf, s);
+  if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);
+  else launch_mlp_fwd(mf, s);
   mark(c, 4);
   launch_composite(NI, it, sm, c->n_fine, 0, s);
   mark(c, 5);
@@ -1193,7 +1197,8 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   launch_encode_fwd(fl, sm.X, s);
   MlpLaunch mf = mlp_launch(c, false);
   mf.app_override = c->eval_app.as<float>();
-  launch_mlp_fwd(mf, s);
+  if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);
+  else launch_mlp_fwd(mf, s);
   launch_composite(NI, it, sm, c->n_fine, 1, s);
   c->launches += 3;
   const uint64_t n = b->n;
@@ -1504,7 +1509,8 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
     TRY(upload(toff, tf.data(), tf.size() * 4, s));
     m.tile_off = toff.as<uint32_t>();
     m.n_tiles = tf[2 * nl];
-    launch_mlp_fwd(m, s);
+    if (c->mlp_impl) launch_mlp_fwd_tc(m, c->num_sms, s);
+    else launch_mlp_fwd(m, s);
     std::vector<float4> h(n);
     CU(cudaMemcpyAsync(h.data(), out.p, n * 16, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
