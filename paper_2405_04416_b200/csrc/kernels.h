@@ -144,6 +144,7 @@ void launch_mlp_fwd(const MlpLaunch& m, cudaStream_t s);
 void launch_mlp_bwd(const MlpLaunch& m, int num_sms, cudaStream_t s);
 // tcgen05 (split-bf16) variants (kernels_mlp_tc.cu); tiles of 128 samples
 void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);
+void launch_mlp_bwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);  // tile_off at 128
 
 // ---- optimizer / init (kernels_adam.cu) ----
 void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, float b1, float b2,

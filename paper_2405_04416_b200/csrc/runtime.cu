@@ -1122,8 +1122,11 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
                         c->cfg.transmittance_clamp, c->loss.as<LossAccum>(), s);
   mark(c, 7);
   // K4b / K3b backward
-  const MlpLaunch mb = mlp_launch(c, true);
-  launch_mlp_bwd(mb, c->num_sms, s);
+  if (c->mlp_impl) {
+    launch_mlp_bwd_tc(mlp_launch(c, false), c->num_sms, s);  // 128-sample tiles
+  } else {
+    launch_mlp_bwd(mlp_launch(c, true), c->num_sms, s);
+  }
   mark(c, 8);
   launch_encode_bwd(fl, sm.dX, s);
   mark(c, 9);
@@ -1528,12 +1531,14 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
     g[i] = make_float4(sig_grad[i], rgb_grad[3 * i], rgb_grad[3 * i + 1], rgb_grad[3 * i + 2]);
   TRY(upload(gin, g.data(), n * 16, s));
   TRY(dX.ensure(n * kEnc * 4 + 16));
-  TRY(upload(toff, tb.data(), tb.size() * 4, s));
+  const std::vector<uint32_t>& tt = c->mlp_impl ? tf : tb;
+  TRY(upload(toff, tt.data(), tt.size() * 4, s));
   m.tile_off = toff.as<uint32_t>();
-  m.n_tiles = tb[2 * nl];
+  m.n_tiles = tt[2 * nl];
   m.grad_in = gin.as<float4>();
   m.dX = dX.as<float>();
-  launch_mlp_bwd(m, c->num_sms, s);
+  if (c->mlp_impl) launch_mlp_bwd_tc(m, c->num_sms, s);
+  else launch_mlp_bwd(m, c->num_sms, s);
   launch_encode_points_bwd(fd, c->grads.as<float>(), pts.as<double>(), dX.as<float>(), n, c->cfg.grid_levels, s);
   c->launches += 3;
   CU(cudaStreamSynchronize(s));
