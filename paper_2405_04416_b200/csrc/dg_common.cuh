@@ -102,9 +102,12 @@ struct __align__(8) RayRec {
 static_assert(sizeof(RayRec) == 72, "RayRec layout");
 
 // Partial record (exchange 2 / eval reply): PartialEntry payload (wire.hpp:143-155).
+// The segment transmittance travels as its optical depth tau (T = exp(-tau)): the same
+// information as T, but 1 - T = -expm1(-tau) stays accurate when T -> 1, where the
+// transmittance loss gradient lambda / (1 - T) (train.cpp:30-33) is largest.
 struct __align__(8) PartialRec {
   float rgb[3];
-  float T;
+  float tau;
   float depth;
   uint32_t ray_id;
 };

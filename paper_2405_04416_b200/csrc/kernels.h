@@ -25,7 +25,7 @@ struct ItemArrays {
   uint32_t* ncb;      // coarse samples before the fine box
   uint32_t* contains; // [P][NI] 1 when partition q is in the schedule and q != mine
   uint32_t* cscan;    // exclusive scan of contains
-  float4* partial;    // rgb, T of my segment
+  float4* partial;    // rgb, optical depth tau (T = exp(-tau)) of my segment
   float* depth;       // depth_sum of my segment
 };
 
@@ -71,8 +71,8 @@ void launch_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* part_
 void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                            const PartDesc* parts, const uint64_t* stream_off, uint32_t P,
                            const PartialRec* recv, SampleArrays sm, uint32_t fine_total,
-                           double lambda_t, double lambda_d, double t_clamp, LossAccum* loss,
-                           cudaStream_t s);
+                           double lambda_t, double lambda_d, double t_clamp, int wire_f32,
+                           LossAccum* loss, cudaStream_t s);
 void launch_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P, const uint32_t* part_item_off,
                         const uint32_t* contains, const uint32_t* cscan, uint32_t* out,
                         cudaStream_t s);

