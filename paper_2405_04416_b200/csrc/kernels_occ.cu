@@ -1,0 +1,112 @@
+// kernels_occ.cu — occupancy-grid update.
+//
+//   OccupancyGrid::decay_and_update (grid.cpp:201-229) + Worker::update_occupancy
+//   (worker.cpp:549-562):  density[i] <- max(density[i] * decay, sigma(jittered point of i))
+//   for the sampled cells, then bitfield = density >= threshold.  The jittered points come
+//   from the reference's own mt19937_64 stream (generated on the host, in the reference's
+//   draw order) so the sampled set is identical; sigma = query_density(p).sigma is evaluated
+//   here: fp64 bit-exact lattice indices, fp32 gathers, density MLP [enc -> 64 ReLU -> raw0].
+#include "geometry.cuh"
+#include "kernels.h"
+
+namespace dg {
+
+namespace {
+
+__global__ void __launch_bounds__(128) k_occ_query(const FieldDesc* __restrict__ field,
+                                                   const float* __restrict__ params,
+                                                   const double* __restrict__ pw, uint64_t n,
+                                                   float* __restrict__ sigma) {
+  __shared__ float w0[kHidden * kEnc];  // [o][i]
+  __shared__ float b0[kHidden];
+  __shared__ float w1[kHidden];         // row 0 of the second layer
+  __shared__ float b1;
+  const FieldDesc& fd = *field;
+  const float* base = params + fd.base;
+  const int enc = (int)fd.L * 2;
+  for (int e = threadIdx.x; e < kHidden * kEnc; e += blockDim.x) {
+    const int o = e / kEnc, i = e % kEnc;
+    w0[e] = i < enc ? base[fd.dw0 + o * enc + i] : 0.f;
+  }
+  for (int e = threadIdx.x; e < kHidden; e += blockDim.x) {
+    b0[e] = base[fd.db0 + e];
+    w1[e] = base[fd.dw1 + e];
+  }
+  if (threadIdx.x == 0) b1 = base[fd.db1];
+  __syncthreads();
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  // worker.cpp:215: p = clamp(box.to_unit(world point), 0, 1)
+  double p[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    p[a] = sclamp(ddiv(dsub(pw[3 * s + a], fd.box_lo[a]), dsub(fd.box_hi[a], fd.box_lo[a])), 0.0, 1.0);
+  float x[kEnc];
+#pragma unroll
+  for (int i = 0; i < kEnc; ++i) x[i] = 0.f;
+  for (uint32_t l = 0; l < fd.L; ++l) {
+    const LevelDesc& lv = fd.lv[l];
+    const AxisW ax = lattice_axis(p[0], lv.n[0]);
+    const AxisW ay = lattice_axis(p[1], lv.n[1]);
+    const AxisW az = lattice_axis(p[2], lv.n[2]);
+    const double fx[2] = {dsub(1.0, ax.frac), ax.frac};
+    const double fy[2] = {dsub(1.0, ay.frac), ay.frac};
+    const double fz[2] = {dsub(1.0, az.frac), az.frac};
+    const float2* table = reinterpret_cast<const float2*>(base + lv.offset);
+    float ax0 = 0.f, ax1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int cx = k & 1, cy = (k >> 1) & 1, cz = (k >> 2) & 1;
+      const double w = dmul(dmul(fx[cx], fy[cy]), fz[cz]);
+      if (w == 0.0) continue;
+      const float2 v = __ldg(table + table_row(lv, cx ? ax.i1 : ax.i0, cy ? ay.i1 : ay.i0,
+                                               cz ? az.i1 : az.i0));
+      ax0 = fmaf((float)w, v.x, ax0);
+      ax1 = fmaf((float)w, v.y, ax1);
+    }
+    x[2 * l] = ax0;
+    x[2 * l + 1] = ax1;
+  }
+  float raw = b1;
+  for (int o = 0; o < kHidden; ++o) {
+    float h = b0[o];
+#pragma unroll
+    for (int i = 0; i < kEnc; ++i) h = fmaf(w0[o * kEnc + i], x[i], h);
+    raw = fmaf(w1[o], h > 0.f ? h : 0.f, raw);
+  }
+  raw = raw > 15.f ? 15.f : (raw < -15.f ? -15.f : raw);
+  sigma[s] = expf(raw);
+}
+
+// Warm-up sweep: every cell exactly once, so the update is a pure element-wise max.
+__global__ void k_occ_apply(float* __restrict__ density, const uint32_t* __restrict__ cells,
+                            const float* __restrict__ sigma, uint64_t n, float decay) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t c = cells[s];
+  density[c] = fmaxf(density[c] * decay, sigma[s]);
+}
+
+__global__ void k_occ_bits(const float* __restrict__ density, uint8_t* __restrict__ bits,
+                           uint64_t n, float threshold) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) bits[s] = density[s] >= threshold ? 1 : 0;
+}
+
+inline unsigned nb(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void launch_occ_query(const FieldDesc* field, const float* params, const double* pw, uint64_t n,
+                      float* sigma, cudaStream_t s) {
+  if (n) k_occ_query<<<nb(n, 128), 128, 0, s>>>(field, params, pw, n, sigma);
+}
+void launch_occ_apply(float* density, const uint32_t* cells, const float* sigma, uint64_t n,
+                      float decay, cudaStream_t s) {
+  if (n) k_occ_apply<<<nb(n, 256), 256, 0, s>>>(density, cells, sigma, n, decay);
+}
+void launch_occ_bits(const float* density, uint8_t* bits, uint64_t n, float threshold, cudaStream_t s) {
+  if (n) k_occ_bits<<<nb(n, 256), 256, 0, s>>>(density, bits, n, threshold);
+}
+
+}  // namespace dg

@@ -119,6 +119,9 @@ struct dg_ctx {
   std::vector<std::vector<dg_array_desc>> layouts;
   uint64_t n_params = 0;
   uint64_t occ_bytes = 0;
+  std::vector<double> occ_thr;            // [n_local][2] current thresholds
+  std::vector<std::mt19937_64> occ_rng;   // Worker::occ_rng_ per local partition (worker.cpp:186)
+  uint64_t occ_updates = 0;
   double step = 0.0;
   uint64_t adam_t = 0;
   uint64_t worker_step = 0;
@@ -133,7 +136,7 @@ struct dg_ctx {
   dg_stage_times times{};
 
   // persistent device state
-  DBuf d_geo, d_parts, d_fields, params, grads, adam_m, adam_v, occ, app, slot_of_part_d,
+  DBuf d_geo, d_parts, d_fields, params, grads, adam_m, adam_v, occ, occ_den, app, slot_of_part_d,
       local_of_global_d, global_of_local_d;
   // per-step scratch
   DBuf h_o, h_d, h_gt, h_img, h_nseg, h_sched, h_flags, h_pos, cub_tmp, small, dropped, loss,
@@ -141,7 +144,7 @@ struct dg_ctx {
       it_off, it_ncb, it_contains, it_cscan, it_partial, it_depth, part_item_off_d, s_t, s_delta,
       s_item, s_X, s_out, s_grad, s_dX, field_off_d, tile_off_f, tile_off_b, stream_send_d,
       stream_recv_d, send_buf, recv_buf, x_send, x_recv, out_rgb, out_T, out_depth, eval_app,
-      perm_tab;
+      perm_tab, occ_pts, occ_cells, occ_sigma;
   // last step (introspection)
   std::vector<uint32_t> part_item_off;   // n_local + 1
   std::vector<uint32_t> field_off;       // 2 n_local + 1
@@ -329,6 +332,16 @@ int ctx_alloc(dg_ctx* c) {
   }
   TRY(c->occ.ensure(c->occ_bytes));
   CU(cudaMemsetAsync(c->occ.p, 1, c->occ_bytes, s));  // fill_occupied (worker.cpp:199-200)
+  // occupancy densities start at the initial threshold (grid.cpp:188-191)
+  const double thr0 = c->cfg.occ_threshold_early * c->cfg.occ_threshold_scale;
+  c->occ_thr.assign(2 * c->local.size(), thr0);
+  TRY(c->occ_den.ensure(c->occ_bytes * sizeof(float)));
+  {
+    std::vector<float> den(c->occ_bytes, float(thr0));
+    CU(cudaMemcpyAsync(c->occ_den.p, den.data(), den.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  for (uint32_t gid : c->local) c->occ_rng.emplace_back(splitmix64(counter_hash(c->cfg.seed, 0x0cc0, gid, 0)));
   // default appearance: one zero row for image 0
   c->app_rows = 1;
   c->n_images = 1;
@@ -749,6 +762,96 @@ int d2h(std::vector<T>& v, const void* src, uint64_t n, cudaStream_t s) {
   return DG_OK;
 }
 
+
+// Worker::update_occupancy (worker.cpp:549-562) + OccupancyGrid::decay_and_update
+// (grid.cpp:201-229).  The jitter points are the reference's mt19937_64 draws in its order
+// (fine grid, then coarse grid, same stream); sigma is evaluated on the device.
+int occupancy_update(dg_ctx* c) {
+  const dg_run_config& cfg = c->cfg;
+  const uint64_t step = c->worker_step;
+  if (!cfg.occupancy_updates || step == 0 || cfg.occ_update_interval == 0 ||
+      step % cfg.occ_update_interval != 0)
+    return DG_OK;
+  cudaStream_t s = c->stream;
+  const double threshold =
+      (step < cfg.occ_threshold_switch_step ? cfg.occ_threshold_early : cfg.occ_threshold_late) *
+      cfg.occ_threshold_scale;
+  const bool warm_up = step <= cfg.occ_warmup_steps;
+  const uint32_t nl = uint32_t(c->local.size());
+  for (uint32_t lp = 0; lp < nl; ++lp) {
+    const PartDesc& pd = c->parts[lp];
+    for (int casc = 0; casc < 2; ++casc) {  // set_threshold: recompute the bitfield
+      const uint64_t n = uint64_t(pd.occ_n[casc][0]) * pd.occ_n[casc][1] * pd.occ_n[casc][2];
+      c->occ_thr[lp * 2 + casc] = threshold;
+      launch_occ_bits(c->occ_den.as<float>() + pd.occ_off[casc], c->occ.as<uint8_t>() + pd.occ_off[casc],
+                      n, float(threshold), s);
+      ++c->launches;
+    }
+    std::mt19937_64& rng = c->occ_rng[lp];
+    auto uni = [&](double lo, double hi) { return lo + (hi - lo) * (double(rng() >> 11) * 0x1.0p-53); };
+    for (int casc = 0; casc < 2; ++casc) {
+      const uint32_t* sh = pd.occ_n[casc];
+      const uint64_t total = uint64_t(sh[0]) * sh[1] * sh[2];
+      const double* lo = casc == 0 ? pd.fine_lo : pd.coarse_lo;
+      const double* hi = casc == 0 ? pd.fine_hi : pd.coarse_hi;
+      double cell[3];
+      for (int a = 0; a < 3; ++a) cell[a] = (hi[a] - lo[a]) / double(sh[a]);
+      std::vector<uint32_t> cells;
+      std::vector<double> pts;
+      auto sample = [&](uint64_t idx) {  // sample_cell (grid.cpp:206-214)
+        const uint64_t ii[3] = {idx % sh[0], (idx / sh[0]) % sh[1], idx / (uint64_t(sh[0]) * sh[1])};
+        double clo[3], chi[3];
+        for (int a = 0; a < 3; ++a) {
+          clo[a] = lo[a] + cell[a] * double(ii[a]);
+          chi[a] = clo[a] + cell[a];
+        }
+        cells.push_back(uint32_t(idx));
+        for (int a = 0; a < 3; ++a) pts.push_back(uni(clo[a], chi[a]));
+      };
+      if (warm_up) {
+        cells.reserve(total);
+        pts.reserve(3 * total);
+        for (uint64_t i = 0; i < total; ++i) sample(i);
+      } else {
+        std::vector<uint8_t> bits(total);
+        CU(cudaMemcpyAsync(bits.data(), c->occ.as<uint8_t>() + pd.occ_off[casc], total,
+                           cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        std::vector<uint64_t> occupied;
+        for (uint64_t i = 0; i < total; ++i)
+          if (bits[i]) occupied.push_back(i);
+        const uint64_t n_uniform = std::max<uint64_t>(total / 4, 1);
+        for (uint64_t i = 0; i < n_uniform; ++i) sample(rng() % total);
+        if (!occupied.empty())
+          for (uint64_t i = 0; i < n_uniform; ++i) sample(occupied[rng() % occupied.size()]);
+      }
+      const uint64_t n = cells.size();
+      TRY(upload(c->occ_pts, pts.data(), pts.size() * sizeof(double), s));
+      TRY(upload(c->occ_cells, cells.data(), n * sizeof(uint32_t), s));
+      TRY(c->occ_sigma.ensure(n * sizeof(float) + 16));
+      const FieldDesc* fd = c->d_fields.as<FieldDesc>() + casc * nl + lp;
+      launch_occ_query(fd, c->params.as<float>(), c->occ_pts.as<double>(), n, c->occ_sigma.as<float>(), s);
+      float* den = c->occ_den.as<float>() + pd.occ_off[casc];
+      if (warm_up) {
+        launch_occ_apply(den, c->occ_cells.as<uint32_t>(), c->occ_sigma.as<float>(), n,
+                         float(cfg.occ_decay), s);
+      } else {  // cells may repeat: apply sequentially in draw order on the host
+        std::vector<float> sig(n), hd(total);
+        CU(cudaMemcpyAsync(sig.data(), c->occ_sigma.p, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hd.data(), den, total * sizeof(float), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        for (uint64_t k = 0; k < n; ++k) hd[cells[k]] = std::max(hd[cells[k]] * float(cfg.occ_decay), sig[k]);
+        CU(cudaMemcpyAsync(den, hd.data(), total * sizeof(float), cudaMemcpyHostToDevice, s));
+      }
+      launch_occ_bits(den, c->occ.as<uint8_t>() + pd.occ_off[casc], total, float(threshold), s);
+      c->launches += 3;
+      c->h2d += pts.size() * sizeof(double) + n * sizeof(uint32_t);
+    }
+  }
+  ++c->occ_updates;
+  return DG_OK;
+}
+
 int check_ctx(const dg_ctx* c) {
   if (!c) return set_err(DG_EINVAL, "null context");
   return DG_OK;
@@ -1043,7 +1146,19 @@ static int occ_copy(dg_ctx* c, uint32_t p, uint32_t cascade, uint8_t* out, const
 }
 
 int dg_set_occupancy(dg_ctx* c, uint32_t p, uint32_t cascade, const uint8_t* bits) {
-  return occ_copy(c, p, cascade, nullptr, bits);
+  TRY(occ_copy(c, p, cascade, nullptr, bits));
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  // density := threshold where occupied, 0 elsewhere (as OccupancyGrid::recompute_bitfield sees it)
+  const PartDesc& pd = c->parts[lp];
+  const uint64_t n = uint64_t(pd.occ_n[cascade][0]) * pd.occ_n[cascade][1] * pd.occ_n[cascade][2];
+  const float thr = float(c->occ_thr[lp * 2 + cascade]);
+  std::vector<float> den(n);
+  for (uint64_t i = 0; i < n; ++i) den[i] = bits[i] ? thr : 0.0f;
+  CU(cudaMemcpyAsync(c->occ_den.as<float>() + pd.occ_off[cascade], den.data(), n * sizeof(float),
+                     cudaMemcpyHostToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
 }
 int dg_get_occupancy(dg_ctx* c, uint32_t p, uint32_t cascade, uint8_t* bits) {
   return occ_copy(c, p, cascade, bits, nullptr);
@@ -1142,6 +1257,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   ++c->launches;
   mark(c, 10);
   c->worker_step = step + 1;
+  TRY(occupancy_update(c));
   LossAccum la;
   CU(cudaMemcpyAsync(&la, c->loss.p, sizeof la, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));

@@ -370,3 +370,30 @@ def test_init_reference_matches_reference_build():
     for g in range(2):
         ctx.init_reference(g)
         assert np.array_equal(ctx.get_params(g), ref.params(g).astype(np.float32))
+
+
+# ------------------------------------------------------------------ occupancy update (§8f row 1)
+@pytest.mark.parametrize("warmup", [4096, 4])
+def test_occupancy_update_matches_reference_stream(warmup):
+    """Steps 14, 15, 16 cross Worker::update_occupancy (worker.cpp:549-562).  The sampled
+    cells and jitter points follow the reference's mt19937_64 stream, so bitfields agree except
+    for cells whose density lies within fp32 resolution of the threshold."""
+    cfg = small_cfg(2, 1, table_log2=12, levels=8, nmax=128, divisor=64, occ_res=16,
+                    inner=((0.2, 0.1, 0.0), (1.7, 0.9, 0.9)))
+    cfg.occ_warmup_steps = warmup
+    cfg.occ_threshold_scale = 1.5  # threshold 0.9 vs sigma ~ exp(small): a mixed bitfield
+    ctx, orc, _ = _pair(cfg, table_scale=0.5, occupancy_fraction=0.7)
+    for step in (14, 15, 16):
+        o, d, gt, img = _rays(cfg, 512, "random", seed=step)
+        sg = ctx.train_step(o, d, gt, img, step=step)
+        so = orc.train_step(o, d, gt, img, step)
+        if step < 15:
+            _check_losses(sg, so)
+    for g in range(2):
+        for c, box in enumerate(layout.region_boxes(cfg, g)):
+            sh = layout.occupancy_shape(cfg, box)
+            n = sh[0] * sh[1] * sh[2]
+            bg = ctx.get_occupancy(g, c)
+            bo = orc.occupancy(g, c, n)
+            assert 0 < bo.mean() < 1 or warmup == 4
+            assert np.mean(bg == bo) > 0.995, (g, c, np.mean(bg == bo))
