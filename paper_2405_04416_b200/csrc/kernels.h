@@ -107,6 +107,8 @@ struct FieldLaunch {
   uint32_t n_total;
   uint32_t n_local;
   uint32_t levels;
+  uint32_t dense_levels;   // leading levels processed together (one-to-one tables), >= 1
+  uint32_t agg_levels;     // levels whose backward scatter is warp-aggregated
   const float* params;
   float* grads;
 };

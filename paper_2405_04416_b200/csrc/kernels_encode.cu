@@ -65,42 +65,102 @@ __device__ __forceinline__ void scatter_level(float2* __restrict__ table, const 
   }
 }
 
-// Level-major launch: grid (sample chunks, levels).  CTAs are dispatched roughly in blockIdx
-// order, so the device works through one level's table at a time: a dense level (<= 2^24
-// rows) or one hashed 2^24-row table (128 MiB) is the live working set, which keeps the L2
-// hit rate high instead of streaming every level's random rows from HBM at once.  Features
-// are stored level-major too (X[l][s] float2), so every store is coalesced.
+// Streaming accesses (sample arrays, features) bypass L2 residency so the hash tables keep it.
+__device__ __forceinline__ float2 ld_stream(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.cs.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_stream(float2* p, float2 v) {
+  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y));
+}
+
+// Warp-aggregated scatter of one level: lanes hold consecutive samples (mostly one ray, in t
+// order), so at coarse levels neighbouring lanes share cells and hence identical corner rows.
+// For each corner slot, runs of equal (field, row) in lane order are summed with a segmented
+// shuffle scan and the run's last lane issues a single float2 red.
+__device__ __forceinline__ void scatter_level_agg(float2* __restrict__ table, const Corners& c,
+                                                  float2 up, uint32_t field, bool valid) {
+  const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t row = valid ? c.row[k] : 0xffffffffu;
+    const uint32_t prev_row = __shfl_up_sync(0xffffffffu, row, 1);
+    const uint32_t prev_fld = __shfl_up_sync(0xffffffffu, field, 1);
+    const bool head = lane == 0 || prev_row != row || prev_fld != field;
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    const unsigned run = 31u - __clz(heads & (0xffffffffu >> (31u - lane)));  // run start lane
+    float vx = c.w[k] * up.x, vy = c.w[k] * up.y;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float tx = __shfl_up_sync(0xffffffffu, vx, off);
+      const float ty = __shfl_up_sync(0xffffffffu, vy, off);
+      if (lane >= (unsigned)off && lane - off >= run) {
+        vx += tx;
+        vy += ty;
+      }
+    }
+    const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
+    if (tail && row != 0xffffffffu && (vx != 0.f || vy != 0.f))
+      atomicAdd(table + row, make_float2(vx, vy));
+  }
+}
+
+// Level-group launch: grid (sample chunks, level groups).  Group 0 holds the leading dense
+// (one-to-one) levels, whose tables fit in L2 together; every hashed level (2^T rows) is its
+// own group.  CTAs are dispatched roughly in blockIdx order, so the device works through one
+// group's tables at a time and they stay L2-resident instead of streaming all 16 levels'
+// random rows from HBM at once.  Features are level-major (X[l][s] float2): coalesced.
 __global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __restrict__ X) {
   const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t l = blockIdx.y;
   if (s >= f.n_total) return;
+  const uint32_t l0 = blockIdx.y == 0 ? 0u : f.dense_levels + blockIdx.y - 1;
+  const uint32_t l1 = blockIdx.y == 0 ? f.dense_levels : l0 + 1;
   const uint32_t casc = s >= f.fine_total ? 1u : 0u;
-  const uint32_t item = f.s_item[s];
+  const uint32_t item = __ldcs(f.s_item + s);
   const FieldDesc& fd = f.fields[casc * f.n_local + f.item_part[item]];
   const RayRec& r = f.rec[item];
   double p[3];
-  normalized_point(fd.box_lo, fd.box_hi, r.o, r.d, f.s_t[s], p);
-  Corners c;
-  level_corners(fd.lv[l], p, c);
-  const float2 acc = gather_level(reinterpret_cast<const float2*>(f.params + fd.base + fd.lv[l].offset), c);
-  reinterpret_cast<float2*>(X)[(uint64_t)l * f.n_total + s] = acc;
+  normalized_point(fd.box_lo, fd.box_hi, r.o, r.d, __ldcs(f.s_t + s), p);
+  for (uint32_t l = l0; l < l1; ++l) {
+    Corners c;
+    level_corners(fd.lv[l], p, c);
+    const float2 acc = gather_level(reinterpret_cast<const float2*>(f.params + fd.base + fd.lv[l].offset), c);
+    st_stream(reinterpret_cast<float2*>(X) + (uint64_t)l * f.n_total + s, acc);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
   const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t l = blockIdx.y;
-  if (s >= f.n_total) return;
-  const float2 up = reinterpret_cast<const float2*>(dX)[(uint64_t)l * f.n_total + s];
-  if (up.x == 0.f && up.y == 0.f) return;
-  const uint32_t casc = s >= f.fine_total ? 1u : 0u;
-  const uint32_t item = f.s_item[s];
-  const FieldDesc& fd = f.fields[casc * f.n_local + f.item_part[item]];
-  const RayRec& r = f.rec[item];
-  double p[3];
-  normalized_point(fd.box_lo, fd.box_hi, r.o, r.d, f.s_t[s], p);
-  Corners c;
-  level_corners(fd.lv[l], p, c);
-  scatter_level(reinterpret_cast<float2*>(f.grads + fd.base + fd.lv[l].offset), c, up);
+  const bool valid = s < f.n_total;
+  const uint32_t l0 = blockIdx.y == 0 ? 0u : f.dense_levels + blockIdx.y - 1;
+  const uint32_t l1 = blockIdx.y == 0 ? f.dense_levels : l0 + 1;
+  uint32_t fidx = 0;
+  double p[3] = {0.0, 0.0, 0.0};
+  const FieldDesc* fdp = f.fields;
+  if (valid) {
+    const uint32_t casc = s >= f.fine_total ? 1u : 0u;
+    const uint32_t item = __ldcs(f.s_item + s);
+    fidx = casc * f.n_local + f.item_part[item];
+    fdp = f.fields + fidx;
+    const RayRec& r = f.rec[item];
+    normalized_point(fdp->box_lo, fdp->box_hi, r.o, r.d, __ldcs(f.s_t + s), p);
+  }
+  const FieldDesc& fd = *fdp;
+  for (uint32_t l = l0; l < l1; ++l) {
+    float2 up = make_float2(0.f, 0.f);
+    Corners c;
+    if (valid) {
+      up = ld_stream(reinterpret_cast<const float2*>(dX) + (uint64_t)l * f.n_total + s);
+      level_corners(fd.lv[l], p, c);
+    }
+    float2* table = reinterpret_cast<float2*>(f.grads + fd.base + fd.lv[l].offset);
+    if (l < f.agg_levels) {  // coarse levels: consecutive samples share corners
+      scatter_level_agg(table, c, up, fidx, valid && (up.x != 0.f || up.y != 0.f));
+    } else if (valid && (up.x != 0.f || up.y != 0.f)) {
+      scatter_level(table, c, up);
+    }
+  }
 }
 
 __global__ void k_encode_points(const FieldDesc* __restrict__ field, const float* __restrict__ params,
@@ -136,16 +196,20 @@ __global__ void k_encode_points_bwd(const FieldDesc* __restrict__ field, float* 
 
 inline dim3 grid_lv(uint64_t n, uint32_t L) { return dim3((unsigned)((n + 255) / 256), L); }
 
+inline dim3 grid_groups(const FieldLaunch& f) {
+  return dim3((unsigned)((f.n_total + 255) / 256), 1u + (f.levels - f.dense_levels));
+}
+
 }  // namespace
 
 void launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s) {
   if (!f.n_total) return;
-  k_encode_fwd<<<grid_lv(f.n_total, f.levels), 256, 0, s>>>(f, X);
+  k_encode_fwd<<<grid_groups(f), 256, 0, s>>>(f, X);
 }
 
 void launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s) {
   if (!f.n_total) return;
-  k_encode_bwd<<<grid_lv(f.n_total, f.levels), 256, 0, s>>>(f, dX);
+  k_encode_bwd<<<grid_groups(f), 256, 0, s>>>(f, dX);
 }
 
 void launch_encode_points(const FieldDesc* field, const float* params, const double* pts,

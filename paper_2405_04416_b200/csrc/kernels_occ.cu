@@ -83,7 +83,7 @@ __global__ void k_occ_apply(float* __restrict__ density, const uint32_t* __restr
                             const float* __restrict__ sigma, uint64_t n, float decay) {
   const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
-  const uint32_t c = cells[s];
+  const uint64_t c = cells ? cells[s] : s;
   density[c] = fmaxf(density[c] * decay, sigma[s]);
 }
 

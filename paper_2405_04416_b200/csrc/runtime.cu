@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <random>
 #include <string>
@@ -122,6 +123,12 @@ struct dg_ctx {
   std::vector<double> occ_thr;            // [n_local][2] current thresholds
   std::vector<std::mt19937_64> occ_rng;   // Worker::occ_rng_ per local partition (worker.cpp:186)
   uint64_t occ_updates = 0;
+  // warm-up updates draw 3 uniforms per cell in a fixed order, independent of the state, so
+  // the next update's jitter points are generated on a host thread while the GPU trains
+  double* occ_host = nullptr;             // pinned, all (partition, cascade) warm-up points
+  uint64_t occ_host_n = 0;                // doubles
+  std::future<void> occ_prefetch;
+  bool occ_prefetched = false;
   double step = 0.0;
   uint64_t adam_t = 0;
   uint64_t worker_step = 0;
@@ -316,6 +323,8 @@ int upload(DBuf& b, const void* src, size_t bytes, cudaStream_t s) {
   return DG_OK;
 }
 
+void occ_start_prefetch(dg_ctx* c);
+
 int ctx_alloc(dg_ctx* c) {
   cudaStream_t s = c->stream;
   TRY(upload(c->d_geo, &c->geo, sizeof(Geo), s));
@@ -342,6 +351,21 @@ int ctx_alloc(dg_ctx* c) {
     CU(cudaStreamSynchronize(s));
   }
   for (uint32_t gid : c->local) c->occ_rng.emplace_back(splitmix64(counter_hash(c->cfg.seed, 0x0cc0, gid, 0)));
+  if (c->cfg.occupancy_updates) {  // buffers for the largest (warm-up) update, allocated once
+    uint64_t max_cells = 0, all_cells = 0;
+    for (const PartDesc& pd : c->parts)
+      for (int casc = 0; casc < 2; ++casc) {
+        const uint64_t n = uint64_t(pd.occ_n[casc][0]) * pd.occ_n[casc][1] * pd.occ_n[casc][2];
+        max_cells = std::max(max_cells, n);
+        all_cells += n;
+      }
+    TRY(c->occ_pts.ensure(max_cells * 3 * sizeof(double) + 16));
+    TRY(c->occ_sigma.ensure(max_cells * sizeof(float) + 16));
+    c->occ_host_n = all_cells * 3;
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&c->occ_host), c->occ_host_n * sizeof(double) + 16,
+                     cudaHostAllocDefault));
+    occ_start_prefetch(c);
+  }
   // default appearance: one zero row for image 0
   c->app_rows = 1;
   c->n_images = 1;
@@ -665,6 +689,26 @@ FieldLaunch field_launch(dg_ctx* c) {
   f.n_total = c->n_fine + c->n_coarse;
   f.n_local = uint32_t(c->local.size());
   f.levels = c->cfg.grid_levels;
+  // level groups: leading one-to-one levels of the first local fine grid go together (their
+  // tables fit in L2 jointly); aggregation where ~2+ consecutive samples share a cell
+  const FieldDesc& f0 = c->fields[0];
+  uint32_t dense = 0, agg = 0;
+  uint64_t dense_bytes = 0;
+  for (uint32_t l = 0; l < f0.L; ++l) {
+    const uint64_t rows = f0.lv[l].hashed ? uint64_t(f0.lv[l].mask) + 1
+                                          : uint64_t(f0.lv[l].n[0]) * f0.lv[l].n[1] * f0.lv[l].n[2];
+    if (f0.lv[l].hashed || dense_bytes + rows * 8 > (96ull << 20)) break;
+    dense_bytes += rows * 8;
+    ++dense;
+  }
+  // ~1.5+ samples per cell along a ray: cell = extent / n vs. the march step
+  const double ext = std::max(f0.box_hi[0] - f0.box_lo[0],
+                              std::max(f0.box_hi[1] - f0.box_lo[1], f0.box_hi[2] - f0.box_lo[2]));
+  const double maxn_agg = ext / (1.5 * c->step);
+  for (uint32_t l = 0; l < f0.L; ++l)
+    if (double(std::max(f0.lv[l].n[0], std::max(f0.lv[l].n[1], f0.lv[l].n[2]))) <= maxn_agg) agg = l + 1;
+  f.dense_levels = std::max<uint32_t>(dense, 1);
+  f.agg_levels = agg;
   f.params = c->params.as<float>();
   f.grads = c->grads.as<float>();
   return f;
@@ -763,6 +807,53 @@ int d2h(std::vector<T>& v, const void* src, uint64_t n, cudaStream_t s) {
 }
 
 
+// The jitter point of one sampled cell (grid.cpp:206-214): cell_box + 3 Rng::uniform draws.
+inline void occ_point(std::mt19937_64& rng, const double lo[3], const double cell[3],
+                      const uint32_t sh[3], uint64_t idx, double* out) {
+  const uint64_t ii[3] = {idx % sh[0], (idx / sh[0]) % sh[1], idx / (uint64_t(sh[0]) * sh[1])};
+  for (int a = 0; a < 3; ++a) {
+    const double clo = lo[a] + cell[a] * double(ii[a]);
+    const double chi = clo + cell[a];
+    out[a] = clo + (chi - clo) * (double(rng() >> 11) * 0x1.0p-53);
+  }
+}
+
+inline void occ_geometry(const PartDesc& pd, int casc, const double*& lo, double cell[3], uint64_t& total) {
+  const uint32_t* sh = pd.occ_n[casc];
+  total = uint64_t(sh[0]) * sh[1] * sh[2];
+  lo = casc == 0 ? pd.fine_lo : pd.coarse_lo;
+  const double* hi = casc == 0 ? pd.fine_hi : pd.coarse_hi;
+  for (int a = 0; a < 3; ++a) cell[a] = (hi[a] - lo[a]) / double(sh[a]);
+}
+
+// Fill the pinned buffer with one warm-up update's points for every local partition, in the
+// reference's order (per partition: fine grid cells 0..n-1, then coarse; 3 draws per cell).
+void occ_generate_warm(dg_ctx* c) {
+  uint64_t k = 0;
+  for (uint32_t lp = 0; lp < c->local.size(); ++lp)
+    for (int casc = 0; casc < 2; ++casc) {
+      const double* lo;
+      double cell[3];
+      uint64_t total;
+      occ_geometry(c->parts[lp], casc, lo, cell, total);
+      for (uint64_t i = 0; i < total; ++i, k += 3)
+        occ_point(c->occ_rng[lp], lo, cell, c->parts[lp].occ_n[casc], i, c->occ_host + k);
+    }
+}
+
+bool next_update_is_warm(const dg_ctx* c, uint64_t after_step) {
+  const uint64_t iv = c->cfg.occ_update_interval;
+  if (!c->cfg.occupancy_updates || iv == 0) return false;
+  const uint64_t next = (after_step / iv + 1) * iv;
+  return next <= c->cfg.occ_warmup_steps;
+}
+
+void occ_start_prefetch(dg_ctx* c) {
+  if (!c->occ_host || !next_update_is_warm(c, c->worker_step)) return;
+  c->occ_prefetch = std::async(std::launch::async, [c] { occ_generate_warm(c); });
+  c->occ_prefetched = true;
+}
+
 // Worker::update_occupancy (worker.cpp:549-562) + OccupancyGrid::decay_and_update
 // (grid.cpp:201-229).  The jitter points are the reference's mt19937_64 draws in its order
 // (fine grid, then coarse grid, same stream); sigma is evaluated on the device.
@@ -778,6 +869,12 @@ int occupancy_update(dg_ctx* c) {
       cfg.occ_threshold_scale;
   const bool warm_up = step <= cfg.occ_warmup_steps;
   const uint32_t nl = uint32_t(c->local.size());
+  if (warm_up) {
+    if (!c->occ_prefetched) occ_start_prefetch(c), c->occ_prefetched = true;
+    if (c->occ_prefetch.valid()) c->occ_prefetch.wait();
+    c->occ_prefetched = false;
+  }
+  uint64_t k = 0;  // offset into the prefetched warm-up points
   for (uint32_t lp = 0; lp < nl; ++lp) {
     const PartDesc& pd = c->parts[lp];
     for (int casc = 0; casc < 2; ++casc) {  // set_threshold: recompute the bitfield
@@ -787,32 +884,22 @@ int occupancy_update(dg_ctx* c) {
                       n, float(threshold), s);
       ++c->launches;
     }
-    std::mt19937_64& rng = c->occ_rng[lp];
-    auto uni = [&](double lo, double hi) { return lo + (hi - lo) * (double(rng() >> 11) * 0x1.0p-53); };
     for (int casc = 0; casc < 2; ++casc) {
-      const uint32_t* sh = pd.occ_n[casc];
-      const uint64_t total = uint64_t(sh[0]) * sh[1] * sh[2];
-      const double* lo = casc == 0 ? pd.fine_lo : pd.coarse_lo;
-      const double* hi = casc == 0 ? pd.fine_hi : pd.coarse_hi;
+      const double* lo;
       double cell[3];
-      for (int a = 0; a < 3; ++a) cell[a] = (hi[a] - lo[a]) / double(sh[a]);
-      std::vector<uint32_t> cells;
-      std::vector<double> pts;
-      auto sample = [&](uint64_t idx) {  // sample_cell (grid.cpp:206-214)
-        const uint64_t ii[3] = {idx % sh[0], (idx / sh[0]) % sh[1], idx / (uint64_t(sh[0]) * sh[1])};
-        double clo[3], chi[3];
-        for (int a = 0; a < 3; ++a) {
-          clo[a] = lo[a] + cell[a] * double(ii[a]);
-          chi[a] = clo[a] + cell[a];
-        }
-        cells.push_back(uint32_t(idx));
-        for (int a = 0; a < 3; ++a) pts.push_back(uni(clo[a], chi[a]));
-      };
-      if (warm_up) {
-        cells.reserve(total);
-        pts.reserve(3 * total);
-        for (uint64_t i = 0; i < total; ++i) sample(i);
+      uint64_t total;
+      occ_geometry(pd, casc, lo, cell, total);
+      const FieldDesc* fd = c->d_fields.as<FieldDesc>() + casc * nl + lp;
+      float* den = c->occ_den.as<float>() + pd.occ_off[casc];
+      if (warm_up) {  // every cell once, in order: cell index == point index
+        CU(cudaMemcpyAsync(c->occ_pts.p, c->occ_host + k, total * 3 * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+        k += 3 * total;
+        launch_occ_query(fd, c->params.as<float>(), c->occ_pts.as<double>(), total, c->occ_sigma.as<float>(), s);
+        launch_occ_apply(den, nullptr, c->occ_sigma.as<float>(), total, float(cfg.occ_decay), s);
+        c->h2d += total * 3 * sizeof(double);
       } else {
+        std::mt19937_64& rng = c->occ_rng[lp];
         std::vector<uint8_t> bits(total);
         CU(cudaMemcpyAsync(bits.data(), c->occ.as<uint8_t>() + pd.occ_off[casc], total,
                            cudaMemcpyDeviceToHost, s));
@@ -821,34 +908,38 @@ int occupancy_update(dg_ctx* c) {
         for (uint64_t i = 0; i < total; ++i)
           if (bits[i]) occupied.push_back(i);
         const uint64_t n_uniform = std::max<uint64_t>(total / 4, 1);
+        std::vector<uint32_t> cells;
+        std::vector<double> pts;
+        auto sample = [&](uint64_t idx) {
+          cells.push_back(uint32_t(idx));
+          pts.resize(pts.size() + 3);
+          occ_point(rng, lo, cell, pd.occ_n[casc], idx, pts.data() + pts.size() - 3);
+        };
         for (uint64_t i = 0; i < n_uniform; ++i) sample(rng() % total);
         if (!occupied.empty())
           for (uint64_t i = 0; i < n_uniform; ++i) sample(occupied[rng() % occupied.size()]);
-      }
-      const uint64_t n = cells.size();
-      TRY(upload(c->occ_pts, pts.data(), pts.size() * sizeof(double), s));
-      TRY(upload(c->occ_cells, cells.data(), n * sizeof(uint32_t), s));
-      TRY(c->occ_sigma.ensure(n * sizeof(float) + 16));
-      const FieldDesc* fd = c->d_fields.as<FieldDesc>() + casc * nl + lp;
-      launch_occ_query(fd, c->params.as<float>(), c->occ_pts.as<double>(), n, c->occ_sigma.as<float>(), s);
-      float* den = c->occ_den.as<float>() + pd.occ_off[casc];
-      if (warm_up) {
-        launch_occ_apply(den, c->occ_cells.as<uint32_t>(), c->occ_sigma.as<float>(), n,
-                         float(cfg.occ_decay), s);
-      } else {  // cells may repeat: apply sequentially in draw order on the host
+        const uint64_t n = cells.size();
+        CU(cudaMemcpyAsync(c->occ_pts.p, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        launch_occ_query(fd, c->params.as<float>(), c->occ_pts.as<double>(), n, c->occ_sigma.as<float>(), s);
+        // cells may repeat: apply sequentially in draw order on the host
         std::vector<float> sig(n), hd(total);
         CU(cudaMemcpyAsync(sig.data(), c->occ_sigma.p, n * sizeof(float), cudaMemcpyDeviceToHost, s));
         CU(cudaMemcpyAsync(hd.data(), den, total * sizeof(float), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
-        for (uint64_t k = 0; k < n; ++k) hd[cells[k]] = std::max(hd[cells[k]] * float(cfg.occ_decay), sig[k]);
+        for (uint64_t q = 0; q < n; ++q) hd[cells[q]] = std::max(hd[cells[q]] * float(cfg.occ_decay), sig[q]);
         CU(cudaMemcpyAsync(den, hd.data(), total * sizeof(float), cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));
+        c->h2d += pts.size() * sizeof(double) + total * sizeof(float);
       }
       launch_occ_bits(den, c->occ.as<uint8_t>() + pd.occ_off[casc], total, float(threshold), s);
       c->launches += 3;
-      c->h2d += pts.size() * sizeof(double) + n * sizeof(uint32_t);
     }
   }
   ++c->occ_updates;
+  if (warm_up) {
+    CU(cudaStreamSynchronize(s));  // the pinned buffer is reused by the next prefetch
+    occ_start_prefetch(c);
+  }
   return DG_OK;
 }
 
@@ -938,6 +1029,8 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
 int dg_ctx_destroy(dg_ctx* c) {
   if (!c) return DG_OK;
   cudaSetDevice(c->device);
+  if (c->occ_prefetch.valid()) c->occ_prefetch.wait();
+  if (c->occ_host) cudaFreeHost(c->occ_host);
   cudaStreamSynchronize(c->stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -1056,6 +1149,7 @@ int dg_get_adam(dg_ctx* c, uint32_t p, float* m, float* v, uint64_t* t) {
 int dg_set_step(dg_ctx* c, uint64_t step) {
   TRY(check_ctx(c));
   c->worker_step = step;
+  if (!c->occ_prefetched) occ_start_prefetch(c);
   return DG_OK;
 }
 
