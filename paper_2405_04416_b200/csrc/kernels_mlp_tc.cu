@@ -25,7 +25,9 @@ namespace dg {
 namespace {
 
 constexpr int TM = 128;   // samples per tile (MMA M)
-constexpr int NTH = 256;  // 8 warps: warp w reads TMEM lane quadrant w % 4, column half w / 4
+constexpr int NTF = 256;  // forward: 8 warps, 2 CTAs/SM (their MMAs and epilogues interleave)
+constexpr int NTB = 512;  // backward: 16 warps, 1 CTA/SM (212 KB of operand tiles)
+// Warp w reads TMEM lane quadrant w % 4 (tcgen05.ld rule) and owns column part w / 4.
 
 // Weight operand tiles (B, K-major): rows = out (padded), cols = in (padded).
 struct TcWeights {
@@ -37,28 +39,51 @@ struct TcWeights {
   float bd0[64], bd1[16], bc0[64], bc1[64], bc2[16];
 };
 
-struct FwdTcSmem {
-  TcWeights w;
-  uint8_t a[2][TM * 64 * 2];  // activation operand (A, K-major), hi / lo
-  float sig_raw[TM];
-  uint64_t mbar;
-  uint32_t tslot;
-};
+// Two fp32 -> packed bf16x2 hi and lo (x = hi + lo + O(2^-17 |x|)); same values as
+// tc::split_bf16, two lanes per cvt.
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 
-__device__ __forceinline__ void put_split(uint8_t* hi, uint8_t* lo, uint32_t off, float v) {
-  uint16_t h, l;
-  tc::split_bf16(v, h, l);
-  *reinterpret_cast<uint16_t*>(hi + off) = h;
-  *reinterpret_cast<uint16_t*>(lo + off) = l;
+// Write 8 consecutive columns [c0, c0+8) of row r into a split tile with TM rows.
+__device__ __forceinline__ void put8(uint8_t* hi, uint8_t* lo, int r, int c0, const float* v) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) split2(v[2 * j], v[2 * j + 1], h[j], l[j]);
+  const uint32_t off = tc::core_offset(r, c0, TM);
+  *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// Read back 8 consecutive columns of row r (hi + lo).
+__device__ __forceinline__ void get8(const uint8_t* hi, const uint8_t* lo, int r, int c0, float* v) {
+  const uint32_t off = tc::core_offset(r, c0, TM);
+  const uint4 h = *reinterpret_cast<const uint4*>(hi + off);
+  const uint4 l = *reinterpret_cast<const uint4*>(lo + off);
+  const uint32_t hh[4] = {h.x, h.y, h.z, h.w}, ll[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[2 * j] = __uint_as_float(hh[j] << 16) + __uint_as_float(ll[j] << 16);
+    v[2 * j + 1] = __uint_as_float(hh[j] & 0xffff0000u) + __uint_as_float(ll[j] & 0xffff0000u);
+  }
 }
 
 // Stage one layer's W[out][in] (fp32, global) as split-bf16 K-major tiles [Np x Kp].
 __device__ void stage_layer(const float* __restrict__ W, int out, int in, int Np, int Kp,
                             uint8_t* hi, uint8_t* lo) {
-  for (int e = threadIdx.x; e < Np * Kp; e += NTH) {
-    const int o = e / Kp, i = e % Kp;
-    const float v = (o < out && i < in) ? W[o * in + i] : 0.f;
-    put_split(hi, lo, tc::core_offset(o, i, Np), v);
+  for (int e = threadIdx.x; e < Np * Kp / 2; e += blockDim.x) {
+    const int o = (2 * e) / Kp, i = (2 * e) % Kp;
+    const float a = (o < out && i < in) ? W[o * in + i] : 0.f;
+    const float b = (o < out && i + 1 < in) ? W[o * in + i + 1] : 0.f;
+    uint32_t h, l;
+    split2(a, b, h, l);
+    const uint32_t off = tc::core_offset(o, i, Np);
+    *reinterpret_cast<uint32_t*>(hi + off) = h;
+    *reinterpret_cast<uint32_t*>(lo + off) = l;
   }
 }
 
@@ -70,38 +95,19 @@ __device__ void stage_weights_tc(const FieldDesc& fd, const float* __restrict__ 
   stage_layer(base + fd.cw0, 64, cin, 64, 48, w.c0[0], w.c0[1]);
   stage_layer(base + fd.cw1, 64, 64, 64, 64, w.c1[0], w.c1[1]);
   stage_layer(base + fd.cw2, 3, 64, 16, 64, w.c2[0], w.c2[1]);
-  for (int e = threadIdx.x; e < 64; e += NTH) {
+  for (int e = threadIdx.x; e < 64; e += blockDim.x) {
     w.bd0[e] = base[fd.db0 + e];
     w.bc0[e] = base[fd.cb0 + e];
     w.bc1[e] = base[fd.cb1 + e];
   }
-  for (int e = threadIdx.x; e < 16; e += NTH) {
+  for (int e = threadIdx.x; e < 16; e += blockDim.x) {
     w.bd1[e] = base[fd.db1 + e];
     w.bc2[e] = e < 3 ? base[fd.cb2 + e] : 0.f;
   }
 }
 
-// D[tm][N] (+)= A[tm x K] . B[N x K]^T, split-bf16 (3 MMAs per 16-wide K step).
+// D[TM x N] = A[TM x K] . B[N x K]^T, split-bf16 (3 MMAs per 16-wide K step).
 // A tile rows = TM (K-major, SBO 128, LBO TM/8*128); B tile rows = N (SBO 128, LBO N/8*128).
-__device__ __forceinline__ void gemm_kmajor(uint32_t d_tmem, const uint8_t (*a)[TM * 64 * 2],
-                                            const uint8_t* b_hi, const uint8_t* b_lo, int N, int K,
-                                            bool accumulate) {
-  const uint32_t id = tc::idesc_bf16(TM, N, 0, 0);
-  const uint32_t a0 = tc::smem_u32(a[0]), a1 = tc::smem_u32(a[1]);
-  const uint32_t b0 = tc::smem_u32(b_hi), b1 = tc::smem_u32(b_lo);
-  const uint32_t a_lbo = (TM / 8) * 128, b_lbo = (N / 8) * 128;
-  for (int k = 0; k < K / 16; ++k) {
-    const uint32_t ao = k * 2 * a_lbo, bo = k * 2 * b_lbo;
-    const uint64_t ah = tc::smem_desc(a0 + ao, a_lbo, 128), al = tc::smem_desc(a1 + ao, a_lbo, 128);
-    const uint64_t bh = tc::smem_desc(b0 + bo, b_lbo, 128), bl = tc::smem_desc(b1 + bo, b_lbo, 128);
-    tc::mma_bf16(d_tmem, ah, bh, id, (accumulate || k > 0) ? 1u : 0u);
-    tc::mma_bf16(d_tmem, ah, bl, id, 1u);
-    tc::mma_bf16(d_tmem, al, bh, id, 1u);
-  }
-}
-
-
-// D[TM x N] = A[TM x K] . B[N x K]^T for an A tile given as hi/lo base pointers.
 __device__ __forceinline__ void gemm_kmajor_t(uint32_t d_tmem, const uint8_t* a_hi, const uint8_t* a_lo,
                                               const uint8_t* b_hi, const uint8_t* b_lo, int N, int K) {
   const uint32_t id = tc::idesc_bf16(TM, N, 0, 0);
@@ -118,50 +124,140 @@ __device__ __forceinline__ void gemm_kmajor_t(uint32_t d_tmem, const uint8_t* a_
   }
 }
 
-// Write 8 consecutive columns [c0, c0+8) of row r of the activation operand.
-__device__ __forceinline__ void put_chunk(uint8_t (*a)[TM * 64 * 2], int r, int c0, const float* v) {
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint16_t h0, l0, h1, l1;
-    tc::split_bf16(v[2 * j], h0, l0);
-    tc::split_bf16(v[2 * j + 1], h1, l1);
-    h[j] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-    l[j] = (uint32_t)l0 | ((uint32_t)l1 << 16);
-  }
-  const uint32_t off = tc::core_offset(r, c0, TM);
-  *reinterpret_cast<uint4*>(a[0] + off) = make_uint4(h[0], h[1], h[2], h[3]);
-  *reinterpret_cast<uint4*>(a[1] + off) = make_uint4(l[0], l[1], l[2], l[3]);
-}
-
-__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+// sigmoid with the SFU exp and reciprocal (relative error ~1e-7 for |x| <= 15-ish inputs).
+__device__ __forceinline__ float sigm(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
 __device__ __forceinline__ float clip15(float v) { return v > 15.f ? 15.f : (v < -15.f ? -15.f : v); }
 
-__device__ __forceinline__ void sh16(float x, float y, float z, float* o) {  // sh.hpp:14-35
+// SH16 components 1..15 (sh.hpp:14-35); component 0 is the constant 0.28209479177387814.
+__device__ __forceinline__ void sh15(float x, float y, float z, float* o) {
   const float xy = x * y, xz = x * z, yz = y * z, x2 = x * x, y2 = y * y, z2 = z * z;
-  o[0] = 0.28209479177387814f;
-  o[1] = -0.48860251190291987f * y;
-  o[2] = 0.48860251190291987f * z;
-  o[3] = -0.48860251190291987f * x;
-  o[4] = 1.0925484305920792f * xy;
-  o[5] = -1.0925484305920792f * yz;
-  o[6] = 0.31539156525252005f * (3.0f * z2 - 1.0f);
-  o[7] = -1.0925484305920792f * xz;
-  o[8] = 0.5462742152960396f * (x2 - y2);
-  o[9] = -0.5900435899266435f * y * (3.0f * x2 - y2);
-  o[10] = 2.890611442640554f * xy * z;
-  o[11] = -0.4570457994644658f * y * (5.0f * z2 - 1.0f);
-  o[12] = 0.3731763325901154f * z * (5.0f * z2 - 3.0f);
-  o[13] = -0.4570457994644658f * x * (5.0f * z2 - 1.0f);
-  o[14] = 1.445305721320277f * z * (x2 - y2);
-  o[15] = -0.5900435899266435f * x * (x2 - 3.0f * y2);
+  o[0] = -0.48860251190291987f * y;
+  o[1] = 0.48860251190291987f * z;
+  o[2] = -0.48860251190291987f * x;
+  o[3] = 1.0925484305920792f * xy;
+  o[4] = -1.0925484305920792f * yz;
+  o[5] = 0.31539156525252005f * (3.0f * z2 - 1.0f);
+  o[6] = -1.0925484305920792f * xz;
+  o[7] = 0.5462742152960396f * (x2 - y2);
+  o[8] = -0.5900435899266435f * y * (3.0f * x2 - y2);
+  o[9] = 2.890611442640554f * xy * z;
+  o[10] = -0.4570457994644658f * y * (5.0f * z2 - 1.0f);
+  o[11] = 0.3731763325901154f * z * (5.0f * z2 - 3.0f);
+  o[12] = -0.4570457994644658f * x * (5.0f * z2 - 1.0f);
+  o[13] = 1.445305721320277f * z * (x2 - y2);
+  o[14] = -0.5900435899266435f * x * (x2 - 3.0f * y2);
 }
+constexpr float kSH0 = 0.28209479177387814f;
 
-__device__ __forceinline__ int tile_field(const MlpLaunch& m, uint32_t tile) {
+struct TileGeo {
+  int f;
+  uint64_t s0;
+  int count;
+};
+__device__ __forceinline__ TileGeo tile_geo(const MlpLaunch& m, uint32_t tile) {
   int f = 0;
   while (f + 1 < (int)m.n_fields && tile >= m.tile_off[f + 1]) ++f;
-  return f;
+  TileGeo g;
+  g.f = f;
+  g.s0 = m.field_off[f] + (uint64_t)(tile - m.tile_off[f]) * TM;
+  const uint64_t rem = m.field_off[f + 1] - g.s0;
+  g.count = rem < (uint64_t)TM ? (int)rem : TM;
+  return g;
 }
+
+// Per-thread register prefetch of one tile's global inputs, issued during the previous tile
+// so the tile's epilogues never wait on HBM/L2:  X (this part's levels), the upstream
+// gradient (part 0), and the dependent chain  item -> RayRec (dir, image) -> appearance row.
+// Column parts of the Cin tile: part 0 = clip(raw1..15) + SH0, part SHP = SH1..15 + app0,
+// part APP = app1..16.
+template <int NP>
+struct Pref {
+  static constexpr int XL = 16 / NP;  // levels per part
+  static constexpr int SHP = 1, APP = NP == 4 ? 2 : 1;
+  float x[2 * XL];
+  float4 g;
+  uint32_t item;
+  uint32_t img;
+  double dir[3];
+  float app[17];
+  uint64_t gs;
+  bool valid;
+
+  __device__ __forceinline__ void start(const MlpLaunch& m, bool v, uint64_t gsample, int part,
+                                        bool want_g) {
+    valid = v;
+    gs = gsample;
+#pragma unroll
+    for (int j = 0; j < XL; ++j) {
+      const int l = part * XL + j;
+      float2 xx = make_float2(0.f, 0.f);
+      if (v && l < (int)m.levels)
+        xx = __ldcs(reinterpret_cast<const float2*>(m.X) + (uint64_t)l * m.x_stride + gs);
+      x[2 * j] = xx.x;
+      x[2 * j + 1] = xx.y;
+    }
+    if (part == SHP || part == APP) item = v ? __ldg(m.s_item + gs) : 0u;
+    if (want_g && part == 0) g = v ? __ldcs(m.grad_in + gs) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ __forceinline__ void grad(const MlpLaunch& m, int part) {
+    if (part == 0) g = valid ? __ldcs(m.grad_in + gs) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ __forceinline__ void rec(const MlpLaunch& m, int part) {
+    if ((part == SHP || part == APP) && valid) {
+      const RayRec& r = m.rec[item];
+      if (part == SHP) {
+        dir[0] = r.d[0];
+        dir[1] = r.d[1];
+        dir[2] = r.d[2];
+      }
+      img = r.img;
+    }
+  }
+  __device__ __forceinline__ void appearance(const MlpLaunch& m, const FieldDesc& fd, int part) {
+    if (part != SHP && part != APP) return;
+    const int dim = (int)fd.app_dim;
+    const float* src = nullptr;
+    if (valid)
+      src = m.app_per_sample ? m.app_override + gs * fd.app_dim
+                             : (m.app_override ? m.app_override : m.app_table + (uint64_t)img * fd.app_dim);
+#pragma unroll
+    for (int i = 0; i < 17; ++i) {
+      const bool mine = (part == SHP && i == 0) || (part == APP && i >= 1);
+      app[i] = (mine && src && i < dim) ? __ldg(src + i) : 0.f;
+    }
+  }
+  // Write this part's columns of Cin (raw16 = clipped density output, part 0 only).
+  __device__ __forceinline__ void put_cin(uint8_t* hi, uint8_t* lo, int row, int part, const float* raw) {
+    if (part == 0) {
+      float c[16];
+#pragma unroll
+      for (int i = 0; i < 15; ++i) c[i] = raw[1 + i];
+      c[15] = valid ? kSH0 : 0.f;
+      put8(hi, lo, row, 0, c);
+      put8(hi, lo, row, 8, c + 8);
+    }
+    if (part == SHP) {
+      float c[16];
+      if (valid) {
+        sh15((float)dir[0], (float)dir[1], (float)dir[2], c);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 15; ++i) c[i] = 0.f;
+      }
+      c[15] = app[0];
+      put8(hi, lo, row, 16, c);
+      put8(hi, lo, row, 24, c + 8);
+    }
+    if (part == APP) {
+      put8(hi, lo, row, 32, app + 1);
+      put8(hi, lo, row, 40, app + 9);
+    }
+  }
+  __device__ __forceinline__ void put_x(uint8_t* hi, uint8_t* lo, int row, int part) {
+#pragma unroll
+    for (int c = 0; c < XL / 4; ++c) put8(hi, lo, row, part * 2 * XL + 8 * c, x + 8 * c);
+  }
+};
 
 // Sync point between an epilogue (generic smem writes / TMEM reads) and the next MMA issue.
 __device__ __forceinline__ void to_mma() {
@@ -171,24 +267,28 @@ __device__ __forceinline__ void to_mma() {
   tc::fence_after();
 }
 
-// Load 32 consecutive TMEM columns [c0, c0+32) of this thread's lane into v.
-__device__ __forceinline__ void ld32(uint32_t taddr, float* v) {
-  float a[16], b[16];
-  tc::tmem_ld16(taddr, a);
-  tc::tmem_ld16(taddr + 16, b);
+// Load 16 consecutive TMEM columns of this thread's lane.
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+  tc::tmem_ld16(taddr, v);
   tc::tmem_wait_ld();
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    v[i] = a[i];
-    v[16 + i] = b[i];
-  }
 }
 
-__global__ void __launch_bounds__(NTH, 2) k_mlp_fwd_tc(MlpLaunch m) {
+struct FwdTcSmem {
+  TcWeights w;
+  uint8_t a[2][TM * 64 * 2];  // activation operand (A, K-major), hi / lo
+  float sig_raw[TM];
+  uint64_t mbar;
+  uint32_t tslot;
+};
+
+// Forward: 2 column parts (warps 0-3 / 4-7) x 4 lane quadrants; each thread owns one sample row
+// and 32 of the 64 hidden columns.  Tiles are strided over the grid.
+__global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
+  constexpr int NP = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   FwdTcSmem& sm = *reinterpret_cast<FwdTcSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quad = warp & 3, half = warp >> 2;
+  const int quad = warp & 3, part = warp >> 2;
   const int row = quad * 32 + lane;  // TMEM lane == sample row of the tile
   if (warp == 0) tc::tmem_alloc(&sm.tslot, 64);
   if (tid == 0) {
@@ -201,138 +301,127 @@ __global__ void __launch_bounds__(NTH, 2) k_mlp_fwd_tc(MlpLaunch m) {
   const uint32_t tmem = sm.tslot;
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
   uint32_t phase = 0;
-  int loaded = -1;
   auto mma_done = [&]() {
     if (tid == 0) tc::commit(&sm.mbar);
     tc::mbar_wait(&sm.mbar, phase);
     phase ^= 1u;
     tc::fence_after();
   };
-  for (uint32_t tile = blockIdx.x; tile < m.n_tiles; tile += gridDim.x) {
-    const int f = tile_field(m, tile);
-    const FieldDesc& fd = m.fields[f];
-    const uint64_t s0 = m.field_off[f] + (uint64_t)(tile - m.tile_off[f]) * TM;
-    const uint64_t rem = m.field_off[f + 1] - s0;
-    const int count = rem < (uint64_t)TM ? (int)rem : TM;
-    if (f != loaded) {
-      __syncthreads();
-      stage_weights_tc(fd, m.params, sm.w);
-      loaded = f;
-    }
-    const int act_c = fd.coarse ? 2 : 1;
-    const bool valid = row < count;
-    const uint64_t gs = s0 + row;
-    // ---- X tile: thread (row, half) writes levels [8 half, 8 half + 8) = 2 chunks ----
-    {
-      float v[16];
+  uint32_t tile = blockIdx.x;
+  if (tile < m.n_tiles) {
+    TileGeo cur = tile_geo(m, tile);
+    Pref<NP> pf;
+    pf.start(m, row < cur.count, cur.s0 + row, part, false);
+    pf.rec(m, part);
+    pf.appearance(m, m.fields[cur.f], part);
+    stage_weights_tc(m.fields[cur.f], m.params, sm.w);
+    int loaded = cur.f;
+    pf.put_x(sm.a[0], sm.a[1], row, part);
+    for (;;) {
+      const FieldDesc& fd = m.fields[cur.f];
+      const int act_c = fd.coarse ? 2 : 1;
+      const bool valid = row < cur.count;
+      const uint64_t gs = cur.s0 + row;
+      const uint32_t next = tile + gridDim.x;
+      const bool has_next = next < m.n_tiles;
+      const TileGeo nx = has_next ? tile_geo(m, next) : cur;
+      to_mma();
+      // ---- L1: H1 = relu(X Wd0^T + b) ----
+      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.d0[0], sm.w.d0[1], 64, 32);
+      float cin_app[17];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int l = half * 8 + j;
-        float2 x = make_float2(0.f, 0.f);
-        if (valid && l < (int)m.levels)
-          x = reinterpret_cast<const float2*>(m.X)[(uint64_t)l * m.x_stride + gs];
-        v[2 * j] = x.x;
-        v[2 * j + 1] = x.y;
+      for (int i = 0; i < 17; ++i) cin_app[i] = pf.app[i];
+      const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
+      pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next tile: X, item
+      mma_done();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        float v[16];
+        ld16(my_lanes + part * 32 + 16 * q, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[part * 32 + 16 * q + i], 0.f);
+        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q, v);
+        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q + 8, v + 8);
       }
-      put_chunk(sm.a, row, half * 16, v);
-      put_chunk(sm.a, row, half * 16 + 8, v + 8);
-    }
-    to_mma();
-    // ---- L1: H1 = relu(X Wd0^T + b) ----
-    if (tid == 0) gemm_kmajor(tmem, sm.a, sm.w.d0[0], sm.w.d0[1], 64, 32, false);
-    mma_done();
-    {
-      float v[32];
-      ld32(my_lanes + half * 32, v);
+      to_mma();
+      // ---- L2: raw16 = H1 Wd1^T + b ; Cin = [clip(raw1..15) | SH16 | app | 0] ----
+      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.d1[0], sm.w.d1[1], 16, 64);
+      mma_done();
+      {
+        float raw[16];
+        if (part == 0) {
+          ld16(my_lanes, raw);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[half * 32 + i], 0.f);
+          for (int i = 0; i < 16; ++i) raw[i] = clip15(raw[i] + sm.w.bd1[i]);
+          sm.sig_raw[row] = raw[0];
+        }
+        // this tile's dir / app were prefetched into the (now next-tile) registers: restore
+        Pref<NP> cp;
+        cp.valid = valid;
+        cp.dir[0] = d0;
+        cp.dir[1] = d1;
+        cp.dir[2] = d2;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) put_chunk(sm.a, row, half * 32 + 8 * c, v + 8 * c);
-    }
-    to_mma();
-    // ---- L2: raw16 = H1 Wd1^T + b ; Cin = [clip(raw1..15) | SH16 | app | 0] ----
-    if (tid == 0) gemm_kmajor(tmem, sm.a, sm.w.d1[0], sm.w.d1[1], 16, 64, false);
-    mma_done();
-    {
-      float raw[16];
-      tc::tmem_ld16(my_lanes, raw);
-      tc::tmem_wait_ld();
-      float cin[48];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) raw[i] = clip15(raw[i] + sm.w.bd1[i]);
-#pragma unroll
-      for (int i = 0; i < 15; ++i) cin[i] = raw[1 + i];
-      float sh[16];
-      const float* app = nullptr;
-      if (valid) {
-        const RayRec& r = m.rec[m.s_item[gs]];
-        sh16((float)r.d[0], (float)r.d[1], (float)r.d[2], sh);
-        app = m.app_per_sample ? m.app_override + gs * fd.app_dim
-                               : (m.app_override ? m.app_override : m.app_table + (uint64_t)r.img * fd.app_dim);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) sh[i] = 0.f;
+        for (int i = 0; i < 17; ++i) cp.app[i] = cin_app[i];
+        cp.put_cin(sm.a[0], sm.a[1], row, part, raw);
       }
+      pf.rec(m, part);  // next tile's RayRec (item arrived during L1/L2)
+      to_mma();
+      // ---- L3: C1 = act(Cin Wc0^T + b) ----
+      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.c0[0], sm.w.c0[1], 64, 48);
+      mma_done();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) cin[15 + i] = sh[i];
-      for (int i = 0; i < 17; ++i) cin[31 + i] = (app && i < (int)fd.app_dim) ? app[i] : 0.f;
-      if (half == 0) {
-        sm.sig_raw[row] = raw[0];
-        put_chunk(sm.a, row, 0, cin);
-        put_chunk(sm.a, row, 8, cin + 8);
-        put_chunk(sm.a, row, 16, cin + 16);
-      } else {
-        put_chunk(sm.a, row, 24, cin + 24);
-        put_chunk(sm.a, row, 32, cin + 32);
-        put_chunk(sm.a, row, 40, cin + 40);
+      for (int q = 0; q < 2; ++q) {
+        float v[16];
+        ld16(my_lanes + part * 32 + 16 * q, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float z = v[i] + sm.w.bc0[part * 32 + 16 * q + i];
+          v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
+        }
+        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q, v);
+        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q + 8, v + 8);
       }
-    }
-    to_mma();
-    // ---- L3: C1 = act(Cin Wc0^T + b) ----
-    if (tid == 0) gemm_kmajor(tmem, sm.a, sm.w.c0[0], sm.w.c0[1], 64, 48, false);
-    mma_done();
-    {
-      float v[32];
-      ld32(my_lanes + half * 32, v);
+      to_mma();
+      // ---- L4: C2 = act(C1 Wc1^T + b) ----
+      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.c1[0], sm.w.c1[1], 64, 64);
+      mma_done();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float z = v[i] + sm.w.bc0[half * 32 + i];
-        v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
+      for (int q = 0; q < 2; ++q) {
+        float v[16];
+        ld16(my_lanes + part * 32 + 16 * q, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float z = v[i] + sm.w.bc1[part * 32 + 16 * q + i];
+          v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
+        }
+        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q, v);
+        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q + 8, v + 8);
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) put_chunk(sm.a, row, half * 32 + 8 * c, v + 8 * c);
-    }
-    to_mma();
-    // ---- L4: C2 = act(C1 Wc1^T + b) ----
-    if (tid == 0) gemm_kmajor(tmem, sm.a, sm.w.c1[0], sm.w.c1[1], 64, 64, false);
-    mma_done();
-    {
-      float v[32];
-      ld32(my_lanes + half * 32, v);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float z = v[i] + sm.w.bc1[half * 32 + i];
-        v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
+      pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
+      to_mma();
+      // ---- L5: rgb = sigmoid(clip(C2 Wc2^T + b)) ----
+      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.c2[0], sm.w.c2[1], 16, 64);
+      mma_done();
+      if (part == 0) {
+        float v[16];
+        ld16(my_lanes, v);
+        if (valid)
+          __stcs(m.out + gs, make_float4(expf(sm.sig_raw[row]), sigm(clip15(v[0] + sm.w.bc2[0])),
+                                         sigm(clip15(v[1] + sm.w.bc2[1])), sigm(clip15(v[2] + sm.w.bc2[2]))));
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) put_chunk(sm.a, row, half * 32 + 8 * c, v + 8 * c);
+      if (!has_next) break;
+      if (nx.f != loaded) {
+        __syncthreads();  // every thread is done with the old biases
+        stage_weights_tc(m.fields[nx.f], m.params, sm.w);
+        loaded = nx.f;
+      }
+      pf.put_x(sm.a[0], sm.a[1], row, part);  // the A tile is free: every MMA has completed
+      tile = next;
+      cur = nx;
     }
-    to_mma();
-    // ---- L5: rgb = sigmoid(clip(C2 Wc2^T + b)) ----
-    if (tid == 0) gemm_kmajor(tmem, sm.a, sm.w.c2[0], sm.w.c2[1], 16, 64, false);
-    mma_done();
-    {
-      float v[16];
-      tc::tmem_ld16(my_lanes, v);
-      tc::tmem_wait_ld();
-      if (half == 0 && valid)
-        m.out[gs] = make_float4(expf(sm.sig_raw[row]), sigm(clip15(v[0] + sm.w.bc2[0])),
-                                sigm(clip15(v[1] + sm.w.bc2[1])), sigm(clip15(v[2] + sm.w.bc2[2])));
-    }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
   }
+  tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_free(tmem, 64);
 }
@@ -350,6 +439,7 @@ __global__ void __launch_bounds__(NTH, 2) k_mlp_fwd_tc(MlpLaunch m) {
 // G and A tiles through MN-major descriptors (no transposed copies) and accumulate in TMEM for
 // every tile a CTA processes; each activation tile carries an extra ones column so the same
 // GEMM yields the bias gradient.  TMEM is flushed with one atomicAdd per weight per CTA.
+// 16 warps: 4 lane quadrants x 4 column parts, so every epilogue is 16 columns per thread.
 constexpr int XW = 40, HW = 72, CW = 56;  // tile widths incl. the ones chunk
 
 struct BwdTcSmem {
@@ -369,35 +459,6 @@ struct BwdTcSmem {
 
 // TMEM columns: [0,64) transient accumulator; dW accumulators (M = 64 rows = out features).
 constexpr uint32_t TD_C2 = 128, TD_C1 = 200, TD_C0 = 272, TD_D1 = 328, TD_D0 = 400;
-
-// Write 8 consecutive columns of row r into a tile with TM rows (any width).
-__device__ __forceinline__ void put8(uint8_t* hi, uint8_t* lo, int r, int c0, const float* v) {
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint16_t h0, l0, h1, l1;
-    tc::split_bf16(v[2 * j], h0, l0);
-    tc::split_bf16(v[2 * j + 1], h1, l1);
-    h[j] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-    l[j] = (uint32_t)l0 | ((uint32_t)l1 << 16);
-  }
-  const uint32_t off = tc::core_offset(r, c0, TM);
-  *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
-  *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
-}
-
-// Read back 8 consecutive columns of row r (hi + lo).
-__device__ __forceinline__ void get8(const uint8_t* hi, const uint8_t* lo, int r, int c0, float* v) {
-  const uint32_t off = tc::core_offset(r, c0, TM);
-  const uint4 h = *reinterpret_cast<const uint4*>(hi + off);
-  const uint4 l = *reinterpret_cast<const uint4*>(lo + off);
-  const uint32_t hh[4] = {h.x, h.y, h.z, h.w}, ll[4] = {l.x, l.y, l.z, l.w};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    v[2 * j] = __uint_as_float(hh[j] << 16) + __uint_as_float(ll[j] << 16);
-    v[2 * j + 1] = __uint_as_float(hh[j] & 0xffff0000u) + __uint_as_float(ll[j] & 0xffff0000u);
-  }
-}
 
 // D (M=64 x N) (+)= G^T A over K = TM samples; G tile (TM x >=64 cols span), A tile (TM x N);
 // both read MN-major (SBO = TM/8*128, LBO = 128).
@@ -443,9 +504,9 @@ __device__ __forceinline__ void gemm_igrad(uint32_t d_tmem, const uint8_t* g_hi,
 __device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, int ones, float* gW,
                          float* gb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quad = warp & 3, half = warp >> 2;
+  const int quad = warp & 3, part = warp >> 2, parts = (int)(blockDim.x >> 7);
   const int o = quad * 16 + lane;
-  for (int g = half; g < N / 8; g += 2) {
+  for (int g = part; g < N / 8; g += parts) {
     float v[8];
     tc::tmem_ld8(tmem + ((uint32_t)(quad * 32) << 16) + col0 + 8 * g, v);
     tc::tmem_wait_ld();
@@ -473,15 +534,28 @@ __device__ void flush_all(uint32_t tmem, const FieldDesc& fd, float* __restrict_
 
 __device__ __forceinline__ void ones_chunk(uint8_t* hi, uint8_t* lo, int c0) {
   float v[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int r = threadIdx.x; r < TM; r += NTH) put8(hi, lo, r, c0, v);
+  for (int r = threadIdx.x; r < TM; r += blockDim.x) put8(hi, lo, r, c0, v);
 }
 
-__global__ void __launch_bounds__(NTH, 1) k_mlp_bwd_tc(MlpLaunch m) {
+// act'(a) * dv for 16 columns of row r of tile (hi, lo), written back in place as G.
+__device__ __forceinline__ void grad_act16(uint8_t* hi, uint8_t* lo, int r, int c0, float* v, int act) {
+  float a[16];
+  get8(hi, lo, r, c0, a);
+  get8(hi, lo, r, c0 + 8, a + 8);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] *= act == 2 ? a[i] * (1.f - a[i]) : (a[i] > 0.f ? 1.f : 0.f);
+  put8(hi, lo, r, c0, v);
+  put8(hi, lo, r, c0 + 8, v + 8);
+}
+
+__global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
+  constexpr int NP = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   BwdTcSmem& sm = *reinterpret_cast<BwdTcSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quad = warp & 3, half = warp >> 2;
+  const int quad = warp & 3, part = warp >> 2;
   const int row = quad * 32 + lane;
+  const int c16 = part * 16;  // this thread's 16 columns of a 64-wide layer
   if (warp == 0) tc::tmem_alloc(&sm.tslot, 512);
   if (tid == 0) {
     tc::mbar_init(&sm.mbar, 1);
@@ -493,7 +567,7 @@ __global__ void __launch_bounds__(NTH, 1) k_mlp_bwd_tc(MlpLaunch m) {
   ones_chunk(sm.cin[0], sm.cin[1], 48);
   ones_chunk(sm.c1[0], sm.c1[1], 64);
   ones_chunk(sm.c2[0], sm.c2[1], 64);
-  for (int e = tid; e < TM * 16 * 2 / 4; e += NTH) {  // G5 columns 3..15 stay zero
+  for (int e = tid; e < TM * 16 * 2 / 4; e += NTB) {  // G5 columns 3..15 stay zero
     reinterpret_cast<uint32_t*>(sm.g5[0])[e] = 0u;
     reinterpret_cast<uint32_t*>(sm.g5[1])[e] = 0u;
   }
@@ -509,136 +583,110 @@ __global__ void __launch_bounds__(NTH, 1) k_mlp_bwd_tc(MlpLaunch m) {
     phase ^= 1u;
     tc::fence_after();
   };
-  const uint32_t per = (m.n_tiles + gridDim.x - 1) / gridDim.x;
-  const uint32_t t_begin = blockIdx.x * per;
-  const uint32_t t_end = min(m.n_tiles, t_begin + per);
+  // balanced contiguous tile range per CTA
+  const uint32_t t_begin = (uint32_t)(((uint64_t)blockIdx.x * m.n_tiles) / gridDim.x);
+  const uint32_t t_end = (uint32_t)(((uint64_t)(blockIdx.x + 1) * m.n_tiles) / gridDim.x);
   int loaded = -1;
-  bool fresh = true;  // next dW GEMMs start a new accumulation
-  for (uint32_t tile = t_begin; tile < t_end; ++tile) {
-    const int f = tile_field(m, tile);
-    const FieldDesc& fd = m.fields[f];
-    const uint64_t s0 = m.field_off[f] + (uint64_t)(tile - m.tile_off[f]) * TM;
-    const uint64_t rem = m.field_off[f + 1] - s0;
-    const int count = rem < (uint64_t)TM ? (int)rem : TM;
-    if (f != loaded) {
-      if (loaded >= 0) flush_all(tmem, m.fields[loaded], m.grads);
-      tc::fence_before();
-      __syncthreads();
-      tc::fence_after();
-      stage_weights_tc(fd, m.params, sm.w);
-      loaded = f;
-      fresh = true;
-    }
-    const int act_c = fd.coarse ? 2 : 1;
-    const bool valid = row < count;
-    const uint64_t gs = s0 + row;
-    // ---------------- forward recompute ----------------
-    {
-      float v[16];
+  if (t_begin < t_end) {
+    uint32_t tile = t_begin;
+    TileGeo cur = tile_geo(m, tile);
+    Pref<NP> pf;
+    pf.start(m, row < cur.count, cur.s0 + row, part, true);
+    pf.rec(m, part);
+    pf.appearance(m, m.fields[cur.f], part);
+    stage_weights_tc(m.fields[cur.f], m.params, sm.w);
+    loaded = cur.f;
+    bool fresh = true;  // next dW GEMMs start a new accumulation
+    pf.put_x(sm.x[0], sm.x[1], row, part);
+    for (;;) {
+      const FieldDesc& fd = m.fields[cur.f];
+      const int act_c = fd.coarse ? 2 : 1;
+      const bool valid = row < cur.count;
+      const uint64_t gs = cur.s0 + row;
+      const uint32_t next = tile + 1;
+      const bool has_next = next < t_end;
+      const TileGeo nx = has_next ? tile_geo(m, next) : cur;
+      // this tile's prefetched dir / app / upstream gradient move out of the prefetch registers
+      float cur_app[17];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int l = half * 8 + j;
-        float2 xx = make_float2(0.f, 0.f);
-        if (valid && l < (int)m.levels)
-          xx = reinterpret_cast<const float2*>(m.X)[(uint64_t)l * m.x_stride + gs];
-        v[2 * j] = xx.x;
-        v[2 * j + 1] = xx.y;
+      for (int i = 0; i < 17; ++i) cur_app[i] = pf.app[i];
+      const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
+      const float4 up = pf.g;
+      to_mma();
+      // ---------------- forward recompute ----------------
+      if (tid == 0) gemm_kmajor_t(tmem, sm.x[0], sm.x[1], sm.w.d0[0], sm.w.d0[1], 64, 32);
+      pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next: X, item
+      mma_done();
+      {
+        float v[16];
+        ld16(my_lanes + c16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[c16 + i], 0.f);
+        put8(sm.h1[0], sm.h1[1], row, c16, v);
+        put8(sm.h1[0], sm.h1[1], row, c16 + 8, v + 8);
       }
-      put8(sm.x[0], sm.x[1], row, half * 16, v);
-      put8(sm.x[0], sm.x[1], row, half * 16 + 8, v + 8);
-    }
-    to_mma();
-    if (tid == 0) gemm_kmajor_t(tmem, sm.x[0], sm.x[1], sm.w.d0[0], sm.w.d0[1], 64, 32);
-    mma_done();
-    {
-      float v[32];
-      ld32(my_lanes + half * 32, v);
+      to_mma();
+      if (tid == 0) gemm_kmajor_t(tmem, sm.h1[0], sm.h1[1], sm.w.d1[0], sm.w.d1[1], 16, 64);
+      mma_done();
+      {
+        float raw[16];
+        if (part == 0) {
+          ld16(my_lanes, raw);
+          uint32_t mask = 0;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[half * 32 + i], 0.f);
+          for (int i = 0; i < 16; ++i) {
+            const float z = raw[i] + sm.w.bd1[i];
+            mask |= (z > 15.f || z < -15.f ? 1u : 0u) << i;
+            raw[i] = clip15(z);
+          }
+          sm.sig_raw[row] = raw[0];
+          sm.dmask[row] = mask;
+        }
+        Pref<NP> cp;
+        cp.valid = valid;
+        cp.dir[0] = d0;
+        cp.dir[1] = d1;
+        cp.dir[2] = d2;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) put8(sm.h1[0], sm.h1[1], row, half * 32 + 8 * c, v + 8 * c);
-    }
-    to_mma();
-    if (tid == 0) gemm_kmajor_t(tmem, sm.h1[0], sm.h1[1], sm.w.d1[0], sm.w.d1[1], 16, 64);
-    mma_done();
-    {
-      float raw[16];
-      tc::tmem_ld16(my_lanes, raw);
-      tc::tmem_wait_ld();
-      float cin[48];
-      uint32_t mask = 0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float z = raw[i] + sm.w.bd1[i];
-        mask |= (z > 15.f || z < -15.f ? 1u : 0u) << i;
-        raw[i] = clip15(z);
+        for (int i = 0; i < 17; ++i) cp.app[i] = cur_app[i];
+        cp.put_cin(sm.cin[0], sm.cin[1], row, part, raw);
       }
+      to_mma();
+      if (tid == 0) gemm_kmajor_t(tmem, sm.cin[0], sm.cin[1], sm.w.c0[0], sm.w.c0[1], 64, 48);
+      mma_done();
+      {
+        float v[16];
+        ld16(my_lanes + c16, v);
 #pragma unroll
-      for (int i = 0; i < 15; ++i) cin[i] = raw[1 + i];
-      float sh[16];
-      const float* app = nullptr;
-      if (valid) {
-        const RayRec& r = m.rec[m.s_item[gs]];
-        sh16((float)r.d[0], (float)r.d[1], (float)r.d[2], sh);
-        app = m.app_per_sample ? m.app_override + gs * fd.app_dim
-                               : (m.app_override ? m.app_override : m.app_table + (uint64_t)r.img * fd.app_dim);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) sh[i] = 0.f;
+        for (int i = 0; i < 16; ++i) {
+          const float z = v[i] + sm.w.bc0[c16 + i];
+          v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
+        }
+        put8(sm.c1[0], sm.c1[1], row, c16, v);
+        put8(sm.c1[0], sm.c1[1], row, c16 + 8, v + 8);
       }
+      pf.rec(m, part);  // next tile's RayRec
+      to_mma();
+      if (tid == 0) gemm_kmajor_t(tmem, sm.c1[0], sm.c1[1], sm.w.c1[0], sm.w.c1[1], 64, 64);
+      mma_done();
+      {
+        float v[16];
+        ld16(my_lanes + c16, v);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) cin[15 + i] = sh[i];
-      for (int i = 0; i < 17; ++i) cin[31 + i] = (app && i < (int)fd.app_dim) ? app[i] : 0.f;
-      if (half == 0) {
-        sm.sig_raw[row] = raw[0];
-        sm.dmask[row] = mask;
-        put8(sm.cin[0], sm.cin[1], row, 0, cin);
-        put8(sm.cin[0], sm.cin[1], row, 8, cin + 8);
-        put8(sm.cin[0], sm.cin[1], row, 16, cin + 16);
-      } else {
-        put8(sm.cin[0], sm.cin[1], row, 24, cin + 24);
-        put8(sm.cin[0], sm.cin[1], row, 32, cin + 32);
-        put8(sm.cin[0], sm.cin[1], row, 40, cin + 40);
+        for (int i = 0; i < 16; ++i) {
+          const float z = v[i] + sm.w.bc1[c16 + i];
+          v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
+        }
+        put8(sm.c2[0], sm.c2[1], row, c16, v);
+        put8(sm.c2[0], sm.c2[1], row, c16 + 8, v + 8);
       }
-    }
-    to_mma();
-    if (tid == 0) gemm_kmajor_t(tmem, sm.cin[0], sm.cin[1], sm.w.c0[0], sm.w.c0[1], 64, 48);
-    mma_done();
-    {
-      float v[32];
-      ld32(my_lanes + half * 32, v);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float z = v[i] + sm.w.bc0[half * 32 + i];
-        v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) put8(sm.c1[0], sm.c1[1], row, half * 32 + 8 * c, v + 8 * c);
-    }
-    to_mma();
-    if (tid == 0) gemm_kmajor_t(tmem, sm.c1[0], sm.c1[1], sm.w.c1[0], sm.w.c1[1], 64, 64);
-    mma_done();
-    {
-      float v[32];
-      ld32(my_lanes + half * 32, v);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float z = v[i] + sm.w.bc1[half * 32 + i];
-        v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) put8(sm.c2[0], sm.c2[1], row, half * 32 + 8 * c, v + 8 * c);
-    }
-    to_mma();
-    if (tid == 0) gemm_kmajor_t(tmem, sm.c2[0], sm.c2[1], sm.w.c2[0], sm.w.c2[1], 16, 64);
-    mma_done();
-    // ---------------- B1: colour head adjoint (field.cpp:298-306) ----------------
-    {
-      float v[16];
-      tc::tmem_ld16(my_lanes, v);
-      tc::tmem_wait_ld();
-      if (half == 0) {
-        const float4 up = valid ? m.grad_in[gs] : make_float4(0.f, 0.f, 0.f, 0.f);
+      to_mma();
+      if (tid == 0) gemm_kmajor_t(tmem, sm.c2[0], sm.c2[1], sm.w.c2[0], sm.w.c2[1], 16, 64);
+      mma_done();
+      // ---------------- B1: colour head adjoint (field.cpp:298-306) ----------------
+      if (part == 0) {
+        float v[16];
+        ld16(my_lanes, v);
         const float ug[3] = {up.y, up.z, up.w};
         float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -652,53 +700,42 @@ __global__ void __launch_bounds__(NTH, 1) k_mlp_bwd_tc(MlpLaunch m) {
         // sigma path of the density raw gradient (field.cpp:313)
         sm.gsig[row] = (sm.dmask[row] & 1u) ? 0.f : up.x * expf(sm.sig_raw[row]);
       }
-    }
-    to_mma();
-    if (tid == 0) {
-      gemm_wgrad(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], HW, !fresh);
-      gemm_igrad(tmem, sm.g5[0], sm.g5[1], sm.w.c2[0], sm.w.c2[1], 16, 64, 16);
-    }
-    mma_done();
-    // ---------------- B2: G4 = dC2 * act'(C2) -> c2 tile ----------------
-    {
-      float v[32], a[32];
-      ld32(my_lanes + half * 32, v);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) get8(sm.c2[0], sm.c2[1], row, half * 32 + 8 * c, a + 8 * c);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= act_c == 2 ? a[i] * (1.f - a[i]) : (a[i] > 0.f ? 1.f : 0.f);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) put8(sm.c2[0], sm.c2[1], row, half * 32 + 8 * c, v + 8 * c);
-    }
-    to_mma();
-    if (tid == 0) {
-      gemm_wgrad(tmem + TD_C1, sm.c2[0], sm.c2[1], sm.c1[0], sm.c1[1], HW, !fresh);
-      gemm_igrad(tmem, sm.c2[0], sm.c2[1], sm.w.c1[0], sm.w.c1[1], 64, 64, 64);
-    }
-    mma_done();
-    // ---------------- B3: G3 = dC1 * act'(C1) -> c1 tile ----------------
-    {
-      float v[32], a[32];
-      ld32(my_lanes + half * 32, v);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) get8(sm.c1[0], sm.c1[1], row, half * 32 + 8 * c, a + 8 * c);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= act_c == 2 ? a[i] * (1.f - a[i]) : (a[i] > 0.f ? 1.f : 0.f);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) put8(sm.c1[0], sm.c1[1], row, half * 32 + 8 * c, v + 8 * c);
-    }
-    to_mma();
-    if (tid == 0) {
-      gemm_wgrad(tmem + TD_C0, sm.c1[0], sm.c1[1], sm.cin[0], sm.cin[1], CW, !fresh);
-      gemm_igrad(tmem, sm.c1[0], sm.c1[1], sm.w.c0[0], sm.w.c0[1], 64, 16, 64);
-    }
-    mma_done();
-    // ---------------- B4: G2 = density raw gradient -> cin tile cols 0..15 ----------------
-    {
-      float v[16];
-      tc::tmem_ld16(my_lanes, v);
-      tc::tmem_wait_ld();
-      if (half == 0) {
+      pf.grad(m, part);  // next tile's upstream gradient
+      to_mma();
+      if (tid == 0) {
+        gemm_wgrad(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], HW, !fresh);
+        gemm_igrad(tmem, sm.g5[0], sm.g5[1], sm.w.c2[0], sm.w.c2[1], 16, 64, 16);
+      }
+      mma_done();
+      // ---------------- B2: G4 = dC2 * act'(C2) -> c2 tile ----------------
+      {
+        float v[16];
+        ld16(my_lanes + c16, v);
+        grad_act16(sm.c2[0], sm.c2[1], row, c16, v, act_c);
+      }
+      to_mma();
+      if (tid == 0) {
+        gemm_wgrad(tmem + TD_C1, sm.c2[0], sm.c2[1], sm.c1[0], sm.c1[1], HW, !fresh);
+        gemm_igrad(tmem, sm.c2[0], sm.c2[1], sm.w.c1[0], sm.w.c1[1], 64, 64, 64);
+      }
+      mma_done();
+      // ---------------- B3: G3 = dC1 * act'(C1) -> c1 tile ----------------
+      {
+        float v[16];
+        ld16(my_lanes + c16, v);
+        grad_act16(sm.c1[0], sm.c1[1], row, c16, v, act_c);
+      }
+      pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
+      to_mma();
+      if (tid == 0) {
+        gemm_wgrad(tmem + TD_C0, sm.c1[0], sm.c1[1], sm.cin[0], sm.cin[1], CW, !fresh);
+        gemm_igrad(tmem, sm.c1[0], sm.c1[1], sm.w.c0[0], sm.w.c0[1], 64, 16, 64);
+      }
+      mma_done();
+      // ---------------- B4: G2 = density raw gradient -> cin tile cols 0..15 ----------------
+      if (part == 0) {
+        float v[16];
+        ld16(my_lanes, v);
         const uint32_t mask = sm.dmask[row];
         float g[16];
         g[0] = sm.gsig[row];
@@ -707,49 +744,58 @@ __global__ void __launch_bounds__(NTH, 1) k_mlp_bwd_tc(MlpLaunch m) {
         put8(sm.cin[0], sm.cin[1], row, 0, g);
         put8(sm.cin[0], sm.cin[1], row, 8, g + 8);
       }
-    }
-    to_mma();
-    if (tid == 0) {
-      gemm_wgrad(tmem + TD_D1, sm.cin[0], sm.cin[1], sm.h1[0], sm.h1[1], HW, !fresh);
-      gemm_igrad(tmem, sm.cin[0], sm.cin[1], sm.w.d1[0], sm.w.d1[1], 16, 64, 16);
-    }
-    mma_done();
-    // ---------------- B5: G1 = dH1 * relu'(H1) -> h1 tile ----------------
-    {
-      float v[32], a[32];
-      ld32(my_lanes + half * 32, v);
+      to_mma();
+      if (tid == 0) {
+        gemm_wgrad(tmem + TD_D1, sm.cin[0], sm.cin[1], sm.h1[0], sm.h1[1], HW, !fresh);
+        gemm_igrad(tmem, sm.cin[0], sm.cin[1], sm.w.d1[0], sm.w.d1[1], 16, 64, 16);
+      }
+      mma_done();
+      // ---------------- B5: G1 = dH1 * relu'(H1) -> h1 tile ----------------
+      {
+        float v[16];
+        ld16(my_lanes + c16, v);
+        grad_act16(sm.h1[0], sm.h1[1], row, c16, v, 1);
+      }
+      to_mma();
+      if (tid == 0) {
+        gemm_wgrad(tmem + TD_D0, sm.h1[0], sm.h1[1], sm.x[0], sm.x[1], XW, !fresh);
+        gemm_igrad(tmem, sm.h1[0], sm.h1[1], sm.w.d0[0], sm.w.d0[1], 64, 32, 64);
+      }
+      mma_done();
+      fresh = false;
+      // ---------------- B6: dX -> global, level-major; next tile's X into the x tile ----------------
+      {
+        float v[8];
+        tc::tmem_ld8(my_lanes + part * 8, v);
+        tc::tmem_wait_ld();
+        if (valid) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) get8(sm.h1[0], sm.h1[1], row, half * 32 + 8 * c, a + 8 * c);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= a[i] > 0.f ? 1.f : 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) put8(sm.h1[0], sm.h1[1], row, half * 32 + 8 * c, v + 8 * c);
-    }
-    to_mma();
-    if (tid == 0) {
-      gemm_wgrad(tmem + TD_D0, sm.h1[0], sm.h1[1], sm.x[0], sm.x[1], XW, !fresh);
-      gemm_igrad(tmem, sm.h1[0], sm.h1[1], sm.w.d0[0], sm.w.d0[1], 64, 32, 64);
-    }
-    mma_done();
-    fresh = false;
-    // ---------------- B6: dX -> global, level-major ----------------
-    {
-      float v[16];
-      tc::tmem_ld16(my_lanes + half * 16, v);
-      tc::tmem_wait_ld();
-      if (valid) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int l = half * 8 + j;
-          if (l < (int)m.levels)
-            reinterpret_cast<float2*>(m.dX)[(uint64_t)l * m.x_stride + gs] = make_float2(v[2 * j], v[2 * j + 1]);
+          for (int j = 0; j < 4; ++j) {
+            const int l = part * 4 + j;
+            if (l < (int)m.levels)
+              __stcs(reinterpret_cast<float2*>(m.dX) + (uint64_t)l * m.x_stride + gs,
+                     make_float2(v[2 * j], v[2 * j + 1]));
+          }
         }
       }
+      if (!has_next) break;
+      if (nx.f != loaded) {
+        flush_all(tmem, m.fields[loaded], m.grads);
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        stage_weights_tc(m.fields[nx.f], m.params, sm.w);
+        loaded = nx.f;
+        fresh = true;
+      }
+      pf.put_x(sm.x[0], sm.x[1], row, part);  // x tile is free: the D0 weight GEMM completed
+      tile = next;
+      cur = nx;
     }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
   }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
   if (loaded >= 0) flush_all(tmem, m.fields[loaded], m.grads);
   tc::fence_before();
   __syncthreads();
@@ -768,7 +814,7 @@ void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
   }
   const uint32_t want = (uint32_t)num_sms * 2;
   const unsigned grid = m.n_tiles < want ? m.n_tiles : want;
-  k_mlp_fwd_tc<<<grid, NTH, smem, s>>>(m);
+  k_mlp_fwd_tc<<<grid, NTF, smem, s>>>(m);
 }
 
 void launch_mlp_bwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
@@ -780,7 +826,7 @@ void launch_mlp_bwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
     attr = true;
   }
   const unsigned grid = m.n_tiles < (uint32_t)num_sms ? m.n_tiles : (uint32_t)num_sms;
-  k_mlp_bwd_tc<<<grid, NTH, smem, s>>>(m);
+  k_mlp_bwd_tc<<<grid, NTB, smem, s>>>(m);
 }
 
 }  // namespace dg
