@@ -58,7 +58,7 @@ struct LevelDesc {
   uint32_t n[3];     // lattice shape (grid.cpp:65-73)
   uint32_t hashed;   // MappingMode::Hashed (grid.cpp:97-99)
   uint32_t mask;     // rows - 1 when hashed
-  uint32_t pad;
+  uint32_t rows;     // table rows (2^T when hashed, n0 n1 n2 when one-to-one)
   uint64_t offset;   // floats from the field base to this level's table (rows x 2)
 };
 

@@ -33,6 +33,8 @@ struct SampleArrays {
   double* t;
   double* delta;
   uint32_t* item;
+  double* p;       // normalised field position (grid.cpp:109 / worker.cpp:215), SoA [3][pn]
+  uint64_t pn;     // samples (stride of p)
   float* X;        // n x 32 encoded features
   float4* out;     // sigma, r, g, b
   float4* grad;    // dsigma, dr, dg, db
@@ -95,6 +97,14 @@ void launch_items_to_records(uint32_t n, const float4* partial, const float* dep
                              PartialRec* out, cudaStream_t s);
 
 // ---- field kernels ----
+// One encode pass: levels [l0, l1) restricted to row slice k of S of each level's table, so
+// the tables a pass touches stay L2-resident (random rows of a 128 MB table miss L2; a
+// 64 MB slice does not).  Slice bounds are even, so a float4 row pair never straddles two.
+struct EncPass {
+  uint8_t l0, l1, k, S;
+};
+constexpr int kMaxEncPass = 96;
+
 struct FieldLaunch {
   const FieldDesc* fields;     // [2][n_local] (cascade-major)
   const PartDesc* parts;
@@ -107,13 +117,19 @@ struct FieldLaunch {
   uint32_t n_total;
   uint32_t n_local;
   uint32_t levels;
-  uint32_t dense_levels;   // leading levels processed together (one-to-one tables), >= 1
   uint32_t agg_levels;     // levels whose backward scatter is warp-aggregated
   const float* params;
   float* grads;
+  uint32_t n_pass;         // passes of this launch (grid.y)
+  EncPass pass[kMaxEncPass];
+  const double* s_p;       // per-sample normalised position, SoA [3][n_total] (k_march_fill)
+  uint32_t n_fields;       // 2 n_local; samples are field-major
+  uint32_t field_off[2 * kMaxPart + 1];
 };
-void launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s);
-void launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s);
+// Forward: one launch per slice index (slice k > 0 adds into X written by slice 0); returns
+// the number of launches.  Backward: one launch over every pass (reds commute).
+int launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s);
+int launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s);
 // stand-alone points variant (stage entry points): all points belong to one field
 void launch_encode_points(const FieldDesc* field, const float* params, const double* pts,
                           uint64_t n, uint32_t levels, float* X, uint32_t* rows, cudaStream_t s);
@@ -141,6 +157,7 @@ struct MlpLaunch {
   float4* out;                 // fwd: sigma, rgb
   const float4* grad_in;       // bwd: dsigma, drgb
   float* dX;                   // bwd, level-major like X
+  unsigned long long* trace;   // DG_TRACE_MLP builds only (tools/trace_mlp.cu): phase clocks
 };
 void launch_mlp_fwd(const MlpLaunch& m, cudaStream_t s);
 void launch_mlp_bwd(const MlpLaunch& m, int num_sms, cudaStream_t s);

@@ -65,6 +65,78 @@ __device__ __forceinline__ void scatter_level(float2* __restrict__ table, const 
   }
 }
 
+// Row pairing: the two x-neighbour corners (cx = 0, 1) of each (cy, cz) land in rows
+// i ^ h and (i + 1) ^ h (hashed) or r and r + 1 (one-to-one); when those differ only in bit 0
+// (half the time) they are one 16-byte aligned float4 (every level table is 16-byte aligned),
+// fetched or reduced with one vector access instead of two.
+__device__ __forceinline__ bool is_pair(uint32_t r0, uint32_t r1) {
+  return r0 != 0xffffffffu && r1 != 0xffffffffu && (r0 ^ r1) == 1u;
+}
+
+__device__ __forceinline__ float2 gather_level_pairs(const float2* __restrict__ table, const Corners& c) {
+  const float4* t4 = reinterpret_cast<const float4*>(table);
+  float4 q[4];
+  float2 b[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t r0 = c.row[2 * j], r1 = c.row[2 * j + 1];
+    if (is_pair(r0, r1)) {
+      q[j] = __ldg(t4 + (r0 >> 1));
+      b[j] = make_float2(0.f, 0.f);
+    } else {
+      const float2 a = r0 != 0xffffffffu ? __ldg(table + r0) : make_float2(0.f, 0.f);
+      q[j] = make_float4(a.x, a.y, 0.f, 0.f);
+      b[j] = r1 != 0xffffffffu ? __ldg(table + r1) : make_float2(0.f, 0.f);
+    }
+  }
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t r0 = c.row[2 * j], r1 = c.row[2 * j + 1];
+    float2 v0, v1;
+    if (is_pair(r0, r1)) {
+      const bool odd = r0 & 1u;
+      v0 = odd ? make_float2(q[j].z, q[j].w) : make_float2(q[j].x, q[j].y);
+      v1 = odd ? make_float2(q[j].x, q[j].y) : make_float2(q[j].z, q[j].w);
+    } else {
+      v0 = make_float2(q[j].x, q[j].y);
+      v1 = b[j];
+    }
+    acc.x = fmaf(c.w[2 * j], v0.x, acc.x);
+    acc.y = fmaf(c.w[2 * j], v0.y, acc.y);
+    acc.x = fmaf(c.w[2 * j + 1], v1.x, acc.x);
+    acc.y = fmaf(c.w[2 * j + 1], v1.y, acc.y);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ void scatter_level_pairs(float2* __restrict__ table, const Corners& c, float2 up) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t r0 = c.row[2 * j], r1 = c.row[2 * j + 1];
+    const float2 g0 = make_float2(c.w[2 * j] * up.x, c.w[2 * j] * up.y);
+    const float2 g1 = make_float2(c.w[2 * j + 1] * up.x, c.w[2 * j + 1] * up.y);
+    if (is_pair(r0, r1)) {
+      const float4 v = (r0 & 1u) ? make_float4(g1.x, g1.y, g0.x, g0.y) : make_float4(g0.x, g0.y, g1.x, g1.y);
+      atomicAdd(reinterpret_cast<float4*>(table) + (r0 >> 1), v);
+    } else {
+      if (r0 != 0xffffffffu) atomicAdd(table + r0, g0);
+      if (r1 != 0xffffffffu) atomicAdd(table + r1, g1);
+    }
+  }
+}
+
+// Keep only the corners whose row lies in this pass's slice of the level table.
+__device__ __forceinline__ void clip_to_slice(const LevelDesc& lv, const EncPass& ps, Corners& c) {
+  if (ps.S == 1) return;
+  const uint64_t rows = lv.rows;
+  const uint32_t lo = (uint32_t)((rows * ps.k / ps.S) & ~1ull);
+  const uint32_t hi = ps.k + 1 == ps.S ? 0xffffffffu : (uint32_t)((rows * (ps.k + 1) / ps.S) & ~1ull);
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (c.row[k] < lo || c.row[k] >= hi) c.row[k] = 0xffffffffu;
+}
+
 // Streaming accesses (sample arrays, features) bypass L2 residency so the hash tables keep it.
 __device__ __forceinline__ float2 ld_stream(const float2* p) {
   float2 v;
@@ -106,59 +178,83 @@ __device__ __forceinline__ void scatter_level_agg(float2* __restrict__ table, co
   }
 }
 
-// Level-group launch: grid (sample chunks, level groups).  Group 0 holds the leading dense
-// (one-to-one) levels, whose tables fit in L2 together; every hashed level (2^T rows) is its
-// own group.  CTAs are dispatched roughly in blockIdx order, so the device works through one
-// group's tables at a time and they stay L2-resident instead of streaming all 16 levels'
-// random rows from HBM at once.  Features are level-major (X[l][s] float2): coalesced.
-__global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __restrict__ X) {
-  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= f.n_total) return;
-  const uint32_t l0 = blockIdx.y == 0 ? 0u : f.dense_levels + blockIdx.y - 1;
-  const uint32_t l1 = blockIdx.y == 0 ? f.dense_levels : l0 + 1;
-  const uint32_t casc = s >= f.fine_total ? 1u : 0u;
-  const uint32_t item = __ldcs(f.s_item + s);
-  const FieldDesc& fd = f.fields[casc * f.n_local + f.item_part[item]];
-  const RayRec& r = f.rec[item];
-  double p[3];
-  normalized_point(fd.box_lo, fd.box_hi, r.o, r.d, __ldcs(f.s_t + s), p);
-  for (uint32_t l = l0; l < l1; ++l) {
-    Corners c;
-    level_corners(fd.lv[l], p, c);
-    const float2 acc = gather_level(reinterpret_cast<const float2*>(f.params + fd.base + fd.lv[l].offset), c);
-    st_stream(reinterpret_cast<float2*>(X) + (uint64_t)l * f.n_total + s, acc);
+// Field of sample s (samples are field-major; field_off lives in the kernel parameters).
+__device__ __forceinline__ uint32_t sample_field(const FieldLaunch& f, uint64_t s) {
+  uint32_t lo = 0, hi = f.n_fields;  // field_off[lo] <= s < field_off[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s >= f.field_off[mid]) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Normalised position of sample s: from the per-sample cache (PC) or re-derived from
+// (item, t) exactly as k_sample_points does (grid.cpp:109 normalisation).
+template <bool PC>
+__device__ __forceinline__ void load_point(const FieldLaunch& f, uint64_t s, const FieldDesc& fd,
+                                           double p[3]) {
+  if (PC) {
+    p[0] = __ldcs(f.s_p + s);
+    p[1] = __ldcs(f.s_p + f.n_total + s);
+    p[2] = __ldcs(f.s_p + 2 * (uint64_t)f.n_total + s);
+  } else {
+    const RayRec& r = f.rec[__ldcs(f.s_item + s)];
+    normalized_point(fd.box_lo, fd.box_hi, r.o, r.d, __ldcs(f.s_t + s), p);
   }
 }
 
+// grid (sample chunks, passes).  CTAs are dispatched roughly in blockIdx order, so the device
+// works through one pass (a few small tables, or one slice of a large one) at a time and
+// that working set stays L2-resident.  Features are level-major (X[l][s] float2): coalesced.
+// Slice k > 0 of a level runs in a later launch and adds into X.  The sample's normalised
+// position (fp64, bit-exact) comes from the march, so a pass is: 3 streaming loads, the
+// lattice math, 8 gathers.
+template <bool PC>
+__global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __restrict__ X) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= f.n_total) return;
+  const EncPass ps = f.pass[blockIdx.y];
+  const FieldDesc& fd = f.fields[sample_field(f, s)];
+  double p[3];
+  load_point<PC>(f, s, fd, p);
+  for (uint32_t l = ps.l0; l < ps.l1; ++l) {
+    Corners c;
+    level_corners(fd.lv[l], p, c);
+    clip_to_slice(fd.lv[l], ps, c);
+    float2 acc = gather_level_pairs(reinterpret_cast<const float2*>(f.params + fd.base + fd.lv[l].offset), c);
+    float2* xp = reinterpret_cast<float2*>(X) + (uint64_t)l * f.n_total + s;
+    if (ps.k > 0) {
+      const float2 o = ld_stream(xp);
+      acc.x += o.x;
+      acc.y += o.y;
+    }
+    st_stream(xp, acc);
+  }
+}
+
+template <bool PC>
 __global__ void __launch_bounds__(256) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
   const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = s < f.n_total;
-  const uint32_t l0 = blockIdx.y == 0 ? 0u : f.dense_levels + blockIdx.y - 1;
-  const uint32_t l1 = blockIdx.y == 0 ? f.dense_levels : l0 + 1;
-  uint32_t fidx = 0;
+  const EncPass ps = f.pass[blockIdx.y];
+  const uint32_t fidx = valid ? sample_field(f, s) : 0u;
   double p[3] = {0.0, 0.0, 0.0};
-  const FieldDesc* fdp = f.fields;
-  if (valid) {
-    const uint32_t casc = s >= f.fine_total ? 1u : 0u;
-    const uint32_t item = __ldcs(f.s_item + s);
-    fidx = casc * f.n_local + f.item_part[item];
-    fdp = f.fields + fidx;
-    const RayRec& r = f.rec[item];
-    normalized_point(fdp->box_lo, fdp->box_hi, r.o, r.d, __ldcs(f.s_t + s), p);
-  }
-  const FieldDesc& fd = *fdp;
-  for (uint32_t l = l0; l < l1; ++l) {
+  const FieldDesc& fd = f.fields[fidx];
+  if (valid) load_point<PC>(f, s, fd, p);
+  for (uint32_t l = ps.l0; l < ps.l1; ++l) {
     float2 up = make_float2(0.f, 0.f);
     Corners c;
     if (valid) {
       up = ld_stream(reinterpret_cast<const float2*>(dX) + (uint64_t)l * f.n_total + s);
       level_corners(fd.lv[l], p, c);
+      clip_to_slice(fd.lv[l], ps, c);
     }
     float2* table = reinterpret_cast<float2*>(f.grads + fd.base + fd.lv[l].offset);
     if (l < f.agg_levels) {  // coarse levels: consecutive samples share corners
       scatter_level_agg(table, c, up, fidx, valid && (up.x != 0.f || up.y != 0.f));
     } else if (valid && (up.x != 0.f || up.y != 0.f)) {
-      scatter_level(table, c, up);
+      scatter_level_pairs(table, c, up);
     }
   }
 }
@@ -196,20 +292,31 @@ __global__ void k_encode_points_bwd(const FieldDesc* __restrict__ field, float* 
 
 inline dim3 grid_lv(uint64_t n, uint32_t L) { return dim3((unsigned)((n + 255) / 256), L); }
 
-inline dim3 grid_groups(const FieldLaunch& f) {
-  return dim3((unsigned)((f.n_total + 255) / 256), 1u + (f.levels - f.dense_levels));
-}
-
 }  // namespace
 
-void launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s) {
-  if (!f.n_total) return;
-  k_encode_fwd<<<grid_groups(f), 256, 0, s>>>(f, X);
+int launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s) {
+  if (!f.n_total || !f.n_pass) return 0;
+  const unsigned nb = (unsigned)((f.n_total + 255) / 256);
+  int launches = 0;
+  for (uint32_t k = 0;; ++k) {  // slice k of every pass group, in pass order
+    FieldLaunch g = f;
+    g.n_pass = 0;
+    for (uint32_t i = 0; i < f.n_pass; ++i)
+      if (f.pass[i].k == k) g.pass[g.n_pass++] = f.pass[i];
+    if (!g.n_pass) break;
+    if (f.s_p) k_encode_fwd<true><<<dim3(nb, g.n_pass), 256, 0, s>>>(g, X);
+    else k_encode_fwd<false><<<dim3(nb, g.n_pass), 256, 0, s>>>(g, X);
+    ++launches;
+  }
+  return launches;
 }
 
-void launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s) {
-  if (!f.n_total) return;
-  k_encode_bwd<<<grid_groups(f), 256, 0, s>>>(f, dX);
+int launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s) {
+  if (!f.n_total || !f.n_pass) return 0;
+  const dim3 grid((unsigned)((f.n_total + 255) / 256), f.n_pass);
+  if (f.s_p) k_encode_bwd<true><<<grid, 256, 0, s>>>(f, dX);
+  else k_encode_bwd<false><<<grid, 256, 0, s>>>(f, dX);
+  return 1;
 }
 
 void launch_encode_points(const FieldDesc* field, const float* params, const double* pts,

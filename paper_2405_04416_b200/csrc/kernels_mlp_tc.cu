@@ -108,19 +108,23 @@ __device__ void stage_weights_tc(const FieldDesc& fd, const float* __restrict__ 
 
 // D[TM x N] = A[TM x K] . B[N x K]^T, split-bf16 (3 MMAs per 16-wide K step).
 // A tile rows = TM (K-major, SBO 128, LBO TM/8*128); B tile rows = N (SBO 128, LBO N/8*128).
+// Descriptors are built once; a K step only advances their 14-bit start-address fields
+// (smem offsets < 256 KB never carry out of the field), so issue is back-to-back UTCHMMAs.
+template <int N, int K>
 __device__ __forceinline__ void gemm_kmajor_t(uint32_t d_tmem, const uint8_t* a_hi, const uint8_t* a_lo,
-                                              const uint8_t* b_hi, const uint8_t* b_lo, int N, int K) {
-  const uint32_t id = tc::idesc_bf16(TM, N, 0, 0);
-  const uint32_t a0 = tc::smem_u32(a_hi), a1 = tc::smem_u32(a_lo);
-  const uint32_t b0 = tc::smem_u32(b_hi), b1 = tc::smem_u32(b_lo);
-  const uint32_t a_lbo = (TM / 8) * 128, b_lbo = (N / 8) * 128;
+                                              const uint8_t* b_hi, const uint8_t* b_lo) {
+  constexpr uint32_t id = tc::idesc_bf16(TM, N, 0, 0);
+  constexpr uint32_t a_lbo = (TM / 8) * 128, b_lbo = (N / 8) * 128;
+  const uint64_t ah = tc::smem_desc(tc::smem_u32(a_hi), a_lbo, 128);
+  const uint64_t al = tc::smem_desc(tc::smem_u32(a_lo), a_lbo, 128);
+  const uint64_t bh = tc::smem_desc(tc::smem_u32(b_hi), b_lbo, 128);
+  const uint64_t bl = tc::smem_desc(tc::smem_u32(b_lo), b_lbo, 128);
+#pragma unroll
   for (int k = 0; k < K / 16; ++k) {
-    const uint32_t ao = k * 2 * a_lbo, bo = k * 2 * b_lbo;
-    const uint64_t ah = tc::smem_desc(a0 + ao, a_lbo, 128), al = tc::smem_desc(a1 + ao, a_lbo, 128);
-    const uint64_t bh = tc::smem_desc(b0 + bo, b_lbo, 128), bl = tc::smem_desc(b1 + bo, b_lbo, 128);
-    tc::mma_bf16(d_tmem, ah, bh, id, k > 0 ? 1u : 0u);
-    tc::mma_bf16(d_tmem, ah, bl, id, 1u);
-    tc::mma_bf16(d_tmem, al, bh, id, 1u);
+    const uint32_t ao = (k * 2 * a_lbo) >> 4, bo = (k * 2 * b_lbo) >> 4;
+    tc::mma_bf16(d_tmem, ah + ao, bh + bo, id, k > 0 ? 1u : 0u);
+    tc::mma_bf16(d_tmem, ah + ao, bl + bo, id, 1u);
+    tc::mma_bf16(d_tmem, al + ao, bh + bo, id, 1u);
   }
 }
 
@@ -273,6 +277,18 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
   tc::tmem_wait_ld();
 }
 
+// The MMAs of a stage and their commit come from one elected lane of warp 0.
+#define ISSUE(...)                      \
+  do {                                  \
+    if (warp == 0) {                    \
+      if (tc::elect_one()) {            \
+        __VA_ARGS__;                    \
+        tc::commit(&sm.mbar);           \
+      }                                 \
+      __syncwarp();                     \
+    }                                   \
+  } while (0)
+
 struct FwdTcSmem {
   TcWeights w;
   uint8_t a[2][TM * 64 * 2];  // activation operand (A, K-major), hi / lo
@@ -302,7 +318,6 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
   uint32_t phase = 0;
   auto mma_done = [&]() {
-    if (tid == 0) tc::commit(&sm.mbar);
     tc::mbar_wait(&sm.mbar, phase);
     phase ^= 1u;
     tc::fence_after();
@@ -327,7 +342,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
       const TileGeo nx = has_next ? tile_geo(m, next) : cur;
       to_mma();
       // ---- L1: H1 = relu(X Wd0^T + b) ----
-      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.d0[0], sm.w.d0[1], 64, 32);
+      ISSUE(gemm_kmajor_t<64, 32>(tmem, sm.a[0], sm.a[1], sm.w.d0[0], sm.w.d0[1]););
       float cin_app[17];
 #pragma unroll
       for (int i = 0; i < 17; ++i) cin_app[i] = pf.app[i];
@@ -345,7 +360,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
       }
       to_mma();
       // ---- L2: raw16 = H1 Wd1^T + b ; Cin = [clip(raw1..15) | SH16 | app | 0] ----
-      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.d1[0], sm.w.d1[1], 16, 64);
+      ISSUE(gemm_kmajor_t<16, 64>(tmem, sm.a[0], sm.a[1], sm.w.d1[0], sm.w.d1[1]););
       mma_done();
       {
         float raw[16];
@@ -368,7 +383,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
       pf.rec(m, part);  // next tile's RayRec (item arrived during L1/L2)
       to_mma();
       // ---- L3: C1 = act(Cin Wc0^T + b) ----
-      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.c0[0], sm.w.c0[1], 64, 48);
+      ISSUE(gemm_kmajor_t<64, 48>(tmem, sm.a[0], sm.a[1], sm.w.c0[0], sm.w.c0[1]););
       mma_done();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -384,7 +399,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
       }
       to_mma();
       // ---- L4: C2 = act(C1 Wc1^T + b) ----
-      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.c1[0], sm.w.c1[1], 64, 64);
+      ISSUE(gemm_kmajor_t<64, 64>(tmem, sm.a[0], sm.a[1], sm.w.c1[0], sm.w.c1[1]););
       mma_done();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -401,7 +416,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
       to_mma();
       // ---- L5: rgb = sigmoid(clip(C2 Wc2^T + b)) ----
-      if (tid == 0) gemm_kmajor_t(tmem, sm.a[0], sm.a[1], sm.w.c2[0], sm.w.c2[1], 16, 64);
+      ISSUE(gemm_kmajor_t<16, 64>(tmem, sm.a[0], sm.a[1], sm.w.c2[0], sm.w.c2[1]););
       mma_done();
       if (part == 0) {
         float v[16];
@@ -462,40 +477,42 @@ constexpr uint32_t TD_C2 = 128, TD_C1 = 200, TD_C0 = 272, TD_D1 = 328, TD_D0 = 4
 
 // D (M=64 x N) (+)= G^T A over K = TM samples; G tile (TM x >=64 cols span), A tile (TM x N);
 // both read MN-major (SBO = TM/8*128, LBO = 128).
+template <int N>
 __device__ __forceinline__ void gemm_wgrad(uint32_t d_tmem, const uint8_t* g_hi, const uint8_t* g_lo,
-                                           const uint8_t* a_hi, const uint8_t* a_lo, int N,
-                                           bool accumulate) {
-  const uint32_t id = tc::idesc_bf16(64, N, 1, 1);
-  const uint32_t g0 = tc::smem_u32(g_hi), g1 = tc::smem_u32(g_lo);
-  const uint32_t a0 = tc::smem_u32(a_hi), a1 = tc::smem_u32(a_lo);
+                                           const uint8_t* a_hi, const uint8_t* a_lo, bool accumulate) {
+  constexpr uint32_t id = tc::idesc_bf16(64, N, 1, 1);
   constexpr uint32_t SBO = (TM / 8) * 128;
+  const uint64_t gh = tc::smem_desc(tc::smem_u32(g_hi), 128, SBO);
+  const uint64_t gl = tc::smem_desc(tc::smem_u32(g_lo), 128, SBO);
+  const uint64_t ah = tc::smem_desc(tc::smem_u32(a_hi), 128, SBO);
+  const uint64_t al = tc::smem_desc(tc::smem_u32(a_lo), 128, SBO);
+  const uint32_t acc0 = accumulate ? 1u : 0u;
+#pragma unroll
   for (int k = 0; k < TM / 16; ++k) {
-    const uint32_t o = k * 256;
-    const uint64_t gh = tc::smem_desc(g0 + o, 128, SBO), gl = tc::smem_desc(g1 + o, 128, SBO);
-    const uint64_t ah = tc::smem_desc(a0 + o, 128, SBO), al = tc::smem_desc(a1 + o, 128, SBO);
-    tc::mma_bf16(d_tmem, gh, ah, id, (accumulate || k > 0) ? 1u : 0u);
-    tc::mma_bf16(d_tmem, gh, al, id, 1u);
-    tc::mma_bf16(d_tmem, gl, ah, id, 1u);
+    const uint32_t o = (k * 256) >> 4;
+    tc::mma_bf16(d_tmem, gh + o, ah + o, id, k > 0 ? 1u : acc0);
+    tc::mma_bf16(d_tmem, gh + o, al + o, id, 1u);
+    tc::mma_bf16(d_tmem, gl + o, ah + o, id, 1u);
   }
 }
 
 // D (TM x N) = G W : G tile K-major [TM x K=out], W tile stored [Wrows=out x cols=in]
 // read MN-major (SBO = Wrows/8*128, LBO = 128); N = number of leading input columns.
+template <int Wrows, int N, int K>
 __device__ __forceinline__ void gemm_igrad(uint32_t d_tmem, const uint8_t* g_hi, const uint8_t* g_lo,
-                                           const uint8_t* w_hi, const uint8_t* w_lo, int Wrows, int N,
-                                           int K) {
-  const uint32_t id = tc::idesc_bf16(TM, N, 0, 1);
-  const uint32_t g0 = tc::smem_u32(g_hi), g1 = tc::smem_u32(g_lo);
-  const uint32_t w0 = tc::smem_u32(w_hi), w1 = tc::smem_u32(w_lo);
-  constexpr uint32_t G_LBO = (TM / 8) * 128;
-  const uint32_t W_SBO = (uint32_t)(Wrows / 8) * 128;
+                                           const uint8_t* w_hi, const uint8_t* w_lo) {
+  constexpr uint32_t id = tc::idesc_bf16(TM, N, 0, 1);
+  constexpr uint32_t G_LBO = (TM / 8) * 128, W_SBO = (uint32_t)(Wrows / 8) * 128;
+  const uint64_t gh = tc::smem_desc(tc::smem_u32(g_hi), G_LBO, 128);
+  const uint64_t gl = tc::smem_desc(tc::smem_u32(g_lo), G_LBO, 128);
+  const uint64_t wh = tc::smem_desc(tc::smem_u32(w_hi), 128, W_SBO);
+  const uint64_t wl = tc::smem_desc(tc::smem_u32(w_lo), 128, W_SBO);
+#pragma unroll
   for (int k = 0; k < K / 16; ++k) {
-    const uint32_t go = k * 2 * G_LBO, wo = k * 256;
-    const uint64_t gh = tc::smem_desc(g0 + go, G_LBO, 128), gl = tc::smem_desc(g1 + go, G_LBO, 128);
-    const uint64_t wh = tc::smem_desc(w0 + wo, 128, W_SBO), wl = tc::smem_desc(w1 + wo, 128, W_SBO);
-    tc::mma_bf16(d_tmem, gh, wh, id, k > 0 ? 1u : 0u);
-    tc::mma_bf16(d_tmem, gh, wl, id, 1u);
-    tc::mma_bf16(d_tmem, gl, wh, id, 1u);
+    const uint32_t go = (k * 2 * G_LBO) >> 4, wo = (k * 256) >> 4;
+    tc::mma_bf16(d_tmem, gh + go, wh + wo, id, k > 0 ? 1u : 0u);
+    tc::mma_bf16(d_tmem, gh + go, wl + wo, id, 1u);
+    tc::mma_bf16(d_tmem, gl + go, wh + wo, id, 1u);
   }
 }
 
@@ -577,11 +594,27 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
   const uint32_t tmem = sm.tslot;
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
   uint32_t phase = 0;
+#ifdef DG_TRACE_MLP
+  // phase clocks of CTA 0 (threads 0 and 480): per stage [barrier entry, barrier exit, MMA done]
+  int tr_tile = 0, tr_pt = 0;
+  auto trace = [&]() {
+    if (blockIdx.x == 0 && (tid == 0 || tid == 480) && tr_tile < 64 && tr_pt < 32)
+      m.trace[(tr_tile * 2 + (tid ? 1 : 0)) * 32 + tr_pt] = clock64();
+    ++tr_pt;
+  };
+#else
+  auto trace = []() {};
+#endif
   auto mma_done = [&]() {
-    if (tid == 0) tc::commit(&sm.mbar);
     tc::mbar_wait(&sm.mbar, phase);
     phase ^= 1u;
     tc::fence_after();
+    trace();
+  };
+  auto sync_mma = [&]() {
+    trace();
+    to_mma();
+    trace();
   };
   // balanced contiguous tile range per CTA
   const uint32_t t_begin = (uint32_t)(((uint64_t)blockIdx.x * m.n_tiles) / gridDim.x);
@@ -612,9 +645,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       for (int i = 0; i < 17; ++i) cur_app[i] = pf.app[i];
       const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
       const float4 up = pf.g;
-      to_mma();
+      sync_mma();
       // ---------------- forward recompute ----------------
-      if (tid == 0) gemm_kmajor_t(tmem, sm.x[0], sm.x[1], sm.w.d0[0], sm.w.d0[1], 64, 32);
+      ISSUE(gemm_kmajor_t<64, 32>(tmem, sm.x[0], sm.x[1], sm.w.d0[0], sm.w.d0[1]););
       pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next: X, item
       mma_done();
       {
@@ -625,8 +658,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         put8(sm.h1[0], sm.h1[1], row, c16, v);
         put8(sm.h1[0], sm.h1[1], row, c16 + 8, v + 8);
       }
-      to_mma();
-      if (tid == 0) gemm_kmajor_t(tmem, sm.h1[0], sm.h1[1], sm.w.d1[0], sm.w.d1[1], 16, 64);
+      sync_mma();
+      ISSUE(gemm_kmajor_t<16, 64>(tmem, sm.h1[0], sm.h1[1], sm.w.d1[0], sm.w.d1[1]););
       mma_done();
       {
         float raw[16];
@@ -651,8 +684,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         for (int i = 0; i < 17; ++i) cp.app[i] = cur_app[i];
         cp.put_cin(sm.cin[0], sm.cin[1], row, part, raw);
       }
-      to_mma();
-      if (tid == 0) gemm_kmajor_t(tmem, sm.cin[0], sm.cin[1], sm.w.c0[0], sm.w.c0[1], 64, 48);
+      sync_mma();
+      ISSUE(gemm_kmajor_t<64, 48>(tmem, sm.cin[0], sm.cin[1], sm.w.c0[0], sm.w.c0[1]););
       mma_done();
       {
         float v[16];
@@ -666,8 +699,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         put8(sm.c1[0], sm.c1[1], row, c16 + 8, v + 8);
       }
       pf.rec(m, part);  // next tile's RayRec
-      to_mma();
-      if (tid == 0) gemm_kmajor_t(tmem, sm.c1[0], sm.c1[1], sm.w.c1[0], sm.w.c1[1], 64, 64);
+      sync_mma();
+      ISSUE(gemm_kmajor_t<64, 64>(tmem, sm.c1[0], sm.c1[1], sm.w.c1[0], sm.w.c1[1]););
       mma_done();
       {
         float v[16];
@@ -680,8 +713,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         put8(sm.c2[0], sm.c2[1], row, c16, v);
         put8(sm.c2[0], sm.c2[1], row, c16 + 8, v + 8);
       }
-      to_mma();
-      if (tid == 0) gemm_kmajor_t(tmem, sm.c2[0], sm.c2[1], sm.w.c2[0], sm.w.c2[1], 16, 64);
+      sync_mma();
+      ISSUE(gemm_kmajor_t<16, 64>(tmem, sm.c2[0], sm.c2[1], sm.w.c2[0], sm.w.c2[1]););
       mma_done();
       // ---------------- B1: colour head adjoint (field.cpp:298-306) ----------------
       if (part == 0) {
@@ -701,11 +734,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         sm.gsig[row] = (sm.dmask[row] & 1u) ? 0.f : up.x * expf(sm.sig_raw[row]);
       }
       pf.grad(m, part);  // next tile's upstream gradient
-      to_mma();
-      if (tid == 0) {
-        gemm_wgrad(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], HW, !fresh);
-        gemm_igrad(tmem, sm.g5[0], sm.g5[1], sm.w.c2[0], sm.w.c2[1], 16, 64, 16);
-      }
+      sync_mma();
+      ISSUE(gemm_wgrad<HW>(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], !fresh);
+        gemm_igrad<16, 64, 16>(tmem, sm.g5[0], sm.g5[1], sm.w.c2[0], sm.w.c2[1]););
       mma_done();
       // ---------------- B2: G4 = dC2 * act'(C2) -> c2 tile ----------------
       {
@@ -713,11 +744,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         ld16(my_lanes + c16, v);
         grad_act16(sm.c2[0], sm.c2[1], row, c16, v, act_c);
       }
-      to_mma();
-      if (tid == 0) {
-        gemm_wgrad(tmem + TD_C1, sm.c2[0], sm.c2[1], sm.c1[0], sm.c1[1], HW, !fresh);
-        gemm_igrad(tmem, sm.c2[0], sm.c2[1], sm.w.c1[0], sm.w.c1[1], 64, 64, 64);
-      }
+      sync_mma();
+      ISSUE(gemm_wgrad<HW>(tmem + TD_C1, sm.c2[0], sm.c2[1], sm.c1[0], sm.c1[1], !fresh);
+        gemm_igrad<64, 64, 64>(tmem, sm.c2[0], sm.c2[1], sm.w.c1[0], sm.w.c1[1]););
       mma_done();
       // ---------------- B3: G3 = dC1 * act'(C1) -> c1 tile ----------------
       {
@@ -726,11 +755,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         grad_act16(sm.c1[0], sm.c1[1], row, c16, v, act_c);
       }
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
-      to_mma();
-      if (tid == 0) {
-        gemm_wgrad(tmem + TD_C0, sm.c1[0], sm.c1[1], sm.cin[0], sm.cin[1], CW, !fresh);
-        gemm_igrad(tmem, sm.c1[0], sm.c1[1], sm.w.c0[0], sm.w.c0[1], 64, 16, 64);
-      }
+      sync_mma();
+      ISSUE(gemm_wgrad<CW>(tmem + TD_C0, sm.c1[0], sm.c1[1], sm.cin[0], sm.cin[1], !fresh);
+        gemm_igrad<64, 16, 64>(tmem, sm.c1[0], sm.c1[1], sm.w.c0[0], sm.w.c0[1]););
       mma_done();
       // ---------------- B4: G2 = density raw gradient -> cin tile cols 0..15 ----------------
       if (part == 0) {
@@ -744,11 +771,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         put8(sm.cin[0], sm.cin[1], row, 0, g);
         put8(sm.cin[0], sm.cin[1], row, 8, g + 8);
       }
-      to_mma();
-      if (tid == 0) {
-        gemm_wgrad(tmem + TD_D1, sm.cin[0], sm.cin[1], sm.h1[0], sm.h1[1], HW, !fresh);
-        gemm_igrad(tmem, sm.cin[0], sm.cin[1], sm.w.d1[0], sm.w.d1[1], 16, 64, 16);
-      }
+      sync_mma();
+      ISSUE(gemm_wgrad<HW>(tmem + TD_D1, sm.cin[0], sm.cin[1], sm.h1[0], sm.h1[1], !fresh);
+        gemm_igrad<16, 64, 16>(tmem, sm.cin[0], sm.cin[1], sm.w.d1[0], sm.w.d1[1]););
       mma_done();
       // ---------------- B5: G1 = dH1 * relu'(H1) -> h1 tile ----------------
       {
@@ -756,11 +781,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         ld16(my_lanes + c16, v);
         grad_act16(sm.h1[0], sm.h1[1], row, c16, v, 1);
       }
-      to_mma();
-      if (tid == 0) {
-        gemm_wgrad(tmem + TD_D0, sm.h1[0], sm.h1[1], sm.x[0], sm.x[1], XW, !fresh);
-        gemm_igrad(tmem, sm.h1[0], sm.h1[1], sm.w.d0[0], sm.w.d0[1], 64, 32, 64);
-      }
+      sync_mma();
+      ISSUE(gemm_wgrad<XW>(tmem + TD_D0, sm.h1[0], sm.h1[1], sm.x[0], sm.x[1], !fresh);
+        gemm_igrad<64, 32, 64>(tmem, sm.h1[0], sm.h1[1], sm.w.d0[0], sm.w.d0[1]););
       mma_done();
       fresh = false;
       // ---------------- B6: dX -> global, level-major; next tile's X into the x tile ----------------
@@ -778,6 +801,10 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
           }
         }
       }
+#ifdef DG_TRACE_MLP
+      ++tr_tile;
+      tr_pt = 0;
+#endif
       if (!has_next) break;
       if (nx.f != loaded) {
         flush_all(tmem, m.fields[loaded], m.grads);

@@ -178,6 +178,24 @@ __global__ void k_march_fill(const PartDesc* __restrict__ parts, const uint8_t* 
   cascade_march(pd, occ, r.o, r.d, it.te[i], it.tx[i], step, offset, fa, fb, emit);
 }
 
+// Per-sample normalised field position (grid.cpp:109 normalisation, fp64 bit-exact), written
+// once, coalesced, so every encode pass reads 24 B instead of re-deriving it from (item, t).
+__global__ void k_sample_points(const PartDesc* __restrict__ parts, ItemArrays it, SampleArrays sm,
+                                uint32_t n_fine) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= sm.pn) return;
+  const uint32_t i = __ldg(sm.item + s);
+  const PartDesc& pd = parts[it.part[i]];
+  const RayRec& r = it.rec[i];
+  const bool coarse = s >= n_fine;
+  double p[3];
+  normalized_point(coarse ? pd.coarse_lo : pd.fine_lo, coarse ? pd.coarse_hi : pd.fine_hi, r.o, r.d,
+                   __ldg(sm.t + s), p);
+  sm.p[s] = p[0];
+  sm.p[sm.pn + s] = p[1];
+  sm.p[2 * sm.pn + s] = p[2];
+}
+
 // Visit an item's samples in t order: coarse-before, fine, coarse-after.
 template <class F>
 __device__ __forceinline__ void for_item_samples(const ItemArrays& it, uint32_t n_items, uint32_t i,
@@ -549,11 +567,13 @@ void launch_item_setup(const Geo* geo, const PartDesc* parts, const uint8_t* occ
 }
 
 void launch_march_fill(const PartDesc* parts, const uint8_t* occ, uint32_t n_items,
-                       ItemArrays it, SampleArrays sm, uint32_t, double step, uint64_t seed,
+                       ItemArrays it, SampleArrays sm, uint32_t n_fine, double step, uint64_t seed,
                        uint64_t batch_id, int jitter, cudaStream_t s) {
   if (!n_items) return;
   k_march_fill<<<blocks(n_items, 128), 128, 0, s>>>(parts, occ, n_items, it, sm, step, seed,
                                                     batch_id, jitter);
+  if (sm.pn && sm.p)
+    k_sample_points<<<(unsigned)((sm.pn + 255) / 256), 256, 0, s>>>(parts, it, sm, n_fine);
 }
 
 void launch_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, uint32_t,

@@ -116,8 +116,17 @@ struct dg_ctx {
   std::vector<uint64_t> part_param_off; // per local partition (floats, device layout)
   std::vector<uint64_t> part_param_cnt; // flat (reference-order) count
   std::vector<uint64_t> field_dev_off;  // [2][n_local] device offset of each field
-  std::vector<uint64_t> field_size;     // [2][n_local]
+  std::vector<uint64_t> field_size;     // [2][n_local] flat (reference-order) floats
+  // flat <-> device mapping of one field: every level table starts 16-byte aligned on the
+  // device (paired-row float4 gathers / reds), so the device layout has small gaps
+  struct Seg {
+    uint64_t dev, flat, count;  // relative to the field's device base / flat start
+  };
+  std::vector<std::vector<Seg>> field_segs;  // [2][n_local]
   std::vector<std::vector<dg_array_desc>> layouts;
+  uint64_t enc_budget_fwd = 256ull << 20;  // encode pass budgets (DG_ENC_FWD_MB / DG_ENC_BWD_MB)
+  uint64_t enc_budget_bwd = 128ull << 20;
+  bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
   uint64_t n_params = 0;
   uint64_t occ_bytes = 0;
   std::vector<double> occ_thr;            // [n_local][2] current thresholds
@@ -148,7 +157,7 @@ struct dg_ctx {
   // per-step scratch
   DBuf h_o, h_d, h_gt, h_img, h_nseg, h_sched, h_flags, h_pos, cub_tmp, small, dropped, loss,
       error, rec, it_te, it_tx, it_t0, it_t1, it_nseg, it_order, it_part, it_sched, it_cnt,
-      it_off, it_ncb, it_contains, it_cscan, it_partial, it_depth, part_item_off_d, s_t, s_delta,
+      it_off, it_ncb, it_contains, it_cscan, it_partial, it_depth, part_item_off_d, s_t, s_delta, s_p,
       s_item, s_X, s_out, s_grad, s_dX, field_off_d, tile_off_f, tile_off_b, stream_send_d,
       stream_recv_d, send_buf, recv_buf, x_send, x_recv, out_rgb, out_T, out_depth, eval_app,
       perm_tab, occ_pts, occ_cells, occ_sigma;
@@ -231,6 +240,7 @@ int ctx_setup(dg_ctx* c) {
   c->layouts.resize(nl);
   c->field_dev_off.assign(2 * nl, 0);
   c->field_size.assign(2 * nl, 0);
+  c->field_segs.assign(2 * nl, {});
   uint64_t poff = 0, ooff = 0;
   for (uint32_t lp = 0; lp < nl; ++lp) {
     const uint32_t gid = c->local[lp];
@@ -274,7 +284,15 @@ int ctx_setup(dg_ctx* c) {
       fd.part = lp;
       fd.base = poff;
       const uint32_t T = 1u << (casc == 0 ? cfg.fine_table_log2 : cfg.coarse_table_log2);
-      uint64_t o = 0;
+      std::vector<dg_ctx::Seg>& segs = c->field_segs[casc * nl + lp];
+      uint64_t o = 0, of = 0;  // device / flat offsets within the field
+      auto seg = [&](uint64_t count) {
+        if (!segs.empty() && segs.back().dev + segs.back().count == o &&
+            segs.back().flat + segs.back().count == of)
+          segs.back().count += count;
+        else
+          segs.push_back({o, of, count});
+      };
       for (uint32_t l = 0; l < cfg.grid_levels; ++l) {
         LevelDesc& lv = fd.lv[l];
         const uint32_t n = level_resolution(cfg.grid_levels, cfg.base_resolution, cfg.max_resolution, l);
@@ -283,15 +301,21 @@ int ctx_setup(dg_ctx* c) {
         lv.hashed = vox <= T ? 0u : 1u;
         const uint64_t rows = lv.hashed ? T : vox;
         lv.mask = lv.hashed ? T - 1 : 0u;
+        lv.rows = uint32_t(rows);
+        o = (o + 3) & ~uint64_t(3);  // 16-byte aligned table: row pairs (2m, 2m+1) are float4s
         lv.offset = o;
-        c->layouts[lp].push_back({flat + o, rows * 2, uint32_t(casc), 0u, l, 0u});
+        c->layouts[lp].push_back({flat + of, rows * 2, uint32_t(casc), 0u, l, 0u});
+        seg(rows * 2);
         o += rows * 2;
+        of += rows * 2;
       }
       const uint32_t enc = cfg.grid_levels * 2, cin = 31 + cfg.appearance_dim;
       auto add = [&](uint64_t& field_off, uint64_t size, uint32_t kind, uint32_t idx) {
         field_off = o;
-        c->layouts[lp].push_back({flat + o, size, uint32_t(casc), kind, idx, 0u});
+        c->layouts[lp].push_back({flat + of, size, uint32_t(casc), kind, idx, 0u});
+        seg(size);
         o += size;
+        of += size;
       };
       add(fd.dw0, 64ull * enc, 1, 0);
       add(fd.db0, 64, 2, 0);
@@ -305,8 +329,8 @@ int ctx_setup(dg_ctx* c) {
       add(fd.cb2, 3, 4, 2);
       fd.size = o;
       c->field_dev_off[casc * nl + lp] = poff;
-      c->field_size[casc * nl + lp] = o;
-      flat += o;
+      c->field_size[casc * nl + lp] = of;
+      flat += of;
       poff += o;
       poff = (poff + 3) & ~uint64_t(3);  // 16-byte alignment of every field (float2/float4 access)
     }
@@ -417,6 +441,8 @@ SampleArrays sample_arrays(dg_ctx* c) {
   sm.t = c->s_t.as<double>();
   sm.delta = c->s_delta.as<double>();
   sm.item = c->s_item.as<uint32_t>();
+  sm.p = c->enc_pcache ? c->s_p.as<double>() : nullptr;
+  sm.pn = uint64_t(c->n_fine) + c->n_coarse;
   sm.X = c->s_X.as<float>();
   sm.out = c->s_out.as<float4>();
   sm.grad = c->s_grad.as<float4>();
@@ -653,6 +679,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   TRY(c->s_t.ensure(NS * 8 + 16));
   TRY(c->s_delta.ensure(NS * 8 + 16));
   TRY(c->s_item.ensure(NS * 4 + 16));
+  if (c->enc_pcache) TRY(c->s_p.ensure(NS * 24 + 16));
   TRY(c->s_X.ensure(NS * kEnc * 4 + 16));
   TRY(c->s_out.ensure(NS * 16 + 16));
   TRY(c->s_grad.ensure(NS * 16 + 16));
@@ -660,7 +687,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   SampleArrays sm = sample_arrays(c);
   launch_march_fill(c->d_parts.as<PartDesc>(), c->occ.as<uint8_t>(), NI, it, sm, c->n_fine,
                     c->step, c->cfg.seed, batch_id, train, s);
-  ++c->launches;
+  c->launches += c->enc_pcache ? 2 : 1;  // march fill (+ sample points)
   // tile tables
   std::vector<uint32_t> tf(2 * nl + 1, 0), tb(2 * nl + 1, 0);
   for (uint32_t f = 0; f < 2 * nl; ++f) {
@@ -677,7 +704,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   return DG_OK;
 }
 
-FieldLaunch field_launch(dg_ctx* c) {
+FieldLaunch field_launch(dg_ctx* c, uint64_t budget) {
   FieldLaunch f{};
   f.fields = c->d_fields.as<FieldDesc>();
   f.parts = c->d_parts.as<PartDesc>();
@@ -689,28 +716,39 @@ FieldLaunch field_launch(dg_ctx* c) {
   f.n_total = c->n_fine + c->n_coarse;
   f.n_local = uint32_t(c->local.size());
   f.levels = c->cfg.grid_levels;
-  // level groups: leading one-to-one levels of the first local fine grid go together (their
-  // tables fit in L2 jointly); aggregation where ~2+ consecutive samples share a cell
-  const FieldDesc& f0 = c->fields[0];
-  uint32_t dense = 0, agg = 0;
-  uint64_t dense_bytes = 0;
-  for (uint32_t l = 0; l < f0.L; ++l) {
-    const uint64_t rows = f0.lv[l].hashed ? uint64_t(f0.lv[l].mask) + 1
-                                          : uint64_t(f0.lv[l].n[0]) * f0.lv[l].n[1] * f0.lv[l].n[2];
-    if (f0.lv[l].hashed || dense_bytes + rows * 8 > (96ull << 20)) break;
-    dense_bytes += rows * 8;
-    ++dense;
+  // Passes: runs of consecutive levels whose tables (summed over the local fields) fit the
+  // slice budget go together; a larger level is cut into S row slices of <= budget each.
+  // Measured on B200 (tools/ubench/l2_random.cu): random float2 gathers / reds run 2.2x /
+  // 3.5x faster on a 64 MB table than on a 128 MB one.
+  auto level_bytes = [&](uint32_t l) {
+    uint64_t b = 0;
+    for (const FieldDesc& fd : c->fields) b += uint64_t(fd.lv[l].rows) * 8;
+    return b;
+  };
+  f.n_pass = 0;
+  for (uint32_t l = 0; l < f.levels;) {
+    uint32_t l1 = l + 1;
+    uint64_t bytes = level_bytes(l);
+    while (l1 < f.levels && bytes + level_bytes(l1) <= budget) bytes += level_bytes(l1++);
+    const uint32_t S = std::min<uint64_t>(8, std::max<uint64_t>(1, (bytes + budget - 1) / budget));
+    for (uint32_t k = 0; k < S && f.n_pass < kMaxEncPass; ++k)
+      f.pass[f.n_pass++] = EncPass{uint8_t(l), uint8_t(l1), uint8_t(k), uint8_t(S)};
+    l = l1;
   }
-  // ~1.5+ samples per cell along a ray: cell = extent / n vs. the march step
+  // warp aggregation where ~1.5+ consecutive samples share a cell: cell = extent / n vs. step
+  const FieldDesc& f0 = c->fields[0];
+  uint32_t agg = 0;
   const double ext = std::max(f0.box_hi[0] - f0.box_lo[0],
                               std::max(f0.box_hi[1] - f0.box_lo[1], f0.box_hi[2] - f0.box_lo[2]));
   const double maxn_agg = ext / (1.5 * c->step);
   for (uint32_t l = 0; l < f0.L; ++l)
     if (double(std::max(f0.lv[l].n[0], std::max(f0.lv[l].n[1], f0.lv[l].n[2]))) <= maxn_agg) agg = l + 1;
-  f.dense_levels = std::max<uint32_t>(dense, 1);
   f.agg_levels = agg;
   f.params = c->params.as<float>();
   f.grads = c->grads.as<float>();
+  f.s_p = c->enc_pcache ? c->s_p.as<double>() : nullptr;
+  f.n_fields = uint32_t(c->field_off.size() - 1);
+  for (size_t i = 0; i < c->field_off.size(); ++i) f.field_off[i] = c->field_off[i];
   return f;
 }
 
@@ -1019,6 +1057,11 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   CU(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   TRY(ctx_setup(c.get()));
   if (const char* e = std::getenv("DG_MLP")) c->mlp_impl = std::strcmp(e, "ffma") == 0 ? 0 : 1;
+  if (const char* e = std::getenv("DG_ENC_FWD_MB"))
+    c->enc_budget_fwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
+  if (const char* e = std::getenv("DG_ENC_PCACHE")) c->enc_pcache = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("DG_ENC_BWD_MB"))
+    c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) CU(cudaEventCreate(&e));
   TRY(ctx_alloc(c.get()));
@@ -1112,9 +1155,11 @@ static int copy_part(dg_ctx* c, uint32_t p, DBuf& buf, float* host, const float*
   uint64_t flat = 0;
   for (int casc = 0; casc < 2; ++casc) {
     float* dev = buf.as<float>() + c->field_dev_off[casc * nl + lp];
-    const size_t bytes = c->field_size[casc * nl + lp] * sizeof(float);
-    if (in) CU(cudaMemcpyAsync(dev, in + flat, bytes, cudaMemcpyHostToDevice, c->stream));
-    else CU(cudaMemcpyAsync(host + flat, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    for (const dg_ctx::Seg& g : c->field_segs[casc * nl + lp]) {
+      const size_t bytes = g.count * sizeof(float);
+      if (in) CU(cudaMemcpyAsync(dev + g.dev, in + flat + g.flat, bytes, cudaMemcpyHostToDevice, c->stream));
+      else CU(cudaMemcpyAsync(host + flat + g.flat, dev + g.dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
     flat += c->field_size[casc * nl + lp];
   }
   CU(cudaStreamSynchronize(c->stream));
@@ -1172,20 +1217,25 @@ int dg_init_params_reference(dg_ctx* c, uint32_t p) {
       return lo + (hi - lo) * (double(eng() >> 11) * 0x1.0p-53);
     };
     const FieldDesc& fd = c->fields[casc * c->local.size() + lp];
-    const uint64_t fb = casc == 0 ? 0 : c->field_size[lp];
+    // flat offsets of this field's arrays (dg_array_desc: kind 0 = level table, 1/3 = weights)
+    auto flat_of = [&](uint32_t kind, uint32_t idx) -> uint64_t {
+      for (const dg_array_desc& a : c->layouts[lp])
+        if (a.cascade == uint32_t(casc) && a.kind == kind && a.index == idx) return a.offset;
+      return 0;
+    };
     for (uint32_t l = 0; l < fd.L; ++l) {
-      const LevelDesc& lv = fd.lv[l];
-      const uint64_t rows = lv.hashed ? uint64_t(lv.mask) + 1 : uint64_t(lv.n[0]) * lv.n[1] * lv.n[2];
-      for (uint64_t k = 0; k < rows * 2; ++k) host[fb + lv.offset + k] = float(uni(-1e-4, 1e-4));
+      const uint64_t off = flat_of(0, l), rows = fd.lv[l].rows;
+      for (uint64_t k = 0; k < rows * 2; ++k) host[off + k] = float(uni(-1e-4, 1e-4));
     }
     const uint32_t enc = fd.L * 2, cin = 31 + fd.app_dim;
     struct L3 {
       uint64_t off;
       uint32_t in, out;
-    } layers[] = {{fd.dw0, enc, 64}, {fd.dw1, 64, 16}, {fd.cw0, cin, 64}, {fd.cw1, 64, 64}, {fd.cw2, 64, 3}};
+    } layers[] = {{flat_of(1, 0), enc, 64}, {flat_of(1, 1), 64, 16}, {flat_of(3, 0), cin, 64},
+                  {flat_of(3, 1), 64, 64}, {flat_of(3, 2), 64, 3}};
     for (const L3& L : layers) {
       const double bound = std::sqrt(6.0 / double(L.in + L.out));
-      for (uint64_t k = 0; k < uint64_t(L.in) * L.out; ++k) host[fb + L.off + k] = float(uni(-bound, bound));
+      for (uint64_t k = 0; k < uint64_t(L.in) * L.out; ++k) host[L.off + k] = float(uni(-bound, bound));
     }
   }
   return dg_set_params(c, p, host.data());
@@ -1305,8 +1355,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   }
   CU(cudaMemsetAsync(c->loss.p, 0, sizeof(LossAccum), s));
   // K3 / K4 forward
-  const FieldLaunch fl = field_launch(c);
-  launch_encode_fwd(fl, sm.X, s);
+  c->launches += launch_encode_fwd(field_launch(c, c->enc_budget_fwd), sm.X, s) - 1;
   mark(c, 3);
   const MlpLaunch mf = mlp_launch(c, false);
   if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);
@@ -1337,7 +1386,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
     launch_mlp_bwd(mlp_launch(c, true), c->num_sms, s);
   }
   mark(c, 8);
-  launch_encode_bwd(fl, sm.dX, s);
+  c->launches += launch_encode_bwd(field_launch(c, c->enc_budget_bwd), sm.dX, s) - 1;
   mark(c, 9);
   c->launches += 3;
   // K6 Adam over every local parameter, lr at the pre-increment step (worker.cpp:544)
@@ -1406,8 +1455,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   const uint32_t NI = c->n_items;
   ItemArrays it = item_arrays(c);
   SampleArrays sm = sample_arrays(c);
-  const FieldLaunch fl = field_launch(c);
-  launch_encode_fwd(fl, sm.X, s);
+  c->launches += launch_encode_fwd(field_launch(c, c->enc_budget_fwd), sm.X, s) - 1;
   MlpLaunch mf = mlp_launch(c, false);
   mf.app_override = c->eval_app.as<float>();
   if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);

@@ -1,7 +1,8 @@
 """Top CUDA source lines by warp-stall samples (ncu source page, cuda+sass correlation)."""
 import csv, subprocess, sys
 rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'cuda,sass'],
+kern = sys.argv[3] if len(sys.argv) > 3 else None
+out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'cuda,sass'] + (['-k', 'regex:' + kern] if kern else []),
                      capture_output=True, text=True).stdout
 fname = None; rows = []
 for r in csv.reader(out.splitlines()):
