@@ -125,7 +125,7 @@ struct dg_ctx {
   std::vector<std::vector<Seg>> field_segs;  // [2][n_local]
   std::vector<std::vector<dg_array_desc>> layouts;
   uint64_t enc_budget_fwd = 256ull << 20;  // encode pass budgets (DG_ENC_FWD_MB / DG_ENC_BWD_MB)
-  uint64_t enc_budget_bwd = 128ull << 20;
+  uint64_t enc_budget_bwd = 96ull << 20;
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
   uint64_t n_params = 0;
   uint64_t occ_bytes = 0;
