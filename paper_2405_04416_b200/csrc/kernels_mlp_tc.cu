@@ -49,8 +49,37 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
-// Write 8 consecutive columns [c0, c0+8) of row r into a split tile with TM rows.
-__device__ __forceinline__ void put8(uint8_t* hi, uint8_t* lo, int r, int c0, const float* v) {
+// TMEM A-operand region (tcgen05.mma A from TMEM, tools/ubench/tmem_a.cu): the next GEMM's
+// activation / gradient tile, hi halves at columns [A_HI, A_HI + K/2), lo at + A_LO_OFF.
+// Reading A from TMEM instead of shared memory removes the 4 KB/MMA smem A-read that bounds
+// a small-N tcgen05.mma at ~39 cycles (11 cycles from TMEM at N = 16; tools/ubench/mma_latency.cu).
+constexpr uint32_t A_HI = 64, A_LO_OFF = 32;
+
+// Destination of an operand tile row: the smem copy (K-major core-matrix layout, hi / lo;
+// null when the tile is consumed only from TMEM) and this thread's lane of the TMEM A region.
+struct Sink {
+  uint8_t* hi;
+  uint8_t* lo;
+  uint32_t ta;  // lane base | A_HI
+};
+
+// Write 8 consecutive columns [c0, c0+8) of row r (split once, stored to both copies).
+// Warp-uniform (tcgen05.st is .sync.aligned).
+__device__ __forceinline__ void put8(const Sink& k, int r, int c0, const float* v) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) split2(v[2 * j], v[2 * j + 1], h[j], l[j]);
+  if (k.hi) {
+    const uint32_t off = tc::core_offset(r, c0, TM);
+    *reinterpret_cast<uint4*>(k.hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(k.lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+  }
+  tc::tmem_st4(k.ta + (uint32_t)(c0 >> 1), h);
+  tc::tmem_st4(k.ta + A_LO_OFF + (uint32_t)(c0 >> 1), l);
+}
+
+// smem-only variant (ones columns, weight-gradient operands that never feed a TMEM-A GEMM).
+__device__ __forceinline__ void put8s(uint8_t* hi, uint8_t* lo, int r, int c0, const float* v) {
   uint32_t h[4], l[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) split2(v[2 * j], v[2 * j + 1], h[j], l[j]);
@@ -106,25 +135,22 @@ __device__ void stage_weights_tc(const FieldDesc& fd, const float* __restrict__ 
   }
 }
 
-// D[TM x N] = A[TM x K] . B[N x K]^T, split-bf16 (3 MMAs per 16-wide K step).
-// A tile rows = TM (K-major, SBO 128, LBO TM/8*128); B tile rows = N (SBO 128, LBO N/8*128).
-// Descriptors are built once; a K step only advances their 14-bit start-address fields
-// (smem offsets < 256 KB never carry out of the field), so issue is back-to-back UTCHMMAs.
+// D[TM x N] = A[TM x K] . B[N x K]^T, split-bf16 (3 MMAs per 16-wide K step), A in the TMEM
+// A region (hi at column a, lo at a + A_LO_OFF; 8 columns per K step), B in smem (K-major,
+// rows = N: SBO 128, LBO N/8*128).  Descriptors are built once; a K step only advances the
+// 14-bit start-address field (smem offsets < 256 KB never carry out of it).
 template <int N, int K>
-__device__ __forceinline__ void gemm_kmajor_t(uint32_t d_tmem, const uint8_t* a_hi, const uint8_t* a_lo,
-                                              const uint8_t* b_hi, const uint8_t* b_lo) {
+__device__ __forceinline__ void gemm_ts(uint32_t d_tmem, uint32_t a, const uint8_t* b_hi, const uint8_t* b_lo) {
   constexpr uint32_t id = tc::idesc_bf16(TM, N, 0, 0);
-  constexpr uint32_t a_lbo = (TM / 8) * 128, b_lbo = (N / 8) * 128;
-  const uint64_t ah = tc::smem_desc(tc::smem_u32(a_hi), a_lbo, 128);
-  const uint64_t al = tc::smem_desc(tc::smem_u32(a_lo), a_lbo, 128);
+  constexpr uint32_t b_lbo = (N / 8) * 128;
   const uint64_t bh = tc::smem_desc(tc::smem_u32(b_hi), b_lbo, 128);
   const uint64_t bl = tc::smem_desc(tc::smem_u32(b_lo), b_lbo, 128);
 #pragma unroll
   for (int k = 0; k < K / 16; ++k) {
-    const uint32_t ao = (k * 2 * a_lbo) >> 4, bo = (k * 2 * b_lbo) >> 4;
-    tc::mma_bf16(d_tmem, ah + ao, bh + bo, id, k > 0 ? 1u : 0u);
-    tc::mma_bf16(d_tmem, ah + ao, bl + bo, id, 1u);
-    tc::mma_bf16(d_tmem, al + ao, bh + bo, id, 1u);
+    const uint32_t bo = (k * 2 * b_lbo) >> 4;
+    tc::mma_bf16_ts(d_tmem, a + 8 * k, bh + bo, id, k > 0 ? 1u : 0u);
+    tc::mma_bf16_ts(d_tmem, a + 8 * k, bl + bo, id, 1u);
+    tc::mma_bf16_ts(d_tmem, a + A_LO_OFF + 8 * k, bh + bo, id, 1u);
   }
 }
 
@@ -231,14 +257,14 @@ struct Pref {
     }
   }
   // Write this part's columns of Cin (raw16 = clipped density output, part 0 only).
-  __device__ __forceinline__ void put_cin(uint8_t* hi, uint8_t* lo, int row, int part, const float* raw) {
+  __device__ __forceinline__ void put_cin(const Sink& k, int row, int part, const float* raw) {
     if (part == 0) {
       float c[16];
 #pragma unroll
       for (int i = 0; i < 15; ++i) c[i] = raw[1 + i];
       c[15] = valid ? kSH0 : 0.f;
-      put8(hi, lo, row, 0, c);
-      put8(hi, lo, row, 8, c + 8);
+      put8(k, row, 0, c);
+      put8(k, row, 8, c + 8);
     }
     if (part == SHP) {
       float c[16];
@@ -249,22 +275,23 @@ struct Pref {
         for (int i = 0; i < 15; ++i) c[i] = 0.f;
       }
       c[15] = app[0];
-      put8(hi, lo, row, 16, c);
-      put8(hi, lo, row, 24, c + 8);
+      put8(k, row, 16, c);
+      put8(k, row, 24, c + 8);
     }
     if (part == APP) {
-      put8(hi, lo, row, 32, app + 1);
-      put8(hi, lo, row, 40, app + 9);
+      put8(k, row, 32, app + 1);
+      put8(k, row, 40, app + 9);
     }
   }
-  __device__ __forceinline__ void put_x(uint8_t* hi, uint8_t* lo, int row, int part) {
+  __device__ __forceinline__ void put_x(const Sink& k, int row, int part) {
 #pragma unroll
-    for (int c = 0; c < XL / 4; ++c) put8(hi, lo, row, part * 2 * XL + 8 * c, x + 8 * c);
+    for (int c = 0; c < XL / 4; ++c) put8(k, row, part * 2 * XL + 8 * c, x + 8 * c);
   }
 };
 
-// Sync point between an epilogue (generic smem writes / TMEM reads) and the next MMA issue.
+// Sync point between an epilogue (generic smem writes, TMEM loads / stores) and the next MMA.
 __device__ __forceinline__ void to_mma() {
+  tc::tmem_wait_st();
   tc::fence_async_smem();
   tc::fence_before();
   __syncthreads();
@@ -289,16 +316,31 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
     }                                   \
   } while (0)
 
+// Critical MMAs, their commit (the next epilogue waits for it), then background MMAs whose
+// completion a later commit covers (commit tracks every earlier tcgen05 op of the thread).
+template <class Crit, class Back>
+__device__ __forceinline__ void issue2(int warp, uint64_t* mbar, Crit crit, Back back) {
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      crit();
+      tc::commit(mbar);
+      back();
+    }
+    __syncwarp();
+  }
+}
+
 struct FwdTcSmem {
   TcWeights w;
-  uint8_t a[2][TM * 64 * 2];  // activation operand (A, K-major), hi / lo
   float sig_raw[TM];
   uint64_t mbar;
   uint32_t tslot;
 };
 
 // Forward: 2 column parts (warps 0-3 / 4-7) x 4 lane quadrants; each thread owns one sample row
-// and 32 of the 64 hidden columns.  Tiles are strided over the grid.
+// and 32 of the 64 hidden columns.  Activations never touch shared memory: each epilogue
+// writes the next layer's split operand straight into the TMEM A region.  TMEM: [0, 64) the
+// accumulator, [64, 128) the A operand.  Tiles are strided over the grid.
 __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
   constexpr int NP = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -306,7 +348,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quad = warp & 3, part = warp >> 2;
   const int row = quad * 32 + lane;  // TMEM lane == sample row of the tile
-  if (warp == 0) tc::tmem_alloc(&sm.tslot, 64);
+  if (warp == 0) tc::tmem_alloc(&sm.tslot, 128);
   if (tid == 0) {
     tc::mbar_init(&sm.mbar, 1);
     tc::fence_mbar_init();
@@ -316,6 +358,8 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
   tc::fence_after();
   const uint32_t tmem = sm.tslot;
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
+  const Sink act{nullptr, nullptr, my_lanes + A_HI};
+  const uint32_t a_op = tmem + A_HI;
   uint32_t phase = 0;
   auto mma_done = [&]() {
     tc::mbar_wait(&sm.mbar, phase);
@@ -331,7 +375,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
     pf.appearance(m, m.fields[cur.f], part);
     stage_weights_tc(m.fields[cur.f], m.params, sm.w);
     int loaded = cur.f;
-    pf.put_x(sm.a[0], sm.a[1], row, part);
+    pf.put_x(act, row, part);
     for (;;) {
       const FieldDesc& fd = m.fields[cur.f];
       const int act_c = fd.coarse ? 2 : 1;
@@ -342,7 +386,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
       const TileGeo nx = has_next ? tile_geo(m, next) : cur;
       to_mma();
       // ---- L1: H1 = relu(X Wd0^T + b) ----
-      ISSUE(gemm_kmajor_t<64, 32>(tmem, sm.a[0], sm.a[1], sm.w.d0[0], sm.w.d0[1]););
+      ISSUE(gemm_ts<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
       float cin_app[17];
 #pragma unroll
       for (int i = 0; i < 17; ++i) cin_app[i] = pf.app[i];
@@ -355,12 +399,12 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
         ld16(my_lanes + part * 32 + 16 * q, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[part * 32 + 16 * q + i], 0.f);
-        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q, v);
-        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q + 8, v + 8);
+        put8(act, row, part * 32 + 16 * q, v);
+        put8(act, row, part * 32 + 16 * q + 8, v + 8);
       }
       to_mma();
       // ---- L2: raw16 = H1 Wd1^T + b ; Cin = [clip(raw1..15) | SH16 | app | 0] ----
-      ISSUE(gemm_kmajor_t<16, 64>(tmem, sm.a[0], sm.a[1], sm.w.d1[0], sm.w.d1[1]););
+      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]));
       mma_done();
       {
         float raw[16];
@@ -378,12 +422,12 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
         cp.dir[2] = d2;
 #pragma unroll
         for (int i = 0; i < 17; ++i) cp.app[i] = cin_app[i];
-        cp.put_cin(sm.a[0], sm.a[1], row, part, raw);
+        cp.put_cin(act, row, part, raw);
       }
       pf.rec(m, part);  // next tile's RayRec (item arrived during L1/L2)
       to_mma();
       // ---- L3: C1 = act(Cin Wc0^T + b) ----
-      ISSUE(gemm_kmajor_t<64, 48>(tmem, sm.a[0], sm.a[1], sm.w.c0[0], sm.w.c0[1]););
+      ISSUE(gemm_ts<64, 48>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]));
       mma_done();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -394,12 +438,12 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
           const float z = v[i] + sm.w.bc0[part * 32 + 16 * q + i];
           v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
         }
-        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q, v);
-        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q + 8, v + 8);
+        put8(act, row, part * 32 + 16 * q, v);
+        put8(act, row, part * 32 + 16 * q + 8, v + 8);
       }
       to_mma();
       // ---- L4: C2 = act(C1 Wc1^T + b) ----
-      ISSUE(gemm_kmajor_t<64, 64>(tmem, sm.a[0], sm.a[1], sm.w.c1[0], sm.w.c1[1]););
+      ISSUE(gemm_ts<64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]));
       mma_done();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -410,13 +454,13 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
           const float z = v[i] + sm.w.bc1[part * 32 + 16 * q + i];
           v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
         }
-        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q, v);
-        put8(sm.a[0], sm.a[1], row, part * 32 + 16 * q + 8, v + 8);
+        put8(act, row, part * 32 + 16 * q, v);
+        put8(act, row, part * 32 + 16 * q + 8, v + 8);
       }
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
       to_mma();
       // ---- L5: rgb = sigmoid(clip(C2 Wc2^T + b)) ----
-      ISSUE(gemm_kmajor_t<16, 64>(tmem, sm.a[0], sm.a[1], sm.w.c2[0], sm.w.c2[1]););
+      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
       mma_done();
       if (part == 0) {
         float v[16];
@@ -431,14 +475,14 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
         stage_weights_tc(m.fields[nx.f], m.params, sm.w);
         loaded = nx.f;
       }
-      pf.put_x(sm.a[0], sm.a[1], row, part);  // the A tile is free: every MMA has completed
+      pf.put_x(act, row, part);  // the A region is free: every MMA has completed
       tile = next;
       cur = nx;
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free(tmem, 64);
+  if (warp == 0) tc::tmem_free(tmem, 128);
 }
 
 
@@ -450,12 +494,18 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
 //   B4  G2  = [sigma path, clip-masked dCin[0..14]]       dWd1 += G2^T H1 ; dH1 = G2 Wd1
 //   B5  G1  = dH1 * relu'(H1)                             dWd0 += G1^T X  ; dX = G1 Wd0
 //   B6  dX -> global (level-major), for the hash-grid backward.
-// The weight gradients dW = G^T A are M=64 tcgen05 GEMMs over K = 128 samples that read the
-// G and A tiles through MN-major descriptors (no transposed copies) and accumulate in TMEM for
-// every tile a CTA processes; each activation tile carries an extra ones column so the same
-// GEMM yields the bias gradient.  TMEM is flushed with one atomicAdd per weight per CTA.
+// Input-gradient GEMMs (dC2, ...) take G from the TMEM A region.  The weight gradients
+// dW = G^T A are M=64 tcgen05 GEMMs over K = 128 samples reading the G and activation tiles
+// in smem through MN-major descriptors (no transposed copies); bias gradients are G^T . 1
+// against a constant ones tile.  Both accumulate in TMEM over every tile a CTA processes and
+// are flushed with one atomicAdd per weight per CTA.
+// Weight-gradient GEMMs are off the critical path: a stage issues its input-gradient GEMM,
+// commits (the next epilogue waits only for that), then issues the weight-gradient GEMMs.  The
+// G tiles rotate through buffers no in-flight weight-gradient GEMM reads:
+//   G5 -> g5, G4 -> s, G3 -> c2, G2 -> s, G1 -> c2,  and the next tile's x reaches smem only at
+//   its first epilogue (the previous tile's dWd0 GEMM reads x).
 // 16 warps: 4 lane quadrants x 4 column parts, so every epilogue is 16 columns per thread.
-constexpr int XW = 40, HW = 72, CW = 56;  // tile widths incl. the ones chunk
+constexpr int XW = 32, HW = 64, CW = 48;  // activation tile widths
 
 struct BwdTcSmem {
   TcWeights w;
@@ -465,6 +515,8 @@ struct BwdTcSmem {
   uint8_t cin[2][TM * CW * 2];
   uint8_t c1[2][TM * HW * 2];
   uint8_t c2[2][TM * HW * 2];
+  uint8_t s[2][TM * 64 * 2];   // G4 / G2
+  uint8_t ones[TM * 8 * 2];    // bias-gradient B operand: column 0 = 1
   float sig_raw[TM];
   float gsig[TM];
   uint32_t dmask[TM];
@@ -472,8 +524,12 @@ struct BwdTcSmem {
   uint32_t tslot;
 };
 
-// TMEM columns: [0,64) transient accumulator; dW accumulators (M = 64 rows = out features).
-constexpr uint32_t TD_C2 = 128, TD_C1 = 200, TD_C0 = 272, TD_D1 = 328, TD_D0 = 400;
+static_assert(sizeof(BwdTcSmem) <= 232448, "backward tile set exceeds 227 KB of shared memory");
+
+// TMEM columns: [0,64) accumulator, [64,128) A operand; dW accumulators (M = 64 rows = out
+// features, row o at lane (o % 16) + 32 (o / 16)); bias accumulators (column 0 of 8).
+constexpr uint32_t TD_C2 = 128, TD_C1 = 192, TD_C0 = 256, TD_D1 = 304, TD_D0 = 368;
+constexpr uint32_t TB_C2 = 400, TB_C1 = 408, TB_C0 = 416, TB_D1 = 424, TB_D0 = 432;
 
 // D (M=64 x N) (+)= G^T A over K = TM samples; G tile (TM x >=64 cols span), A tile (TM x N);
 // both read MN-major (SBO = TM/8*128, LBO = 128).
@@ -496,44 +552,63 @@ __device__ __forceinline__ void gemm_wgrad(uint32_t d_tmem, const uint8_t* g_hi,
   }
 }
 
-// D (TM x N) = G W : G tile K-major [TM x K=out], W tile stored [Wrows=out x cols=in]
-// read MN-major (SBO = Wrows/8*128, LBO = 128); N = number of leading input columns.
+// Bias gradient D (M=64 x 8) (+)= G^T . ones (column 0 of the ones tile): 2 MMAs per K step
+// (ones are exact in bf16, so G_hi . 1 + G_lo . 1).
+__device__ __forceinline__ void gemm_bias(uint32_t d_tmem, const uint8_t* g_hi, const uint8_t* g_lo,
+                                          const uint8_t* ones, bool accumulate) {
+  constexpr uint32_t id = tc::idesc_bf16(64, 8, 1, 1);
+  constexpr uint32_t SBO = (TM / 8) * 128;
+  const uint64_t gh = tc::smem_desc(tc::smem_u32(g_hi), 128, SBO);
+  const uint64_t gl = tc::smem_desc(tc::smem_u32(g_lo), 128, SBO);
+  const uint64_t on = tc::smem_desc(tc::smem_u32(ones), 128, SBO);
+  const uint32_t acc0 = accumulate ? 1u : 0u;
+#pragma unroll
+  for (int k = 0; k < TM / 16; ++k) {
+    const uint32_t o = (k * 256) >> 4;
+    tc::mma_bf16(d_tmem, gh + o, on + o, id, k > 0 ? 1u : acc0);
+    tc::mma_bf16(d_tmem, gl + o, on + o, id, 1u);
+  }
+}
+
+// D (TM x N) = G W : G in the TMEM A region [TM x K=out], W tile stored [Wrows=out x cols=in]
+// in smem read MN-major (SBO = Wrows/8*128, LBO = 128); N = number of leading input columns.
 template <int Wrows, int N, int K>
-__device__ __forceinline__ void gemm_igrad(uint32_t d_tmem, const uint8_t* g_hi, const uint8_t* g_lo,
-                                           const uint8_t* w_hi, const uint8_t* w_lo) {
+__device__ __forceinline__ void gemm_igrad(uint32_t d_tmem, uint32_t a, const uint8_t* w_hi,
+                                           const uint8_t* w_lo) {
   constexpr uint32_t id = tc::idesc_bf16(TM, N, 0, 1);
-  constexpr uint32_t G_LBO = (TM / 8) * 128, W_SBO = (uint32_t)(Wrows / 8) * 128;
-  const uint64_t gh = tc::smem_desc(tc::smem_u32(g_hi), G_LBO, 128);
-  const uint64_t gl = tc::smem_desc(tc::smem_u32(g_lo), G_LBO, 128);
+  constexpr uint32_t W_SBO = (uint32_t)(Wrows / 8) * 128;
   const uint64_t wh = tc::smem_desc(tc::smem_u32(w_hi), 128, W_SBO);
   const uint64_t wl = tc::smem_desc(tc::smem_u32(w_lo), 128, W_SBO);
 #pragma unroll
   for (int k = 0; k < K / 16; ++k) {
-    const uint32_t go = (k * 2 * G_LBO) >> 4, wo = (k * 256) >> 4;
-    tc::mma_bf16(d_tmem, gh + go, wh + wo, id, k > 0 ? 1u : 0u);
-    tc::mma_bf16(d_tmem, gh + go, wl + wo, id, 1u);
-    tc::mma_bf16(d_tmem, gl + go, wh + wo, id, 1u);
+    const uint32_t wo = (k * 256) >> 4;
+    tc::mma_bf16_ts(d_tmem, a + 8 * k, wh + wo, id, k > 0 ? 1u : 0u);
+    tc::mma_bf16_ts(d_tmem, a + 8 * k, wl + wo, id, 1u);
+    tc::mma_bf16_ts(d_tmem, a + A_LO_OFF + 8 * k, wh + wo, id, 1u);
   }
 }
 
-// One dW accumulator (M=64 layout: row o in TMEM lane (o % 16) + 32 (o / 16)) -> atomics.
-// Columns [0, in) are dW, column `ones` (the ones chunk) is the bias gradient.
-__device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, int ones, float* gW,
+// One dW accumulator (M=64 layout: row o in TMEM lane (o % 16) + 32 (o / 16)) -> atomics:
+// columns [0, in) of col0 are dW, column 0 of bcol is the bias gradient.
+__device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, uint32_t bcol, float* gW,
                          float* gb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int quad = warp & 3, part = warp >> 2, parts = (int)(blockDim.x >> 7);
   const int o = quad * 16 + lane;
-  for (int g = part; g < N / 8; g += parts) {
+  const uint32_t lanes = tmem + ((uint32_t)(quad * 32) << 16);
+  for (int g = part; g <= N / 8; g += parts) {
     float v[8];
-    tc::tmem_ld8(tmem + ((uint32_t)(quad * 32) << 16) + col0 + 8 * g, v);
+    tc::tmem_ld8(lanes + (g < N / 8 ? col0 + 8 * g : bcol), v);
     tc::tmem_wait_ld();
     if (lane < 16 && o < out) {
+      if (g == N / 8) {
+        if (v[0] != 0.f) atomicAdd(gb + o, v[0]);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int i = 8 * g + j;
-        if (v[j] == 0.f) continue;
-        if (i < in) atomicAdd(gW + o * in + i, v[j]);
-        else if (i == ones) atomicAdd(gb + o, v[j]);
+        for (int j = 0; j < 8; ++j) {
+          const int i = 8 * g + j;
+          if (i < in && v[j] != 0.f) atomicAdd(gW + o * in + i, v[j]);
+        }
       }
     }
   }
@@ -542,27 +617,24 @@ __device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, i
 __device__ void flush_all(uint32_t tmem, const FieldDesc& fd, float* __restrict__ grads) {
   float* base = grads + fd.base;
   const int enc = (int)fd.L * 2, cin = 31 + (int)fd.app_dim;
-  flush_dw(tmem, TD_C2, HW, 3, 64, 64, base + fd.cw2, base + fd.cb2);
-  flush_dw(tmem, TD_C1, HW, 64, 64, 64, base + fd.cw1, base + fd.cb1);
-  flush_dw(tmem, TD_C0, CW, 64, cin, 48, base + fd.cw0, base + fd.cb0);
-  flush_dw(tmem, TD_D1, HW, 16, 64, 64, base + fd.dw1, base + fd.db1);
-  flush_dw(tmem, TD_D0, XW, 64, enc, 32, base + fd.dw0, base + fd.db0);
+  flush_dw(tmem, TD_C2, HW, 3, 64, TB_C2, base + fd.cw2, base + fd.cb2);
+  flush_dw(tmem, TD_C1, HW, 64, 64, TB_C1, base + fd.cw1, base + fd.cb1);
+  flush_dw(tmem, TD_C0, CW, 64, cin, TB_C0, base + fd.cw0, base + fd.cb0);
+  flush_dw(tmem, TD_D1, HW, 16, 64, TB_D1, base + fd.dw1, base + fd.db1);
+  flush_dw(tmem, TD_D0, XW, 64, enc, TB_D0, base + fd.dw0, base + fd.db0);
 }
 
-__device__ __forceinline__ void ones_chunk(uint8_t* hi, uint8_t* lo, int c0) {
-  float v[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int r = threadIdx.x; r < TM; r += blockDim.x) put8(hi, lo, r, c0, v);
-}
-
-// act'(a) * dv for 16 columns of row r of tile (hi, lo), written back in place as G.
-__device__ __forceinline__ void grad_act16(uint8_t* hi, uint8_t* lo, int r, int c0, float* v, int act) {
+// G = act'(a) * dv for 16 columns of row r; a is read back from the activation tile (hi, lo),
+// G goes to `out` (its smem tile for the weight gradient + the TMEM A region).
+__device__ __forceinline__ void grad_act16(const uint8_t* a_hi, const uint8_t* a_lo, const Sink& out,
+                                           int r, int c0, float* v, int act) {
   float a[16];
-  get8(hi, lo, r, c0, a);
-  get8(hi, lo, r, c0 + 8, a + 8);
+  get8(a_hi, a_lo, r, c0, a);
+  get8(a_hi, a_lo, r, c0 + 8, a + 8);
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] *= act == 2 ? a[i] * (1.f - a[i]) : (a[i] > 0.f ? 1.f : 0.f);
-  put8(hi, lo, r, c0, v);
-  put8(hi, lo, r, c0 + 8, v + 8);
+  put8(out, r, c0, v);
+  put8(out, r, c0 + 8, v + 8);
 }
 
 __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
@@ -578,21 +650,20 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
     tc::mbar_init(&sm.mbar, 1);
     tc::fence_mbar_init();
   }
-  // ones columns (bias gradients through the dW GEMMs); never overwritten below
-  ones_chunk(sm.x[0], sm.x[1], 32);
-  ones_chunk(sm.h1[0], sm.h1[1], 64);
-  ones_chunk(sm.cin[0], sm.cin[1], 48);
-  ones_chunk(sm.c1[0], sm.c1[1], 64);
-  ones_chunk(sm.c2[0], sm.c2[1], 64);
-  for (int e = tid; e < TM * 16 * 2 / 4; e += NTB) {  // G5 columns 3..15 stay zero
-    reinterpret_cast<uint32_t*>(sm.g5[0])[e] = 0u;
-    reinterpret_cast<uint32_t*>(sm.g5[1])[e] = 0u;
-  }
+  // ones tile (bias-gradient B operand, MN-major [K = 128 samples x N = 8]): column 0 = 1
+  for (int r = tid; r < TM; r += NTB)
+    *reinterpret_cast<uint4*>(sm.ones + tc::core_offset(r, 0, TM)) = make_uint4(0x3f80u, 0u, 0u, 0u);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = sm.tslot;
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
+  const uint32_t a_op = tmem + A_HI, ta = my_lanes + A_HI;
+  // operand tiles: smem copy (weight-gradient GEMMs) + TMEM A region (the next GEMM)
+  const Sink sxt{nullptr, nullptr, ta}, sh1{sm.h1[0], sm.h1[1], ta}, scin{sm.cin[0], sm.cin[1], ta};
+  const Sink sc1{sm.c1[0], sm.c1[1], ta}, sc2{sm.c2[0], sm.c2[1], ta}, sg5{sm.g5[0], sm.g5[1], ta};
+  const Sink ss{sm.s[0], sm.s[1], ta};
+  float xk[8];  // this tile's X chunk: TMEM A at once, the smem copy at the first epilogue
   uint32_t phase = 0;
 #ifdef DG_TRACE_MLP
   // phase clocks of CTA 0 (threads 0 and 480): per stage [barrier entry, barrier exit, MMA done]
@@ -630,7 +701,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
     stage_weights_tc(m.fields[cur.f], m.params, sm.w);
     loaded = cur.f;
     bool fresh = true;  // next dW GEMMs start a new accumulation
-    pf.put_x(sm.x[0], sm.x[1], row, part);
+    pf.put_x(sxt, row, part);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xk[i] = pf.x[i];
     for (;;) {
       const FieldDesc& fd = m.fields[cur.f];
       const int act_c = fd.coarse ? 2 : 1;
@@ -646,20 +719,21 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
       const float4 up = pf.g;
       sync_mma();
-      // ---------------- forward recompute ----------------
-      ISSUE(gemm_kmajor_t<64, 32>(tmem, sm.x[0], sm.x[1], sm.w.d0[0], sm.w.d0[1]););
+      // ---------------- forward recompute (A operands from TMEM) ----------------
+      ISSUE(gemm_ts<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
       pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next: X, item
       mma_done();
       {
+        put8s(sm.x[0], sm.x[1], row, part * 8, xk);  // the previous tile's dWd0 GEMM is done
         float v[16];
         ld16(my_lanes + c16, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[c16 + i], 0.f);
-        put8(sm.h1[0], sm.h1[1], row, c16, v);
-        put8(sm.h1[0], sm.h1[1], row, c16 + 8, v + 8);
+        put8(sh1, row, c16, v);
+        put8(sh1, row, c16 + 8, v + 8);
       }
       sync_mma();
-      ISSUE(gemm_kmajor_t<16, 64>(tmem, sm.h1[0], sm.h1[1], sm.w.d1[0], sm.w.d1[1]););
+      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]));
       mma_done();
       {
         float raw[16];
@@ -682,10 +756,10 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         cp.dir[2] = d2;
 #pragma unroll
         for (int i = 0; i < 17; ++i) cp.app[i] = cur_app[i];
-        cp.put_cin(sm.cin[0], sm.cin[1], row, part, raw);
+        cp.put_cin(scin, row, part, raw);
       }
       sync_mma();
-      ISSUE(gemm_kmajor_t<64, 48>(tmem, sm.cin[0], sm.cin[1], sm.w.c0[0], sm.w.c0[1]););
+      ISSUE(gemm_ts<64, 48>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]));
       mma_done();
       {
         float v[16];
@@ -695,12 +769,12 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
           const float z = v[i] + sm.w.bc0[c16 + i];
           v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
         }
-        put8(sm.c1[0], sm.c1[1], row, c16, v);
-        put8(sm.c1[0], sm.c1[1], row, c16 + 8, v + 8);
+        put8(sc1, row, c16, v);
+        put8(sc1, row, c16 + 8, v + 8);
       }
       pf.rec(m, part);  // next tile's RayRec
       sync_mma();
-      ISSUE(gemm_kmajor_t<64, 64>(tmem, sm.c1[0], sm.c1[1], sm.w.c1[0], sm.w.c1[1]););
+      ISSUE(gemm_ts<64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]));
       mma_done();
       {
         float v[16];
@@ -710,18 +784,20 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
           const float z = v[i] + sm.w.bc1[c16 + i];
           v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
         }
-        put8(sm.c2[0], sm.c2[1], row, c16, v);
-        put8(sm.c2[0], sm.c2[1], row, c16 + 8, v + 8);
+        put8(sc2, row, c16, v);
+        put8(sc2, row, c16 + 8, v + 8);
       }
       sync_mma();
-      ISSUE(gemm_kmajor_t<16, 64>(tmem, sm.c2[0], sm.c2[1], sm.w.c2[0], sm.w.c2[1]););
+      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
       mma_done();
       // ---------------- B1: colour head adjoint (field.cpp:298-306) ----------------
       if (part == 0) {
         float v[16];
         ld16(my_lanes, v);
         const float ug[3] = {up.y, up.z, up.w};
-        float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float g[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) g[k] = 0.f;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           const float z = v[k] + sm.w.bc2[k];
@@ -729,37 +805,41 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
           const float sg = sigm(clip15(z));
           g[k] = clipped ? 0.f : ug[k] * sg * (1.f - sg);
         }
-        put8(sm.g5[0], sm.g5[1], row, 0, g);
+        put8(sg5, row, 0, g);
+        put8(sg5, row, 8, g + 8);
         // sigma path of the density raw gradient (field.cpp:313)
         sm.gsig[row] = (sm.dmask[row] & 1u) ? 0.f : up.x * expf(sm.sig_raw[row]);
       }
       pf.grad(m, part);  // next tile's upstream gradient
       sync_mma();
-      ISSUE(gemm_wgrad<HW>(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], !fresh);
-        gemm_igrad<16, 64, 16>(tmem, sm.g5[0], sm.g5[1], sm.w.c2[0], sm.w.c2[1]););
+      issue2(warp, &sm.mbar, [&] { gemm_igrad<16, 64, 16>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]); },
+             [&] { gemm_wgrad<HW>(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], !fresh);
+                    gemm_bias(tmem + TB_C2, sm.g5[0], sm.g5[1], sm.ones, !fresh); });
       mma_done();
-      // ---------------- B2: G4 = dC2 * act'(C2) -> c2 tile ----------------
+      // ---------------- B2: G4 = dC2 * act'(C2) -> s ----------------
       {
         float v[16];
         ld16(my_lanes + c16, v);
-        grad_act16(sm.c2[0], sm.c2[1], row, c16, v, act_c);
+        grad_act16(sm.c2[0], sm.c2[1], ss, row, c16, v, act_c);
       }
       sync_mma();
-      ISSUE(gemm_wgrad<HW>(tmem + TD_C1, sm.c2[0], sm.c2[1], sm.c1[0], sm.c1[1], !fresh);
-        gemm_igrad<64, 64, 64>(tmem, sm.c2[0], sm.c2[1], sm.w.c1[0], sm.w.c1[1]););
+      issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]); },
+             [&] { gemm_wgrad<HW>(tmem + TD_C1, sm.s[0], sm.s[1], sm.c1[0], sm.c1[1], !fresh);
+                    gemm_bias(tmem + TB_C1, sm.s[0], sm.s[1], sm.ones, !fresh); });
       mma_done();
-      // ---------------- B3: G3 = dC1 * act'(C1) -> c1 tile ----------------
+      // ---------------- B3: G3 = dC1 * act'(C1) -> c2 ----------------
       {
         float v[16];
         ld16(my_lanes + c16, v);
-        grad_act16(sm.c1[0], sm.c1[1], row, c16, v, act_c);
+        grad_act16(sm.c1[0], sm.c1[1], sc2, row, c16, v, act_c);
       }
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
       sync_mma();
-      ISSUE(gemm_wgrad<CW>(tmem + TD_C0, sm.c1[0], sm.c1[1], sm.cin[0], sm.cin[1], !fresh);
-        gemm_igrad<64, 16, 64>(tmem, sm.c1[0], sm.c1[1], sm.w.c0[0], sm.w.c0[1]););
+      issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 16, 64>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]); },
+             [&] { gemm_wgrad<CW>(tmem + TD_C0, sm.c2[0], sm.c2[1], sm.cin[0], sm.cin[1], !fresh);
+                    gemm_bias(tmem + TB_C0, sm.c2[0], sm.c2[1], sm.ones, !fresh); });
       mma_done();
-      // ---------------- B4: G2 = density raw gradient -> cin tile cols 0..15 ----------------
+      // ---------------- B4: G2 = density raw gradient -> s cols 0..15 ----------------
       if (part == 0) {
         float v[16];
         ld16(my_lanes, v);
@@ -768,22 +848,24 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         g[0] = sm.gsig[row];
 #pragma unroll
         for (int k = 1; k < 16; ++k) g[k] = ((mask >> k) & 1u) ? 0.f : v[k - 1];
-        put8(sm.cin[0], sm.cin[1], row, 0, g);
-        put8(sm.cin[0], sm.cin[1], row, 8, g + 8);
+        put8(ss, row, 0, g);
+        put8(ss, row, 8, g + 8);
       }
       sync_mma();
-      ISSUE(gemm_wgrad<HW>(tmem + TD_D1, sm.cin[0], sm.cin[1], sm.h1[0], sm.h1[1], !fresh);
-        gemm_igrad<16, 64, 16>(tmem, sm.cin[0], sm.cin[1], sm.w.d1[0], sm.w.d1[1]););
+      issue2(warp, &sm.mbar, [&] { gemm_igrad<16, 64, 16>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]); },
+             [&] { gemm_wgrad<HW>(tmem + TD_D1, sm.s[0], sm.s[1], sm.h1[0], sm.h1[1], !fresh);
+                    gemm_bias(tmem + TB_D1, sm.s[0], sm.s[1], sm.ones, !fresh); });
       mma_done();
-      // ---------------- B5: G1 = dH1 * relu'(H1) -> h1 tile ----------------
+      // ---------------- B5: G1 = dH1 * relu'(H1) -> c2 ----------------
       {
         float v[16];
         ld16(my_lanes + c16, v);
-        grad_act16(sm.h1[0], sm.h1[1], row, c16, v, 1);
+        grad_act16(sm.h1[0], sm.h1[1], sc2, row, c16, v, 1);
       }
       sync_mma();
-      ISSUE(gemm_wgrad<XW>(tmem + TD_D0, sm.h1[0], sm.h1[1], sm.x[0], sm.x[1], !fresh);
-        gemm_igrad<64, 32, 64>(tmem, sm.h1[0], sm.h1[1], sm.w.d0[0], sm.w.d0[1]););
+      issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 32, 64>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]); },
+             [&] { gemm_wgrad<XW>(tmem + TD_D0, sm.c2[0], sm.c2[1], sm.x[0], sm.x[1], !fresh);
+                    gemm_bias(tmem + TB_D0, sm.c2[0], sm.c2[1], sm.ones, !fresh); });
       mma_done();
       fresh = false;
       // ---------------- B6: dX -> global, level-major; next tile's X into the x tile ----------------
@@ -805,6 +887,13 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       ++tr_tile;
       tr_pt = 0;
 #endif
+      if (!has_next || nx.f != loaded) {  // the weight-gradient GEMMs must land before a flush
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        issue2(warp, &sm.mbar, [] {}, [] {});
+        mma_done();
+      }
       if (!has_next) break;
       if (nx.f != loaded) {
         flush_all(tmem, m.fields[loaded], m.grads);
@@ -815,7 +904,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         loaded = nx.f;
         fresh = true;
       }
-      pf.put_x(sm.x[0], sm.x[1], row, part);  // x tile is free: the D0 weight GEMM completed
+      pf.put_x(sxt, row, part);  // A region is free (the dX GEMM completed); smem x at F1
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xk[i] = pf.x[i];
       tile = next;
       cur = nx;
     }
@@ -847,7 +938,7 @@ void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
 void launch_mlp_bwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
   if (!m.n_tiles) return;
   static bool attr = false;
-  const int smem = (int)sizeof(BwdTcSmem) + 1024;
+  const int smem = (int)sizeof(BwdTcSmem);  // no-swizzle operands need 16-byte alignment only
   if (!attr) {
     cudaFuncSetAttribute(k_mlp_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;

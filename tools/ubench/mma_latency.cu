@@ -6,6 +6,13 @@
 #include "../../paper_2405_04416_b200/csrc/tc.cuh"
 using namespace dg;
 
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d), "r"(a_tmem), "l"(b),
+      "r"(idesc), "r"(acc));
+}
+
 __global__ void k_lat(unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t mbar;
@@ -26,7 +33,7 @@ __global__ void k_lat(unsigned long long* out) {
   int o = 0;
   for (int ni = 0; ni < 3; ++ni) {
     const uint32_t id = tc::idesc_bf16(128, Ns[ni], 0, 0);
-    for (int mode = 0; mode < 2; ++mode) {       // 0: dependent chain, 1: independent accumulators
+    for (int mode = 0; mode < 3; ++mode) {       // 0: chain, 1: independent accumulators, 2: chain, A in TMEM
       for (int cnt = 1; cnt <= 32; cnt *= 2) {
         unsigned long long best = ~0ull;
         for (int rep = 0; rep < 5; ++rep) {
@@ -34,8 +41,10 @@ __global__ void k_lat(unsigned long long* out) {
           const unsigned long long t0 = clock64();
           if (warp == 0) {
             if (tc::elect_one()) {
-              for (int i = 0; i < cnt; ++i)
-                tc::mma_bf16(tmem + (mode ? (uint32_t)((i % 4) * 128) : 0u), a, b, id, i > 0 ? 1u : 0u);
+              for (int i = 0; i < cnt; ++i) {
+                if (mode == 2) mma_ts(tmem, tmem + 256, b, id, i > 0 ? 1u : 0u);
+                else tc::mma_bf16(tmem + (mode ? (uint32_t)((i % 4) * 64) : 0u), a, b, id, i > 0 ? 1u : 0u);
+              }
               tc::commit(&mbar);
             }
             __syncwarp();
@@ -57,17 +66,17 @@ __global__ void k_lat(unsigned long long* out) {
 
 int main() {
   unsigned long long* d;
-  cudaMalloc(&d, 64 * 8);
+  cudaMalloc(&d, 64 * 8); cudaMemset(d, 0, 64 * 8);
   cudaFuncSetAttribute(k_lat, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
   k_lat<<<1, 128, 80 * 1024>>>(d);
-  unsigned long long h[64];
+  unsigned long long h[64] = {};
   cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   const int Ns[3] = {16, 64, 128};
   int o = 0;
   for (int ni = 0; ni < 3; ++ni)
-    for (int mode = 0; mode < 2; ++mode) {
-      printf("N=%3d %s:", Ns[ni], mode ? "indep" : "chain");
+    for (int mode = 0; mode < 3; ++mode) {
+      printf("N=%3d %s:", Ns[ni], mode == 2 ? "ts-ch" : mode ? "indep" : "chain");
       for (int cnt = 1; cnt <= 32; cnt *= 2) printf("  %2d:%5llu", cnt, h[o++]);
       printf("\n");
     }
