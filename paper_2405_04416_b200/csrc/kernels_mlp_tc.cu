@@ -179,6 +179,19 @@ __device__ __forceinline__ void sh15(float x, float y, float z, float* o) {
 }
 constexpr float kSH0 = 0.28209479177387814f;
 
+// Colour-MLP hidden activation of 16 pre-activations z = v + b (field.cpp:196-199: sigmoid in
+// the coarse field, ReLU in the fine one).  The branch is uniform, so a ReLU tile never pays
+// for the two SFU ops of the sigmoid.
+__device__ __forceinline__ void act16(float* v, const float* b, int act) {
+  if (act == 2) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = sigm(v[i] + b[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + b[i], 0.f);
+  }
+}
+
 struct TileGeo {
   int f;
   uint64_t s0;
@@ -433,11 +446,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
       for (int q = 0; q < 2; ++q) {
         float v[16];
         ld16(my_lanes + part * 32 + 16 * q, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float z = v[i] + sm.w.bc0[part * 32 + 16 * q + i];
-          v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
-        }
+        act16(v, sm.w.bc0 + part * 32 + 16 * q, act_c);
         put8(act, row, part * 32 + 16 * q, v);
         put8(act, row, part * 32 + 16 * q + 8, v + 8);
       }
@@ -449,11 +458,7 @@ __global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
       for (int q = 0; q < 2; ++q) {
         float v[16];
         ld16(my_lanes + part * 32 + 16 * q, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float z = v[i] + sm.w.bc1[part * 32 + 16 * q + i];
-          v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
-        }
+        act16(v, sm.w.bc1 + part * 32 + 16 * q, act_c);
         put8(act, row, part * 32 + 16 * q, v);
         put8(act, row, part * 32 + 16 * q + 8, v + 8);
       }
