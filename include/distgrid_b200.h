@@ -215,6 +215,20 @@ typedef int (*dg_alltoallv_fn)(void* user, const void* send, const uint64_t* sen
                                 void* recv, const uint64_t* recv_bytes);
 int dg_comm_init_host(dg_ctx* ctx, dg_alltoallv_fn fn, void* user);
 
+/* ---- exchange planning (host only, no context or device needed) ----
+ * The layouts both per-step exchanges use (exchange_plan.h), exported so multi-process tests
+ * can check the protocol on CPU.  Partition p lives on rank p % world.
+ * dg_plan_dispatch: send_cnt[P] records this rank sends to each partition, cnt_recv[W*P] the
+ * count vectors of every rank -> send/recv bytes per rank (72-byte records), item_off[nl+1]
+ * of the local partitions, and the W*nl block permutation recv [src][lp] -> items [lp][src].
+ * dg_plan_partials: pair_cnt[nl*P] (items of local lq whose schedule contains p) -> P*P
+ * stream offsets (records) and send/recv bytes per rank (24-byte records). */
+int dg_plan_dispatch(int rank, int world, uint32_t P, const uint64_t* send_cnt, const uint64_t* cnt_recv,
+                     uint64_t* send_bytes, uint64_t* recv_bytes, uint32_t* item_off, uint64_t* block_src,
+                     uint64_t* block_dst);
+int dg_plan_partials(int rank, int world, uint32_t P, const uint32_t* pair_cnt, uint64_t* send_off,
+                     uint64_t* recv_off, uint64_t* send_bytes, uint64_t* recv_bytes);
+
 /* ---- stage entry points (per-stage parity + the facade's batched overloads) ---- */
 /* segment_ray over a batch (partition.cpp:254-296, geometry.cpp:7-28): nseg per ray,
  * region/t_enter/t_exit in n x DG_MAX_SEGMENTS slots.  Bit-exact fp64. */

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "comm.h"
+#include "exchange_plan.h"
 #include "geometry.cuh"
 #include "kernels.h"
 
@@ -574,45 +575,19 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
     CU(cudaStreamSynchronize(s));
     c->h2d += cnt_send.size() * 8;
     c->d2h += cnt_recv.size() * 8;
-    // cnt_recv[src][p]: records src sends to partition p
-    std::vector<uint64_t> sbytes(W, 0), rbytes(W, 0);
-    for (uint32_t p = 0; p < P; ++p) sbytes[c->part_rank[p]] += send_cnt[p] * sizeof(RayRec);
-    for (int r = 0; r < W; ++r)
-      for (uint32_t lp = 0; lp < nl; ++lp) rbytes[r] += cnt_recv[uint64_t(r) * P + c->local[lp]] * sizeof(RayRec);
-    uint64_t rtotal = 0;
-    for (int r = 0; r < W; ++r) rtotal += rbytes[r];
-    n_items = rtotal / sizeof(RayRec);
-    TRY(c->x_recv.ensure(rtotal + 16));
-    rc = c->comm->alltoallv(c->x_send.p, sbytes, c->x_recv.p, rbytes, s, err);
+    // cnt_recv[src][p]: records src sends to partition p -> layouts (exchange_plan.cpp)
+    DispatchPlan plan;
+    plan_dispatch(c->rank, W, P, send_cnt.data(), cnt_recv.data(), sizeof(RayRec), plan);
+    n_items = plan.n_items;
+    TRY(c->x_recv.ensure(n_items * sizeof(RayRec) + 16));
+    rc = c->comm->alltoallv(c->x_send.p, plan.send_bytes, c->x_recv.p, plan.recv_bytes, s, err);
     if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
     for (int r = 0; r < W; ++r)
-      if (r != c->rank) *bytes_sent += sbytes[r];
-    // transpose [src][lp] -> [lp][src]
-    for (uint32_t lp = 0; lp < nl; ++lp) {
-      uint64_t t = 0;
-      for (int r = 0; r < W; ++r) t += cnt_recv[uint64_t(r) * P + c->local[lp]];
-      pio[lp + 1] = pio[lp] + uint32_t(t);
-    }
-    std::vector<uint64_t> tab;
+      if (r != c->rank) *bytes_sent += plan.send_bytes[r];
+    pio = plan.item_off;
     const uint32_t nblk = nl * uint32_t(W);
-    std::vector<uint64_t> src_start(nblk), dst_start(nblk);
-    uint64_t acc = 0;
-    for (int r = 0; r < W; ++r)  // recv layout [src][lp]
-      for (uint32_t lp = 0; lp < nl; ++lp) {
-        src_start[uint64_t(r) * nl + lp] = acc;
-        acc += cnt_recv[uint64_t(r) * P + c->local[lp]];
-      }
-    // blocks enumerated in recv order; dst offsets in [lp][src]
-    std::vector<uint64_t> dst_off_lp(nl, 0);
-    for (uint32_t lp = 0; lp < nl; ++lp) dst_off_lp[lp] = pio[lp];
-    std::vector<uint64_t> run(nl, 0);
-    for (int r = 0; r < W; ++r)
-      for (uint32_t lp = 0; lp < nl; ++lp) {
-        dst_start[uint64_t(r) * nl + lp] = dst_off_lp[lp] + run[lp];
-        run[lp] += cnt_recv[uint64_t(r) * P + c->local[lp]];
-      }
-    tab.insert(tab.end(), src_start.begin(), src_start.end());
-    tab.insert(tab.end(), dst_start.begin(), dst_start.end());
+    std::vector<uint64_t> tab(plan.block_src);
+    tab.insert(tab.end(), plan.block_dst.begin(), plan.block_dst.end());
     TRY(upload(c->perm_tab, tab.data(), tab.size() * 8, s));
     TRY(c->rec.ensure(n_items * sizeof(RayRec) + 16));
     if (n_items) {
@@ -787,34 +762,13 @@ int exchange_partials(dg_ctx* c, const std::vector<uint32_t>& pair_cnt, uint64_t
   cudaStream_t s = c->stream;
   const uint32_t P = c->P, nl = uint32_t(c->local.size());
   const int W = c->world;
-  auto cnt = [&](uint32_t q, uint32_t p) -> uint64_t {  // records in stream q -> p
-    if (c->local_of_global[q] != 0xff) return pair_cnt[uint64_t(c->local_of_global[q]) * P + p];
-    return pair_cnt[uint64_t(c->local_of_global[p]) * P + q];  // symmetric
-  };
-  std::vector<uint64_t> send_off(uint64_t(P) * P, 0), recv_off(uint64_t(P) * P, 0);
-  std::vector<uint64_t> sbytes(W, 0), rbytes(W, 0);
-  uint64_t so = 0, ro = 0;
-  for (int r = 0; r < W; ++r) {  // send layout: [dest r][q local][p on r]
-    const uint64_t start = so;
-    for (uint32_t lq = 0; lq < nl; ++lq)
-      for (uint32_t p = 0; p < P; ++p)
-        if (c->part_rank[p] == r && p != c->local[lq]) {
-          send_off[uint64_t(c->local[lq]) * P + p] = so;
-          so += cnt(c->local[lq], p);
-        }
-    sbytes[r] = (so - start) * sizeof(PartialRec);
-  }
-  for (int r = 0; r < W; ++r) {  // recv layout: [src r][q on r][p local]
-    const uint64_t start = ro;
-    for (uint32_t q = 0; q < P; ++q)
-      if (c->part_rank[q] == r)
-        for (uint32_t lp = 0; lp < nl; ++lp)
-          if (q != c->local[lp]) {
-            recv_off[uint64_t(q) * P + c->local[lp]] = ro;
-            ro += cnt(q, c->local[lp]);
-          }
-    rbytes[r] = (ro - start) * sizeof(PartialRec);
-  }
+  PartialPlan plan;
+  plan_partials(c->rank, W, P, pair_cnt.data(), sizeof(PartialRec), plan);
+  const std::vector<uint64_t>& send_off = plan.send_off;
+  const std::vector<uint64_t>& recv_off = plan.recv_off;
+  const std::vector<uint64_t>& sbytes = plan.send_bytes;
+  const std::vector<uint64_t>& rbytes = plan.recv_bytes;
+  const uint64_t so = plan.send_total, ro = plan.recv_total;
   TRY(upload(c->stream_send_d, send_off.data(), send_off.size() * 8, s));
   TRY(upload(c->stream_recv_d, recv_off.data(), recv_off.size() * 8, s));
   c->h2d += (send_off.size() + recv_off.size()) * 8;

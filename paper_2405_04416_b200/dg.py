@@ -393,3 +393,31 @@ def nccl_unique_id():
     buf = (C.c_uint8 * 128)()
     _check(lib().dg_comm_unique_id(buf))
     return bytes(buf)
+
+
+# ---- exchange planning (host only; include/distgrid_b200.h dg_plan_*) ----
+def plan_dispatch(rank, world, P, send_cnt, cnt_recv):
+    """Exchange-1 layouts: (send_bytes[W], recv_bytes[W], item_off[nl+1], block_src, block_dst)."""
+    nl = len([p for p in range(P) if p % world == rank])
+    sc = np.ascontiguousarray(send_cnt, dtype=np.uint64)
+    cr = np.ascontiguousarray(cnt_recv, dtype=np.uint64).reshape(-1)
+    sb = np.zeros(world, np.uint64)
+    rb = np.zeros(world, np.uint64)
+    io = np.zeros(nl + 1, np.uint32)
+    bs = np.zeros(max(1, world * nl), np.uint64)
+    bd = np.zeros(max(1, world * nl), np.uint64)
+    _check(lib().dg_plan_dispatch(C.c_int(rank), C.c_int(world), C.c_uint32(P), _p(sc), _p(cr), _p(sb),
+                                  _p(rb), _p(io), _p(bs), _p(bd)))
+    return sb, rb, io, bs[:world * nl], bd[:world * nl]
+
+
+def plan_partials(rank, world, P, pair_cnt):
+    """Exchange-2 layouts: (send_off[P,P], recv_off[P,P], send_bytes[W], recv_bytes[W])."""
+    pc = np.ascontiguousarray(pair_cnt, dtype=np.uint32).reshape(-1)
+    so = np.zeros(P * P, np.uint64)
+    ro = np.zeros(P * P, np.uint64)
+    sb = np.zeros(world, np.uint64)
+    rb = np.zeros(world, np.uint64)
+    _check(lib().dg_plan_partials(C.c_int(rank), C.c_int(world), C.c_uint32(P), _p(pc), _p(so), _p(ro),
+                                  _p(sb), _p(rb)))
+    return so.reshape(P, P), ro.reshape(P, P), sb, rb

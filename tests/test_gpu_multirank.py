@@ -1,0 +1,127 @@
+"""world = 2 on one GPU: two processes, one dg_ctx each (partition p on rank p % 2), the
+exchanges over the host-staged backend (dg_comm_init_host) with gloo moving the bytes.  Each
+rank trains on its contiguous home shard; the per-rank loss sums and every partition's
+parameters after two steps must match the world = 1 run of the same batch, which the parity
+suite ties to the oracle.  (No kernel waits on another process: the host backend copies to
+the host and back, so sharing one GPU is safe.)"""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from .helpers import app_rows, inject, rel_err, rel_l2, small_cfg
+
+pytestmark = pytest.mark.gpu
+
+KX, KY, N, STEPS = 2, 2, 3000, 2
+
+
+def _cfg():
+    return small_cfg(KX, KY, table_log2=13, levels=8, nmax=256, divisor=128,
+                     inner=((0.3, 0.25, 0.0), (1.6, 1.8, 0.8)), occ_res=24)
+
+
+def _rays():
+    from paper_2405_04416_b200 import workloads
+    return workloads.make_rays(_cfg(), N, "random", seed=3)
+
+
+def _gloo_alltoallv(blocks, recv_sizes):
+    W = dist.get_world_size()
+    send = torch.frombuffer(bytearray(b"".join(blocks)) or bytearray(1), dtype=torch.uint8)[:sum(len(b) for b in blocks)]
+    recv = torch.empty(int(sum(recv_sizes)), dtype=torch.uint8)
+    dist.all_to_all_single(recv, send, [int(r) for r in recv_sizes], [len(b) for b in blocks])
+    out, off = [], 0
+    rb = recv.numpy().tobytes()
+    for r in range(W):
+        out.append(rb[off:off + int(recv_sizes[r])])
+        off += int(recv_sizes[r])
+    return out
+
+
+def _rank_main(rank, world, port, ref_path, errq):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2405_04416_b200 import dg
+        cfg = _cfg()
+        ctx = dg.Context(cfg, device=0, rank=rank, world=world)
+        ctx.comm_init_host(_gloo_alltoallv)
+        inject(cfg, None, [_LocalOnly(ctx)], occupancy_fraction=0.6)
+        ctx.set_appearance(app_rows(1).astype(np.float32))
+        o, d, gt, img = _rays()
+        lo, hi = rank * N // world, (rank + 1) * N // world
+        losses = []
+        for step in range(STEPS):
+            st = ctx.train_step(o[lo:hi], d[lo:hi], gt[lo:hi], img[lo:hi], step=step, first_ray_id=lo)
+            losses.append([st["loss_rgb"], st["loss_transmittance"], st["loss_distortion"]])
+        tot = torch.tensor(np.array(losses, np.float64))
+        dist.all_reduce(tot)
+        ref = np.load(ref_path)
+        assert np.allclose(tot.numpy(), ref["losses"], rtol=1e-6, atol=1e-12), (tot.numpy(), ref["losses"])
+        for g in ctx.local:
+            err = rel_l2(ctx.get_params(g), ref[f"p{g}"])
+            assert err < 1e-5, (rank, g, err)
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        errq.put((rank, traceback.format_exc()))
+        raise
+
+
+class _LocalOnly:
+    """inject() target that only writes the partitions this rank owns."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+
+    def set_params(self, g, p):
+        if g in self.ctx.local:
+            self.ctx.set_params(g, p)
+
+    def set_occupancy(self, g, c, bits):
+        if g in self.ctx.local:
+            self.ctx.set_occupancy(g, c, bits)
+
+
+def test_two_ranks_match_single_rank():
+    from paper_2405_04416_b200 import dg
+    cfg = _cfg()
+    ctx = dg.Context(cfg, device=0)
+    inject(cfg, ctx, [], occupancy_fraction=0.6)
+    ctx.set_appearance(app_rows(1).astype(np.float32))
+    o, d, gt, img = _rays()
+    losses = []
+    for step in range(STEPS):
+        st = ctx.train_step(o, d, gt, img, step=step)
+        losses.append([st["loss_rgb"], st["loss_transmittance"], st["loss_distortion"]])
+    ref = {"losses": np.array(losses, np.float64)}
+    for g in range(KX * KY):
+        ref[f"p{g}"] = ctx.get_params(g)
+    del ctx
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "ref.npz")
+        np.savez(path, **ref)
+        mpc = mp.get_context("spawn")
+        errq = mpc.SimpleQueue()
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        procs = [mpc.Process(target=_rank_main, args=(r, 2, port, path, errq)) for r in range(2)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(timeout=600)
+        errs = []
+        while not errq.empty():
+            errs.append(errq.get())
+        assert not errs, errs
+        assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
