@@ -49,6 +49,16 @@ def peaks():
         return 6650.0, 1400.0, "fallback"
 
 
+def profile_traffic():
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the hot kernels,
+    from the committed ncu --set full capture summarised in profiles/traffic.json."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return {k: v["dram_bytes_per_launch"] for k, v in json.load(f)["kernels"].items()}
+    except Exception:
+        return {}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -151,7 +161,7 @@ def run_reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=16)  # = occ_update_interval: one update amortised
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rays-per-gpu", type=int, default=131072)
@@ -304,16 +314,22 @@ def main():
     enc_fwd_gbs = enc_bytes / (st["encode_fwd"] / 1e3) / 1e9 if st["encode_fwd"] > 0 else 0.0
     enc_bwd_gbs = 2 * enc_bytes / (st["encode_bwd"] / 1e3) / 1e9 if st["encode_bwd"] > 0 else 0.0
     mlp_tflops = samples_rank * MLP_FLOP_TRAIN / ((st["mlp_fwd"] + st["mlp_bwd"]) / 1e3) / 1e12
+    traffic = profile_traffic()
     if dominant in ("mlp_fwd", "mlp_bwd"):
-        roof = {"kernel": "mlp_fwd+mlp_bwd (FFMA fp32)", "bound": "tensor", "achieved": mlp_tflops,
+        roof = {"kernel": "k_mlp_fwd_tc+k_mlp_bwd_tc", "bound": "tensor", "achieved": mlp_tflops,
                 "peak": tensor_peak, "unit": "TFLOP/s", "frac": mlp_tflops / tensor_peak,
-                "traffic": None,
-                "note": f"{MLP_FLOP_TRAIN} FLOP/sample x {samples_rank} samples; peak = {peak_kind} "
-                        f"sustained bf16 (the kernel runs on the fp32 FMA pipe)"}
+                "traffic": traffic.get("k_mlp_bwd_tc"),
+                "note": f"{MLP_FLOP_TRAIN} algorithmic FLOP/sample x {samples_rank} samples; the "
+                        f"tcgen05 split-bf16 kernels execute 3 bf16 MMAs per product; peak = "
+                        f"{peak_kind} sustained dense bf16"}
     else:
         ach = {"encode_fwd": enc_fwd_gbs, "encode_bwd": enc_bwd_gbs}.get(dominant, enc_fwd_gbs)
-        roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": None}
+        kname = {"encode_fwd": "k_encode_fwd", "encode_bwd": "k_encode_bwd"}.get(dominant, dominant)
+        roof = {"kernel": kname, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": traffic.get(kname),
+                "note": "achieved = algorithmic bytes (SURVEY 8d) / the kernel's live CUDA-event time; "
+                        "traffic = DRAM read+write bytes per launch from the committed ncu --set full "
+                        "capture (profiles/traffic.json)"}
     roof["stage_ms"] = st
     roofline_encode = {"encode_fwd": {"achieved": enc_fwd_gbs, "peak": hbm, "unit": "GB/s",
                                       "frac": enc_fwd_gbs / hbm,

@@ -29,11 +29,13 @@ __global__ void k_lat(unsigned long long* out) {
   uint32_t phase = 0;
   const uint64_t a = tc::smem_desc(tc::smem_u32(sm), 2048, 128);
   const uint64_t b = tc::smem_desc(tc::smem_u32(sm + 32768), 1024, 128);
-  const int Ns[3] = {16, 64, 128};
+  const int Ns[3] = {8, 64, 128};
   int o = 0;
   for (int ni = 0; ni < 3; ++ni) {
     const uint32_t id = tc::idesc_bf16(128, Ns[ni], 0, 0);
-    for (int mode = 0; mode < 3; ++mode) {       // 0: chain, 1: independent accumulators, 2: chain, A in TMEM
+    const uint32_t id64mn = tc::idesc_bf16(64, Ns[ni], 1, 1), id64k = tc::idesc_bf16(64, Ns[ni], 0, 0);
+    const uint64_t amn = tc::smem_desc(tc::smem_u32(sm), 128, 2048), bmn = tc::smem_desc(tc::smem_u32(sm + 32768), 128, 2048);
+    for (int mode = 0; mode < 5; ++mode) {       // 0: chain, 1: indep, 2: A in TMEM, 3: M=64 MN-major SS, 4: M=64 K-major SS
       for (int cnt = 1; cnt <= 32; cnt *= 2) {
         unsigned long long best = ~0ull;
         for (int rep = 0; rep < 5; ++rep) {
@@ -43,6 +45,8 @@ __global__ void k_lat(unsigned long long* out) {
             if (tc::elect_one()) {
               for (int i = 0; i < cnt; ++i) {
                 if (mode == 2) mma_ts(tmem, tmem + 256, b, id, i > 0 ? 1u : 0u);
+                else if (mode == 3) tc::mma_bf16(tmem, amn, bmn, id64mn, i > 0 ? 1u : 0u);
+                else if (mode == 4) tc::mma_bf16(tmem, a, b, id64k, i > 0 ? 1u : 0u);
                 else tc::mma_bf16(tmem + (mode ? (uint32_t)((i % 4) * 64) : 0u), a, b, id, i > 0 ? 1u : 0u);
               }
               tc::commit(&mbar);
@@ -66,17 +70,18 @@ __global__ void k_lat(unsigned long long* out) {
 
 int main() {
   unsigned long long* d;
-  cudaMalloc(&d, 64 * 8); cudaMemset(d, 0, 64 * 8);
+  cudaMalloc(&d, 128 * 8); cudaMemset(d, 0, 128 * 8);
   cudaFuncSetAttribute(k_lat, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
   k_lat<<<1, 128, 80 * 1024>>>(d);
-  unsigned long long h[64] = {};
+  unsigned long long h[128] = {};
   cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
-  const int Ns[3] = {16, 64, 128};
+  const int Ns[3] = {8, 64, 128};
   int o = 0;
   for (int ni = 0; ni < 3; ++ni)
-    for (int mode = 0; mode < 3; ++mode) {
-      printf("N=%3d %s:", Ns[ni], mode == 2 ? "ts-ch" : mode ? "indep" : "chain");
+    for (int mode = 0; mode < 5; ++mode) {
+      const char* nm[5] = {"chain", "indep", "ts-ch", "m64mn", "m64k "};
+      printf("N=%3d %s:", Ns[ni], nm[mode]);
       for (int cnt = 1; cnt <= 32; cnt *= 2) printf("  %2d:%5llu", cnt, h[o++]);
       printf("\n");
     }
