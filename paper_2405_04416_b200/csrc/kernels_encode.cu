@@ -24,8 +24,10 @@ struct Corners {
   float w[8];
 };
 
-// Lattice corners of one level for normalised point p; zero-weight corners get w = 0 and
-// are skipped by the callers exactly as the reference skips them (grid.cpp:119-120).
+// Lattice corners of one level for normalised point p; zero-weight corners get row = NONE
+// and are skipped by the callers exactly as the reference skips them (grid.cpp:119-120).
+// Lattice indices, fractions and corner weights are fp64 (bit-exact rows; the weight rounds
+// once to fp32, features accumulate in fp32); the row arithmetic is hoisted per axis.
 __device__ __forceinline__ void level_corners(const LevelDesc& lv, const double p[3], Corners& c) {
   const AxisW ax = lattice_axis(p[0], lv.n[0]);
   const AxisW ay = lattice_axis(p[1], lv.n[1]);
@@ -33,13 +35,30 @@ __device__ __forceinline__ void level_corners(const LevelDesc& lv, const double 
   const double fx[2] = {dsub(1.0, ax.frac), ax.frac};
   const double fy[2] = {dsub(1.0, ay.frac), ay.frac};
   const double fz[2] = {dsub(1.0, az.frac), az.frac};
+  // row = x ^ (y * P1) ^ (z * P2) (hashed) or x + nx (y + ny z) (one-to-one), per axis parts
+  uint32_t rx[2], ry[2], rz[2];
+  if (lv.hashed) {
+    rx[0] = ax.i0;
+    rx[1] = ax.i1;
+    ry[0] = ay.i0 * 2654435761u;
+    ry[1] = ay.i1 * 2654435761u;
+    rz[0] = az.i0 * 805459861u;
+    rz[1] = az.i1 * 805459861u;
+  } else {
+    rx[0] = ax.i0;
+    rx[1] = ax.i1;
+    ry[0] = lv.n[0] * ay.i0;
+    ry[1] = lv.n[0] * ay.i1;
+    rz[0] = lv.n[0] * lv.n[1] * az.i0;
+    rz[1] = lv.n[0] * lv.n[1] * az.i1;
+  }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int cx = k & 1, cy = (k >> 1) & 1, cz = (k >> 2) & 1;
     const double w = dmul(dmul(fx[cx], fy[cy]), fz[cz]);
     c.w[k] = (float)w;
-    c.row[k] = w == 0.0 ? 0xffffffffu
-                        : table_row(lv, cx ? ax.i1 : ax.i0, cy ? ay.i1 : ay.i0, cz ? az.i1 : az.i0);
+    const uint32_t row = lv.hashed ? ((rx[cx] ^ ry[cy] ^ rz[cz]) & lv.mask) : (rx[cx] + ry[cy] + rz[cz]);
+    c.row[k] = w == 0.0 ? 0xffffffffu : row;
   }
 }
 
