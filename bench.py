@@ -169,7 +169,8 @@ def main():
     ap.add_argument("--render-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--ref-rays", type=int, default=512)
+    ap.add_argument("--ref-rays", type=int, default=512, help="rays per step of the --impl reference arm")
+    ap.add_argument("--cpu-rays", type=int, default=2048, help="rays of the cpu_baseline sample (~10 s)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -342,7 +343,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         o, d, gt, _ = batches_host[0]
-        cpu, why = cpu_reference(cfg, o, d, gt, args.ref_rays, 1, 0)
+        cpu, why = cpu_reference(cfg, o, d, gt, args.cpu_rays, 1, 0)
         if cpu is None:
             cpu = {"value": None, "unit": "rays/s", "cores": 0, "kind": "reference", "sample": why}
         else:

@@ -37,6 +37,7 @@ def _box_config(outer_hi, kx, ky, table_log2, divisor, levels=16, nmax=2048):
     c.appearance_dim = 16
     c.march_step_divisor = float(divisor)
     c.total_steps = 1000
+    c.wire_f32 = 1  # benchmark mode: f32 partial payload (SURVEY 8d common settings)
     return c
 
 
