@@ -215,6 +215,29 @@ typedef int (*dg_alltoallv_fn)(void* user, const void* send, const uint64_t* sen
                                 void* recv, const uint64_t* recv_bytes);
 int dg_comm_init_host(dg_ctx* ctx, dg_alltoallv_fn fn, void* user);
 
+/* ---- ray cache / pixel-ray batch feed ----
+ * RayCache (train.cpp:117-159) over a dataset uploaded once: images (u8 RGB, row-major) and
+ * camera poses (partition.hpp:15-28).  refresh() samples `count` (train image, pixel) pairs
+ * from the reference's refresh stream and builds the rays on the device with make_pixel_ray
+ * (dataset.cpp:312-324); draw() picks entries with the reference's draw stream and gathers
+ * them into a device-resident dg_ray_batch (owned by the cache, valid until the next draw)
+ * that dg_train_step consumes directly. */
+typedef struct dg_camera {
+  uint32_t image_id, width, height, is_train;
+  double rotation[9]; /* camera-to-world, row-major */
+  double translation[3];
+  double fx, fy, cx, cy;
+} dg_camera;
+typedef struct dg_ray_cache dg_ray_cache;
+int dg_ray_cache_create(int device, const dg_camera* cams, const uint8_t* const* images, uint32_t n_images,
+                        uint64_t capacity, uint64_t seed, dg_ray_cache** out);
+void dg_ray_cache_destroy(dg_ray_cache* cache);
+int dg_ray_cache_size(const dg_ray_cache* cache, uint64_t* size, uint64_t* capacity);
+int dg_ray_cache_refresh(dg_ray_cache* cache, uint64_t count);
+int dg_ray_cache_draw(dg_ray_cache* cache, uint64_t n, dg_ray_batch* out);
+int dg_ray_cache_snapshot(dg_ray_cache* cache, double* origin, double* dir, float* color_gt,
+                          uint32_t* image_id, uint64_t* pixel_id);
+
 /* ---- exchange planning (host only, no context or device needed) ----
  * The layouts both per-step exchanges use (exchange_plan.h), exported so multi-process tests
  * can check the protocol on CPU.  Partition p lives on rank p % world.

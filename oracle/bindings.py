@@ -458,3 +458,93 @@ class OracleModel:
         self.lib.or_stage_field_backward(self.ptr, g, cascade, _ptr(params), _ptr(grads),
                                          *[_ptr(x) for x in a], n)
         return grads
+
+
+# ---- ray cache: C restatement and the reference's own RayCache ----
+class _CacheBase:
+    def __init__(self, poses, images, capacity, seed):
+        from paper_2405_04416_b200.abi import cameras
+        self._cams = cameras(poses)
+        self._imgs = [np.ascontiguousarray(im, dtype=np.uint8) for im in images]
+        self._ptrs = (C.c_void_p * len(self._imgs))(*[im.ctypes.data for im in self._imgs])
+
+    @staticmethod
+    def _bufs(n):
+        return (np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 3)), np.zeros(n, np.uint32),
+                np.zeros(n, np.uint64))
+
+
+class OracleRayCache(_CacheBase):
+    def __init__(self, poses, images, capacity, seed):
+        super().__init__(poses, images, capacity, seed)
+        L = oracle_lib()
+        L.or_ray_cache_create.restype = P
+        L.or_ray_cache_create.argtypes = [P, P, C.c_uint32, C.c_uint64, C.c_uint64]
+        L.or_ray_cache_destroy.argtypes = [P]
+        L.or_ray_cache_size.restype = C.c_uint64
+        L.or_ray_cache_size.argtypes = [P]
+        L.or_ray_cache_refresh.argtypes = [P, C.c_uint64]
+        L.or_ray_cache_draw.argtypes = [P, C.c_uint64, P, P, P, P, P]
+        L.or_ray_cache_snapshot.argtypes = [P, P, P, P, P, P]
+        self.L = L
+        self.h = L.or_ray_cache_create(C.cast(self._cams, P), C.cast(self._ptrs, P), len(self._imgs),
+                                       capacity, seed)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.or_ray_cache_destroy(self.h)
+            self.h = None
+
+    def size(self):
+        return self.L.or_ray_cache_size(self.h)
+
+    def refresh(self, count):
+        assert self.L.or_ray_cache_refresh(self.h, count) == 0
+
+    def draw(self, n):
+        out = self._bufs(n)
+        assert self.L.or_ray_cache_draw(self.h, n, *[_ptr(a) for a in out]) == 0
+        return out
+
+    def snapshot(self):
+        out = self._bufs(self.size())
+        self.L.or_ray_cache_snapshot(self.h, *[_ptr(a) for a in out])
+        return out
+
+
+class RefRayCache(_CacheBase):
+    def __init__(self, poses, images, capacity, seed):
+        super().__init__(poses, images, capacity, seed)
+        L = ref_lib()
+        L.refh_ray_cache_create.restype = P
+        L.refh_ray_cache_create.argtypes = [P, P, C.c_uint32, C.c_uint64, C.c_uint64]
+        L.refh_ray_cache_destroy.argtypes = [P]
+        L.refh_ray_cache_refresh.argtypes = [P, C.c_uint64]
+        L.refh_ray_cache_snapshot.restype = C.c_uint64
+        L.refh_ray_cache_snapshot.argtypes = [P, P, P, P, P, P]
+        L.refh_ray_cache_draw.argtypes = [P, C.c_uint64, P, P, P, P, P]
+        self.L = L
+        self.h = L.refh_ray_cache_create(C.cast(self._cams, P), C.cast(self._ptrs, P), len(self._imgs),
+                                         capacity, seed)
+        assert self.h, L.refh_last_error()
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.refh_ray_cache_destroy(self.h)
+            self.h = None
+
+    def size(self):
+        return int(self.L.refh_ray_cache_snapshot(self.h, None, None, None, None, None))
+
+    def refresh(self, count):
+        assert self.L.refh_ray_cache_refresh(self.h, count) == 0, self.L.refh_last_error()
+
+    def draw(self, n):
+        out = self._bufs(n)
+        assert self.L.refh_ray_cache_draw(self.h, n, *[_ptr(a) for a in out]) == 0, self.L.refh_last_error()
+        return out
+
+    def snapshot(self):
+        out = self._bufs(self.size())
+        self.L.refh_ray_cache_snapshot(self.h, *[_ptr(a) for a in out])
+        return out

@@ -1309,3 +1309,120 @@ void or_stage_field_backward(const or_model* m, uint32_t region, uint32_t cascad
     or_field_backward(f, params + off, grads + off, &c, dsigma[i], drgb + 3 * i);
   }
 }
+
+
+/* ======================================================================== ray cache */
+/* partition.cpp:30-33: normalize(rotation * ((x - cx) / fx, (y - cy) / fy, 1)); Mat3 * Vec3
+ * row by row left to right (vecmath.hpp), normalize = v / sqrt(dot(v, v)). */
+void or_make_pixel_ray(const or_camera* cam, const uint8_t* rgb, uint32_t x, uint32_t y, double origin[3],
+                       double dir[3], double color[3], uint32_t* image_id, uint64_t* pixel_id) {
+  const double px = (double)x + 0.5, py = (double)y + 0.5; /* dataset.cpp:317 */
+  const double c[3] = {(px - cam->cx) / cam->fx, (py - cam->cy) / cam->fy, 1.0};
+  double v[3];
+  for (int r = 0; r < 3; ++r)
+    v[r] = cam->rotation[3 * r] * c[0] + cam->rotation[3 * r + 1] * c[1] + cam->rotation[3 * r + 2] * c[2];
+  const double len = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  for (int a = 0; a < 3; ++a) {
+    origin[a] = cam->translation[a];
+    dir[a] = v[a] / len;
+    /* Image::pixel_channel, dataset.hpp:19-21 */
+    color[a] = (double)rgb[((size_t)y * cam->width + x) * 3 + a] / 255.0;
+  }
+  *image_id = cam->image_id;
+  *pixel_id = ((uint64_t)cam->image_id << 32) | ((uint64_t)y * cam->width + x);
+}
+
+struct or_ray_cache {
+  uint64_t capacity, size, cursor;
+  or_mt64 refresh_rng, draw_rng;
+  uint32_t n_images, n_train;
+  const or_camera* cams;
+  const uint8_t* const* images;
+  uint32_t* train;
+  double *origin, *dir, *color;
+  uint32_t* image_id;
+  uint64_t* pixel_id;
+};
+
+/* train.cpp:117-121: Rng(splitmix64(seed ^ tag)) per stream (Rng seeds its engine with
+ * splitmix64 of its argument again, rng.hpp:34). */
+or_ray_cache* or_ray_cache_create(const or_camera* cams, const uint8_t* const* images, uint32_t n_images,
+                                  uint64_t capacity, uint64_t seed) {
+  if (capacity == 0 || n_images == 0) return NULL;
+  or_ray_cache* c = (or_ray_cache*)calloc(1, sizeof(or_ray_cache));
+  c->capacity = capacity;
+  or_rng_init(&c->refresh_rng, or_splitmix64(seed ^ 0x5261794361636865ull));
+  or_rng_init(&c->draw_rng, or_splitmix64(seed ^ 0x4261746368447277ull));
+  c->n_images = n_images;
+  c->cams = cams;
+  c->images = images;
+  c->train = (uint32_t*)malloc(sizeof(uint32_t) * n_images);
+  for (uint32_t i = 0; i < n_images; ++i)
+    if (cams[i].is_train) c->train[c->n_train++] = i;
+  c->origin = (double*)malloc(sizeof(double) * 3 * capacity);
+  c->dir = (double*)malloc(sizeof(double) * 3 * capacity);
+  c->color = (double*)malloc(sizeof(double) * 3 * capacity);
+  c->image_id = (uint32_t*)malloc(sizeof(uint32_t) * capacity);
+  c->pixel_id = (uint64_t*)malloc(sizeof(uint64_t) * capacity);
+  return c;
+}
+
+void or_ray_cache_destroy(or_ray_cache* c) {
+  if (!c) return;
+  free(c->train);
+  free(c->origin);
+  free(c->dir);
+  free(c->color);
+  free(c->image_id);
+  free(c->pixel_id);
+  free(c);
+}
+
+uint64_t or_ray_cache_size(const or_ray_cache* c) { return c->size; }
+
+/* train.cpp:123-143 */
+int or_ray_cache_refresh(or_ray_cache* c, uint64_t count) {
+  if (c->n_train == 0) return DG_EINVAL;
+  for (uint64_t i = 0; i < count; ++i) {
+    const uint32_t img = c->train[or_mt64_next(&c->refresh_rng) % c->n_train];
+    const or_camera* cam = &c->cams[img];
+    const uint32_t x = (uint32_t)(or_mt64_next(&c->refresh_rng) % cam->width);
+    const uint32_t y = (uint32_t)(or_mt64_next(&c->refresh_rng) % cam->height);
+    uint64_t slot;
+    if (c->size < c->capacity) {
+      slot = c->size++;
+    } else {
+      slot = c->cursor;
+      c->cursor = (c->cursor + 1) % c->capacity;
+    }
+    or_make_pixel_ray(cam, c->images[img], x, y, c->origin + 3 * slot, c->dir + 3 * slot,
+                      c->color + 3 * slot, c->image_id + slot, c->pixel_id + slot);
+  }
+  return DG_OK;
+}
+
+/* train.cpp:150-157 */
+int or_ray_cache_draw(or_ray_cache* c, uint64_t n, double* origin, double* dir, double* color,
+                      uint32_t* image_id, uint64_t* pixel_id) {
+  if (c->size == 0) return DG_EPROTO;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t e = or_mt64_next(&c->draw_rng) % c->size;
+    for (int a = 0; a < 3; ++a) {
+      if (origin) origin[3 * i + a] = c->origin[3 * e + a];
+      if (dir) dir[3 * i + a] = c->dir[3 * e + a];
+      if (color) color[3 * i + a] = c->color[3 * e + a];
+    }
+    if (image_id) image_id[i] = c->image_id[e];
+    if (pixel_id) pixel_id[i] = c->pixel_id[e];
+  }
+  return DG_OK;
+}
+
+void or_ray_cache_snapshot(const or_ray_cache* c, double* origin, double* dir, double* color,
+                           uint32_t* image_id, uint64_t* pixel_id) {
+  memcpy(origin, c->origin, sizeof(double) * 3 * c->size);
+  memcpy(dir, c->dir, sizeof(double) * 3 * c->size);
+  memcpy(color, c->color, sizeof(double) * 3 * c->size);
+  memcpy(image_id, c->image_id, sizeof(uint32_t) * c->size);
+  memcpy(pixel_id, c->pixel_id, sizeof(uint64_t) * c->size);
+}

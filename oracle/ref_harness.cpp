@@ -20,9 +20,11 @@
 #include <vector>
 
 #include "distgrid/config.hpp"
+#include "distgrid/dataset.hpp"
 #include "distgrid/field.hpp"
 #include "distgrid/partition.hpp"
 #include "distgrid/render.hpp"
+#include "distgrid/train.hpp"
 #include "distgrid/worker.hpp"
 #include "distgrid_b200.h"
 
@@ -551,6 +553,91 @@ double refh_time_replicas(void* const* runs, uint32_t n_runs, const double* orig
       }
     }
   return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// ---- RayCache / make_pixel_ray (train.cpp:117-159, dataset.cpp:312-324) ----
+struct RefRayCache {
+  Dataset dataset;
+  std::unique_ptr<RayCache> cache;
+};
+
+void* refh_ray_cache_create(const dg_camera* cams, const uint8_t* const* images, uint32_t n_images,
+                            uint64_t capacity, uint64_t seed) {
+  try {
+    auto r = std::make_unique<RefRayCache>();
+    for (uint32_t i = 0; i < n_images; ++i) {
+      const dg_camera& k = cams[i];
+      CameraPose pose;
+      pose.image_id = k.image_id;
+      for (int j = 0; j < 9; ++j) pose.rotation.m[j] = k.rotation[j];
+      pose.translation = Vec3{k.translation[0], k.translation[1], k.translation[2]};
+      pose.fx = k.fx;
+      pose.fy = k.fy;
+      pose.cx = k.cx;
+      pose.cy = k.cy;
+      pose.width = k.width;
+      pose.height = k.height;
+      Image img;
+      img.width = k.width;
+      img.height = k.height;
+      img.rgb.assign(images[i], images[i] + size_t(k.width) * k.height * 3);
+      r->dataset.poses.push_back(pose);
+      r->dataset.images.push_back(std::move(img));
+      r->dataset.is_train.push_back(k.is_train ? 1 : 0);
+    }
+    r->cache = std::make_unique<RayCache>(capacity, seed);
+    return r.release();
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+void refh_ray_cache_destroy(void* p) { delete static_cast<RefRayCache*>(p); }
+
+int refh_ray_cache_refresh(void* p, uint64_t count) {
+  try {
+    auto* r = static_cast<RefRayCache*>(p);
+    r->cache->refresh(r->dataset, count);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+static void put_ray(const SupervisedRay& s, uint64_t i, double* origin, double* dir, double* color,
+                    uint32_t* image_id, uint64_t* pixel_id) {
+  const double o[3] = {s.ray.origin.x, s.ray.origin.y, s.ray.origin.z};
+  const double d[3] = {s.ray.dir.x, s.ray.dir.y, s.ray.dir.z};
+  const double c[3] = {s.color_gt.x, s.color_gt.y, s.color_gt.z};
+  for (int a = 0; a < 3; ++a) {
+    origin[3 * i + a] = o[a];
+    dir[3 * i + a] = d[a];
+    color[3 * i + a] = c[a];
+  }
+  image_id[i] = s.image_id;
+  pixel_id[i] = s.ray.pixel_id;
+}
+
+uint64_t refh_ray_cache_snapshot(void* p, double* origin, double* dir, double* color, uint32_t* image_id,
+                                 uint64_t* pixel_id) {
+  auto* r = static_cast<RefRayCache*>(p);
+  const std::vector<SupervisedRay> e = r->cache->snapshot();
+  if (origin)
+    for (uint64_t i = 0; i < e.size(); ++i) put_ray(e[i], i, origin, dir, color, image_id, pixel_id);
+  return e.size();
+}
+
+int refh_ray_cache_draw(void* p, uint64_t n, double* origin, double* dir, double* color, uint32_t* image_id,
+                        uint64_t* pixel_id) {
+  try {
+    auto* r = static_cast<RefRayCache*>(p);
+    const std::vector<SupervisedRay> b = r->cache->draw_batch(n);
+    for (uint64_t i = 0; i < b.size(); ++i) put_ray(b[i], i, origin, dir, color, image_id, pixel_id);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
 }
 
 }  // extern "C"

@@ -5,6 +5,8 @@ product binding (paper_2405_04416_b200/dg.py) without importing the CUDA library
 """
 import ctypes as C
 
+import numpy as np
+
 DG_MAX_SEGMENTS = 16
 DG_MAX_PARTITIONS = 64
 DG_MAX_LEVELS = 16
@@ -79,6 +81,27 @@ class ArrayDesc(C.Structure):
 
 class ItemView(C.Structure):
     _fields_ = [("n_items", C.c_uint64), ("n_fine", C.c_uint64), ("n_coarse", C.c_uint64)]
+
+
+class Camera(C.Structure):
+    """dg_camera: CameraPose (partition.hpp:15-28) + split flag."""
+    _fields_ = [("image_id", C.c_uint32), ("width", C.c_uint32), ("height", C.c_uint32),
+                ("is_train", C.c_uint32), ("rotation", C.c_double * 9), ("translation", C.c_double * 3),
+                ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double)]
+
+
+def cameras(poses):
+    """Array of Camera from dicts {image_id, width, height, is_train, rotation (3x3), translation, fx, fy, cx, cy}."""
+    arr = (Camera * len(poses))()
+    for i, p in enumerate(poses):
+        c = arr[i]
+        c.image_id, c.width, c.height, c.is_train = p["image_id"], p["width"], p["height"], int(p["is_train"])
+        for j, v in enumerate(list(np.asarray(p["rotation"], dtype=np.float64).reshape(9))):
+            c.rotation[j] = float(v)
+        for j in range(3):
+            c.translation[j] = float(p["translation"][j])
+        c.fx, c.fy, c.cx, c.cy = (float(p[k]) for k in ("fx", "fy", "cx", "cy"))
+    return arr
 
 
 class StageTimes(C.Structure):

@@ -61,6 +61,15 @@ int set_err(int code, const char* fmt, ...) {
     if (rc_ != DG_OK) return rc_; \
   } while (0)
 
+}  // namespace
+
+namespace dg {
+// Error reporting for the other host translation units (ray_cache.cu): sets dg_last_error.
+int set_error(int code, const char* msg) { return set_err(code, "%s", msg); }
+}  // namespace dg
+
+namespace {
+
 // ---------------------------------------------------------------- host layout math
 uint32_t level_resolution(uint32_t levels, uint32_t base, uint32_t maxr, uint32_t level) {
   if (levels == 1) return base;  // grid.cpp:56-63

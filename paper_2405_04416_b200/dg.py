@@ -421,3 +421,45 @@ def plan_partials(rank, world, P, pair_cnt):
     _check(lib().dg_plan_partials(C.c_int(rank), C.c_int(world), C.c_uint32(P), _p(pc), _p(so), _p(ro),
                                   _p(sb), _p(rb)))
     return so.reshape(P, P), ro.reshape(P, P), sb, rb
+
+
+# ---- ray cache / pixel-ray batch feed (dg_ray_cache_*) ----
+class RayCache:
+    """Device-resident RayCache (train.cpp:117-159): images + poses uploaded once; refresh()
+    builds rays on the GPU, draw() returns a device RayBatch that train_step_raw consumes."""
+
+    def __init__(self, poses, images, capacity, seed, device=-1):
+        from .abi import cameras
+        self._cams = cameras(poses)
+        self._imgs = [np.ascontiguousarray(im, dtype=np.uint8) for im in images]
+        ptrs = (C.c_void_p * len(self._imgs))(*[im.ctypes.data for im in self._imgs])
+        self.h = P()
+        _check(lib().dg_ray_cache_create(C.c_int(device), self._cams, ptrs, C.c_uint32(len(self._imgs)),
+                                         C.c_uint64(capacity), C.c_uint64(seed), C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().dg_ray_cache_destroy(self.h)
+            self.h = None
+
+    def size(self):
+        n, cap = C.c_uint64(), C.c_uint64()
+        _check(lib().dg_ray_cache_size(self.h, C.byref(n), C.byref(cap)))
+        return n.value
+
+    def refresh(self, count):
+        _check(lib().dg_ray_cache_refresh(self.h, C.c_uint64(count)))
+
+    def draw(self, n):
+        b = RayBatch()
+        _check(lib().dg_ray_cache_draw(self.h, C.c_uint64(n), C.byref(b)))
+        return b
+
+    def snapshot(self):
+        n = self.size()
+        o, d = np.zeros((n, 3)), np.zeros((n, 3))
+        gt = np.zeros((n, 3), np.float32)
+        img = np.zeros(n, np.uint32)
+        pix = np.zeros(n, np.uint64)
+        _check(lib().dg_ray_cache_snapshot(self.h, _p(o), _p(d), _p(gt), _p(img), _p(pix)))
+        return o, d, gt, img, pix
