@@ -193,6 +193,22 @@ int dg_init_params_fast(dg_ctx* ctx, uint32_t partition, uint64_t seed);
 int dg_occupancy_shape(const dg_ctx* ctx, uint32_t partition, uint32_t cascade, uint32_t shape[3]);
 int dg_set_occupancy(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const uint8_t* bits);
 int dg_get_occupancy(dg_ctx* ctx, uint32_t partition, uint32_t cascade, uint8_t* bits);
+/* OccupancyGrid density (fp32 here, f64 in the reference) and current threshold; set
+ * recomputes the bitfield as density >= threshold (grid.hpp:99-141). */
+int dg_get_occupancy_density(dg_ctx* ctx, uint32_t partition, uint32_t cascade, float* density,
+                             double* threshold);
+int dg_set_occupancy_density(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const float* density,
+                             double threshold);
+int dg_get_config(const dg_ctx* ctx, dg_run_config* out);
+
+/* ---- checkpoint interop: the reference's per-worker .dgcw file
+ * (checkpoint.cpp:241-283, v1): both cascade fields as f32 tables / MLPs behind shape headers,
+ * both occupancy grids (f32 density, f32 threshold), Adam moments as f64.  config_hash is the
+ * caller's RunConfig::hash() (config.cpp:163-166), written verbatim and returned on load;
+ * region_id = partition.  A GPU-trained partition can be loaded by the reference
+ * (Worker::load_state) and vice versa. */
+int dg_save_checkpoint(dg_ctx* ctx, uint32_t partition, uint64_t config_hash, const char* path);
+int dg_load_checkpoint(dg_ctx* ctx, uint32_t partition, const char* path, uint64_t* config_hash);
 /* Appearance rows (field.hpp:21-29 AppearanceTable); image ids must be < 2^20. */
 int dg_set_appearance(dg_ctx* ctx, const uint32_t* image_ids, const float* rows, uint32_t n_images);
 

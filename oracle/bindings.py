@@ -111,6 +111,8 @@ def ref_lib():
         lib.refh_march_step.argtypes = [P]
         lib.refh_default_config.argtypes = [C.POINTER(RunConfig)]
         lib.refh_last_error.restype = C.c_char_p
+        lib.refh_save_checkpoint.argtypes = [P, C.c_uint32, C.c_uint64, C.c_char_p]
+        lib.refh_load_checkpoint.argtypes = [P, C.c_uint32, C.c_char_p, P]
         lib.refh_time_replicas.restype = C.c_double
         lib.refh_time_replicas.argtypes = [P, C.c_uint32, P, P, P, C.c_uint64, C.c_uint64,
                                            C.c_uint64]
@@ -230,6 +232,14 @@ class RefRun(_RunBase):
 
     def nparams(self, g):
         return int(self.lib.refh_param_count(self.h, g))
+
+    def save_checkpoint(self, g, config_hash, path):
+        self._check(self.lib.refh_save_checkpoint(self.h, g, config_hash, path.encode()))
+
+    def load_checkpoint(self, g, path):
+        h = C.c_uint64()
+        self._check(self.lib.refh_load_checkpoint(self.h, g, path.encode(), C.byref(h)))
+        return h.value
 
     def params(self, g):
         out = np.zeros(self.nparams(g))

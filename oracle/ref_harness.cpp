@@ -19,6 +19,7 @@
 #include <thread>
 #include <vector>
 
+#include "distgrid/checkpoint.hpp"
 #include "distgrid/config.hpp"
 #include "distgrid/dataset.hpp"
 #include "distgrid/field.hpp"
@@ -553,6 +554,29 @@ double refh_time_replicas(void* const* runs, uint32_t n_runs, const double* orig
       }
     }
   return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// ---- .dgcw checkpoints (checkpoint.cpp:241-283) through the Worker's own state calls ----
+int refh_save_checkpoint(void* p, uint32_t region, uint64_t config_hash, const char* path) {
+  try {
+    auto* h = static_cast<Harness*>(p);
+    save_worker_checkpoint(path, h->run->worker(region).make_checkpoint(config_hash));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int refh_load_checkpoint(void* p, uint32_t region, const char* path, uint64_t* config_hash) {
+  try {
+    auto* h = static_cast<Harness*>(p);
+    const WorkerCheckpoint ck = load_worker_checkpoint(path);
+    h->run->worker(region).load_state(ck);
+    if (config_hash) *config_hash = ck.config_hash;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
 }
 
 // ---- RayCache / make_pixel_ray (train.cpp:117-159, dataset.cpp:312-324) ----

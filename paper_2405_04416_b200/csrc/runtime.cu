@@ -1271,6 +1271,47 @@ int dg_get_occupancy(dg_ctx* c, uint32_t p, uint32_t cascade, uint8_t* bits) {
   return occ_copy(c, p, cascade, bits, nullptr);
 }
 
+// OccupancyGrid density + threshold (grid.hpp:99-141); the set variant recomputes the
+// bitfield (recompute_bitfield: density >= threshold) on the device.
+int dg_get_occupancy_density(dg_ctx* c, uint32_t p, uint32_t cascade, float* density, double* threshold) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  CU(cudaSetDevice(c->device));
+  const PartDesc& pd = c->parts[lp];
+  const uint64_t n = uint64_t(pd.occ_n[cascade][0]) * pd.occ_n[cascade][1] * pd.occ_n[cascade][2];
+  if (density)
+    CU(cudaMemcpyAsync(density, c->occ_den.as<float>() + pd.occ_off[cascade], n * sizeof(float),
+                       cudaMemcpyDeviceToHost, c->stream));
+  if (threshold) *threshold = c->occ_thr[lp * 2 + cascade];
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+int dg_set_occupancy_density(dg_ctx* c, uint32_t p, uint32_t cascade, const float* density, double threshold) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1 || !density) return set_err(DG_EINVAL, "cascade must be 0 or 1, density non-null");
+  CU(cudaSetDevice(c->device));
+  const PartDesc& pd = c->parts[lp];
+  const uint64_t n = uint64_t(pd.occ_n[cascade][0]) * pd.occ_n[cascade][1] * pd.occ_n[cascade][2];
+  CU(cudaMemcpyAsync(c->occ_den.as<float>() + pd.occ_off[cascade], density, n * sizeof(float),
+                     cudaMemcpyHostToDevice, c->stream));
+  c->occ_thr[lp * 2 + cascade] = threshold;
+  launch_occ_bits(c->occ_den.as<float>() + pd.occ_off[cascade], c->occ.as<uint8_t>() + pd.occ_off[cascade], n,
+                  float(threshold), c->stream);
+  ++c->launches;
+  CU(cudaStreamSynchronize(c->stream));
+  return DG_OK;
+}
+
+int dg_get_config(const dg_ctx* c, dg_run_config* out) {
+  TRY(check_ctx(c));
+  if (!out) return set_err(DG_EINVAL, "null config");
+  *out = c->cfg;
+  return DG_OK;
+}
+
 int dg_set_appearance(dg_ctx* c, const uint32_t* ids, const float* rows, uint32_t n) {
   TRY(check_ctx(c));
   uint32_t max_id = 0;

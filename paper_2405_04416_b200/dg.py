@@ -193,6 +193,23 @@ class Context:
         _check(lib().dg_get_occupancy(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(bits)))
         return bits
 
+    def save_checkpoint(self, g, config_hash, path):
+        """The reference's .dgcw file for partition g (checkpoint.cpp:241-258)."""
+        _check(lib().dg_save_checkpoint(self.h, C.c_uint32(g), C.c_uint64(config_hash), str(path).encode()))
+
+    def load_checkpoint(self, g, path):
+        """Load a .dgcw (reference- or GPU-written) into partition g; returns its config hash."""
+        h = C.c_uint64()
+        _check(lib().dg_load_checkpoint(self.h, C.c_uint32(g), str(path).encode(), C.byref(h)))
+        return h.value
+
+    def occupancy_density(self, g, cascade):
+        sh = self.occupancy_shape(g, cascade)
+        den = np.zeros(int(np.prod(sh)), np.float32)
+        thr = C.c_double()
+        _check(lib().dg_get_occupancy_density(self.h, C.c_uint32(g), C.c_uint32(cascade), _p(den), C.byref(thr)))
+        return den, thr.value
+
     def set_appearance(self, rows, ids=None):
         rows = _c32(np.atleast_2d(rows))
         ids = np.arange(rows.shape[0], dtype=np.uint32) if ids is None else \
