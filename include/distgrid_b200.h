@@ -91,7 +91,8 @@ typedef struct dg_run_config {
   uint32_t wire_f32;                    /* config.hpp:21 (partials are f32 on this path) */
   uint32_t distortion_cross_correction; /* config.hpp:56; must be 0 */
   uint32_t occupancy_updates;           /* 1: run Worker::update_occupancy cadence */
-  uint32_t reserved;
+  uint32_t eval_early_termination;      /* config.hpp:60 (dispatch_eval, worker.cpp:815-818) */
+  double eval_termination_threshold;    /* config.hpp:61 */
 } dg_run_config;
 
 /* RunConfig defaults (config.hpp:13-78) with inner = outer = [0,1]^3. */
@@ -132,6 +133,7 @@ typedef struct dg_merged {
   float* rgb;           /* n x 3 */
   float* transmittance; /* n */
   float* depth;         /* n */
+  float* attribution;   /* n x 3 or NULL: region-attribution colour (evaluate_image, worker.cpp:864-878) */
   int32_t mem;
   int32_t reserved;
 } dg_merged;
@@ -220,6 +222,11 @@ int dg_train_step(dg_ctx* ctx, const dg_ray_batch* batch, uint64_t step, dg_step
 /* DistributedRun::evaluate_rays (worker.cpp:757-834): jitter off, partials merged at the
  * home rank in schedule order, depth carried.  appearance: appearance_dim floats (host). */
 int dg_render(dg_ctx* ctx, const dg_ray_batch* batch, const float* appearance, dg_merged* out);
+/* DistributedRun::evaluate_image (worker.cpp:836-880): every pixel of one camera (dg_camera,
+ * declared with the ray cache below), rays built on the device; out holds width*height
+ * entries row-major, attribution (region palette weighted by absorbed transmittance) if set. */
+struct dg_camera;
+int dg_render_image(dg_ctx* ctx, const struct dg_camera* camera, const float* appearance, dg_merged* out);
 
 /* ---- communicator (replaces transport.hpp:30-98) ---- */
 #define DG_NCCL_UNIQUE_ID_BYTES 128

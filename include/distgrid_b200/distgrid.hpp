@@ -216,7 +216,7 @@ class DistributedRun {
     std::vector<float> app(appearance_vec.begin(), appearance_vec.end());
     std::vector<float> rgb(3 * n), T(n), depth(n);
     dg_ray_batch b{o_.data(), d_.data(), nullptr, nullptr, n, 0, DG_MEM_HOST, 0};
-    dg_merged m{rgb.data(), T.data(), depth.data(), DG_MEM_HOST, 0};
+    dg_merged m{rgb.data(), T.data(), depth.data(), nullptr, DG_MEM_HOST, 0};
     check(dg_render(ctx_, &b, app.data(), &m));
     std::vector<MergedRender> out(n);
     for (size_t i = 0; i < n; ++i) {

@@ -209,6 +209,17 @@ class OracleRun(_RunBase):
             raise RuntimeError(self.lib.or_last_error().decode())
         return rgb, T, depth
 
+    def eval_rays_attribution(self, o, d, app_vec):
+        n = len(o)
+        rgb, T, depth, attr = np.zeros((n, 3)), np.zeros(n), np.zeros(n), np.zeros((n, 3))
+        app_vec = np.ascontiguousarray(app_vec, dtype=np.float64)
+        self.lib.or_run_eval_rays_ex.argtypes = [P, P, P, C.c_uint64, P, P, P, P, P]
+        rc = self.lib.or_run_eval_rays_ex(self.h, _ptr(o), _ptr(d), n, _ptr(app_vec), _ptr(rgb),
+                                          _ptr(T), _ptr(depth), _ptr(attr))
+        if rc != 0:
+            raise RuntimeError(self.lib.or_last_error().decode())
+        return rgb, T, depth, attr
+
 
 class RefRun(_RunBase):
     """The reference DistributedRun itself, through oracle/ref_harness.cpp."""
@@ -291,6 +302,18 @@ class RefRun(_RunBase):
         self._check(self.lib.refh_eval_rays(self.h, _ptr(o), _ptr(d), n, _ptr(app_vec), _ptr(rgb),
                                             _ptr(T), _ptr(depth)))
         return rgb, T, depth
+
+    def eval_image(self, camera, app_vec):
+        """DistributedRun::evaluate_image for one camera dict -> (rgb, T, depth, attribution)."""
+        from paper_2405_04416_b200.abi import cameras
+        cam = cameras([camera])
+        n = camera["width"] * camera["height"]
+        rgb, T, depth, attr = np.zeros((n, 3)), np.zeros(n), np.zeros(n), np.zeros((n, 3))
+        app_vec = np.ascontiguousarray(app_vec, dtype=np.float64)
+        self.lib.refh_eval_image.argtypes = [P, P, P, P, P, P, P]
+        self._check(self.lib.refh_eval_image(self.h, C.cast(cam, P), _ptr(app_vec), _ptr(rgb), _ptr(T),
+                                             _ptr(depth), _ptr(attr)))
+        return rgb, T, depth, attr
 
     # ---- stage functions ----
     def cascade_march(self, g, o, d, t0, t1, ray_id, jitter, batch_id, capacity=None):

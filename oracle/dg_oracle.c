@@ -1204,9 +1204,20 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
   return rc;
 }
 
-/* DistributedRun::dispatch_eval + Worker::handle_eval_request (worker.cpp:564-600,757-829) */
+/* DistributedRun::dispatch_eval + Worker::handle_eval_request (worker.cpp:564-600,757-829),
+ * with the driver's early termination (worker.cpp:815-818) and, when attribution != NULL, the
+ * region-attribution colour of evaluate_image (worker.cpp:864-878) over the merged partials. */
+int or_run_eval_rays_ex(or_run* r, const double* origin, const double* dir, uint64_t n,
+                        const double* appearance, double* rgb, double* T, double* depth,
+                        double* attribution);
 int or_run_eval_rays(or_run* r, const double* origin, const double* dir, uint64_t n,
                      const double* appearance, double* rgb, double* T, double* depth) {
+  return or_run_eval_rays_ex(r, origin, dir, n, appearance, rgb, T, depth, NULL);
+}
+
+int or_run_eval_rays_ex(or_run* r, const double* origin, const double* dir, uint64_t n,
+                        const double* appearance, double* rgb, double* T, double* depth,
+                        double* attribution) {
   const or_model* m = &r->m;
   const dg_run_config* cfg = &m->cfg;
   const int f32 = cfg->wire_f32 != 0;
@@ -1221,6 +1232,7 @@ int or_run_eval_rays(or_run* r, const double* origin, const double* dir, uint64_
     rgb[3 * i] = rgb[3 * i + 1] = rgb[3 * i + 2] = 0.0;
     T[i] = 1.0;
     depth[i] = 0.0;
+    if (attribution) attribution[3 * i] = attribution[3 * i + 1] = attribution[3 * i + 2] = 0.0;
     if (d.nseg == 0) continue;
     d.ray_id = i;
     for (int a = 0; a < 3; ++a) {
@@ -1246,11 +1258,34 @@ int or_run_eval_rays(or_run* r, const double* origin, const double* dir, uint64_
       pT[s] = fround(tt, f32);
       pdep[s] = fround(dep, f32);
     }
+    int used = d.nseg;
+    if (cfg->eval_early_termination) { /* worker.cpp:815-818: keep the entry that crosses */
+      double prefix = 1.0;
+      for (int s = 0; s < d.nseg; ++s) {
+        prefix *= pT[s];
+        if (prefix < cfg->eval_termination_threshold) {
+          used = s + 1;
+          break;
+        }
+      }
+    }
     double C[3], TT, D;
-    or_merge_forward(prgb, pT, pdep, d.nseg, C, &TT, &D);
+    or_merge_forward(prgb, pT, pdep, used, C, &TT, &D);
     for (int a = 0; a < 3; ++a) rgb[3 * i + a] = C[a];
     T[i] = TT;
     depth[i] = D;
+    if (attribution) { /* worker.cpp:864-878 */
+      double prefix = 1.0, at[3] = {0.0, 0.0, 0.0};
+      for (int s = 0; s < used; ++s) {
+        const double weight = prefix * (1.0 - pT[s]);
+        const double hue = (double)d.region[s] * 0.61803398875;
+        const double pal[3] = {0.5 + 0.5 * cos(6.2831853 * hue), 0.5 + 0.5 * cos(6.2831853 * (hue + 1.0 / 3.0)),
+                               0.5 + 0.5 * cos(6.2831853 * (hue + 2.0 / 3.0))};
+        for (int a = 0; a < 3; ++a) at[a] += pal[a] * weight;
+        prefix *= pT[s];
+      }
+      for (int a = 0; a < 3; ++a) attribution[3 * i + a] = at[a];
+    }
   }
   return 0;
 }

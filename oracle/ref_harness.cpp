@@ -70,6 +70,8 @@ RunConfig to_run_config(const dg_run_config& c) {
   r.lr_start = c.lr_start;
   r.lr_end = c.lr_end;
   r.distortion_cross_correction = c.distortion_cross_correction != 0;
+  r.eval_early_termination = c.eval_early_termination != 0;
+  r.eval_termination_threshold = c.eval_termination_threshold;
   return r;
 }
 
@@ -297,6 +299,46 @@ int refh_eval_rays(void* p, const double* origin, const double* dir, uint64_t n,
   }
 }
 
+// DistributedRun::evaluate_image (worker.cpp:836-880): colour, T, depth, attribution per pixel.
+int refh_eval_image(void* p, const dg_camera* cam, const double* appearance, double* rgb,
+                    double* transmittance, double* depth, double* attribution) {
+  auto* h = static_cast<Harness*>(p);
+  try {
+    CameraPose pose;
+    pose.image_id = cam->image_id;
+    for (int j = 0; j < 9; ++j) pose.rotation.m[j] = cam->rotation[j];
+    pose.translation = Vec3{cam->translation[0], cam->translation[1], cam->translation[2]};
+    pose.fx = cam->fx;
+    pose.fy = cam->fy;
+    pose.cx = cam->cx;
+    pose.cy = cam->cy;
+    pose.width = cam->width;
+    pose.height = cam->height;
+    std::vector<double> app(appearance, appearance + h->config.appearance_dim);
+    h->run->start();
+    EvalImage img;
+    try {
+      img = h->run->evaluate_image(pose, app);
+    } catch (...) {
+      h->run->stop();
+      throw;
+    }
+    h->run->stop();
+    const uint64_t n = uint64_t(cam->width) * cam->height;
+    for (uint64_t i = 0; i < n; ++i) {
+      for (int k = 0; k < 3; ++k) {
+        rgb[3 * i + k] = img.color[i][k];
+        attribution[3 * i + k] = img.attribution[i][k];
+      }
+      transmittance[i] = img.transmittance[i];
+      depth[i] = img.depth[i];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // ---- stage functions ----
 
 int refh_segment_rays(const dg_run_config* cfg, const double* origin, const double* dir,
@@ -511,6 +553,8 @@ void refh_default_config(dg_run_config* c) {
   c->wire_f32 = r.wire_f32;
   c->distortion_cross_correction = r.distortion_cross_correction;
   c->occupancy_updates = 1;
+  c->eval_early_termination = r.eval_early_termination;
+  c->eval_termination_threshold = r.eval_termination_threshold;
 }
 
 // ---- CPU baseline: T replicas of the reference DistributedRun, one per host thread ----

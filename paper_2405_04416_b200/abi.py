@@ -39,7 +39,8 @@ class RunConfig(C.Structure):
         ("transmittance_clamp", C.c_double),
         ("adam_beta1", C.c_double), ("adam_beta2", C.c_double), ("adam_eps", C.c_double),
         ("wire_f32", C.c_uint32), ("distortion_cross_correction", C.c_uint32),
-        ("occupancy_updates", C.c_uint32), ("reserved", C.c_uint32),
+        ("occupancy_updates", C.c_uint32), ("eval_early_termination", C.c_uint32),
+        ("eval_termination_threshold", C.c_double),
     ]
 
     def copy(self):
@@ -71,7 +72,7 @@ class StepStats(C.Structure):
 
 class Merged(C.Structure):
     _fields_ = [("rgb", C.c_void_p), ("transmittance", C.c_void_p), ("depth", C.c_void_p),
-                ("mem", C.c_int32), ("reserved", C.c_int32)]
+                ("attribution", C.c_void_p), ("mem", C.c_int32), ("reserved", C.c_int32)]
 
 
 class ArrayDesc(C.Structure):
@@ -150,4 +151,6 @@ def default_config():
     c.wire_f32 = 0
     c.distortion_cross_correction = 0
     c.occupancy_updates = 1
+    c.eval_early_termination = 0
+    c.eval_termination_threshold = 1e-4
     return c

@@ -251,4 +251,18 @@ __device__ __forceinline__ uint32_t table_row(const LevelDesc& lv, uint32_t ix, 
   return (ix ^ (iy * 2654435761u) ^ (iz * 805459861u)) & lv.mask;
 }
 
+// CameraPose::pixel_ray_dir (partition.cpp:30-33): normalize(R * ((x - cx)/fx, (y - cy)/fy, 1)),
+// Mat3 * Vec3 row by row left to right, normalize = v / sqrt(dot(v, v)); fp64, bit-exact.
+__device__ __forceinline__ void pixel_ray_dir(const double R[9], double fx, double fy, double cx, double cy,
+                                              double x, double y, double out[3]) {
+  const double cam[3] = {ddiv(dsub(x, cx), fx), ddiv(dsub(y, cy), fy), 1.0};
+  double v[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    v[r] = dadd(dadd(dmul(R[3 * r], cam[0]), dmul(R[3 * r + 1], cam[1])), dmul(R[3 * r + 2], cam[2]));
+  const double len = __dsqrt_rn(dadd(dadd(dmul(v[0], v[0]), dmul(v[1], v[1])), dmul(v[2], v[2])));
+#pragma unroll
+  for (int a = 0; a < 3; ++a) out[a] = ddiv(v[a], len);
+}
+
 }  // namespace dg

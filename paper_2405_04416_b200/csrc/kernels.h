@@ -81,8 +81,11 @@ void launch_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P, const ui
 // eval: home merge in schedule order from item partials (world == 1) or reply records
 void launch_home_merge(uint64_t n, uint32_t P, const uint8_t* nseg, const uint8_t* sched,
                        const uint8_t* slot_of_part, const uint32_t* pos, const float4* partial,
-                       const float* depth, const PartialRec* reply, int wire_f32, float* rgb,
-                       float* trans, float* depth_out, cudaStream_t s);
+                       const float* depth, const PartialRec* reply, int wire_f32, float* rgb, float* trans,
+                       float* depth_out, int early_term, double term_thr, float* attribution,
+                       cudaStream_t s);
+void launch_camera_rays(const double* pose, uint32_t width, uint64_t n, double* o, double* d,
+                        cudaStream_t s);
 
 // stage-entry helpers
 void launch_segment_full(const Geo* geo, const double* o, const double* d, uint64_t n, uint8_t* nseg,

@@ -428,16 +428,21 @@ __global__ void k_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P,
   out[t] = cscan[row + part_item_off[lp + 1]] - cscan[row + part_item_off[lp]];
 }
 
+// dispatch_eval's driver merge in schedule order (worker.cpp:801-826): optional early
+// termination once the running transmittance drops below the threshold (the crossing entry
+// is kept, worker.cpp:815-818) and the region-attribution colour of evaluate_image
+// (worker.cpp:864-878) over the merged entries.
 __global__ void k_home_merge(uint64_t n, const uint8_t* __restrict__ nseg,
                              const uint8_t* __restrict__ sched, const uint8_t* __restrict__ slot_of_part,
                              const uint32_t* __restrict__ pos, const float4* __restrict__ partial,
                              const float* __restrict__ depth, const PartialRec* __restrict__ reply,
                              float* __restrict__ rgb, float* __restrict__ trans,
-                             float* __restrict__ depth_out) {
+                             float* __restrict__ depth_out, int early_term, double term_thr,
+                             float* __restrict__ attribution) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int ns = nseg[i];
-  double C[3] = {0.0, 0.0, 0.0}, prefix = 1.0, dep = 0.0;
+  double C[3] = {0.0, 0.0, 0.0}, prefix = 1.0, dep = 0.0, at[3] = {0.0, 0.0, 0.0};
   for (int s = 0; s < ns; ++s) {
     const uint32_t p = sched[i * kMaxSeg + s];
     const uint32_t idx = pos[(uint64_t)slot_of_part[p] * n + i];
@@ -455,13 +460,45 @@ __global__ void k_home_merge(uint64_t n, const uint8_t* __restrict__ nseg,
     C[1] += v.y * prefix;
     C[2] += v.z * prefix;
     dep += dp * prefix;
-    prefix *= exp(-(double)v.w);
+    const double Ts = exp(-(double)v.w);
+    if (attribution) {
+      const double w = prefix * (1.0 - Ts), hue = (double)p * 0.61803398875;
+      at[0] += (0.5 + 0.5 * cos(6.2831853 * hue)) * w;
+      at[1] += (0.5 + 0.5 * cos(6.2831853 * (hue + 1.0 / 3.0))) * w;
+      at[2] += (0.5 + 0.5 * cos(6.2831853 * (hue + 2.0 / 3.0))) * w;
+    }
+    prefix *= Ts;
+    if (early_term && prefix < term_thr) break;
   }
   rgb[3 * i] = (float)C[0];
   rgb[3 * i + 1] = (float)C[1];
   rgb[3 * i + 2] = (float)C[2];
   trans[i] = (float)prefix;
   depth_out[i] = (float)dep;
+  if (attribution) {
+    attribution[3 * i] = (float)at[0];
+    attribution[3 * i + 1] = (float)at[1];
+    attribution[3 * i + 2] = (float)at[2];
+  }
+}
+
+// evaluate_image ray generation (worker.cpp:841-853): pixel (x, y) of one camera, row-major.
+__global__ void k_camera_rays(const double* __restrict__ pose, uint32_t width, uint64_t n,
+                              double* __restrict__ o, double* __restrict__ d) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t x = (uint32_t)(i % width), y = (uint32_t)(i / width);
+  // pose: R[9], t[3], fx, fy, cx, cy
+  double R[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = pose[k];
+  double dd[3];
+  pixel_ray_dir(R, pose[12], pose[13], pose[14], pose[15], dadd((double)x, 0.5), dadd((double)y, 0.5), dd);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    o[3 * i + a] = pose[9 + a];
+    d[3 * i + a] = dd[a];
+  }
 }
 
 __global__ void k_segment_full(const Geo* __restrict__ geo, const double* __restrict__ o,
@@ -610,10 +647,18 @@ void launch_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P, const ui
 void launch_home_merge(uint64_t n, uint32_t, const uint8_t* nseg, const uint8_t* sched,
                        const uint8_t* slot_of_part, const uint32_t* pos, const float4* partial,
                        const float* depth, const PartialRec* reply, int, float* rgb, float* trans,
-                       float* depth_out, cudaStream_t s) {
+                       float* depth_out, int early_term, double term_thr, float* attribution,
+                       cudaStream_t s) {
   if (!n) return;
   k_home_merge<<<blocks(n, 256), 256, 0, s>>>(n, nseg, sched, slot_of_part, pos, partial, depth,
-                                              reply, rgb, trans, depth_out);
+                                              reply, rgb, trans, depth_out, early_term, term_thr,
+                                              attribution);
+}
+
+void launch_camera_rays(const double* pose, uint32_t width, uint64_t n, double* o, double* d,
+                        cudaStream_t s) {
+  if (!n) return;
+  k_camera_rays<<<blocks(n, 128), 128, 0, s>>>(pose, width, n, o, d);
 }
 
 void launch_segment_full(const Geo* geo, const double* o, const double* d, uint64_t n, uint8_t* nseg,

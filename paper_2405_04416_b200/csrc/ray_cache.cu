@@ -16,7 +16,7 @@
 #include <string>
 #include <vector>
 
-#include "dg_common.cuh"
+#include "geometry.cuh"
 
 namespace dg {
 int set_error(int code, const char* msg);
@@ -40,18 +40,13 @@ __global__ void k_make_pixel_rays(const DevPose* __restrict__ poses, const uint8
   if (i >= n) return;
   const uint32_t img = req[4 * i], x = req[4 * i + 1], y = req[4 * i + 2], slot = req[4 * i + 3];
   const DevPose& p = poses[img];
-  const double cam[3] = {ddiv(dsub(dadd((double)x, 0.5), p.cx), p.fx),
-                         ddiv(dsub(dadd((double)y, 0.5), p.cy), p.fy), 1.0};
-  double v[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-    v[r] = dadd(dadd(dmul(p.R[3 * r], cam[0]), dmul(p.R[3 * r + 1], cam[1])), dmul(p.R[3 * r + 2], cam[2]));
-  const double len = __dsqrt_rn(dadd(dadd(dmul(v[0], v[0]), dmul(v[1], v[1])), dmul(v[2], v[2])));
+  double dd[3];
+  pixel_ray_dir(p.R, p.fx, p.fy, p.cx, p.cy, dadd((double)x, 0.5), dadd((double)y, 0.5), dd);  // dataset.cpp:317
   const uint8_t* px = pixels + p.pixel_off + ((uint64_t)y * p.width + x) * 3;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     origin[3 * (uint64_t)slot + a] = p.t[a];
-    dir[3 * (uint64_t)slot + a] = ddiv(v[a], len);
+    dir[3 * (uint64_t)slot + a] = dd[a];
     gt[3 * (uint64_t)slot + a] = (float)ddiv((double)px[a], 255.0);  // Image::pixel_channel
   }
   image[slot] = p.image_id;

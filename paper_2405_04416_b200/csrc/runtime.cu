@@ -162,6 +162,7 @@ struct dg_ctx {
   dg_stage_times times{};
 
   // persistent device state
+  DBuf out_attr, cam_o, cam_d, cam_pose;
   DBuf d_geo, d_parts, d_fields, params, grads, adam_m, adam_v, occ, occ_den, app, slot_of_part_d,
       local_of_global_d, global_of_local_d;
   // per-step scratch
@@ -1000,6 +1001,8 @@ void dg_default_config(dg_run_config* c) {
   c->adam_beta2 = 0.99;
   c->adam_eps = 1e-15;
   c->occupancy_updates = 1;
+  c->eval_early_termination = 0;          // config.hpp:60-61
+  c->eval_termination_threshold = 1e-4;
 }
 
 double dg_lr_at(const dg_run_config* cfg, uint64_t step) {  // train.cpp:77-80
@@ -1470,6 +1473,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   float* rgb = out->rgb;
   float* tr = out->transmittance;
   float* dep = out->depth;
+  float* attr = out->attribution;
   if (out->mem != DG_MEM_DEVICE) {
     TRY(c->out_rgb.ensure(n * 12 + 16));
     TRY(c->out_T.ensure(n * 4 + 16));
@@ -1477,6 +1481,10 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
     rgb = c->out_rgb.as<float>();
     tr = c->out_T.as<float>();
     dep = c->out_depth.as<float>();
+    if (attr) {
+      TRY(c->out_attr.ensure(n * 12 + 16));
+      attr = c->out_attr.as<float>();
+    }
   }
   const PartialRec* reply = nullptr;
   if (c->world > 1) {
@@ -1547,15 +1555,43 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   }
   launch_home_merge(n, c->P, c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(),
                     c->slot_of_part_d.as<uint8_t>(), c->h_pos.as<uint32_t>(), it.partial, it.depth,
-                    reply, int(c->cfg.wire_f32), rgb, tr, dep, s);
+                    reply, int(c->cfg.wire_f32), rgb, tr, dep, int(c->cfg.eval_early_termination),
+                    c->cfg.eval_termination_threshold, attr, s);
   ++c->launches;
   if (out->mem != DG_MEM_DEVICE && n) {
     CU(cudaMemcpyAsync(out->rgb, rgb, n * 12, cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(out->transmittance, tr, n * 4, cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(out->depth, dep, n * 4, cudaMemcpyDeviceToHost, s));
+    if (attr) CU(cudaMemcpyAsync(out->attribution, attr, n * 12, cudaMemcpyDeviceToHost, s));
   }
   CU(cudaStreamSynchronize(s));
   return DG_OK;
+}
+
+// DistributedRun::evaluate_image (worker.cpp:836-880): one ray per pixel (row-major, pixel
+// centres, CameraPose::pixel_ray_dir) generated on the device, rendered through dg_render;
+// out arrays hold width * height entries (attribution optional).  Ray ids are pixel indices.
+int dg_render_image(dg_ctx* c, const dg_camera* cam, const float* appearance, dg_merged* out) {
+  TRY(check_ctx(c));
+  if (!cam || !out || cam->width == 0 || cam->height == 0) return set_err(DG_EINVAL, "render_image: bad camera");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const uint64_t n = uint64_t(cam->width) * cam->height;
+  double pose[16];
+  for (int k = 0; k < 9; ++k) pose[k] = cam->rotation[k];
+  for (int k = 0; k < 3; ++k) pose[9 + k] = cam->translation[k];
+  pose[12] = cam->fx;
+  pose[13] = cam->fy;
+  pose[14] = cam->cx;
+  pose[15] = cam->cy;
+  TRY(upload(c->cam_pose, pose, sizeof pose, s));
+  TRY(c->cam_o.ensure(n * 24 + 16));
+  TRY(c->cam_d.ensure(n * 24 + 16));
+  launch_camera_rays(c->cam_pose.as<double>(), cam->width, n, c->cam_o.as<double>(), c->cam_d.as<double>(), s);
+  ++c->launches;
+  std::vector<uint32_t> img(1, cam->image_id);
+  dg_ray_batch b{c->cam_o.as<double>(), c->cam_d.as<double>(), nullptr, nullptr, n, 0, DG_MEM_DEVICE, 0};
+  return dg_render(c, &b, appearance, out);
 }
 
 int dg_comm_unique_id(uint8_t id[DG_NCCL_UNIQUE_ID_BYTES]) {

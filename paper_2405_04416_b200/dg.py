@@ -239,17 +239,32 @@ class Context:
         """Zero-copy variant for pre-built RayBatch structs (device or pinned host)."""
         return lib().dg_train_step(self.h, C.byref(batch), C.c_uint64(step), C.byref(stats))
 
-    def render(self, origin, dir, appearance, first_ray_id=0):
+    def render_image(self, camera, appearance):
+        """evaluate_image (worker.cpp:836-880) for a camera dict: rgb, T, depth, attribution."""
+        from .abi import cameras
+        cam = cameras([camera])
+        n = camera["width"] * camera["height"]
+        rgb, T, depth = np.zeros((n, 3), np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        attr = np.zeros((n, 3), np.float32)
+        m = Merged()
+        m.rgb, m.transmittance, m.depth, m.attribution, m.mem = _p(rgb), _p(T), _p(depth), _p(attr), DG_MEM_HOST
+        app = _c32(appearance)
+        _check(lib().dg_render_image(self.h, cam, _p(app), C.byref(m)))
+        return rgb, T, depth, attr
+
+    def render(self, origin, dir, appearance, first_ray_id=0, attribution=False):
         b = self._batch(origin, dir, None, None, first_ray_id)
         n = b.n
         rgb = np.zeros((n, 3), dtype=np.float32)
         T = np.zeros(n, dtype=np.float32)
         depth = np.zeros(n, dtype=np.float32)
+        attr = np.zeros((n, 3), dtype=np.float32) if attribution else None
         m = Merged()
         m.rgb, m.transmittance, m.depth, m.mem = _p(rgb), _p(T), _p(depth), DG_MEM_HOST
+        m.attribution = _p(attr)
         app = _c32(appearance)
         _check(lib().dg_render(self.h, C.byref(b), _p(app), C.byref(m)))
-        return rgb, T, depth
+        return (rgb, T, depth, attr) if attribution else (rgb, T, depth)
 
     def render_raw(self, batch, app, merged):
         return lib().dg_render(self.h, C.byref(batch), _p(app), C.byref(merged))

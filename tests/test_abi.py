@@ -26,10 +26,10 @@ def test_exports_every_header_symbol():
 
 def test_struct_sizes_match_header():
     # sizes the C side expects (checked against offsets of trailing fields)
-    assert C.sizeof(abi.RunConfig) == 312
+    assert C.sizeof(abi.RunConfig) == 320
     assert C.sizeof(abi.RayBatch) == 56
     assert C.sizeof(abi.StepStats) == 96
-    assert C.sizeof(abi.Merged) == 32
+    assert C.sizeof(abi.Merged) == 40
 
 
 def test_default_config_matches_reference_defaults():

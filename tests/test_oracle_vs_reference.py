@@ -114,3 +114,57 @@ def test_train_and_eval_identical(kx, ky, wire_f32, occ):
     b = orc.eval_rays(o, d, app[1])
     for x, y in zip(a, b):
         assert same(x, y)
+
+
+def _camera_rays(cam):
+    """Pixel-centre rays of a camera (row-major) through the oracle's make_pixel_ray, which
+    tests/test_ray_cache.py pins bitwise to the reference."""
+    import ctypes as C
+    from oracle.bindings import oracle_lib
+    from paper_2405_04416_b200.abi import cameras
+    L = oracle_lib()
+    L.or_make_pixel_ray.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p]
+    k = cameras([cam])
+    img = np.zeros((cam["height"], cam["width"], 3), np.uint8)
+    n = cam["width"] * cam["height"]
+    o, d, col = np.zeros((n, 3)), np.zeros((n, 3)), np.zeros(3)
+    iid, pid = C.c_uint32(), C.c_uint64()
+    for y in range(cam["height"]):
+        for x in range(cam["width"]):
+            i = y * cam["width"] + x
+            L.or_make_pixel_ray(C.cast(k, C.c_void_p), img.ctypes.data, x, y, o[i].ctypes.data, d[i].ctypes.data,
+                                col.ctypes.data, C.byref(iid), C.byref(pid))
+    return o, d
+
+
+def eval_camera(kx=2, ky=2):
+    """A camera above a kx x ky scene looking down at its centre (rays cross regions)."""
+    pos = np.array([kx * 0.5 + 0.3, ky * 0.5 - 0.2, 2.2])
+    fwd = np.array([kx * 0.5, ky * 0.5, 0.0]) - pos
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, [0.0, 1.0, 0.0])
+    right /= np.linalg.norm(right)
+    down = np.cross(fwd, right)
+    return dict(image_id=0, width=24, height=18, is_train=1, rotation=np.stack([right, down, fwd], axis=1),
+                translation=pos, fx=14.0, fy=14.5, cx=12.2, cy=8.9)
+
+
+@pytest.mark.parametrize("early", [0, 1])
+def test_eval_image_attribution_and_early_termination(early):
+    """evaluate_image (worker.cpp:836-880) with and without the driver's early termination
+    (worker.cpp:815-818): the restatement's colour, T, depth and attribution are the
+    reference's, bitwise."""
+    cfg = small_cfg(2, 2, table_log2=12, levels=6, nmax=128, divisor=48, occ_res=16)
+    cfg.eval_early_termination = early
+    cfg.eval_termination_threshold = 0.6
+    app = app_rows(1)
+    ref, orc = RefRun(cfg, app), OracleRun(cfg, app)
+    inject(cfg, None, [ref, orc], table_scale=0.5)
+    cam = eval_camera()
+    o, d = _camera_rays(cam)
+    a = ref.eval_image(cam, app[0])
+    b = orc.eval_rays_attribution(o, d, app[0])
+    for x, y in zip(a, b):
+        assert same(x, y)
+    assert np.abs(a[3]).sum() > 0
