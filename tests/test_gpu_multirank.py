@@ -125,3 +125,17 @@ def test_two_ranks_match_single_rank():
             errs.append(errq.get())
         assert not errs, errs
         assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+def test_nccl_backend_initialises_single_rank():
+    """The NCCL backend loads (dlopen of libnccl.so.2, torch's copy when present) and builds a
+    communicator; with one rank the exchanges alias, so a step runs unchanged."""
+    from paper_2405_04416_b200 import dg
+    cfg = _cfg()
+    ctx = dg.Context(cfg, device=0)
+    ctx.comm_init_nccl(dg.nccl_unique_id())
+    inject(cfg, ctx, [], occupancy_fraction=0.6)
+    ctx.set_appearance(app_rows(1).astype(np.float32))
+    o, d, gt, img = _rays()
+    st = ctx.train_step(o[:500], d[:500], gt[:500], img[:500], step=0)
+    assert st["rays"] == 500
