@@ -19,7 +19,7 @@ from .abi import (DG_MAX_SEGMENTS, DG_MEM_DEVICE, DG_MEM_HOST, ArrayDesc, ItemVi
                   RayBatch, RunConfig, StageTimes, StepStats)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdg_b200.so")
+LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg_b200.so")  # DG_LIB: A/B builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "distgrid_b200.h")
 
 P = C.c_void_p
