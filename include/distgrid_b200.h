@@ -89,7 +89,7 @@ typedef struct dg_run_config {
   double transmittance_clamp;
   double adam_beta1, adam_beta2, adam_eps;
   uint32_t wire_f32;                    /* config.hpp:21 (partials are f32 on this path) */
-  uint32_t distortion_cross_correction; /* config.hpp:56; must be 0 */
+  uint32_t distortion_cross_correction; /* config.hpp:56 (worker.cpp:289-299, 453-511) */
   uint32_t occupancy_updates;           /* 1: run Worker::update_occupancy cadence */
   uint32_t eval_early_termination;      /* config.hpp:60 (dispatch_eval, worker.cpp:815-818) */
   double eval_termination_threshold;    /* config.hpp:61 */

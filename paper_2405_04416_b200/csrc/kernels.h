@@ -27,6 +27,8 @@ struct ItemArrays {
   uint32_t* cscan;    // exclusive scan of contains
   float4* partial;    // rgb, optical depth tau (T = exp(-tau)) of my segment
   float* depth;       // depth_sum of my segment
+  float4* xdist;      // distortion_cross_correction only (else null): weight_sum,
+                      // weight_moment, distortion_local of my segment (worker.cpp:289-299)
 };
 
 struct SampleArrays {
@@ -69,12 +71,12 @@ void launch_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, uint32_t
                       int with_depth, cudaStream_t s);
 void launch_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                           const uint8_t* local_of_global, const uint64_t* stream_off,
-                          uint32_t P, PartialRec* send, cudaStream_t s);
+                          uint32_t P, PartialRec* send, float4* send_x, cudaStream_t s);
 void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                            const PartDesc* parts, const uint64_t* stream_off, uint32_t P,
-                           const PartialRec* recv, SampleArrays sm, uint32_t fine_total,
-                           double lambda_t, double lambda_d, double t_clamp, int wire_f32,
-                           LossAccum* loss, cudaStream_t s);
+                           const PartialRec* recv, const float4* recv_x, SampleArrays sm,
+                           uint32_t fine_total, double lambda_t, double lambda_d, double t_clamp,
+                           int wire_f32, LossAccum* loss, cudaStream_t s);
 void launch_pair_counts(uint32_t n_items, uint32_t n_local, uint32_t P, const uint32_t* part_item_off,
                         const uint32_t* contains, const uint32_t* cscan, uint32_t* out,
                         cudaStream_t s);

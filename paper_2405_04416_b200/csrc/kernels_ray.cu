@@ -221,6 +221,12 @@ __global__ void k_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, in
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_items) return;
   float T = 1.0f, tau = 0.0f, r = 0.0f, g = 0.0f, b = 0.0f, dep = 0.0f;
+  // distortion aggregates for the cross-segment correction (local_distortion_inputs,
+  // worker.cpp:62-75, and loss_distortion, train.cpp:38-57): s, ds on the ray's [t0, t1]
+  const bool xd = it.xdist != nullptr;
+  const double ray_t0 = xd ? it.t0[i] : 0.0;
+  const float inv_span = xd ? (float)(1.0 / (it.t1[i] - ray_t0)) : 0.0f;
+  float Wp = 0.0f, Mp = 0.0f, pair = 0.0f, interval = 0.0f;
   for_item_samples(it, n_items, i, [&](uint32_t s) {
     const float4 o = sm.out[s];
     const float x = o.x * (float)sm.delta[s];
@@ -230,11 +236,20 @@ __global__ void k_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, in
     g = fmaf(o.z, w, g);
     b = fmaf(o.w, w, b);
     if (with_depth) dep = fmaf(w, (float)sm.t[s], dep);
+    if (xd) {
+      const float ss = (float)(sm.t[s] - ray_t0) * inv_span;
+      const float ds = (float)sm.delta[s] * inv_span;
+      pair += 2.0f * w * (ss * Wp - Mp);
+      interval += w * w * ds;
+      Wp += w;
+      Mp += w * ss;
+    }
     T *= expf(-x);
     tau += x;
   });
   it.partial[i] = make_float4(r, g, b, tau);
   it.depth[i] = dep;
+  if (xd) it.xdist[i] = make_float4(Wp, Mp, pair + interval / 3.0f, 0.0f);
 }
 
 __device__ __forceinline__ uint32_t ordinal(const ItemArrays& it, uint32_t n_items,
@@ -247,7 +262,7 @@ __device__ __forceinline__ uint32_t ordinal(const ItemArrays& it, uint32_t n_ite
 __global__ void k_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* __restrict__ part_item_off,
                                 const uint8_t* __restrict__ global_of_local,
                                 const uint64_t* __restrict__ stream_off, uint32_t P,
-                                PartialRec* __restrict__ send) {
+                                PartialRec* __restrict__ send, float4* __restrict__ send_x) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_items) return;
   const uint32_t lp = it.part[i];
@@ -263,10 +278,13 @@ __global__ void k_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t*
   rec.depth = it.depth[i];
   rec.ray_id = it.rec[i].ray_id;
   const uint8_t* sc = it.sched + (uint64_t)i * kMaxSeg;
+  const float4 x = send_x ? it.xdist[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = 0; s < ns; ++s) {
     const uint32_t q = sc[s];
     if (q == gid) continue;
-    send[stream_off[gid * P + q] + ordinal(it, n_items, part_item_off, lp, q, i)] = rec;
+    const uint64_t at = stream_off[gid * P + q] + ordinal(it, n_items, part_item_off, lp, q, i);
+    send[at] = rec;
+    if (send_x) send_x[at] = x;
   }
 }
 
@@ -280,9 +298,9 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
                                  const uint32_t* __restrict__ part_item_off,
                                  const PartDesc* __restrict__ parts,
                                  const uint64_t* __restrict__ stream_off, uint32_t P,
-                                 const PartialRec* __restrict__ recv, SampleArrays sm,
-                                 double lambda_t, double lambda_d, double t_clamp, int wire_f32,
-                                 LossAccum* __restrict__ loss) {
+                                 const PartialRec* __restrict__ recv, const float4* __restrict__ recv_x,
+                                 SampleArrays sm, double lambda_t, double lambda_d, double t_clamp,
+                                 int wire_f32, LossAccum* __restrict__ loss) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double l_rgb = 0.0, l_t = 0.0, l_d = 0.0;
   uint32_t lp = 0;
@@ -294,18 +312,25 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
     const RayRec& rr = it.rec[i];
     const uint8_t* sc = it.sched + (uint64_t)i * kMaxSeg;
     double pc[kMaxSeg][3], pT[kMaxSeg], tau_tot = 0.0;
+    double xW[kMaxSeg], xM[kMaxSeg], xD[kMaxSeg];  // cross-correction aggregates per segment
+    const bool cross = it.xdist != nullptr;
     bool bad = false;
     for (int s = 0; s < ns; ++s) {
-      float4 v;
+      float4 v, xv = make_float4(0.f, 0.f, 0.f, 0.f);
       if (s == mo) {
         v = it.partial[i];
+        if (cross) xv = it.xdist[i];
       } else {
         const uint32_t q = sc[s];
-        const PartialRec rec =
-            recv[stream_off[q * P + gid] + ordinal(it, n_items, part_item_off, lp, q, i)];
+        const uint64_t at = stream_off[q * P + gid] + ordinal(it, n_items, part_item_off, lp, q, i);
+        const PartialRec rec = recv[at];
         if (rec.ray_id != rr.ray_id) bad = true;
         v = make_float4(rec.rgb[0], rec.rgb[1], rec.rgb[2], rec.tau);
+        if (cross) xv = recv_x[at];
       }
+      xW[s] = xv.x;
+      xM[s] = xv.y;
+      xD[s] = xv.z;
       pc[s][0] = v.x;
       pc[s][1] = v.y;
       pc[s][2] = v.z;
@@ -345,7 +370,39 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
       color_term += running * (up_c[0] * pc[k][0] + up_c[1] * pc[k][1] + up_c[2] * pc[k][2]);
       running *= pT[k];
     }
-    const double g_t = up_t * pre[mo] * suffix + pre[mo] * color_term;
+    double g_t = up_t * pre[mo] * suffix + pre[mo] * color_term;
+    // cross-segment distortion (worker.cpp:453-511): ray-level loss at the first owner, the
+    // cross terms of my samples' weight gradient, and d L / d T_mine through later prefixes
+    double lw = 0.0, lm = 0.0, ew = 0.0, em = 0.0, l_full = 0.0;
+    if (cross) {
+      if (sc[0] == gid) {
+        for (int m = 0; m < ns; ++m) l_full += pre[m] * pre[m] * xD[m];
+        for (int a = 0; a < ns; ++a)
+          for (int m = a + 1; m < ns; ++m) l_full += 2.0 * pre[a] * pre[m] * (xW[a] * xM[m] - xM[a] * xW[m]);
+      }
+      if (lambda_d > 0.0) {
+        for (int m = 0; m < ns; ++m) {
+          if (m > mo) {
+            lw += pre[m] * xW[m];
+            lm += pre[m] * xM[m];
+          } else if (m < mo) {
+            ew += pre[m] * xW[m];
+            em += pre[m] * xM[m];
+          }
+        }
+        double t_grad = 0.0;
+        for (int m = mo + 1; m < ns; ++m) {
+          double dl = 2.0 * pre[m] * xD[m];
+          for (int a = 0; a < m; ++a) dl += 2.0 * pre[a] * (xW[a] * xM[m] - xM[a] * xW[m]);
+          for (int m2 = m + 1; m2 < ns; ++m2) dl += 2.0 * pre[m2] * (xW[m] * xM[m2] - xM[m] * xW[m2]);
+          double prod_excl = 1.0;
+          for (int j = 0; j < m; ++j)
+            if (j != mo) prod_excl *= pT[j];
+          t_grad += dl * prod_excl;
+        }
+        g_t += lambda_d * t_grad;
+      }
+    }
     // local forward recompute: prefix per sample, distortion totals (worker.cpp:435-451)
     const double ray_t0 = it.t0[i];
     const float inv_span = (float)(1.0 / (it.t1[i] - ray_t0));
@@ -367,7 +424,9 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
     });
     Wt = Wp;
     Mt = Mp;
-    if (n > 0) l_d = (double)(pair + interval / 3.0f);
+    if (cross) l_d = l_full;  // only the first owner reports, the whole ray
+    else if (n > 0) l_d = (double)(pair + interval / 3.0f);
+    const float xp = (float)pre[mo], xlw = (float)lw, xlm = (float)lm, xew = (float)ew, xem = (float)em;
     // reverse sweep: local_render_backward with the distortion weight channel
     const float ucx = (float)g_c[0], ucy = (float)g_c[1], ucz = (float)g_c[2];
     const float ut = (float)g_t;
@@ -387,7 +446,7 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
       if (ld > 0.0f) {
         const float Wl = Wt - Ws - w, Ml = Mt - Ms - w * ss;
         const float gd = 2.0f * (ss * Wl - Ml) + 2.0f * (Ms - ss * Ws) + (2.0f / 3.0f) * w * ds;
-        wup = ld * gd;
+        wup = cross ? ld * (xp * xp * gd + 2.0f * xp * (xlm - ss * xlw + ss * xew - xem)) : ld * gd;
       }
       const float u = ucx * o.y + ucy * o.z + ucz * o.w + wup;
       const float alpha_grad = pf * (u - tail_c) - ut * pf * tail_t;
@@ -621,20 +680,20 @@ void launch_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, uint32_t
 
 void launch_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                           const uint8_t* global_of_local, const uint64_t* stream_off, uint32_t P,
-                          PartialRec* send, cudaStream_t s) {
+                          PartialRec* send, float4* send_x, cudaStream_t s) {
   if (!n_items) return;
   k_pack_partials<<<blocks(n_items, 256), 256, 0, s>>>(n_items, it, part_item_off, global_of_local,
-                                                       stream_off, P, send);
+                                                       stream_off, P, send, send_x);
 }
 
 void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                            const PartDesc* parts, const uint64_t* stream_off, uint32_t P,
-                           const PartialRec* recv, SampleArrays sm, uint32_t, double lambda_t,
-                           double lambda_d, double t_clamp, int wire_f32, LossAccum* loss,
-                           cudaStream_t s) {
+                           const PartialRec* recv, const float4* recv_x, SampleArrays sm, uint32_t,
+                           double lambda_t, double lambda_d, double t_clamp, int wire_f32,
+                           LossAccum* loss, cudaStream_t s) {
   if (!n_items) return;
   k_merge_backward<<<blocks(n_items, 128), 128, 0, s>>>(n_items, it, part_item_off, parts,
-                                                        stream_off, P, recv, sm, lambda_t,
+                                                        stream_off, P, recv, recv_x, sm, lambda_t,
                                                         lambda_d, t_clamp, wire_f32, loss);
 }
 

@@ -162,7 +162,8 @@ struct dg_ctx {
   dg_stage_times times{};
 
   // persistent device state
-  DBuf out_attr, cam_o, cam_d, cam_pose;
+  DBuf out_attr, cam_o, cam_d, cam_pose, it_xdist, send_x, recv_x;
+  bool cross_active = false;  // training step with distortion_cross_correction
   DBuf d_geo, d_parts, d_fields, params, grads, adam_m, adam_v, occ, occ_den, app, slot_of_part_d,
       local_of_global_d, global_of_local_d;
   // per-step scratch
@@ -196,8 +197,6 @@ int ctx_setup(dg_ctx* c) {
   if (cfg.base_resolution > cfg.max_resolution)
     return set_err(DG_EINVAL, "grid: base_resolution must be <= max_resolution");
   if (!(cfg.march_step_divisor > 0.0)) return set_err(DG_EINVAL, "march_step_divisor must be positive");
-  if (cfg.distortion_cross_correction)
-    return set_err(DG_EINVAL, "distortion_cross_correction is not supported on the device path");
   if (!(cfg.transmittance_clamp > 0.0 && cfg.transmittance_clamp < 1.0))
     return set_err(DG_EINVAL, "config: transmittance clamp must be in (0,1)");
   c->P = cfg.kx * cfg.ky;
@@ -444,6 +443,7 @@ ItemArrays item_arrays(dg_ctx* c) {
   it.cscan = c->it_cscan.as<uint32_t>();
   it.partial = c->it_partial.as<float4>();
   it.depth = c->it_depth.as<float>();
+  it.xdist = c->cross_active ? c->it_xdist.as<float4>() : nullptr;
   return it;
 }
 
@@ -629,6 +629,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   TRY(c->it_cscan.ensure((uint64_t(P) * NI + 1) * 4));
   TRY(c->it_partial.ensure(uint64_t(NI) * 16 + 16));
   TRY(c->it_depth.ensure(uint64_t(NI) * 4 + 16));
+  if (c->cfg.distortion_cross_correction) TRY(c->it_xdist.ensure(uint64_t(NI) * 16 + 16));
   CU(cudaMemsetAsync(c->it_cnt.as<uint32_t>() + 2ull * NI, 0, 4, s));
   CU(cudaMemsetAsync(c->it_contains.as<uint32_t>() + uint64_t(P) * NI, 0, 4, s));
   ItemArrays it = item_arrays(c);
@@ -768,7 +769,7 @@ MlpLaunch mlp_launch(dg_ctx* c, bool bwd) {
 // Exchange-2 stream tables.  Stream (q -> p) carries the partials of q's items whose
 // schedule contains p, in ray order; pair_cnt[lq][p] is known locally and is symmetric.
 int exchange_partials(dg_ctx* c, const std::vector<uint32_t>& pair_cnt, uint64_t* bytes_sent,
-                      const PartialRec** recv_out) {
+                      const PartialRec** recv_out, const float4** recv_x_out) {
   cudaStream_t s = c->stream;
   const uint32_t P = c->P, nl = uint32_t(c->local.size());
   const int W = c->world;
@@ -783,21 +784,38 @@ int exchange_partials(dg_ctx* c, const std::vector<uint32_t>& pair_cnt, uint64_t
   TRY(upload(c->stream_recv_d, recv_off.data(), recv_off.size() * 8, s));
   c->h2d += (send_off.size() + recv_off.size()) * 8;
   TRY(c->send_buf.ensure(so * sizeof(PartialRec) + 16));
+  // cross-segment distortion: the three aggregates travel in a parallel stream (16 B/record)
+  const bool cross = c->cross_active;
+  if (cross) TRY(c->send_x.ensure(so * sizeof(float4) + 16));
   launch_pack_partials(c->n_items, item_arrays(c), c->part_item_off_d.as<uint32_t>(),
                        c->global_of_local_d.as<uint8_t>(), c->stream_send_d.as<uint64_t>(), P,
-                       c->send_buf.as<PartialRec>(), s);
+                       c->send_buf.as<PartialRec>(), cross ? c->send_x.as<float4>() : nullptr, s);
   ++c->launches;
+  *recv_x_out = cross ? c->send_x.as<float4>() : nullptr;
   if (W == 1) {
     *recv_out = c->send_buf.as<PartialRec>();  // single rank: the streams alias
     return DG_OK;
   }
   TRY(c->recv_buf.ensure(ro * sizeof(PartialRec) + 16));
   std::string err;
-  const int rc = c->comm->alltoallv(c->send_buf.p, sbytes, c->recv_buf.p, rbytes, s, err);
+  int rc = c->comm->alltoallv(c->send_buf.p, sbytes, c->recv_buf.p, rbytes, s, err);
   if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
   for (int r = 0; r < W; ++r)
     if (r != c->rank) *bytes_sent += sbytes[r];
   *recv_out = c->recv_buf.as<PartialRec>();
+  if (cross) {
+    std::vector<uint64_t> xs(W), xr(W);
+    for (int r = 0; r < W; ++r) {
+      xs[r] = sbytes[r] / sizeof(PartialRec) * sizeof(float4);
+      xr[r] = rbytes[r] / sizeof(PartialRec) * sizeof(float4);
+    }
+    TRY(c->recv_x.ensure(ro * sizeof(float4) + 16));
+    rc = c->comm->alltoallv(c->send_x.p, xs, c->recv_x.p, xr, s, err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    for (int r = 0; r < W; ++r)
+      if (r != c->rank) *bytes_sent += xs[r];
+    *recv_x_out = c->recv_x.as<float4>();
+  }
   return DG_OK;
 }
 
@@ -1346,6 +1364,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   const uint32_t P = c->P, nl = uint32_t(c->local.size());
   uint64_t dropped = 0, bytes = 0;
   c->h2d = c->d2h = 0;
+  c->cross_active = c->cfg.distortion_cross_correction != 0;
   TRY(front_half(c, b, 1, step, &dropped, &bytes));
   const uint32_t NI = c->n_items;
   ItemArrays it = item_arrays(c);
@@ -1374,15 +1393,16 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   // X2: partial exchange (alias on a single rank)
   CU(cudaStreamSynchronize(s));  // pair counts on the host
   const PartialRec* recv = c->send_buf.as<PartialRec>();
+  const float4* recv_x = nullptr;
   if (P > 1) {
-    TRY(exchange_partials(c, pair_cnt, &bytes, &recv));
+    TRY(exchange_partials(c, pair_cnt, &bytes, &recv, &recv_x));
   } else {
     TRY(c->stream_recv_d.ensure(16));
   }
   mark(c, 6);
   // K5b merge / losses / composite backward
   launch_merge_backward(NI, it, c->part_item_off_d.as<uint32_t>(), c->d_parts.as<PartDesc>(),
-                        P > 1 ? c->stream_recv_d.as<uint64_t>() : nullptr, P, recv, sm,
+                        P > 1 ? c->stream_recv_d.as<uint64_t>() : nullptr, P, recv, recv_x, sm,
                         c->n_fine, c->cfg.lambda_transmittance, c->cfg.lambda_distortion,
                         c->cfg.transmittance_clamp, int(c->cfg.wire_f32), c->loss.as<LossAccum>(), s);
   mark(c, 7);
@@ -1447,6 +1467,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   CU(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
   uint64_t dropped = 0, bytes = 0;
+  c->cross_active = false;  // evaluation carries no distortion aggregates
   dg_ray_batch bb = *b;
   bb.color_gt = nullptr;
   bb.image_id = nullptr;

@@ -21,9 +21,13 @@ pytestmark = pytest.mark.gpu
 KX, KY, N, STEPS = 2, 2, 3000, 2
 
 
-def _cfg():
-    return small_cfg(KX, KY, table_log2=13, levels=8, nmax=256, divisor=128,
-                     inner=((0.3, 0.25, 0.0), (1.6, 1.8, 0.8)), occ_res=24)
+def _cfg(cross=0):
+    c = small_cfg(KX, KY, table_log2=13, levels=8, nmax=256, divisor=128,
+                  inner=((0.3, 0.25, 0.0), (1.6, 1.8, 0.8)), occ_res=24)
+    c.distortion_cross_correction = cross
+    if cross:
+        c.lambda_distortion = 0.05
+    return c
 
 
 def _rays():
@@ -44,13 +48,13 @@ def _gloo_alltoallv(blocks, recv_sizes):
     return out
 
 
-def _rank_main(rank, world, port, ref_path, errq):
+def _rank_main(rank, world, port, ref_path, errq, cross=0):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         from paper_2405_04416_b200 import dg
-        cfg = _cfg()
+        cfg = _cfg(cross)
         ctx = dg.Context(cfg, device=0, rank=rank, world=world)
         ctx.comm_init_host(_gloo_alltoallv)
         inject(cfg, None, [_LocalOnly(ctx)], occupancy_fraction=0.6)
@@ -91,9 +95,10 @@ class _LocalOnly:
             self.ctx.set_occupancy(g, c, bits)
 
 
-def test_two_ranks_match_single_rank():
+@pytest.mark.parametrize("cross", [0, 1])
+def test_two_ranks_match_single_rank(cross):
     from paper_2405_04416_b200 import dg
-    cfg = _cfg()
+    cfg = _cfg(cross)
     ctx = dg.Context(cfg, device=0)
     inject(cfg, ctx, [], occupancy_fraction=0.6)
     ctx.set_appearance(app_rows(1).astype(np.float32))
@@ -115,7 +120,7 @@ def test_two_ranks_match_single_rank():
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
         s.close()
-        procs = [mpc.Process(target=_rank_main, args=(r, 2, port, path, errq)) for r in range(2)]
+        procs = [mpc.Process(target=_rank_main, args=(r, 2, port, path, errq, cross)) for r in range(2)]
         for p in procs:
             p.start()
         for p in procs:
