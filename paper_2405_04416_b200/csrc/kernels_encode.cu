@@ -12,6 +12,8 @@
 //
 // Algorithmic traffic: 8 corners x L levels x 8 B = 1024 B/sample gathered
 // forward; the backward read-modify-writes the same 1024 B.
+#include <cstdlib>
+
 #include "geometry.cuh"
 #include "kernels.h"
 
@@ -169,7 +171,8 @@ __device__ __forceinline__ void st_stream(float2* p, float2 v) {
 // Warp-aggregated scatter of one level: lanes hold consecutive samples (mostly one ray, in t
 // order), so at coarse levels neighbouring lanes share cells and hence identical corner rows.
 // For each corner slot, runs of equal (field, row) in lane order are summed with a segmented
-// shuffle scan and the run's last lane issues a single float2 red.
+// shuffle scan and the run's last lane issues a single float2 red.  The scan runs only
+// ceil(log2(longest run)) steps (warp-uniform, from the run-head ballot).
 __device__ __forceinline__ void scatter_level_agg(float2* __restrict__ table, const Corners& c,
                                                   float2 up, uint32_t field, bool valid) {
   const unsigned lane = threadIdx.x & 31;
@@ -181,12 +184,15 @@ __device__ __forceinline__ void scatter_level_agg(float2* __restrict__ table, co
     const bool head = lane == 0 || prev_row != row || prev_fld != field;
     const unsigned heads = __ballot_sync(0xffffffffu, head);
     const unsigned run = 31u - __clz(heads & (0xffffffffu >> (31u - lane)));  // run start lane
+    // run length seen from its head lane: distance to the next head (or the warp end)
+    const unsigned later = lane < 31 ? heads & (0xfffffffeu << lane) : 0u;
+    const unsigned len = head ? (later ? (unsigned)(__ffs(later) - 1) : 32u) - lane : 0u;
+    const unsigned longest = __reduce_max_sync(0xffffffffu, len);
     float vx = c.w[k] * up.x, vy = c.w[k] * up.y;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
+    for (unsigned off = 1; off < longest; off <<= 1) {
       const float tx = __shfl_up_sync(0xffffffffu, vx, off);
       const float ty = __shfl_up_sync(0xffffffffu, vy, off);
-      if (lane >= (unsigned)off && lane - off >= run) {
+      if (lane >= off && lane - off >= run) {
         vx += tx;
         vy += ty;
       }
@@ -323,15 +329,35 @@ int launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s) {
     for (uint32_t i = 0; i < f.n_pass; ++i)
       if (f.pass[i].k == k) g.pass[g.n_pass++] = f.pass[i];
     if (!g.n_pass) break;
-    if (f.s_p) k_encode_fwd<true><<<dim3(nb, g.n_pass), 256, 0, s>>>(g, X);
-    else k_encode_fwd<false><<<dim3(nb, g.n_pass), 256, 0, s>>>(g, X);
-    ++launches;
+    static const bool split = std::getenv("DG_ENC_SPLIT_LAUNCH") != nullptr;  // per-pass timing
+    for (uint32_t i = 0; i < (split ? g.n_pass : 1u); ++i) {
+      FieldLaunch h = g;
+      if (split) {
+        h.n_pass = 1;
+        h.pass[0] = g.pass[i];
+      }
+      if (f.s_p) k_encode_fwd<true><<<dim3(nb, h.n_pass), 256, 0, s>>>(h, X);
+      else k_encode_fwd<false><<<dim3(nb, h.n_pass), 256, 0, s>>>(h, X);
+      ++launches;
+    }
   }
   return launches;
 }
 
 int launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s) {
   if (!f.n_total || !f.n_pass) return 0;
+  static const bool split = std::getenv("DG_ENC_SPLIT_LAUNCH") != nullptr;  // per-pass timing
+  if (split) {
+    for (uint32_t i = 0; i < f.n_pass; ++i) {
+      FieldLaunch g = f;
+      g.n_pass = 1;
+      g.pass[0] = f.pass[i];
+      const dim3 grid1((unsigned)((f.n_total + 255) / 256), 1);
+      if (f.s_p) k_encode_bwd<true><<<grid1, 256, 0, s>>>(g, dX);
+      else k_encode_bwd<false><<<grid1, 256, 0, s>>>(g, dX);
+    }
+    return int(f.n_pass);
+  }
   const dim3 grid((unsigned)((f.n_total + 255) / 256), f.n_pass);
   if (f.s_p) k_encode_bwd<true><<<grid, 256, 0, s>>>(f, dX);
   else k_encode_bwd<false><<<grid, 256, 0, s>>>(f, dX);

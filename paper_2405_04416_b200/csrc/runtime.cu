@@ -137,6 +137,7 @@ struct dg_ctx {
   uint64_t enc_budget_fwd = 256ull << 20;  // encode pass budgets (DG_ENC_FWD_MB / DG_ENC_BWD_MB)
   uint64_t enc_budget_bwd = 96ull << 20;
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
+  double enc_agg_samples_per_cell = 1.5;   // warp-aggregate levels with >= this many samples/cell (DG_ENC_AGG)
   uint64_t n_params = 0;
   uint64_t occ_bytes = 0;
   std::vector<double> occ_thr;            // [n_local][2] current thresholds
@@ -726,7 +727,7 @@ FieldLaunch field_launch(dg_ctx* c, uint64_t budget) {
   uint32_t agg = 0;
   const double ext = std::max(f0.box_hi[0] - f0.box_lo[0],
                               std::max(f0.box_hi[1] - f0.box_lo[1], f0.box_hi[2] - f0.box_lo[2]));
-  const double maxn_agg = ext / (1.5 * c->step);
+  const double maxn_agg = ext / (c->enc_agg_samples_per_cell * c->step);
   for (uint32_t l = 0; l < f0.L; ++l)
     if (double(std::max(f0.lv[l].n[0], std::max(f0.lv[l].n[1], f0.lv[l].n[2]))) <= maxn_agg) agg = l + 1;
   f.agg_levels = agg;
@@ -1044,6 +1045,7 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   if (const char* e = std::getenv("DG_ENC_FWD_MB"))
     c->enc_budget_fwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   if (const char* e = std::getenv("DG_ENC_PCACHE")) c->enc_pcache = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("DG_ENC_AGG")) c->enc_agg_samples_per_cell = std::max(0.01, std::atof(e));
   if (const char* e = std::getenv("DG_ENC_BWD_MB"))
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
