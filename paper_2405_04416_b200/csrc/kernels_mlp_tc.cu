@@ -25,7 +25,10 @@ namespace dg {
 namespace {
 
 constexpr int TM = 128;   // samples per tile (MMA M)
-constexpr int NTF = 256;  // forward: 8 warps, 2 CTAs/SM (their MMAs and epilogues interleave)
+#ifndef MLP_FWD_MINB
+#define MLP_FWD_MINB 2
+#endif
+constexpr int NTF = 256;  // forward: 8 warps, MLP_FWD_MINB CTAs/SM (their MMAs and epilogues interleave)
 constexpr int NTB = 512;  // backward: 16 warps, 1 CTA/SM (212 KB of operand tiles)
 // Warp w reads TMEM lane quadrant w % 4 (tcgen05.ld rule) and owns column part w / 4.
 
@@ -354,7 +357,7 @@ struct FwdTcSmem {
 // and 32 of the 64 hidden columns.  Activations never touch shared memory: each epilogue
 // writes the next layer's split operand straight into the TMEM A region.  TMEM: [0, 64) the
 // accumulator, [64, 128) the A operand.  Tiles are strided over the grid.
-__global__ void __launch_bounds__(NTF, 2) k_mlp_fwd_tc(MlpLaunch m) {
+__global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
   constexpr int NP = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   FwdTcSmem& sm = *reinterpret_cast<FwdTcSmem*>(smem_raw);
@@ -935,7 +938,7 @@ void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
     cudaFuncSetAttribute(k_mlp_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  const uint32_t want = (uint32_t)num_sms * 2;
+  const uint32_t want = (uint32_t)num_sms * MLP_FWD_MINB;
   const unsigned grid = m.n_tiles < want ? m.n_tiles : want;
   k_mlp_fwd_tc<<<grid, NTF, smem, s>>>(m);
 }
