@@ -474,6 +474,15 @@ class OracleModel:
                                  _ptr(rows))
         return out, rows
 
+    def encode_rows(self, g, cascade, pts):
+        """Hash-table rows only (no tables needed, any table size)."""
+        n = len(pts)
+        out = np.zeros((n, self.cfg.grid_levels * self.cfg.grid_features))
+        rows = np.zeros((n, self.cfg.grid_levels, 8), dtype=np.uint32)
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        self.lib.or_stage_encode(self.ptr, g, cascade, None, _ptr(pts), n, _ptr(out), _ptr(rows))
+        return rows
+
     def field_forward(self, g, cascade, params, pts, dirs, app):
         n = len(pts)
         sigma = np.zeros(n)

@@ -527,6 +527,7 @@ void or_encode(const or_grid* g, const double* table, const double p[3], double*
       }
       const uint32_t row = corner_row(g, l, &cw, c);
       if (rows) rows[l * 8 + c] = row;
+      if (!table) continue; /* rows only (full-size index checks without the tables) */
       const double* src = table + g->offset[l] + (size_t)row * F;
       for (uint32_t k = 0; k < F; ++k) dst[k] += w * src[k];
     }
@@ -1313,7 +1314,7 @@ int or_stage_cascade_march(const or_model* m, uint32_t region, const uint8_t* oc
 void or_stage_encode(const or_model* m, uint32_t region, uint32_t cascade, const double* params,
                      const double* pts, uint64_t n, double* out, uint32_t* rows) {
   const or_field_layout* f = &m->field[region][cascade];
-  const double* base = params + (cascade == 0 ? 0 : m->field[region][0].size);
+  const double* base = params ? params + (cascade == 0 ? 0 : m->field[region][0].size) : NULL;
   for (uint64_t i = 0; i < n; ++i)
     or_encode(&f->grid, base, pts + 3 * i, out + i * f->enc_width,
               rows ? rows + i * f->grid.L * 8 : NULL);
