@@ -78,7 +78,9 @@ struct PartDesc {    // one local partition (region)
   double fine_lo[3], fine_hi[3];
   double coarse_lo[3], coarse_hi[3];
   uint32_t occ_n[2][3];
-  uint64_t occ_off[2];  // byte offsets into the occupancy buffer
+  uint32_t occ_nb[2][3];  // bricks per axis of the bitfield (occ_addr)
+  uint64_t occ_off[2];    // byte offsets of the bricked bitfields in the occupancy buffer
+  uint64_t den_off[2];    // float offsets of the (linear) densities
   uint32_t global_id;
   uint32_t pad;
 };
@@ -88,6 +90,16 @@ struct Geo {         // PartitionManifest planes + outer box (partition.cpp:206-
   double xp[kMaxPart + 1], yp[kMaxPart + 1];
   uint32_t kx, ky, P, pad;
 };
+
+// Occupancy bitfield layout: 4 x 4 x 8 cell bricks of 128 bytes (one L1 line), bricks in
+// x-fastest order.  A ray's DDA walk (grid.cpp:235-304) touches a new line every 4-8 cells
+// instead of every cell a linear z-stride layout would cost.
+constexpr uint32_t kOccBX = 4, kOccBY = 4, kOccBZ = 8;
+__host__ __device__ __forceinline__ uint64_t occ_addr(const uint32_t nb[3], uint32_t x, uint32_t y,
+                                                       uint32_t z) {
+  const uint64_t brick = ((uint64_t)(z / kOccBZ) * nb[1] + y / kOccBY) * nb[0] + x / kOccBX;
+  return brick * (kOccBX * kOccBY * kOccBZ) + ((z % kOccBZ) * kOccBY + y % kOccBY) * kOccBX + x % kOccBX;
+}
 
 // Dispatch record (exchange 1): DispatchRay minus the schedule, which the owner
 // recomputes bit-exactly from (origin, dir).

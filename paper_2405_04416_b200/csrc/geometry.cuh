@@ -116,8 +116,8 @@ __device__ __forceinline__ void ladder(double iv_lo, double iv_hi, double t_ente
 template <class OnRun>
 __device__ __forceinline__ void occupancy_walk(const double o[3], const double d[3], double t0,
                                                double t1, const double lo[3], const double hi[3],
-                                               const uint32_t n[3], const uint8_t* bits,
-                                               OnRun& on_run) {
+                                               const uint32_t n[3], const uint32_t nb[3],
+                                               const uint8_t* bits, OnRun& on_run) {
   if (!(t1 > t0)) return;
   double cell[3], entry[3], t_next[3], t_delta[3];
   int idx[3], stp[3];
@@ -158,9 +158,7 @@ __device__ __forceinline__ void occupancy_walk(const double o[3], const double d
     if (t_next[1] < t_next[ea]) ea = 1;
     if (t_next[2] < t_next[ea]) ea = 2;
     const double t_exit = smin(t_next[ea], t1);
-    const uint64_t cidx =
-        (uint64_t)idx[0] + (uint64_t)n[0] * ((uint64_t)idx[1] + (uint64_t)n[1] * (uint64_t)idx[2]);
-    const bool occupied = bits[cidx] != 0;
+    const bool occupied = __ldg(bits + occ_addr(nb, (uint32_t)idx[0], (uint32_t)idx[1], (uint32_t)idx[2])) != 0;
     if (occupied && !run_open) {
       run_open = true;
       run_start = t_cur;
@@ -204,11 +202,13 @@ __device__ __forceinline__ bool cascade_march(const PartDesc& pd, const uint8_t*
   const uint8_t* occ_f = occ + pd.occ_off[0];
   const uint8_t* occ_c = occ + pd.occ_off[1];
   if (has_fine) {
-    if (fa > t0) occupancy_walk(o, d, t0, fa, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], occ_c, run);
-    occupancy_walk(o, d, fa, fb, pd.fine_lo, pd.fine_hi, pd.occ_n[0], occ_f, run);
-    if (fb < t1) occupancy_walk(o, d, fb, t1, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], occ_c, run);
+    if (fa > t0)
+      occupancy_walk(o, d, t0, fa, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], pd.occ_nb[1], occ_c, run);
+    occupancy_walk(o, d, fa, fb, pd.fine_lo, pd.fine_hi, pd.occ_n[0], pd.occ_nb[0], occ_f, run);
+    if (fb < t1)
+      occupancy_walk(o, d, fb, t1, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], pd.occ_nb[1], occ_c, run);
   } else {
-    occupancy_walk(o, d, t0, t1, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], occ_c, run);
+    occupancy_walk(o, d, t0, t1, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], pd.occ_nb[1], occ_c, run);
   }
   return has_fine;
 }

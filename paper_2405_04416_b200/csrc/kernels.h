@@ -180,7 +180,8 @@ void launch_occ_query(const FieldDesc* field, const float* params, const double*
                       float* sigma, cudaStream_t s);
 void launch_occ_apply(float* density, const uint32_t* cells, const float* sigma, uint64_t n,
                       float decay, cudaStream_t s);
-void launch_occ_bits(const float* density, uint8_t* bits, uint64_t n, float threshold, cudaStream_t s);
+void launch_occ_bits(const float* density, uint8_t* bits, const uint32_t shape[3], float threshold,
+                     cudaStream_t s);
 
 // ---- tcgen05 self-test (kernels_tc.cu) ----
 int tc_selftest(const float* A, const float* B, const float* X, float* Y0, float* Y1, float* Y2,

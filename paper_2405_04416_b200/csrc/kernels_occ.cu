@@ -87,10 +87,15 @@ __global__ void k_occ_apply(float* __restrict__ density, const uint32_t* __restr
   density[c] = fmaxf(density[c] * decay, sigma[s]);
 }
 
-__global__ void k_occ_bits(const float* __restrict__ density, uint8_t* __restrict__ bits,
-                           uint64_t n, float threshold) {
+// recompute_bitfield: density (linear, x fastest) >= threshold, into the bricked bitfield.
+__global__ void k_occ_bits(const float* __restrict__ density, uint8_t* __restrict__ bits, uint32_t nx,
+                           uint32_t ny, uint32_t nz, float threshold) {
   const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < n) bits[s] = density[s] >= threshold ? 1 : 0;
+  const uint64_t n = (uint64_t)nx * ny * nz;
+  if (s >= n) return;
+  const uint32_t x = (uint32_t)(s % nx), y = (uint32_t)((s / nx) % ny), z = (uint32_t)(s / ((uint64_t)nx * ny));
+  const uint32_t nb[3] = {(nx + kOccBX - 1) / kOccBX, (ny + kOccBY - 1) / kOccBY, (nz + kOccBZ - 1) / kOccBZ};
+  bits[occ_addr(nb, x, y, z)] = density[s] >= threshold ? 1 : 0;
 }
 
 inline unsigned nb(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
@@ -105,8 +110,10 @@ void launch_occ_apply(float* density, const uint32_t* cells, const float* sigma,
                       float decay, cudaStream_t s) {
   if (n) k_occ_apply<<<nb(n, 256), 256, 0, s>>>(density, cells, sigma, n, decay);
 }
-void launch_occ_bits(const float* density, uint8_t* bits, uint64_t n, float threshold, cudaStream_t s) {
-  if (n) k_occ_bits<<<nb(n, 256), 256, 0, s>>>(density, bits, n, threshold);
+void launch_occ_bits(const float* density, uint8_t* bits, const uint32_t shape[3], float threshold,
+                     cudaStream_t s) {
+  const uint64_t n = (uint64_t)shape[0] * shape[1] * shape[2];
+  if (n) k_occ_bits<<<nb(n, 256), 256, 0, s>>>(density, bits, shape[0], shape[1], shape[2], threshold);
 }
 
 }  // namespace dg

@@ -139,7 +139,8 @@ struct dg_ctx {
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
   double enc_agg_samples_per_cell = 1.5;   // warp-aggregate levels with >= this many samples/cell (DG_ENC_AGG)
   uint64_t n_params = 0;
-  uint64_t occ_bytes = 0;
+  uint64_t occ_bytes = 0;                 // bricked bitfields (all local partitions, both cascades)
+  uint64_t occ_den_n = 0;                 // linear densities (floats)
   std::vector<double> occ_thr;            // [n_local][2] current thresholds
   std::vector<std::mt19937_64> occ_rng;   // Worker::occ_rng_ per local partition (worker.cpp:186)
   uint64_t occ_updates = 0;
@@ -252,7 +253,7 @@ int ctx_setup(dg_ctx* c) {
   c->field_dev_off.assign(2 * nl, 0);
   c->field_size.assign(2 * nl, 0);
   c->field_segs.assign(2 * nl, {});
-  uint64_t poff = 0, ooff = 0;
+  uint64_t poff = 0, ooff = 0, doff = 0;
   for (uint32_t lp = 0; lp < nl; ++lp) {
     const uint32_t gid = c->local[lp];
     const uint32_t ix = gid % cfg.kx, iy = gid / cfg.kx;
@@ -279,9 +280,16 @@ int ctx_setup(dg_ctx* c) {
       const double aspect[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
       // occupancy grid (grid.cpp:161-172)
       grid_shape(aspect, cfg.occ_resolution, pd.occ_n[casc]);
-      pd.occ_off[casc] = ooff;
-      ooff += uint64_t(pd.occ_n[casc][0]) * pd.occ_n[casc][1] * pd.occ_n[casc][2];
-      ooff = (ooff + 15) & ~uint64_t(15);
+      const uint32_t bdim[3] = {kOccBX, kOccBY, kOccBZ};
+      uint64_t bricks = 1;
+      for (int a = 0; a < 3; ++a) {
+        pd.occ_nb[casc][a] = (pd.occ_n[casc][a] + bdim[a] - 1) / bdim[a];
+        bricks *= pd.occ_nb[casc][a];
+      }
+      pd.occ_off[casc] = ooff;  // bricked bitfield
+      ooff += bricks * (kOccBX * kOccBY * kOccBZ);
+      pd.den_off[casc] = doff;  // linear density
+      doff += uint64_t(pd.occ_n[casc][0]) * pd.occ_n[casc][1] * pd.occ_n[casc][2];
       // hash grid (grid.cpp:90-105) + MLPs (field.cpp:189-201)
       FieldDesc& fd = c->fields[casc * nl + lp];
       std::memset(&fd, 0, sizeof fd);
@@ -349,6 +357,7 @@ int ctx_setup(dg_ctx* c) {
   }
   c->n_params = poff;
   c->occ_bytes = std::max<uint64_t>(ooff, 16);
+  c->occ_den_n = std::max<uint64_t>(doff, 16);
   return DG_OK;
 }
 
@@ -379,9 +388,9 @@ int ctx_alloc(dg_ctx* c) {
   // occupancy densities start at the initial threshold (grid.cpp:188-191)
   const double thr0 = c->cfg.occ_threshold_early * c->cfg.occ_threshold_scale;
   c->occ_thr.assign(2 * c->local.size(), thr0);
-  TRY(c->occ_den.ensure(c->occ_bytes * sizeof(float)));
+  TRY(c->occ_den.ensure(c->occ_den_n * sizeof(float)));
   {
-    std::vector<float> den(c->occ_bytes, float(thr0));
+    std::vector<float> den(c->occ_den_n, float(thr0));
     CU(cudaMemcpyAsync(c->occ_den.p, den.data(), den.size() * sizeof(float), cudaMemcpyHostToDevice, s));
     CU(cudaStreamSynchronize(s));
   }
@@ -899,10 +908,9 @@ int occupancy_update(dg_ctx* c) {
   for (uint32_t lp = 0; lp < nl; ++lp) {
     const PartDesc& pd = c->parts[lp];
     for (int casc = 0; casc < 2; ++casc) {  // set_threshold: recompute the bitfield
-      const uint64_t n = uint64_t(pd.occ_n[casc][0]) * pd.occ_n[casc][1] * pd.occ_n[casc][2];
       c->occ_thr[lp * 2 + casc] = threshold;
-      launch_occ_bits(c->occ_den.as<float>() + pd.occ_off[casc], c->occ.as<uint8_t>() + pd.occ_off[casc],
-                      n, float(threshold), s);
+      launch_occ_bits(c->occ_den.as<float>() + pd.den_off[casc], c->occ.as<uint8_t>() + pd.occ_off[casc],
+                      pd.occ_n[casc], float(threshold), s);
       ++c->launches;
     }
     for (int casc = 0; casc < 2; ++casc) {
@@ -911,7 +919,7 @@ int occupancy_update(dg_ctx* c) {
       uint64_t total;
       occ_geometry(pd, casc, lo, cell, total);
       const FieldDesc* fd = c->d_fields.as<FieldDesc>() + casc * nl + lp;
-      float* den = c->occ_den.as<float>() + pd.occ_off[casc];
+      float* den = c->occ_den.as<float>() + pd.den_off[casc];
       if (warm_up) {  // every cell once, in order: cell index == point index
         CU(cudaMemcpyAsync(c->occ_pts.p, c->occ_host + k, total * 3 * sizeof(double),
                            cudaMemcpyHostToDevice, s));
@@ -921,13 +929,13 @@ int occupancy_update(dg_ctx* c) {
         c->h2d += total * 3 * sizeof(double);
       } else {
         std::mt19937_64& rng = c->occ_rng[lp];
-        std::vector<uint8_t> bits(total);
-        CU(cudaMemcpyAsync(bits.data(), c->occ.as<uint8_t>() + pd.occ_off[casc], total,
-                           cudaMemcpyDeviceToHost, s));
+        // occupied cells = the bitfield just recomputed (density >= threshold, k_occ_bits)
+        std::vector<float> hd(total);
+        CU(cudaMemcpyAsync(hd.data(), den, total * sizeof(float), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
         std::vector<uint64_t> occupied;
         for (uint64_t i = 0; i < total; ++i)
-          if (bits[i]) occupied.push_back(i);
+          if (hd[i] >= float(threshold)) occupied.push_back(i);
         const uint64_t n_uniform = std::max<uint64_t>(total / 4, 1);
         std::vector<uint32_t> cells;
         std::vector<double> pts;
@@ -943,16 +951,15 @@ int occupancy_update(dg_ctx* c) {
         CU(cudaMemcpyAsync(c->occ_pts.p, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         launch_occ_query(fd, c->params.as<float>(), c->occ_pts.as<double>(), n, c->occ_sigma.as<float>(), s);
         // cells may repeat: apply sequentially in draw order on the host
-        std::vector<float> sig(n), hd(total);
+        std::vector<float> sig(n);
         CU(cudaMemcpyAsync(sig.data(), c->occ_sigma.p, n * sizeof(float), cudaMemcpyDeviceToHost, s));
-        CU(cudaMemcpyAsync(hd.data(), den, total * sizeof(float), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
         for (uint64_t q = 0; q < n; ++q) hd[cells[q]] = std::max(hd[cells[q]] * float(cfg.occ_decay), sig[q]);
         CU(cudaMemcpyAsync(den, hd.data(), total * sizeof(float), cudaMemcpyHostToDevice, s));
         CU(cudaStreamSynchronize(s));
         c->h2d += pts.size() * sizeof(double) + total * sizeof(float);
       }
-      launch_occ_bits(den, c->occ.as<uint8_t>() + pd.occ_off[casc], total, float(threshold), s);
+      launch_occ_bits(den, c->occ.as<uint8_t>() + pd.occ_off[casc], pd.occ_n[casc], float(threshold), s);
       c->launches += 3;
     }
   }
@@ -1267,11 +1274,24 @@ static int occ_copy(dg_ctx* c, uint32_t p, uint32_t cascade, uint8_t* out, const
   TRY(check_part(c, p, &lp));
   if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
   const PartDesc& pd = c->parts[lp];
-  const uint64_t n = uint64_t(pd.occ_n[cascade][0]) * pd.occ_n[cascade][1] * pd.occ_n[cascade][2];
+  const uint32_t* sh = pd.occ_n[cascade];
+  const uint32_t* nb = pd.occ_nb[cascade];
+  const uint64_t bytes = uint64_t(nb[0]) * nb[1] * nb[2] * (kOccBX * kOccBY * kOccBZ);
   uint8_t* dev = c->occ.as<uint8_t>() + pd.occ_off[cascade];
-  if (in) CU(cudaMemcpyAsync(dev, in, n, cudaMemcpyHostToDevice, c->stream));
-  else CU(cudaMemcpyAsync(out, dev, n, cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
+  std::vector<uint8_t> br(bytes, 1);  // bricked image (padding cells stay occupied, never walked)
+  if (in) {
+    for (uint32_t z = 0; z < sh[2]; ++z)
+      for (uint32_t y = 0; y < sh[1]; ++y)
+        for (uint32_t x = 0; x < sh[0]; ++x) br[occ_addr(nb, x, y, z)] = in[(uint64_t(z) * sh[1] + y) * sh[0] + x];
+    CU(cudaMemcpyAsync(dev, br.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  } else {
+    CU(cudaMemcpyAsync(br.data(), dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    for (uint32_t z = 0; z < sh[2]; ++z)
+      for (uint32_t y = 0; y < sh[1]; ++y)
+        for (uint32_t x = 0; x < sh[0]; ++x) out[(uint64_t(z) * sh[1] + y) * sh[0] + x] = br[occ_addr(nb, x, y, z)];
+  }
   return DG_OK;
 }
 
@@ -1285,7 +1305,7 @@ int dg_set_occupancy(dg_ctx* c, uint32_t p, uint32_t cascade, const uint8_t* bit
   const float thr = float(c->occ_thr[lp * 2 + cascade]);
   std::vector<float> den(n);
   for (uint64_t i = 0; i < n; ++i) den[i] = bits[i] ? thr : 0.0f;
-  CU(cudaMemcpyAsync(c->occ_den.as<float>() + pd.occ_off[cascade], den.data(), n * sizeof(float),
+  CU(cudaMemcpyAsync(c->occ_den.as<float>() + pd.den_off[cascade], den.data(), n * sizeof(float),
                      cudaMemcpyHostToDevice, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return DG_OK;
@@ -1304,7 +1324,7 @@ int dg_get_occupancy_density(dg_ctx* c, uint32_t p, uint32_t cascade, float* den
   const PartDesc& pd = c->parts[lp];
   const uint64_t n = uint64_t(pd.occ_n[cascade][0]) * pd.occ_n[cascade][1] * pd.occ_n[cascade][2];
   if (density)
-    CU(cudaMemcpyAsync(density, c->occ_den.as<float>() + pd.occ_off[cascade], n * sizeof(float),
+    CU(cudaMemcpyAsync(density, c->occ_den.as<float>() + pd.den_off[cascade], n * sizeof(float),
                        cudaMemcpyDeviceToHost, c->stream));
   if (threshold) *threshold = c->occ_thr[lp * 2 + cascade];
   CU(cudaStreamSynchronize(c->stream));
@@ -1318,11 +1338,11 @@ int dg_set_occupancy_density(dg_ctx* c, uint32_t p, uint32_t cascade, const floa
   CU(cudaSetDevice(c->device));
   const PartDesc& pd = c->parts[lp];
   const uint64_t n = uint64_t(pd.occ_n[cascade][0]) * pd.occ_n[cascade][1] * pd.occ_n[cascade][2];
-  CU(cudaMemcpyAsync(c->occ_den.as<float>() + pd.occ_off[cascade], density, n * sizeof(float),
+  CU(cudaMemcpyAsync(c->occ_den.as<float>() + pd.den_off[cascade], density, n * sizeof(float),
                      cudaMemcpyHostToDevice, c->stream));
   c->occ_thr[lp * 2 + cascade] = threshold;
-  launch_occ_bits(c->occ_den.as<float>() + pd.occ_off[cascade], c->occ.as<uint8_t>() + pd.occ_off[cascade], n,
-                  float(threshold), c->stream);
+  launch_occ_bits(c->occ_den.as<float>() + pd.den_off[cascade], c->occ.as<uint8_t>() + pd.occ_off[cascade],
+                  pd.occ_n[cascade], float(threshold), c->stream);
   ++c->launches;
   CU(cudaStreamSynchronize(c->stream));
   return DG_OK;
