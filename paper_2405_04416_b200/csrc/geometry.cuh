@@ -178,6 +178,58 @@ __device__ __forceinline__ void occupancy_walk(const double o[3], const double d
   if (run_open) on_run(run_start, t_cur);
 }
 
+// Closed-form sample count of ladder(): the first k with t_k >= hi minus k0.  t_k =
+// base + k step is non-decreasing in k under round-to-nearest, so the estimate is corrected by
+// evaluating t_k exactly as the ladder does at the boundary (bit-exact count).
+__device__ __forceinline__ uint32_t ladder_count(double iv_lo, double iv_hi, double t_enter, double t_exit,
+                                                 double offset, double step) {
+  const double lo = smax(iv_lo, t_enter);
+  const double hi = smin(iv_hi, t_exit);
+  if (!(hi > lo)) return 0;
+  long long k0 = (long long)ceil(ddiv(dsub(dsub(lo, t_enter), offset), step));
+  if (k0 < 0) k0 = 0;
+  const double base = dadd(t_enter, offset);
+  long long k1 = (long long)ceil(ddiv(dsub(hi, base), step));
+  if (k1 < k0) k1 = k0;
+  while (k1 > k0 && dadd(base, dmul((double)(k1 - 1), step)) >= hi) --k1;
+  while (dadd(base, dmul((double)k1, step)) < hi) ++k1;
+  return (uint32_t)(k1 - k0);
+}
+
+// cascade_march's occupancy walks (worker.cpp:79-110) as runs: on_run(lo, hi, cascade) for
+// every occupied run in increasing t; the fine-box walk's runs are cascade 0, the coarse
+// walks' runs cascade 1 (the ladder's per-sample tag t in [fine_a, fine_b) is constant on a
+// run).  Returns has_fine.
+template <class OnRun>
+__device__ __forceinline__ bool cascade_runs(const PartDesc& pd, const uint8_t* occ, const double o[3],
+                                             const double d[3], double t0, double t1, double& fine_a,
+                                             double& fine_b, OnRun& on_run) {
+  fine_a = t1;
+  fine_b = t1;
+  bool has_fine = false;
+  double tn, tf;
+  if (ray_aabb(o, d, pd.fine_lo, pd.fine_hi, tn, tf)) {
+    fine_a = sclamp(tn, t0, t1);
+    fine_b = sclamp(tf, t0, t1);
+    has_fine = fine_b > fine_a;
+  }
+  const double fa = fine_a, fb = fine_b;
+  auto coarse = [&](double a, double b) { on_run(a, b, 1); };
+  auto fine = [&](double a, double b) { on_run(a, b, 0); };
+  const uint8_t* occ_f = occ + pd.occ_off[0];
+  const uint8_t* occ_c = occ + pd.occ_off[1];
+  if (has_fine) {
+    if (fa > t0)
+      occupancy_walk(o, d, t0, fa, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], pd.occ_nb[1], occ_c, coarse);
+    occupancy_walk(o, d, fa, fb, pd.fine_lo, pd.fine_hi, pd.occ_n[0], pd.occ_nb[0], occ_f, fine);
+    if (fb < t1)
+      occupancy_walk(o, d, fb, t1, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], pd.occ_nb[1], occ_c, coarse);
+  } else {
+    occupancy_walk(o, d, t0, t1, pd.coarse_lo, pd.coarse_hi, pd.occ_n[1], pd.occ_nb[1], occ_c, coarse);
+  }
+  return has_fine;
+}
+
 // cascade_march (worker.cpp:79-110).  emit(t, delta, cascade) in increasing t.
 // Returns has_fine and fills fine_a/fine_b (the cascade split) for the caller.
 template <class Emit>

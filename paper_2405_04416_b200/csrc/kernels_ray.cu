@@ -143,21 +143,24 @@ __global__ void k_item_setup(const Geo* __restrict__ geo, const PartDesc* __rest
                                : dmul(0.5, step);
   uint32_t nf = 0, nc = 0, ncb = 0;
   double fa, fb;
-  auto count = [&](double, double, int casc) {
+  auto count = [&](double a, double b, int casc) {  // O(1) per occupied run
+    const uint32_t k = ladder_count(a, b, t0, t1, offset, step);
     if (casc == 0) {
-      ++nf;
+      nf += k;
     } else {
-      ++nc;
-      if (nf == 0) ++ncb;
+      nc += k;
+      if (nf == 0) ncb += k;
     }
   };
-  const bool has_fine = cascade_march(pd, occ, r.o, r.d, t0, t1, step, offset, fa, fb, count);
+  const bool has_fine = cascade_runs(pd, occ, r.o, r.d, t0, t1, fa, fb, count);
   if (!has_fine) ncb = nc;
   it.cnt[i] = nf;
   it.cnt[n_items + i] = nc;
   it.ncb[i] = ncb;
 }
 
+// One thread per item: the occupancy walk (the dominant cost) runs once per item; each run's
+// ladder is emitted in order (render.cpp:21-35).
 __global__ void k_march_fill(const PartDesc* __restrict__ parts, const uint8_t* __restrict__ occ,
                              uint32_t n_items, ItemArrays it, SampleArrays sm, double step,
                              uint64_t seed, uint64_t batch_id, int jitter) {
