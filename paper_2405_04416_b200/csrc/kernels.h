@@ -10,6 +10,9 @@
 namespace dg {
 
 // Per-item state after setup (structure of arrays, capacity NI).
+constexpr int kMaxRuns = 16;
+constexpr uint8_t kRunsOverflow = 0xff;
+
 struct ItemArrays {
   RayRec* rec;        // dispatch record (origin/dir rounded in place when wire_f32)
   double* te;         // my segment t_enter / t_exit
@@ -23,6 +26,9 @@ struct ItemArrays {
   uint32_t* cnt;      // [2][NI]: fine, coarse sample counts (scanned in place -> offsets)
   uint32_t* off;      // [2][NI] exclusive offsets (fine region, coarse region)
   uint32_t* ncb;      // coarse samples before the fine box
+  double2* runs;      // [NI][kMaxRuns] occupied runs of the cascade march (lo, hi), from item setup
+  uint8_t* run_casc;  // [NI][kMaxRuns] cascade of each run
+  uint8_t* nrun;      // runs recorded per item; kRunsOverflow: more than kMaxRuns (walk again)
   uint32_t* contains; // [P][NI] 1 when partition q is in the schedule and q != mine
   uint32_t* cscan;    // exclusive scan of contains
   float4* partial;    // rgb, optical depth tau (T = exp(-tau)) of my segment

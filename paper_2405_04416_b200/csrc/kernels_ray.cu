@@ -141,7 +141,7 @@ __global__ void k_item_setup(const Geo* __restrict__ geo, const PartDesc* __rest
   // sample counts of cascade_march
   const double offset = jitter ? dmul(step, counter_uniform(seed, (uint64_t)r.ray_id, batch_id))
                                : dmul(0.5, step);
-  uint32_t nf = 0, nc = 0, ncb = 0;
+  uint32_t nf = 0, nc = 0, ncb = 0, nr = 0;
   double fa, fb;
   auto count = [&](double a, double b, int casc) {  // O(1) per occupied run
     const uint32_t k = ladder_count(a, b, t0, t1, offset, step);
@@ -151,21 +151,71 @@ __global__ void k_item_setup(const Geo* __restrict__ geo, const PartDesc* __rest
       nc += k;
       if (nf == 0) ncb += k;
     }
+    if (k && nr < (uint32_t)kMaxRuns) {  // the fill kernel replays the runs instead of walking
+      it.runs[(uint64_t)i * kMaxRuns + nr] = make_double2(a, b);
+      it.run_casc[(uint64_t)i * kMaxRuns + nr] = (uint8_t)casc;
+    }
+    if (k) ++nr;
   };
   const bool has_fine = cascade_runs(pd, occ, r.o, r.d, t0, t1, fa, fb, count);
   if (!has_fine) ncb = nc;
+  it.nrun[i] = nr <= (uint32_t)kMaxRuns ? (uint8_t)nr : kRunsOverflow;
   it.cnt[i] = nf;
   it.cnt[n_items + i] = nc;
   it.ncb[i] = ncb;
 }
 
-// One thread per item: the occupancy walk (the dominant cost) runs once per item; each run's
-// ladder is emitted in order (render.cpp:21-35).
+// One warp per item.  The occupied runs recorded by the item setup are replayed, each run's
+// ladder (render.cpp:21-35) emitted 32 samples at a time: t_k is non-decreasing in k, so the
+// lanes below hi are a prefix, and the sample writes coalesce.  Items with more than
+// kMaxRuns runs walk the occupancy grid again (all lanes in lock-step, uniform control flow).
 __global__ void k_march_fill(const PartDesc* __restrict__ parts, const uint8_t* __restrict__ occ,
                              uint32_t n_items, ItemArrays it, SampleArrays sm, double step,
                              uint64_t seed, uint64_t batch_id, int jitter) {
+  const uint32_t i = (uint32_t)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const uint32_t lane = threadIdx.x & 31;
+  if (i >= n_items) return;  // warp-uniform
+  const RayRec& r = it.rec[i];
+  const double te = it.te[i], tx = it.tx[i];
+  const double offset = jitter ? dmul(step, counter_uniform(seed, (uint64_t)r.ray_id, batch_id))
+                               : dmul(0.5, step);
+  const double base = dadd(te, offset), half = dmul(0.5, step);
+  uint32_t pf = it.off[i], pc = it.off[n_items + i];
+  auto run = [&](double a, double b, int casc) {
+    const double lo = smax(a, te), hi = smin(b, tx);
+    if (!(hi > lo)) return;
+    long long k0 = (long long)ceil(ddiv(dsub(dsub(lo, te), offset), step));
+    if (k0 < 0) k0 = 0;
+    uint32_t& cur = casc == 0 ? pf : pc;
+    for (long long kb = k0;; kb += 32) {
+      const double t = dadd(base, dmul((double)(kb + lane), step));
+      const bool v = t < hi;
+      const unsigned m = __ballot_sync(0xffffffffu, v);
+      if (v) {
+        const uint32_t s = cur + lane;
+        sm.t[s] = t;
+        sm.delta[s] = smin(step, dsub(hi, dsub(t, half)));
+        sm.item[s] = i;
+      }
+      cur += __popc(m);
+      if (m != 0xffffffffu) break;
+    }
+  };
+  const uint8_t nr = it.nrun[i];
+  if (nr == kRunsOverflow) return;  // k_march_fill_walk
+  for (int k = 0; k < nr; ++k) {
+    const double2 rr = it.runs[(uint64_t)i * kMaxRuns + k];
+    run(rr.x, rr.y, it.run_casc[(uint64_t)i * kMaxRuns + k]);
+  }
+}
+
+// Items whose runs overflowed kMaxRuns: one thread per item walks the grid again and emits
+// in order (cascade_march, worker.cpp:79-110).
+__global__ void k_march_fill_walk(const PartDesc* __restrict__ parts, const uint8_t* __restrict__ occ,
+                                  uint32_t n_items, ItemArrays it, SampleArrays sm, double step,
+                                  uint64_t seed, uint64_t batch_id, int jitter) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_items) return;
+  if (i >= n_items || it.nrun[i] != kRunsOverflow) return;
   const PartDesc& pd = parts[it.part[i]];
   const RayRec& r = it.rec[i];
   const double offset = jitter ? dmul(step, counter_uniform(seed, (uint64_t)r.ray_id, batch_id))
@@ -669,8 +719,10 @@ void launch_march_fill(const PartDesc* parts, const uint8_t* occ, uint32_t n_ite
                        ItemArrays it, SampleArrays sm, uint32_t n_fine, double step, uint64_t seed,
                        uint64_t batch_id, int jitter, cudaStream_t s) {
   if (!n_items) return;
-  k_march_fill<<<blocks(n_items, 128), 128, 0, s>>>(parts, occ, n_items, it, sm, step, seed,
-                                                    batch_id, jitter);
+  k_march_fill<<<blocks((uint64_t)n_items * 32, 128), 128, 0, s>>>(parts, occ, n_items, it, sm, step, seed,
+                                                                   batch_id, jitter);
+  k_march_fill_walk<<<blocks(n_items, 128), 128, 0, s>>>(parts, occ, n_items, it, sm, step, seed, batch_id,
+                                                         jitter);
   if (sm.pn && sm.p)
     k_sample_points<<<(unsigned)((sm.pn + 255) / 256), 256, 0, s>>>(parts, it, sm, n_fine);
 }

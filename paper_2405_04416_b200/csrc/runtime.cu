@@ -164,7 +164,7 @@ struct dg_ctx {
   dg_stage_times times{};
 
   // persistent device state
-  DBuf out_attr, cam_o, cam_d, cam_pose, it_xdist, send_x, recv_x;
+  DBuf out_attr, cam_o, cam_d, cam_pose, it_xdist, send_x, recv_x, it_runs, it_runc, it_nrun;
   bool cross_active = false;  // training step with distortion_cross_correction
   DBuf d_geo, d_parts, d_fields, params, grads, adam_m, adam_v, occ, occ_den, app, slot_of_part_d,
       local_of_global_d, global_of_local_d;
@@ -449,6 +449,9 @@ ItemArrays item_arrays(dg_ctx* c) {
   it.cnt = c->it_cnt.as<uint32_t>();
   it.off = c->it_off.as<uint32_t>();
   it.ncb = c->it_ncb.as<uint32_t>();
+  it.runs = c->it_runs.as<double2>();
+  it.run_casc = c->it_runc.as<uint8_t>();
+  it.nrun = c->it_nrun.as<uint8_t>();
   it.contains = c->it_contains.as<uint32_t>();
   it.cscan = c->it_cscan.as<uint32_t>();
   it.partial = c->it_partial.as<float4>();
@@ -635,6 +638,9 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   TRY(c->it_cnt.ensure((2ull * NI + 1) * 4));
   TRY(c->it_off.ensure((2ull * NI + 1) * 4));
   TRY(c->it_ncb.ensure(uint64_t(NI) * 4 + 16));
+  TRY(c->it_runs.ensure(uint64_t(NI) * kMaxRuns * sizeof(double2) + 16));
+  TRY(c->it_runc.ensure(uint64_t(NI) * kMaxRuns + 16));
+  TRY(c->it_nrun.ensure(uint64_t(NI) + 16));
   TRY(c->it_contains.ensure((uint64_t(P) * NI + 1) * 4));
   TRY(c->it_cscan.ensure((uint64_t(P) * NI + 1) * 4));
   TRY(c->it_partial.ensure(uint64_t(NI) * 16 + 16));
@@ -683,7 +689,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   SampleArrays sm = sample_arrays(c);
   launch_march_fill(c->d_parts.as<PartDesc>(), c->occ.as<uint8_t>(), NI, it, sm, c->n_fine,
                     c->step, c->cfg.seed, batch_id, train, s);
-  c->launches += c->enc_pcache ? 2 : 1;  // march fill (+ sample points)
+  c->launches += c->enc_pcache ? 3 : 2;  // march fill (runs + overflow walk) (+ sample points)
   // tile tables
   std::vector<uint32_t> tf(2 * nl + 1, 0), tb(2 * nl + 1, 0);
   for (uint32_t f = 0; f < 2 * nl; ++f) {
