@@ -341,11 +341,34 @@ __global__ void k_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t*
   }
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
+__device__ __forceinline__ float warp_sum_f(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// exclusive prefix sum over lanes (lane 0 gets 0)
+__device__ __forceinline__ float warp_excl_scan(float v) {
+  const unsigned lane = threadIdx.x & 31;
+  float x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  return x - v;
+}
+// exclusive suffix sum over lanes (lane 31 gets 0)
+__device__ __forceinline__ float warp_excl_rscan(float v) {
+  const unsigned lane = threadIdx.x & 31;
+  float x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_down_sync(0xffffffffu, x, o);
+    if (lane + o < 32) x += y;
+  }
+  return x - v;
+}
+
 
 __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
                                  const uint32_t* __restrict__ part_item_off,
@@ -354,7 +377,10 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
                                  const PartialRec* __restrict__ recv, const float4* __restrict__ recv_x,
                                  SampleArrays sm, double lambda_t, double lambda_d, double t_clamp,
                                  int wire_f32, LossAccum* __restrict__ loss) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per item: the per-item merge is computed by every lane (broadcast loads), the
+  // per-sample passes run 32 samples at a time with warp scans
+  const uint32_t i = (uint32_t)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const uint32_t lane = threadIdx.x & 31;
   double l_rgb = 0.0, l_t = 0.0, l_d = 0.0;
   uint32_t lp = 0;
   if (i < n_items) {
@@ -459,74 +485,122 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
     // local forward recompute: prefix per sample, distortion totals (worker.cpp:435-451)
     const double ray_t0 = it.t0[i];
     const float inv_span = (float)(1.0 / (it.t1[i] - ray_t0));
-    float Tl = 1.0f, Wt = 0.0f, Mt = 0.0f, Wp = 0.0f, Mp = 0.0f, pair = 0.0f, interval = 0.0f;
-    uint32_t n = 0;
-    for_item_samples(it, n_items, i, [&](uint32_t s) {
-      const float x = sm.out[s].x * (float)sm.delta[s];
+    const uint32_t fo = it.off[i], nf = it.cnt[i];
+    const uint32_t co = it.off[n_items + i], nc = it.cnt[n_items + i], ncb = it.ncb[i];
+    const uint32_t n = nf + nc;
+    auto sample_at = [&](uint32_t j) {  // t order: coarse-before, fine, coarse-after
+      return j < ncb ? co + j : (j < ncb + nf ? fo + (j - ncb) : co + j - nf);
+    };
+    float cx = 0.0f, cW = 0.0f, cM = 0.0f, pair = 0.0f, interval = 0.0f;
+    for (uint32_t jb = 0; jb < n; jb += 32) {
+      const uint32_t j = jb + lane;
+      const bool v = j < n;
+      const uint32_t s = v ? sample_at(j) : 0u;
+      const float x = v ? sm.out[s].x * (float)sm.delta[s] : 0.0f;
+      const float ex_x = warp_excl_scan(x);
+      const float Tl = expf(-(cx + ex_x));
       const float alpha = -expm1f(-x);
-      const float w = Tl * alpha;
-      const float ss = (float)((sm.t[s] - ray_t0)) * inv_span;
-      const float ds = (float)sm.delta[s] * inv_span;
+      const float w = v ? Tl * alpha : 0.0f;
+      const float ss = v ? (float)((sm.t[s] - ray_t0)) * inv_span : 0.0f;
+      const float ds = v ? (float)sm.delta[s] * inv_span : 0.0f;
+      const float Wp = cW + warp_excl_scan(w), Mp = cM + warp_excl_scan(w * ss);
       pair += 2.0f * w * (ss * Wp - Mp);
       interval += w * w * ds;
-      Wp += w;
-      Mp += w * ss;
-      sm.grad[s] = make_float4(Tl, 0.f, 0.f, 0.f);  // stash prefix for the reverse sweep
-      Tl *= expf(-x);
-      ++n;
-    });
-    Wt = Wp;
-    Mt = Mp;
+      if (v) sm.grad[s] = make_float4(Tl, 0.f, 0.f, 0.f);  // stash prefix for the reverse sweep
+      cx += warp_sum_f(x);
+      cW += warp_sum_f(w);
+      cM += warp_sum_f(w * ss);
+    }
+    const float Wt = cW, Mt = cM;
+    pair = warp_sum_f(pair);
+    interval = warp_sum_f(interval);
     if (cross) l_d = l_full;  // only the first owner reports, the whole ray
     else if (n > 0) l_d = (double)(pair + interval / 3.0f);
     const float xp = (float)pre[mo], xlw = (float)lw, xlm = (float)lm, xew = (float)ew, xem = (float)em;
-    // reverse sweep: local_render_backward with the distortion weight channel
+    // reverse sweep: local_render_backward with the distortion weight channel (render.cpp:145-179);
+    // suffix sums by reverse warp scans, the tail colour recurrence c <- alpha u + om c as an
+    // affine-map suffix scan
     const float ucx = (float)g_c[0], ucy = (float)g_c[1], ucz = (float)g_c[2];
     const float ut = (float)g_t;
     const float ld = (float)lambda_d;
-    float tail_c = 0.0f, tail_t = 1.0f, Ws = 0.0f, Ms = 0.0f;
-    for_item_samples_rev(it, n_items, i, [&](uint32_t s) {
-      const float4 o = sm.out[s];
-      const float delta = (float)sm.delta[s];
-      const float x = o.x * delta;
-      const float alpha = -expm1f(-x);
-      const float om = expf(-x);
-      const float pf = sm.grad[s].x;
-      const float w = pf * alpha;
-      const float ss = (float)((sm.t[s] - ray_t0)) * inv_span;
-      const float ds = delta * inv_span;
-      float wup = 0.0f;
-      if (ld > 0.0f) {
-        const float Wl = Wt - Ws - w, Ml = Mt - Ms - w * ss;
-        const float gd = 2.0f * (ss * Wl - Ml) + 2.0f * (Ms - ss * Ws) + (2.0f / 3.0f) * w * ds;
-        wup = cross ? ld * (xp * xp * gd + 2.0f * xp * (xlm - ss * xlw + ss * xew - xem)) : ld * gd;
+    float cWs = 0.0f, cMs = 0.0f, cxs = 0.0f, ctc = 0.0f;
+    if (n > 0) {
+      for (int64_t jb = (int64_t)((n - 1) / 32) * 32; jb >= 0; jb -= 32) {
+        const uint32_t j = (uint32_t)jb + lane;
+        const bool v = j < n;
+        const uint32_t s = v ? sample_at(j) : 0u;
+        const float4 o = v ? sm.out[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float delta = v ? (float)sm.delta[s] : 0.0f;
+        const float x = o.x * delta;
+        const float alpha = -expm1f(-x);
+        const float om = v ? expf(-x) : 1.0f;
+        const float pf = v ? sm.grad[s].x : 0.0f;
+        const float w = pf * alpha;
+        const float ss = v ? (float)((sm.t[s] - ray_t0)) * inv_span : 0.0f;
+        const float ds = delta * inv_span;
+        const float Ws = cWs + warp_excl_rscan(w), Ms = cMs + warp_excl_rscan(w * ss);
+        const float tail_t = expf(-(cxs + warp_excl_rscan(x)));
+        float wup = 0.0f;
+        if (ld > 0.0f) {
+          const float Wl = Wt - Ws - w, Ml = Mt - Ms - w * ss;
+          const float gd = 2.0f * (ss * Wl - Ml) + 2.0f * (Ms - ss * Ws) + (2.0f / 3.0f) * w * ds;
+          wup = cross ? ld * (xp * xp * gd + 2.0f * xp * (xlm - ss * xlw + ss * xew - xem)) : ld * gd;
+        }
+        const float u = ucx * o.y + ucy * o.z + ucz * o.w + wup;
+        // suffix composition of c -> a c + b (a = om, b = alpha u) over the later lanes
+        float A = om, B = v ? alpha * u : 0.0f;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float A2 = __shfl_down_sync(0xffffffffu, A, off), B2 = __shfl_down_sync(0xffffffffu, B, off);
+          if (lane + off < 32) {
+            B = A * B2 + B;
+            A = A * A2;
+          }
+        }
+        float An = __shfl_down_sync(0xffffffffu, A, 1), Bn = __shfl_down_sync(0xffffffffu, B, 1);
+        if (lane == 31) {
+          An = 1.0f;
+          Bn = 0.0f;
+        }
+        const float tail_c = An * ctc + Bn;
+        const float alpha_grad = pf * (u - tail_c) - ut * pf * tail_t;
+        const float dsig = alpha_grad * delta * om;
+        const float cw = pf * alpha;
+        if (v) sm.grad[s] = make_float4(dsig, ucx * cw, ucy * cw, ucz * cw);
+        ctc = __shfl_sync(0xffffffffu, A, 0) * ctc + __shfl_sync(0xffffffffu, B, 0);
+        cWs += warp_sum_f(w);
+        cMs += warp_sum_f(w * ss);
+        cxs += warp_sum_f(x);
       }
-      const float u = ucx * o.y + ucy * o.z + ucz * o.w + wup;
-      const float alpha_grad = pf * (u - tail_c) - ut * pf * tail_t;
-      const float dsig = alpha_grad * delta * om;
-      const float cw = pf * alpha;
-      sm.grad[s] = make_float4(dsig, ucx * cw, ucy * cw, ucz * cw);
-      tail_c = alpha * u + om * tail_c;
-      tail_t *= om;
-      Ws += w;
-      Ms += w * ss;
-    });
-  }
-  // per-partition loss sums: warp-reduce when the warp is uniform, else per-lane atomics
-  const unsigned active = __ballot_sync(0xffffffffu, i < n_items);
-  const uint32_t lp0 = __shfl_sync(0xffffffffu, lp, 0);
-  const bool uniform = __all_sync(0xffffffffu, lp == lp0 || i >= n_items);
-  if (uniform) {
-    const double a = warp_sum(l_rgb), b = warp_sum(l_t), c = warp_sum(l_d);
-    if ((threadIdx.x & 31) == 0 && active) {
-      atomicAdd(&loss->rgb[lp0], a);
-      atomicAdd(&loss->trans[lp0], b);
-      atomicAdd(&loss->dist[lp0], c);
     }
-  } else if (i < n_items) {
-    atomicAdd(&loss->rgb[lp], l_rgb);
-    atomicAdd(&loss->trans[lp], l_t);
-    atomicAdd(&loss->dist[lp], l_d);
+  }
+  // per-partition loss sums: lane 0 of each item's warp; items of a block share a partition
+  // almost always, so one atomic per block and partition
+  __shared__ double red[3][4];
+  __shared__ uint32_t red_lp[4];
+  const uint32_t wib = threadIdx.x >> 5;  // 4 warps (items) per block
+  if (lane == 0) {
+    red[0][wib] = i < n_items ? l_rgb : 0.0;
+    red[1][wib] = i < n_items ? l_t : 0.0;
+    red[2][wib] = i < n_items ? l_d : 0.0;
+    red_lp[wib] = i < n_items ? lp : 0xffffffffu;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < 4; ++a) {
+      if (red_lp[a] == 0xffffffffu) continue;
+      double x0 = red[0][a], x1 = red[1][a], x2 = red[2][a];
+      for (int b = a + 1; b < 4; ++b)
+        if (red_lp[b] == red_lp[a]) {
+          x0 += red[0][b];
+          x1 += red[1][b];
+          x2 += red[2][b];
+          red_lp[b] = 0xffffffffu;
+        }
+      atomicAdd(&loss->rgb[red_lp[a]], x0);
+      atomicAdd(&loss->trans[red_lp[a]], x1);
+      atomicAdd(&loss->dist[red_lp[a]], x2);
+    }
   }
 }
 
@@ -747,7 +821,7 @@ void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part
                            double lambda_t, double lambda_d, double t_clamp, int wire_f32,
                            LossAccum* loss, cudaStream_t s) {
   if (!n_items) return;
-  k_merge_backward<<<blocks(n_items, 128), 128, 0, s>>>(n_items, it, part_item_off, parts,
+  k_merge_backward<<<blocks((uint64_t)n_items * 32, 128), 128, 0, s>>>(n_items, it, part_item_off, parts,
                                                         stream_off, P, recv, recv_x, sm, lambda_t,
                                                         lambda_d, t_clamp, wire_f32, loss);
 }
