@@ -182,8 +182,8 @@ void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, f
 void launch_fill_uniform(float* p, uint64_t n, float lo, float hi, uint64_t seed, cudaStream_t s);
 
 // ---- occupancy update (kernels_occ.cu) ----
-void launch_occ_query(const FieldDesc* field, const float* params, const double* pw, uint64_t n,
-                      float* sigma, cudaStream_t s);
+int launch_occ_query(const FieldDesc* field, const float* params, const double* pw, uint64_t n,
+                     float* sigma, cudaStream_t s);
 void launch_occ_apply(float* density, const uint32_t* cells, const float* sigma, uint64_t n,
                       float decay, cudaStream_t s);
 void launch_occ_bits(const float* density, uint8_t* bits, const uint32_t shape[3], float threshold,

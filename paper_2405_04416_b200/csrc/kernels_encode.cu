@@ -14,55 +14,13 @@
 // forward; the backward read-modify-writes the same 1024 B.
 #include <cstdlib>
 
+#include "encode_common.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
 
 namespace dg {
 
 namespace {
-
-struct Corners {
-  uint32_t row[8];
-  float w[8];
-};
-
-// Lattice corners of one level for normalised point p; zero-weight corners get row = NONE
-// and are skipped by the callers exactly as the reference skips them (grid.cpp:119-120).
-// Lattice indices, fractions and corner weights are fp64 (bit-exact rows; the weight rounds
-// once to fp32, features accumulate in fp32); the row arithmetic is hoisted per axis.
-__device__ __forceinline__ void level_corners(const LevelDesc& lv, const double p[3], Corners& c) {
-  const AxisW ax = lattice_axis(p[0], lv.n[0]);
-  const AxisW ay = lattice_axis(p[1], lv.n[1]);
-  const AxisW az = lattice_axis(p[2], lv.n[2]);
-  const double fx[2] = {dsub(1.0, ax.frac), ax.frac};
-  const double fy[2] = {dsub(1.0, ay.frac), ay.frac};
-  const double fz[2] = {dsub(1.0, az.frac), az.frac};
-  // row = x ^ (y * P1) ^ (z * P2) (hashed) or x + nx (y + ny z) (one-to-one), per axis parts
-  uint32_t rx[2], ry[2], rz[2];
-  if (lv.hashed) {
-    rx[0] = ax.i0;
-    rx[1] = ax.i1;
-    ry[0] = ay.i0 * 2654435761u;
-    ry[1] = ay.i1 * 2654435761u;
-    rz[0] = az.i0 * 805459861u;
-    rz[1] = az.i1 * 805459861u;
-  } else {
-    rx[0] = ax.i0;
-    rx[1] = ax.i1;
-    ry[0] = lv.n[0] * ay.i0;
-    ry[1] = lv.n[0] * ay.i1;
-    rz[0] = lv.n[0] * lv.n[1] * az.i0;
-    rz[1] = lv.n[0] * lv.n[1] * az.i1;
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int cx = k & 1, cy = (k >> 1) & 1, cz = (k >> 2) & 1;
-    const double w = dmul(dmul(fx[cx], fy[cy]), fz[cz]);
-    c.w[k] = (float)w;
-    const uint32_t row = lv.hashed ? ((rx[cx] ^ ry[cy] ^ rz[cz]) & lv.mask) : (rx[cx] + ry[cy] + rz[cz]);
-    c.row[k] = w == 0.0 ? 0xffffffffu : row;
-  }
-}
 
 __device__ __forceinline__ float2 gather_level(const float2* __restrict__ table, const Corners& c) {
   float2 v[8];
@@ -84,51 +42,6 @@ __device__ __forceinline__ void scatter_level(float2* __restrict__ table, const 
     if (c.row[k] == 0xffffffffu) continue;
     atomicAdd(table + c.row[k], make_float2(c.w[k] * up.x, c.w[k] * up.y));
   }
-}
-
-// Row pairing: the two x-neighbour corners (cx = 0, 1) of each (cy, cz) land in rows
-// i ^ h and (i + 1) ^ h (hashed) or r and r + 1 (one-to-one); when those differ only in bit 0
-// (half the time) they are one 16-byte aligned float4 (every level table is 16-byte aligned),
-// fetched or reduced with one vector access instead of two.
-__device__ __forceinline__ bool is_pair(uint32_t r0, uint32_t r1) {
-  return r0 != 0xffffffffu && r1 != 0xffffffffu && (r0 ^ r1) == 1u;
-}
-
-__device__ __forceinline__ float2 gather_level_pairs(const float2* __restrict__ table, const Corners& c) {
-  const float4* t4 = reinterpret_cast<const float4*>(table);
-  float4 q[4];
-  float2 b[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t r0 = c.row[2 * j], r1 = c.row[2 * j + 1];
-    if (is_pair(r0, r1)) {
-      q[j] = __ldg(t4 + (r0 >> 1));
-      b[j] = make_float2(0.f, 0.f);
-    } else {
-      const float2 a = r0 != 0xffffffffu ? __ldg(table + r0) : make_float2(0.f, 0.f);
-      q[j] = make_float4(a.x, a.y, 0.f, 0.f);
-      b[j] = r1 != 0xffffffffu ? __ldg(table + r1) : make_float2(0.f, 0.f);
-    }
-  }
-  float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t r0 = c.row[2 * j], r1 = c.row[2 * j + 1];
-    float2 v0, v1;
-    if (is_pair(r0, r1)) {
-      const bool odd = r0 & 1u;
-      v0 = odd ? make_float2(q[j].z, q[j].w) : make_float2(q[j].x, q[j].y);
-      v1 = odd ? make_float2(q[j].x, q[j].y) : make_float2(q[j].z, q[j].w);
-    } else {
-      v0 = make_float2(q[j].x, q[j].y);
-      v1 = b[j];
-    }
-    acc.x = fmaf(c.w[2 * j], v0.x, acc.x);
-    acc.y = fmaf(c.w[2 * j], v0.y, acc.y);
-    acc.x = fmaf(c.w[2 * j + 1], v1.x, acc.x);
-    acc.y = fmaf(c.w[2 * j + 1], v1.y, acc.y);
-  }
-  return acc;
 }
 
 __device__ __forceinline__ void scatter_level_pairs(float2* __restrict__ table, const Corners& c, float2 up) {

@@ -413,19 +413,6 @@ __device__ __forceinline__ void zero_regs(GradRegs& g) {
   g.bias = 0.f;
 }
 
-// bias ownership: [0,64) dc0-hidden1 (cb0), [64,128) cb1, [128,131) cb2, [131,195) db0,
-// [195,211) db1.
-__device__ __forceinline__ void bias_row(int tid, const float*& row, int& which) {
-  which = -1;
-  row = nullptr;
-  (void)row;
-  if (tid < 64) which = 0;
-  else if (tid < 128) which = 1;
-  else if (tid < 131) which = 2;
-  else if (tid < 195) which = 3;
-  else if (tid < 211) which = 4;
-}
-
 __device__ void flush_grads(GradRegs& g, const FieldDesc& fd, float* __restrict__ grads) {
   float* base = grads + fd.base;
   const int enc = (int)fd.L * 2;

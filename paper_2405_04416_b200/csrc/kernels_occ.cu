@@ -6,6 +6,7 @@
 //   from the reference's own mt19937_64 stream (generated on the host, in the reference's
 //   draw order) so the sampled set is identical; sigma = query_density(p).sigma is evaluated
 //   here: fp64 bit-exact lattice indices, fp32 gathers, density MLP [enc -> 64 ReLU -> raw0].
+#include "encode_common.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
 
@@ -13,11 +14,15 @@ namespace dg {
 
 namespace {
 
+// sigma = query_density(p).sigma at the jittered points: the training encode's corners and
+// paired-row gathers (same rows, weights and accumulation order), then the density MLP
+// [enc -> 64 ReLU -> raw0] with the weights broadcast from shared memory.  One thread per
+// cell; a level-pass split (encode kernel + MLP kernel) measured slower.
 __global__ void __launch_bounds__(128) k_occ_query(const FieldDesc* __restrict__ field,
                                                    const float* __restrict__ params,
                                                    const double* __restrict__ pw, uint64_t n,
                                                    float* __restrict__ sigma) {
-  __shared__ float w0[kHidden * kEnc];  // [o][i]
+  __shared__ __align__(16) float w0[kHidden * kEnc];  // [o][i]
   __shared__ float b0[kHidden];
   __shared__ float w1[kHidden];         // row 0 of the second layer
   __shared__ float b1;
@@ -45,33 +50,24 @@ __global__ void __launch_bounds__(128) k_occ_query(const FieldDesc* __restrict__
 #pragma unroll
   for (int i = 0; i < kEnc; ++i) x[i] = 0.f;
   for (uint32_t l = 0; l < fd.L; ++l) {
-    const LevelDesc& lv = fd.lv[l];
-    const AxisW ax = lattice_axis(p[0], lv.n[0]);
-    const AxisW ay = lattice_axis(p[1], lv.n[1]);
-    const AxisW az = lattice_axis(p[2], lv.n[2]);
-    const double fx[2] = {dsub(1.0, ax.frac), ax.frac};
-    const double fy[2] = {dsub(1.0, ay.frac), ay.frac};
-    const double fz[2] = {dsub(1.0, az.frac), az.frac};
-    const float2* table = reinterpret_cast<const float2*>(base + lv.offset);
-    float ax0 = 0.f, ax1 = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int cx = k & 1, cy = (k >> 1) & 1, cz = (k >> 2) & 1;
-      const double w = dmul(dmul(fx[cx], fy[cy]), fz[cz]);
-      if (w == 0.0) continue;
-      const float2 v = __ldg(table + table_row(lv, cx ? ax.i1 : ax.i0, cy ? ay.i1 : ay.i0,
-                                               cz ? az.i1 : az.i0));
-      ax0 = fmaf((float)w, v.x, ax0);
-      ax1 = fmaf((float)w, v.y, ax1);
-    }
-    x[2 * l] = ax0;
-    x[2 * l + 1] = ax1;
+    Corners c;
+    level_corners(fd.lv[l], p, c);
+    const float2 v = gather_level_pairs(reinterpret_cast<const float2*>(base + fd.lv[l].offset), c);
+    x[2 * l] = v.x;
+    x[2 * l + 1] = v.y;
   }
   float raw = b1;
+  const float4* w04 = reinterpret_cast<const float4*>(w0);
   for (int o = 0; o < kHidden; ++o) {
     float h = b0[o];
 #pragma unroll
-    for (int i = 0; i < kEnc; ++i) h = fmaf(w0[o * kEnc + i], x[i], h);
+    for (int q = 0; q < kEnc / 4; ++q) {  // broadcast 16-byte shared loads
+      const float4 w = w04[o * (kEnc / 4) + q];
+      h = fmaf(w.x, x[4 * q], h);
+      h = fmaf(w.y, x[4 * q + 1], h);
+      h = fmaf(w.z, x[4 * q + 2], h);
+      h = fmaf(w.w, x[4 * q + 3], h);
+    }
     raw = fmaf(w1[o], h > 0.f ? h : 0.f, raw);
   }
   raw = raw > 15.f ? 15.f : (raw < -15.f ? -15.f : raw);
@@ -102,9 +98,11 @@ inline unsigned nb(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t);
 
 }  // namespace
 
-void launch_occ_query(const FieldDesc* field, const float* params, const double* pw, uint64_t n,
-                      float* sigma, cudaStream_t s) {
-  if (n) k_occ_query<<<nb(n, 128), 128, 0, s>>>(field, params, pw, n, sigma);
+int launch_occ_query(const FieldDesc* field, const float* params, const double* pw, uint64_t n,
+                     float* sigma, cudaStream_t s) {
+  if (!n) return 0;
+  k_occ_query<<<nb(n, 128), 128, 0, s>>>(field, params, pw, n, sigma);
+  return 1;
 }
 void launch_occ_apply(float* density, const uint32_t* cells, const float* sigma, uint64_t n,
                       float decay, cudaStream_t s) {

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <future>
 #include <memory>
 #include <random>
@@ -150,6 +151,11 @@ struct dg_ctx {
   uint64_t occ_host_n = 0;                // doubles
   std::future<void> occ_prefetch;
   bool occ_prefetched = false;
+  // ... and go up to the device on a copy stream as soon as they are drawn, so the 24 B/cell
+  // transfer overlaps the training steps before the update instead of stalling it
+  cudaStream_t stream_copy = nullptr;
+  cudaEvent_t ev_occ_up = nullptr, ev_occ_used = nullptr;
+  bool occ_uploaded = false;
   double step = 0.0;
   uint64_t adam_t = 0;
   uint64_t worker_step = 0;
@@ -174,7 +180,7 @@ struct dg_ctx {
       it_off, it_ncb, it_contains, it_cscan, it_partial, it_depth, part_item_off_d, s_t, s_delta, s_p,
       s_item, s_X, s_out, s_grad, s_dX, field_off_d, tile_off_f, tile_off_b, stream_send_d,
       stream_recv_d, send_buf, recv_buf, x_send, x_recv, out_rgb, out_T, out_depth, eval_app,
-      perm_tab, occ_pts, occ_cells, occ_sigma;
+      perm_tab, occ_pts, occ_cells, occ_sigma, occ_pts_warm;
   // last step (introspection)
   std::vector<uint32_t> part_item_off;   // n_local + 1
   std::vector<uint32_t> field_off;       // 2 n_local + 1
@@ -408,6 +414,7 @@ int ctx_alloc(dg_ctx* c) {
     c->occ_host_n = all_cells * 3;
     CU(cudaHostAlloc(reinterpret_cast<void**>(&c->occ_host), c->occ_host_n * sizeof(double) + 16,
                      cudaHostAllocDefault));
+    TRY(c->occ_pts_warm.ensure(c->occ_host_n * sizeof(double) + 16));
     occ_start_prefetch(c);
   }
   // default appearance: one zero row for image 0
@@ -888,6 +895,23 @@ void occ_start_prefetch(dg_ctx* c) {
   if (!c->occ_host || !next_update_is_warm(c, c->worker_step)) return;
   c->occ_prefetch = std::async(std::launch::async, [c] { occ_generate_warm(c); });
   c->occ_prefetched = true;
+  c->occ_uploaded = false;
+}
+
+// Drawn warm-up points -> device on the copy stream (non-blocking unless `block`).  The copy
+// waits for the previous update's queries to be done with the device buffer.
+int occ_try_upload(dg_ctx* c, bool block) {
+  if (c->occ_uploaded || !c->occ_prefetched || !c->occ_prefetch.valid()) return DG_OK;
+  if (!block && c->occ_prefetch.wait_for(std::chrono::seconds(0)) != std::future_status::ready)
+    return DG_OK;
+  c->occ_prefetch.wait();
+  CU(cudaStreamWaitEvent(c->stream_copy, c->ev_occ_used, 0));
+  CU(cudaMemcpyAsync(c->occ_pts_warm.p, c->occ_host, c->occ_host_n * sizeof(double),
+                     cudaMemcpyHostToDevice, c->stream_copy));
+  CU(cudaEventRecord(c->ev_occ_up, c->stream_copy));
+  c->h2d += c->occ_host_n * sizeof(double);
+  c->occ_uploaded = true;
+  return DG_OK;
 }
 
 // Worker::update_occupancy (worker.cpp:549-562) + OccupancyGrid::decay_and_update
@@ -906,9 +930,13 @@ int occupancy_update(dg_ctx* c) {
   const bool warm_up = step <= cfg.occ_warmup_steps;
   const uint32_t nl = uint32_t(c->local.size());
   if (warm_up) {
-    if (!c->occ_prefetched) occ_start_prefetch(c), c->occ_prefetched = true;
-    if (c->occ_prefetch.valid()) c->occ_prefetch.wait();
-    c->occ_prefetched = false;
+    if (!c->occ_prefetched) {  // nothing drawn ahead (e.g. state just injected): draw now
+      c->occ_prefetch = std::async(std::launch::deferred, [c] { occ_generate_warm(c); });
+      c->occ_prefetched = true;
+      c->occ_uploaded = false;
+    }
+    TRY(occ_try_upload(c, true));
+    CU(cudaStreamWaitEvent(s, c->ev_occ_up, 0));
   }
   uint64_t k = 0;  // offset into the prefetched warm-up points
   for (uint32_t lp = 0; lp < nl; ++lp) {
@@ -927,12 +955,10 @@ int occupancy_update(dg_ctx* c) {
       const FieldDesc* fd = c->d_fields.as<FieldDesc>() + casc * nl + lp;
       float* den = c->occ_den.as<float>() + pd.den_off[casc];
       if (warm_up) {  // every cell once, in order: cell index == point index
-        CU(cudaMemcpyAsync(c->occ_pts.p, c->occ_host + k, total * 3 * sizeof(double),
-                           cudaMemcpyHostToDevice, s));
+        c->launches += launch_occ_query(fd, c->params.as<float>(), c->occ_pts_warm.as<double>() + k, total,
+                                        c->occ_sigma.as<float>(), s);
         k += 3 * total;
-        launch_occ_query(fd, c->params.as<float>(), c->occ_pts.as<double>(), total, c->occ_sigma.as<float>(), s);
         launch_occ_apply(den, nullptr, c->occ_sigma.as<float>(), total, float(cfg.occ_decay), s);
-        c->h2d += total * 3 * sizeof(double);
       } else {
         std::mt19937_64& rng = c->occ_rng[lp];
         // occupied cells = the bitfield just recomputed (density >= threshold, k_occ_bits)
@@ -955,7 +981,8 @@ int occupancy_update(dg_ctx* c) {
           for (uint64_t i = 0; i < n_uniform; ++i) sample(occupied[rng() % occupied.size()]);
         const uint64_t n = cells.size();
         CU(cudaMemcpyAsync(c->occ_pts.p, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-        launch_occ_query(fd, c->params.as<float>(), c->occ_pts.as<double>(), n, c->occ_sigma.as<float>(), s);
+        c->launches += launch_occ_query(fd, c->params.as<float>(), c->occ_pts.as<double>(), n,
+                                        c->occ_sigma.as<float>(), s);
         // cells may repeat: apply sequentially in draw order on the host
         std::vector<float> sig(n);
         CU(cudaMemcpyAsync(sig.data(), c->occ_sigma.p, n * sizeof(float), cudaMemcpyDeviceToHost, s));
@@ -966,12 +993,14 @@ int occupancy_update(dg_ctx* c) {
         c->h2d += pts.size() * sizeof(double) + total * sizeof(float);
       }
       launch_occ_bits(den, c->occ.as<uint8_t>() + pd.occ_off[casc], pd.occ_n[casc], float(threshold), s);
-      c->launches += 3;
+      c->launches += warm_up ? 2 : 1;  // (apply +) bits
     }
   }
   ++c->occ_updates;
   if (warm_up) {
-    CU(cudaStreamSynchronize(s));  // the pinned buffer is reused by the next prefetch
+    CU(cudaEventRecord(c->ev_occ_used, s));
+    CU(cudaEventSynchronize(c->ev_occ_up));  // the pinned buffer is reused by the next prefetch
+    c->occ_prefetched = c->occ_uploaded = false;
     occ_start_prefetch(c);
   }
   return DG_OK;
@@ -1062,6 +1091,9 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   if (const char* e = std::getenv("DG_ENC_BWD_MB"))
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&c->ev_occ_up, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&c->ev_occ_used, cudaEventDisableTiming));
   for (auto& e : c->ev) CU(cudaEventCreate(&e));
   TRY(ctx_alloc(c.get()));
   *out = c.release();
@@ -1074,11 +1106,15 @@ int dg_ctx_destroy(dg_ctx* c) {
   if (c->occ_prefetch.valid()) c->occ_prefetch.wait();
   if (c->occ_host) cudaFreeHost(c->occ_host);
   cudaStreamSynchronize(c->stream);
+  if (c->stream_copy) cudaStreamSynchronize(c->stream_copy);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
-  cudaStream_t s = c->stream;
+  if (c->ev_occ_up) cudaEventDestroy(c->ev_occ_up);
+  if (c->ev_occ_used) cudaEventDestroy(c->ev_occ_used);
+  cudaStream_t s = c->stream, sc = c->stream_copy;
   delete c;
   if (s) cudaStreamDestroy(s);
+  if (sc) cudaStreamDestroy(sc);
   return DG_OK;
 }
 
@@ -1393,6 +1429,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   uint64_t dropped = 0, bytes = 0;
   c->h2d = c->d2h = 0;
   c->cross_active = c->cfg.distortion_cross_correction != 0;
+  TRY(occ_try_upload(c, false));
   TRY(front_half(c, b, 1, step, &dropped, &bytes));
   const uint32_t NI = c->n_items;
   ItemArrays it = item_arrays(c);

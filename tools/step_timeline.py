@@ -22,10 +22,12 @@ b = abi.RayBatch()
 b.origin, b.dir, b.color_gt, b.image_id = (t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), t[3].data_ptr())
 b.n, b.first_ray_id, b.mem = len(o), 0, abi.DG_MEM_DEVICE
 st = abi.StepStats()
+ctx.enable_stage_timing(True)
 for i in range(40):
     torch.cuda.synchronize()
     a = time.perf_counter()
     assert ctx.train_step_raw(b, i, st) == 0
     torch.cuda.synchronize()
     w = (time.perf_counter() - a) * 1e3
-    print(f"step {i:3d} wall {w:7.2f} ms  launches {ctx.kernel_launches()}")
+    tot = ctx.stage_times()["total"]
+    print(f"step {i:3d} wall {w:7.2f} ms  device(marks) {tot:7.2f} ms  launches {ctx.kernel_launches()}")
