@@ -178,14 +178,21 @@ __device__ __forceinline__ void occupancy_walk(const double o[3], const double d
   if (run_open) on_run(run_start, t_cur);
 }
 
-// Closed-form sample count of ladder(): the first k with t_k >= hi minus k0.  t_k =
-// base + k step is non-decreasing in k under round-to-nearest, so the estimate is corrected by
-// evaluating t_k exactly as the ladder does at the boundary (bit-exact count).
-__device__ __forceinline__ uint32_t ladder_count(double iv_lo, double iv_hi, double t_enter, double t_exit,
-                                                 double offset, double step) {
+// Closed-form sample range of ladder() on one run: first index k0 and count n of the t_k =
+// base + k step in [lo, hi).  t_k is non-decreasing in k under round-to-nearest, so the
+// estimate is corrected by evaluating t_k exactly as the ladder does at the boundary
+// (bit-exact count).
+struct Ladder {
+  long long k0;
+  uint32_t n;
+  double hi;
+};
+
+__device__ __forceinline__ Ladder ladder_range(double iv_lo, double iv_hi, double t_enter, double t_exit,
+                                               double offset, double step) {
   const double lo = smax(iv_lo, t_enter);
   const double hi = smin(iv_hi, t_exit);
-  if (!(hi > lo)) return 0;
+  if (!(hi > lo)) return Ladder{0, 0u, hi};
   long long k0 = (long long)ceil(ddiv(dsub(dsub(lo, t_enter), offset), step));
   if (k0 < 0) k0 = 0;
   const double base = dadd(t_enter, offset);
@@ -193,7 +200,12 @@ __device__ __forceinline__ uint32_t ladder_count(double iv_lo, double iv_hi, dou
   if (k1 < k0) k1 = k0;
   while (k1 > k0 && dadd(base, dmul((double)(k1 - 1), step)) >= hi) --k1;
   while (dadd(base, dmul((double)k1, step)) < hi) ++k1;
-  return (uint32_t)(k1 - k0);
+  return Ladder{k0, (uint32_t)(k1 - k0), hi};
+}
+
+__device__ __forceinline__ uint32_t ladder_count(double iv_lo, double iv_hi, double t_enter, double t_exit,
+                                                 double offset, double step) {
+  return ladder_range(iv_lo, iv_hi, t_enter, t_exit, offset, step).n;
 }
 
 // cascade_march's occupancy walks (worker.cpp:79-110) as runs: on_run(lo, hi, cascade) for

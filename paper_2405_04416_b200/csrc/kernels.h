@@ -10,7 +10,7 @@
 namespace dg {
 
 // Per-item state after setup (structure of arrays, capacity NI).
-constexpr int kMaxRuns = 16;
+constexpr int kMaxRuns = 64;
 constexpr uint8_t kRunsOverflow = 0xff;
 
 struct ItemArrays {

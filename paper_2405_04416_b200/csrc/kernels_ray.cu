@@ -165,47 +165,84 @@ __global__ void k_item_setup(const Geo* __restrict__ geo, const PartDesc* __rest
   it.ncb[i] = ncb;
 }
 
-// One warp per item.  The occupied runs recorded by the item setup are replayed, each run's
-// ladder (render.cpp:21-35) emitted 32 samples at a time: t_k is non-decreasing in k, so the
-// lanes below hi are a prefix, and the sample writes coalesce.  Items with more than
-// kMaxRuns runs walk the occupancy grid again (all lanes in lock-step, uniform control flow).
-__global__ void k_march_fill(const PartDesc* __restrict__ parts, const uint8_t* __restrict__ occ,
-                             uint32_t n_items, ItemArrays it, SampleArrays sm, double step,
-                             uint64_t seed, uint64_t batch_id, int jitter) {
+// One warp per item, replaying the occupied runs recorded by the item setup.  A lane per run
+// computes the run's ladder range (first index k0, count n) and warp scans turn the counts
+// into output slots (fine and coarse samples keep march order in their own arrays); then the
+// item's samples are emitted 32 at a time, each lane locating its run by binary search over
+// the run prefix, so long runs (a mostly occupied grid) and many short runs (a fragmented
+// one after occupancy updates) both keep every lane busy and the writes coalesce.  Items with
+// more than kMaxRuns runs are left to k_march_fill_walk.
+__device__ __forceinline__ uint32_t warp_excl_scan_u(uint32_t v) {
+  const unsigned lane = threadIdx.x & 31;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  return x - v;
+}
+
+constexpr int kFillWarps = 4;
+
+__global__ void __launch_bounds__(32 * kFillWarps) k_march_fill(const PartDesc* __restrict__ parts,
+                                                               const uint8_t* __restrict__ occ,
+                                                               uint32_t n_items, ItemArrays it,
+                                                               SampleArrays sm, double step, uint64_t seed,
+                                                               uint64_t batch_id, int jitter) {
+  __shared__ uint32_t s_excl[kFillWarps][kMaxRuns];  // exclusive prefix of the run counts
+  __shared__ uint32_t s_out[kFillWarps][kMaxRuns];   // output slot of the run's first sample
+  __shared__ long long s_k0[kFillWarps][kMaxRuns];
+  __shared__ double s_hi[kFillWarps][kMaxRuns];
+  const uint32_t w = threadIdx.x >> 5;
   const uint32_t i = (uint32_t)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const uint32_t lane = threadIdx.x & 31;
   if (i >= n_items) return;  // warp-uniform
+  const uint8_t nr = it.nrun[i];
+  if (nr == kRunsOverflow) return;  // k_march_fill_walk
   const RayRec& r = it.rec[i];
   const double te = it.te[i], tx = it.tx[i];
   const double offset = jitter ? dmul(step, counter_uniform(seed, (uint64_t)r.ray_id, batch_id))
                                : dmul(0.5, step);
   const double base = dadd(te, offset), half = dmul(0.5, step);
-  uint32_t pf = it.off[i], pc = it.off[n_items + i];
-  auto run = [&](double a, double b, int casc) {
-    const double lo = smax(a, te), hi = smin(b, tx);
-    if (!(hi > lo)) return;
-    long long k0 = (long long)ceil(ddiv(dsub(dsub(lo, te), offset), step));
-    if (k0 < 0) k0 = 0;
-    uint32_t& cur = casc == 0 ? pf : pc;
-    for (long long kb = k0;; kb += 32) {
-      const double t = dadd(base, dmul((double)(kb + lane), step));
-      const bool v = t < hi;
-      const unsigned m = __ballot_sync(0xffffffffu, v);
-      if (v) {
-        const uint32_t s = cur + lane;
-        sm.t[s] = t;
-        sm.delta[s] = smin(step, dsub(hi, dsub(t, half)));
-        sm.item[s] = i;
-      }
-      cur += __popc(m);
-      if (m != 0xffffffffu) break;
+  const uint32_t pf = it.off[i], pc = it.off[n_items + i];
+  uint32_t tot = 0, tot_f = 0, tot_c = 0;
+  for (uint32_t r0 = 0; r0 < nr; r0 += 32) {
+    const uint32_t k = r0 + lane;
+    Ladder L{0, 0u, 0.0};
+    uint32_t casc = 0;
+    if (k < nr) {
+      const double2 rr = it.runs[(uint64_t)i * kMaxRuns + k];
+      casc = it.run_casc[(uint64_t)i * kMaxRuns + k];
+      L = ladder_range(rr.x, rr.y, te, tx, offset, step);
     }
-  };
-  const uint8_t nr = it.nrun[i];
-  if (nr == kRunsOverflow) return;  // k_march_fill_walk
-  for (int k = 0; k < nr; ++k) {
-    const double2 rr = it.runs[(uint64_t)i * kMaxRuns + k];
-    run(rr.x, rr.y, it.run_casc[(uint64_t)i * kMaxRuns + k]);
+    const uint32_t nf = casc == 0 ? L.n : 0u, nc = casc == 0 ? 0u : L.n;
+    const uint32_t ex = warp_excl_scan_u(L.n), exf = warp_excl_scan_u(nf), exc = warp_excl_scan_u(nc);
+    if (k < nr) {
+      s_excl[w][k] = tot + ex;
+      s_out[w][k] = casc == 0 ? pf + tot_f + exf : pc + tot_c + exc;
+      s_k0[w][k] = L.k0;
+      s_hi[w][k] = L.hi;
+    }
+    tot += __shfl_sync(0xffffffffu, ex + L.n, 31);
+    tot_f += __shfl_sync(0xffffffffu, exf + nf, 31);
+    tot_c += __shfl_sync(0xffffffffu, exc + nc, 31);
+  }
+  __syncwarp();
+  for (uint32_t q = lane; q < tot; q += 32) {
+    // the run holding q: the last run whose exclusive prefix is <= q (recorded runs are non-empty)
+    uint32_t lo = 0, hi = nr;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_excl[w][mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t j = q - s_excl[w][lo];
+    const double t = dadd(base, dmul((double)(s_k0[w][lo] + j), step));
+    const uint32_t o = s_out[w][lo] + j;
+    sm.t[o] = t;
+    sm.delta[o] = smin(step, dsub(s_hi[w][lo], dsub(t, half)));
+    sm.item[o] = i;
   }
 }
 
@@ -793,8 +830,8 @@ void launch_march_fill(const PartDesc* parts, const uint8_t* occ, uint32_t n_ite
                        ItemArrays it, SampleArrays sm, uint32_t n_fine, double step, uint64_t seed,
                        uint64_t batch_id, int jitter, cudaStream_t s) {
   if (!n_items) return;
-  k_march_fill<<<blocks((uint64_t)n_items * 32, 128), 128, 0, s>>>(parts, occ, n_items, it, sm, step, seed,
-                                                                   batch_id, jitter);
+  k_march_fill<<<blocks((uint64_t)n_items * 32, 32 * kFillWarps), 32 * kFillWarps, 0, s>>>(
+      parts, occ, n_items, it, sm, step, seed, batch_id, jitter);
   k_march_fill_walk<<<blocks(n_items, 128), 128, 0, s>>>(parts, occ, n_items, it, sm, step, seed, batch_id,
                                                          jitter);
   if (sm.pn && sm.p)

@@ -154,6 +154,12 @@ struct dg_ctx {
   // ... and go up to the device on a copy stream as soon as they are drawn, so the 24 B/cell
   // transfer overlaps the training steps before the update instead of stalling it
   cudaStream_t stream_copy = nullptr;
+  // Pinned staging arena for the step's small host <-> device transfers.  A pageable source
+  // makes cudaMemcpyAsync wait for the stream to drain and a pageable destination makes it
+  // synchronous, so every plan upload / count readback would otherwise cost a full pipeline
+  // bubble.  Bump-allocated per API call (pin_reset) after the stream is idle.
+  uint8_t* pin = nullptr;
+  size_t pin_cap = 0, pin_used = 0;
   cudaEvent_t ev_occ_up = nullptr, ev_occ_used = nullptr;
   bool occ_uploaded = false;
   double step = 0.0;
@@ -373,6 +379,36 @@ int upload(DBuf& b, const void* src, size_t bytes, cudaStream_t s) {
   return DG_OK;
 }
 
+void* pin_alloc(dg_ctx* c, size_t bytes) {
+  const size_t at = (c->pin_used + 15) & ~size_t(15);
+  if (!c->pin || at + bytes > c->pin_cap) return nullptr;
+  c->pin_used = at + bytes;
+  return c->pin + at;
+}
+
+int pin_reset(dg_ctx* c) {
+  CU(cudaStreamSynchronize(c->stream));  // nothing in flight reads the arena any more
+  c->pin_used = 0;
+  return DG_OK;
+}
+
+// Small step-time upload through the pinned arena (falls back to a plain copy when full).
+int upload_small(dg_ctx* c, DBuf& b, const void* src, size_t bytes) {
+  void* h = bytes ? pin_alloc(c, bytes) : nullptr;
+  if (!h) return upload(b, src, bytes, c->stream);
+  std::memcpy(h, src, bytes);
+  TRY(b.ensure(bytes));
+  CU(cudaMemcpyAsync(b.p, h, bytes, cudaMemcpyHostToDevice, c->stream));
+  return DG_OK;
+}
+
+// Pinned landing slot for a small readback (nullptr when the arena is full: callers then
+// read into their own memory).
+template <class T>
+T* pin_slot(dg_ctx* c, size_t count) {
+  return static_cast<T*>(pin_alloc(c, count * sizeof(T)));
+}
+
 void occ_start_prefetch(dg_ctx* c);
 
 int ctx_alloc(dg_ctx* c) {
@@ -559,11 +595,15 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   // per-slot dispatch counts: pos[slot * n] for slot = 0..P
   TRY(c->small.ensure(4096 * 4));
   std::vector<uint32_t> slot_start(P + 1);
-  CU(cudaMemcpy2DAsync(slot_start.data(), 4, c->h_pos.as<uint32_t>(), n ? n * 4 : 4, 4, P + 1,
-                       cudaMemcpyDeviceToHost, s));
+  uint32_t* ss_pin = pin_slot<uint32_t>(c, P + 1);
+  unsigned long long* dr_pin = pin_slot<unsigned long long>(c, 1);
   unsigned long long dropped = 0;
-  CU(cudaMemcpyAsync(&dropped, c->dropped.p, 8, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpy2DAsync(ss_pin ? ss_pin : slot_start.data(), 4, c->h_pos.as<uint32_t>(), n ? n * 4 : 4, 4,
+                       P + 1, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(dr_pin ? dr_pin : &dropped, c->dropped.p, 8, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  if (ss_pin) std::memcpy(slot_start.data(), ss_pin, (P + 1) * 4);
+  if (dr_pin) dropped = *dr_pin;
   c->d2h += (P + 1) * 4 + 8;
   if (n == 0)
     for (auto& v : slot_start) v = 0;
@@ -596,13 +636,16 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
       for (uint32_t p = 0; p < P; ++p) cnt_send[uint64_t(r) * P + p] = send_cnt[p];
     TRY(c->send_buf.ensure(cnt_send.size() * 8));
     TRY(c->recv_buf.ensure(cnt_recv.size() * 8));
-    CU(cudaMemcpyAsync(c->send_buf.p, cnt_send.data(), cnt_send.size() * 8, cudaMemcpyHostToDevice, s));
+    TRY(upload_small(c, c->send_buf, cnt_send.data(), cnt_send.size() * 8));
     std::vector<uint64_t> sb(W, uint64_t(P) * 8), rb(W, uint64_t(P) * 8);
     std::string err;
     int rc = c->comm->alltoallv(c->send_buf.p, sb, c->recv_buf.p, rb, s, err);
     if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
-    CU(cudaMemcpyAsync(cnt_recv.data(), c->recv_buf.p, cnt_recv.size() * 8, cudaMemcpyDeviceToHost, s));
+    uint64_t* cr_pin = pin_slot<uint64_t>(c, cnt_recv.size());
+    CU(cudaMemcpyAsync(cr_pin ? cr_pin : cnt_recv.data(), c->recv_buf.p, cnt_recv.size() * 8,
+                       cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    if (cr_pin) std::memcpy(cnt_recv.data(), cr_pin, cnt_recv.size() * 8);
     c->h2d += cnt_send.size() * 8;
     c->d2h += cnt_recv.size() * 8;
     // cnt_recv[src][p]: records src sends to partition p -> layouts (exchange_plan.cpp)
@@ -618,7 +661,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
     const uint32_t nblk = nl * uint32_t(W);
     std::vector<uint64_t> tab(plan.block_src);
     tab.insert(tab.end(), plan.block_dst.begin(), plan.block_dst.end());
-    TRY(upload(c->perm_tab, tab.data(), tab.size() * 8, s));
+    TRY(upload_small(c, c->perm_tab, tab.data(), tab.size() * 8));
     TRY(c->rec.ensure(n_items * sizeof(RayRec) + 16));
     if (n_items) {
       k_block_permute<<<unsigned((n_items + 255) / 256), 256, 0, s>>>(
@@ -632,7 +675,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   const uint32_t NI = uint32_t(n_items);
   c->n_items = NI;
   c->part_item_off = pio;
-  TRY(upload(c->part_item_off_d, pio.data(), pio.size() * 4, s));
+  TRY(upload_small(c, c->part_item_off_d, pio.data(), pio.size() * 4));
   c->h2d += pio.size() * 4;
   TRY(c->it_te.ensure(uint64_t(NI) * 8 + 16));
   TRY(c->it_tx.ensure(uint64_t(NI) * 8 + 16));
@@ -666,14 +709,20 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
                        uint64_t(P) * NI + 1));
   // field sample ranges: off[pio[lp]] (fine) and off[NI + pio[lp]] (coarse), lp = 0..nl
   std::vector<uint32_t> fo(2 * (nl + 1));
+  uint32_t* fo_pin = pin_slot<uint32_t>(c, fo.size() + 1);  // + the error flag
+  uint32_t* fo_dst = fo_pin ? fo_pin : fo.data();
+  uint32_t err_flag = 0;
   for (uint32_t k = 0; k <= nl; ++k) {
-    CU(cudaMemcpyAsync(&fo[k], c->it_off.as<uint32_t>() + pio[k], 4, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(&fo[nl + 1 + k], c->it_off.as<uint32_t>() + NI + pio[k], 4,
+    CU(cudaMemcpyAsync(&fo_dst[k], c->it_off.as<uint32_t>() + pio[k], 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&fo_dst[nl + 1 + k], c->it_off.as<uint32_t>() + NI + pio[k], 4,
                        cudaMemcpyDeviceToHost, s));
   }
-  uint32_t err_flag = 0;
-  CU(cudaMemcpyAsync(&err_flag, c->error.p, 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(fo_pin ? &fo_pin[fo.size()] : &err_flag, c->error.p, 4, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  if (fo_pin) {
+    std::memcpy(fo.data(), fo_pin, fo.size() * 4);
+    err_flag = fo_pin[fo.size()];
+  }
   c->d2h += fo.size() * 4 + 4;
   if (err_flag & 1u) return set_err(DG_ERANGE, "appearance: unknown image id");
   if (err_flag & 2u) return set_err(DG_EPROTO, "worker: dispatched ray does not intersect this region");
@@ -704,9 +753,9 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
     tf[f + 1] = tf[f] + (cnt + 127) / 128;
     tb[f + 1] = tb[f] + (cnt + 63) / 64;
   }
-  TRY(upload(c->field_off_d, c->field_off.data(), c->field_off.size() * 4, s));
-  TRY(upload(c->tile_off_f, tf.data(), tf.size() * 4, s));
-  TRY(upload(c->tile_off_b, tb.data(), tb.size() * 4, s));
+  TRY(upload_small(c, c->field_off_d, c->field_off.data(), c->field_off.size() * 4));
+  TRY(upload_small(c, c->tile_off_f, tf.data(), tf.size() * 4));
+  TRY(upload_small(c, c->tile_off_b, tb.data(), tb.size() * 4));
   c->h2d += (c->field_off.size() + tf.size() + tb.size()) * 4;
   mark(c, 2);
   c->have_last = true;
@@ -803,8 +852,8 @@ int exchange_partials(dg_ctx* c, const std::vector<uint32_t>& pair_cnt, uint64_t
   const std::vector<uint64_t>& sbytes = plan.send_bytes;
   const std::vector<uint64_t>& rbytes = plan.recv_bytes;
   const uint64_t so = plan.send_total, ro = plan.recv_total;
-  TRY(upload(c->stream_send_d, send_off.data(), send_off.size() * 8, s));
-  TRY(upload(c->stream_recv_d, recv_off.data(), recv_off.size() * 8, s));
+  TRY(upload_small(c, c->stream_send_d, send_off.data(), send_off.size() * 8));
+  TRY(upload_small(c, c->stream_recv_d, recv_off.data(), recv_off.size() * 8));
   c->h2d += (send_off.size() + recv_off.size()) * 8;
   TRY(c->send_buf.ensure(so * sizeof(PartialRec) + 16));
   // cross-segment distortion: the three aggregates travel in a parallel stream (16 B/record)
@@ -1092,6 +1141,8 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
+  c->pin_cap = 1 << 20;
+  CU(cudaHostAlloc(reinterpret_cast<void**>(&c->pin), c->pin_cap, cudaHostAllocDefault));
   CU(cudaEventCreateWithFlags(&c->ev_occ_up, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&c->ev_occ_used, cudaEventDisableTiming));
   for (auto& e : c->ev) CU(cudaEventCreate(&e));
@@ -1105,6 +1156,7 @@ int dg_ctx_destroy(dg_ctx* c) {
   cudaSetDevice(c->device);
   if (c->occ_prefetch.valid()) c->occ_prefetch.wait();
   if (c->occ_host) cudaFreeHost(c->occ_host);
+  if (c->pin) cudaFreeHost(c->pin);
   cudaStreamSynchronize(c->stream);
   if (c->stream_copy) cudaStreamSynchronize(c->stream_copy);
   for (auto& e : c->ev)
@@ -1428,6 +1480,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   const uint32_t P = c->P, nl = uint32_t(c->local.size());
   uint64_t dropped = 0, bytes = 0;
   c->h2d = c->d2h = 0;
+  TRY(pin_reset(c));
   c->cross_active = c->cfg.distortion_cross_correction != 0;
   TRY(occ_try_upload(c, false));
   TRY(front_half(c, b, 1, step, &dropped, &bytes));
@@ -1436,12 +1489,15 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   SampleArrays sm = sample_arrays(c);
   // pair counts for exchange 2 (P > 1)
   std::vector<uint32_t> pair_cnt(uint64_t(nl) * P, 0);
+  uint32_t* pair_pin = nullptr;
   if (P > 1 && NI) {
     TRY(c->small.ensure(uint64_t(nl) * P * 4 + 16));
     launch_pair_counts(NI, nl, P, c->part_item_off_d.as<uint32_t>(), nullptr,
                        c->it_cscan.as<uint32_t>(), c->small.as<uint32_t>(), s);
     ++c->launches;
-    CU(cudaMemcpyAsync(pair_cnt.data(), c->small.p, pair_cnt.size() * 4, cudaMemcpyDeviceToHost, s));
+    pair_pin = pin_slot<uint32_t>(c, pair_cnt.size());
+    CU(cudaMemcpyAsync(pair_pin ? pair_pin : pair_cnt.data(), c->small.p, pair_cnt.size() * 4,
+                       cudaMemcpyDeviceToHost, s));
     c->d2h += pair_cnt.size() * 4;
   }
   CU(cudaMemsetAsync(c->loss.p, 0, sizeof(LossAccum), s));
@@ -1457,6 +1513,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   c->launches += 3;
   // X2: partial exchange (alias on a single rank)
   CU(cudaStreamSynchronize(s));  // pair counts on the host
+  if (pair_pin) std::memcpy(pair_cnt.data(), pair_pin, pair_cnt.size() * 4);
   const PartialRec* recv = c->send_buf.as<PartialRec>();
   const float4* recv_x = nullptr;
   if (P > 1) {
@@ -1494,8 +1551,10 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   c->worker_step = step + 1;
   TRY(occupancy_update(c));
   LossAccum la;
-  CU(cudaMemcpyAsync(&la, c->loss.p, sizeof la, cudaMemcpyDeviceToHost, s));
+  LossAccum* la_pin = pin_slot<LossAccum>(c, 1);
+  CU(cudaMemcpyAsync(la_pin ? la_pin : &la, c->loss.p, sizeof la, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  if (la_pin) la = *la_pin;
   c->d2h += sizeof la;
   if (la.error & 2u) return set_err(DG_EPROTO, "worker: missing partial in batch %llu", (unsigned long long)step);
   if (c->timing) {
@@ -1539,7 +1598,8 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   // eval appearance vector through the wire (EvalRequest reals, wire.cpp:170-176)
   std::vector<float> app(c->cfg.appearance_dim + 1, 0.0f);
   for (uint32_t k = 0; k < c->cfg.appearance_dim; ++k) app[k] = appearance ? appearance[k] : 0.0f;
-  TRY(upload(c->eval_app, app.data(), app.size() * sizeof(float), s));
+  TRY(pin_reset(c));
+  TRY(upload_small(c, c->eval_app, app.data(), app.size() * sizeof(float)));
   const uint32_t saved_rows = c->app_rows;
   c->app_rows = std::max<uint32_t>(c->app_rows, 1);
   const int rc = front_half(c, &bb, 0, 0, &dropped, &bytes);

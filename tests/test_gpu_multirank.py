@@ -69,9 +69,15 @@ def _rank_main(rank, world, port, ref_path, errq, cross=0):
         dist.all_reduce(tot)
         ref = np.load(ref_path)
         assert np.allclose(tot.numpy(), ref["losses"], rtol=1e-6, atol=1e-12), (tot.numpy(), ref["losses"])
+        # Reds sum in a different order on 1 and 2 ranks; Adam turns a sign flip of a
+        # near-zero gradient into a full +-lr step of that entry, so the bar is on the
+        # fraction of entries off by more than 1e-3 lr (as the parity suite's Adam check) plus
+        # a loose rel L2.
         for g in ctx.local:
-            err = rel_l2(ctx.get_params(g), ref[f"p{g}"])
-            assert err < 1e-5, (rank, g, err)
+            a, b = ctx.get_params(g), ref[f"p{g}"]
+            off = float(np.mean(np.abs(a.astype(np.float64) - b) > 1e-3 * cfg.lr_start))
+            err = rel_l2(a, b)
+            assert off <= 1e-3 and err < 1e-4, (rank, g, off, err)
         dist.barrier()
         dist.destroy_process_group()
     except Exception:
