@@ -307,6 +307,43 @@ int dg_field_backward(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const d
 int dg_adam_step(dg_ctx* ctx, double lr);
 double dg_lr_at(const dg_run_config* cfg, uint64_t step);
 
+/* ---- compositing stages (batched overloads of render.hpp / train.hpp, fp64 inside) ----
+ * Segment g owns samples [seg_off[g], seg_off[g+1]) (seg_off: n_seg + 1 entries from 0, in
+ * march order); ray r owns segments [ray_off[r], ray_off[r+1]) in schedule order.  rgb is
+ * 3 floats per sample / segment / ray.  All arrays on the host or all on the device (mem). */
+/* local_render (render.cpp:46-78): per segment rgb, transmittance and depth_sum (optional);
+ * with out_distortion (3 per segment: weight_sum, weight_moment, distortion_local) also
+ * accumulate_distortion_stats (render.cpp:80-99) over the ray span [ray_t0, ray_t1]. */
+int dg_local_render(dg_ctx* ctx, const double* t, const double* delta, const float* sigma,
+                    const float* rgb, const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0,
+                    const double* ray_t1, float* out_rgb, float* out_transmittance,
+                    float* out_depth_sum, double* out_distortion, int32_t mem);
+/* local_render_backward (render.cpp:145-179): per-sample sigma / rgb gradients from the
+ * segment upstream (d_rgb, d_transmittance) and an optional per-sample weight upstream. */
+int dg_local_render_backward(dg_ctx* ctx, const double* t, const double* delta, const float* sigma,
+                             const float* rgb, const uint64_t* seg_off, uint64_t n_seg,
+                             const float* d_rgb, const float* d_transmittance,
+                             const float* weight_upstream, float* sigma_grad, float* rgb_grad,
+                             int32_t mem);
+/* merge_forward (render.cpp:101-116); DG_EINVAL for a ray with no partials. */
+int dg_merge_forward(dg_ctx* ctx, const float* seg_rgb, const float* seg_transmittance,
+                     const float* seg_depth_sum, const uint64_t* ray_off, uint64_t n_rays,
+                     float* rgb, float* transmittance, float* depth, int32_t mem);
+/* merge_backward (render.cpp:118-143): per-segment dL/dC_i, dL/dT_i. */
+int dg_merge_backward(dg_ctx* ctx, const float* seg_rgb, const float* seg_transmittance,
+                      const uint64_t* ray_off, uint64_t n_rays, const float* d_rgb,
+                      const float* d_transmittance, float* seg_d_rgb, float* seg_d_transmittance,
+                      int32_t mem);
+/* loss_rgb / loss_rgb_grad, loss_transmittance_single / loss_transmittance_grad
+ * (train.cpp:8-36) per ray; any output may be NULL. */
+int dg_ray_losses(dg_ctx* ctx, const float* rgb, const float* color_gt, const float* transmittance,
+                  uint64_t n, double eps, double* loss_rgb, double* loss_transmittance, float* d_rgb,
+                  float* d_transmittance, int32_t mem);
+/* loss_distortion + loss_distortion_grad (train.cpp:38-75) per segment. */
+int dg_distortion_loss(dg_ctx* ctx, const double* weights, const double* midpoints,
+                       const double* interval_lengths, const uint64_t* seg_off, uint64_t n_seg,
+                       double* loss, double* grads, int32_t mem);
+
 /* ---- introspection of the last dg_train_step / dg_render on this rank ---- */
 typedef struct dg_item_view {
   uint64_t n_items;       /* (ray, partition) segments of this partition */

@@ -58,6 +58,24 @@ struct MergedRender {
   double depth = 0.0;
 };
 
+// CameraPose (partition.hpp:15-30): camera-to-world rotation (row-major), pinhole intrinsics.
+struct CameraPose {
+  uint32_t image_id = 0;
+  double rotation[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  Vec3 translation;
+  double fx = 0.0, fy = 0.0, cx = 0.0, cy = 0.0;
+  uint32_t width = 0, height = 0;
+};
+
+// EvalImage (worker.hpp:164-171).
+struct EvalImage {
+  uint32_t width = 0, height = 0;
+  std::vector<Vec3> color;
+  std::vector<double> transmittance;
+  std::vector<double> depth;
+  std::vector<Vec3> attribution;
+};
+
 struct StepStats {
   uint64_t step = 0;
   double loss_rgb = 0.0;
@@ -224,6 +242,42 @@ class DistributedRun {
       out[i].color = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
       out[i].transmittance = T[i];
       out[i].depth = depth[i];
+    }
+    return out;
+  }
+
+  // DistributedRun::evaluate_image (worker.cpp:836-880): one ray per pixel centre, merged
+  // colour / transmittance / depth and the per-region attribution.
+  EvalImage evaluate_image(const CameraPose& pose, std::span<const double> appearance_vec) {
+    dg_camera cam{};
+    cam.image_id = pose.image_id;
+    cam.width = pose.width;
+    cam.height = pose.height;
+    for (int k = 0; k < 9; ++k) cam.rotation[k] = pose.rotation[k];
+    cam.translation[0] = pose.translation.x;
+    cam.translation[1] = pose.translation.y;
+    cam.translation[2] = pose.translation.z;
+    cam.fx = pose.fx;
+    cam.fy = pose.fy;
+    cam.cx = pose.cx;
+    cam.cy = pose.cy;
+    const size_t n = size_t(pose.width) * pose.height;
+    std::vector<float> app(appearance_vec.begin(), appearance_vec.end());
+    std::vector<float> rgb(3 * n), T(n), depth(n), attr(3 * n);
+    dg_merged m{rgb.data(), T.data(), depth.data(), attr.data(), DG_MEM_HOST, 0};
+    check(dg_render_image(ctx_, &cam, app.empty() ? nullptr : app.data(), &m));
+    EvalImage out;
+    out.width = pose.width;
+    out.height = pose.height;
+    out.color.resize(n);
+    out.transmittance.resize(n);
+    out.depth.resize(n);
+    out.attribution.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+      out.color[i] = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+      out.transmittance[i] = T[i];
+      out.depth[i] = depth[i];
+      out.attribution[i] = {attr[3 * i], attr[3 * i + 1], attr[3 * i + 2]};
     }
     return out;
   }

@@ -176,6 +176,23 @@ void launch_mlp_bwd(const MlpLaunch& m, int num_sms, cudaStream_t s);
 void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);
 void launch_mlp_bwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);  // tile_off at 128
 
+// ---- compositing stage entry points (kernels_render_api.cu), fp64 like the reference ----
+void launch_local_render(const double* t, const double* delta, const float* sigma, const float* rgb,
+                         const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0,
+                         const double* ray_t1, float* out_rgb, float* out_T, float* out_depth,
+                         double* out_dist, double* cache, cudaStream_t s);
+void launch_local_render_bwd(const double* delta, const float* rgb, const uint64_t* seg_off, uint64_t n_seg,
+                             const double* cache, const float* d_rgb, const float* d_T, const float* w_up,
+                             float* sigma_grad, float* rgb_grad, cudaStream_t s);
+void launch_merge_fwd(const float* srgb, const float* sT, const float* sdepth, const uint64_t* ray_off,
+                      uint64_t n_rays, float* rgb, float* T, float* depth, cudaStream_t s);
+void launch_merge_bwd(const float* srgb, const float* sT, const uint64_t* ray_off, uint64_t n_rays,
+                      const float* d_rgb, const float* d_T, float* sd_rgb, float* sd_T, cudaStream_t s);
+void launch_ray_losses(const float* rgb, const float* gt, const float* T, uint64_t n, double eps,
+                       double* l_rgb, double* l_T, float* d_rgb, float* d_T, cudaStream_t s);
+void launch_distortion(const double* w, const double* s_, const double* ds, const uint64_t* seg_off,
+                       uint64_t n_seg, double* loss, double* grad, cudaStream_t s);
+
 // ---- optimizer / init (kernels_adam.cu) ----
 void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, float b1, float b2,
                  float eps, float inv_bias1, float inv_sqrt_bias2, cudaStream_t s);

@@ -22,6 +22,7 @@
 #include <cstring>
 #include <chrono>
 #include <future>
+#include <tuple>
 #include <memory>
 #include <random>
 #include <string>
@@ -2001,6 +2002,231 @@ int dg_field_backward(dg_ctx* c, uint32_t p, uint32_t cascade, const double* poi
   if (mem == DG_MEM_DEVICE) return set_err(DG_EINVAL, "dg_field_backward: host buffers only");
   if (!sigma_grad || !rgb_grad) return set_err(DG_EINVAL, "null gradients");
   return field_stage(c, p, cascade, points, dirs, app, n, sigma_grad, rgb_grad, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------- compositing stage entry points
+}  // extern "C"
+
+namespace {
+
+// Inputs / outputs of a stage call: device pointers pass through, host arrays are staged.
+struct StageIo {
+  dg_ctx* c;
+  int32_t mem;
+  std::vector<std::unique_ptr<DBuf>> tmp;
+  std::vector<std::tuple<void*, const DBuf*, size_t>> back;  // host dst, device src, bytes
+  template <class T>
+  int in(const T* p, uint64_t n, const T** out) {
+    if (!p || mem == DG_MEM_DEVICE || n == 0) {
+      *out = p;
+      return DG_OK;
+    }
+    tmp.emplace_back(new DBuf);
+    TRY(upload(*tmp.back(), p, n * sizeof(T), c->stream));
+    *out = tmp.back()->as<T>();
+    return DG_OK;
+  }
+  template <class T>
+  int out(T* p, uint64_t n, T** dev) {
+    if (!p || mem == DG_MEM_DEVICE || n == 0) {
+      *dev = p;
+      return DG_OK;
+    }
+    tmp.emplace_back(new DBuf);
+    TRY(tmp.back()->ensure(n * sizeof(T)));
+    back.emplace_back(p, tmp.back().get(), n * sizeof(T));
+    *dev = tmp.back()->as<T>();
+    return DG_OK;
+  }
+  int finish() {
+    for (auto& [h, d, bytes] : back) CU(cudaMemcpyAsync(h, d->p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return DG_OK;
+  }
+};
+
+// Segment offsets (n + 1 entries, non-decreasing, from 0) on the host, for validation and
+// for the sample totals.
+int host_offsets(dg_ctx* c, const uint64_t* off, uint64_t n, int32_t mem, std::vector<uint64_t>& h) {
+  if (!off) return set_err(DG_EINVAL, "null offsets");
+  h.resize(n + 1);
+  if (mem == DG_MEM_DEVICE) CU(cudaMemcpy(h.data(), off, (n + 1) * 8, cudaMemcpyDeviceToHost));
+  else std::memcpy(h.data(), off, (n + 1) * 8);
+  if (h[0] != 0) return set_err(DG_EINVAL, "offsets must start at 0");
+  for (uint64_t i = 0; i < n; ++i)
+    if (h[i + 1] < h[i]) return set_err(DG_EINVAL, "offsets must be non-decreasing");
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dg_local_render(dg_ctx* c, const double* t, const double* delta, const float* sigma, const float* rgb,
+                    const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0, const double* ray_t1,
+                    float* out_rgb, float* out_T, float* out_depth_sum, double* out_distortion,
+                    int32_t mem) {
+  TRY(check_ctx(c));
+  if (!out_rgb || !out_T) return set_err(DG_EINVAL, "null outputs");
+  std::vector<uint64_t> off;
+  TRY(host_offsets(c, seg_off, n_seg, mem, off));
+  const uint64_t ns = off[n_seg];
+  if (ns && (!t || !delta || !sigma || !rgb)) return set_err(DG_EINVAL, "null sample arrays");
+  if (out_distortion && (!ray_t0 || !ray_t1)) return set_err(DG_EINVAL, "distortion stats need the ray span");
+  StageIo io{c, mem, {}, {}};
+  const double *dt, *dd, *t0 = nullptr, *t1 = nullptr;
+  const float *dsig, *drgb;
+  const uint64_t* doff;
+  TRY(io.in(t, ns, &dt));
+  TRY(io.in(delta, ns, &dd));
+  TRY(io.in(sigma, ns, &dsig));
+  TRY(io.in(rgb, 3 * ns, &drgb));
+  TRY(io.in(seg_off, n_seg + 1, &doff));
+  TRY(io.in(ray_t0, n_seg, &t0));
+  TRY(io.in(ray_t1, n_seg, &t1));
+  float *orgb, *oT, *odep;
+  double* odist;
+  TRY(io.out(out_rgb, 3 * n_seg, &orgb));
+  TRY(io.out(out_T, n_seg, &oT));
+  TRY(io.out(out_depth_sum, n_seg, &odep));
+  TRY(io.out(out_distortion, 3 * n_seg, &odist));
+  launch_local_render(dt, dd, dsig, drgb, doff, n_seg, out_distortion ? t0 : nullptr,
+                      out_distortion ? t1 : nullptr, orgb, oT, odep, odist, nullptr, c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
+int dg_local_render_backward(dg_ctx* c, const double* t, const double* delta, const float* sigma,
+                             const float* rgb, const uint64_t* seg_off, uint64_t n_seg, const float* d_rgb,
+                             const float* d_transmittance, const float* weight_upstream, float* sigma_grad,
+                             float* rgb_grad, int32_t mem) {
+  TRY(check_ctx(c));
+  if (!d_rgb || !d_transmittance) return set_err(DG_EINVAL, "null upstream");
+  std::vector<uint64_t> off;
+  TRY(host_offsets(c, seg_off, n_seg, mem, off));
+  const uint64_t ns = off[n_seg];
+  if (ns && (!t || !delta || !sigma || !rgb || !sigma_grad || !rgb_grad))
+    return set_err(DG_EINVAL, "null sample arrays");
+  StageIo io{c, mem, {}, {}};
+  const double *dt, *dd;
+  const float *dsig, *drgb, *ug, *ut, *uw;
+  const uint64_t* doff;
+  TRY(io.in(t, ns, &dt));
+  TRY(io.in(delta, ns, &dd));
+  TRY(io.in(sigma, ns, &dsig));
+  TRY(io.in(rgb, 3 * ns, &drgb));
+  TRY(io.in(seg_off, n_seg + 1, &doff));
+  TRY(io.in(d_rgb, 3 * n_seg, &ug));
+  TRY(io.in(d_transmittance, n_seg, &ut));
+  TRY(io.in(weight_upstream, ns, &uw));
+  float *sg, *cg;
+  TRY(io.out(sigma_grad, ns, &sg));
+  TRY(io.out(rgb_grad, 3 * ns, &cg));
+  // the forward sweep's (alpha, prefix) cache (LocalRenderCache), then the reverse sweep
+  DBuf cache, scratch;
+  TRY(cache.ensure(ns * 16 + 16));
+  TRY(scratch.ensure(n_seg * 20 + 16));
+  float* srgb = scratch.as<float>();
+  launch_local_render(dt, dd, dsig, drgb, doff, n_seg, nullptr, nullptr, srgb, srgb + 3 * n_seg, nullptr,
+                      nullptr, cache.as<double>(), c->stream);
+  launch_local_render_bwd(dd, drgb, doff, n_seg, cache.as<double>(), ug, ut, uw, sg, cg, c->stream);
+  c->launches += 2;
+  return io.finish();
+}
+
+int dg_merge_forward(dg_ctx* c, const float* seg_rgb, const float* seg_transmittance,
+                     const float* seg_depth_sum, const uint64_t* ray_off, uint64_t n_rays, float* rgb,
+                     float* transmittance, float* depth, int32_t mem) {
+  TRY(check_ctx(c));
+  if (!rgb || !transmittance) return set_err(DG_EINVAL, "null outputs");
+  std::vector<uint64_t> off;
+  TRY(host_offsets(c, ray_off, n_rays, mem, off));
+  for (uint64_t r = 0; r < n_rays; ++r)
+    if (off[r + 1] == off[r]) return set_err(DG_EINVAL, "merge: no partials");  // render.cpp:102
+  const uint64_t ns = off[n_rays];
+  StageIo io{c, mem, {}, {}};
+  const float *sr, *sT, *sd;
+  const uint64_t* doff;
+  TRY(io.in(seg_rgb, 3 * ns, &sr));
+  TRY(io.in(seg_transmittance, ns, &sT));
+  TRY(io.in(seg_depth_sum, ns, &sd));
+  TRY(io.in(ray_off, n_rays + 1, &doff));
+  float *orgb, *oT, *od;
+  TRY(io.out(rgb, 3 * n_rays, &orgb));
+  TRY(io.out(transmittance, n_rays, &oT));
+  TRY(io.out(depth, n_rays, &od));
+  launch_merge_fwd(sr, sT, sd, doff, n_rays, orgb, oT, od, c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
+int dg_merge_backward(dg_ctx* c, const float* seg_rgb, const float* seg_transmittance, const uint64_t* ray_off,
+                      uint64_t n_rays, const float* d_rgb, const float* d_transmittance, float* seg_d_rgb,
+                      float* seg_d_transmittance, int32_t mem) {
+  TRY(check_ctx(c));
+  if (!d_rgb || !d_transmittance || !seg_d_rgb || !seg_d_transmittance) return set_err(DG_EINVAL, "null argument");
+  std::vector<uint64_t> off;
+  TRY(host_offsets(c, ray_off, n_rays, mem, off));
+  for (uint64_t r = 0; r < n_rays; ++r)
+    if (off[r + 1] - off[r] > uint64_t(kMaxSeg)) return set_err(DG_EINVAL, "merge: more than %d partials", kMaxSeg);
+  const uint64_t ns = off[n_rays];
+  StageIo io{c, mem, {}, {}};
+  const float *sr, *sT, *ug, *ut;
+  const uint64_t* doff;
+  TRY(io.in(seg_rgb, 3 * ns, &sr));
+  TRY(io.in(seg_transmittance, ns, &sT));
+  TRY(io.in(ray_off, n_rays + 1, &doff));
+  TRY(io.in(d_rgb, 3 * n_rays, &ug));
+  TRY(io.in(d_transmittance, n_rays, &ut));
+  float *og, *ot;
+  TRY(io.out(seg_d_rgb, 3 * ns, &og));
+  TRY(io.out(seg_d_transmittance, ns, &ot));
+  launch_merge_bwd(sr, sT, doff, n_rays, ug, ut, og, ot, c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
+int dg_ray_losses(dg_ctx* c, const float* rgb, const float* color_gt, const float* transmittance, uint64_t n,
+                  double eps, double* loss_rgb, double* loss_transmittance, float* d_rgb, float* d_transmittance,
+                  int32_t mem) {
+  TRY(check_ctx(c));
+  if (n && (!rgb || !color_gt || !transmittance)) return set_err(DG_EINVAL, "null inputs");
+  StageIo io{c, mem, {}, {}};
+  const float *r, *g, *T;
+  TRY(io.in(rgb, 3 * n, &r));
+  TRY(io.in(color_gt, 3 * n, &g));
+  TRY(io.in(transmittance, n, &T));
+  double *lr, *lt;
+  float *dr, *dt;
+  TRY(io.out(loss_rgb, n, &lr));
+  TRY(io.out(loss_transmittance, n, &lt));
+  TRY(io.out(d_rgb, 3 * n, &dr));
+  TRY(io.out(d_transmittance, n, &dt));
+  launch_ray_losses(r, g, T, n, eps, lr, lt, dr, dt, c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
+int dg_distortion_loss(dg_ctx* c, const double* weights, const double* midpoints, const double* interval_lengths,
+                       const uint64_t* seg_off, uint64_t n_seg, double* loss, double* grads, int32_t mem) {
+  TRY(check_ctx(c));
+  std::vector<uint64_t> off;
+  TRY(host_offsets(c, seg_off, n_seg, mem, off));
+  const uint64_t ns = off[n_seg];
+  if (ns && (!weights || !midpoints || !interval_lengths)) return set_err(DG_EINVAL, "null inputs");
+  StageIo io{c, mem, {}, {}};
+  const double *w, *m, *ds;
+  const uint64_t* doff;
+  TRY(io.in(weights, ns, &w));
+  TRY(io.in(midpoints, ns, &m));
+  TRY(io.in(interval_lengths, ns, &ds));
+  TRY(io.in(seg_off, n_seg + 1, &doff));
+  double *ol, *og;
+  TRY(io.out(loss, n_seg, &ol));
+  TRY(io.out(grads, ns, &og));
+  launch_distortion(w, m, ds, doff, n_seg, ol, og, c->stream);
+  ++c->launches;
+  return io.finish();
 }
 
 int dg_adam_step(dg_ctx* c, double lr) {

@@ -367,6 +367,68 @@ class Context:
     def adam_step(self, lr):
         _check(lib().dg_adam_step(self.h, C.c_double(lr)))
 
+    # ---- compositing stages (render.hpp / train.hpp, batched; host arrays) ----
+    def local_render(self, t, delta, sigma, rgb, seg_off, ray_t0=None, ray_t1=None):
+        """local_render per segment (+ accumulate_distortion_stats when the ray span is given).
+        Returns rgb [n_seg, 3], T, depth_sum (and distortion stats [n_seg, 3])."""
+        off = np.ascontiguousarray(seg_off, dtype=np.uint64)
+        ns = len(off) - 1
+        out_rgb = np.zeros((ns, 3), np.float32)
+        out_T = np.zeros(ns, np.float32)
+        out_d = np.zeros(ns, np.float32)
+        dist = None if ray_t0 is None else np.zeros((ns, 3))
+        _check(lib().dg_local_render(self.h, _p(_c64(t)), _p(_c64(delta)), _p(_c32(sigma)), _p(_c32(rgb)),
+                                     _p(off), C.c_uint64(ns), _p(None if ray_t0 is None else _c64(ray_t0)),
+                                     _p(None if ray_t1 is None else _c64(ray_t1)), _p(out_rgb), _p(out_T),
+                                     _p(out_d), _p(dist), DG_MEM_HOST))
+        return (out_rgb, out_T, out_d) if dist is None else (out_rgb, out_T, out_d, dist)
+
+    def local_render_backward(self, t, delta, sigma, rgb, seg_off, d_rgb, d_T, weight_up=None):
+        off = np.ascontiguousarray(seg_off, dtype=np.uint64)
+        ns, n = len(off) - 1, int(off[-1])
+        sg = np.zeros(n, np.float32)
+        cg = np.zeros((n, 3), np.float32)
+        _check(lib().dg_local_render_backward(self.h, _p(_c64(t)), _p(_c64(delta)), _p(_c32(sigma)),
+                                              _p(_c32(rgb)), _p(off), C.c_uint64(ns), _p(_c32(d_rgb)),
+                                              _p(_c32(d_T)), _p(None if weight_up is None else _c32(weight_up)),
+                                              _p(sg), _p(cg), DG_MEM_HOST))
+        return sg, cg
+
+    def merge_forward(self, seg_rgb, seg_T, seg_depth, ray_off):
+        off = np.ascontiguousarray(ray_off, dtype=np.uint64)
+        nr = len(off) - 1
+        rgb = np.zeros((nr, 3), np.float32)
+        T = np.zeros(nr, np.float32)
+        depth = np.zeros(nr, np.float32)
+        _check(lib().dg_merge_forward(self.h, _p(_c32(seg_rgb)), _p(_c32(seg_T)), _p(_c32(seg_depth)), _p(off),
+                                      C.c_uint64(nr), _p(rgb), _p(T), _p(depth), DG_MEM_HOST))
+        return rgb, T, depth
+
+    def merge_backward(self, seg_rgb, seg_T, ray_off, d_rgb, d_T):
+        off = np.ascontiguousarray(ray_off, dtype=np.uint64)
+        nr, ns = len(off) - 1, int(off[-1])
+        g_rgb = np.zeros((ns, 3), np.float32)
+        g_T = np.zeros(ns, np.float32)
+        _check(lib().dg_merge_backward(self.h, _p(_c32(seg_rgb)), _p(_c32(seg_T)), _p(off), C.c_uint64(nr),
+                                       _p(_c32(d_rgb)), _p(_c32(d_T)), _p(g_rgb), _p(g_T), DG_MEM_HOST))
+        return g_rgb, g_T
+
+    def ray_losses(self, rgb, gt, T, eps=1e-6):
+        n = len(T)
+        lr, lt = np.zeros(n), np.zeros(n)
+        dr, dt = np.zeros((n, 3), np.float32), np.zeros(n, np.float32)
+        _check(lib().dg_ray_losses(self.h, _p(_c32(rgb)), _p(_c32(gt)), _p(_c32(T)), C.c_uint64(n),
+                                   C.c_double(eps), _p(lr), _p(lt), _p(dr), _p(dt), DG_MEM_HOST))
+        return lr, lt, dr, dt
+
+    def distortion_loss(self, w, s, ds, seg_off):
+        off = np.ascontiguousarray(seg_off, dtype=np.uint64)
+        ns, n = len(off) - 1, int(off[-1])
+        loss, grads = np.zeros(ns), np.zeros(n)
+        _check(lib().dg_distortion_loss(self.h, _p(_c64(w)), _p(_c64(s)), _p(_c64(ds)), _p(off), C.c_uint64(ns),
+                                        _p(loss), _p(grads), DG_MEM_HOST))
+        return loss, grads
+
     # ---- introspection ----
     def last_items(self, g):
         v = ItemView()

@@ -44,6 +44,21 @@ int main(int argc, char** argv) {
   for (uint64_t i = 0; i < n; ++i)
     std::fprintf(out, "ray %.9g %.9g %.9g %.9g %.9g\n", merged[i].color.x, merged[i].color.y,
                  merged[i].color.z, merged[i].transmittance, merged[i].depth);
+  distgrid::CameraPose pose;  // looking down -z from above the scene
+  pose.rotation[0] = 1; pose.rotation[4] = -1; pose.rotation[8] = -1;
+  pose.translation = {1.0, 0.5, 3.0};
+  pose.fx = pose.fy = 20.0;
+  pose.cx = 8.0;
+  pose.cy = 6.0;
+  pose.width = 16;
+  pose.height = 12;
+  const auto image = run.evaluate_image(pose, appd);
+  double csum = 0.0, asum = 0.0;
+  for (size_t i = 0; i < image.color.size(); ++i) {
+    csum += image.color[i].x + image.color[i].y + image.color[i].z;
+    asum += image.attribution[i].x + image.attribution[i].y + image.attribution[i].z;
+  }
+  std::fprintf(out, "image %u %u %.9g %.9g\n", image.width, image.height, csum, asum);
   const auto segs = run.segment_rays(rays);
   uint64_t total = 0;
   for (const auto& s : segs) total += s.size();

@@ -52,6 +52,10 @@ def test_cpp_facade_train_and_render(tmp_path):
     # after two Adam steps the states drift apart slightly (fp32 vs fp64); renders stay close
     assert np.allclose(vals[:, :3], rgb, rtol=2e-2, atol=2e-3)
     assert "logic_error ok" in lines
+    img_line = [l for l in lines if l.startswith("image ")]
+    assert img_line and img_line[0].split()[1:3] == ["16", "12"], img_line
+    csum, asum = (float(x) for x in img_line[0].split()[3:5])
+    assert np.isfinite(csum) and csum > 0 and np.isfinite(asum), img_line
     if ref_available():
         ref = RefRun(cfg, app)
         for g in range(2):  # reference-exact init, rounded to fp32

@@ -30,4 +30,7 @@ for i in range(40):
     torch.cuda.synchronize()
     w = (time.perf_counter() - a) * 1e3
     tot = ctx.stage_times()["total"]
-    print(f"step {i:3d} wall {w:7.2f} ms  device(marks) {tot:7.2f} ms  launches {ctx.kernel_launches()}")
+    print(f"step {i:3d} wall {w:7.2f} ms  device(marks) {tot:7.2f} ms  launches {ctx.kernel_launches()}"
+          f"  samples {st.samples}")
+    if i in (14, 20, 39):
+        print("   stages:", {k: round(v, 3) for k, v in ctx.stage_times().items()})
