@@ -106,7 +106,52 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_reference(cfg, o, d, gt, rays, steps, warmup):
+def host_cpu():
+    import os
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    return n, model
+
+
+def cpu_stage_baseline(run, o, d):
+    """the reference's stage functions (segment_ray + cascade_march, encode,
+    query_density + query_color, field_backward incl. encode_backward, AdamState::step) on a
+    std::thread pool over every host core.  The backward gives each thread its own FieldGrads
+    sink (a full table-shaped copy), so its thread count is capped by host memory."""
+    nproc, model = host_cpu()
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16 << 30
+    sink = run.nparams(0) * 8
+    bwd_threads = int(max(1, min(nproc, (0.4 * avail) // max(sink, 1))))
+    rng = np.random.default_rng(11)
+    n_pts = 65536
+    pts = rng.uniform(0.0, 1.0, (n_pts, 3))
+    dirs = rng.normal(size=(n_pts, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    t0 = time.perf_counter()
+    run.stage_bench(o[:1024], d[:1024], pts[:4096], dirs[:4096], nproc, bwd_threads)  # warm-up (page-in)
+    res = run.stage_bench(o, d, pts, dirs, nproc, bwd_threads)
+    res.update({"threads": nproc, "bwd_threads": bwd_threads, "cpu": model,
+                "sample": f"{len(o)} rays (segment+march), {n_pts} uniform points (encode / field), "
+                          f"one Adam step over the fine field; wall {time.perf_counter() - t0:.1f}s"})
+    return res
+
+
+def cpu_reference(cfg, o, d, gt, rays, steps, warmup, stages=False):
     """The unmodified reference DistributedRun (oracle/_ref) on this host: each step is a
     bounded sample of `rays` rays of the same workload (its K=1 worker thread + driver)."""
     from oracle.bindings import RefRun, ref_available
@@ -125,12 +170,18 @@ def cpu_reference(cfg, o, d, gt, rays, steps, warmup):
         run.train_step(o[lo:lo + rays], d[lo:lo + rays], gt[lo:lo + rays].astype(np.float64), img, s)
         if s >= warmup:
             times.append(time.perf_counter() - a)
+    stage = None
+    if stages:
+        try:
+            stage = cpu_stage_baseline(run, o, d)
+        except Exception as e:  # the headline baseline stands without it
+            stage = {"unavailable": str(e)[:200]}
     del run
     sec = float(np.sum(times))
     return {"value": rays * len(times) / sec, "unit": "rays/s", "cores": 1, "kind": "reference",
             "sample": f"{len(times)} x DistributedRun::training_step on {rays} rays of the bench "
                       f"workload (K=1 worker thread; reference init {init_s:.1f}s excluded)",
-            "ms_per_step": 1000 * sec / len(times)}, None
+            "ms_per_step": 1000 * sec / len(times), "stages": stage}, None
 
 
 def run_reference_arm(args):
@@ -169,6 +220,7 @@ def main():
     ap.add_argument("--render-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-stages", action="store_true", help="skip the all-core stage baseline")
     ap.add_argument("--ref-rays", type=int, default=512, help="rays per step of the --impl reference arm")
     ap.add_argument("--cpu-rays", type=int, default=2048, help="rays of the cpu_baseline sample (~10 s)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
@@ -343,11 +395,22 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         o, d, gt, _ = batches_host[0]
-        cpu, why = cpu_reference(cfg, o, d, gt, args.cpu_rays, 1, 0)
+        cpu, why = cpu_reference(cfg, o, d, gt, args.cpu_rays, 1, 0, stages=not args.no_cpu_stages)
         if cpu is None:
             cpu = {"value": None, "unit": "rays/s", "cores": 0, "kind": "reference", "sample": why}
         else:
             cpu.pop("ms_per_step", None)
+            cpu_stages = cpu.pop("stages", None)
+            if cpu_stages and "unavailable" not in cpu_stages:
+                # the same stages on the GPU, from this run's per-stage device times
+                ms = lambda *k: sum(st[x] for x in k) / 1000.0
+                cpu_stages["gpu_same_stages"] = {
+                    "segment_march_rays_per_s": B / ms("segment", "march"),
+                    "encode_samples_per_s": samples_rank / ms("encode_fwd"),
+                    "field_fwd_samples_per_s": samples_rank / ms("encode_fwd", "mlp_fwd"),
+                    "field_bwd_samples_per_s": samples_rank / ms("mlp_bwd", "encode_bwd"),
+                    "adam_params_per_s": sum(ctx.param_count(g) for g in ctx.local) / ms("adam")}
+            cpu["stages"] = cpu_stages
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,

@@ -113,6 +113,7 @@ def ref_lib():
         lib.refh_last_error.restype = C.c_char_p
         lib.refh_save_checkpoint.argtypes = [P, C.c_uint32, C.c_uint64, C.c_char_p]
         lib.refh_load_checkpoint.argtypes = [P, C.c_uint32, C.c_char_p, P]
+        lib.refh_stage_bench.argtypes = [P, P, P, C.c_uint64, P, P, C.c_uint64, C.c_int, C.c_int, P]
         lib.refh_time_replicas.restype = C.c_double
         lib.refh_time_replicas.argtypes = [P, C.c_uint32, P, P, P, C.c_uint64, C.c_uint64,
                                            C.c_uint64]
@@ -243,6 +244,17 @@ class RefRun(_RunBase):
 
     def nparams(self, g):
         return int(self.lib.refh_param_count(self.h, g))
+
+    def stage_bench(self, o, d, pts, dirs, threads, bwd_threads):
+        """Region 0's stage functions on a host thread pool (ref_harness.cpp refh_stage_bench)."""
+        o, d = np.ascontiguousarray(o, np.float64), np.ascontiguousarray(d, np.float64)
+        pts, dirs = np.ascontiguousarray(pts, np.float64), np.ascontiguousarray(dirs, np.float64)
+        out = np.zeros(5)
+        self._check(self.lib.refh_stage_bench(self.h, _ptr(o), _ptr(d), len(o), _ptr(pts), _ptr(dirs), len(pts),
+                                              int(threads), int(bwd_threads), _ptr(out)))
+        return {"segment_march_rays_per_s": out[0], "encode_samples_per_s": out[1],
+                "field_fwd_samples_per_s": out[2], "field_bwd_samples_per_s": out[3],
+                "adam_params_per_s": out[4]}
 
     def save_checkpoint(self, g, config_hash, path):
         self._check(self.lib.refh_save_checkpoint(self.h, g, config_hash, path.encode()))

@@ -600,6 +600,114 @@ double refh_time_replicas(void* const* runs, uint32_t n_runs, const double* orig
   return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// ---- CPU baseline (ii): the reference's stage functions on a host thread pool ----
+// Throughputs of region 0's own functions: out[0] segment_ray + cascade_march (rays/s),
+// out[1] HashGrid::encode (samples/s), out[2] query_density + query_color (samples/s),
+// out[3] forward-with-cache + field_backward incl. encode_backward into per-thread FieldGrads
+// sinks (samples/s, bwd_threads threads: each sink is a full copy of the tables' shape),
+// out[4] AdamState::step over the fine field's arrays, chunked across threads (params/s).
+// Reads of grids and fields are thread-safe (const); nothing is written but the sinks.
+int refh_stage_bench(void* p, const double* origin, const double* dir, uint64_t n_rays,
+                     const double* points, const double* dirs, uint64_t n_pts, int threads,
+                     int bwd_threads, double* out) {
+  auto* h = static_cast<Harness*>(p);
+  try {
+    Worker& w = h->run->worker(0);
+    const FieldParams& f = w.fine_field();
+    const uint32_t dapp = h->config.appearance_dim;
+    const std::vector<double> app(dapp, 0.1);
+    auto pool = [](int nt, uint64_t n, auto&& body) {
+      std::vector<std::thread> ts;
+      std::vector<std::exception_ptr> errs(nt);
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int k = 0; k < nt; ++k)
+        ts.emplace_back([&, k] {
+          try {
+            body(k, n * k / nt, n * (k + 1) / nt);
+          } catch (...) {
+            errs[k] = std::current_exception();
+          }
+        });
+      for (auto& t : ts) t.join();
+      for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+      return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    MarchConfig march;
+    march.step = march_step_for(h->config, h->manifest.outer);
+    march.jitter = true;
+    march.jitter_seed = h->config.seed;
+    march.jitter_step = 1;
+    double sec = pool(threads, n_rays, [&](int, uint64_t lo, uint64_t hi) {
+      uint64_t sink = 0;
+      for (uint64_t i = lo; i < hi; ++i) {
+        Ray ray{{origin[3 * i], origin[3 * i + 1], origin[3 * i + 2]},
+                {dir[3 * i], dir[3 * i + 1], dir[3 * i + 2]}, i, 0};
+        for (const RaySegment& sg : segment_ray(ray, h->manifest))
+          if (sg.region_id == 0)
+            sink += cascade_march(ray, w.region(), w.occ_fine(), w.occ_coarse(), sg.t_enter, sg.t_exit, march, i).size();
+      }
+      if (sink == 0xffffffffffffffffull) throw std::runtime_error("unreachable");
+    });
+    out[0] = double(n_rays) / sec;
+    const uint32_t width = f.grid.feature_width();
+    sec = pool(threads, n_pts, [&](int, uint64_t lo, uint64_t hi) {
+      std::vector<double> x(width);
+      for (uint64_t i = lo; i < hi; ++i)
+        f.grid.encode(Vec3{points[3 * i], points[3 * i + 1], points[3 * i + 2]}, x);
+    });
+    out[1] = double(n_pts) / sec;
+    sec = pool(threads, n_pts, [&](int, uint64_t lo, uint64_t hi) {
+      for (uint64_t i = lo; i < hi; ++i) {
+        const DensityResult r = query_density(Vec3{points[3 * i], points[3 * i + 1], points[3 * i + 2]}, f);
+        query_color(r.feature, Vec3{dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]}, app, f);
+      }
+    });
+    out[2] = double(n_pts) / sec;
+    std::vector<FieldGrads> sinks;
+    for (int k = 0; k < bwd_threads; ++k) sinks.push_back(make_field_grads(f));
+    sec = pool(bwd_threads, n_pts, [&](int k, uint64_t lo, uint64_t hi) {
+      for (uint64_t i = lo; i < hi; ++i) {
+        FieldSampleCache cache;
+        const DensityResult r =
+            query_density(Vec3{points[3 * i], points[3 * i + 1], points[3 * i + 2]}, f, &cache);
+        query_color(r.feature, Vec3{dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2]}, app, f, &cache);
+        field_backward(f, cache, r.sigma, 0.01, Vec3{0.01, -0.02, 0.03}, sinks[k]);
+      }
+    });
+    out[3] = double(n_pts) / sec;
+    sinks.clear();
+    // Adam over every fine array, each array cut into `threads` chunks with its own state
+    std::vector<std::span<double>> arrays;
+    for (auto& a : w.fine_field().parameter_arrays()) arrays.push_back(a);
+    uint64_t n_par = 0;
+    for (auto& a : arrays) n_par += a.size();
+    std::vector<std::vector<double>> params(arrays.size()), grads(arrays.size());
+    for (size_t a = 0; a < arrays.size(); ++a) {
+      params[a].assign(arrays[a].begin(), arrays[a].end());
+      grads[a].assign(arrays[a].size(), 1e-3);
+    }
+    std::vector<AdamState> states(threads);
+    std::vector<std::vector<std::span<double>>> tp(threads);
+    std::vector<std::vector<std::span<const double>>> tg(threads);
+    for (int k = 0; k < threads; ++k) {
+      std::vector<size_t> sizes;
+      for (size_t a = 0; a < arrays.size(); ++a) {
+        const size_t n = params[a].size(), lo = n * k / threads, hi = n * (k + 1) / threads;
+        tp[k].emplace_back(params[a].data() + lo, hi - lo);
+        tg[k].emplace_back(grads[a].data() + lo, hi - lo);
+        sizes.push_back(hi - lo);
+      }
+      states[k] = AdamState(sizes);
+    }
+    sec = pool(threads, uint64_t(threads), [&](int k, uint64_t, uint64_t) { states[k].step(tp[k], tg[k], 0.01); });
+    out[4] = double(n_par) / sec;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // ---- .dgcw checkpoints (checkpoint.cpp:241-283) through the Worker's own state calls ----
 int refh_save_checkpoint(void* p, uint32_t region, uint64_t config_hash, const char* path) {
   try {
