@@ -184,14 +184,61 @@ def cpu_reference(cfg, o, d, gt, rays, steps, warmup, stages=False):
             "ms_per_step": 1000 * sec / len(times), "stages": stage}, None
 
 
+REF_REPLICA_BYTES = 11.5e9  # one reference DistributedRun at T = 2^24 (tools/diag/ref_rss.py: 10.7 GB)
+
+
+def cpu_reference_replicas(cfg, rays, steps, warmup, generator):
+    """All host threads the reference can use: it parallelises only across partitions (one
+    worker thread each), so at the 1-GPU point (K = 1) the host runs independent replicas of
+    the reference DistributedRun, one per thread, each training on its own ray slice in lock
+    step (ref_harness.cpp refh_time_replicas).  The replica count is capped by host memory."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.bindings import RefRun, ref_available, ref_lib
+    from paper_2405_04416_b200 import workloads
+    if not ref_available():
+        return None, "oracle/_ref not built"
+    nproc, model = host_cpu()
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 32e9
+    per = REF_REPLICA_BYTES * (1 << max(0, cfg.fine_table_log2 - 24)) if cfg.fine_table_log2 >= 24 else 2e9
+    n_rep = int(max(1, min(nproc, (0.45 * avail) // per)))
+    o, d, gt, _ = workloads.make_rays(cfg, n_rep * rays, generator, seed=1)
+    app = workloads.appearance_rows(cfg.appearance_dim, 1)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(n_rep) as ex:  # refh_create runs without the GIL
+        runs = list(ex.map(lambda _: RefRun(cfg, app), range(n_rep)))
+    init_s = time.perf_counter() - t0
+    lib = ref_lib()
+    handles = (C.c_void_p * n_rep)(*[r.h for r in runs])
+    o, d, gt = (np.ascontiguousarray(x, np.float64) for x in (o, d, gt))
+    args = (handles, n_rep, o.ctypes.data_as(C.c_void_p), d.ctypes.data_as(C.c_void_p),
+            gt.ctypes.data_as(C.c_void_p), rays)
+    if warmup and lib.refh_time_replicas(*args, warmup, 0) < 0:
+        return None, lib.refh_last_error().decode()
+    sec = lib.refh_time_replicas(*args, steps, warmup)
+    if sec < 0:
+        return None, lib.refh_last_error().decode()
+    del runs
+    value = n_rep * rays * steps / sec
+    return {"value": value, "unit": "rays/s", "cores": n_rep, "kind": "reference",
+            "sample": f"{n_rep} replicas of the reference DistributedRun (K=1 worker thread each; "
+                      f"the reference parallelises only across partitions), {rays} rays/step each, "
+                      f"{steps} lock-step steps; {nproc}-thread host ({model}); init {init_s:.1f}s excluded",
+            "ms_per_step": 1000 * sec / steps}, None
+
+
 def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
     from paper_2405_04416_b200 import workloads
     wl = workloads.weak(1, rays_per_gpu=args.rays_per_gpu, table_log2=args.table_log2)
-    o, d, gt, _ = workloads.make_rays(wl.cfg, 4096, wl.generator, seed=1)
-    res, why = cpu_reference(wl.cfg, o, d, gt, args.ref_rays, args.steps, min(args.warmup, 1))
+    res, why = cpu_reference_replicas(wl.cfg, args.ref_rays, args.steps, min(args.warmup, 1), wl.generator)
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": why}))
         return 0
@@ -199,7 +246,7 @@ def run_reference_arm(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.name + " (CPU sample)", "rays_per_step": args.ref_rays,
+            "config": {"workload": wl.name + " (CPU sample)", "rays_per_step_per_replica": args.ref_rays,
                        "table_log2": args.table_log2, "partitions": 1},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": "rays/s", "h2d_bytes_per_step": 0,
@@ -221,7 +268,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cpu-stages", action="store_true", help="skip the all-core stage baseline")
-    ap.add_argument("--ref-rays", type=int, default=512, help="rays per step of the --impl reference arm")
+    ap.add_argument("--ref-rays", type=int, default=1024, help="rays per step per replica of the --impl reference arm")
     ap.add_argument("--cpu-rays", type=int, default=2048, help="rays of the cpu_baseline sample (~10 s)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     args = ap.parse_args()
