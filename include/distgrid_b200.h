@@ -376,6 +376,9 @@ int dg_selftest_tcgen05(const float* A, const float* B, const float* X, float* Y
                         float* Y2);
 /* the context's CUDA stream (cudaStream_t) so callers can record events on it */
 int dg_get_stream(dg_ctx* ctx, void** stream);
+/* run every later call of this context on the caller's cudaStream_t (NULL: back to the
+ * context's own stream); waits for the work already queued on the current stream */
+int dg_set_stream(dg_ctx* ctx, void* stream);
 
 #ifdef __cplusplus
 }

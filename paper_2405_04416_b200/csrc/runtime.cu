@@ -167,7 +167,8 @@ struct dg_ctx {
   uint64_t adam_t = 0;
   uint64_t worker_step = 0;
   uint32_t n_images = 0, app_rows = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // the stream every call runs on (dg_set_stream)
+  cudaStream_t own_stream = nullptr;  // the context's own stream
   int num_sms = 148;
   int mlp_impl = 1;  // 1: tcgen05 split-bf16 forward (default), 0: FFMA fp32 (DG_MLP=ffma)
   std::unique_ptr<Comm> comm;
@@ -1141,6 +1142,7 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   if (const char* e = std::getenv("DG_ENC_BWD_MB"))
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->own_stream = c->stream;
   CU(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
   c->pin_cap = 1 << 20;
   CU(cudaHostAlloc(reinterpret_cast<void**>(&c->pin), c->pin_cap, cudaHostAllocDefault));
@@ -1164,7 +1166,7 @@ int dg_ctx_destroy(dg_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->ev_occ_up) cudaEventDestroy(c->ev_occ_up);
   if (c->ev_occ_used) cudaEventDestroy(c->ev_occ_used);
-  cudaStream_t s = c->stream, sc = c->stream_copy;
+  cudaStream_t s = c->own_stream, sc = c->stream_copy;
   delete c;
   if (s) cudaStreamDestroy(s);
   if (sc) cudaStreamDestroy(sc);
@@ -2369,6 +2371,14 @@ int dg_selftest_tcgen05(const float* A, const float* B, const float* X, float* Y
 int dg_get_stream(dg_ctx* c, void** stream) {
   TRY(check_ctx(c));
   *stream = (void*)c->stream;
+  return DG_OK;
+}
+
+int dg_set_stream(dg_ctx* c, void* stream) {
+  TRY(check_ctx(c));
+  CU(cudaSetDevice(c->device));
+  CU(cudaStreamSynchronize(c->stream));  // work queued on the previous stream is done
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
   return DG_OK;
 }
 

@@ -462,6 +462,16 @@ class Context:
         _check(lib().dg_last_partials(self.h, C.c_uint32(g), _p(rgb), _p(T)))
         return rgb, T
 
+    def stream(self):
+        v = C.c_void_p()
+        _check(lib().dg_get_stream(self.h, C.byref(v)))
+        return v.value
+
+    def set_stream(self, stream_ptr):
+        """Run later calls on the caller's cudaStream_t (an int handle, e.g.
+        torch.cuda.Stream().cuda_stream); None returns to the context's own stream."""
+        _check(lib().dg_set_stream(self.h, C.c_void_p(stream_ptr)))
+
     def kernel_launches(self):
         v = C.c_uint64()
         _check(lib().dg_kernel_launches(self.h, C.byref(v)))
