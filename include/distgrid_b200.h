@@ -237,6 +237,13 @@ int dg_comm_init_nccl(dg_ctx* ctx, const uint8_t id[DG_NCCL_UNIQUE_ID_BYTES]);
 typedef int (*dg_alltoallv_fn)(void* user, const void* send, const uint64_t* send_bytes,
                                 void* recv, const uint64_t* recv_bytes);
 int dg_comm_init_host(dg_ctx* ctx, dg_alltoallv_fn fn, void* user);
+/* Peer-memory backend (one node): every rank's receive buffers are CUDA-IPC mapped into the
+ * others, and the dispatch / partial pack kernels store each record directly into its owner's
+ * buffer in the owner's final layout.  fn is a host all-gather (recv = world x bytes, rank
+ * order) that carries the per-step count matrices, the IPC handles and the barriers; the
+ * caller implements it over its launcher's channel (MPI, torch.distributed, sockets). */
+typedef int (*dg_allgather_fn)(void* user, const void* send, uint64_t bytes, void* recv);
+int dg_comm_init_peer(dg_ctx* ctx, dg_allgather_fn fn, void* user);
 
 /* ---- ray cache / pixel-ray batch feed ----
  * RayCache (train.cpp:117-159) over a dataset uploaded once: images (u8 RGB, row-major) and

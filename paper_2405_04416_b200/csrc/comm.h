@@ -15,15 +15,58 @@
 
 namespace dg {
 
+class PeerComm;
+
 class Comm {
  public:
   virtual ~Comm() = default;
+  // the peer-memory backend, whose receive buffers the pack kernels write directly
+  virtual PeerComm* peer() { return nullptr; }
   // send/recv: device buffers; bytes per peer (rank order).  Returns DG_OK or an error code;
   // err receives a message.
   virtual int alltoallv(const void* send, const std::vector<uint64_t>& send_bytes, void* recv,
                         const std::vector<uint64_t>& recv_bytes, cudaStream_t s,
                         std::string& err) = 0;
   virtual const char* name() const = 0;
+};
+
+// Exchanges over peer memory (one node, NVLink / NVSwitch): every rank's receive buffers are
+// CUDA-IPC mapped into every other rank, so the two pack kernels store each record straight
+// into its owner's buffer, in the owner's final layout — no staging buffer, no collective copy
+// kernel, no receive-side permute.  The host all-gather callback carries the per-step count
+// matrices, the IPC handles and the barriers (stream sync + all-gather: after it every rank's
+// pack kernel has completed, so every record is in place; no kernel ever waits on a peer).
+class PeerComm final : public Comm {
+ public:
+  enum { kItems = 0, kPartials = 1, kCross = 2, kStage = 3, kBufs = 4 };
+  PeerComm(dg_allgather_fn fn, void* user, int rank, int world);
+  ~PeerComm() override;
+  // generic all-to-all-v (staged through kStage) for the exchanges without a fused pack
+  int alltoallv(const void* send, const std::vector<uint64_t>& send_bytes, void* recv,
+                const std::vector<uint64_t>& recv_bytes, cudaStream_t s, std::string& err) override;
+  const char* name() const override { return "peer"; }
+  PeerComm* peer() override { return this; }
+  int allgather(const void* send, uint64_t bytes, void* recv, std::string& err);
+  int barrier(cudaStream_t s, std::string& err);
+  // collective: every rank's buffer k holds >= need bytes afterwards (need identical on all ranks)
+  int reserve(int k, uint64_t need, std::string& err);
+  void* local(int k) const { return buf_[k].local; }
+  void* const* peers_dev(int k) const { return buf_[k].dev; }
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+
+ private:
+  struct Buf {
+    void* local = nullptr;
+    uint64_t cap = 0;
+    std::vector<void*> peer;  // mapped bases (own rank: local)
+    void** dev = nullptr;     // the same pointers on the device
+  };
+  void unmap(Buf& b);
+  dg_allgather_fn fn_;
+  void* user_;
+  int rank_, world_;
+  Buf buf_[kBufs];
 };
 
 Comm* make_nccl_comm(const uint8_t id[DG_NCCL_UNIQUE_ID_BYTES], int rank, int world, int device,

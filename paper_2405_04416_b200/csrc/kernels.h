@@ -57,6 +57,15 @@ struct LossAccum {
   uint32_t pad;
 };
 
+// Peer-memory destinations of a pack kernel (PeerComm): base[r] is rank r's receive buffer
+// mapped into this process (CUDA IPC; the own rank's is local), off[p] a per-partition record
+// offset.  base == nullptr: pack into the local send buffer instead.
+struct PeerDst {
+  void* const* base;
+  const uint64_t* off;
+  uint32_t world;
+};
+
 // ---- ray-side kernels (kernels_ray.cu) ----
 void launch_segment_home(const Geo* geo, const double* o, const double* d, uint64_t n,
                          const uint8_t* slot_of_part, uint8_t* nseg, uint8_t* sched,
@@ -64,7 +73,7 @@ void launch_segment_home(const Geo* geo, const double* o, const double* d, uint6
 void launch_pack_dispatch(uint64_t n, uint32_t P, const uint8_t* nseg, const uint8_t* sched,
                           const uint8_t* slot_of_part, const uint32_t* pos, const double* o,
                           const double* d, const float* gt, const uint32_t* img,
-                          uint64_t first_ray_id, RayRec* out, cudaStream_t s);
+                          uint64_t first_ray_id, RayRec* out, PeerDst peer, cudaStream_t s);
 void launch_item_setup(const Geo* geo, const PartDesc* parts, const uint8_t* occ,
                        const uint32_t* part_item_off, uint32_t n_local, uint32_t n_items,
                        ItemArrays it, uint32_t P, double step, uint64_t seed, uint64_t batch_id,
@@ -77,7 +86,8 @@ void launch_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, uint32_t
                       int with_depth, cudaStream_t s);
 void launch_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                           const uint8_t* local_of_global, const uint64_t* stream_off,
-                          uint32_t P, PartialRec* send, float4* send_x, cudaStream_t s);
+                          uint32_t P, PartialRec* send, float4* send_x, PeerDst peer, PeerDst peer_x,
+                          cudaStream_t s);
 void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                            const PartDesc* parts, const uint64_t* stream_off, uint32_t P,
                            const PartialRec* recv, const float4* recv_x, SampleArrays sm,

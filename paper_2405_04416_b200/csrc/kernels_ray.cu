@@ -57,7 +57,7 @@ __global__ void k_pack_dispatch(uint64_t n, const uint8_t* __restrict__ nseg,
                                 const uint32_t* __restrict__ pos, const double* __restrict__ o,
                                 const double* __restrict__ d, const float* __restrict__ gt,
                                 const uint32_t* __restrict__ img, uint64_t first_ray_id,
-                                RayRec* __restrict__ out) {
+                                RayRec* __restrict__ out, PeerDst peer) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int ns = nseg[i];
@@ -73,8 +73,15 @@ __global__ void k_pack_dispatch(uint64_t n, const uint8_t* __restrict__ nseg,
   r.pad = 0;
   for (int s = 0; s < ns; ++s) {
     const uint32_t p = sched[i * kMaxSeg + s];
-    out[pos[(uint64_t)slot_of_part[p] * n + i]] = r;
+    const uint64_t slot = slot_of_part[p];
+    if (peer.base) {  // straight into the owner's item array (peer store over NVLink)
+      RayRec* dst = static_cast<RayRec*>(peer.base[p % peer.world]);
+      dst[peer.off[p] + pos[slot * n + i] - pos[slot * n]] = r;
+    } else {
+      out[pos[slot * n + i]] = r;
+    }
   }
+  if (peer.base) __threadfence_system();
 }
 
 __device__ __forceinline__ uint32_t part_of_item(const uint32_t* off, uint32_t n_local, uint32_t i) {
@@ -352,7 +359,8 @@ __device__ __forceinline__ uint32_t ordinal(const ItemArrays& it, uint32_t n_ite
 __global__ void k_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* __restrict__ part_item_off,
                                 const uint8_t* __restrict__ global_of_local,
                                 const uint64_t* __restrict__ stream_off, uint32_t P,
-                                PartialRec* __restrict__ send, float4* __restrict__ send_x) {
+                                PartialRec* __restrict__ send, float4* __restrict__ send_x,
+                                PeerDst peer, PeerDst peer_x) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_items) return;
   const uint32_t lp = it.part[i];
@@ -368,14 +376,23 @@ __global__ void k_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t*
   rec.depth = it.depth[i];
   rec.ray_id = it.rec[i].ray_id;
   const uint8_t* sc = it.sched + (uint64_t)i * kMaxSeg;
-  const float4 x = send_x ? it.xdist[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool cross = send_x || peer_x.base;
+  const float4 x = cross ? it.xdist[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = 0; s < ns; ++s) {
     const uint32_t q = sc[s];
     if (q == gid) continue;
+    // stream (gid -> q) starts at stream_off: in the local send buffer, or (peer mode) in the
+    // receive buffer of q's owner, written there directly
     const uint64_t at = stream_off[gid * P + q] + ordinal(it, n_items, part_item_off, lp, q, i);
-    send[at] = rec;
-    if (send_x) send_x[at] = x;
+    if (peer.base) {
+      static_cast<PartialRec*>(peer.base[q % peer.world])[at] = rec;
+      if (peer_x.base) static_cast<float4*>(peer_x.base[q % peer.world])[at] = x;
+    } else {
+      send[at] = rec;
+      if (send_x) send_x[at] = x;
+    }
   }
+  if (peer.base) __threadfence_system();
 }
 
 __device__ __forceinline__ float warp_sum_f(float v) {
@@ -809,10 +826,10 @@ void launch_segment_home(const Geo* geo, const double* o, const double* d, uint6
 void launch_pack_dispatch(uint64_t n, uint32_t, const uint8_t* nseg, const uint8_t* sched,
                           const uint8_t* slot_of_part, const uint32_t* pos, const double* o,
                           const double* d, const float* gt, const uint32_t* img,
-                          uint64_t first_ray_id, RayRec* out, cudaStream_t s) {
+                          uint64_t first_ray_id, RayRec* out, PeerDst peer, cudaStream_t s) {
   if (!n) return;
   k_pack_dispatch<<<blocks(n, 256), 256, 0, s>>>(n, nseg, sched, slot_of_part, pos, o, d, gt, img,
-                                                 first_ray_id, out);
+                                                 first_ray_id, out, peer);
 }
 
 void launch_item_setup(const Geo* geo, const PartDesc* parts, const uint8_t* occ,
@@ -846,10 +863,11 @@ void launch_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, uint32_t
 
 void launch_pack_partials(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,
                           const uint8_t* global_of_local, const uint64_t* stream_off, uint32_t P,
-                          PartialRec* send, float4* send_x, cudaStream_t s) {
+                          PartialRec* send, float4* send_x, PeerDst peer, PeerDst peer_x,
+                          cudaStream_t s) {
   if (!n_items) return;
   k_pack_partials<<<blocks(n_items, 256), 256, 0, s>>>(n_items, it, part_item_off, global_of_local,
-                                                       stream_off, P, send, send_x);
+                                                       stream_off, P, send, send_x, peer, peer_x);
 }
 
 void launch_merge_backward(uint32_t n_items, ItemArrays it, const uint32_t* part_item_off,

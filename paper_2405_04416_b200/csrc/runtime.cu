@@ -180,6 +180,8 @@ struct dg_ctx {
   // persistent device state
   DBuf out_attr, cam_o, cam_d, cam_pose, it_xdist, send_x, recv_x, it_runs, it_runc, it_nrun;
   bool cross_active = false;  // training step with distortion_cross_correction
+  RayRec* items_rec = nullptr;  // this step's item records: rec, or the peer backend's item buffer
+  DBuf peer_off;                // per-partition record offsets of the peer-memory dispatch
   DBuf d_geo, d_parts, d_fields, params, grads, adam_m, adam_v, occ, occ_den, app, slot_of_part_d,
       local_of_global_d, global_of_local_d;
   // per-step scratch
@@ -482,7 +484,7 @@ void mark(dg_ctx* c, int i) {
 
 ItemArrays item_arrays(dg_ctx* c) {
   ItemArrays it;
-  it.rec = c->rec.as<RayRec>();
+  it.rec = c->items_rec;
   it.te = c->it_te.as<double>();
   it.tx = c->it_tx.as<double>();
   it.t0 = c->it_t0.as<double>();
@@ -623,14 +625,63 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
     TRY(c->rec.ensure(n_items * sizeof(RayRec) + 16));
     launch_pack_dispatch(n, P, c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(),
                          c->slot_of_part_d.as<uint8_t>(), c->h_pos.as<uint32_t>(), o, d, gt, img,
-                         b->first_ray_id, c->rec.as<RayRec>(), s);
+                         b->first_ray_id, c->rec.as<RayRec>(), PeerDst{nullptr, nullptr, 1}, s);
     ++c->launches;
+    c->items_rec = c->rec.as<RayRec>();
+  } else if (PeerComm* pc = c->comm->peer()) {
+    // Exchange 1 over peer memory: the full count matrix (every rank's per-partition counts)
+    // gives every owner's item layout [local partition][src rank][ray]; the pack kernel then
+    // stores each record at its final place in the owner's item array, so neither the
+    // all-to-all copy nor the receive-side block permute exists.
+    const int W = c->world;
+    std::string err;
+    std::vector<uint64_t> all(uint64_t(W) * P);  // all[src * P + p]
+    int rc = pc->allgather(send_cnt.data(), uint64_t(P) * 8, all.data(), err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    std::vector<uint64_t> part_base(P, 0), items_of(W, 0);
+    for (int r = 0; r < W; ++r) {
+      uint64_t off = 0;
+      for (uint32_t p : local_partitions(r, W, P))
+        for (int src = 0; src < W; ++src) {
+          if (src == c->rank) part_base[p] = off;
+          off += all[uint64_t(src) * P + p];
+        }
+      items_of[r] = off;
+    }
+    for (uint32_t lp = 0; lp < nl; ++lp) {
+      uint64_t t = 0;
+      for (int src = 0; src < W; ++src) t += all[uint64_t(src) * P + c->local[lp]];
+      pio[lp + 1] = pio[lp] + uint32_t(t);
+    }
+    n_items = items_of[c->rank];
+    rc = pc->reserve(PeerComm::kItems, *std::max_element(items_of.begin(), items_of.end()) * sizeof(RayRec) + 16,
+                     err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    TRY(upload_small(c, c->peer_off, part_base.data(), part_base.size() * 8));
+    {  // the block table of the staged path: the render's reply exchange walks it back
+      DispatchPlan plan;
+      plan_dispatch(c->rank, W, P, send_cnt.data(), all.data(), sizeof(RayRec), plan);
+      std::vector<uint64_t> tab(plan.block_src);
+      tab.insert(tab.end(), plan.block_dst.begin(), plan.block_dst.end());
+      TRY(upload_small(c, c->perm_tab, tab.data(), tab.size() * 8));
+    }
+    launch_pack_dispatch(n, P, c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(),
+                         c->slot_of_part_d.as<uint8_t>(), c->h_pos.as<uint32_t>(), o, d, gt, img,
+                         b->first_ray_id, nullptr,
+                         PeerDst{pc->peers_dev(PeerComm::kItems), c->peer_off.as<uint64_t>(), uint32_t(W)}, s);
+    ++c->launches;
+    for (uint32_t p = 0; p < P; ++p)
+      if (int(p % uint32_t(W)) != c->rank) *bytes_sent += send_cnt[p] * sizeof(RayRec);
+    rc = pc->barrier(s, err);  // every rank's records are in place
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    c->h2d += P * 8;
+    c->items_rec = static_cast<RayRec*>(pc->local(PeerComm::kItems));
   } else {
     const int W = c->world;
     TRY(c->x_send.ensure(total_send * sizeof(RayRec) + 16));
     launch_pack_dispatch(n, P, c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(),
                          c->slot_of_part_d.as<uint8_t>(), c->h_pos.as<uint32_t>(), o, d, gt, img,
-                         b->first_ray_id, c->x_send.as<RayRec>(), s);
+                         b->first_ray_id, c->x_send.as<RayRec>(), PeerDst{nullptr, nullptr, 1}, s);
     ++c->launches;
     // counts exchange: every rank sends its full per-partition count vector to every peer
     std::vector<uint64_t> cnt_send(uint64_t(W) * P), cnt_recv(uint64_t(W) * P);
@@ -671,6 +722,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
           c->perm_tab.as<uint64_t>(), nblk, n_items);
       ++c->launches;
     }
+    c->items_rec = c->rec.as<RayRec>();
   }
   mark(c, 1);
   // ---- K2: item setup + counts ----
@@ -768,7 +820,7 @@ FieldLaunch field_launch(dg_ctx* c, uint64_t budget) {
   FieldLaunch f{};
   f.fields = c->d_fields.as<FieldDesc>();
   f.parts = c->d_parts.as<PartDesc>();
-  f.rec = c->rec.as<RayRec>();
+  f.rec = c->items_rec;
   f.item_part = c->it_part.as<uint8_t>();
   f.s_t = c->s_t.as<double>();
   f.s_item = c->s_item.as<uint32_t>();
@@ -829,7 +881,7 @@ MlpLaunch mlp_launch(dg_ctx* c, bool bwd) {
   m.X = c->s_X.as<float>();
   m.x_stride = uint64_t(c->n_fine) + c->n_coarse;
   m.levels = c->cfg.grid_levels;
-  m.rec = c->rec.as<RayRec>();
+  m.rec = c->items_rec;
   m.s_item = c->s_item.as<uint32_t>();
   m.app_table = c->app.as<float>();
   m.params = c->params.as<float>();
@@ -847,6 +899,49 @@ int exchange_partials(dg_ctx* c, const std::vector<uint32_t>& pair_cnt, uint64_t
   cudaStream_t s = c->stream;
   const uint32_t P = c->P, nl = uint32_t(c->local.size());
   const int W = c->world;
+  const bool cross = c->cross_active;
+  if (PeerComm* pc = W > 1 ? c->comm->peer() : nullptr) {
+    // Exchange 2 over peer memory: with every rank's pair counts, every receiver's stream
+    // layout is known, so the pack kernel stores each partial (and its cross-distortion
+    // aggregates) straight into the receiving owner's buffer.
+    const uint32_t nl_max = (P + uint32_t(W) - 1) / uint32_t(W);
+    std::vector<uint32_t> mine(uint64_t(nl_max) * P, 0), all(uint64_t(W) * nl_max * P);
+    std::copy(pair_cnt.begin(), pair_cnt.end(), mine.begin());
+    std::string err;
+    int rc = pc->allgather(mine.data(), mine.size() * 4, all.data(), err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    std::vector<PartialPlan> plans(W);
+    uint64_t need = 0;
+    for (int r = 0; r < W; ++r) {
+      plan_partials(r, W, P, all.data() + uint64_t(r) * nl_max * P, sizeof(PartialRec), plans[r]);
+      need = std::max(need, plans[r].recv_total);
+    }
+    rc = pc->reserve(PeerComm::kPartials, need * sizeof(PartialRec) + 16, err);
+    if (rc == DG_OK && cross) rc = pc->reserve(PeerComm::kCross, need * sizeof(float4) + 16, err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    std::vector<uint64_t> dst(uint64_t(P) * P, 0);  // stream (q -> p): offset in p's owner's buffer
+    for (uint32_t q : c->local)
+      for (uint32_t p = 0; p < P; ++p)
+        if (p != q) dst[uint64_t(q) * P + p] = plans[p % uint32_t(W)].recv_off[uint64_t(q) * P + p];
+    TRY(upload_small(c, c->stream_send_d, dst.data(), dst.size() * 8));
+    TRY(upload_small(c, c->stream_recv_d, plans[c->rank].recv_off.data(), plans[c->rank].recv_off.size() * 8));
+    c->h2d += (dst.size() + plans[c->rank].recv_off.size()) * 8;
+    const PeerDst pd{pc->peers_dev(PeerComm::kPartials), nullptr, uint32_t(W)};
+    const PeerDst px{cross ? pc->peers_dev(PeerComm::kCross) : nullptr, nullptr, uint32_t(W)};
+    launch_pack_partials(c->n_items, item_arrays(c), c->part_item_off_d.as<uint32_t>(),
+                         c->global_of_local_d.as<uint8_t>(), c->stream_send_d.as<uint64_t>(), P, nullptr,
+                         nullptr, pd, px, s);
+    ++c->launches;
+    for (uint32_t lq = 0; lq < nl; ++lq)  // records to other ranks (both streams)
+      for (uint32_t p = 0; p < P; ++p)
+        if (int(p % uint32_t(W)) != c->rank && p != c->local[lq])
+          *bytes_sent += uint64_t(pair_cnt[uint64_t(lq) * P + p]) * (sizeof(PartialRec) + (cross ? sizeof(float4) : 0));
+    rc = pc->barrier(s, err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    *recv_out = static_cast<const PartialRec*>(pc->local(PeerComm::kPartials));
+    *recv_x_out = cross ? static_cast<const float4*>(pc->local(PeerComm::kCross)) : nullptr;
+    return DG_OK;
+  }
   PartialPlan plan;
   plan_partials(c->rank, W, P, pair_cnt.data(), sizeof(PartialRec), plan);
   const std::vector<uint64_t>& send_off = plan.send_off;
@@ -859,11 +954,11 @@ int exchange_partials(dg_ctx* c, const std::vector<uint32_t>& pair_cnt, uint64_t
   c->h2d += (send_off.size() + recv_off.size()) * 8;
   TRY(c->send_buf.ensure(so * sizeof(PartialRec) + 16));
   // cross-segment distortion: the three aggregates travel in a parallel stream (16 B/record)
-  const bool cross = c->cross_active;
   if (cross) TRY(c->send_x.ensure(so * sizeof(float4) + 16));
   launch_pack_partials(c->n_items, item_arrays(c), c->part_item_off_d.as<uint32_t>(),
                        c->global_of_local_d.as<uint8_t>(), c->stream_send_d.as<uint64_t>(), P,
-                       c->send_buf.as<PartialRec>(), cross ? c->send_x.as<float4>() : nullptr, s);
+                       c->send_buf.as<PartialRec>(), cross ? c->send_x.as<float4>() : nullptr,
+                       PeerDst{nullptr, nullptr, 1}, PeerDst{nullptr, nullptr, 1}, s);
   ++c->launches;
   *recv_x_out = cross ? c->send_x.as<float4>() : nullptr;
   if (W == 1) {
@@ -1766,6 +1861,14 @@ int dg_comm_init_host(dg_ctx* c, dg_alltoallv_fn fn, void* user) {
   return DG_OK;
 }
 
+int dg_comm_init_peer(dg_ctx* c, dg_allgather_fn fn, void* user) {
+  TRY(check_ctx(c));
+  if (!fn) return set_err(DG_EINVAL, "null callback");
+  CU(cudaSetDevice(c->device));
+  c->comm.reset(new PeerComm(fn, user, c->rank, c->world));
+  return DG_OK;
+}
+
 // ---------------------------------------------------------------- stage entry points
 int dg_segment_rays(dg_ctx* c, const double* origin, const double* dir, uint64_t n, uint8_t* nseg,
                     uint16_t* region, double* t_enter, double* t_exit, int32_t mem) {
@@ -2267,7 +2370,7 @@ int dg_last_item_data(dg_ctx* c, uint32_t p, uint64_t* ray_id, uint8_t* order, d
   std::vector<uint8_t> ord;
   std::vector<double> vte, vtx;
   std::vector<uint32_t> cnt;
-  TRY(d2h(rec, c->rec.as<RayRec>() + a, n, s));
+  TRY(d2h(rec, c->items_rec + a, n, s));
   TRY(d2h(ord, c->it_order.as<uint8_t>() + a, n, s));
   TRY(d2h(vte, c->it_te.as<double>() + a, n, s));
   TRY(d2h(vtx, c->it_tx.as<double>() + a, n, s));

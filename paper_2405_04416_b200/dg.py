@@ -305,6 +305,29 @@ class Context:
         self._cb = proto(cb)
         _check(lib().dg_comm_init_host(self.h, self._cb, None))
 
+    def comm_init_peer(self, allgather):
+        """Peer-memory backend (dg_comm_init_peer): allgather(bytes) -> list of every rank's
+        bytes (rank order), e.g. torch.distributed.all_gather_object over gloo."""
+        proto = C.CFUNCTYPE(C.c_int, P, P, C.c_uint64, P)
+
+        def cb(user, send, nbytes, recv):
+            try:
+                got = allgather(C.string_at(send, nbytes) if nbytes else b"")
+                off = 0
+                for blob in got:
+                    assert len(blob) == nbytes, (len(blob), nbytes)
+                    if nbytes:
+                        C.memmove(recv + off, blob, nbytes)
+                    off += nbytes
+                return 0
+            except Exception:  # surfaces as DG_ETIMEOUT
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._cb = proto(cb)
+        _check(lib().dg_comm_init_peer(self.h, self._cb, None))
+
     # ---- stage entry points ----
     def segment_rays(self, origin, dir):
         o, d = _c64(origin), _c64(dir)

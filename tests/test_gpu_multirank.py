@@ -1,9 +1,12 @@
 """world = 2 on one GPU: two processes, one dg_ctx each (partition p on rank p % 2), the
-exchanges over the host-staged backend (dg_comm_init_host) with gloo moving the bytes.  Each
-rank trains on its contiguous home shard; the per-rank loss sums and every partition's
-parameters after two steps must match the world = 1 run of the same batch, which the parity
-suite ties to the oracle.  (No kernel waits on another process: the host backend copies to
-the host and back, so sharing one GPU is safe.)"""
+exchanges over either the host-staged backend (dg_comm_init_host, gloo moves the bytes) or the
+peer-memory backend (dg_comm_init_peer: CUDA-IPC mapped receive buffers written directly by the
+pack kernels; gloo carries only the count matrices, handles and barriers).  Each rank renders
+and then trains on its contiguous home shard; the renders, the per-rank loss sums and every
+partition's parameters after two steps must match the world = 1 run of the same batch, which
+the parity suite ties to the oracle.  (No kernel waits on another process: the host backend
+copies through the host, and the peer backend's barriers are host-side (stream sync +
+all-gather), so sharing one GPU is safe.)"""
 import os
 import socket
 import tempfile
@@ -48,7 +51,14 @@ def _gloo_alltoallv(blocks, recv_sizes):
     return out
 
 
-def _rank_main(rank, world, port, ref_path, errq, cross=0):
+def _gloo_allgather(blob):
+    W = dist.get_world_size()
+    out = [None] * W
+    dist.all_gather_object(out, blob)
+    return out
+
+
+def _rank_main(rank, world, port, ref_path, errq, cross=0, backend="host"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -56,18 +66,26 @@ def _rank_main(rank, world, port, ref_path, errq, cross=0):
         from paper_2405_04416_b200 import dg
         cfg = _cfg(cross)
         ctx = dg.Context(cfg, device=0, rank=rank, world=world)
-        ctx.comm_init_host(_gloo_alltoallv)
+        if backend == "peer":
+            ctx.comm_init_peer(_gloo_allgather)
+        else:
+            ctx.comm_init_host(_gloo_alltoallv)
         inject(cfg, None, [_LocalOnly(ctx)], occupancy_fraction=0.6)
         ctx.set_appearance(app_rows(1).astype(np.float32))
         o, d, gt, img = _rays()
         lo, hi = rank * N // world, (rank + 1) * N // world
+        ref = np.load(ref_path)
+        # evaluate_rays before training: the home merge runs the generic all-to-all-v
+        rgb, T, depth = ctx.render(o[lo:hi], d[lo:hi], ref["app"], first_ray_id=lo)
+        assert np.allclose(rgb, ref["rgb"][lo:hi], rtol=1e-5, atol=1e-6), np.abs(rgb - ref["rgb"][lo:hi]).max()
+        assert np.allclose(T, ref["T"][lo:hi], rtol=1e-5, atol=1e-6)
+        assert np.allclose(depth, ref["depth"][lo:hi], rtol=1e-5, atol=1e-5)
         losses = []
         for step in range(STEPS):
             st = ctx.train_step(o[lo:hi], d[lo:hi], gt[lo:hi], img[lo:hi], step=step, first_ray_id=lo)
             losses.append([st["loss_rgb"], st["loss_transmittance"], st["loss_distortion"]])
         tot = torch.tensor(np.array(losses, np.float64))
         dist.all_reduce(tot)
-        ref = np.load(ref_path)
         assert np.allclose(tot.numpy(), ref["losses"], rtol=1e-6, atol=1e-12), (tot.numpy(), ref["losses"])
         # Reds sum in a different order on 1 and 2 ranks; Adam turns a sign flip of a
         # near-zero gradient into a full +-lr step of that entry, so the bar is on the
@@ -101,19 +119,22 @@ class _LocalOnly:
             self.ctx.set_occupancy(g, c, bits)
 
 
+@pytest.mark.parametrize("backend", ["host", "peer"])
 @pytest.mark.parametrize("cross", [0, 1])
-def test_two_ranks_match_single_rank(cross):
+def test_two_ranks_match_single_rank(cross, backend):
     from paper_2405_04416_b200 import dg
     cfg = _cfg(cross)
     ctx = dg.Context(cfg, device=0)
     inject(cfg, ctx, [], occupancy_fraction=0.6)
     ctx.set_appearance(app_rows(1).astype(np.float32))
     o, d, gt, img = _rays()
+    app = app_rows(1)[0].astype(np.float32)
+    rgb, T, depth = ctx.render(o, d, app)
     losses = []
     for step in range(STEPS):
         st = ctx.train_step(o, d, gt, img, step=step)
         losses.append([st["loss_rgb"], st["loss_transmittance"], st["loss_distortion"]])
-    ref = {"losses": np.array(losses, np.float64)}
+    ref = {"losses": np.array(losses, np.float64), "rgb": rgb, "T": T, "depth": depth, "app": app}
     for g in range(KX * KY):
         ref[f"p{g}"] = ctx.get_params(g)
     del ctx
@@ -126,7 +147,7 @@ def test_two_ranks_match_single_rank(cross):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
         s.close()
-        procs = [mpc.Process(target=_rank_main, args=(r, 2, port, path, errq, cross)) for r in range(2)]
+        procs = [mpc.Process(target=_rank_main, args=(r, 2, port, path, errq, cross, backend)) for r in range(2)]
         for p in procs:
             p.start()
         for p in procs:
