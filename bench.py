@@ -267,6 +267,8 @@ def main():
     ap.add_argument("--render-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                    help="exchange backend for N > 1: NCCL all-to-all-v, or peer-memory pack kernels")
     ap.add_argument("--no-cpu-stages", action="store_true", help="skip the all-core stage baseline")
     ap.add_argument("--ref-rays", type=int, default=1024, help="rays per step per replica of the --impl reference arm")
     ap.add_argument("--cpu-rays", type=int, default=2048, help="rays of the cpu_baseline sample (~10 s)")
@@ -302,7 +304,17 @@ def main():
         if rank == 0:
             uid.copy_(torch.tensor(list(dg.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
-        ctx.comm_init_nccl(bytes(uid.cpu().tolist()))
+        if args.comm == "peer":  # pack kernels write the owners' buffers over CUDA IPC
+            gloo = dist.new_group(backend="gloo")
+
+            def allgather(blob):
+                out = [None] * world
+                dist.all_gather_object(out, blob, group=gloo)
+                return out
+
+            ctx.comm_init_peer(allgather)
+        else:
+            ctx.comm_init_nccl(bytes(uid.cpu().tolist()))
     for g in ctx.local:
         ctx.init_fast(g, seed=1)
     ctx.set_appearance(workloads.appearance_rows(cfg.appearance_dim, 1))
