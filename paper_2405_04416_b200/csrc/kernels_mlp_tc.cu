@@ -515,16 +515,27 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
 // 16 warps: 4 lane quadrants x 4 column parts, so every epilogue is 16 columns per thread.
 constexpr int XW = 32, HW = 64, CW = 48;  // activation tile widths
 
+// Bias gradients ride in the weight-gradient GEMMs: the hi activation tiles of x / cin sit
+// right before, and those of h1 / c1 right after, a 2 KB chunk whose column 0 is 1 (bf16
+// exact, so its lo part is 0 and the hi.lo product skips it): B = [A | 1] (append) or
+// [1 | A] (prepend) gives dW and db in one N+8-wide MMA.  The output layer's 3 bias
+// gradients are warp-reduced in the B1 epilogue instead.
 struct BwdTcSmem {
   TcWeights w;
   uint8_t g5[2][TM * 16 * 2];  // followed by >= 12 KB of valid smem (M=64 MN-major reads 64 cols)
-  uint8_t x[2][TM * XW * 2];
-  uint8_t h1[2][TM * HW * 2];
-  uint8_t cin[2][TM * CW * 2];
-  uint8_t c1[2][TM * HW * 2];
+  uint8_t x_hi[TM * XW * 2];
+  uint8_t ones_a[TM * 8 * 2];  // [x | 1] and [1 | h1]
+  uint8_t h1_hi[TM * HW * 2];
+  uint8_t cin_hi[TM * CW * 2];
+  uint8_t ones_b[TM * 8 * 2];  // [cin | 1] and [1 | c1]
+  uint8_t c1_hi[TM * HW * 2];
+  uint8_t x_lo[TM * XW * 2];
+  uint8_t h1_lo[TM * HW * 2];
+  uint8_t cin_lo[TM * CW * 2];
+  uint8_t c1_lo[TM * HW * 2];
   uint8_t c2[2][TM * HW * 2];
   uint8_t s[2][TM * 64 * 2];   // G4 / G2
-  uint8_t ones[TM * 8 * 2];    // bias-gradient B operand: column 0 = 1
+  float bias_c2[4];            // output-layer bias gradient, summed over the CTA's tiles
   float sig_raw[TM];
   float gsig[TM];
   uint32_t dmask[TM];
@@ -535,9 +546,14 @@ struct BwdTcSmem {
 static_assert(sizeof(BwdTcSmem) <= 232448, "backward tile set exceeds 227 KB of shared memory");
 
 // TMEM columns: [0,64) accumulator, [64,128) A operand; dW accumulators (M = 64 rows = out
-// features, row o at lane (o % 16) + 32 (o / 16)); bias accumulators (column 0 of 8).
-constexpr uint32_t TD_C2 = 128, TD_C1 = 192, TD_C0 = 256, TD_D1 = 304, TD_D0 = 368;
-constexpr uint32_t TB_C2 = 400, TB_C1 = 408, TB_C0 = 416, TB_D1 = 424, TB_D0 = 432;
+// features, row o at lane (o % 16) + 32 (o / 16)) with the bias column folded in: appended
+// after dW (C0: [cin | 1], D0: [x | 1]) or prepended (C1: [1 | c1], D1: [1 | h1]).
+constexpr uint32_t TD_C2 = 128;                    // 64 (bias: epilogue)
+constexpr uint32_t TB_C1 = 192, TD_C1 = 200;       // 8 + 64
+constexpr uint32_t TD_C0 = 264, TB_C0 = 312;       // 48 + 8
+constexpr uint32_t TB_D1 = 320, TD_D1 = 328;       // 8 + 64
+constexpr uint32_t TD_D0 = 392, TB_D0 = 424;       // 32 + 8
+constexpr uint32_t kNoBias = 0xffffffffu;
 
 // D (M=64 x N) (+)= G^T A over K = TM samples; G tile (TM x >=64 cols span), A tile (TM x N);
 // both read MN-major (SBO = TM/8*128, LBO = 128).
@@ -560,21 +576,28 @@ __device__ __forceinline__ void gemm_wgrad(uint32_t d_tmem, const uint8_t* g_hi,
   }
 }
 
-// Bias gradient D (M=64 x 8) (+)= G^T . ones (column 0 of the ones tile): 2 MMAs per K step
-// (ones are exact in bf16, so G_hi . 1 + G_lo . 1).
-__device__ __forceinline__ void gemm_bias(uint32_t d_tmem, const uint8_t* g_hi, const uint8_t* g_lo,
-                                          const uint8_t* ones, bool accumulate) {
-  constexpr uint32_t id = tc::idesc_bf16(64, 8, 1, 1);
+// dW and db in one accumulation: B = the hi tile extended by the ones chunk (N + 8 columns,
+// b_ext = the first chunk: the ones chunk when prepended, the tile when appended) for the
+// hi.hi and lo.hi products; the hi.lo product uses the lo tile alone (N columns, at d_lo =
+// d + 8 when prepended), the ones' lo part being 0.
+template <int N, bool kPrepend>
+__device__ __forceinline__ void gemm_wgrad_bias(uint32_t d_tmem, const uint8_t* g_hi, const uint8_t* g_lo,
+                                                const uint8_t* b_ext, const uint8_t* a_lo, bool accumulate) {
+  constexpr uint32_t id_ext = tc::idesc_bf16(64, N + 8, 1, 1);
+  constexpr uint32_t id = tc::idesc_bf16(64, N, 1, 1);
   constexpr uint32_t SBO = (TM / 8) * 128;
   const uint64_t gh = tc::smem_desc(tc::smem_u32(g_hi), 128, SBO);
   const uint64_t gl = tc::smem_desc(tc::smem_u32(g_lo), 128, SBO);
-  const uint64_t on = tc::smem_desc(tc::smem_u32(ones), 128, SBO);
+  const uint64_t be = tc::smem_desc(tc::smem_u32(b_ext), 128, SBO);
+  const uint64_t al = tc::smem_desc(tc::smem_u32(a_lo), 128, SBO);
   const uint32_t acc0 = accumulate ? 1u : 0u;
+  const uint32_t d_lo = kPrepend ? d_tmem + 8 : d_tmem;
 #pragma unroll
   for (int k = 0; k < TM / 16; ++k) {
     const uint32_t o = (k * 256) >> 4;
-    tc::mma_bf16(d_tmem, gh + o, on + o, id, k > 0 ? 1u : acc0);
-    tc::mma_bf16(d_tmem, gl + o, on + o, id, 1u);
+    tc::mma_bf16(d_tmem, gh + o, be + o, id_ext, k > 0 ? 1u : acc0);
+    tc::mma_bf16(d_lo, gh + o, al + o, id, 1u);
+    tc::mma_bf16(d_tmem, gl + o, be + o, id_ext, 1u);
   }
 }
 
@@ -605,6 +628,7 @@ __device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, u
   const int o = quad * 16 + lane;
   const uint32_t lanes = tmem + ((uint32_t)(quad * 32) << 16);
   for (int g = part; g <= N / 8; g += parts) {
+    if (g == N / 8 && bcol == kNoBias) break;
     float v[8];
     tc::tmem_ld8(lanes + (g < N / 8 ? col0 + 8 * g : bcol), v);
     tc::tmem_wait_ld();
@@ -622,10 +646,14 @@ __device__ void flush_dw(uint32_t tmem, uint32_t col0, int N, int out, int in, u
   }
 }
 
-__device__ void flush_all(uint32_t tmem, const FieldDesc& fd, float* __restrict__ grads) {
+__device__ void flush_all(uint32_t tmem, const FieldDesc& fd, float* __restrict__ grads, float* bias_c2) {
   float* base = grads + fd.base;
   const int enc = (int)fd.L * 2, cin = 31 + (int)fd.app_dim;
-  flush_dw(tmem, TD_C2, HW, 3, 64, TB_C2, base + fd.cw2, base + fd.cb2);
+  if (threadIdx.x < 3) {  // the epilogue-reduced output-layer bias
+    if (bias_c2[threadIdx.x] != 0.f) atomicAdd(base + fd.cb2 + threadIdx.x, bias_c2[threadIdx.x]);
+    bias_c2[threadIdx.x] = 0.f;
+  }
+  flush_dw(tmem, TD_C2, HW, 3, 64, kNoBias, base + fd.cw2, base + fd.cb2);
   flush_dw(tmem, TD_C1, HW, 64, 64, TB_C1, base + fd.cw1, base + fd.cb1);
   flush_dw(tmem, TD_C0, CW, 64, cin, TB_C0, base + fd.cw0, base + fd.cb0);
   flush_dw(tmem, TD_D1, HW, 16, 64, TB_D1, base + fd.dw1, base + fd.db1);
@@ -659,8 +687,11 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
     tc::fence_mbar_init();
   }
   // ones tile (bias-gradient B operand, MN-major [K = 128 samples x N = 8]): column 0 = 1
-  for (int r = tid; r < TM; r += NTB)
-    *reinterpret_cast<uint4*>(sm.ones + tc::core_offset(r, 0, TM)) = make_uint4(0x3f80u, 0u, 0u, 0u);
+  for (int r = tid; r < TM; r += NTB) {
+    *reinterpret_cast<uint4*>(sm.ones_a + tc::core_offset(r, 0, TM)) = make_uint4(0x3f80u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sm.ones_b + tc::core_offset(r, 0, TM)) = make_uint4(0x3f80u, 0u, 0u, 0u);
+  }
+  if (tid < 4) sm.bias_c2[tid] = 0.f;
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -668,8 +699,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t a_op = tmem + A_HI, ta = my_lanes + A_HI;
   // operand tiles: smem copy (weight-gradient GEMMs) + TMEM A region (the next GEMM)
-  const Sink sxt{nullptr, nullptr, ta}, sh1{sm.h1[0], sm.h1[1], ta}, scin{sm.cin[0], sm.cin[1], ta};
-  const Sink sc1{sm.c1[0], sm.c1[1], ta}, sc2{sm.c2[0], sm.c2[1], ta}, sg5{sm.g5[0], sm.g5[1], ta};
+  const Sink sxt{nullptr, nullptr, ta}, sh1{sm.h1_hi, sm.h1_lo, ta}, scin{sm.cin_hi, sm.cin_lo, ta};
+  const Sink sc1{sm.c1_hi, sm.c1_lo, ta}, sc2{sm.c2[0], sm.c2[1], ta}, sg5{sm.g5[0], sm.g5[1], ta};
   const Sink ss{sm.s[0], sm.s[1], ta};
   float xk[8];  // this tile's X chunk: TMEM A at once, the smem copy at the first epilogue
   uint32_t phase = 0;
@@ -732,7 +763,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next: X, item
       mma_done();
       {
-        put8s(sm.x[0], sm.x[1], row, part * 8, xk);  // the previous tile's dWd0 GEMM is done
+        put8s(sm.x_hi, sm.x_lo, row, part * 8, xk);  // the previous tile's dWd0 GEMM is done
         float v[16];
         ld16(my_lanes + c16, v);
 #pragma unroll
@@ -815,14 +846,26 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         }
         put8(sg5, row, 0, g);
         put8(sg5, row, 8, g + 8);
+        // output-layer bias gradient db = G5^T . 1: the quadrant's 32 rows, warp-reduced
+        float b0 = g[0], b1 = g[1], b2 = g[2];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          b0 += __shfl_xor_sync(0xffffffffu, b0, o);
+          b1 += __shfl_xor_sync(0xffffffffu, b1, o);
+          b2 += __shfl_xor_sync(0xffffffffu, b2, o);
+        }
+        if (lane == 0) {
+          atomicAdd(&sm.bias_c2[0], b0);
+          atomicAdd(&sm.bias_c2[1], b1);
+          atomicAdd(&sm.bias_c2[2], b2);
+        }
         // sigma path of the density raw gradient (field.cpp:313)
         sm.gsig[row] = (sm.dmask[row] & 1u) ? 0.f : up.x * expf(sm.sig_raw[row]);
       }
       pf.grad(m, part);  // next tile's upstream gradient
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<16, 64, 16>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]); },
-             [&] { gemm_wgrad<HW>(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], !fresh);
-                    gemm_bias(tmem + TB_C2, sm.g5[0], sm.g5[1], sm.ones, !fresh); });
+             [&] { gemm_wgrad<HW>(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], !fresh); });
       mma_done();
       // ---------------- B2: G4 = dC2 * act'(C2) -> s ----------------
       {
@@ -832,20 +875,18 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       }
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]); },
-             [&] { gemm_wgrad<HW>(tmem + TD_C1, sm.s[0], sm.s[1], sm.c1[0], sm.c1[1], !fresh);
-                    gemm_bias(tmem + TB_C1, sm.s[0], sm.s[1], sm.ones, !fresh); });
+             [&] { gemm_wgrad_bias<HW, true>(tmem + TB_C1, sm.s[0], sm.s[1], sm.ones_b, sm.c1_lo, !fresh); });
       mma_done();
       // ---------------- B3: G3 = dC1 * act'(C1) -> c2 ----------------
       {
         float v[16];
         ld16(my_lanes + c16, v);
-        grad_act16(sm.c1[0], sm.c1[1], sc2, row, c16, v, act_c);
+        grad_act16(sm.c1_hi, sm.c1_lo, sc2, row, c16, v, act_c);
       }
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 16, 64>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]); },
-             [&] { gemm_wgrad<CW>(tmem + TD_C0, sm.c2[0], sm.c2[1], sm.cin[0], sm.cin[1], !fresh);
-                    gemm_bias(tmem + TB_C0, sm.c2[0], sm.c2[1], sm.ones, !fresh); });
+             [&] { gemm_wgrad_bias<CW, false>(tmem + TD_C0, sm.c2[0], sm.c2[1], sm.cin_hi, sm.cin_lo, !fresh); });
       mma_done();
       // ---------------- B4: G2 = density raw gradient -> s cols 0..15 ----------------
       if (part == 0) {
@@ -861,19 +902,17 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       }
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<16, 64, 16>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]); },
-             [&] { gemm_wgrad<HW>(tmem + TD_D1, sm.s[0], sm.s[1], sm.h1[0], sm.h1[1], !fresh);
-                    gemm_bias(tmem + TB_D1, sm.s[0], sm.s[1], sm.ones, !fresh); });
+             [&] { gemm_wgrad_bias<HW, true>(tmem + TB_D1, sm.s[0], sm.s[1], sm.ones_a, sm.h1_lo, !fresh); });
       mma_done();
       // ---------------- B5: G1 = dH1 * relu'(H1) -> c2 ----------------
       {
         float v[16];
         ld16(my_lanes + c16, v);
-        grad_act16(sm.h1[0], sm.h1[1], sc2, row, c16, v, 1);
+        grad_act16(sm.h1_hi, sm.h1_lo, sc2, row, c16, v, 1);
       }
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 32, 64>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]); },
-             [&] { gemm_wgrad<XW>(tmem + TD_D0, sm.c2[0], sm.c2[1], sm.x[0], sm.x[1], !fresh);
-                    gemm_bias(tmem + TB_D0, sm.c2[0], sm.c2[1], sm.ones, !fresh); });
+             [&] { gemm_wgrad_bias<XW, false>(tmem + TD_D0, sm.c2[0], sm.c2[1], sm.x_hi, sm.x_lo, !fresh); });
       mma_done();
       fresh = false;
       // ---------------- B6: dX -> global, level-major; next tile's X into the x tile ----------------
@@ -904,7 +943,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       }
       if (!has_next) break;
       if (nx.f != loaded) {
-        flush_all(tmem, m.fields[loaded], m.grads);
+        flush_all(tmem, m.fields[loaded], m.grads, sm.bias_c2);
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
@@ -922,7 +961,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  if (loaded >= 0) flush_all(tmem, m.fields[loaded], m.grads);
+  if (loaded >= 0) flush_all(tmem, m.fields[loaded], m.grads, sm.bias_c2);
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_free(tmem, 512);
