@@ -443,6 +443,23 @@ def main():
                         "traffic = DRAM read+write bytes per launch from the committed ncu --set full "
                         "capture (profiles/traffic.json)"}
     roof["stage_ms"] = st
+    # every hot kernel against its own roof (the dominant stage above can flip between the
+    # MLP backward and the encoding backward from run to run)
+    n_par = sum(ctx.param_count(g) for g in ctx.local)
+    adam_gbs = 32.0 * n_par / (st["adam"] / 1e3) / 1e9 if st["adam"] > 0 else 0.0
+    roofline_kernels = {
+        "k_encode_fwd": {"bound": "hbm", "achieved": enc_fwd_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": enc_fwd_gbs / hbm, "traffic": traffic.get("k_encode_fwd"),
+                         "algorithmic": f"{ENCODE_BYTES_PER_SAMPLE} B/sample"},
+        "k_encode_bwd": {"bound": "hbm (L2 atomics)", "achieved": enc_bwd_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": enc_bwd_gbs / hbm, "traffic": traffic.get("k_encode_bwd"),
+                         "algorithmic": f"{2 * ENCODE_BYTES_PER_SAMPLE} B/sample (RMW)"},
+        "k_mlp_fwd_tc+k_mlp_bwd_tc": {"bound": "tensor", "achieved": mlp_tflops, "peak": tensor_peak,
+                                      "unit": "TFLOP/s", "frac": mlp_tflops / tensor_peak,
+                                      "traffic": traffic.get("k_mlp_bwd_tc"),
+                                      "algorithmic": f"{MLP_FLOP_TRAIN} FLOP/sample (x3 bf16 MMAs executed)"},
+        "k_adam": {"bound": "hbm", "achieved": adam_gbs, "peak": hbm, "unit": "GB/s", "frac": adam_gbs / hbm,
+                   "traffic": traffic.get("k_adam"), "algorithmic": f"32 B/param x {n_par}"}}
     roofline_encode = {"encode_fwd": {"achieved": enc_fwd_gbs, "peak": hbm, "unit": "GB/s",
                                       "frac": enc_fwd_gbs / hbm,
                                       "bytes": f"{ENCODE_BYTES_PER_SAMPLE} B/sample x {samples_rank}"},
@@ -468,7 +485,7 @@ def main():
                     "encode_samples_per_s": samples_rank / ms("encode_fwd"),
                     "field_fwd_samples_per_s": samples_rank / ms("encode_fwd", "mlp_fwd"),
                     "field_bwd_samples_per_s": samples_rank / ms("mlp_bwd", "encode_bwd"),
-                    "adam_params_per_s": sum(ctx.param_count(g) for g in ctx.local) / ms("adam")}
+                    "adam_params_per_s": n_par / ms("adam")}
             cpu["stages"] = cpu_stages
 
     if rank == 0:
@@ -486,7 +503,8 @@ def main():
                 "render_rays_per_s": render_value, "render_ms": rms,
                 "encode_gbs": enc_fwd_gbs, "exchange_bytes_rank0": bytes_sent,
                 "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
-                "roofline": roof, "roofline_encode": roofline_encode, "cpu_baseline": cpu}
+                "roofline": roof, "roofline_kernels": roofline_kernels, "roofline_encode": roofline_encode,
+                "cpu_baseline": cpu}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
