@@ -197,17 +197,30 @@ __device__ __forceinline__ void act16(float* v, const float* b, int act) {
 
 struct TileGeo {
   int f;
-  uint64_t s0;
+  uint32_t s0;  // first sample (sample counts fit 32 bits, the ray ids do)
   int count;
+  uint32_t t_end, s_end;  // the field's tile / sample end: the next tile of the same field
+                          // is derived without touching the offset tables
 };
 __device__ __forceinline__ TileGeo tile_geo(const MlpLaunch& m, uint32_t tile) {
   int f = 0;
-  while (f + 1 < (int)m.n_fields && tile >= m.tile_off[f + 1]) ++f;
+  while (f + 1 < (int)m.n_fields && tile >= __ldg(m.tile_off + f + 1)) ++f;
   TileGeo g;
   g.f = f;
-  g.s0 = m.field_off[f] + (uint64_t)(tile - m.tile_off[f]) * TM;
-  const uint64_t rem = m.field_off[f + 1] - g.s0;
-  g.count = rem < (uint64_t)TM ? (int)rem : TM;
+  g.s0 = __ldg(m.field_off + f) + (tile - __ldg(m.tile_off + f)) * (uint32_t)TM;
+  g.t_end = __ldg(m.tile_off + f + 1);
+  g.s_end = __ldg(m.field_off + f + 1);
+  const uint32_t rem = g.s_end - g.s0;
+  g.count = rem < (uint32_t)TM ? (int)rem : TM;
+  return g;
+}
+// the tile after `c` (consecutive tiles of one CTA)
+__device__ __forceinline__ TileGeo tile_geo_next(const MlpLaunch& m, const TileGeo& c, uint32_t tile) {
+  if (tile >= c.t_end) return tile_geo(m, tile);
+  TileGeo g = c;
+  g.s0 = c.s0 + (uint32_t)TM;
+  const uint32_t rem = c.s_end - g.s0;
+  g.count = rem < (uint32_t)TM ? (int)rem : TM;
   return g;
 }
 
@@ -750,7 +763,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       const uint64_t gs = cur.s0 + row;
       const uint32_t next = tile + 1;
       const bool has_next = next < t_end;
-      const TileGeo nx = has_next ? tile_geo(m, next) : cur;
+      const TileGeo nx = has_next ? tile_geo_next(m, cur, next) : cur;
       // this tile's prefetched dir / app / upstream gradient move out of the prefetch registers
       float cur_app[17];
 #pragma unroll
