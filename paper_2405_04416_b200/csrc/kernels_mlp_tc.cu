@@ -404,10 +404,9 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
     pf.appearance(m, m.fields[cur.f], part);
     stage_weights_tc(m.fields[cur.f], m.params, sm.w);
     int loaded = cur.f;
+    int act_c = m.fields[cur.f].coarse ? 2 : 1;  // colour activation of the loaded field
     pf.put_x(act, row, part);
     for (;;) {
-      const FieldDesc& fd = m.fields[cur.f];
-      const int act_c = fd.coarse ? 2 : 1;
       const bool valid = row < cur.count;
       const uint64_t gs = cur.s0 + row;
       const uint32_t next = tile + gridDim.x;
@@ -495,6 +494,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
         __syncthreads();  // every thread is done with the old biases
         stage_weights_tc(m.fields[nx.f], m.params, sm.w);
         loaded = nx.f;
+        act_c = m.fields[nx.f].coarse ? 2 : 1;
       }
       pf.put_x(act, row, part);  // the A region is free: every MMA has completed
       tile = next;
@@ -753,12 +753,11 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
     stage_weights_tc(m.fields[cur.f], m.params, sm.w);
     loaded = cur.f;
     bool fresh = true;  // next dW GEMMs start a new accumulation
+    int act_c = m.fields[cur.f].coarse ? 2 : 1;  // colour activation of the loaded field
     pf.put_x(sxt, row, part);
 #pragma unroll
     for (int i = 0; i < 8; ++i) xk[i] = pf.x[i];
     for (;;) {
-      const FieldDesc& fd = m.fields[cur.f];
-      const int act_c = fd.coarse ? 2 : 1;
       const bool valid = row < cur.count;
       const uint64_t gs = cur.s0 + row;
       const uint32_t next = tile + 1;
@@ -962,6 +961,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         tc::fence_after();
         stage_weights_tc(m.fields[nx.f], m.params, sm.w);
         loaded = nx.f;
+        act_c = m.fields[nx.f].coarse ? 2 : 1;
         fresh = true;
       }
       pf.put_x(sxt, row, part);  // A region is free (the dX GEMM completed); smem x at F1
