@@ -201,6 +201,7 @@ struct TileGeo {
   int count;
   uint32_t t_end, s_end;  // the field's tile / sample end: the next tile of the same field
                           // is derived without touching the offset tables
+  uint32_t t_beg, s_beg;  // the field's first tile / sample
 };
 __device__ __forceinline__ TileGeo tile_geo(const MlpLaunch& m, uint32_t tile) {
   int f = 0;
@@ -210,7 +211,18 @@ __device__ __forceinline__ TileGeo tile_geo(const MlpLaunch& m, uint32_t tile) {
   g.s0 = __ldg(m.field_off + f) + (tile - __ldg(m.tile_off + f)) * (uint32_t)TM;
   g.t_end = __ldg(m.tile_off + f + 1);
   g.s_end = __ldg(m.field_off + f + 1);
+  g.t_beg = __ldg(m.tile_off + f);
+  g.s_beg = __ldg(m.field_off + f);
   const uint32_t rem = g.s_end - g.s0;
+  g.count = rem < (uint32_t)TM ? (int)rem : TM;
+  return g;
+}
+// any later tile (the forward strides its tiles over the grid)
+__device__ __forceinline__ TileGeo tile_geo_at(const MlpLaunch& m, const TileGeo& c, uint32_t tile) {
+  if (tile >= c.t_end) return tile_geo(m, tile);
+  TileGeo g = c;
+  g.s0 = c.s_beg + (tile - c.t_beg) * (uint32_t)TM;
+  const uint32_t rem = c.s_end - g.s0;
   g.count = rem < (uint32_t)TM ? (int)rem : TM;
   return g;
 }
@@ -411,7 +423,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
       const uint64_t gs = cur.s0 + row;
       const uint32_t next = tile + gridDim.x;
       const bool has_next = next < m.n_tiles;
-      const TileGeo nx = has_next ? tile_geo(m, next) : cur;
+      const TileGeo nx = has_next ? tile_geo_at(m, cur, next) : cur;
       to_mma();
       // ---- L1: H1 = relu(X Wd0^T + b) ----
       ISSUE(gemm_ts<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
