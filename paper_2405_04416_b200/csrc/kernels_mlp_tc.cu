@@ -870,19 +870,6 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         }
         put8(sg5, row, 0, g);
         put8(sg5, row, 8, g + 8);
-        // output-layer bias gradient db = G5^T . 1: the quadrant's 32 rows, warp-reduced
-        float b0 = g[0], b1 = g[1], b2 = g[2];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          b0 += __shfl_xor_sync(0xffffffffu, b0, o);
-          b1 += __shfl_xor_sync(0xffffffffu, b1, o);
-          b2 += __shfl_xor_sync(0xffffffffu, b2, o);
-        }
-        if (lane == 0) {
-          atomicAdd(&sm.bias_c2[0], b0);
-          atomicAdd(&sm.bias_c2[1], b1);
-          atomicAdd(&sm.bias_c2[2], b2);
-        }
         // sigma path of the density raw gradient (field.cpp:313)
         sm.gsig[row] = (sm.dmask[row] & 1u) ? 0.f : up.x * expf(sm.sig_raw[row]);
       }
@@ -923,6 +910,23 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         for (int k = 1; k < 16; ++k) g[k] = ((mask >> k) & 1u) ? 0.f : v[k - 1];
         put8(ss, row, 0, g);
         put8(ss, row, 8, g + 8);
+      } else if (part == 1) {
+        // output-layer bias gradient db = G5^T . 1 (off the critical path: part 1 is idle in
+        // this 16-column epilogue; G5 stays in smem until the next tile's B1)
+        float g5[8];
+        get8(sm.g5[0], sm.g5[1], row, 0, g5);
+        float b0 = g5[0], b1 = g5[1], b2 = g5[2];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          b0 += __shfl_xor_sync(0xffffffffu, b0, o);
+          b1 += __shfl_xor_sync(0xffffffffu, b1, o);
+          b2 += __shfl_xor_sync(0xffffffffu, b2, o);
+        }
+        if (lane == 0) {
+          atomicAdd(&sm.bias_c2[0], b0);
+          atomicAdd(&sm.bias_c2[1], b1);
+          atomicAdd(&sm.bias_c2[2], b2);
+        }
       }
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<16, 64, 16>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]); },
