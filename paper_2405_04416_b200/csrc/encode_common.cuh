@@ -50,6 +50,45 @@ __device__ __forceinline__ void level_corners(const LevelDesc& lv, const double 
   }
 }
 
+// The backward's variant: the same fp64 indices and fractions, but the corner weights are
+// formed in fp32 from the fp64 factors rounded once (<= 2 ulp from the rounded fp64 product;
+// a weight only scales the upstream gradient, it never feeds a nonlinearity), and a corner is
+// skipped exactly when one fp64 factor is 0 (the fp64 product cannot underflow).
+__device__ __forceinline__ void level_corners_w32(const LevelDesc& lv, const double p[3], Corners& c) {
+  const AxisW ax = lattice_axis(p[0], lv.n[0]);
+  const AxisW ay = lattice_axis(p[1], lv.n[1]);
+  const AxisW az = lattice_axis(p[2], lv.n[2]);
+  const double fx[2] = {dsub(1.0, ax.frac), ax.frac};
+  const double fy[2] = {dsub(1.0, ay.frac), ay.frac};
+  const double fz[2] = {dsub(1.0, az.frac), az.frac};
+  const float gx[2] = {(float)fx[0], (float)fx[1]}, gy[2] = {(float)fy[0], (float)fy[1]};
+  const float gz[2] = {(float)fz[0], (float)fz[1]};
+  uint32_t rx[2], ry[2], rz[2];
+  if (lv.hashed) {
+    rx[0] = ax.i0;
+    rx[1] = ax.i1;
+    ry[0] = ay.i0 * 2654435761u;
+    ry[1] = ay.i1 * 2654435761u;
+    rz[0] = az.i0 * 805459861u;
+    rz[1] = az.i1 * 805459861u;
+  } else {
+    rx[0] = ax.i0;
+    rx[1] = ax.i1;
+    ry[0] = lv.n[0] * ay.i0;
+    ry[1] = lv.n[0] * ay.i1;
+    rz[0] = lv.n[0] * lv.n[1] * az.i0;
+    rz[1] = lv.n[0] * lv.n[1] * az.i1;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int cx = k & 1, cy = (k >> 1) & 1, cz = (k >> 2) & 1;
+    c.w[k] = __fmul_rn(__fmul_rn(gx[cx], gy[cy]), gz[cz]);
+    const bool zero = fx[cx] == 0.0 || fy[cy] == 0.0 || fz[cz] == 0.0;
+    const uint32_t row = lv.hashed ? ((rx[cx] ^ ry[cy] ^ rz[cz]) & lv.mask) : (rx[cx] + ry[cy] + rz[cz]);
+    c.row[k] = zero ? 0xffffffffu : row;
+  }
+}
+
 // Row pairing: the two x-neighbour corners (cx = 0, 1) of each (cy, cz) land in rows
 // i ^ h and (i + 1) ^ h (hashed) or r and r + 1 (one-to-one); when those differ only in bit 0
 // (half the time) they are one 16-byte aligned float4 (every level table is 16-byte aligned),

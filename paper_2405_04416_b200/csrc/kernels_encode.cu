@@ -172,7 +172,10 @@ __global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __rest
 }
 
 template <bool PC>
-__global__ void __launch_bounds__(256) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
+#ifndef ENC_BWD_MINB
+#define ENC_BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(256, ENC_BWD_MINB) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
   const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = s < f.n_total;
   const EncPass ps = f.pass[blockIdx.y];
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(256) k_encode_bwd(FieldLaunch f, const float* 
     Corners c;
     if (valid) {
       up = ld_stream(reinterpret_cast<const float2*>(dX) + (uint64_t)l * f.n_total + s);
-      level_corners(fd.lv[l], p, c);
+      level_corners_w32(fd.lv[l], p, c);
       clip_to_slice(fd.lv[l], ps, c);
     }
     float2* table = reinterpret_cast<float2*>(f.grads + fd.base + fd.lv[l].offset);
