@@ -75,7 +75,11 @@ def _rank_main(rank, world, port, ref_path, errq, cross=0, backend="host"):
         o, d, gt, img = _rays()
         lo, hi = rank * N // world, (rank + 1) * N // world
         ref = np.load(ref_path)
-        # evaluate_rays before training: the home merge runs the generic all-to-all-v
+        # evaluate_rays before training: the home merge runs the generic all-to-all-v; a small
+        # batch first, so the full one grows the (peer backend's) receive buffers
+        q = lo + (hi - lo) // 5
+        rgb, T, depth = ctx.render(o[lo:q], d[lo:q], ref["app"], first_ray_id=lo)
+        assert np.allclose(rgb, ref["rgb"][lo:q], rtol=1e-5, atol=1e-6), np.abs(rgb - ref["rgb"][lo:q]).max()
         rgb, T, depth = ctx.render(o[lo:hi], d[lo:hi], ref["app"], first_ray_id=lo)
         assert np.allclose(rgb, ref["rgb"][lo:hi], rtol=1e-5, atol=1e-6), np.abs(rgb - ref["rgb"][lo:hi]).max()
         assert np.allclose(T, ref["T"][lo:hi], rtol=1e-5, atol=1e-6)
