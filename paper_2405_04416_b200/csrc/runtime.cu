@@ -136,7 +136,7 @@ struct dg_ctx {
   };
   std::vector<std::vector<Seg>> field_segs;  // [2][n_local]
   std::vector<std::vector<dg_array_desc>> layouts;
-  uint64_t enc_budget_fwd = 256ull << 20;  // encode pass budgets (DG_ENC_FWD_MB / DG_ENC_BWD_MB)
+  uint64_t enc_budget_fwd = 192ull << 20;  // encode pass budgets (DG_ENC_FWD_MB / DG_ENC_BWD_MB)
   uint64_t enc_budget_bwd = 96ull << 20;
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
   double enc_agg_samples_per_cell = 1.5;   // warp-aggregate levels with >= this many samples/cell (DG_ENC_AGG)
