@@ -717,6 +717,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
     *reinterpret_cast<uint4*>(sm.ones_b + tc::core_offset(r, 0, TM)) = make_uint4(0x3f80u, 0u, 0u, 0u);
   }
   if (tid < 4) sm.bias_c2[tid] = 0.f;
+  for (int i = tid; i < (int)(sizeof(sm.g5) / 16); i += NTB)  // G5 columns 3-15 stay 0
+    reinterpret_cast<uint4*>(sm.g5)[i] = make_uint4(0u, 0u, 0u, 0u);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -868,8 +870,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
           const float sg = sigm(clip15(z));
           g[k] = clipped ? 0.f : ug[k] * sg * (1.f - sg);
         }
+        // columns 8-15 of G5 are always 0: zeroed once in shared memory; in the TMEM A region
+        // they keep the previous operand's finite values, which meet zero-padded Wc2 rows
         put8(sg5, row, 0, g);
-        put8(sg5, row, 8, g + 8);
         // sigma path of the density raw gradient (field.cpp:313)
         sm.gsig[row] = (sm.dmask[row] & 1u) ? 0.f : up.x * expf(sm.sig_raw[row]);
       }
