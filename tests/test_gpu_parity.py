@@ -402,3 +402,20 @@ def test_occupancy_update_matches_reference_stream(warmup):
             assert np.mean(bg == bo) > 0.995, (g, c, np.mean(bg == bo))
             mixed |= 0 < bo.mean() < 1
     assert mixed
+
+
+def test_train_step_nmax_8192(impl):
+    """N_max = 8192 (the paper's setting, SURVEY §8 notation): finest levels far beyond the
+    table, so every level above the dense ones hashes; losses and gradients within the bars."""
+    cfg = small_cfg(1, 1, table_log2=14, levels=16, nmax=8192, divisor=96)
+    ctx, orc, _ = _pair(cfg, table_scale=0.5)
+    from .helpers import params_for
+    o, d, gt, img = _rays(cfg, 1500, "independent", seed=21)
+    p0 = [params_for(cfg, 0, table_scale=0.5)]
+    sg = ctx.train_step(o, d, gt, img, step=0)
+    so = orc.train_step(o, d, gt, img, 0)
+    _check_losses(sg, so)
+    shapes, modes, rows = ctx.grid_levels(0, 0)
+    assert shapes.max() >= 8000 and modes[-1] == 1
+    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, "trained")],
+                  adam_frac=0.999 if impl == "ffma" else 0.99)
