@@ -1610,8 +1610,10 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   mark(c, 5);
   c->launches += 3;
   // X2: partial exchange (alias on a single rank)
-  CU(cudaStreamSynchronize(s));  // pair counts on the host
-  if (pair_pin) std::memcpy(pair_cnt.data(), pair_pin, pair_cnt.size() * 4);
+  if (P > 1) {
+    CU(cudaStreamSynchronize(s));  // pair counts on the host
+    if (pair_pin) std::memcpy(pair_cnt.data(), pair_pin, pair_cnt.size() * 4);
+  }
   const PartialRec* recv = c->send_buf.as<PartialRec>();
   const float4* recv_x = nullptr;
   if (P > 1) {
