@@ -128,7 +128,7 @@ __device__ __forceinline__ uint32_t sample_field(const FieldLaunch& f, uint64_t 
 }
 
 // Normalised position of sample s: from the per-sample cache (PC) or re-derived from
-// (item, t) exactly as k_sample_points does (grid.cpp:109 normalisation).
+// (item, t) exactly as the march fill does (grid.cpp:109 normalisation).
 template <bool PC>
 __device__ __forceinline__ void load_point(const FieldLaunch& f, uint64_t s, const FieldDesc& fd,
                                            double p[3]) {

@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(32 * kFillWarps) k_march_fill(const PartDesc* 
                                                                const uint8_t* __restrict__ occ,
                                                                uint32_t n_items, ItemArrays it,
                                                                SampleArrays sm, double step, uint64_t seed,
-                                                               uint64_t batch_id, int jitter) {
+                                                               uint64_t batch_id, int jitter, uint32_t n_fine) {
   __shared__ uint32_t s_excl[kFillWarps][kMaxRuns];  // exclusive prefix of the run counts
   __shared__ uint32_t s_out[kFillWarps][kMaxRuns];   // output slot of the run's first sample
   __shared__ long long s_k0[kFillWarps][kMaxRuns];
@@ -250,6 +250,15 @@ __global__ void __launch_bounds__(32 * kFillWarps) k_march_fill(const PartDesc* 
     sm.t[o] = t;
     sm.delta[o] = smin(step, dsub(s_hi[w][lo], dsub(t, half)));
     sm.item[o] = i;
+    if (sm.p) {  // the per-sample position cache (normalised once, here, from the same t)
+      const PartDesc& pd = parts[it.part[i]];
+      const bool coarse = o >= n_fine;
+      double pp[3];
+      normalized_point(coarse ? pd.coarse_lo : pd.fine_lo, coarse ? pd.coarse_hi : pd.fine_hi, r.o, r.d, t, pp);
+      sm.p[o] = pp[0];
+      sm.p[sm.pn + o] = pp[1];
+      sm.p[2 * sm.pn + o] = pp[2];
+    }
   }
 }
 
@@ -271,26 +280,15 @@ __global__ void k_march_fill_walk(const PartDesc* __restrict__ parts, const uint
     sm.t[s] = t;
     sm.delta[s] = delta;
     sm.item[s] = i;
+    if (sm.p) {
+      double pp[3];
+      normalized_point(casc ? pd.coarse_lo : pd.fine_lo, casc ? pd.coarse_hi : pd.fine_hi, r.o, r.d, t, pp);
+      sm.p[s] = pp[0];
+      sm.p[sm.pn + s] = pp[1];
+      sm.p[2 * sm.pn + s] = pp[2];
+    }
   };
   cascade_march(pd, occ, r.o, r.d, it.te[i], it.tx[i], step, offset, fa, fb, emit);
-}
-
-// Per-sample normalised field position (grid.cpp:109 normalisation, fp64 bit-exact), written
-// once, coalesced, so every encode pass reads 24 B instead of re-deriving it from (item, t).
-__global__ void k_sample_points(const PartDesc* __restrict__ parts, ItemArrays it, SampleArrays sm,
-                                uint32_t n_fine) {
-  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= sm.pn) return;
-  const uint32_t i = __ldg(sm.item + s);
-  const PartDesc& pd = parts[it.part[i]];
-  const RayRec& r = it.rec[i];
-  const bool coarse = s >= n_fine;
-  double p[3];
-  normalized_point(coarse ? pd.coarse_lo : pd.fine_lo, coarse ? pd.coarse_hi : pd.fine_hi, r.o, r.d,
-                   __ldg(sm.t + s), p);
-  sm.p[s] = p[0];
-  sm.p[sm.pn + s] = p[1];
-  sm.p[2 * sm.pn + s] = p[2];
 }
 
 // Visit an item's samples in t order: coarse-before, fine, coarse-after.
@@ -848,11 +846,9 @@ void launch_march_fill(const PartDesc* parts, const uint8_t* occ, uint32_t n_ite
                        uint64_t batch_id, int jitter, cudaStream_t s) {
   if (!n_items) return;
   k_march_fill<<<blocks((uint64_t)n_items * 32, 32 * kFillWarps), 32 * kFillWarps, 0, s>>>(
-      parts, occ, n_items, it, sm, step, seed, batch_id, jitter);
+      parts, occ, n_items, it, sm, step, seed, batch_id, jitter, n_fine);
   k_march_fill_walk<<<blocks(n_items, 128), 128, 0, s>>>(parts, occ, n_items, it, sm, step, seed, batch_id,
                                                          jitter);
-  if (sm.pn && sm.p)
-    k_sample_points<<<(unsigned)((sm.pn + 255) / 256), 256, 0, s>>>(parts, it, sm, n_fine);
 }
 
 void launch_composite(uint32_t n_items, ItemArrays it, SampleArrays sm, uint32_t,

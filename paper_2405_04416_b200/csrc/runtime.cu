@@ -799,7 +799,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   SampleArrays sm = sample_arrays(c);
   launch_march_fill(c->d_parts.as<PartDesc>(), c->occ.as<uint8_t>(), NI, it, sm, c->n_fine,
                     c->step, c->cfg.seed, batch_id, train, s);
-  c->launches += c->enc_pcache ? 3 : 2;  // march fill (runs + overflow walk) (+ sample points)
+  c->launches += 2;  // march fill (runs, with the position cache) + overflow walk
   // tile tables
   std::vector<uint32_t> tf(2 * nl + 1, 0), tb(2 * nl + 1, 0);
   for (uint32_t f = 0; f < 2 * nl; ++f) {
