@@ -1,6 +1,6 @@
 """Diagnostic: where does the level-0 gradient mismatch of multi-partition steps come from?"""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from oracle.bindings import OracleRun, OracleModel
 from paper_2405_04416_b200 import dg, workloads

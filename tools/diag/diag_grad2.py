@@ -1,6 +1,6 @@
 """Bisect the level-0 gradient mismatch of test_train_step_parity[2-1-independent-2048-init]."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from oracle.bindings import OracleRun, OracleModel
 from paper_2405_04416_b200 import dg, workloads

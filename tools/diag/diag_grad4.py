@@ -1,6 +1,6 @@
 """Gradient precision by state: reference init (ReLU kinks everywhere) vs a kink-free state."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from oracle.bindings import OracleRun
 from paper_2405_04416_b200 import dg, workloads
