@@ -35,6 +35,9 @@ def test_segments_bit_exact(kx, ky, gen):
     d[:4] = [[0.0, 0.0, -1.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]]
     d[4:8] = [[-1.0, 0.0, 0.0], [0.6, 0.8, 0.0], [0.0, -0.6, -0.8], [0.0, 0.0, -1.0]]
     o[7] = [kx + 5.0, 0.5, 0.5]  # misses the box
+    # rays running exactly on partition planes / plane intersections, and grazing a box face
+    o[8:12] = [[1.0, 0.5, 2.0], [1.0, 1.0, 2.0], [0.25, 1.0, 2.0], [0.0, 0.3, 2.0]]
+    d[8:12] = [[0.0, 0.0, -1.0]] * 4
     ctx = dg.Context(cfg, device=0)
     ns_g, reg_g, te_g, tx_g = ctx.segment_rays(o, d)
     ns_o, reg_o, te_o, tx_o = OracleModel(cfg).segment_rays(o, d)
