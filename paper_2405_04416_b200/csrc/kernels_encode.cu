@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __rest
 
 template <bool PC>
 #ifndef ENC_BWD_MINB
-#define ENC_BWD_MINB 1
+#define ENC_BWD_MINB 5  // 5 CTAs per SM (48 registers, 16 B of spills): ~1 % faster than 4
 #endif
 __global__ void __launch_bounds__(256, ENC_BWD_MINB) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
   const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
