@@ -267,6 +267,8 @@ def main():
     ap.add_argument("--render-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="weak", choices=["weak", "C1", "C2", "C3", "C4", "C5"],
+                    help="weak: the C4 weak-scaling point (default); C1..C5: a BASELINE config whole")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
                     help="exchange backend for N > 1: NCCL all-to-all-v, or peer-memory pack kernels")
     ap.add_argument("--no-cpu-stages", action="store_true", help="skip the all-core stage baseline")
@@ -287,7 +289,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", rank=rank, world_size=world,
                                 device_id=torch.device("cuda", local))
-    wl = workloads.weak(world, rays_per_gpu=args.rays_per_gpu, table_log2=args.table_log2)
+    if args.workload == "weak":
+        wl = workloads.weak(world, rays_per_gpu=args.rays_per_gpu, table_log2=args.table_log2)
+    else:  # a BASELINE config as a whole on `world` GPUs (partition p on rank p % world)
+        wl = workloads.by_name(args.workload)
+        args.no_cpu = True
     cfg = wl.cfg
     B = wl.n_rays
     shard = B // world

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -121,10 +122,14 @@ void launch_items_to_records(uint32_t n, const float4* partial, const float* dep
 // One encode pass: levels [l0, l1) restricted to row slice k of S of each level's table, so
 // the tables a pass touches stay L2-resident (random rows of a 128 MB table miss L2; a
 // 64 MB slice does not).  Slice bounds are even, so a float4 row pair never straddles two.
+// One encode pass: levels [l0, l1) of field f, row slice k of S (a slice's table rows fit the
+// pass's L2 budget); the pass covers only field f's samples.
 struct EncPass {
   uint8_t l0, l1, k, S;
+  uint8_t f, pad0, pad1, pad2;
 };
-constexpr int kMaxEncPass = 96;
+constexpr int kMaxEncPass = 256;  // per launch; longer pass lists are launched in chunks
+constexpr uint8_t kAllFields = 0xff;  // EncPass.f: every local field's samples in one pass
 
 struct FieldLaunch {
   const FieldDesc* fields;     // [2][n_local] (cascade-major)
@@ -149,8 +154,8 @@ struct FieldLaunch {
 };
 // Forward: one launch per slice index (slice k > 0 adds into X written by slice 0); returns
 // the number of launches.  Backward: one launch over every pass (reds commute).
-int launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s);
-int launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s);
+int launch_encode_fwd(const FieldLaunch& f, const std::vector<EncPass>& passes, float* X, cudaStream_t s);
+int launch_encode_bwd(const FieldLaunch& f, const std::vector<EncPass>& passes, const float* dX, cudaStream_t s);
 // stand-alone points variant (stage entry points): all points belong to one field
 void launch_encode_points(const FieldDesc* field, const float* params, const double* pts,
                           uint64_t n, uint32_t levels, float* X, uint32_t* rows, cudaStream_t s);

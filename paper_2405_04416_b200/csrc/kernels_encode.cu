@@ -12,6 +12,7 @@
 //
 // Algorithmic traffic: 8 corners x L levels x 8 B = 1024 B/sample gathered
 // forward; the backward read-modify-writes the same 1024 B.
+#include <algorithm>
 #include <cstdlib>
 
 #include "encode_common.cuh"
@@ -148,12 +149,14 @@ __device__ __forceinline__ void load_point(const FieldLaunch& f, uint64_t s, con
 // Slice k > 0 of a level runs in a later launch and adds into X.  The sample's normalised
 // position (fp64, bit-exact) comes from the march, so a pass is: 3 streaming loads, the
 // lattice math, 8 gathers.
-template <bool PC>
+// ALL: every pass of the launch covers every local field's samples (one partition per GPU);
+// otherwise each pass covers one field's samples (several partitions per GPU).
+template <bool PC, bool ALL>
 __global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __restrict__ X) {
-  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= f.n_total) return;
   const EncPass ps = f.pass[blockIdx.y];
-  const FieldDesc& fd = f.fields[sample_field(f, s)];
+  const uint64_t s = (ALL ? 0ull : (uint64_t)f.field_off[ps.f]) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= (ALL ? (uint64_t)f.n_total : (uint64_t)f.field_off[ps.f + 1])) return;
+  const FieldDesc& fd = f.fields[ALL ? sample_field(f, s) : ps.f];
   double p[3];
   load_point<PC>(f, s, fd, p);
   for (uint32_t l = ps.l0; l < ps.l1; ++l) {
@@ -171,15 +174,15 @@ __global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __rest
   }
 }
 
-template <bool PC>
 #ifndef ENC_BWD_MINB
 #define ENC_BWD_MINB 5  // 5 CTAs per SM (48 registers, 16 B of spills): ~1 % faster than 4
 #endif
+template <bool PC, bool ALL>
 __global__ void __launch_bounds__(256, ENC_BWD_MINB) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
-  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = s < f.n_total;
   const EncPass ps = f.pass[blockIdx.y];
-  const uint32_t fidx = valid ? sample_field(f, s) : 0u;
+  const uint64_t s = (ALL ? 0ull : (uint64_t)f.field_off[ps.f]) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = s < (ALL ? (uint64_t)f.n_total : (uint64_t)f.field_off[ps.f + 1]);
+  const uint32_t fidx = ALL ? (valid ? sample_field(f, s) : 0u) : ps.f;
   double p[3] = {0.0, 0.0, 0.0};
   const FieldDesc& fd = f.fields[fidx];
   if (valid) load_point<PC>(f, s, fd, p);
@@ -235,49 +238,66 @@ inline dim3 grid_lv(uint64_t n, uint32_t L) { return dim3((unsigned)((n + 255) /
 
 }  // namespace
 
-int launch_encode_fwd(const FieldLaunch& f, float* X, cudaStream_t s) {
-  if (!f.n_total || !f.n_pass) return 0;
-  const unsigned nb = (unsigned)((f.n_total + 255) / 256);
+namespace {
+// CTAs along x for a chunk of passes: the largest field among them
+unsigned pass_blocks(const FieldLaunch& f, const EncPass* p, uint32_t n) {
+  uint64_t m = 0;
+  for (uint32_t i = 0; i < n; ++i)
+    m = std::max<uint64_t>(m, p[i].f == kAllFields ? (uint64_t)f.n_total : f.field_off[p[i].f + 1] - f.field_off[p[i].f]);
+  return (unsigned)((m + 255) / 256);
+}
+}  // namespace
+
+int launch_encode_fwd(const FieldLaunch& f, const std::vector<EncPass>& passes, float* X, cudaStream_t s) {
+  if (!f.n_total || passes.empty()) return 0;
+  static const bool split = std::getenv("DG_ENC_SPLIT_LAUNCH") != nullptr;  // per-pass timing
   int launches = 0;
-  for (uint32_t k = 0;; ++k) {  // slice k of every pass group, in pass order
-    FieldLaunch g = f;
-    g.n_pass = 0;
-    for (uint32_t i = 0; i < f.n_pass; ++i)
-      if (f.pass[i].k == k) g.pass[g.n_pass++] = f.pass[i];
-    if (!g.n_pass) break;
-    static const bool split = std::getenv("DG_ENC_SPLIT_LAUNCH") != nullptr;  // per-pass timing
-    for (uint32_t i = 0; i < (split ? g.n_pass : 1u); ++i) {
-      FieldLaunch h = g;
-      if (split) {
-        h.n_pass = 1;
-        h.pass[0] = g.pass[i];
+  for (uint32_t k = 0;; ++k) {  // slice k of every pass group, in pass order (k > 0 adds into X)
+    std::vector<EncPass> pk;
+    for (const EncPass& p : passes)
+      if (p.k == k) pk.push_back(p);
+    if (pk.empty()) break;
+    const uint32_t chunk = split ? 1u : (uint32_t)kMaxEncPass;
+    for (uint32_t i = 0; i < pk.size(); i += chunk) {
+      FieldLaunch h = f;
+      h.n_pass = std::min<uint32_t>(chunk, (uint32_t)pk.size() - i);
+      for (uint32_t j = 0; j < h.n_pass; ++j) h.pass[j] = pk[i + j];
+      const dim3 grid(pass_blocks(h, h.pass, h.n_pass), h.n_pass);
+      const bool all = h.pass[0].f == kAllFields;  // a pass list is all-fields or per-field
+      if (f.s_p) {
+        if (all) k_encode_fwd<true, true><<<grid, 256, 0, s>>>(h, X);
+        else k_encode_fwd<true, false><<<grid, 256, 0, s>>>(h, X);
+      } else {
+        if (all) k_encode_fwd<false, true><<<grid, 256, 0, s>>>(h, X);
+        else k_encode_fwd<false, false><<<grid, 256, 0, s>>>(h, X);
       }
-      if (f.s_p) k_encode_fwd<true><<<dim3(nb, h.n_pass), 256, 0, s>>>(h, X);
-      else k_encode_fwd<false><<<dim3(nb, h.n_pass), 256, 0, s>>>(h, X);
       ++launches;
     }
   }
   return launches;
 }
 
-int launch_encode_bwd(const FieldLaunch& f, const float* dX, cudaStream_t s) {
-  if (!f.n_total || !f.n_pass) return 0;
+int launch_encode_bwd(const FieldLaunch& f, const std::vector<EncPass>& passes, const float* dX, cudaStream_t s) {
+  if (!f.n_total || passes.empty()) return 0;
   static const bool split = std::getenv("DG_ENC_SPLIT_LAUNCH") != nullptr;  // per-pass timing
-  if (split) {
-    for (uint32_t i = 0; i < f.n_pass; ++i) {
-      FieldLaunch g = f;
-      g.n_pass = 1;
-      g.pass[0] = f.pass[i];
-      const dim3 grid1((unsigned)((f.n_total + 255) / 256), 1);
-      if (f.s_p) k_encode_bwd<true><<<grid1, 256, 0, s>>>(g, dX);
-      else k_encode_bwd<false><<<grid1, 256, 0, s>>>(g, dX);
+  const uint32_t chunk = split ? 1u : (uint32_t)kMaxEncPass;
+  int launches = 0;
+  for (uint32_t i = 0; i < passes.size(); i += chunk) {  // reds commute: any grouping
+    FieldLaunch h = f;
+    h.n_pass = std::min<uint32_t>(chunk, (uint32_t)passes.size() - i);
+    for (uint32_t j = 0; j < h.n_pass; ++j) h.pass[j] = passes[i + j];
+    const dim3 grid(pass_blocks(h, h.pass, h.n_pass), h.n_pass);
+    const bool all = h.pass[0].f == kAllFields;
+    if (f.s_p) {
+      if (all) k_encode_bwd<true, true><<<grid, 256, 0, s>>>(h, dX);
+      else k_encode_bwd<true, false><<<grid, 256, 0, s>>>(h, dX);
+    } else {
+      if (all) k_encode_bwd<false, true><<<grid, 256, 0, s>>>(h, dX);
+      else k_encode_bwd<false, false><<<grid, 256, 0, s>>>(h, dX);
     }
-    return int(f.n_pass);
+    ++launches;
   }
-  const dim3 grid((unsigned)((f.n_total + 255) / 256), f.n_pass);
-  if (f.s_p) k_encode_bwd<true><<<grid, 256, 0, s>>>(f, dX);
-  else k_encode_bwd<false><<<grid, 256, 0, s>>>(f, dX);
-  return 1;
+  return launches;
 }
 
 void launch_encode_points(const FieldDesc* field, const float* params, const double* pts,

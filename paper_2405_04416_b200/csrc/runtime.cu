@@ -816,7 +816,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   return DG_OK;
 }
 
-FieldLaunch field_launch(dg_ctx* c, uint64_t budget) {
+FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passes) {
   FieldLaunch f{};
   f.fields = c->d_fields.as<FieldDesc>();
   f.parts = c->d_parts.as<PartDesc>();
@@ -828,25 +828,37 @@ FieldLaunch field_launch(dg_ctx* c, uint64_t budget) {
   f.n_total = c->n_fine + c->n_coarse;
   f.n_local = uint32_t(c->local.size());
   f.levels = c->cfg.grid_levels;
-  // Passes: runs of consecutive levels whose tables (summed over the local fields) fit the
-  // slice budget go together; a larger level is cut into S row slices of <= budget each.
-  // Measured on B200 (tools/ubench/l2_random.cu): random float2 gathers / reds run 2.2x /
-  // 3.5x faster on a 64 MB table than on a 128 MB one.
-  auto level_bytes = [&](uint32_t l) {
-    uint64_t b = 0;
-    for (const FieldDesc& fd : c->fields) b += uint64_t(fd.lv[l].rows) * 8;
-    return b;
-  };
-  f.n_pass = 0;
-  for (uint32_t l = 0; l < f.levels;) {
-    uint32_t l1 = l + 1;
-    uint64_t bytes = level_bytes(l);
-    while (l1 < f.levels && bytes + level_bytes(l1) <= budget) bytes += level_bytes(l1++);
-    const uint32_t S = std::min<uint64_t>(8, std::max<uint64_t>(1, (bytes + budget - 1) / budget));
-    for (uint32_t k = 0; k < S && f.n_pass < kMaxEncPass; ++k)
-      f.pass[f.n_pass++] = EncPass{uint8_t(l), uint8_t(l1), uint8_t(k), uint8_t(S)};
-    l = l1;
+  // Passes, per field (a partition's fine or coarse sub-field) that has samples: runs of
+  // consecutive levels whose tables fit the slice budget go together; a larger level is cut
+  // into S row slices of <= budget each.  Each pass covers only its field's samples, so with
+  // several partitions on a GPU the L2 working set is still one table slice.  Measured on
+  // B200 (tools/ubench/l2_random.cu): random float2 gathers / reds run 2.2x / 3.5x faster on
+  // a 64 MB table than on a 128 MB one.
+  // With a single partition per GPU (the fine + coarse fields of one region) one pass covers
+  // both fields' samples (kAllFields), as measured fastest there.
+  passes.clear();
+  const uint32_t nf = uint32_t(c->field_off.size() - 1);
+  const bool merged = c->local.size() == 1;
+  for (uint32_t fi = 0; fi < (merged ? 1u : nf); ++fi) {
+    if (!merged && c->field_off[fi + 1] == c->field_off[fi]) continue;  // no samples in this field
+    auto level_bytes = [&](uint32_t l) {
+      if (!merged) return uint64_t(c->fields[fi].lv[l].rows) * 8;
+      uint64_t b = 0;
+      for (const FieldDesc& fd : c->fields) b += uint64_t(fd.lv[l].rows) * 8;
+      return b;
+    };
+    for (uint32_t l = 0; l < f.levels;) {
+      uint32_t l1 = l + 1;
+      uint64_t bytes = level_bytes(l);
+      while (l1 < f.levels && bytes + level_bytes(l1) <= budget) bytes += level_bytes(l1++);
+      const uint32_t S = std::min<uint64_t>(64, std::max<uint64_t>(1, (bytes + budget - 1) / budget));
+      for (uint32_t k = 0; k < S; ++k)
+        passes.push_back(EncPass{uint8_t(l), uint8_t(l1), uint8_t(k), uint8_t(S),
+                                 merged ? kAllFields : uint8_t(fi), 0, 0, 0});
+      l = l1;
+    }
   }
+  f.n_pass = 0;
   // warp aggregation where ~1.5+ consecutive samples share a cell: cell = extent / n vs. step
   const FieldDesc& f0 = c->fields[0];
   uint32_t agg = 0;
@@ -1600,7 +1612,11 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   }
   CU(cudaMemsetAsync(c->loss.p, 0, sizeof(LossAccum), s));
   // K3 / K4 forward
-  c->launches += launch_encode_fwd(field_launch(c, c->enc_budget_fwd), sm.X, s) - 1;
+  {
+    std::vector<EncPass> passes;
+    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes);
+    c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
+  }
   mark(c, 3);
   const MlpLaunch mf = mlp_launch(c, false);
   if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);
@@ -1635,7 +1651,11 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
     launch_mlp_bwd(mlp_launch(c, true), c->num_sms, s);
   }
   mark(c, 8);
-  c->launches += launch_encode_bwd(field_launch(c, c->enc_budget_bwd), sm.dX, s) - 1;
+  {
+    std::vector<EncPass> passes;
+    const FieldLaunch fl = field_launch(c, c->enc_budget_bwd, passes);
+    c->launches += launch_encode_bwd(fl, passes, sm.dX, s) - 1;
+  }
   mark(c, 9);
   c->launches += 3;
   // K6 Adam over every local parameter, lr at the pre-increment step (worker.cpp:544)
@@ -1708,7 +1728,11 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   const uint32_t NI = c->n_items;
   ItemArrays it = item_arrays(c);
   SampleArrays sm = sample_arrays(c);
-  c->launches += launch_encode_fwd(field_launch(c, c->enc_budget_fwd), sm.X, s) - 1;
+  {
+    std::vector<EncPass> passes;
+    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes);
+    c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
+  }
   MlpLaunch mf = mlp_launch(c, false);
   mf.app_override = c->eval_app.as<float>();
   if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);
