@@ -123,9 +123,10 @@ class _LocalOnly:
             self.ctx.set_occupancy(g, c, bits)
 
 
-@pytest.mark.parametrize("backend", ["host", "peer"])
+@pytest.mark.parametrize("backend,world", [("host", 2), ("peer", 2), ("peer", 3)])
 @pytest.mark.parametrize("cross", [0, 1])
-def test_two_ranks_match_single_rank(cross, backend):
+def test_two_ranks_match_single_rank(cross, backend, world):
+    """world = 3 puts partitions {0, 3}, {1}, {2} on the three ranks (uneven ownership)."""
     from paper_2405_04416_b200 import dg
     cfg = _cfg(cross)
     ctx = dg.Context(cfg, device=0)
@@ -151,7 +152,8 @@ def test_two_ranks_match_single_rank(cross, backend):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
         s.close()
-        procs = [mpc.Process(target=_rank_main, args=(r, 2, port, path, errq, cross, backend)) for r in range(2)]
+        procs = [mpc.Process(target=_rank_main, args=(r, world, port, path, errq, cross, backend))
+                 for r in range(world)]
         for p in procs:
             p.start()
         for p in procs:
