@@ -123,10 +123,11 @@ class _LocalOnly:
             self.ctx.set_occupancy(g, c, bits)
 
 
-@pytest.mark.parametrize("backend,world", [("host", 2), ("peer", 2), ("peer", 3)])
+@pytest.mark.parametrize("backend,world", [("host", 2), ("peer", 2), ("peer", 3), ("peer", 4)])
 @pytest.mark.parametrize("cross", [0, 1])
 def test_two_ranks_match_single_rank(cross, backend, world):
-    """world = 3 puts partitions {0, 3}, {1}, {2} on the three ranks (uneven ownership)."""
+    """world = 3 puts partitions {0, 3}, {1}, {2} on the three ranks (uneven ownership); world = 4
+    is the deployment layout, one partition per rank."""
     from paper_2405_04416_b200 import dg
     cfg = _cfg(cross)
     ctx = dg.Context(cfg, device=0)
