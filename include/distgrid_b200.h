@@ -363,6 +363,12 @@ int dg_last_item_data(dg_ctx* ctx, uint32_t partition, uint64_t* ray_id, uint8_t
                       double* t_enter, double* t_exit, uint32_t* n_samples);
 /* per item samples in t order (concatenated in item order): t, delta, cascade */
 int dg_last_samples(dg_ctx* ctx, uint32_t partition, double* t, double* delta, uint8_t* cascade);
+/* per sample of the last training step, in dg_last_samples order (each output optional):
+ * normalised field position [n][3] (worker.cpp:46), encoded features [n][2L], field output
+ * [n][4] (sigma, rgb), compositing upstream [n][4] (dsigma, drgb), features gradient [n][2L],
+ * the forward's ReLU / clip mask words [n][7] (tcgen05 path) */
+int dg_last_sample_data(dg_ctx* ctx, uint32_t partition, double* pos, float* features,
+                        float* field_out, float* upstream, float* d_features, uint32_t* masks);
 /* per item own partial (rgb, T) as computed by the composite kernel */
 int dg_last_partials(dg_ctx* ctx, uint32_t partition, float* rgb, float* transmittance);
 /* launches of this library's kernels since the context was created */

@@ -61,6 +61,11 @@ def oracle_lib():
         lib.or_run_occ_bits.argtypes = [P, C.c_uint32, C.c_uint32]
         lib.or_run_set_occupancy.argtypes = [P, C.c_uint32, C.c_uint32, P]
         lib.or_run_train_step.argtypes = [P, P, P, P, P, C.c_uint64, C.c_uint64, P]
+        lib.or_run_sample_log.argtypes = [P, C.c_int32, P, C.c_uint64]
+        lib.or_run_mask_override.argtypes = [P, C.c_uint32, P, C.c_uint64]
+        lib.or_run_override_stats.argtypes = [P, P, P]
+        lib.or_run_sample_log_count.argtypes = [P]
+        lib.or_run_sample_log_count.restype = C.c_uint64
         lib.or_run_eval_rays.argtypes = [P, P, P, C.c_uint64, P, P, P, P]
         lib.or_last_error.restype = C.c_char_p
         lib.or_run_model.restype = P
@@ -187,6 +192,45 @@ class OracleRun(_RunBase):
     def occupancy(self, g, cascade, ncells):
         return self._arr(self.lib.or_run_occ_bits(self.h, g, cascade), ncells).copy()
 
+    def log_samples(self, g, capacity):
+        """Record every training sample of partition g in the next train_step (test-only):
+        sample_log() then returns (pos, features, field_out, upstream, d_features) in the GPU's
+        dg_last_sample_data order."""
+        self._slog = np.zeros((capacity, 96))
+        self.lib.or_run_sample_log(self.h, g, _ptr(self._slog), capacity)
+
+    def sample_log(self):
+        n = int(self.lib.or_run_sample_log_count(self.h))
+        L2 = 2 * self.cfg.grid_levels
+        r = self._slog[:n]
+        return r[:, 0:3], r[:, 3:3 + L2], r[:, 35:39], r[:, 39:43], r[:, 43:43 + L2]
+
+    def mask_override(self, g, words):
+        """Test-only: the ReLU decisions [n, 6] (h1 lo/hi, c1 lo/hi, c2 lo/hi 32-bit words) of
+        partition g's training samples in the next train_step(s), in sample-log order (None: off).
+        See gpu_mask_words for the GPU's mask layout."""
+        keep = self.__dict__.setdefault("_movr", {})
+        if words is None:
+            keep.pop(g, None)
+            self.lib.or_run_mask_override(self.h, g, None, 0)
+            return
+        keep[g] = np.ascontiguousarray(words, dtype=np.uint32)
+        self.lib.or_run_mask_override(self.h, g, _ptr(keep[g]), len(words))
+
+    def override_stats(self):
+        """(units whose overridden decision went against the sign of z, their largest |z|) over
+        the last train_step."""
+        n, z = C.c_uint64(), C.c_double()
+        self.lib.or_run_override_stats(self.h, C.byref(n), C.byref(z))
+        return n.value, z.value
+
+    def sample_log_masks(self):
+        """ReLU signs (h1 lo/hi, c1 lo/hi, c2 lo/hi 32-bit words) and the smallest |pre-activation|
+        of h1, c1, c2 per logged sample."""
+        n = int(self.lib.or_run_sample_log_count(self.h))
+        r = self._slog[:n]
+        return r[:, 75:81].astype(np.uint32), r[:, 81:84]
+
     def train_step(self, o, d, gt, img, step):
         stats = np.zeros(8)
         gt64 = np.ascontiguousarray(gt, dtype=np.float64)
@@ -296,6 +340,45 @@ class RefRun(_RunBase):
         self.lib.refh_get_occupancy(self.h, g, cascade, _ptr(bits), None)
         return bits
 
+    def log_samples(self, g, capacity):
+        """Record every training sample of partition g in the next train_step (test-only):
+        sample_log() then returns (pos, features, field_out, upstream, d_features) in the GPU's
+        dg_last_sample_data order."""
+        self._slog = np.zeros((capacity, 96))
+        self.lib.or_run_sample_log(self.h, g, _ptr(self._slog), capacity)
+
+    def sample_log(self):
+        n = int(self.lib.or_run_sample_log_count(self.h))
+        L2 = 2 * self.cfg.grid_levels
+        r = self._slog[:n]
+        return r[:, 0:3], r[:, 3:3 + L2], r[:, 35:39], r[:, 39:43], r[:, 43:43 + L2]
+
+    def mask_override(self, g, words):
+        """Test-only: the ReLU decisions [n, 6] (h1 lo/hi, c1 lo/hi, c2 lo/hi 32-bit words) of
+        partition g's training samples in the next train_step(s), in sample-log order (None: off).
+        See gpu_mask_words for the GPU's mask layout."""
+        keep = self.__dict__.setdefault("_movr", {})
+        if words is None:
+            keep.pop(g, None)
+            self.lib.or_run_mask_override(self.h, g, None, 0)
+            return
+        keep[g] = np.ascontiguousarray(words, dtype=np.uint32)
+        self.lib.or_run_mask_override(self.h, g, _ptr(keep[g]), len(words))
+
+    def override_stats(self):
+        """(units whose overridden decision went against the sign of z, their largest |z|) over
+        the last train_step."""
+        n, z = C.c_uint64(), C.c_double()
+        self.lib.or_run_override_stats(self.h, C.byref(n), C.byref(z))
+        return n.value, z.value
+
+    def sample_log_masks(self):
+        """ReLU signs (h1 lo/hi, c1 lo/hi, c2 lo/hi 32-bit words) and the smallest |pre-activation|
+        of h1, c1, c2 per logged sample."""
+        n = int(self.lib.or_run_sample_log_count(self.h))
+        r = self._slog[:n]
+        return r[:, 75:81].astype(np.uint32), r[:, 81:84]
+
     def train_step(self, o, d, gt, img, step):
         stats = np.zeros(8)
         gt64 = np.ascontiguousarray(gt, dtype=np.float64)
@@ -372,6 +455,17 @@ class RefRun(_RunBase):
         out = np.zeros(self.nparams(g))
         self.lib.refh_stage_grads(self.h, g, _ptr(out), int(zero))
         return out
+
+
+def gpu_mask_words(masks):
+    """The GPU's per-sample mask words [n, 7] (kernels_mlp_tc.cu k_mlp_fwd_tc: words 0-3 = h1 |
+    c1 << 16 of 16-column part p, 4-5 = c2) -> the oracle's [n, 6] (h1, c1, c2 lo/hi)."""
+    m = np.asarray(masks, dtype=np.uint64)
+    lo16 = lambda w: m[:, w] & 0xffff
+    hi16 = lambda w: m[:, w] >> 16
+    out = np.stack([lo16(0) | (lo16(1) << 16), lo16(2) | (lo16(3) << 16),
+                    hi16(0) | (hi16(1) << 16), hi16(2) | (hi16(3) << 16), m[:, 4], m[:, 5]], 1)
+    return out.astype(np.uint32)
 
 
 def ref_segment_rays(cfg, o, d):

@@ -37,6 +37,9 @@ static inline int iclamp(int v, int lo, int hi) { return (v < lo) ? lo : ((hi < 
  * parallel array g_abs (same offsets as the grads base g_gbase).  Used to state the gradient
  * tolerance relative to sum |contributions| (the standard bound for reordered fp sums). */
 static double* g_abs = NULL;
+/* Test-only sample log (or_run_sample_log): the encoding's upstream gradient of the current
+ * field_backward call lands here when set. */
+static double* g_enc_grad_out = NULL;
 static const double* g_gbase = NULL;
 #define OR_ABS(ptr, val)                                     \
   do {                                                       \
@@ -588,6 +591,21 @@ static inline double act_grad(double z, int sigmoid) {
   return z > 0.0 ? 1.0 : 0.0;
 }
 
+/* Test-only ReLU decision override (or_run_mask_override): a unit whose pre-activation lies
+ * within fp32 noise of 0 may round to either side; with c->ovr set, the ReLU layers (h1, and
+ * c1 / c2 of the fine field) take their on/off decision from c->mask instead of the sign of z. */
+static inline int relu_on(const or_field_cache* c, int layer, int r, double z) {
+  return c->ovr ? (int)((c->mask[layer] >> r) & 1u) : z > 0.0;
+}
+static inline double act_m(const or_field_cache* c, int layer, int r, double z, int sigmoid) {
+  if (sigmoid || !c->ovr) return act(z, sigmoid);
+  return relu_on(c, layer, r, z) ? z : 0.0;
+}
+static inline double act_grad_m(const or_field_cache* c, int layer, int r, double z, int sigmoid) {
+  if (sigmoid || !c->ovr) return act_grad(z, sigmoid);
+  return relu_on(c, layer, r, z) ? 1.0 : 0.0;
+}
+
 /* One dense layer: y = b + W x, bias-first sequential dot (mlp.cpp:64-71). */
 static void dense(const double* W, const double* b, const double* x, uint32_t in, uint32_t out,
                   double* y) {
@@ -620,7 +638,7 @@ void or_field_forward(const or_field_layout* f, const double* params, const doub
   /* density MLP: [enc -> 64 ReLU -> 16] */
   dense(params + f->dw0, params + f->db0, c->enc, f->enc_width, 64, c->h1);
   double a1[64];
-  for (int r = 0; r < 64; ++r) a1[r] = act(c->h1[r], 0);
+  for (int r = 0; r < 64; ++r) a1[r] = act_m(c, 0, r, c->h1[r], 0);
   double raw[16];
   dense(params + f->dw1, params + f->db1, a1, 64, 16, raw);
   for (int k = 0; k < 16; ++k) c->draw[k] = clip_output(raw[k], &c->dclip[k]);
@@ -633,9 +651,9 @@ void or_field_forward(const or_field_layout* f, const double* params, const doub
   const int sig = f->coarse != 0;
   dense(params + f->cw0, params + f->cb0, c->cin, f->color_in, 64, c->c1);
   double a2[64], a3[64];
-  for (int r = 0; r < 64; ++r) a2[r] = act(c->c1[r], sig);
+  for (int r = 0; r < 64; ++r) a2[r] = act_m(c, 1, r, c->c1[r], sig);
   dense(params + f->cw1, params + f->cb1, a2, 64, 64, c->c2);
-  for (int r = 0; r < 64; ++r) a3[r] = act(c->c2[r], sig);
+  for (int r = 0; r < 64; ++r) a3[r] = act_m(c, 2, r, c->c2[r], sig);
   double craw[3];
   dense(params + f->cw2, params + f->cb2, a3, 64, 3, craw);
   for (int k = 0; k < 3; ++k) {
@@ -684,13 +702,13 @@ void or_field_backward(const or_field_layout* f, const double* params, double* g
     /* colour MLP backward: layers 2, 1, 0 */
     double a2[64], a3[64], d3[64], d2[64];
     for (int r = 0; r < 64; ++r) {
-      a2[r] = act(c->c1[r], sig);
-      a3[r] = act(c->c2[r], sig);
+      a2[r] = act_m(c, 1, r, c->c1[r], sig);
+      a3[r] = act_m(c, 2, r, c->c2[r], sig);
     }
     dense_backward(params + f->cw2, grads + f->cw2, grads + f->cb2, a3, draw3, 64, 3, d3);
-    for (int r = 0; r < 64; ++r) d3[r] *= act_grad(c->c2[r], sig);
+    for (int r = 0; r < 64; ++r) d3[r] *= act_grad_m(c, 2, r, c->c2[r], sig);
     dense_backward(params + f->cw1, grads + f->cw1, grads + f->cb1, a2, d3, 64, 64, d2);
-    for (int r = 0; r < 64; ++r) d2[r] *= act_grad(c->c1[r], sig);
+    for (int r = 0; r < 64; ++r) d2[r] *= act_grad_m(c, 1, r, c->c1[r], sig);
     dense_backward(params + f->cw0, grads + f->cw0, grads + f->cb0, c->cin, d2, f->color_in, 64,
                    cin_grad);
   }
@@ -705,12 +723,13 @@ void or_field_backward(const or_field_layout* f, const double* params, double* g
     }
   if (!any) return;
   double a1[64], d1[64];
-  for (int r = 0; r < 64; ++r) a1[r] = act(c->h1[r], 0);
+  for (int r = 0; r < 64; ++r) a1[r] = act_m(c, 0, r, c->h1[r], 0);
   dense_backward(params + f->dw1, grads + f->dw1, grads + f->db1, a1, draw, 64, 16, d1);
-  for (int r = 0; r < 64; ++r) d1[r] *= act_grad(c->h1[r], 0);
+  for (int r = 0; r < 64; ++r) d1[r] *= act_grad_m(c, 0, r, c->h1[r], 0);
   double enc_grad[2 * OR_MAX_LEVELS * 4];
   dense_backward(params + f->dw0, grads + f->dw0, grads + f->db0, c->enc, d1, f->enc_width, 64,
                  enc_grad);
+  if (g_enc_grad_out) memcpy(g_enc_grad_out, enc_grad, sizeof(double) * f->enc_width);
   or_encode_backward(&f->grid, grads, c->point, enc_grad);
 }
 
@@ -861,7 +880,54 @@ struct or_run {
   or_mt64 occ_rng[DG_MAX_PARTITIONS];
   uint32_t n_images;
   double* app;
+  /* test-only per-sample log of one region's training samples (or_run_sample_log) */
+  int32_t slog_region;
+  double* slog;
+  uint64_t slog_cap, slog_n;
+  /* test-only ReLU decisions per training sample of a region (or_run_mask_override) */
+  const uint32_t* movr[DG_MAX_PARTITIONS];
+  uint64_t movr_n[DG_MAX_PARTITIONS];
+  uint64_t ovr_units; /* over the last train step: decisions against the sign of z, largest |z| */
+  double ovr_max_z;
 };
+
+int or_run_mask_override(or_run* r, uint32_t region, const uint32_t* words, uint64_t n) {
+  if (region >= DG_MAX_PARTITIONS) return or_fail("mask override: region out of range");
+  r->movr[region] = words;
+  r->movr_n[region] = words ? n : 0;
+  return 0;
+}
+
+static const uint32_t* mask_ovr(const or_run* r, uint32_t g, uint64_t k) {
+  return r->movr[g] && k < r->movr_n[g] ? r->movr[g] + 6 * k : NULL;
+}
+
+void or_run_override_stats(const or_run* r, uint64_t* units, double* max_abs_z) {
+  *units = r->ovr_units;
+  *max_abs_z = r->ovr_max_z;
+}
+
+/* Count the units of one overridden sample whose decision goes against the sign of z (the
+ * ReLU layers: h1 always, c1 / c2 in the fine field). */
+static void ovr_account(or_run* r, const or_field_cache* c, int coarse) {
+  if (!c->ovr) return;
+  const double* pre[3] = {c->h1, c->c1, c->c2};
+  for (int q = 0; q < (coarse ? 1 : 3); ++q)
+    for (int u = 0; u < 64; ++u)
+      if (((c->mask[q] >> u) & 1u) != (pre[q][u] > 0.0 ? 1u : 0u)) {
+        r->ovr_units += 1;
+        r->ovr_max_z = fmax(r->ovr_max_z, fabs(pre[q][u]));
+      }
+}
+
+int or_run_sample_log(or_run* r, int32_t region, double* buf, uint64_t capacity) {
+  r->slog_region = region;
+  r->slog = buf;
+  r->slog_cap = capacity;
+  r->slog_n = 0;
+  return 0;
+}
+uint64_t or_run_sample_log_count(const or_run* r) { return r->slog_n; }
 
 const or_model* or_run_model(const or_run* r) { return &r->m; }
 double* or_run_params(or_run* r, uint32_t g) { return r->params[g]; }
@@ -994,7 +1060,7 @@ static void occupancy_update(or_run* r, uint32_t g) {
     for (int a_ = 0; a_ < 3; ++a_) pw_[a_] = or_rng_uniform_range(rng, lo_[a_], hi_[a_]);  \
     for (int a_ = 0; a_ < 3; ++a_)                                                         \
       pu_[a_] = sclamp((pw_[a_] - box->lo[a_]) / (box->hi[a_] - box->lo[a_]), 0.0, 1.0);   \
-    or_field_cache fc_;                                                                    \
+    or_field_cache fc_ = {0};                                                                 \
     const double zero3_[3] = {0.0, 0.0, 1.0};                                              \
     or_field_forward(f, params, pu_, zero3_, r->app, &fc_);                                \
     den[idx_] = smax(den[idx_] * cfg->occ_decay, fc_.sigma);                               \
@@ -1025,10 +1091,12 @@ static void occupancy_update(or_run* r, uint32_t g) {
 
 /* shade one sample (worker.cpp:35-52) */
 static void shade(or_run* r, uint32_t g, int cascade, const or_dray* dr, double t,
-                  const double* app, or_field_cache* fc) {
+                  const double* app, or_field_cache* fc, const uint32_t* ovr) {
   const or_box* box = cascade == 0 ? &r->m.fine[g] : &r->m.coarse[g];
   double p[3];
   or_normalized_point(box, dr->o, dr->d, t, p);
+  fc->ovr = ovr != NULL;
+  for (int q = 0; q < 3 && ovr; ++q) fc->mask[q] = (uint64_t)ovr[2 * q] | ((uint64_t)ovr[2 * q + 1] << 32);
   const double* params = r->params[g] + (cascade == 0 ? 0 : r->m.field[g][0].size);
   or_field_forward(&r->m.field[g][cascade], params, p, dr->d, app, fc);
 }
@@ -1045,6 +1113,8 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
   if (cfg->distortion_cross_correction) return or_fail("oracle: cross correction unsupported");
   or_dray* rays = (or_dray*)calloc(n ? n : 1, sizeof(or_dray));
   uint64_t dropped = 0;
+  r->ovr_units = 0;
+  r->ovr_max_z = 0.0;
   /* plan_batch (worker.cpp:141-165) + wire rounding (wire.cpp:29-46) */
   for (uint64_t i = 0; i < n; ++i) {
     or_dray* d = &rays[i];
@@ -1079,6 +1149,7 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
   double loss_rgb[DG_MAX_PARTITIONS], loss_t[DG_MAX_PARTITIONS], loss_d[DG_MAX_PARTITIONS];
   /* Phase 1 for every worker (independent across workers). */
   for (uint32_t g = 0; g < m->P && rc == 0; ++g) {
+    uint64_t ks = 0; /* the region's sample ordinal (mask override index) */
     for (uint64_t i = 0; i < n; ++i) {
       const or_dray* d = &rays[i];
       int mo = -1;
@@ -1098,7 +1169,7 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
       }
       for (int k = 0; k < ns; ++k) {
         or_field_cache fc;
-        shade(r, g, sc[k], d, st[k], app, &fc);
+        shade(r, g, sc[k], d, st[k], app, &fc, mask_ovr(r, g, ks++));
         ssig[k] = fc.sigma;
         for (int a = 0; a < 3; ++a) srgb[3 * k + a] = fc.rgb[a];
       }
@@ -1114,6 +1185,7 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
     memset(r->abs_grads[g], 0, sizeof(double) * m->nparams[g]);
     g_abs = r->abs_grads[g];
     g_gbase = r->grads[g];
+    uint64_t ks = 0;
     for (uint64_t i = 0; i < n; ++i) {
       const or_dray* d = &rays[i];
       int mo = -1;
@@ -1145,7 +1217,8 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
         break;
       }
       for (int k = 0; k < ns; ++k) {
-        shade(r, g, sc[k], d, st[k], app, &fcache[k]);
+        shade(r, g, sc[k], d, st[k], app, &fcache[k], mask_ovr(r, g, ks++));
+        ovr_account(r, &fcache[k], r->m.field[g][sc[k]].coarse);
         ssig[k] = fcache[k].sigma;
         for (int a = 0; a < 3; ++a) srgb[3 * k + a] = fcache[k].rgb[a];
       }
@@ -1172,7 +1245,37 @@ int or_run_train_step(or_run* r, const double* origin, const double* dir, const 
         const int casc = sc[k];
         const or_field_layout* f = &m->field[g][casc];
         const uint64_t off = casc == 0 ? 0 : m->field[g][0].size;
+        double* rec = NULL;
+        if (r->slog && (int32_t)g == r->slog_region && r->slog_n < r->slog_cap) {
+          /* pos 3 | features 32 | sigma, rgb | dsigma, drgb | d features 32  (OR_SLOG_REC) */
+          rec = r->slog + r->slog_n * OR_SLOG_REC;
+          memset(rec, 0, sizeof(double) * OR_SLOG_REC);
+          memcpy(rec, fcache[k].point, sizeof(double) * 3);
+          memcpy(rec + 3, fcache[k].enc, sizeof(double) * f->enc_width);
+          rec[35] = fcache[k].sigma;
+          memcpy(rec + 36, fcache[k].rgb, sizeof(double) * 3);
+          rec[39] = sgs[k];
+          memcpy(rec + 40, sgc + 3 * k, sizeof(double) * 3);
+          const double* pre[3] = {fcache[k].h1, fcache[k].c1, fcache[k].c2};
+          for (int q = 0; q < 3; ++q) {
+            uint32_t w0 = 0, w1 = 0;
+            double mn = INFINITY;
+            for (int u = 0; u < 64; ++u) {
+              if (pre[q][u] > 0.0) {
+                if (u < 32) w0 |= 1u << u;
+                else w1 |= 1u << (u - 32);
+              }
+              mn = fmin(mn, fabs(pre[q][u]));
+            }
+            rec[75 + 2 * q] = (double)w0;
+            rec[76 + 2 * q] = (double)w1;
+            rec[81 + q] = mn;
+          }
+          g_enc_grad_out = rec + 43;
+          ++r->slog_n;
+        }
         or_field_backward(f, r->params[g] + off, r->grads[g] + off, &fcache[k], sgs[k], sgc + 3 * k);
+        g_enc_grad_out = NULL;
       }
     }
     g_abs = NULL;
@@ -1249,7 +1352,7 @@ int or_run_eval_rays_ex(or_run* r, const double* origin, const double* dir, uint
       if (ns < 0) return -1;
       for (int k = 0; k < ns; ++k) {
         or_field_cache fc;
-        shade(r, g, sc[k], &d, st[k], app, &fc);
+        shade(r, g, sc[k], &d, st[k], app, &fc, NULL);
         ssig[k] = fc.sigma;
         for (int a = 0; a < 3; ++a) srgb[3 * k + a] = fc.rgb[a];
       }
@@ -1325,7 +1428,7 @@ void or_stage_field_forward(const or_model* m, uint32_t region, uint32_t cascade
                             const double* app, uint64_t n, double* sigma, double* rgb) {
   const or_field_layout* f = &m->field[region][cascade];
   const double* base = params + (cascade == 0 ? 0 : m->field[region][0].size);
-  or_field_cache c;
+  or_field_cache c = {0};
   for (uint64_t i = 0; i < n; ++i) {
     or_field_forward(f, base, pts + 3 * i, dirs + 3 * i, app + i * m->cfg.appearance_dim, &c);
     sigma[i] = c.sigma;
@@ -1339,7 +1442,7 @@ void or_stage_field_backward(const or_model* m, uint32_t region, uint32_t cascad
                              const double* drgb, uint64_t n) {
   const or_field_layout* f = &m->field[region][cascade];
   const uint64_t off = cascade == 0 ? 0 : m->field[region][0].size;
-  or_field_cache c;
+  or_field_cache c = {0};
   for (uint64_t i = 0; i < n; ++i) {
     or_field_forward(f, params + off, pts + 3 * i, dirs + 3 * i, app + i * m->cfg.appearance_dim, &c);
     or_field_backward(f, params + off, grads + off, &c, dsigma[i], drgb + 3 * i);

@@ -183,6 +183,8 @@ struct MlpLaunch {
   float4* out;                 // fwd: sigma, rgb
   const float4* grad_in;       // bwd: dsigma, drgb
   float* dX;                   // bwd, level-major like X
+  uint32_t* masks;             // tc path: [7][x_stride] ReLU / clip masks, written by the forward,
+                               // read by the backward (kernels_mlp_tc.cu); null: not stored
   unsigned long long* trace;   // DG_TRACE_MLP builds only (tools/trace_mlp.cu): phase clocks
 };
 void launch_mlp_fwd(const MlpLaunch& m, cudaStream_t s);

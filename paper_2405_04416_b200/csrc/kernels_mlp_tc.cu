@@ -158,7 +158,11 @@ __device__ __forceinline__ void gemm_ts(uint32_t d_tmem, uint32_t a, const uint8
 }
 
 // sigmoid with the SFU exp and reciprocal (relative error ~1e-7 for |x| <= 15-ish inputs).
+#ifdef DG_TC_PRECISE_SIGM
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+#else
 __device__ __forceinline__ float sigm(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+#endif
 __device__ __forceinline__ float clip15(float v) { return v > 15.f ? 15.f : (v < -15.f ? -15.f : v); }
 
 // SH16 components 1..15 (sh.hpp:14-35); component 0 is the constant 0.28209479177387814.
@@ -188,10 +192,10 @@ constexpr float kSH0 = 0.28209479177387814f;
 __device__ __forceinline__ void act16(float* v, const float* b, int act) {
   if (act == 2) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = sigm(v[i] + b[i]);
+    for (int i = 0; i < 16; ++i) v[i] = sigm(v[i] + (b ? b[i] : 0.f));
   } else {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + b[i], 0.f);
+    for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + (b ? b[i] : 0.f), 0.f);
   }
 }
 
@@ -270,6 +274,7 @@ struct Pref {
     if (part == SHP || part == APP) item = v ? __ldg(m.s_item + gs) : 0u;
     if (want_g && part == 0) g = v ? __ldcs(m.grad_in + gs) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+
   __device__ __forceinline__ void grad(const MlpLaunch& m, int part) {
     if (part == 0) g = valid ? __ldcs(m.grad_in + gs) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -371,8 +376,100 @@ __device__ __forceinline__ void issue2(int warp, uint64_t* mbar, Crit crit, Back
   }
 }
 
+// ---------------------------------------------------------------------------- forward
+// The forward runs in split-tf32 (x = hi + lo + O(2^-22 |x|), hi.hi + hi.lo + lo.hi exact in
+// the fp32 accumulator): its pre-activations decide the ReLU / clip masks the backward uses
+// (MlpLaunch::masks), and a mask must agree with the fp64 reference's for every unit that is
+// not within fp32 noise of its kink.  Split-bf16 (2^-17) flipped ~1.5e-4 of the samples'
+// masks in a trained state (tools/diag/diag_mlp_prec.py), each flip switching a whole unit's
+// gradient contribution on or off.
+
+// tf32 weight tiles (B, K-major, 32-bit core matrices): rows = out (padded), cols = in.
+struct TcWeights32 {
+  uint32_t d0[2][64 * 32];
+  uint32_t d1[2][16 * 64];
+  uint32_t c0[2][64 * 48];
+  uint32_t c1[2][64 * 64];
+  uint32_t c2[2][16 * 64];
+  float bd0[64], bd1[16], bc0[64], bc1[64], bc2[16];
+};
+
+__device__ void stage_layer32(const float* __restrict__ W, int out, int in, int Np, int Kp, uint32_t* hi,
+                              uint32_t* lo) {
+  for (int e = threadIdx.x; e < Np * Kp; e += blockDim.x) {
+    const int o = e / Kp, i = e % Kp;
+    const float a = (o < out && i < in) ? W[o * in + i] : 0.f;
+    uint32_t h, l;
+    tc::split_tf32(a, h, l);
+    const uint32_t off = tc::core_offset32(o, i, Np) >> 2;
+    hi[off] = h;
+    lo[off] = l;
+  }
+}
+
+__device__ void stage_weights_tf32(const FieldDesc& fd, const float* __restrict__ params, TcWeights32& w) {
+  const float* base = params + fd.base;
+  const int enc = (int)fd.L * 2, cin = 31 + (int)fd.app_dim;
+  stage_layer32(base + fd.dw0, 64, enc, 64, 32, w.d0[0], w.d0[1]);
+  stage_layer32(base + fd.dw1, 16, 64, 16, 64, w.d1[0], w.d1[1]);
+  stage_layer32(base + fd.cw0, 64, cin, 64, 48, w.c0[0], w.c0[1]);
+  stage_layer32(base + fd.cw1, 64, 64, 64, 64, w.c1[0], w.c1[1]);
+  stage_layer32(base + fd.cw2, 3, 64, 16, 64, w.c2[0], w.c2[1]);
+  for (int e = threadIdx.x; e < 64; e += blockDim.x) {
+    w.bd0[e] = base[fd.db0 + e];
+    w.bc0[e] = base[fd.cb0 + e];
+    w.bc1[e] = base[fd.cb1 + e];
+  }
+  for (int e = threadIdx.x; e < 16; e += blockDim.x) {
+    w.bd1[e] = base[fd.db1 + e];
+    w.bc2[e] = e < 3 ? base[fd.cb2 + e] : 0.f;
+  }
+}
+
+// TMEM A region of the forward: hi at [A32_HI, A32_HI + K), lo at + A32_LO_OFF (one column per k).
+constexpr uint32_t A32_HI = 64, A32_LO_OFF = 64;
+
+// 8 consecutive columns [c0, c0 + 8) of this thread's row into the tf32 A region.
+__device__ __forceinline__ void put8_32(uint32_t ta, int c0, const float* v) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tc::split_tf32(v[4 * q + j], h[j], l[j]);
+    tc::tmem_st4(ta + (uint32_t)(c0 + 4 * q), h);
+    tc::tmem_st4(ta + A32_LO_OFF + (uint32_t)(c0 + 4 * q), l);
+  }
+}
+
+// D[TM x N] = A[TM x K] . B[N x K]^T in split-tf32 (3 MMAs per 8-wide K step); A in the TMEM
+// A region, B in smem (K-major 32-bit core matrices: SBO 128, LBO N/8*128).
+template <int N, int K>
+__device__ __forceinline__ void gemm_ts32(uint32_t d_tmem, uint32_t a, const uint32_t* b_hi, const uint32_t* b_lo) {
+  constexpr uint32_t id = tc::idesc_tf32(TM, N, 0, 0);
+  constexpr uint32_t b_lbo = (N / 8) * 128;
+  const uint64_t bh = tc::smem_desc(tc::smem_u32(b_hi), b_lbo, 128);
+  const uint64_t bl = tc::smem_desc(tc::smem_u32(b_lo), b_lbo, 128);
+#pragma unroll
+  for (int k = 0; k < K / 8; ++k) {
+    const uint32_t bo = (k * 2 * b_lbo) >> 4;
+    tc::mma_tf32_ts(d_tmem, a + 8 * k, bh + bo, id, k > 0 ? 1u : 0u);
+    tc::mma_tf32_ts(d_tmem, a + 8 * k, bl + bo, id, 1u);
+    tc::mma_tf32_ts(d_tmem, a + A32_LO_OFF + 8 * k, bh + bo, id, 1u);
+  }
+}
+
+// bits i of the ReLU mask (z > 0) of 16 pre-activations
+__device__ __forceinline__ uint32_t relu_bits16(const float* z) {
+  uint32_t b = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) b |= (z[i] > 0.f ? 1u : 0u) << i;
+  return b;
+}
+
+constexpr int kCinS = 36;  // row stride (floats) of the staged Cin columns: conflict-free float4s
 struct FwdTcSmem {
-  TcWeights w;
+  TcWeights32 w;
+  float cin_s[TM * kCinS];
   float sig_raw[TM];
   uint64_t mbar;
   uint32_t tslot;
@@ -381,7 +478,11 @@ struct FwdTcSmem {
 // Forward: 2 column parts (warps 0-3 / 4-7) x 4 lane quadrants; each thread owns one sample row
 // and 32 of the 64 hidden columns.  Activations never touch shared memory: each epilogue
 // writes the next layer's split operand straight into the TMEM A region.  TMEM: [0, 64) the
-// accumulator, [64, 128) the A operand.  Tiles are strided over the grid.
+// accumulator, [64, 192) the A operand (hi, lo).  Tiles are strided over the grid.  With
+// m.masks set, each pre-activation's sign (and the two clip flags) go to HBM for the backward:
+// mask word w of sample s at masks[w * x_stride + s]: w = 0..3, one per 16-column part p of
+// the backward: h1 bits of columns 16p..16p+15 | c1 bits << 16; w = 4, 5: c2 columns 0-31,
+// 32-63; w = 6: raw clip bits 0-15 | colour clip bits 16-18.
 __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
   constexpr int NP = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -389,7 +490,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quad = warp & 3, part = warp >> 2;
   const int row = quad * 32 + lane;  // TMEM lane == sample row of the tile
-  if (warp == 0) tc::tmem_alloc(&sm.tslot, 128);
+  if (warp == 0) tc::tmem_alloc(&sm.tslot, 256);
   if (tid == 0) {
     tc::mbar_init(&sm.mbar, 1);
     tc::fence_mbar_init();
@@ -399,8 +500,9 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
   tc::fence_after();
   const uint32_t tmem = sm.tslot;
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
-  const Sink act{nullptr, nullptr, my_lanes + A_HI};
-  const uint32_t a_op = tmem + A_HI;
+  const uint32_t ta = my_lanes + A32_HI;
+  const uint32_t a_op = tmem + A32_HI;
+  uint32_t* const masks = m.masks;
   uint32_t phase = 0;
   auto mma_done = [&]() {
     tc::mbar_wait(&sm.mbar, phase);
@@ -413,111 +515,189 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
     Pref<NP> pf;
     pf.start(m, row < cur.count, cur.s0 + row, part, false);
     pf.rec(m, part);
-    pf.appearance(m, m.fields[cur.f], part);
-    stage_weights_tc(m.fields[cur.f], m.params, sm.w);
+    stage_weights_tf32(m.fields[cur.f], m.params, sm.w);
     int loaded = cur.f;
     int act_c = m.fields[cur.f].coarse ? 2 : 1;  // colour activation of the loaded field
-    pf.put_x(act, row, part);
+    auto put_x = [&]() {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) put8_32(ta, part * 16 + 8 * c, pf.x + 8 * c);
+    };
+    put_x();
     for (;;) {
       const bool valid = row < cur.count;
       const uint64_t gs = cur.s0 + row;
       const uint32_t next = tile + gridDim.x;
       const bool has_next = next < m.n_tiles;
       const TileGeo nx = has_next ? tile_geo_at(m, cur, next) : cur;
+      const bool store_mask = masks != nullptr && valid;
       to_mma();
       // ---- L1: H1 = relu(X Wd0^T + b) ----
-      ISSUE(gemm_ts<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
-      float cin_app[17];
+      ISSUE(gemm_ts32<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
+      if (part == 1) {  // Cin columns 16-47 (SH1..15, appearance) of this tile's row -> smem
+        float* cs = sm.cin_s + row * kCinS;
+        float c[16];
+        if (valid) {
+          sh15((float)pf.dir[0], (float)pf.dir[1], (float)pf.dir[2], c);
+        } else {
 #pragma unroll
-      for (int i = 0; i < 17; ++i) cin_app[i] = pf.app[i];
-      const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
+          for (int i = 0; i < 15; ++i) c[i] = 0.f;
+        }
+        // appearance row (L2-resident table; read here, used at L2's epilogue)
+        const int dim = (int)m.fields[cur.f].app_dim;
+        const float* src = nullptr;
+        if (valid)
+          src = m.app_per_sample ? m.app_override + gs * (uint32_t)dim
+                                 : (m.app_override ? m.app_override : m.app_table + (uint64_t)pf.img * dim);
+        float a[17];
+#pragma unroll
+        for (int i = 0; i < 17; ++i) a[i] = (src && i < dim) ? __ldg(src + i) : 0.f;
+        c[15] = a[0];
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(cs + i) = make_float4(c[i], c[i + 1], c[i + 2], c[i + 3]);
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(cs + 16 + i) = make_float4(a[1 + i], a[2 + i], a[3 + i], a[4 + i]);
+      }
       pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next tile: X, item
       mma_done();
+      {
+        uint32_t bits = 0;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float v[16];
-        ld16(my_lanes + part * 32 + 16 * q, v);
+        for (int q = 0; q < 2; ++q) {
+          float v[16];
+          ld16(my_lanes + part * 32 + 16 * q, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[part * 32 + 16 * q + i], 0.f);
-        put8(act, row, part * 32 + 16 * q, v);
-        put8(act, row, part * 32 + 16 * q + 8, v + 8);
+          for (int i = 0; i < 16; ++i) v[i] += sm.w.bd0[part * 32 + 16 * q + i];
+          bits |= relu_bits16(v) << (16 * q);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+          put8_32(ta, part * 32 + 16 * q, v);
+          put8_32(ta, part * 32 + 16 * q + 8, v + 8);
+        }
+        if (store_mask) {  // low halves of words 2 part, 2 part + 1 (the backward's 16-column parts)
+          uint16_t* mh = reinterpret_cast<uint16_t*>(masks + (uint64_t)(2 * part) * m.x_stride + gs);
+          __stcs(mh, (uint16_t)(bits & 0xffffu));
+          __stcs(mh + 2 * m.x_stride, (uint16_t)(bits >> 16));
+        }
       }
       to_mma();
       // ---- L2: raw16 = H1 Wd1^T + b ; Cin = [clip(raw1..15) | SH16 | app | 0] ----
-      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]));
+      ISSUE(gemm_ts32<16, 64>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]));
       mma_done();
+      uint32_t clip_bits = 0;
       {
         float raw[16];
         if (part == 0) {
           ld16(my_lanes, raw);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) raw[i] = clip15(raw[i] + sm.w.bd1[i]);
+          for (int i = 0; i < 16; ++i) {
+            const float z = raw[i] + sm.w.bd1[i];
+            clip_bits |= (z > 15.f || z < -15.f ? 1u : 0u) << i;
+            raw[i] = clip15(z);
+          }
           sm.sig_raw[row] = raw[0];
         }
-        // this tile's dir / app were prefetched into the (now next-tile) registers: restore
-        Pref<NP> cp;
-        cp.valid = valid;
-        cp.dir[0] = d0;
-        cp.dir[1] = d1;
-        cp.dir[2] = d2;
+        float c[16];
+        if (part == 0) {
 #pragma unroll
-        for (int i = 0; i < 17; ++i) cp.app[i] = cin_app[i];
-        cp.put_cin(act, row, part, raw);
+          for (int i = 0; i < 15; ++i) c[i] = raw[1 + i];
+          c[15] = valid ? kSH0 : 0.f;
+          put8_32(ta, 0, c);
+          put8_32(ta, 8, c + 8);
+        } else {  // part 1: the SH / appearance columns staged at the tile start
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float* cs = sm.cin_s + row * kCinS + 16 * h;
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              const float4 q = *reinterpret_cast<const float4*>(cs + i);
+              c[i] = q.x;
+              c[i + 1] = q.y;
+              c[i + 2] = q.z;
+              c[i + 3] = q.w;
+            }
+            put8_32(ta, 16 + 16 * h, c);
+            put8_32(ta, 24 + 16 * h, c + 8);
+          }
+        }
       }
       pf.rec(m, part);  // next tile's RayRec (item arrived during L1/L2)
       to_mma();
       // ---- L3: C1 = act(Cin Wc0^T + b) ----
-      ISSUE(gemm_ts<64, 48>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]));
+      ISSUE(gemm_ts32<64, 48>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]));
       mma_done();
+      {
+        uint32_t bits = 0;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float v[16];
-        ld16(my_lanes + part * 32 + 16 * q, v);
-        act16(v, sm.w.bc0 + part * 32 + 16 * q, act_c);
-        put8(act, row, part * 32 + 16 * q, v);
-        put8(act, row, part * 32 + 16 * q + 8, v + 8);
+        for (int q = 0; q < 2; ++q) {
+          float v[16];
+          ld16(my_lanes + part * 32 + 16 * q, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += sm.w.bc0[part * 32 + 16 * q + i];
+          bits |= relu_bits16(v) << (16 * q);
+          act16(v, nullptr, act_c);
+          put8_32(ta, part * 32 + 16 * q, v);
+          put8_32(ta, part * 32 + 16 * q + 8, v + 8);
+        }
+        if (store_mask) {  // high halves of words 2 part, 2 part + 1
+          uint16_t* mh = reinterpret_cast<uint16_t*>(masks + (uint64_t)(2 * part) * m.x_stride + gs) + 1;
+          __stcs(mh, (uint16_t)(bits & 0xffffu));
+          __stcs(mh + 2 * m.x_stride, (uint16_t)(bits >> 16));
+        }
       }
       to_mma();
       // ---- L4: C2 = act(C1 Wc1^T + b) ----
-      ISSUE(gemm_ts<64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]));
+      ISSUE(gemm_ts32<64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]));
       mma_done();
+      {
+        uint32_t bits = 0;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float v[16];
-        ld16(my_lanes + part * 32 + 16 * q, v);
-        act16(v, sm.w.bc1 + part * 32 + 16 * q, act_c);
-        put8(act, row, part * 32 + 16 * q, v);
-        put8(act, row, part * 32 + 16 * q + 8, v + 8);
+        for (int q = 0; q < 2; ++q) {
+          float v[16];
+          ld16(my_lanes + part * 32 + 16 * q, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += sm.w.bc1[part * 32 + 16 * q + i];
+          bits |= relu_bits16(v) << (16 * q);
+          act16(v, nullptr, act_c);
+          put8_32(ta, part * 32 + 16 * q, v);
+          put8_32(ta, part * 32 + 16 * q + 8, v + 8);
+        }
+        if (store_mask) __stcs(masks + (uint64_t)(4 + part) * m.x_stride + gs, bits);
       }
-      pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
       to_mma();
       // ---- L5: rgb = sigmoid(clip(C2 Wc2^T + b)) ----
-      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
+      ISSUE(gemm_ts32<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
       mma_done();
       if (part == 0) {
         float v[16];
         ld16(my_lanes, v);
+        float z[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          z[k] = v[k] + sm.w.bc2[k];
+          clip_bits |= (z[k] > 15.f || z[k] < -15.f ? 1u : 0u) << (16 + k);
+        }
         if (valid)
-          __stcs(m.out + gs, make_float4(expf(sm.sig_raw[row]), sigm(clip15(v[0] + sm.w.bc2[0])),
-                                         sigm(clip15(v[1] + sm.w.bc2[1])), sigm(clip15(v[2] + sm.w.bc2[2]))));
+          __stcs(m.out + gs, make_float4(expf(sm.sig_raw[row]), sigm(clip15(z[0])), sigm(clip15(z[1])),
+                                         sigm(clip15(z[2]))));
+        if (store_mask) __stcs(masks + 6ull * m.x_stride + gs, clip_bits);
       }
       if (!has_next) break;
       if (nx.f != loaded) {
         __syncthreads();  // every thread is done with the old biases
-        stage_weights_tc(m.fields[nx.f], m.params, sm.w);
+        stage_weights_tf32(m.fields[nx.f], m.params, sm.w);
         loaded = nx.f;
         act_c = m.fields[nx.f].coarse ? 2 : 1;
       }
-      pf.put_x(act, row, part);  // the A region is free: every MMA has completed
+      put_x();  // the A region is free: every MMA has completed
       tile = next;
       cur = nx;
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free(tmem, 128);
+  if (warp == 0) tc::tmem_free(tmem, 256);
 }
-
 
 // ============================================================================ backward
 // Per tile of 128 samples: recompute the forward (keeping every layer input in smem), then
@@ -687,13 +867,20 @@ __device__ void flush_all(uint32_t tmem, const FieldDesc& fd, float* __restrict_
 
 // G = act'(a) * dv for 16 columns of row r; a is read back from the activation tile (hi, lo),
 // G goes to `out` (its smem tile for the weight gradient + the TMEM A region).
+// ReLU layers use the forward's mask bits (the sign of the split-tf32 pre-activation); the
+// sigmoid derivative comes from the activation value.
 __device__ __forceinline__ void grad_act16(const uint8_t* a_hi, const uint8_t* a_lo, const Sink& out,
-                                           int r, int c0, float* v, int act) {
-  float a[16];
-  get8(a_hi, a_lo, r, c0, a);
-  get8(a_hi, a_lo, r, c0 + 8, a + 8);
+                                           int r, int c0, float* v, int act, uint32_t bits) {
+  if (act == 2) {
+    float a[16];
+    get8(a_hi, a_lo, r, c0, a);
+    get8(a_hi, a_lo, r, c0 + 8, a + 8);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] *= act == 2 ? a[i] * (1.f - a[i]) : (a[i] > 0.f ? 1.f : 0.f);
+    for (int i = 0; i < 16; ++i) v[i] *= a[i] * (1.f - a[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = ((bits >> i) & 1u) ? v[i] : 0.f;
+  }
   put8(out, r, c0, v);
   put8(out, r, c0 + 8, v + 8);
 }
@@ -783,6 +970,15 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       for (int i = 0; i < 17; ++i) cur_app[i] = pf.app[i];
       const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
       const float4 up = pf.g;
+      // the forward's masks of this tile: first needed at B1, five epilogues from now, so the
+      // loads are issued here rather than held in prefetch registers through the previous tile
+      // (this part's 16 columns: h1 bits 0-15 | c1 bits 16-31, the c2 word; part 0: clip word)
+      uint32_t mk_relu = 0u, mk_c2 = 0u, mk_clip = 0u;
+      if (valid) {
+        mk_relu = __ldcs(m.masks + (uint64_t)part * m.x_stride + gs);
+        mk_c2 = __ldcs(m.masks + (uint64_t)(4 + (part >> 1)) * m.x_stride + gs);
+        if (part == 0) mk_clip = __ldcs(m.masks + 6ull * m.x_stride + gs);
+      }
       sync_mma();
       // ---------------- forward recompute (A operands from TMEM) ----------------
       ISSUE(gemm_ts<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
@@ -804,15 +1000,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
         float raw[16];
         if (part == 0) {
           ld16(my_lanes, raw);
-          uint32_t mask = 0;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float z = raw[i] + sm.w.bd1[i];
-            mask |= (z > 15.f || z < -15.f ? 1u : 0u) << i;
-            raw[i] = clip15(z);
-          }
+          for (int i = 0; i < 16; ++i) raw[i] = clip15(raw[i] + sm.w.bd1[i]);
           sm.sig_raw[row] = raw[0];
-          sm.dmask[row] = mask;
         }
         Pref<NP> cp;
         cp.valid = valid;
@@ -855,8 +1045,10 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       sync_mma();
       ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
       mma_done();
+      mk_c2 = (mk_c2 >> (((uint32_t)part & 1u) * 16u)) & 0xffffu;
       // ---------------- B1: colour head adjoint (field.cpp:298-306) ----------------
       if (part == 0) {
+        sm.dmask[row] = mk_clip & 0xffffu;  // the forward's clip flags
         float v[16];
         ld16(my_lanes, v);
         const float ug[3] = {up.y, up.z, up.w};
@@ -866,7 +1058,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           const float z = v[k] + sm.w.bc2[k];
-          const bool clipped = z > 15.f || z < -15.f;
+          const bool clipped = (mk_clip >> (16 + k)) & 1u;
           const float sg = sigm(clip15(z));
           g[k] = clipped ? 0.f : ug[k] * sg * (1.f - sg);
         }
@@ -885,7 +1077,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       {
         float v[16];
         ld16(my_lanes + c16, v);
-        grad_act16(sm.c2[0], sm.c2[1], ss, row, c16, v, act_c);
+        grad_act16(sm.c2[0], sm.c2[1], ss, row, c16, v, act_c, mk_c2);
       }
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]); },
@@ -895,7 +1087,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       {
         float v[16];
         ld16(my_lanes + c16, v);
-        grad_act16(sm.c1_hi, sm.c1_lo, sc2, row, c16, v, act_c);
+        grad_act16(sm.c1_hi, sm.c1_lo, sc2, row, c16, v, act_c, mk_relu >> 16);
       }
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
       sync_mma();
@@ -939,7 +1131,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       {
         float v[16];
         ld16(my_lanes + c16, v);
-        grad_act16(sm.h1_hi, sm.h1_lo, sc2, row, c16, v, 1);
+        grad_act16(sm.h1_hi, sm.h1_lo, sc2, row, c16, v, 1, mk_relu & 0xffffu);
       }
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 32, 64>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]); },

@@ -188,7 +188,7 @@ struct dg_ctx {
   DBuf h_o, h_d, h_gt, h_img, h_nseg, h_sched, h_flags, h_pos, cub_tmp, small, dropped, loss,
       error, rec, it_te, it_tx, it_t0, it_t1, it_nseg, it_order, it_part, it_sched, it_cnt,
       it_off, it_ncb, it_contains, it_cscan, it_partial, it_depth, part_item_off_d, s_t, s_delta, s_p,
-      s_item, s_X, s_out, s_grad, s_dX, field_off_d, tile_off_f, tile_off_b, stream_send_d,
+      s_item, s_X, s_out, s_grad, s_dX, s_mask, field_off_d, tile_off_f, tile_off_b, stream_send_d,
       stream_recv_d, send_buf, recv_buf, x_send, x_recv, out_rgb, out_T, out_depth, eval_app,
       perm_tab, occ_pts, occ_cells, occ_sigma, occ_pts_warm;
   // last step (introspection)
@@ -796,6 +796,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   TRY(c->s_out.ensure(NS * 16 + 16));
   TRY(c->s_grad.ensure(NS * 16 + 16));
   TRY(c->s_dX.ensure(NS * kEnc * 4 + 16));
+  if (train && c->mlp_impl) TRY(c->s_mask.ensure(NS * 7 * 4 + 16));
   SampleArrays sm = sample_arrays(c);
   launch_march_fill(c->d_parts.as<PartDesc>(), c->occ.as<uint8_t>(), NI, it, sm, c->n_fine,
                     c->step, c->cfg.seed, batch_id, train, s);
@@ -901,6 +902,7 @@ MlpLaunch mlp_launch(dg_ctx* c, bool bwd) {
   m.out = c->s_out.as<float4>();
   m.grad_in = c->s_grad.as<float4>();
   m.dX = c->s_dX.as<float>();
+  m.masks = c->s_mask.as<uint32_t>();  // set by the training step's forward, read by its backward
   return m;
 }
 
@@ -1734,6 +1736,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
     c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
   }
   MlpLaunch mf = mlp_launch(c, false);
+  mf.masks = nullptr;  // evaluation has no backward
   mf.app_override = c->eval_app.as<float>();
   if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);
   else launch_mlp_fwd(mf, s);
@@ -2084,6 +2087,7 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
   m.grads = c->grads.as<float>();
   TRY(out.ensure(n * 16 + 16));
   m.out = out.as<float4>();
+  DBuf masks;
   if (!sig_grad) {
     TRY(upload(toff, tf.data(), tf.size() * 4, s));
     m.tile_off = toff.as<uint32_t>();
@@ -2107,6 +2111,15 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
     g[i] = make_float4(sig_grad[i], rgb_grad[3 * i], rgb_grad[3 * i + 1], rgb_grad[3 * i + 2]);
   TRY(upload(gin, g.data(), n * 16, s));
   TRY(dX.ensure(n * kEnc * 4 + 16));
+  if (c->mlp_impl) {  // the tcgen05 backward takes its ReLU / clip masks from the forward
+    TRY(masks.ensure(n * 7 * 4 + 16));
+    m.masks = masks.as<uint32_t>();
+    TRY(upload(toff, tf.data(), tf.size() * 4, s));
+    m.tile_off = toff.as<uint32_t>();
+    m.n_tiles = tf[2 * nl];
+    launch_mlp_fwd_tc(m, c->num_sms, s);
+    ++c->launches;
+  }
   const std::vector<uint32_t>& tt = c->mlp_impl ? tf : tb;
   TRY(upload(toff, tt.data(), tt.size() * 4, s));
   m.tile_off = toff.as<uint32_t>();
@@ -2438,6 +2451,61 @@ int dg_last_samples(dg_ctx* c, uint32_t p, double* t, double* delta, uint8_t* ca
     for (uint32_t j = 0; j < ncb[i]; ++j) put(off[NI + i] + j, 1);
     for (uint32_t j = 0; j < cnt[i]; ++j) put(off[i] + j, 0);
     for (uint32_t j = ncb[i]; j < cnt[NI + i]; ++j) put(off[NI + i] + j, 1);
+  }
+  return DG_OK;
+}
+
+// Per-sample state of the last training step, in dg_last_samples order: the normalised field
+// position the march wrote and the encode read (worker.cpp:46), the encoded features
+// (k_encode_fwd), the field outputs (k_mlp_fwd*: sigma, rgb), the upstream gradient of the
+// merge / compositing backward (k_merge_backward: dsigma, drgb) and the encoding's upstream
+// (k_mlp_bwd*: dL/dfeatures) and the forward's ReLU / clip mask words (tcgen05 path, the layout
+// of kernels_mlp_tc.cu's k_mlp_fwd_tc).  Every output is optional.
+int dg_last_sample_data(dg_ctx* c, uint32_t p, double* pos, float* features, float* field_out,
+                        float* upstream, float* d_features, uint32_t* masks) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (!c->have_last) return set_err(DG_EINVAL, "no step has run");
+  if (pos && !c->enc_pcache) return set_err(DG_EINVAL, "position cache disabled (DG_ENC_PCACHE=0)");
+  cudaStream_t s = c->stream;
+  const uint32_t NI = c->n_items, L = c->cfg.grid_levels;
+  const uint64_t NS = uint64_t(c->n_fine) + c->n_coarse;
+  std::vector<uint32_t> cnt, off, ncb;
+  std::vector<double> hp;
+  std::vector<float> hx, ho, hg, hdx;
+  TRY(d2h(cnt, c->it_cnt.p, 2ull * NI, s));
+  TRY(d2h(off, c->it_off.p, 2ull * NI, s));
+  TRY(d2h(ncb, c->it_ncb.p, NI, s));
+  if (pos) TRY(d2h(hp, c->s_p.p, 3 * NS, s));
+  if (features) TRY(d2h(hx, c->s_X.p, 2ull * L * NS, s));
+  if (field_out) TRY(d2h(ho, c->s_out.p, 4 * NS, s));
+  if (upstream) TRY(d2h(hg, c->s_grad.p, 4 * NS, s));
+  if (d_features) TRY(d2h(hdx, c->s_dX.p, 2ull * L * NS, s));
+  std::vector<uint32_t> hm;
+  if (masks) {
+    if (!c->mlp_impl) return set_err(DG_EINVAL, "masks exist on the tcgen05 path only");
+    TRY(d2h(hm, c->s_mask.p, 7 * NS, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  uint64_t k = 0;
+  auto put = [&](uint64_t idx) {
+    for (int a = 0; a < 3 && pos; ++a) pos[3 * k + a] = hp[a * NS + idx];
+    for (uint32_t l = 0; l < L; ++l)
+      for (int f = 0; f < 2; ++f) {
+        if (features) features[(k * L + l) * 2 + f] = hx[(l * NS + idx) * 2 + f];
+        if (d_features) d_features[(k * L + l) * 2 + f] = hdx[(l * NS + idx) * 2 + f];
+      }
+    for (int a = 0; a < 4; ++a) {
+      if (field_out) field_out[4 * k + a] = ho[4 * idx + a];
+      if (upstream) upstream[4 * k + a] = hg[4 * idx + a];
+    }
+    for (int w = 0; w < 7 && masks; ++w) masks[7 * k + w] = hm[w * NS + idx];
+    ++k;
+  };
+  for (uint32_t i = c->part_item_off[lp]; i < c->part_item_off[lp + 1]; ++i) {
+    for (uint32_t j = 0; j < ncb[i]; ++j) put(off[NI + i] + j);
+    for (uint32_t j = 0; j < cnt[i]; ++j) put(off[i] + j);
+    for (uint32_t j = ncb[i]; j < cnt[NI + i]; ++j) put(off[NI + i] + j);
   }
   return DG_OK;
 }

@@ -161,6 +161,47 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ---- tf32 (kind::tf32): 32-bit elements, a core matrix is 8 rows x 4 elements (16 B) ----
+__device__ __forceinline__ uint32_t core_offset32(uint32_t r, uint32_t c, uint32_t R) {
+  return ((c >> 2) * (R >> 3) + (r >> 3)) * 128u + (r & 7u) * 16u + (c & 3u) * 4u;
+}
+
+// Instruction descriptor for kind::tf32 (atype = btype = TF32) with fp32 D.
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, uint32_t a_mn_major,
+                                                  uint32_t b_mn_major) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn_major << 15) | (b_mn_major << 16) |
+         ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// tcgen05.mma kind::tf32 with A in TMEM (lane = row, one 32-bit column per k; an 8-wide K
+// step reads 8 columns).
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+// tf32 hi/lo split, both rounded to nearest (ties away) on the bit pattern: adding half an
+// ulp of the 10-bit mantissa and clearing the 13 low bits is two integer ops, where the
+// cvt.rna.tf32.f32 conversion runs at a fraction of the ALU rate.  x = hi + lo + O(2^-22 |x|);
+// the products hi.hi + hi.lo + lo.hi are exact in the fp32 accumulator.
+__device__ __forceinline__ uint32_t round_tf32(float x) {
+  return (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+}
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = round_tf32(x);
+  lo = round_tf32(x - __uint_as_float(hi));
+}
+
 // bf16 hi/lo split (x = hi + lo + O(2^-17 |x|)), round-to-nearest.
 __device__ __forceinline__ void split_bf16(float x, uint16_t& hi, uint16_t& lo) {
   const __nv_bfloat16 h = __float2bfloat16_rn(x);

@@ -478,6 +478,32 @@ class Context:
         _check(lib().dg_last_samples(self.h, C.c_uint32(g), _p(t), _p(d), _p(c)))
         return t[:tot], d[:tot], c[:tot]
 
+    def last_sample_data(self, g, masks=False):
+        """(pos [n,3], features [n,2L], field_out [n,4], upstream [n,4], d_features [n,2L]
+        [, masks [n,7]]) of the last training step's samples of partition g, in last_samples
+        order."""
+        _, nf, nc = self.last_items(g)
+        n, L2 = nf + nc, 2 * self.cfg.grid_levels
+        pos = np.zeros((max(n, 1), 3))
+        x = np.zeros((max(n, 1), L2), dtype=np.float32)
+        out = np.zeros((max(n, 1), 4), dtype=np.float32)
+        up = np.zeros((max(n, 1), 4), dtype=np.float32)
+        dx = np.zeros((max(n, 1), L2), dtype=np.float32)
+        mk = np.zeros((max(n, 1), 7), dtype=np.uint32) if masks else None
+        _check(lib().dg_last_sample_data(self.h, C.c_uint32(g), _p(pos), _p(x), _p(out), _p(up), _p(dx),
+                                         _p(mk)))
+        res = (pos[:n], x[:n], out[:n], up[:n], dx[:n])
+        return res + (mk[:n],) if masks else res
+
+    def last_masks(self, g):
+        """The tcgen05 forward's ReLU / clip mask words [n, 7] of the last training step's samples
+        of partition g (last_samples order); raises DG_EINVAL on the FFMA path."""
+        _, nf, nc = self.last_items(g)
+        n = nf + nc
+        mk = np.zeros((max(n, 1), 7), dtype=np.uint32)
+        _check(lib().dg_last_sample_data(self.h, C.c_uint32(g), None, None, None, None, None, _p(mk)))
+        return mk[:n]
+
     def last_partials(self, g):
         n, _, _ = self.last_items(g)
         rgb = np.zeros((n, 3), dtype=np.float32)

@@ -76,3 +76,28 @@ def rel_l2(a, b):
 
 def rel_err(a, b, floor=1e-12):
     return abs(a - b) / max(abs(b), floor)
+
+
+def tied_train_step(ctx, orc, o, d, gt, img, step, partitions=None):
+    """One training step on the GPU, then the oracle's on the same batch with the GPU's ReLU
+    on/off decisions (tcgen05 path: the split-tf32 forward's masks) for every sample.  A unit
+    whose fp64 pre-activation lies within fp32 noise of 0 may round to either side, and its
+    whole gradient contribution switches with it; tying the decisions compares everything else
+    at full precision.  Returns (gpu stats, oracle stats, (units decided against the fp64 sign,
+    their largest |z|)) -- a test bounds the latter so only genuine near-ties are absorbed.
+    On the FFMA path (no masks) the oracle runs untied."""
+    from oracle.bindings import gpu_mask_words
+    sg = ctx.train_step(o, d, gt, img, step=step)
+    tied = []
+    for g in (partitions if partitions is not None else ctx.local):
+        try:
+            words = gpu_mask_words(ctx.last_masks(g))
+        except Exception:  # FFMA: no masks
+            break
+        orc.mask_override(g, words)
+        tied.append(g)
+    so = orc.train_step(o, d, gt, img, step)
+    ovr = orc.override_stats()
+    for g in tied:
+        orc.mask_override(g, None)
+    return sg, so, ovr

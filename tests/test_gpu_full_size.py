@@ -76,3 +76,99 @@ def test_full_size_index_path_bit_exact():
     st2 = ctx2.train_step(o, d, gt, img, step=0)
     for k in ("loss_rgb", "loss_transmittance", "loss_distortion"):
         assert abs(st2[k] - st[k]) <= 1e-9 * abs(st[k]), k
+
+
+# ------------------------------------------------------------------ value parity at the bench config
+def _full_pair(wl, table_scale=0.5):
+    """GPU context + oracle run of a whole workload config from identical injected fp32 state."""
+    from oracle.bindings import OracleRun
+
+    from .helpers import app_rows, inject
+    cfg = wl.cfg
+    app = app_rows(1)
+    ctx = dg.Context(cfg, device=0)
+    ctx.set_appearance(app)
+    orc = OracleRun(cfg, app)
+    inject(cfg, ctx, [orc], table_scale=table_scale)
+    return ctx, orc
+
+
+def _grad_parity(cfg, ctx, orc, p0, lr, tol=1e-4):
+    from .helpers import rel_l2
+    for g in range(cfg.kx * cfg.ky):
+        m_g, _, _ = ctx.get_adam(g)
+        grad_g = m_g.astype(np.float64) / (1.0 - cfg.adam_beta1)  # first Adam step from m = 0
+        grad_o = orc.grads(g)
+        worst = 0.0
+        for arr in ctx.param_layout(g):
+            a = slice(arr["offset"], arr["offset"] + arr["size"])
+            if np.abs(grad_o[a]).max() == 0:
+                assert np.abs(grad_g[a]).max() < 1e-20, arr
+                continue
+            e = rel_l2(grad_g[a], grad_o[a])
+            worst = max(worst, e)
+            assert e < tol, (arr, e)
+        big = np.abs(grad_o) > 1e-6 * np.abs(grad_o).max()
+        err = np.abs((ctx.get_params(g).astype(np.float64) - p0[g]) - (orc.params(g) - p0[g]))
+        assert np.mean(err[big] <= 1e-3 * lr) >= 0.999, np.mean(err[big] <= 1e-3 * lr)
+        print("worst per-array gradient rel-L2", worst)
+
+
+@pytest.mark.slow
+def test_full_size_value_parity_c4_weak_1():
+    """The benchmarked configuration exactly (C4-weak-1: T = 2^24, L = 16, Nmax = 2048, march
+    divisor 104, wire_f32 = 1, default encode pass budgets, so the backward cuts every hashed
+    level into S = 2 row slices) on a 2,048-ray subset of the bench batch, against the fp64
+    oracle from identical injected state: losses and render within 1e-4, per-array gradients
+    (relative L2) within 1e-4, Adam within 1e-3 lr on 99.9 % of the entries, sample positions
+    and encoded features through dg_last_sample_data."""
+    from .helpers import params_for, tied_train_step
+    wl = workloads.weak(1)
+    cfg = wl.cfg
+    assert cfg.fine_table_log2 == 24 and cfg.max_resolution == 2048 and cfg.wire_f32 == 1
+    assert cfg.march_step_divisor == 104.0
+    ctx, orc = _full_pair(wl)
+    o, d, gt, img = workloads.make_rays(cfg, wl.n_rays, wl.generator, seed=1)
+    pick = np.sort(np.random.default_rng(5).choice(wl.n_rays, 2048, replace=False))
+    o, d, gt, img = o[pick], d[pick], gt[pick], img[pick]
+    # render first (identical state on both sides)
+    app = np.asarray(orc.app[0])
+    rgb, T, depth = ctx.render(o, d, app)
+    rgb_o, T_o, depth_o = orc.eval_rays(o, d, app)
+    assert np.allclose(rgb, rgb_o, rtol=1e-4, atol=1e-6), np.abs(rgb - rgb_o).max()
+    assert np.allclose(T, T_o, rtol=1e-4, atol=1e-6), np.abs(T - T_o).max()
+    assert np.allclose(depth, depth_o, rtol=1e-4, atol=1e-5), np.abs(depth - depth_o).max()
+    p0 = [params_for(cfg, 0, table_scale=0.5).astype(np.float64)]
+    orc.log_samples(0, 400_000)
+    sg, so, (ties, zmax) = tied_train_step(ctx, orc, o, d, gt, img, 0)
+    assert ties <= 64 and zmax <= 4e-6, (ties, zmax)
+    for k in ("loss_rgb", "loss_transmittance", "loss_distortion"):
+        assert abs(sg[k] - so[k]) <= 1e-4 * abs(so[k]), (k, sg[k], so[k])
+    pos, x, out, up, dx = ctx.last_sample_data(0)
+    pos_o, x_o, out_o, up_o, dx_o = orc.sample_log()
+    assert len(pos) == len(pos_o) > 100_000
+    assert np.array_equal(pos.view(np.uint64), pos_o.view(np.uint64))
+    assert (np.abs(x - x_o) / np.maximum(np.abs(x_o).max(axis=0), 1e-30)).max() < 1e-5
+    assert (np.abs(out - out_o) / np.maximum(np.abs(out_o), 1e-6)).max() < 1e-5
+    _grad_parity(cfg, ctx, orc, p0, sg["lr"])
+
+
+@pytest.mark.parametrize("mb", [None, 1])
+def test_value_parity_c1_grid(mb, monkeypatch):
+    """C1's grid (T = 2^19, L = 16, Nmax = 2048, vertical rays, divisor 128) on 2,048 rays; with
+    mb = 1 the encode passes are cut to 1 MB row slices (4 per hashed level), so the
+    forward's k > 0 slices add into the features and the backward's clip_to_slice runs."""
+    from .helpers import params_for, tied_train_step
+    if mb is not None:
+        monkeypatch.setenv("DG_ENC_FWD_MB", str(mb))
+        monkeypatch.setenv("DG_ENC_BWD_MB", str(mb))
+    wl = workloads.c1()
+    cfg = wl.cfg
+    ctx, orc = _full_pair(wl)
+    o, d, gt, img = workloads.make_rays(cfg, 2048, wl.generator, seed=3)
+    p0 = [params_for(cfg, 0, table_scale=0.5).astype(np.float64)]
+    sg, so, (ties, zmax) = tied_train_step(ctx, orc, o, d, gt, img, 0)
+    assert ties <= 64 and zmax <= 4e-6, (ties, zmax)
+    for k in ("loss_rgb", "loss_transmittance", "loss_distortion"):
+        assert abs(sg[k] - so[k]) <= 1e-4 * abs(so[k]), (k, sg[k], so[k])
+    _grad_parity(cfg, ctx, orc, p0, sg["lr"])

@@ -3,8 +3,14 @@
 Bars (BASELINE.json north_star):
   * ray-segment assignment, sample positions (t, delta, cascade) and hash indices: bit-exact;
   * rendered RGB / T / depth and the three losses: within 1e-4 relative (fp32 path);
-  * gradients: relative L2 <= 1e-4 over each parameter array (atomics reorder sums);
-  * Adam: |dp_gpu - dp_ref| <= 1e-3 * lr for entries with |g| > 1e-6 * max|g|.
+  * gradients: relative L2 <= 1e-4 over each parameter array on the default tcgen05 path
+    (atomics reorder sums), with the oracle given the GPU's ReLU on/off decisions
+    (helpers.tied_train_step): a unit whose fp64 pre-activation lies within fp32 noise of 0
+    rounds to either side and switches its whole gradient contribution, so each such tie is
+    checked separately -- at most a handful per step, every one with |z| <= 4e-6;
+  * Adam: |dp_gpu - dp_ref| <= 1e-3 * lr for >= 99.9 % of the entries with |g| > 1e-6 * max|g|.
+The FFMA fp32 path (DG_MLP=ffma) recomputes its masks in the backward and is compared untied
+(its bars in TOLS).
 """
 import numpy as np
 import pytest
@@ -12,7 +18,7 @@ import pytest
 from oracle.bindings import OracleModel, OracleRun
 from paper_2405_04416_b200 import dg, layout, workloads
 
-from .helpers import app_rows, inject, rel_err, rel_l2, small_cfg
+from .helpers import app_rows, inject, rel_err, rel_l2, small_cfg, tied_train_step
 
 pytestmark = pytest.mark.gpu
 
@@ -214,21 +220,23 @@ def _check_losses(sg, so):
 
 
 # Stated gradient tolerance (per parameter array, relative L2 against the fp64 oracle).
-# Two effects bound what any fp32-parameter implementation can match, and set the bars:
-#  * ReLU kinks: the reference's init state parks every ReLU pre-activation near 0
-#    (test_field.cpp:205-207), so a few (sample, unit) pairs flip between fp32 and fp64 and
-#    their whole contribution to the density W0 / hash-table gradients switches on or off;
-#  * conditioning: at init every sample shades to nearly the same colour, so the density
-#    gradient is a difference of near-equal colours (render.cpp:163, u - tail_color).
-# Measured (tools/diag_grad4.py): fp32 FFMA path <= 1.4e-3 on grid levels at init, ~1e-6
-# from a trained-like state except isolated kink flips (<= 1e-4); MLP arrays <= 5e-5.
-# The tcgen05 split-bf16 path adds ~2^-17 operand error: grid <= 6e-3, MLP <= 3e-4.
-# Bars carry ~2-3x headroom over those measurements.  Forward outputs (rgb, T, depth,
-# losses) meet 1e-4 relative on both paths (asserted separately).
+# tcgen05 (default): the oracle is tied to the GPU's ReLU decisions (see the module
+# docstring); what remains is the split-bf16 backward GEMMs' 2^-17 operand error and fp32
+# atomics: measured <= 2e-5 on every array in every state (tools/diag/diag_grad5.py).
+# FFMA (untied): at the reference's init every ReLU pre-activation sits near 0, so a few
+# (sample, unit) pairs flip between fp32 and fp64 (measured <= 1.4e-3 on grid levels at init,
+# ~1e-6 trained, MLP <= 5e-5).
 TOLS = {  # (impl, state) -> (grid tol, mlp tol)
     ("ffma", "init"): (3e-3, 2e-4), ("ffma", "trained"): (3e-4, 2e-4),
-    ("tc", "init"): (1.5e-2, 2e-3), ("tc", "trained"): (1.5e-2, 2e-3),
+    ("tc", "init"): (1e-4, 1e-4), ("tc", "trained"): (1e-4, 1e-4),
 }
+MAX_TIES, TIE_Z = 64, 4e-6  # tied units per step and their largest |pre-activation|
+
+
+def _step(ctx, orc, o, d, gt, img, step):
+    sg, so, (ties, zmax) = tied_train_step(ctx, orc, o, d, gt, img, step)
+    assert ties <= MAX_TIES and zmax <= TIE_Z, (ties, zmax)
+    return sg, so
 
 
 def _check_update(cfg, ctx, orc, p0, lr, tols=(1e-4, 1e-4), adam_frac=0.999):
@@ -268,8 +276,7 @@ def test_train_step_parity(kx, ky, gen, n, state, impl):
     ctx, orc, _ = _pair(cfg, table_scale=scale)
     o, d, gt, img = _rays(cfg, n, gen, seed=kx + 7 * ky)
     p0 = [params_for(cfg, g, table_scale=scale) for g in range(kx * ky)]
-    sg = ctx.train_step(o, d, gt, img, step=0)
-    so = orc.train_step(o, d, gt, img, 0)
+    sg, so = _step(ctx, orc, o, d, gt, img, 0)
     _check_losses(sg, so)
     # sample positions bit-exact against cascade_march of the same items
     om = OracleModel(cfg)
@@ -285,8 +292,7 @@ def test_train_step_parity(kx, ky, gen, n, state, impl):
         assert np.array_equal(cnt, co)
         assert np.array_equal(t_g.view(np.uint64), to.view(np.uint64))
         assert np.array_equal(d_g.view(np.uint64), do.view(np.uint64))
-    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, state)],
-                  adam_frac=0.999 if impl == "ffma" else 0.99)
+    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, state)])
 
 
 def test_train_step_coarse_cascade_and_partial_occupancy(impl):
@@ -295,12 +301,10 @@ def test_train_step_coarse_cascade_and_partial_occupancy(impl):
     ctx, orc, _ = _pair(cfg, occupancy_fraction=0.6)
     o, d, gt, img = _rays(cfg, 3000, "random", seed=3)
     p0 = [layout.reference_like_init(cfg, g) for g in range(4)]
-    sg = ctx.train_step(o, d, gt, img, step=0)
-    so = orc.train_step(o, d, gt, img, 0)
+    sg, so = _step(ctx, orc, o, d, gt, img, 0)
     _check_losses(sg, so)
     assert any(ctx.last_items(g)[2] > 0 for g in range(4))  # coarse samples exist
-    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, "init")],
-                  adam_frac=0.999 if impl == "ffma" else 0.99)
+    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, "init")])
 
 
 def test_train_step_wire_f32():
@@ -317,11 +321,51 @@ def test_multi_step_tracks_oracle():
     ctx, orc, _ = _pair(cfg)
     for step in range(3):
         o, d, gt, img = _rays(cfg, 1024, "independent", seed=100 + step)
-        sg = ctx.train_step(o, d, gt, img, step=step)
-        so = orc.train_step(o, d, gt, img, step)
-        for k in LOSSES:  # state drifts slowly (Adam amplifies tiny differences): looser bar
-            assert rel_err(sg[k], so[k], 1e-9) < (1e-4 if step == 0 else 2e-2), (step, k)
+        sg, so = _step(ctx, orc, o, d, gt, img, step)
+        for k in LOSSES:  # state drifts slowly (Adam turns noise-level gradients into +-lr steps)
+            assert rel_err(sg[k], so[k], 1e-9) < (1e-4 if step == 0 else 2e-3), (step, k)
     assert ctx.get_step() == 3
+
+
+@pytest.mark.parametrize("t", [7, 300])
+def test_adam_from_injected_moments(t, impl):
+    """AdamState::step (train.cpp:91-115) past step 1: identical params, first / second moments
+    and step counts injected on both sides, one training step at worker step t, then the new
+    moments and parameters compared (the update is no longer -lr * sign(g))."""
+    cfg = small_cfg(2, 1, table_log2=13, levels=8, nmax=256, divisor=96)
+    ctx, orc, _ = _pair(cfg, table_scale=0.5)
+    rng = np.random.default_rng(t)
+    m0, v0, p0 = [], [], []
+    for g in range(2):
+        n = ctx.param_count(g)
+        m = (rng.normal(size=n) * 1e-3).astype(np.float32)
+        v = (rng.uniform(0.1, 4.0, n) * m.astype(np.float64) ** 2 + 1e-12).astype(np.float32)
+        ctx.set_adam(g, m, v, t)
+        orc.set_adam(g, m.astype(np.float64), v.astype(np.float64), t, t)
+        m0.append(m.astype(np.float64))
+        v0.append(v.astype(np.float64))
+        p0.append(ctx.get_params(g).astype(np.float64))
+    ctx.set_step(t)
+    o, d, gt, img = _rays(cfg, 2048, "independent", seed=77)
+    sg, so = _step(ctx, orc, o, d, gt, img, t)
+    _check_losses(sg, so)
+    lr = sg["lr"]
+    for g in range(2):
+        m_g, v_g, t_g = ctx.get_adam(g)
+        m_o, v_o, t_o, _ = orc.adam(g)
+        assert t_g == t_o == t + 1
+        grad_o = orc.grads(g)
+        for arr in ctx.param_layout(g):  # m = b1 m0 + (1 - b1) g, v = b2 v0 + (1 - b2) g^2
+            a = slice(arr["offset"], arr["offset"] + arr["size"])
+            assert rel_l2(m_g[a], m_o[a]) < 1e-4 and rel_l2(v_g[a], v_o[a]) < 1e-4, arr
+        big = np.abs(grad_o) > 1e-6 * np.abs(grad_o).max()
+        dp_g = ctx.get_params(g).astype(np.float64) - p0[g]
+        dp_o = orc.params(g) - p0[g]
+        err = np.abs(dp_g - dp_o)
+        assert np.mean(err[big] <= 1e-3 * lr) >= 0.999, (g, np.mean(err[big] <= 1e-3 * lr))
+        assert np.mean(err <= 1e-3 * lr) >= 0.999
+        # the update is the bias-corrected ratio, not a sign step
+        assert np.std(np.abs(dp_o[big]) / lr) > 0.05
 
 
 def test_dropped_rays_and_empty_batch():
@@ -415,10 +459,8 @@ def test_train_step_nmax_8192(impl):
     from .helpers import params_for
     o, d, gt, img = _rays(cfg, 1500, "independent", seed=21)
     p0 = [params_for(cfg, 0, table_scale=0.5)]
-    sg = ctx.train_step(o, d, gt, img, step=0)
-    so = orc.train_step(o, d, gt, img, 0)
+    sg, so = _step(ctx, orc, o, d, gt, img, 0)
     _check_losses(sg, so)
     shapes, modes, rows = ctx.grid_levels(0, 0)
     assert shapes.max() >= 8000 and modes[-1] == 1
-    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, "trained")],
-                  adam_frac=0.999 if impl == "ffma" else 0.99)
+    _check_update(cfg, ctx, orc, p0, sg["lr"], TOLS[(impl, "trained")])
