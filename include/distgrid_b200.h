@@ -184,6 +184,11 @@ int dg_get_adam(dg_ctx* ctx, uint32_t partition, float* m, float* v, uint64_t* s
 /* Worker::step_ (worker.hpp:144): the lr schedule index of the next step. */
 int dg_set_step(dg_ctx* ctx, uint64_t step);
 int dg_get_step(const dg_ctx* ctx, uint64_t* step);
+/* In-memory snapshot of the whole training state on the device (parameters, Adam moments
+ * and t, occupancy bitfields / densities / thresholds / sampling stream, step counter):
+ * restore = 0 takes it, restore = 1 puts it back (gradients zeroed), so a window of steps
+ * can be replayed from identical state. */
+int dg_state_snapshot(dg_ctx* ctx, int restore);
 /* Reference-exact initialisation (worker.cpp:186-190, grid.cpp:90-105, mlp.cpp:38-53):
  * mt19937_64 streams seeded with counter_hash(seed, 0xf1e1d|0xc0a45e, region), rounded
  * to fp32.  Host-side, once per partition (not on the per-step path). */
@@ -244,6 +249,11 @@ int dg_comm_init_host(dg_ctx* ctx, dg_alltoallv_fn fn, void* user);
  * caller implements it over its launcher's channel (MPI, torch.distributed, sockets). */
 typedef int (*dg_allgather_fn)(void* user, const void* send, uint64_t bytes, void* recv);
 int dg_comm_init_peer(dg_ctx* ctx, dg_allgather_fn fn, void* user);
+/* How long a step waits for its peers before failing (Worker::Setup::recv_timeout,
+ * worker.hpp:82; default 120000 ms).  On expiry the step returns DG_ETIMEOUT ("missing
+ * PartialScatter", worker.cpp:340-347) and an NCCL communicator is aborted (ncclCommAbort);
+ * an asynchronous NCCL failure returns DG_ENCCL.  An aborted context must be recreated. */
+int dg_set_comm_timeout(dg_ctx* ctx, uint64_t timeout_ms);
 
 /* ---- ray cache / pixel-ray batch feed ----
  * RayCache (train.cpp:117-159) over a dataset uploaded once: images (u8 RGB, row-major) and
@@ -377,7 +387,10 @@ int dg_kernel_launches(const dg_ctx* ctx, uint64_t* n);
 typedef struct dg_stage_times {
   float segment, march, encode_fwd, mlp_fwd, composite, exchange, merge_bwd, mlp_bwd, encode_bwd,
       adam, total;
-  float reserved[5];
+  /* exchange 1 alone (dispatch records to the owners; inside `segment`), and the bytes this
+   * rank sent to other ranks in exchange 1 / exchange 2 (MB) */
+  float dispatch_exchange, dispatch_mb, partial_mb;
+  float reserved[2];
 } dg_stage_times;
 int dg_enable_stage_timing(dg_ctx* ctx, int enable);
 int dg_last_stage_times(dg_ctx* ctx, dg_stage_times* t);

@@ -340,6 +340,12 @@ class RefRun(_RunBase):
         self.lib.refh_get_occupancy(self.h, g, cascade, _ptr(bits), None)
         return bits
 
+    def occupancy_density(self, g, cascade, ncells):
+        den = np.zeros(ncells)
+        bits = np.zeros(ncells, dtype=U8)
+        self.lib.refh_get_occupancy(self.h, g, cascade, _ptr(bits), _ptr(den))
+        return den
+
     def log_samples(self, g, capacity):
         """Record every training sample of partition g in the next train_step (test-only):
         sample_log() then returns (pos, features, field_out, upstream, d_features) in the GPU's

@@ -108,7 +108,8 @@ def cameras(poses):
 class StageTimes(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("segment", "march", "encode_fwd", "mlp_fwd", "composite",
                                          "exchange", "merge_bwd", "mlp_bwd", "encode_bwd",
-                                         "adam", "total")] + [("reserved", C.c_float * 5)]
+                                         "adam", "total", "dispatch_exchange", "dispatch_mb",
+                                         "partial_mb")] + [("reserved", C.c_float * 2)]
 
     def as_dict(self):
         return {n: float(getattr(self, n)) for n, _ in self._fields_ if n != "reserved"}

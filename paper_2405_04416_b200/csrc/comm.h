@@ -5,6 +5,7 @@
 // a host-staged backend that hands the blocks to a caller-provided callback (gloo).
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -28,6 +29,16 @@ class Comm {
                         const std::vector<uint64_t>& recv_bytes, cudaStream_t s,
                         std::string& err) = 0;
   virtual const char* name() const = 0;
+  // Asynchronous failure of the backend (a dead or failed peer): DG_OK or an error code.
+  virtual int poll(std::string& err) { return DG_OK; }
+  // Give up on every in-flight exchange (the device work waiting on peers returns).
+  virtual void abort() {}
+  // How long a step may wait for its peers (Worker::Setup::recv_timeout, worker.hpp:82).
+  virtual void set_timeout(std::chrono::milliseconds t) { timeout_ = t; }
+  virtual std::chrono::milliseconds timeout() const { return timeout_; }
+
+ protected:
+  std::chrono::milliseconds timeout_{120000};
 };
 
 // Exchanges over peer memory (one node, NVLink / NVSwitch): every rank's receive buffers are
@@ -70,7 +81,7 @@ class PeerComm final : public Comm {
 };
 
 Comm* make_nccl_comm(const uint8_t id[DG_NCCL_UNIQUE_ID_BYTES], int rank, int world, int device,
-                     std::string& err);
+                     std::string& err, std::chrono::milliseconds timeout);
 Comm* make_host_comm(dg_alltoallv_fn fn, void* user, int rank, int world);
 int nccl_unique_id(uint8_t id[DG_NCCL_UNIQUE_ID_BYTES], std::string& err);
 

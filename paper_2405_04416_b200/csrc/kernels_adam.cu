@@ -22,7 +22,16 @@ __device__ __forceinline__ void adam1(float& p, float& g, float& m, float& v, fl
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __restrict__ g,
                                               float4* __restrict__ m, float4* __restrict__ v,
                                               uint64_t n4, float lr, float b1, float b2, float eps,
-                                              float inv_bias1, float inv_bias2) {
+                                              float inv_bias1, float inv_bias2,
+                                              const uint32_t* __restrict__ abort_flag, uint32_t abort_mask) {
+  // An aborted step (e.g. a missing partial, worker.cpp:371-376) must leave p, m, v untouched,
+  // as the reference throws before apply_updates; its gradients are discarded.
+  if (abort_flag && (*abort_flag & abort_mask)) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (uint64_t)gridDim.x * blockDim.x)
+      g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (uint64_t)gridDim.x * blockDim.x) {
     float4 pp = p[i], gg = g[i], mm = m[i], vv = v[i];
@@ -39,9 +48,13 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __
 
 __global__ void k_adam_tail(float* p, float* g, float* m, float* v, uint64_t start, uint64_t n,
                             float lr, float b1, float b2, float eps, float inv_bias1,
-                            float inv_bias2) {
+                            float inv_bias2, const uint32_t* abort_flag, uint32_t abort_mask) {
   const uint64_t i = start + threadIdx.x;
-  if (i < n) adam1(p[i], g[i], m[i], v[i], lr, b1, b2, eps, inv_bias1, inv_bias2);
+  if (i >= n) return;
+  if (abort_flag && (*abort_flag & abort_mask))
+    g[i] = 0.f;
+  else
+    adam1(p[i], g[i], m[i], v[i], lr, b1, b2, eps, inv_bias1, inv_bias2);
 }
 
 __global__ void k_fill_uniform(float* __restrict__ p, uint64_t n, float lo, float hi, uint64_t seed) {
@@ -56,7 +69,8 @@ __global__ void k_fill_uniform(float* __restrict__ p, uint64_t n, float lo, floa
 }  // namespace
 
 void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, float b1, float b2,
-                 float eps, float inv_bias1, float inv_bias2, cudaStream_t s) {
+                 float eps, float inv_bias1, float inv_bias2, cudaStream_t s, const uint32_t* abort_flag,
+                 uint32_t abort_mask) {
   const uint64_t n4 = n / 4;
   if (n4) {
     int dev = 0, sms = 148;
@@ -66,9 +80,11 @@ void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, f
     const unsigned grid = (unsigned)(want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8);
     k_adam<<<grid, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<float4*>(g),
                                 reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, lr,
-                                b1, b2, eps, inv_bias1, inv_bias2);
+                                b1, b2, eps, inv_bias1, inv_bias2, abort_flag, abort_mask);
   }
-  if (n % 4) k_adam_tail<<<1, 4, 0, s>>>(p, g, m, v, n4 * 4, n, lr, b1, b2, eps, inv_bias1, inv_bias2);
+  if (n % 4)
+    k_adam_tail<<<1, 4, 0, s>>>(p, g, m, v, n4 * 4, n, lr, b1, b2, eps, inv_bias1, inv_bias2, abort_flag,
+                                abort_mask);
 }
 
 void launch_fill_uniform(float* p, uint64_t n, float lo, float hi, uint64_t seed, cudaStream_t s) {

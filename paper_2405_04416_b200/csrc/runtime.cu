@@ -22,6 +22,7 @@
 #include <cstring>
 #include <chrono>
 #include <future>
+#include <thread>
 #include <tuple>
 #include <memory>
 #include <random>
@@ -152,6 +153,10 @@ struct dg_ctx {
   uint64_t occ_host_n = 0;                // doubles
   std::future<void> occ_prefetch;
   bool occ_prefetched = false;
+  // occ_rng before the pending prefetch drew from it: restored when the step is moved
+  // (dg_set_step / checkpoint load) so the stream holds exactly the draws of the updates that
+  // actually ran, as the reference's occ_rng_ does (load_state leaves it alone, worker.cpp:615-626)
+  std::vector<std::mt19937_64> occ_rng_before;
   // ... and go up to the device on a copy stream as soon as they are drawn, so the 24 B/cell
   // transfer overlaps the training steps before the update instead of stalling it
   cudaStream_t stream_copy = nullptr;
@@ -172,11 +177,20 @@ struct dg_ctx {
   int num_sms = 148;
   int mlp_impl = 1;  // 1: tcgen05 split-bf16 forward (default), 0: FFMA fp32 (DG_MLP=ffma)
   std::unique_ptr<Comm> comm;
+  uint64_t comm_timeout_ms = 120000;  // Worker::Setup::recv_timeout (worker.hpp:82)
   uint64_t launches = 0;
   bool timing = false;
   cudaEvent_t ev[12] = {};
   dg_stage_times times{};
 
+  // in-memory snapshot of the training state (dg_state_snapshot)
+  struct Snapshot {
+    DBuf params, m, v, occ, occ_den;
+    std::vector<double> occ_thr;
+    std::vector<std::mt19937_64> occ_rng;
+    uint64_t adam_t = 0, worker_step = 0;
+    bool valid = false;
+  } snap;
   // persistent device state
   DBuf out_attr, cam_o, cam_d, cam_pose, it_xdist, send_x, recv_x, it_runs, it_runc, it_nrun;
   bool cross_active = false;  // training step with distortion_cross_correction
@@ -390,8 +404,36 @@ void* pin_alloc(dg_ctx* c, size_t bytes) {
   return c->pin + at;
 }
 
+// Wait for the step's stream.  With a multi-rank backend the wait polls the backend for
+// asynchronous failures and gives up after its timeout (Worker::Setup::recv_timeout,
+// worker.hpp:82): a dead or stalled peer turns into DG_ETIMEOUT / DG_ENCCL (the reference
+// throws "missing PartialScatter", worker.cpp:340-347) instead of a hang; the backend is then
+// aborted so the device work blocked on the peer returns.
+int step_sync(dg_ctx* c) {
+  if (!c->comm || c->world == 1) {
+    CU(cudaStreamSynchronize(c->stream));
+    return DG_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto deadline = t0 + c->comm->timeout();
+  for (uint32_t spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(c->stream);
+    if (e == cudaSuccess) return DG_OK;
+    if (e != cudaErrorNotReady) return set_err(DG_ECUDA, "CUDA error: %s", cudaGetErrorString(e));
+    std::string err;
+    const int rc = c->comm->poll(err);
+    if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
+    if (std::chrono::steady_clock::now() > deadline) {
+      c->comm->abort();
+      return set_err(DG_ETIMEOUT, "worker: missing PartialScatter (no progress from peers within %lld ms)",
+                     (long long)c->comm->timeout().count());
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
 int pin_reset(dg_ctx* c) {
-  CU(cudaStreamSynchronize(c->stream));  // nothing in flight reads the arena any more
+  TRY(step_sync(c));  // nothing in flight reads the arena any more
   c->pin_used = 0;
   return DG_OK;
 }
@@ -605,7 +647,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   CU(cudaMemcpy2DAsync(ss_pin ? ss_pin : slot_start.data(), 4, c->h_pos.as<uint32_t>(), n ? n * 4 : 4, 4,
                        P + 1, cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(dr_pin ? dr_pin : &dropped, c->dropped.p, 8, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
+  TRY(step_sync(c));
   if (ss_pin) std::memcpy(slot_start.data(), ss_pin, (P + 1) * 4);
   if (dr_pin) dropped = *dr_pin;
   c->d2h += (P + 1) * 4 + 8;
@@ -620,6 +662,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   std::vector<uint32_t> pio(nl + 1, 0);
   uint64_t n_items = 0;
   if (c->world == 1) {
+    mark(c, 11);
     for (uint32_t lp = 0; lp < nl; ++lp) pio[lp + 1] = pio[lp] + uint32_t(send_cnt[c->local[lp]]);
     n_items = total_send;
     TRY(c->rec.ensure(n_items * sizeof(RayRec) + 16));
@@ -665,6 +708,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
       tab.insert(tab.end(), plan.block_dst.begin(), plan.block_dst.end());
       TRY(upload_small(c, c->perm_tab, tab.data(), tab.size() * 8));
     }
+    mark(c, 11);
     launch_pack_dispatch(n, P, c->h_nseg.as<uint8_t>(), c->h_sched.as<uint8_t>(),
                          c->slot_of_part_d.as<uint8_t>(), c->h_pos.as<uint32_t>(), o, d, gt, img,
                          b->first_ray_id, nullptr,
@@ -697,7 +741,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
     uint64_t* cr_pin = pin_slot<uint64_t>(c, cnt_recv.size());
     CU(cudaMemcpyAsync(cr_pin ? cr_pin : cnt_recv.data(), c->recv_buf.p, cnt_recv.size() * 8,
                        cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
+    TRY(step_sync(c));
     if (cr_pin) std::memcpy(cnt_recv.data(), cr_pin, cnt_recv.size() * 8);
     c->h2d += cnt_send.size() * 8;
     c->d2h += cnt_recv.size() * 8;
@@ -706,6 +750,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
     plan_dispatch(c->rank, W, P, send_cnt.data(), cnt_recv.data(), sizeof(RayRec), plan);
     n_items = plan.n_items;
     TRY(c->x_recv.ensure(n_items * sizeof(RayRec) + 16));
+    mark(c, 11);
     rc = c->comm->alltoallv(c->x_send.p, plan.send_bytes, c->x_recv.p, plan.recv_bytes, s, err);
     if (rc != DG_OK) return set_err(rc, "%s", err.c_str());
     for (int r = 0; r < W; ++r)
@@ -772,7 +817,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
                        cudaMemcpyDeviceToHost, s));
   }
   CU(cudaMemcpyAsync(fo_pin ? &fo_pin[fo.size()] : &err_flag, c->error.p, 4, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
+  TRY(step_sync(c));
   if (fo_pin) {
     std::memcpy(fo.data(), fo_pin, fo.size() * 4);
     err_flag = fo_pin[fo.size()];
@@ -1053,6 +1098,7 @@ bool next_update_is_warm(const dg_ctx* c, uint64_t after_step) {
 
 void occ_start_prefetch(dg_ctx* c) {
   if (!c->occ_host || !next_update_is_warm(c, c->worker_step)) return;
+  c->occ_rng_before = c->occ_rng;
   c->occ_prefetch = std::async(std::launch::async, [c] { occ_generate_warm(c); });
   c->occ_prefetched = true;
   c->occ_uploaded = false;
@@ -1091,6 +1137,7 @@ int occupancy_update(dg_ctx* c) {
   const uint32_t nl = uint32_t(c->local.size());
   if (warm_up) {
     if (!c->occ_prefetched) {  // nothing drawn ahead (e.g. state just injected): draw now
+      c->occ_rng_before = c->occ_rng;
       c->occ_prefetch = std::async(std::launch::deferred, [c] { occ_generate_warm(c); });
       c->occ_prefetched = true;
       c->occ_uploaded = false;
@@ -1392,14 +1439,66 @@ int dg_get_adam(dg_ctx* c, uint32_t p, float* m, float* v, uint64_t* t) {
 
 int dg_set_step(dg_ctx* c, uint64_t step) {
   TRY(check_ctx(c));
+  if (c->occ_prefetched) {
+    // undo the draws of a prefetch made for the old step: wait for the drawing thread and the
+    // upload that reads its pinned buffer, then rewind the stream to before it
+    if (c->occ_prefetch.valid()) c->occ_prefetch.wait();
+    if (c->occ_uploaded) CU(cudaEventSynchronize(c->ev_occ_up));
+    c->occ_rng = c->occ_rng_before;
+    c->occ_prefetched = c->occ_uploaded = false;
+  }
   c->worker_step = step;
-  if (!c->occ_prefetched) occ_start_prefetch(c);
+  occ_start_prefetch(c);
   return DG_OK;
 }
 
 int dg_get_step(const dg_ctx* c, uint64_t* step) {
   TRY(check_ctx(c));
   *step = c->worker_step;
+  return DG_OK;
+}
+
+// Device-side copy of everything a training step mutates (parameters, Adam moments and t,
+// occupancy bitfields / densities / thresholds / sampling stream, the step counter), so a
+// window of steps can be replayed from the same state (e.g. bench.py's end-to-end pass).
+int dg_state_snapshot(dg_ctx* c, int restore) {
+  TRY(check_ctx(c));
+  CU(cudaSetDevice(c->device));
+  dg_ctx::Snapshot& sn = c->snap;
+  const size_t pb = std::max<uint64_t>(c->n_params, 4) * sizeof(float);
+  const size_t ob = c->occ_bytes, db = c->occ_den_n * sizeof(float);
+  struct Pair {
+    DBuf* live;
+    DBuf* copy;
+    size_t bytes;
+  } pairs[] = {{&c->params, &sn.params, pb}, {&c->adam_m, &sn.m, pb}, {&c->adam_v, &sn.v, pb},
+               {&c->occ, &sn.occ, ob}, {&c->occ_den, &sn.occ_den, db}};
+  TRY(step_sync(c));
+  if (c->occ_prefetch.valid()) c->occ_prefetch.wait();
+  if (c->occ_uploaded) CU(cudaEventSynchronize(c->ev_occ_up));
+  if (!restore) {
+    for (Pair& p : pairs) {
+      TRY(p.copy->ensure(p.bytes));
+      CU(cudaMemcpyAsync(p.copy->p, p.live->p, p.bytes, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    sn.occ_thr = c->occ_thr;
+    sn.occ_rng = c->occ_prefetched ? c->occ_rng_before : c->occ_rng;
+    sn.adam_t = c->adam_t;
+    sn.worker_step = c->worker_step;
+    sn.valid = true;
+  } else {
+    if (!sn.valid) return set_err(DG_EINVAL, "no snapshot taken");
+    for (Pair& p : pairs)
+      CU(cudaMemcpyAsync(p.live->p, p.copy->p, p.bytes, cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemsetAsync(c->grads.p, 0, pb, c->stream));
+    c->occ_thr = sn.occ_thr;
+    c->occ_rng = sn.occ_rng;
+    c->adam_t = sn.adam_t;
+    c->worker_step = sn.worker_step;
+    c->occ_prefetched = c->occ_uploaded = false;
+    occ_start_prefetch(c);
+  }
+  CU(cudaStreamSynchronize(c->stream));
   return DG_OK;
 }
 
@@ -1596,6 +1695,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   c->cross_active = c->cfg.distortion_cross_correction != 0;
   TRY(occ_try_upload(c, false));
   TRY(front_half(c, b, 1, step, &dropped, &bytes));
+  const uint64_t bytes_x1 = bytes;
   const uint32_t NI = c->n_items;
   ItemArrays it = item_arrays(c);
   SampleArrays sm = sample_arrays(c);
@@ -1629,7 +1729,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   c->launches += 3;
   // X2: partial exchange (alias on a single rank)
   if (P > 1) {
-    CU(cudaStreamSynchronize(s));  // pair counts on the host
+    TRY(step_sync(c));  // pair counts on the host
     if (pair_pin) std::memcpy(pair_cnt.data(), pair_pin, pair_cnt.size() * 4);
   }
   const PartialRec* recv = c->send_buf.as<PartialRec>();
@@ -1662,27 +1762,34 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   c->launches += 3;
   // K6 Adam over every local parameter, lr at the pre-increment step (worker.cpp:544)
   const double lr = dg_lr_at(&c->cfg, c->worker_step);
-  c->adam_t += 1;
-  const double bias1 = 1.0 - std::pow(c->cfg.adam_beta1, double(c->adam_t));
-  const double bias2 = 1.0 - std::pow(c->cfg.adam_beta2, double(c->adam_t));
+  const double bias1 = 1.0 - std::pow(c->cfg.adam_beta1, double(c->adam_t + 1));
+  const double bias2 = 1.0 - std::pow(c->cfg.adam_beta2, double(c->adam_t + 1));
+  // k_adam skips the update (and discards the gradients) when the merge flagged a missing
+  // partial, so an aborted step leaves params, moments, t and the step counter untouched
+  // (the reference throws before apply_updates, worker.cpp:371-380)
   launch_adam(c->params.as<float>(), c->grads.as<float>(), c->adam_m.as<float>(), c->adam_v.as<float>(),
               c->n_params, float(lr), float(c->cfg.adam_beta1), float(c->cfg.adam_beta2),
-              float(c->cfg.adam_eps), float(1.0 / bias1), float(1.0 / bias2), s);
+              float(c->cfg.adam_eps), float(1.0 / bias1), float(1.0 / bias2), s,
+              &c->loss.as<LossAccum>()->error, 2u);
   ++c->launches;
   mark(c, 10);
-  c->worker_step = step + 1;
-  TRY(occupancy_update(c));
   LossAccum la;
   LossAccum* la_pin = pin_slot<LossAccum>(c, 1);
   CU(cudaMemcpyAsync(la_pin ? la_pin : &la, c->loss.p, sizeof la, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
+  TRY(step_sync(c));
   if (la_pin) la = *la_pin;
   c->d2h += sizeof la;
   if (la.error & 2u) return set_err(DG_EPROTO, "worker: missing partial in batch %llu", (unsigned long long)step);
+  c->adam_t += 1;
+  c->worker_step = step + 1;
+  TRY(occupancy_update(c));
   if (c->timing) {
     float* t = &c->times.segment;
     for (int k = 0; k < 10; ++k) cudaEventElapsedTime(&t[k], c->ev[k], c->ev[k + 1]);
     cudaEventElapsedTime(&c->times.total, c->ev[0], c->ev[10]);
+    cudaEventElapsedTime(&c->times.dispatch_exchange, c->ev[11], c->ev[1]);
+    c->times.dispatch_mb = float(double(bytes_x1) * 1e-6);
+    c->times.partial_mb = float(double(bytes - bytes_x1) * 1e-6);
   }
   if (stats) {
     std::memset(stats, 0, sizeof *stats);
@@ -1769,7 +1876,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
     // re-derive counts from the perm table (src_start, dst_start) uploaded in front_half
     std::vector<uint64_t> perm(2 * uint64_t(nl) * W);
     CU(cudaMemcpyAsync(perm.data(), c->perm_tab.p, perm.size() * 8, cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
+    TRY(step_sync(c));
     const uint32_t nblk = nl * uint32_t(W);
     std::vector<uint64_t> cnt(nblk);
     for (uint32_t k = 0; k < nblk; ++k)
@@ -1814,7 +1921,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
     std::vector<uint32_t> slot_start(c->P + 1);
     CU(cudaMemcpy2DAsync(slot_start.data(), 4, c->h_pos.as<uint32_t>(), n ? n * 4 : 4, 4, c->P + 1,
                          cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
+    TRY(step_sync(c));
     for (uint32_t p = 0; p < c->P; ++p)
       rbytes[c->part_rank[p]] +=
           uint64_t(slot_start[c->slot_of_part[p] + 1] - slot_start[c->slot_of_part[p]]) * sizeof(PartialRec);
@@ -1837,7 +1944,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
     CU(cudaMemcpyAsync(out->depth, dep, n * 4, cudaMemcpyDeviceToHost, s));
     if (attr) CU(cudaMemcpyAsync(out->attribution, attr, n * 12, cudaMemcpyDeviceToHost, s));
   }
-  CU(cudaStreamSynchronize(s));
+  TRY(step_sync(c));
   return DG_OK;
 }
 
@@ -1877,9 +1984,18 @@ int dg_comm_unique_id(uint8_t id[DG_NCCL_UNIQUE_ID_BYTES]) {
 int dg_comm_init_nccl(dg_ctx* c, const uint8_t id[DG_NCCL_UNIQUE_ID_BYTES]) {
   TRY(check_ctx(c));
   std::string err;
-  Comm* comm = make_nccl_comm(id, c->rank, c->world, c->device, err);
+  Comm* comm = make_nccl_comm(id, c->rank, c->world, c->device, err,
+                              std::chrono::milliseconds(c->comm_timeout_ms));
   if (!comm) return set_err(DG_ENCCL, "%s", err.c_str());
   c->comm.reset(comm);
+  return DG_OK;
+}
+
+int dg_set_comm_timeout(dg_ctx* c, uint64_t timeout_ms) {
+  TRY(check_ctx(c));
+  if (timeout_ms == 0) return set_err(DG_EINVAL, "timeout must be positive");
+  c->comm_timeout_ms = timeout_ms;
+  if (c->comm) c->comm->set_timeout(std::chrono::milliseconds(timeout_ms));
   return DG_OK;
 }
 
@@ -1887,6 +2003,7 @@ int dg_comm_init_host(dg_ctx* c, dg_alltoallv_fn fn, void* user) {
   TRY(check_ctx(c));
   if (!fn) return set_err(DG_EINVAL, "null callback");
   c->comm.reset(make_host_comm(fn, user, c->rank, c->world));
+  c->comm->set_timeout(std::chrono::milliseconds(c->comm_timeout_ms));
   return DG_OK;
 }
 
@@ -1895,6 +2012,7 @@ int dg_comm_init_peer(dg_ctx* c, dg_allgather_fn fn, void* user) {
   if (!fn) return set_err(DG_EINVAL, "null callback");
   CU(cudaSetDevice(c->device));
   c->comm.reset(new PeerComm(fn, user, c->rank, c->world));
+  c->comm->set_timeout(std::chrono::milliseconds(c->comm_timeout_ms));
   return DG_OK;
 }
 

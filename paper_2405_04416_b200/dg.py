@@ -177,6 +177,10 @@ class Context:
         _check(lib().dg_get_step(self.h, C.byref(v)))
         return v.value
 
+    def snapshot(self, restore=False):
+        """dg_state_snapshot: take (restore=False) or restore the device-side training state."""
+        _check(lib().dg_state_snapshot(self.h, 1 if restore else 0))
+
     def init_reference(self, g):
         _check(lib().dg_init_params_reference(self.h, C.c_uint32(g)))
 
@@ -273,6 +277,10 @@ class Context:
     def comm_init_nccl(self, uid_bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid_bytes))
         _check(lib().dg_comm_init_nccl(self.h, buf))
+
+    def set_comm_timeout(self, ms):
+        """Worker::Setup::recv_timeout (worker.hpp:82): DG_ETIMEOUT after `ms` without peers."""
+        _check(lib().dg_set_comm_timeout(self.h, C.c_uint64(int(ms))))
 
     def comm_init_host(self, fn):
         """fn(send: bytes-like per peer list, recv_sizes) -> list of received bytes (rank order)."""

@@ -98,3 +98,45 @@ def test_checkpoint_rejects_mismatch():
             f.write(b"XXXX")
         with pytest.raises(dg.DGError):
             ctx.load_checkpoint(0, path)
+
+
+def test_resume_past_warmup_keeps_occupancy_stream():
+    """a fresh context draws the next warm-up update's jitter points ahead of time
+    from its occupancy mt19937_64 stream.  Loading a checkpoint past the warm-up must rewind
+    those draws, so the first sampled (non-warm-up) update after the resume takes the same
+    cells and jitter points as the reference's fresh Worker after load_state
+    (worker.cpp:549-562, 615-626)."""
+    cfg = small_cfg(2, 1, table_log2=12, levels=8, nmax=128, divisor=64, occ_res=16,
+                    inner=((0.2, 0.1, 0.0), (1.7, 0.9, 0.9)))
+    cfg.occ_warmup_steps = 8
+    cfg.occ_update_interval = 4
+    cfg.occ_threshold_scale = 2.5  # a mixed bitfield
+    app = app_rows(1)
+    ctx = dg.Context(cfg, device=0)  # prefetches the warm-up update of step 4 from a fresh stream
+    ctx.set_appearance(app.astype(np.float32))
+    src = RefRun(cfg, app)
+    inject(cfg, None, [src], occupancy_fraction=0.7, table_scale=0.5)
+    for g in range(2):
+        m, v, _, _ = src.adam(g)
+        src.set_adam(g, m, v, 10, 10)  # a state saved at step 10 > occ_warmup_steps
+    ref = RefRun(cfg, app)  # fresh Worker + load_state, as a resumed reference run
+    with tempfile.TemporaryDirectory() as td:
+        for g in range(2):
+            path = os.path.join(td, f"s{g}.dgcw")
+            src.save_checkpoint(g, HASH, path)
+            ctx.load_checkpoint(g, path)
+            ref.load_checkpoint(g, path)
+    assert ctx.get_step() == 10
+    for step in (10, 11):  # the update after step 11 samples 1/4 uniform + 1/4 occupied cells
+        o, d, gt, img = workloads.make_rays(cfg, 512, "random", seed=step)
+        ctx.train_step(o, d, gt, img, step=step)
+        ref.train_step(o, d, gt, img, step)
+    for g in range(2):
+        for c, box in enumerate(layout.region_boxes(cfg, g)):
+            n = int(np.prod(layout.occupancy_shape(cfg, box)))
+            dg_den, _ = ctx.occupancy_density(g, c)
+            rf_den = ref.occupancy_density(g, c, n)
+            close = np.abs(dg_den - rf_den) <= 1e-3 * np.abs(rf_den) + 1e-6
+            # a different stream would decay and refresh different cells (~40 % of them)
+            assert close.mean() > 0.995, (g, c, close.mean())
+            assert np.mean(ctx.get_occupancy(g, c) == ref.occupancy(g, c, n)) > 0.995

@@ -58,7 +58,29 @@ def _gloo_allgather(blob):
     return out
 
 
-def _rank_main(rank, world, port, ref_path, errq, cross=0, backend="host"):
+class _Corrupting:
+    """Host all-to-all that, while armed, bumps the ray id of every partial record of the
+    step's third exchange (counts, dispatch records, partials): every owner then sees a
+    "missing partial" (worker.cpp:371-376)."""
+
+    def __init__(self):
+        self.armed, self.calls = False, 0
+
+    def __call__(self, blocks, recv_sizes):
+        got = _gloo_alltoallv(blocks, recv_sizes)
+        self.calls += 1
+        if self.armed and self.calls == 3:
+            out = []
+            for b in got:
+                a = np.frombuffer(b, np.uint32).copy()
+                assert a.size % 6 == 0
+                a[5::6] += 1
+                out.append(a.tobytes())
+            return out
+        return got
+
+
+def _rank_main(rank, world, port, ref_path, errq, cross=0, backend="host", corrupt=False):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -66,10 +88,11 @@ def _rank_main(rank, world, port, ref_path, errq, cross=0, backend="host"):
         from paper_2405_04416_b200 import dg
         cfg = _cfg(cross)
         ctx = dg.Context(cfg, device=0, rank=rank, world=world)
+        corr = _Corrupting()
         if backend == "peer":
             ctx.comm_init_peer(_gloo_allgather)
         else:
-            ctx.comm_init_host(_gloo_alltoallv)
+            ctx.comm_init_host(corr if corrupt else _gloo_alltoallv)
         inject(cfg, None, [_LocalOnly(ctx)], occupancy_fraction=0.6)
         ctx.set_appearance(app_rows(1).astype(np.float32))
         o, d, gt, img = _rays()
@@ -84,6 +107,22 @@ def _rank_main(rank, world, port, ref_path, errq, cross=0, backend="host"):
         assert np.allclose(rgb, ref["rgb"][lo:hi], rtol=1e-5, atol=1e-6), np.abs(rgb - ref["rgb"][lo:hi]).max()
         assert np.allclose(T, ref["T"][lo:hi], rtol=1e-5, atol=1e-6)
         assert np.allclose(depth, ref["depth"][lo:hi], rtol=1e-5, atol=1e-5)
+        if corrupt:
+            # a step whose partials do not match aborts with DG_EPROTO before anything is
+            # committed: params, Adam moments / t and the step counter are untouched and the
+            # gradients are discarded, so the retried step equals the clean run
+            before = {g: ctx.get_params(g) for g in ctx.local}
+            corr.armed, corr.calls = True, 0
+            with pytest.raises(dg.DGError) as e:
+                ctx.train_step(o[lo:hi], d[lo:hi], gt[lo:hi], img[lo:hi], step=0, first_ray_id=lo)
+            assert e.value.status == "DG_EPROTO" and "missing partial" in str(e.value), e.value
+            corr.armed = False
+            assert ctx.get_step() == 0
+            for g in ctx.local:
+                assert np.array_equal(ctx.get_params(g), before[g])
+                m, v, t = ctx.get_adam(g)
+                assert t == 0 and not m.any() and not v.any()
+                assert not ctx.get_grads(g).any()
         losses = []
         for step in range(STEPS):
             st = ctx.train_step(o[lo:hi], d[lo:hi], gt[lo:hi], img[lo:hi], step=step, first_ray_id=lo)
@@ -123,11 +162,7 @@ class _LocalOnly:
             self.ctx.set_occupancy(g, c, bits)
 
 
-@pytest.mark.parametrize("backend,world", [("host", 2), ("peer", 2), ("peer", 3), ("peer", 4)])
-@pytest.mark.parametrize("cross", [0, 1])
-def test_two_ranks_match_single_rank(cross, backend, world):
-    """world = 3 puts partitions {0, 3}, {1}, {2} on the three ranks (uneven ownership); world = 4
-    is the deployment layout, one partition per rank."""
+def _run_ranks(cross, backend, world, corrupt=False):
     from paper_2405_04416_b200 import dg
     cfg = _cfg(cross)
     ctx = dg.Context(cfg, device=0)
@@ -153,7 +188,7 @@ def test_two_ranks_match_single_rank(cross, backend, world):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
         s.close()
-        procs = [mpc.Process(target=_rank_main, args=(r, world, port, path, errq, cross, backend))
+        procs = [mpc.Process(target=_rank_main, args=(r, world, port, path, errq, cross, backend, corrupt))
                  for r in range(world)]
         for p in procs:
             p.start()
@@ -164,6 +199,21 @@ def test_two_ranks_match_single_rank(cross, backend, world):
             errs.append(errq.get())
         assert not errs, errs
         assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+@pytest.mark.parametrize("backend,world", [("host", 2), ("peer", 2), ("peer", 3), ("peer", 4)])
+@pytest.mark.parametrize("cross", [0, 1])
+def test_two_ranks_match_single_rank(cross, backend, world):
+    """world = 3 puts partitions {0, 3}, {1}, {2} on the three ranks (uneven ownership); world = 4
+    is the deployment layout, one partition per rank."""
+    _run_ranks(cross, backend, world)
+
+
+def test_missing_partial_aborts_step_without_commit():
+    """a step that fails the partial protocol check must not reach Adam, the step
+    counter or the occupancy update (the reference throws before apply_updates,
+    worker.cpp:371-380); retrying the batch then reproduces the clean world = 1 run."""
+    _run_ranks(0, "host", 2, corrupt=True)
 
 
 def test_nccl_backend_initialises_single_rank():
