@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 1
+#define DG_ABI_VERSION 2
 #define DG_MAX_SEGMENTS 16   /* kx + ky - 1 <= 16  (partition.cpp:254-296) */
 #define DG_MAX_PARTITIONS 64 /* kx * ky <= 64 */
 #define DG_MAX_LEVELS 16     /* grid_levels; F must be 2 on the device path */
@@ -126,6 +126,10 @@ typedef struct dg_step_stats {
   uint64_t items;        /* (ray, partition) segments owned by this rank */
   uint64_t h2d_bytes;    /* host->device bytes this call moved (batch staging + tables) */
   uint64_t d2h_bytes;    /* device->host bytes this call moved (counts, losses) */
+  /* exchange 2 alone (PartialScatter, wire.cpp:72-90): bytes and records this rank sent to
+   * other ranks (DistributedRun::scatter_payload_bytes / scatter_entries) */
+  uint64_t partial_bytes_sent;
+  uint64_t partial_records_sent;
 } dg_step_stats;
 
 /* render.hpp:38-43 MergedRender, structure of arrays. */
@@ -315,6 +319,14 @@ int dg_encode_backward(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const 
 int dg_field_forward(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const double* points,
                      const float* dirs, const float* appearance, uint64_t n, float* sigma,
                      float* rgb, int32_t mem);
+/* query_density (field.cpp:230-254) alone: sigma = exp(clip(raw0)) and the 15 clipped density
+ * features per point (host buffers). */
+int dg_field_density(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const double* points, uint64_t n,
+                     float* sigma, float* features);
+/* query_color (field.cpp:256-288) alone from caller-given density features (n x 15), unit
+ * directions and appearance rows (n x appearance_dim) -> rgb (host buffers). */
+int dg_field_color(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const float* features, const float* dirs,
+                   const float* appearance, uint64_t n, float* rgb);
 /* field_backward (field.cpp:290-327): accumulates into the grad sink. */
 int dg_field_backward(dg_ctx* ctx, uint32_t partition, uint32_t cascade, const double* points,
                       const float* dirs, const float* appearance, const float* sigma_grad,
@@ -360,6 +372,52 @@ int dg_ray_losses(dg_ctx* ctx, const float* rgb, const float* color_gt, const fl
 int dg_distortion_loss(dg_ctx* ctx, const double* weights, const double* midpoints,
                        const double* interval_lengths, const uint64_t* seg_off, uint64_t n_seg,
                        double* loss, double* grads, int32_t mem);
+
+/* ---- fp64 twins of the compositing stages (the C++ facade's reference-precision path,
+ * include/distgrid/render.hpp, train.hpp): the same kernels with double inputs / outputs.
+ * dg_local_render_f64 can also return the LocalRenderCache (alpha, prefix per sample). */
+int dg_local_render_f64(dg_ctx* ctx, const double* t, const double* delta, const double* sigma,
+                        const double* rgb, const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0,
+                        const double* ray_t1, double* out_rgb, double* out_transmittance,
+                        double* out_depth_sum, double* out_distortion, double* out_cache, int32_t mem);
+int dg_local_render_backward_f64(dg_ctx* ctx, const double* t, const double* delta, const double* sigma,
+                                 const double* rgb, const uint64_t* seg_off, uint64_t n_seg,
+                                 const double* d_rgb, const double* d_transmittance,
+                                 const double* weight_upstream, double* sigma_grad, double* rgb_grad,
+                                 int32_t mem);
+int dg_merge_forward_f64(dg_ctx* ctx, const double* seg_rgb, const double* seg_transmittance,
+                         const double* seg_depth_sum, const uint64_t* ray_off, uint64_t n_rays, double* rgb,
+                         double* transmittance, double* depth, int32_t mem);
+int dg_merge_backward_f64(dg_ctx* ctx, const double* seg_rgb, const double* seg_transmittance,
+                          const uint64_t* ray_off, uint64_t n_rays, const double* d_rgb,
+                          const double* d_transmittance, double* seg_d_rgb, double* seg_d_transmittance,
+                          int32_t mem);
+int dg_ray_losses_f64(dg_ctx* ctx, const double* rgb, const double* color_gt, const double* transmittance,
+                      uint64_t n, double eps, double* loss_rgb, double* loss_transmittance, double* d_rgb,
+                      double* d_transmittance, int32_t mem);
+/* accumulate_distortion_stats (render.cpp:80-99) from a LocalRenderCache (alpha, prefix per
+ * sample, as dg_local_render_f64 returns it): out[3 * g] = weight_sum, weight_moment,
+ * distortion_local of segment g over its ray span; segments with an empty span are left as
+ * they are (out is read and written). */
+int dg_distortion_stats_f64(dg_ctx* ctx, const double* t, const double* delta, const double* cache,
+                            const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0, const double* ray_t1,
+                            double* out, int32_t mem);
+/* ray_aabb_intersect (geometry.cpp:7-28) of n rays against one box: hit, t_near, t_far. */
+int dg_ray_aabb(dg_ctx* ctx, const double* origin, const double* dir, uint64_t n, const double box_lo[3],
+                const double box_hi[3], uint8_t* hit, double* t_near, double* t_far, int32_t mem);
+/* march_segment (render.cpp:10-37) over caller-given occupied intervals: segment g spans
+ * [t_enter[g], t_exit[g]) with intervals [interval_off[g], interval_off[g+1]) of `intervals`
+ * (t_near, t_far pairs).  Two phases as dg_cascade_march: counts only (t == NULL), then the
+ * samples at offsets[g].  jitter: offset = step * counter_uniform(jitter_seed, ray_id[g],
+ * jitter_step), else step / 2.  DG_EINVAL unless step > 0. */
+int dg_march_segment(dg_ctx* ctx, const double* t_enter, const double* t_exit, const uint64_t* interval_off,
+                     const double* intervals, const uint64_t* ray_id, uint64_t n, double step, int32_t jitter,
+                     uint64_t jitter_seed, uint64_t jitter_step, uint32_t* counts, const uint64_t* offsets,
+                     double* t, double* delta, int32_t mem);
+/* AdamState::step (train.cpp:91-115) on one caller-owned fp64 array: m, v updated in place,
+ * t = the step count after this step (bias corrections 1 - beta^t). */
+int dg_adam_update_f64(dg_ctx* ctx, double* params, const double* grads, double* m, double* v, uint64_t n,
+                       uint64_t t, double lr, double beta1, double beta2, double eps, int32_t mem);
 
 /* ---- introspection of the last dg_train_step / dg_render on this rank ---- */
 typedef struct dg_item_view {

@@ -67,7 +67,8 @@ class StepStats(C.Structure):
                 ("loss_transmittance", C.c_double), ("loss_distortion", C.c_double),
                 ("lr", C.c_double), ("rays", C.c_uint64), ("dropped_rays", C.c_uint64),
                 ("bytes_sent", C.c_uint64), ("samples", C.c_uint64), ("items", C.c_uint64),
-                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("partial_bytes_sent", C.c_uint64), ("partial_records_sent", C.c_uint64)]
 
 
 class Merged(C.Structure):

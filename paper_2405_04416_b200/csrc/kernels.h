@@ -194,21 +194,45 @@ void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);
 void launch_mlp_bwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);  // tile_off at 128
 
 // ---- compositing stage entry points (kernels_render_api.cu), fp64 like the reference ----
-void launch_local_render(const double* t, const double* delta, const float* sigma, const float* rgb,
+// fp64 arithmetic in the reference's order; R = float (the C ABI's fp32 stage I/O) or double
+// (the *_f64 entry points behind the C++ facade, include/distgrid/*.hpp)
+template <class R>
+void launch_local_render(const double* t, const double* delta, const R* sigma, const R* rgb,
                          const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0,
-                         const double* ray_t1, float* out_rgb, float* out_T, float* out_depth,
+                         const double* ray_t1, R* out_rgb, R* out_T, R* out_depth,
                          double* out_dist, double* cache, cudaStream_t s);
-void launch_local_render_bwd(const double* delta, const float* rgb, const uint64_t* seg_off, uint64_t n_seg,
-                             const double* cache, const float* d_rgb, const float* d_T, const float* w_up,
-                             float* sigma_grad, float* rgb_grad, cudaStream_t s);
-void launch_merge_fwd(const float* srgb, const float* sT, const float* sdepth, const uint64_t* ray_off,
-                      uint64_t n_rays, float* rgb, float* T, float* depth, cudaStream_t s);
-void launch_merge_bwd(const float* srgb, const float* sT, const uint64_t* ray_off, uint64_t n_rays,
-                      const float* d_rgb, const float* d_T, float* sd_rgb, float* sd_T, cudaStream_t s);
-void launch_ray_losses(const float* rgb, const float* gt, const float* T, uint64_t n, double eps,
-                       double* l_rgb, double* l_T, float* d_rgb, float* d_T, cudaStream_t s);
+template <class R>
+void launch_local_render_bwd(const double* delta, const R* rgb, const uint64_t* seg_off, uint64_t n_seg,
+                             const double* cache, const R* d_rgb, const R* d_T, const R* w_up,
+                             R* sigma_grad, R* rgb_grad, cudaStream_t s);
+template <class R>
+void launch_merge_fwd(const R* srgb, const R* sT, const R* sdepth, const uint64_t* ray_off,
+                      uint64_t n_rays, R* rgb, R* T, R* depth, cudaStream_t s);
+template <class R>
+void launch_merge_bwd(const R* srgb, const R* sT, const uint64_t* ray_off, uint64_t n_rays,
+                      const R* d_rgb, const R* d_T, R* sd_rgb, R* sd_T, cudaStream_t s);
+template <class R>
+void launch_ray_losses(const R* rgb, const R* gt, const R* T, uint64_t n, double eps,
+                       double* l_rgb, double* l_T, R* d_rgb, R* d_T, cudaStream_t s);
+void launch_distortion_stats(const double* t, const double* delta, const double* cache, const uint64_t* seg_off,
+                             uint64_t n_seg, const double* ray_t0, const double* ray_t1, double* out,
+                             cudaStream_t s);
 void launch_distortion(const double* w, const double* s_, const double* ds, const uint64_t* seg_off,
                        uint64_t n_seg, double* loss, double* grad, cudaStream_t s);
+
+// ---- per-function stage entry points of the facade (kernels_stage_api.cu) ----
+void launch_ray_aabb(const double* o, const double* d, uint64_t n, const double lo[3], const double hi[3],
+                     uint8_t* hit, double* tn, double* tf, cudaStream_t s);
+void launch_march_segment(const double* te, const double* tx, const uint64_t* iv_off, const double* iv,
+                          const uint64_t* ray_id, uint64_t n, double step, int jitter, uint64_t seed,
+                          uint64_t batch, uint32_t* counts, const uint64_t* out_off, double* t, double* delta,
+                          cudaStream_t s);
+void launch_field_density(const FieldDesc* field, const float* params, const float* X, uint64_t n, float* sigma,
+                          float* feat, cudaStream_t s);
+void launch_field_color(const FieldDesc* field, const float* params, const float* feat, const float* dirs,
+                        const float* app, uint64_t n, float* rgb, cudaStream_t s);
+void launch_adam_f64(double* p, const double* g, double* m, double* v, uint64_t n, double lr, double b1,
+                     double b2, double eps, double bias1, double bias2, cudaStream_t s);
 
 // ---- optimizer / init (kernels_adam.cu) ----
 void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, float b1, float b2,

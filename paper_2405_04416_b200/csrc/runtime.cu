@@ -1808,6 +1808,9 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
     stats->items = NI;
     stats->h2d_bytes = c->h2d;
     stats->d2h_bytes = c->d2h;
+    stats->partial_bytes_sent = bytes - bytes_x1;
+    stats->partial_records_sent =
+        (bytes - bytes_x1) / (sizeof(PartialRec) + (c->cross_active ? sizeof(float4) : 0));
   }
   return DG_OK;
 }
@@ -2258,6 +2261,50 @@ int dg_field_forward(dg_ctx* c, uint32_t p, uint32_t cascade, const double* poin
   return field_stage(c, p, cascade, points, dirs, app, n, nullptr, nullptr, sigma, rgb);
 }
 
+int dg_field_density(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points, uint64_t n, float* sigma,
+                     float* features) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  if (n && (!points || !sigma || !features)) return set_err(DG_EINVAL, "null argument");
+  if (!n) return DG_OK;
+  cudaStream_t s = c->stream;
+  const FieldDesc* fd = c->d_fields.as<FieldDesc>() + cascade * c->local.size() + lp;
+  DBuf pts, X, sg, ft;
+  TRY(upload(pts, points, n * 24, s));
+  TRY(X.ensure(n * kEnc * 4 + 16));
+  TRY(sg.ensure(n * 4 + 16));
+  TRY(ft.ensure(n * 60 + 16));
+  launch_encode_points(fd, c->params.as<float>(), pts.as<double>(), n, c->cfg.grid_levels, X.as<float>(), nullptr, s);
+  launch_field_density(fd, c->params.as<float>(), X.as<float>(), n, sg.as<float>(), ft.as<float>(), s);
+  c->launches += 2;
+  CU(cudaMemcpyAsync(sigma, sg.p, n * 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(features, ft.p, n * 60, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
+int dg_field_color(dg_ctx* c, uint32_t p, uint32_t cascade, const float* features, const float* dirs,
+                   const float* app, uint64_t n, float* rgb) {
+  uint32_t lp;
+  TRY(check_part(c, p, &lp));
+  if (cascade > 1) return set_err(DG_EINVAL, "cascade must be 0 or 1");
+  if (n && (!features || !dirs || !rgb || (c->cfg.appearance_dim && !app))) return set_err(DG_EINVAL, "null argument");
+  if (!n) return DG_OK;
+  cudaStream_t s = c->stream;
+  const FieldDesc* fd = c->d_fields.as<FieldDesc>() + cascade * c->local.size() + lp;
+  DBuf ft, dr, ap, out;
+  TRY(upload(ft, features, n * 60, s));
+  TRY(upload(dr, dirs, n * 12, s));
+  TRY(upload(ap, app, n * c->cfg.appearance_dim * 4, s));
+  TRY(out.ensure(n * 12 + 16));
+  launch_field_color(fd, c->params.as<float>(), ft.as<float>(), dr.as<float>(), ap.as<float>(), n, out.as<float>(), s);
+  ++c->launches;
+  CU(cudaMemcpyAsync(rgb, out.p, n * 12, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return DG_OK;
+}
+
 int dg_field_backward(dg_ctx* c, uint32_t p, uint32_t cascade, const double* points, const float* dirs,
                       const float* app, const float* sigma_grad, const float* rgb_grad, uint64_t n,
                       int32_t mem) {
@@ -2320,14 +2367,11 @@ int host_offsets(dg_ctx* c, const uint64_t* off, uint64_t n, int32_t mem, std::v
   return DG_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int dg_local_render(dg_ctx* c, const double* t, const double* delta, const float* sigma, const float* rgb,
+template <class R>
+int local_render_impl(dg_ctx* c, const double* t, const double* delta, const R* sigma, const R* rgb,
                     const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0, const double* ray_t1,
-                    float* out_rgb, float* out_T, float* out_depth_sum, double* out_distortion,
-                    int32_t mem) {
+                    R* out_rgb, R* out_T, R* out_depth_sum, double* out_distortion,
+                    int32_t mem, double* out_cache = nullptr) {
   TRY(check_ctx(c));
   if (!out_rgb || !out_T) return set_err(DG_EINVAL, "null outputs");
   std::vector<uint64_t> off;
@@ -2337,7 +2381,7 @@ int dg_local_render(dg_ctx* c, const double* t, const double* delta, const float
   if (out_distortion && (!ray_t0 || !ray_t1)) return set_err(DG_EINVAL, "distortion stats need the ray span");
   StageIo io{c, mem, {}, {}};
   const double *dt, *dd, *t0 = nullptr, *t1 = nullptr;
-  const float *dsig, *drgb;
+  const R *dsig, *drgb;
   const uint64_t* doff;
   TRY(io.in(t, ns, &dt));
   TRY(io.in(delta, ns, &dd));
@@ -2346,22 +2390,25 @@ int dg_local_render(dg_ctx* c, const double* t, const double* delta, const float
   TRY(io.in(seg_off, n_seg + 1, &doff));
   TRY(io.in(ray_t0, n_seg, &t0));
   TRY(io.in(ray_t1, n_seg, &t1));
-  float *orgb, *oT, *odep;
+  R *orgb, *oT, *odep;
   double* odist;
   TRY(io.out(out_rgb, 3 * n_seg, &orgb));
   TRY(io.out(out_T, n_seg, &oT));
   TRY(io.out(out_depth_sum, n_seg, &odep));
   TRY(io.out(out_distortion, 3 * n_seg, &odist));
+  double* ocache;
+  TRY(io.out(out_cache, 2 * ns, &ocache));
   launch_local_render(dt, dd, dsig, drgb, doff, n_seg, out_distortion ? t0 : nullptr,
-                      out_distortion ? t1 : nullptr, orgb, oT, odep, odist, nullptr, c->stream);
+                      out_distortion ? t1 : nullptr, orgb, oT, odep, odist, ocache, c->stream);
   ++c->launches;
   return io.finish();
 }
 
-int dg_local_render_backward(dg_ctx* c, const double* t, const double* delta, const float* sigma,
-                             const float* rgb, const uint64_t* seg_off, uint64_t n_seg, const float* d_rgb,
-                             const float* d_transmittance, const float* weight_upstream, float* sigma_grad,
-                             float* rgb_grad, int32_t mem) {
+template <class R>
+int local_render_backward_impl(dg_ctx* c, const double* t, const double* delta, const R* sigma,
+                             const R* rgb, const uint64_t* seg_off, uint64_t n_seg, const R* d_rgb,
+                             const R* d_transmittance, const R* weight_upstream, R* sigma_grad,
+                             R* rgb_grad, int32_t mem) {
   TRY(check_ctx(c));
   if (!d_rgb || !d_transmittance) return set_err(DG_EINVAL, "null upstream");
   std::vector<uint64_t> off;
@@ -2371,7 +2418,7 @@ int dg_local_render_backward(dg_ctx* c, const double* t, const double* delta, co
     return set_err(DG_EINVAL, "null sample arrays");
   StageIo io{c, mem, {}, {}};
   const double *dt, *dd;
-  const float *dsig, *drgb, *ug, *ut, *uw;
+  const R *dsig, *drgb, *ug, *ut, *uw;
   const uint64_t* doff;
   TRY(io.in(t, ns, &dt));
   TRY(io.in(delta, ns, &dd));
@@ -2381,24 +2428,25 @@ int dg_local_render_backward(dg_ctx* c, const double* t, const double* delta, co
   TRY(io.in(d_rgb, 3 * n_seg, &ug));
   TRY(io.in(d_transmittance, n_seg, &ut));
   TRY(io.in(weight_upstream, ns, &uw));
-  float *sg, *cg;
+  R *sg, *cg;
   TRY(io.out(sigma_grad, ns, &sg));
   TRY(io.out(rgb_grad, 3 * ns, &cg));
   // the forward sweep's (alpha, prefix) cache (LocalRenderCache), then the reverse sweep
   DBuf cache, scratch;
   TRY(cache.ensure(ns * 16 + 16));
-  TRY(scratch.ensure(n_seg * 20 + 16));
-  float* srgb = scratch.as<float>();
-  launch_local_render(dt, dd, dsig, drgb, doff, n_seg, nullptr, nullptr, srgb, srgb + 3 * n_seg, nullptr,
-                      nullptr, cache.as<double>(), c->stream);
+  TRY(scratch.ensure(n_seg * 4 * sizeof(R) + 16));
+  R* srgb = scratch.as<R>();
+  launch_local_render<R>(dt, dd, dsig, drgb, doff, n_seg, nullptr, nullptr, srgb, srgb + 3 * n_seg,
+                         static_cast<R*>(nullptr), nullptr, cache.as<double>(), c->stream);
   launch_local_render_bwd(dd, drgb, doff, n_seg, cache.as<double>(), ug, ut, uw, sg, cg, c->stream);
   c->launches += 2;
   return io.finish();
 }
 
-int dg_merge_forward(dg_ctx* c, const float* seg_rgb, const float* seg_transmittance,
-                     const float* seg_depth_sum, const uint64_t* ray_off, uint64_t n_rays, float* rgb,
-                     float* transmittance, float* depth, int32_t mem) {
+template <class R>
+int merge_forward_impl(dg_ctx* c, const R* seg_rgb, const R* seg_transmittance,
+                     const R* seg_depth_sum, const uint64_t* ray_off, uint64_t n_rays, R* rgb,
+                     R* transmittance, R* depth, int32_t mem) {
   TRY(check_ctx(c));
   if (!rgb || !transmittance) return set_err(DG_EINVAL, "null outputs");
   std::vector<uint64_t> off;
@@ -2407,13 +2455,13 @@ int dg_merge_forward(dg_ctx* c, const float* seg_rgb, const float* seg_transmitt
     if (off[r + 1] == off[r]) return set_err(DG_EINVAL, "merge: no partials");  // render.cpp:102
   const uint64_t ns = off[n_rays];
   StageIo io{c, mem, {}, {}};
-  const float *sr, *sT, *sd;
+  const R *sr, *sT, *sd;
   const uint64_t* doff;
   TRY(io.in(seg_rgb, 3 * ns, &sr));
   TRY(io.in(seg_transmittance, ns, &sT));
   TRY(io.in(seg_depth_sum, ns, &sd));
   TRY(io.in(ray_off, n_rays + 1, &doff));
-  float *orgb, *oT, *od;
+  R *orgb, *oT, *od;
   TRY(io.out(rgb, 3 * n_rays, &orgb));
   TRY(io.out(transmittance, n_rays, &oT));
   TRY(io.out(depth, n_rays, &od));
@@ -2422,9 +2470,10 @@ int dg_merge_forward(dg_ctx* c, const float* seg_rgb, const float* seg_transmitt
   return io.finish();
 }
 
-int dg_merge_backward(dg_ctx* c, const float* seg_rgb, const float* seg_transmittance, const uint64_t* ray_off,
-                      uint64_t n_rays, const float* d_rgb, const float* d_transmittance, float* seg_d_rgb,
-                      float* seg_d_transmittance, int32_t mem) {
+template <class R>
+int merge_backward_impl(dg_ctx* c, const R* seg_rgb, const R* seg_transmittance, const uint64_t* ray_off,
+                      uint64_t n_rays, const R* d_rgb, const R* d_transmittance, R* seg_d_rgb,
+                      R* seg_d_transmittance, int32_t mem) {
   TRY(check_ctx(c));
   if (!d_rgb || !d_transmittance || !seg_d_rgb || !seg_d_transmittance) return set_err(DG_EINVAL, "null argument");
   std::vector<uint64_t> off;
@@ -2433,14 +2482,14 @@ int dg_merge_backward(dg_ctx* c, const float* seg_rgb, const float* seg_transmit
     if (off[r + 1] - off[r] > uint64_t(kMaxSeg)) return set_err(DG_EINVAL, "merge: more than %d partials", kMaxSeg);
   const uint64_t ns = off[n_rays];
   StageIo io{c, mem, {}, {}};
-  const float *sr, *sT, *ug, *ut;
+  const R *sr, *sT, *ug, *ut;
   const uint64_t* doff;
   TRY(io.in(seg_rgb, 3 * ns, &sr));
   TRY(io.in(seg_transmittance, ns, &sT));
   TRY(io.in(ray_off, n_rays + 1, &doff));
   TRY(io.in(d_rgb, 3 * n_rays, &ug));
   TRY(io.in(d_transmittance, n_rays, &ut));
-  float *og, *ot;
+  R *og, *ot;
   TRY(io.out(seg_d_rgb, 3 * ns, &og));
   TRY(io.out(seg_d_transmittance, ns, &ot));
   launch_merge_bwd(sr, sT, doff, n_rays, ug, ut, og, ot, c->stream);
@@ -2448,18 +2497,19 @@ int dg_merge_backward(dg_ctx* c, const float* seg_rgb, const float* seg_transmit
   return io.finish();
 }
 
-int dg_ray_losses(dg_ctx* c, const float* rgb, const float* color_gt, const float* transmittance, uint64_t n,
-                  double eps, double* loss_rgb, double* loss_transmittance, float* d_rgb, float* d_transmittance,
+template <class R>
+int ray_losses_impl(dg_ctx* c, const R* rgb, const R* color_gt, const R* transmittance, uint64_t n,
+                  double eps, double* loss_rgb, double* loss_transmittance, R* d_rgb, R* d_transmittance,
                   int32_t mem) {
   TRY(check_ctx(c));
   if (n && (!rgb || !color_gt || !transmittance)) return set_err(DG_EINVAL, "null inputs");
   StageIo io{c, mem, {}, {}};
-  const float *r, *g, *T;
+  const R *r, *g, *T;
   TRY(io.in(rgb, 3 * n, &r));
   TRY(io.in(color_gt, 3 * n, &g));
   TRY(io.in(transmittance, n, &T));
   double *lr, *lt;
-  float *dr, *dt;
+  R *dr, *dt;
   TRY(io.out(loss_rgb, n, &lr));
   TRY(io.out(loss_transmittance, n, &lt));
   TRY(io.out(d_rgb, 3 * n, &dr));
@@ -2467,6 +2517,75 @@ int dg_ray_losses(dg_ctx* c, const float* rgb, const float* color_gt, const floa
   launch_ray_losses(r, g, T, n, eps, lr, lt, dr, dt, c->stream);
   ++c->launches;
   return io.finish();
+}
+
+}  // namespace
+
+extern "C" {
+
+int dg_local_render(dg_ctx* c, const double* t, const double* delta, const float* sigma, const float* rgb,
+                    const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0, const double* ray_t1,
+                    float* out_rgb, float* out_T, float* out_depth_sum, double* out_distortion,
+                    int32_t mem) {
+  return local_render_impl<float>(c, t, delta, sigma, rgb, seg_off, n_seg, ray_t0, ray_t1, out_rgb, out_T, out_depth_sum, out_distortion, mem);
+}
+
+int dg_local_render_f64(dg_ctx* c, const double* t, const double* delta, const double* sigma, const double* rgb,
+                    const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0, const double* ray_t1,
+                    double* out_rgb, double* out_T, double* out_depth_sum, double* out_distortion,
+                    double* out_cache, int32_t mem) {
+  return local_render_impl<double>(c, t, delta, sigma, rgb, seg_off, n_seg, ray_t0, ray_t1, out_rgb, out_T,
+                                   out_depth_sum, out_distortion, mem, out_cache);
+}
+
+int dg_local_render_backward(dg_ctx* c, const double* t, const double* delta, const float* sigma,
+                             const float* rgb, const uint64_t* seg_off, uint64_t n_seg, const float* d_rgb,
+                             const float* d_transmittance, const float* weight_upstream, float* sigma_grad,
+                             float* rgb_grad, int32_t mem) {
+  return local_render_backward_impl<float>(c, t, delta, sigma, rgb, seg_off, n_seg, d_rgb, d_transmittance, weight_upstream, sigma_grad, rgb_grad, mem);
+}
+
+int dg_local_render_backward_f64(dg_ctx* c, const double* t, const double* delta, const double* sigma,
+                             const double* rgb, const uint64_t* seg_off, uint64_t n_seg, const double* d_rgb,
+                             const double* d_transmittance, const double* weight_upstream, double* sigma_grad,
+                             double* rgb_grad, int32_t mem) {
+  return local_render_backward_impl<double>(c, t, delta, sigma, rgb, seg_off, n_seg, d_rgb, d_transmittance, weight_upstream, sigma_grad, rgb_grad, mem);
+}
+
+int dg_merge_forward(dg_ctx* c, const float* seg_rgb, const float* seg_transmittance,
+                     const float* seg_depth_sum, const uint64_t* ray_off, uint64_t n_rays, float* rgb,
+                     float* transmittance, float* depth, int32_t mem) {
+  return merge_forward_impl<float>(c, seg_rgb, seg_transmittance, seg_depth_sum, ray_off, n_rays, rgb, transmittance, depth, mem);
+}
+
+int dg_merge_forward_f64(dg_ctx* c, const double* seg_rgb, const double* seg_transmittance,
+                     const double* seg_depth_sum, const uint64_t* ray_off, uint64_t n_rays, double* rgb,
+                     double* transmittance, double* depth, int32_t mem) {
+  return merge_forward_impl<double>(c, seg_rgb, seg_transmittance, seg_depth_sum, ray_off, n_rays, rgb, transmittance, depth, mem);
+}
+
+int dg_merge_backward(dg_ctx* c, const float* seg_rgb, const float* seg_transmittance, const uint64_t* ray_off,
+                      uint64_t n_rays, const float* d_rgb, const float* d_transmittance, float* seg_d_rgb,
+                      float* seg_d_transmittance, int32_t mem) {
+  return merge_backward_impl<float>(c, seg_rgb, seg_transmittance, ray_off, n_rays, d_rgb, d_transmittance, seg_d_rgb, seg_d_transmittance, mem);
+}
+
+int dg_merge_backward_f64(dg_ctx* c, const double* seg_rgb, const double* seg_transmittance, const uint64_t* ray_off,
+                      uint64_t n_rays, const double* d_rgb, const double* d_transmittance, double* seg_d_rgb,
+                      double* seg_d_transmittance, int32_t mem) {
+  return merge_backward_impl<double>(c, seg_rgb, seg_transmittance, ray_off, n_rays, d_rgb, d_transmittance, seg_d_rgb, seg_d_transmittance, mem);
+}
+
+int dg_ray_losses(dg_ctx* c, const float* rgb, const float* color_gt, const float* transmittance, uint64_t n,
+                  double eps, double* loss_rgb, double* loss_transmittance, float* d_rgb, float* d_transmittance,
+                  int32_t mem) {
+  return ray_losses_impl<float>(c, rgb, color_gt, transmittance, n, eps, loss_rgb, loss_transmittance, d_rgb, d_transmittance, mem);
+}
+
+int dg_ray_losses_f64(dg_ctx* c, const double* rgb, const double* color_gt, const double* transmittance, uint64_t n,
+                  double eps, double* loss_rgb, double* loss_transmittance, double* d_rgb, double* d_transmittance,
+                  int32_t mem) {
+  return ray_losses_impl<double>(c, rgb, color_gt, transmittance, n, eps, loss_rgb, loss_transmittance, d_rgb, d_transmittance, mem);
 }
 
 int dg_distortion_loss(dg_ctx* c, const double* weights, const double* midpoints, const double* interval_lengths,
@@ -2487,6 +2606,117 @@ int dg_distortion_loss(dg_ctx* c, const double* weights, const double* midpoints
   TRY(io.out(loss, n_seg, &ol));
   TRY(io.out(grads, ns, &og));
   launch_distortion(w, m, ds, doff, n_seg, ol, og, c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
+int dg_distortion_stats_f64(dg_ctx* c, const double* t, const double* delta, const double* cache,
+                            const uint64_t* seg_off, uint64_t n_seg, const double* ray_t0, const double* ray_t1,
+                            double* out, int32_t mem) {
+  TRY(check_ctx(c));
+  std::vector<uint64_t> off;
+  TRY(host_offsets(c, seg_off, n_seg, mem, off));
+  const uint64_t ns = off[n_seg];
+  if (!out || (n_seg && (!ray_t0 || !ray_t1)) || (ns && (!t || !delta || !cache)))
+    return set_err(DG_EINVAL, "null argument");
+  StageIo io{c, mem, {}, {}};
+  const double *dt, *dd, *dc, *t0, *t1;
+  const uint64_t* doff;
+  TRY(io.in(t, ns, &dt));
+  TRY(io.in(delta, ns, &dd));
+  TRY(io.in(cache, 2 * ns, &dc));
+  TRY(io.in(seg_off, n_seg + 1, &doff));
+  TRY(io.in(ray_t0, n_seg, &t0));
+  TRY(io.in(ray_t1, n_seg, &t1));
+  double* o;
+  TRY(io.in(static_cast<const double*>(out), 3 * n_seg, const_cast<const double**>(&o)));
+  if (mem != DG_MEM_DEVICE && n_seg) io.back.emplace_back(out, io.tmp.back().get(), 3 * n_seg * 8);
+  launch_distortion_stats(dt, dd, dc, doff, n_seg, t0, t1, o, c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
+int dg_ray_aabb(dg_ctx* c, const double* origin, const double* dir, uint64_t n, const double box_lo[3],
+                const double box_hi[3], uint8_t* hit, double* t_near, double* t_far, int32_t mem) {
+  TRY(check_ctx(c));
+  if (!box_lo || !box_hi || (n && (!origin || !dir || !hit || !t_near || !t_far)))
+    return set_err(DG_EINVAL, "null argument");
+  StageIo io{c, mem, {}, {}};
+  const double *o, *d;
+  TRY(io.in(origin, 3 * n, &o));
+  TRY(io.in(dir, 3 * n, &d));
+  uint8_t* h;
+  double *tn, *tf;
+  TRY(io.out(hit, n, &h));
+  TRY(io.out(t_near, n, &tn));
+  TRY(io.out(t_far, n, &tf));
+  launch_ray_aabb(o, d, n, box_lo, box_hi, h, tn, tf, c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
+int dg_march_segment(dg_ctx* c, const double* t_enter, const double* t_exit, const uint64_t* interval_off,
+                     const double* intervals, const uint64_t* ray_id, uint64_t n, double step, int32_t jitter,
+                     uint64_t jitter_seed, uint64_t jitter_step, uint32_t* counts, const uint64_t* offsets,
+                     double* t, double* delta, int32_t mem) {
+  TRY(check_ctx(c));
+  if (!(step > 0.0)) return set_err(DG_EINVAL, "march: step must be positive");  // render.cpp:13
+  if (!counts && !t) return set_err(DG_EINVAL, "march: need counts or outputs");
+  if (t && (!offsets || !delta)) return set_err(DG_EINVAL, "march: outputs need offsets and delta");
+  std::vector<uint64_t> ivo;
+  TRY(host_offsets(c, interval_off, n, mem, ivo));
+  const uint64_t niv = ivo[n];
+  if (niv && !intervals) return set_err(DG_EINVAL, "null intervals");
+  if (n && (!t_enter || !t_exit)) return set_err(DG_EINVAL, "null segment bounds");
+  StageIo io{c, mem, {}, {}};
+  const double *te, *tx, *iv;
+  const uint64_t *ivd, *rid, *od = nullptr;
+  TRY(io.in(t_enter, n, &te));
+  TRY(io.in(t_exit, n, &tx));
+  TRY(io.in(interval_off, n + 1, &ivd));
+  TRY(io.in(intervals, 2 * niv, &iv));
+  TRY(io.in(ray_id, n, &rid));
+  uint32_t* cnt;
+  TRY(io.out(counts, n, &cnt));
+  double *ot = nullptr, *odl = nullptr;
+  if (t) {
+    std::vector<uint64_t> oo;
+    TRY(host_offsets(c, offsets, n, mem, oo));
+    TRY(io.in(offsets, n + 1, &od));
+    TRY(io.out(t, oo[n], &ot));
+    TRY(io.out(delta, oo[n], &odl));
+  }
+  launch_march_segment(te, tx, ivd, iv, rid, n, step, jitter, jitter_seed, jitter_step, cnt, od, ot, odl,
+                       c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
+int dg_adam_update_f64(dg_ctx* c, double* params, const double* grads, double* m, double* v, uint64_t n,
+                       uint64_t t, double lr, double beta1, double beta2, double eps, int32_t mem) {
+  TRY(check_ctx(c));
+  if (n && (!params || !grads || !m || !v)) return set_err(DG_EINVAL, "null argument");
+  if (t == 0) return set_err(DG_EINVAL, "adam: t counts the steps taken, including this one (>= 1)");
+  StageIo io{c, mem, {}, {}};
+  const double* g;
+  double *p, *dm, *dv;
+  TRY(io.in(grads, n, &g));
+  // in/out arrays: upload, update in place, read back
+  const double *pi, *mi, *vi;
+  TRY(io.in(static_cast<const double*>(params), n, &pi));
+  TRY(io.in(static_cast<const double*>(m), n, &mi));
+  TRY(io.in(static_cast<const double*>(v), n, &vi));
+  p = const_cast<double*>(pi);
+  dm = const_cast<double*>(mi);
+  dv = const_cast<double*>(vi);
+  if (mem != DG_MEM_DEVICE && n) {
+    io.back.emplace_back(params, io.tmp[1].get(), n * 8);
+    io.back.emplace_back(m, io.tmp[2].get(), n * 8);
+    io.back.emplace_back(v, io.tmp[3].get(), n * 8);
+  }
+  const double bias1 = 1.0 - std::pow(beta1, double(t));
+  const double bias2 = 1.0 - std::pow(beta2, double(t));
+  launch_adam_f64(p, g, dm, dv, n, lr, beta1, beta2, eps, bias1, bias2, c->stream);
   ++c->launches;
   return io.finish();
 }

@@ -27,11 +27,16 @@ int main(int argc, char** argv) {
   cfg.fine_table_log2 = 12;
   cfg.march_step_divisor = 64;
   cfg.total_steps = 1000;
+  cfg.partitions_x = 2;
+  cfg.partitions_y = 1;
   const distgrid::Aabb box{{0, 0, 0}, {2, 1, 1}};
   const auto manifest = distgrid::split_regions(box, box, 2, 1, 0.0);
-  const uint32_t ids[1] = {0};
+  distgrid::AppearanceTable table;  // the reference constructor (worker.hpp:177-178)
+  table.dim = 16;
+  table.image_ids = {0};
+  table.rows.assign(16, 0.25);
   std::vector<float> app(16, 0.25f);
-  distgrid::DistributedRun run(cfg, manifest, ids, app);
+  distgrid::DistributedRun run(cfg, manifest, table);
   run.start();
   std::FILE* out = std::fopen(argv[2], "w");
   for (uint64_t step = 0; step < 2; ++step) {
@@ -45,7 +50,8 @@ int main(int argc, char** argv) {
     std::fprintf(out, "ray %.9g %.9g %.9g %.9g %.9g\n", merged[i].color.x, merged[i].color.y,
                  merged[i].color.z, merged[i].transmittance, merged[i].depth);
   distgrid::CameraPose pose;  // looking down -z from above the scene
-  pose.rotation[0] = 1; pose.rotation[4] = -1; pose.rotation[8] = -1;
+  pose.rotation(1, 1) = -1;
+  pose.rotation(2, 2) = -1;
   pose.translation = {1.0, 0.5, 3.0};
   pose.fx = pose.fy = 20.0;
   pose.cx = 8.0;
@@ -59,10 +65,18 @@ int main(int argc, char** argv) {
     asum += image.attribution[i].x + image.attribution[i].y + image.attribution[i].z;
   }
   std::fprintf(out, "image %u %u %.9g %.9g\n", image.width, image.height, csum, asum);
-  const auto segs = run.segment_rays(rays);
+  const auto segs = distgrid::segment_rays(rays, manifest);
   uint64_t total = 0;
   for (const auto& s : segs) total += s.size();
   std::fprintf(out, "segments %llu\n", (unsigned long long)total);
+  // worker views and the traffic counters of the reference's DistributedRun
+  std::fprintf(out, "workers %u step %llu %llu bytes %llu %llu %llu\n", run.worker_count(),
+               (unsigned long long)run.worker(0).step(), (unsigned long long)run.worker(1).step(),
+               (unsigned long long)run.worker_bytes_sent(), (unsigned long long)run.scatter_payload_bytes(),
+               (unsigned long long)run.scatter_entries());
+  const distgrid::FieldParams fine = run.worker(1).fine_field();
+  std::fprintf(out, "fine_field levels %zu density_in %u color_in %u region %u\n", fine.grid.levels().size(),
+               fine.density_mlp.input_width(), fine.color_mlp.input_width(), run.worker(1).region().region_id);
   run.stop();
   try {
     run.stop();

@@ -28,7 +28,7 @@ def test_struct_sizes_match_header():
     # sizes the C side expects (checked against offsets of trailing fields)
     assert C.sizeof(abi.RunConfig) == 320
     assert C.sizeof(abi.RayBatch) == 56
-    assert C.sizeof(abi.StepStats) == 96
+    assert C.sizeof(abi.StepStats) == 112
     assert C.sizeof(abi.Merged) == 40
 
 
@@ -59,3 +59,13 @@ def test_error_mapping_on_bad_config():
     with pytest.raises(dg.DGError) as e:
         dg.Context(c, device=0)
     assert e.value.status in ("DG_EINVAL", "DG_ECUDA")
+
+
+@pytest.mark.parametrize("src", ["tests/cpp/facade_demo.cpp", "tests/cpp/facade_stages.cpp"])
+def test_facade_headers_compile(src):
+    """The C++ facade (include/distgrid/*.hpp) compiles as a reference user's code would."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-I", os.path.join(root, "include"),
+                        os.path.join(root, src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
