@@ -6,12 +6,16 @@
 // tables, fp32 accumulation, red.global scatters) on the grid's own context, and have batched
 // overloads for whole point sets.  The host tables are the reference's double arrays; the device
 // copy is fp32 (tables are fp32 on the training path).
-// Not here: OccupancyGrid::decay_and_update (it takes a host density callback; the device update
-// runs inside dg_train_step) and occupancy_skip (the device DDA runs inside the march).
+// occupancy_skip runs the device DDA (k_occupancy_skip, the march's walk over a row-major
+// bitfield).  OccupancyGrid::decay_and_update takes the caller's host density callback, so it is
+// host bookkeeping around that callback here; the training path's update runs on the device
+// inside dg_train_step.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <functional>
 #include <span>
 #include <stdexcept>
 #include <vector>
@@ -245,6 +249,34 @@ class OccupancyGrid {
   void recompute_bitfield() {
     for (size_t i = 0; i < density_.size(); ++i) bitfield_[i] = density_[i] >= threshold_ ? 1 : 0;
   }
+  // density[i] <- max(density[i] * decay, density_at(jittered point of cell i)) over every cell
+  // (warm-up) or 1/4 uniform + 1/4 occupied cells, then the bitfield (grid.cpp:201-229)
+  void decay_and_update(const std::function<double(const Vec3&)>& density_at, uint64_t step, bool warm_up,
+                        Rng& rng) {
+    (void)step;
+    const uint64_t total = cell_count();
+    auto visit = [&](uint64_t idx) {
+      const uint32_t ix = uint32_t(idx % shape_.nx), iy = uint32_t((idx / shape_.nx) % shape_.ny),
+                     iz = uint32_t(idx / (uint64_t(shape_.nx) * shape_.ny));
+      const Aabb c = cell_box(ix, iy, iz);
+      const double px = rng.uniform(c.lo.x, c.hi.x);
+      const double py = rng.uniform(c.lo.y, c.hi.y);
+      const double pz = rng.uniform(c.lo.z, c.hi.z);
+      density_[idx] = std::max(density_[idx] * decay_, density_at(Vec3(px, py, pz)));
+    };
+    if (warm_up) {
+      for (uint64_t i = 0; i < total; ++i) visit(i);
+    } else {
+      std::vector<uint64_t> occ;
+      for (uint64_t i = 0; i < total; ++i)
+        if (bitfield_[i]) occ.push_back(i);
+      const uint64_t k = std::max<uint64_t>(total / 4, 1);
+      for (uint64_t i = 0; i < k; ++i) visit(rng.uniform_index(total));
+      if (!occ.empty())
+        for (uint64_t i = 0; i < k; ++i) visit(occ[rng.uniform_index(occ.size())]);
+    }
+    recompute_bitfield();
+  }
   // device snapshot (Worker views)
   void assign(std::vector<double> density, std::vector<uint8_t> bits, double threshold) {
     density_ = std::move(density);
@@ -260,5 +292,42 @@ class OccupancyGrid {
   double decay_ = 0.99;
   double threshold_ = 0.6;
 };
+
+// Batched occupancy_skip: the occupied runs of [t0[i], t1[i]] along rays[i], in increasing t
+// (runs of consecutive occupied cells merged; the caller keeps [t0, t1] inside the box).
+inline std::vector<std::vector<RayInterval>> occupancy_skip(std::span<const Ray> rays, std::span<const double> t0,
+                                                            std::span<const double> t1, const OccupancyGrid& occ) {
+  const size_t n = rays.size();
+  if (t0.size() != n || t1.size() != n) throw std::invalid_argument("occupancy_skip: size mismatch");
+  std::vector<double> o(3 * n), d(3 * n);
+  for (size_t i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      o[3 * i + a] = rays[i].origin[a];
+      d[3 * i + a] = rays[i].dir[a];
+    }
+  const LevelShape sh = occ.shape();
+  const uint32_t shape[3] = {sh.nx, sh.ny, sh.nz};
+  const double lo[3] = {occ.box().lo.x, occ.box().lo.y, occ.box().lo.z};
+  const double hi[3] = {occ.box().hi.x, occ.box().hi.y, occ.box().hi.z};
+  std::vector<uint32_t> cnt(n);
+  dg_ctx* c = detail::stage_ctx();
+  detail::check(dg_occupancy_skip(c, occ.bitfield().data(), shape, lo, hi, o.data(), d.data(), t0.data(), t1.data(),
+                                  n, cnt.data(), nullptr, nullptr, DG_MEM_HOST));
+  std::vector<uint64_t> off(n + 1, 0);
+  for (size_t i = 0; i < n; ++i) off[i + 1] = off[i] + cnt[i];
+  std::vector<double> iv(2 * off[n]);
+  if (off[n])
+    detail::check(dg_occupancy_skip(c, occ.bitfield().data(), shape, lo, hi, o.data(), d.data(), t0.data(),
+                                    t1.data(), n, nullptr, off.data(), iv.data(), DG_MEM_HOST));
+  std::vector<std::vector<RayInterval>> out(n);
+  for (size_t i = 0; i < n; ++i)
+    for (uint64_t k = off[i]; k < off[i + 1]; ++k) out[i].push_back(RayInterval{iv[2 * k], iv[2 * k + 1]});
+  return out;
+}
+
+inline std::vector<RayInterval> occupancy_skip(const Ray& ray, double t0, double t1, const OccupancyGrid& occ) {
+  return occupancy_skip(std::span<const Ray>(&ray, 1), std::span<const double>(&t0, 1),
+                        std::span<const double>(&t1, 1), occ)[0];
+}
 
 }  // namespace distgrid

@@ -17,7 +17,6 @@
 #include <tuple>
 #include <vector>
 
-#include "distgrid/config.hpp"
 #include "distgrid/detail/device.hpp"
 #include "distgrid/geometry.hpp"
 #include "distgrid/render.hpp"
@@ -172,16 +171,21 @@ inline dg_ctx* manifest_ctx(const PartitionManifest& m) {
   const PartitionManifest ref = split_regions(m.inner, m.outer, m.kx, m.ky, m.ground_altitude);
   if (ref.x_planes != m.x_planes || ref.y_planes != m.y_planes)
     throw std::invalid_argument("segment_ray: the device path needs split_regions' equal-width planes");
-  RunConfig r;
-  r.partitions_x = m.kx;
-  r.partitions_y = m.ky;
-  r.grid_levels = 1;
-  r.base_resolution = 2;
-  r.max_resolution = 2;
-  r.fine_table_log2 = 4;
-  r.coarse_table_log2 = 4;
-  r.occ_resolution = 8;
-  dg_run_config c = to_dg_config(r, il, ih, ol, oh, m.ground_altitude);
+  dg_run_config c;
+  dg_default_config(&c);
+  for (int a = 0; a < 3; ++a) {
+    c.inner_lo[a] = il[a];
+    c.inner_hi[a] = ih[a];
+    c.outer_lo[a] = ol[a];
+    c.outer_hi[a] = oh[a];
+  }
+  c.ground_altitude = m.ground_altitude;
+  c.kx = m.kx;
+  c.ky = m.ky;
+  c.grid_levels = 1;  // geometry only: the smallest grids the context accepts
+  c.base_resolution = c.max_resolution = 2;
+  c.fine_table_log2 = c.coarse_table_log2 = 4;
+  c.occ_resolution = 8;
   c.occupancy_updates = 0;
   dg_ctx* raw = nullptr;
   detail::check(dg_ctx_create(&c, -1, 0, 1, &raw));

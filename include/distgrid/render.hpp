@@ -13,6 +13,7 @@
 
 #include "distgrid/detail/device.hpp"
 #include "distgrid/geometry.hpp"
+#include "distgrid/grid.hpp"
 #include "distgrid/vecmath.hpp"
 
 namespace distgrid {
@@ -144,6 +145,14 @@ inline std::vector<MarchSample> march_segment(double t_enter, double t_exit, std
   const std::vector<RayInterval> iv(occupied.begin(), occupied.end());
   return march_segments(std::span<const RaySegment>(&s, 1), std::span<const std::vector<RayInterval>>(&iv, 1),
                         config)[0];
+}
+
+// Convenience overload walking one occupancy grid (render.cpp:39-44): occupancy_skip, then the
+// ladder, both on the device.
+inline std::vector<MarchSample> march_segment(const Ray& ray, const RaySegment& segment, const OccupancyGrid& occ,
+                                              const MarchConfig& config) {
+  const std::vector<RayInterval> iv = occupancy_skip(ray, segment.t_enter, segment.t_exit, occ);
+  return march_segment(segment.t_enter, segment.t_exit, iv, config, segment.ray_id);
 }
 
 // ---- local_render (render.cpp:46-78) + accumulate_distortion_stats (80-99) ---------------

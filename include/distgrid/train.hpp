@@ -3,15 +3,18 @@
 // the per-ray / per-segment device kernels (k_ray_losses, k_distortion; fp64), AdamState::step
 // runs k_adam_f64 over each caller array (train.cpp:91-115, same operation order).  Batch
 // sums are added on the host in batch order, as the reference sums them.
-// Not here: RayCache (it samples a Dataset, which is outside the per-ray path; the GPU batch
-// feed is dg_raycache_* in distgrid_b200.h).
+// RayCache keeps its entries on the device (dg_ray_cache_*: the reference's two mt19937_64
+// streams on the host, pixel rays built and gathered on the GPU).
 #pragma once
 
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <span>
 #include <stdexcept>
 #include <vector>
 
+#include "distgrid/dataset.hpp"
 #include "distgrid/detail/device.hpp"
 #include "distgrid/rng.hpp"
 #include "distgrid/vecmath.hpp"
@@ -175,6 +178,114 @@ class AdamState {
  private:
   std::vector<std::vector<double>> m_, v_;
   uint64_t t_ = 0;
+};
+
+// In-memory reservoir of supervised rays refreshed from a Dataset (train.cpp:117-159).  The
+// entries live on the device; refresh / draw / snapshot are serialised by a mutex, so a draw
+// never sees a half-written entry.  The device cache is built from the dataset passed to the
+// first refresh (and rebuilt if a different dataset object is passed later).
+class RayCache {
+ public:
+  RayCache(size_t capacity, uint64_t seed) : capacity_(capacity), seed_(seed) {
+    if (capacity == 0) throw std::invalid_argument("ray cache: capacity must be positive");
+  }
+  RayCache(const RayCache&) = delete;
+  RayCache& operator=(const RayCache&) = delete;
+  ~RayCache() {
+    if (cache_) dg_ray_cache_destroy(cache_);
+  }
+
+  size_t size() const {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (!cache_) return 0;
+    uint64_t s = 0, cap = 0;
+    detail::check(dg_ray_cache_size(cache_, &s, &cap));
+    return size_t(s);
+  }
+  size_t capacity() const { return capacity_; }
+
+  void refresh(const Dataset& dataset, size_t count) {
+    std::lock_guard<std::mutex> lock(mu_);
+    bind(dataset);
+    detail::check(dg_ray_cache_refresh(cache_, count));
+  }
+
+  std::vector<SupervisedRay> draw_batch(size_t batch_size) {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (!cache_) throw std::runtime_error("ray cache: empty");
+    std::vector<double> o(3 * batch_size), d(3 * batch_size);
+    std::vector<float> gt(3 * batch_size);
+    std::vector<uint32_t> img(batch_size);
+    std::vector<uint64_t> pix(batch_size);
+    detail::check(dg_ray_cache_draw_host(cache_, batch_size, o.data(), d.data(), gt.data(), img.data(), pix.data()));
+    return rays(o, d, gt, img, pix, batch_size);
+  }
+
+  std::vector<SupervisedRay> snapshot() const {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (!cache_) return {};
+    uint64_t n = 0, cap = 0;
+    detail::check(dg_ray_cache_size(cache_, &n, &cap));
+    std::vector<double> o(3 * n), d(3 * n);
+    std::vector<float> gt(3 * n);
+    std::vector<uint32_t> img(n);
+    std::vector<uint64_t> pix(n);
+    detail::check(dg_ray_cache_snapshot(cache_, o.data(), d.data(), gt.data(), img.data(), pix.data()));
+    return rays(o, d, gt, img, pix, n);
+  }
+
+  dg_ray_cache* handle() const { return cache_; }
+
+ private:
+  static std::vector<SupervisedRay> rays(const std::vector<double>& o, const std::vector<double>& d,
+                                         const std::vector<float>& gt, const std::vector<uint32_t>& img,
+                                         const std::vector<uint64_t>& pix, size_t n) {
+    std::vector<SupervisedRay> out(n);
+    for (size_t i = 0; i < n; ++i) {
+      SupervisedRay& r = out[i];
+      r.ray.origin = Vec3(o[3 * i], o[3 * i + 1], o[3 * i + 2]);
+      r.ray.dir = Vec3(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+      r.ray.pixel_id = pix[i];
+      r.ray.image_id = img[i];
+      r.color_gt = Vec3(gt[3 * i], gt[3 * i + 1], gt[3 * i + 2]);
+      r.image_id = img[i];
+    }
+    return out;
+  }
+
+  void bind(const Dataset& ds) {
+    if (cache_ && bound_ == &ds) return;
+    bool any_train = false;
+    for (uint8_t t : ds.is_train) any_train |= t != 0;
+    if (!any_train) throw std::invalid_argument("ray cache: dataset has no train images");
+    std::vector<dg_camera> cams(ds.size());
+    std::vector<const uint8_t*> imgs(ds.size());
+    for (size_t i = 0; i < ds.size(); ++i) {
+      const CameraPose& p = ds.poses[i];
+      dg_camera& c = cams[i];
+      c.image_id = p.image_id;
+      c.width = ds.images[i].width;
+      c.height = ds.images[i].height;
+      c.is_train = ds.is_train[i];
+      for (int k = 0; k < 9; ++k) c.rotation[k] = p.rotation.m[k];
+      for (int a = 0; a < 3; ++a) c.translation[a] = p.translation[a];
+      c.fx = p.fx;
+      c.fy = p.fy;
+      c.cx = p.cx;
+      c.cy = p.cy;
+      imgs[i] = ds.images[i].rgb.data();
+    }
+    if (cache_) dg_ray_cache_destroy(cache_);
+    cache_ = nullptr;
+    detail::check(dg_ray_cache_create(-1, cams.data(), imgs.data(), uint32_t(ds.size()), capacity_, seed_, &cache_));
+    bound_ = &ds;
+  }
+
+  size_t capacity_;
+  uint64_t seed_;
+  const Dataset* bound_ = nullptr;
+  dg_ray_cache* cache_ = nullptr;
+  mutable std::mutex mu_;
 };
 
 }  // namespace distgrid

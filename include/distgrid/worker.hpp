@@ -26,12 +26,6 @@
 
 namespace distgrid {
 
-struct SupervisedRay {
-  Ray ray;
-  Vec3 color_gt;
-  uint32_t image_id = 0;
-};
-
 struct StepStats {
   uint64_t step = 0;
   double loss_rgb = 0.0;

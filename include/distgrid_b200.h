@@ -281,6 +281,9 @@ int dg_ray_cache_refresh(dg_ray_cache* cache, uint64_t count);
 int dg_ray_cache_draw(dg_ray_cache* cache, uint64_t n, dg_ray_batch* out);
 int dg_ray_cache_snapshot(dg_ray_cache* cache, double* origin, double* dir, float* color_gt,
                           uint32_t* image_id, uint64_t* pixel_id);
+/* dg_ray_cache_draw into host arrays (n x 3 origin / dir / colour, n image ids, n pixel ids). */
+int dg_ray_cache_draw_host(dg_ray_cache* cache, uint64_t n, double* origin, double* dir, float* color_gt,
+                           uint32_t* image_id, uint64_t* pixel_id);
 
 /* ---- exchange planning (host only, no context or device needed) ----
  * The layouts both per-step exchanges use (exchange_plan.h), exported so multi-process tests
@@ -414,6 +417,13 @@ int dg_march_segment(dg_ctx* ctx, const double* t_enter, const double* t_exit, c
                      const double* intervals, const uint64_t* ray_id, uint64_t n, double step, int32_t jitter,
                      uint64_t jitter_seed, uint64_t jitter_step, uint32_t* counts, const uint64_t* offsets,
                      double* t, double* delta, int32_t mem);
+/* occupancy_skip (grid.cpp:235-304): the occupied runs of [t0, t1] along each ray through a
+ * caller's bitfield (shape[0] x shape[1] x shape[2] cells, ix fastest, over [box_lo, box_hi]).
+ * Two phases as dg_march_segment: counts, then (t_near, t_far) pairs at offsets. */
+int dg_occupancy_skip(dg_ctx* ctx, const uint8_t* bits, const uint32_t shape[3], const double box_lo[3],
+                      const double box_hi[3], const double* origin, const double* dir, const double* t0,
+                      const double* t1, uint64_t n, uint32_t* counts, const uint64_t* offsets, double* intervals,
+                      int32_t mem);
 /* AdamState::step (train.cpp:91-115) on one caller-owned fp64 array: m, v updated in place,
  * t = the step count after this step (bias corrections 1 - beta^t). */
 int dg_adam_update_f64(dg_ctx* ctx, double* params, const double* grads, double* m, double* v, uint64_t n,

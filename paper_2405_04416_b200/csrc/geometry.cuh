@@ -113,11 +113,11 @@ __device__ __forceinline__ void ladder(double iv_lo, double iv_hi, double t_ente
 
 // Amanatides-Woo walk over one occupancy grid (grid.cpp:235-304); every closed run of
 // occupied cells is passed to on_run(start, end) in increasing t.
-template <class OnRun>
-__device__ __forceinline__ void occupancy_walk(const double o[3], const double d[3], double t0,
-                                               double t1, const double lo[3], const double hi[3],
-                                               const uint32_t n[3], const uint32_t nb[3],
-                                               const uint8_t* bits, OnRun& on_run) {
+template <class Occupied, class OnRun>
+__device__ __forceinline__ void occupancy_walk_fn(const double o[3], const double d[3], double t0,
+                                                  double t1, const double lo[3], const double hi[3],
+                                                  const uint32_t n[3], const Occupied& occupied_at,
+                                                  OnRun& on_run) {
   if (!(t1 > t0)) return;
   double cell[3], entry[3], t_next[3], t_delta[3];
   int idx[3], stp[3];
@@ -158,7 +158,7 @@ __device__ __forceinline__ void occupancy_walk(const double o[3], const double d
     if (t_next[1] < t_next[ea]) ea = 1;
     if (t_next[2] < t_next[ea]) ea = 2;
     const double t_exit = smin(t_next[ea], t1);
-    const bool occupied = __ldg(bits + occ_addr(nb, (uint32_t)idx[0], (uint32_t)idx[1], (uint32_t)idx[2])) != 0;
+    const bool occupied = occupied_at((uint32_t)idx[0], (uint32_t)idx[1], (uint32_t)idx[2]);
     if (occupied && !run_open) {
       run_open = true;
       run_start = t_cur;
@@ -176,6 +176,18 @@ __device__ __forceinline__ void occupancy_walk(const double o[3], const double d
     t_next[ea] = dadd(t_next[ea], t_delta[ea]);
   }
   if (run_open) on_run(run_start, t_cur);
+}
+
+// The walk over the device's bricked bitfield (4x4x8-cell bricks, occ_addr).
+template <class OnRun>
+__device__ __forceinline__ void occupancy_walk(const double o[3], const double d[3], double t0,
+                                               double t1, const double lo[3], const double hi[3],
+                                               const uint32_t n[3], const uint32_t nb[3],
+                                               const uint8_t* bits, OnRun& on_run) {
+  const auto bricked = [&](uint32_t ix, uint32_t iy, uint32_t iz) {
+    return __ldg(bits + occ_addr(nb, ix, iy, iz)) != 0;
+  };
+  occupancy_walk_fn(o, d, t0, t1, lo, hi, n, bricked, on_run);
 }
 
 // Closed-form sample range of ladder() on one run: first index k0 and count n of the t_k =

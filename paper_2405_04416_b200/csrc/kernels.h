@@ -231,6 +231,9 @@ void launch_field_density(const FieldDesc* field, const float* params, const flo
                           float* feat, cudaStream_t s);
 void launch_field_color(const FieldDesc* field, const float* params, const float* feat, const float* dirs,
                         const float* app, uint64_t n, float* rgb, cudaStream_t s);
+void launch_occupancy_skip(const uint8_t* bits, const uint32_t shape[3], const double lo[3], const double hi[3],
+                           const double* o, const double* d, const double* t0, const double* t1, uint64_t n,
+                           uint32_t* counts, const uint64_t* out_off, double* iv, cudaStream_t s);
 void launch_adam_f64(double* p, const double* g, double* m, double* v, uint64_t n, double lr, double b1,
                      double b2, double eps, double bias1, double bias2, cudaStream_t s);
 

@@ -3,6 +3,7 @@
 // batched, fp64 in the reference's evaluation order (no contraction: dadd/dmul/ddiv):
 //   ray_aabb_intersect   geometry.cpp:7-28   one thread per ray, one box per call
 //   march_segment        render.cpp:10-37    one thread per segment over caller intervals
+//   occupancy_skip       grid.cpp:235-304    one thread per query over a caller bitfield
 //   AdamState::step      train.cpp:91-115    fp64 moments over caller arrays
 #include "geometry.cuh"
 #include "kernels.h"
@@ -60,6 +61,37 @@ __global__ void k_march_segment(const double* __restrict__ te, const double* __r
       ladder(iv[2 * k], iv[2 * k + 1], t_enter, t_exit, offset, step, emit);
   }
   if (counts) counts[g] = cnt;
+}
+
+// occupancy_skip (grid.cpp:235-304) over a caller's row-major bitfield (ix fastest): counts
+// (iv == nullptr) or the occupied runs of query q at out_off[q], as (t_near, t_far) pairs.
+__global__ void k_occupancy_skip(const uint8_t* __restrict__ bits, uint32_t nx, uint32_t ny, uint32_t nz,
+                                 double lo0, double lo1, double lo2, double hi0, double hi1, double hi2,
+                                 const double* __restrict__ o, const double* __restrict__ d,
+                                 const double* __restrict__ t0, const double* __restrict__ t1, uint64_t n,
+                                 uint32_t* __restrict__ counts, const uint64_t* __restrict__ out_off,
+                                 double* __restrict__ iv) {
+  const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const double oo[3] = {o[3 * q], o[3 * q + 1], o[3 * q + 2]};
+  const double dd[3] = {d[3 * q], d[3 * q + 1], d[3 * q + 2]};
+  const double lo[3] = {lo0, lo1, lo2}, hi[3] = {hi0, hi1, hi2};
+  const uint32_t sh[3] = {nx, ny, nz};
+  const auto linear = [&](uint32_t ix, uint32_t iy, uint32_t iz) {
+    return bits[ix + (uint64_t)nx * (iy + (uint64_t)ny * iz)] != 0;
+  };
+  uint32_t cnt = 0;
+  uint64_t at = iv ? out_off[q] : 0;
+  auto on_run = [&](double a, double b) {
+    if (iv) {
+      iv[2 * at] = a;
+      iv[2 * at + 1] = b;
+      ++at;
+    }
+    ++cnt;
+  };
+  occupancy_walk_fn(oo, dd, t0[q], t1[q], lo, hi, sh, linear, on_run);
+  if (counts) counts[q] = cnt;
 }
 
 __global__ void k_adam_f64(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
@@ -193,6 +225,14 @@ void launch_field_density(const FieldDesc* field, const float* params, const flo
 void launch_field_color(const FieldDesc* field, const float* params, const float* feat, const float* dirs,
                         const float* app, uint64_t n, float* rgb, cudaStream_t s) {
   if (n) k_field_color<<<nblk(n, 64), 64, 0, s>>>(field, params, feat, dirs, app, n, rgb);
+}
+
+void launch_occupancy_skip(const uint8_t* bits, const uint32_t shape[3], const double lo[3], const double hi[3],
+                           const double* o, const double* d, const double* t0, const double* t1, uint64_t n,
+                           uint32_t* counts, const uint64_t* out_off, double* iv, cudaStream_t s) {
+  if (n)
+    k_occupancy_skip<<<nblk(n, 128), 128, 0, s>>>(bits, shape[0], shape[1], shape[2], lo[0], lo[1], lo[2], hi[0],
+                                                   hi[1], hi[2], o, d, t0, t1, n, counts, out_off, iv);
 }
 
 void launch_adam_f64(double* p, const double* g, double* m, double* v, uint64_t n, double lr, double b1,

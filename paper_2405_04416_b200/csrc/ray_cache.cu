@@ -56,8 +56,9 @@ __global__ void k_make_pixel_rays(const DevPose* __restrict__ poses, const uint8
 // draw_batch: batch[i] = entries[idx[i]]
 __global__ void k_gather_rays(const uint32_t* __restrict__ idx, uint64_t n, const double* __restrict__ o,
                               const double* __restrict__ d, const float* __restrict__ gt,
-                              const uint32_t* __restrict__ img, double* __restrict__ bo, double* __restrict__ bd,
-                              float* __restrict__ bgt, uint32_t* __restrict__ bimg) {
+                              const uint32_t* __restrict__ img, const uint64_t* __restrict__ pix,
+                              double* __restrict__ bo, double* __restrict__ bd, float* __restrict__ bgt,
+                              uint32_t* __restrict__ bimg, uint64_t* __restrict__ bpix) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint64_t e = idx[i];
@@ -68,6 +69,7 @@ __global__ void k_gather_rays(const uint32_t* __restrict__ idx, uint64_t n, cons
     bgt[3 * i + a] = gt[3 * e + a];
   }
   bimg[i] = img[e];
+  bpix[i] = pix[e];
 }
 
 uint64_t splitmix(uint64_t x) {  // rng.hpp:8-15
@@ -116,7 +118,7 @@ struct dg_ray_cache {
   dg::Buf poses, pixels;
   dg::Buf e_origin, e_dir, e_gt, e_img, e_pix;  // entries (capacity)
   dg::Buf req, idx;                             // staging
-  dg::Buf b_origin, b_dir, b_gt, b_img;         // drawn batch
+  dg::Buf b_origin, b_dir, b_gt, b_img, b_pix;  // drawn batch
   std::vector<uint32_t> h_req, h_idx;
   uint64_t batch_cap = 0;
 };
@@ -252,7 +254,7 @@ int dg_ray_cache_draw(dg_ray_cache* c, uint64_t n, dg_ray_batch* out) {
   for (uint64_t i = 0; i < n; ++i) c->h_idx[i] = uint32_t(c->draw_rng() % c->size);
   if (n > c->batch_cap) {
     if (!c->b_origin.ensure(n * 24) || !c->b_dir.ensure(n * 24) || !c->b_gt.ensure(n * 12) ||
-        !c->b_img.ensure(n * 4) || !c->idx.ensure(n * 4))
+        !c->b_img.ensure(n * 4) || !c->b_pix.ensure(n * 8) || !c->idx.ensure(n * 4))
       return set_error(DG_ENOMEM, "ray cache: batch allocation failed");
     c->batch_cap = n;
   }
@@ -260,8 +262,8 @@ int dg_ray_cache_draw(dg_ray_cache* c, uint64_t n, dg_ray_batch* out) {
     RC_CU(cudaMemcpyAsync(c->idx.p, c->h_idx.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
     dg::k_gather_rays<<<unsigned((n + 255) / 256), 256, 0, c->stream>>>(
         c->idx.as<uint32_t>(), n, c->e_origin.as<double>(), c->e_dir.as<double>(), c->e_gt.as<float>(),
-        c->e_img.as<uint32_t>(), c->b_origin.as<double>(), c->b_dir.as<double>(), c->b_gt.as<float>(),
-        c->b_img.as<uint32_t>());
+        c->e_img.as<uint32_t>(), c->e_pix.as<uint64_t>(), c->b_origin.as<double>(), c->b_dir.as<double>(),
+        c->b_gt.as<float>(), c->b_img.as<uint32_t>(), c->b_pix.as<uint64_t>());
     RC_CU(cudaGetLastError());
   }
   RC_CU(cudaStreamSynchronize(c->stream));
@@ -273,6 +275,21 @@ int dg_ray_cache_draw(dg_ray_cache* c, uint64_t n, dg_ray_batch* out) {
   out->first_ray_id = 0;
   out->mem = DG_MEM_DEVICE;
   out->reserved = 0;
+  return DG_OK;
+}
+
+// RayCache::draw_batch (train.cpp:150-158) into host arrays (the facade's RayCache).
+int dg_ray_cache_draw_host(dg_ray_cache* c, uint64_t n, double* origin, double* dir, float* color_gt,
+                           uint32_t* image_id, uint64_t* pixel_id) {
+  dg_ray_batch b;
+  const int rc = dg_ray_cache_draw(c, n, &b);
+  if (rc != DG_OK || n == 0) return rc;
+  if (origin) RC_CU(cudaMemcpyAsync(origin, c->b_origin.p, n * 24, cudaMemcpyDeviceToHost, c->stream));
+  if (dir) RC_CU(cudaMemcpyAsync(dir, c->b_dir.p, n * 24, cudaMemcpyDeviceToHost, c->stream));
+  if (color_gt) RC_CU(cudaMemcpyAsync(color_gt, c->b_gt.p, n * 12, cudaMemcpyDeviceToHost, c->stream));
+  if (image_id) RC_CU(cudaMemcpyAsync(image_id, c->b_img.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (pixel_id) RC_CU(cudaMemcpyAsync(pixel_id, c->b_pix.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  RC_CU(cudaStreamSynchronize(c->stream));
   return DG_OK;
 }
 

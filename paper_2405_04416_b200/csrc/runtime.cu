@@ -2692,6 +2692,39 @@ int dg_march_segment(dg_ctx* c, const double* t_enter, const double* t_exit, con
   return io.finish();
 }
 
+int dg_occupancy_skip(dg_ctx* c, const uint8_t* bits, const uint32_t shape[3], const double box_lo[3],
+                      const double box_hi[3], const double* origin, const double* dir, const double* t0,
+                      const double* t1, uint64_t n, uint32_t* counts, const uint64_t* offsets, double* intervals,
+                      int32_t mem) {
+  TRY(check_ctx(c));
+  if (!bits || !shape || !box_lo || !box_hi) return set_err(DG_EINVAL, "null argument");
+  if (!counts && !intervals) return set_err(DG_EINVAL, "occupancy_skip: need counts or outputs");
+  if (intervals && !offsets) return set_err(DG_EINVAL, "occupancy_skip: outputs need offsets");
+  if (n && (!origin || !dir || !t0 || !t1)) return set_err(DG_EINVAL, "null queries");
+  const uint64_t cells = uint64_t(shape[0]) * shape[1] * shape[2];
+  StageIo io{c, mem, {}, {}};
+  const uint8_t* b;
+  const double *o, *d, *a, *z;
+  const uint64_t* od = nullptr;
+  TRY(io.in(bits, cells, &b));
+  TRY(io.in(origin, 3 * n, &o));
+  TRY(io.in(dir, 3 * n, &d));
+  TRY(io.in(t0, n, &a));
+  TRY(io.in(t1, n, &z));
+  uint32_t* cnt;
+  TRY(io.out(counts, n, &cnt));
+  double* iv = nullptr;
+  if (intervals) {
+    std::vector<uint64_t> oo;
+    TRY(host_offsets(c, offsets, n, mem, oo));
+    TRY(io.in(offsets, n + 1, &od));
+    TRY(io.out(intervals, 2 * oo[n], &iv));
+  }
+  launch_occupancy_skip(b, shape, box_lo, box_hi, o, d, a, z, n, cnt, od, iv, c->stream);
+  ++c->launches;
+  return io.finish();
+}
+
 int dg_adam_update_f64(dg_ctx* c, double* params, const double* grads, double* m, double* v, uint64_t n,
                        uint64_t t, double lr, double beta1, double beta2, double eps, int32_t mem) {
   TRY(check_ctx(c));

@@ -169,17 +169,22 @@ def test_cpp_facade_stage_api(tmp_path):
     assert pos[0] == len(v)
 
 
-def test_reference_render_tests_on_facade():
-    """The reference's own unit-test file tests/test_render.cpp (ray_aabb_intersect,
-    march_segment, local_render, merge_forward / merge_backward, local_render_backward; 16 cases,
-    golden values and finite-difference checks at 1e-6 .. 1e-12), compiled UNMODIFIED against the
-    facade headers (include/distgrid/) with a doctest-compatible shim by __graft_entry__.build()
-    (tests/cpp/Makefile; the reference sources exist only in the build container), run here on
-    the GPU: every case must pass."""
-    exe = os.path.join(ROOT, "tests", "cpp", "_build", "ref_test_render")
+@pytest.mark.parametrize("name,cases", [("render", 16), ("train", 12)])
+def test_reference_unit_tests_on_facade(name, cases):
+    """The reference's own unit-test files, compiled UNMODIFIED against the facade headers
+    (include/distgrid/) with a doctest-compatible shim by __graft_entry__.build()
+    (tests/cpp/Makefile; the reference sources exist only in the build container), run on the
+    GPU; every case must pass:
+      * test_render.cpp (16 cases): ray_aabb_intersect, march_segment, local_render,
+        merge_forward / merge_backward, local_render_backward — golden values and
+        finite-difference checks down to 1e-12 (the fp64 stage kernels);
+      * test_train.cpp (12 cases): losses and their gradients, the lr schedule, Adam's two-step
+        recurrence and shape errors, and the ray cache (refresh ring order, chi-square pixel
+        coverage over 1e6 entries, concurrent refresh / draw) on the device ray cache."""
+    exe = os.path.join(ROOT, "tests", "cpp", "_build", f"ref_test_{name}")
     if not os.path.exists(exe):
-        pytest.skip("tests/cpp/_build/ref_test_render was not built (reference tree absent at build time)")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+        pytest.skip(f"{exe} was not built (reference tree absent at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     summary = [l for l in r.stdout.splitlines() if l.startswith("[doctest] test cases")]
     assert r.returncode == 0 and summary, (r.stdout[-3000:], r.stderr[-3000:])
-    assert "| 0 failed" in summary[0] and "16 passed" in summary[0], summary
+    assert "| 0 failed" in summary[0] and f"{cases} passed" in summary[0], summary
