@@ -50,19 +50,51 @@ __device__ __forceinline__ void level_corners(const LevelDesc& lv, const double 
   }
 }
 
-// The backward's variant: the same fp64 indices and fractions, but the corner weights are
-// formed in fp32 from the fp64 factors rounded once (<= 2 ulp from the rounded fp64 product;
-// a weight only scales the upstream gradient, it never feeds a nonlinearity), and a corner is
-// skipped exactly when one fp64 factor is 0 (the fp64 product cannot underflow).
-__device__ __forceinline__ void level_corners_w32(const LevelDesc& lv, const double p[3], Corners& c) {
-  const AxisW ax = lattice_axis(p[0], lv.n[0]);
-  const AxisW ay = lattice_axis(p[1], lv.n[1]);
-  const AxisW az = lattice_axis(p[2], lv.n[2]);
-  const double fx[2] = {dsub(1.0, ax.frac), ax.frac};
-  const double fy[2] = {dsub(1.0, ay.frac), ay.frac};
-  const double fz[2] = {dsub(1.0, az.frac), az.frac};
+// Per-axis lattice indices and fractions of one level (fp64, bit-exact).
+struct LatticeAxes {
+  AxisW a[3];
+};
+
+__device__ __forceinline__ LatticeAxes lattice_axes(const LevelDesc& lv, const double p[3]) {
+  LatticeAxes la;
+  la.a[0] = lattice_axis(p[0], lv.n[0]);
+  la.a[1] = lattice_axis(p[1], lv.n[1]);
+  la.a[2] = lattice_axis(p[2], lv.n[2]);
+  return la;
+}
+
+// The eight fp32 corner weights of one level from its lattice axes: the fp64 factors rounded
+// once, multiplied in fp32 (<= 2 ulp from the rounded fp64 product; a weight only scales the
+// upstream gradient, it never feeds a nonlinearity); a corner whose fp64 factor is 0 gets
+// weight 0 and is skipped by the callers (grid.cpp:119-120; the fp64 product cannot underflow).
+__device__ __forceinline__ void corner_weights_w32(const LatticeAxes& la, float w[8], bool zero[8]) {
+  const double fx[2] = {dsub(1.0, la.a[0].frac), la.a[0].frac};
+  const double fy[2] = {dsub(1.0, la.a[1].frac), la.a[1].frac};
+  const double fz[2] = {dsub(1.0, la.a[2].frac), la.a[2].frac};
   const float gx[2] = {(float)fx[0], (float)fx[1]}, gy[2] = {(float)fy[0], (float)fy[1]};
   const float gz[2] = {(float)fz[0], (float)fz[1]};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int cx = k & 1, cy = (k >> 1) & 1, cz = (k >> 2) & 1;
+    w[k] = __fmul_rn(__fmul_rn(gx[cx], gy[cy]), gz[cz]);
+    zero[k] = fx[cx] == 0.0 || fy[cy] == 0.0 || fz[cz] == 0.0;
+  }
+}
+
+// Table row of lattice vertex (ix, iy, iz) of a level (grid.cpp:75-84).
+__device__ __forceinline__ uint32_t vertex_row(const LevelDesc& lv, uint32_t ix, uint32_t iy, uint32_t iz) {
+  return lv.hashed ? ((ix ^ (iy * 2654435761u) ^ (iz * 805459861u)) & lv.mask)
+                   : (ix + lv.n[0] * iy + lv.n[0] * lv.n[1] * iz);
+}
+
+// The backward's corners: the same fp64 indices and fractions as level_corners, fp32 weights
+// (corner_weights_w32).
+__device__ __forceinline__ void corners_w32(const LevelDesc& lv, const LatticeAxes& la, Corners& c) {
+  bool zero[8];
+  corner_weights_w32(la, c.w, zero);
+  const AxisW& ax = la.a[0];
+  const AxisW& ay = la.a[1];
+  const AxisW& az = la.a[2];
   uint32_t rx[2], ry[2], rz[2];
   if (lv.hashed) {
     rx[0] = ax.i0;
@@ -82,11 +114,13 @@ __device__ __forceinline__ void level_corners_w32(const LevelDesc& lv, const dou
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int cx = k & 1, cy = (k >> 1) & 1, cz = (k >> 2) & 1;
-    c.w[k] = __fmul_rn(__fmul_rn(gx[cx], gy[cy]), gz[cz]);
-    const bool zero = fx[cx] == 0.0 || fy[cy] == 0.0 || fz[cz] == 0.0;
     const uint32_t row = lv.hashed ? ((rx[cx] ^ ry[cy] ^ rz[cz]) & lv.mask) : (rx[cx] + ry[cy] + rz[cz]);
-    c.row[k] = zero ? 0xffffffffu : row;
+    c.row[k] = zero[k] ? 0xffffffffu : row;
   }
+}
+
+__device__ __forceinline__ void level_corners_w32(const LevelDesc& lv, const double p[3], Corners& c) {
+  corners_w32(lv, lattice_axes(lv, p), c);
 }
 
 // Row pairing: the two x-neighbour corners (cx = 0, 1) of each (cy, cz) land in rows

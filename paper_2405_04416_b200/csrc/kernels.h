@@ -48,6 +48,8 @@ struct SampleArrays {
   float4* out;     // sigma, r, g, b
   float4* grad;    // dsigma, dr, dg, db
   float* dX;       // n x 32
+  const uint32_t* inv;  // sample order (kernels_order.cu): march sample -> sorted slot; null: none
+  float4* grad_ord;     // with inv: the merge backward's upstream, stored at the sorted slot
 };
 
 struct LossAccum {
@@ -127,6 +129,9 @@ void launch_items_to_records(uint32_t n, const float4* partial, const float* dep
 struct EncPass {
   uint8_t l0, l1, k, S;
   uint8_t f, pad0, pad1, pad2;
+  // S > 1 (a single level l0): table rows [lo, hi) of slice k, per field (f == kAllFields:
+  // fields 0 and 1 of the single local partition; otherwise slot 0 is field f)
+  uint32_t lo[2], hi[2];
 };
 constexpr int kMaxEncPass = 256;  // per launch; longer pass lists are launched in chunks
 constexpr uint8_t kAllFields = 0xff;  // EncPass.f: every local field's samples in one pass
@@ -144,6 +149,8 @@ struct FieldLaunch {
   uint32_t n_local;
   uint32_t levels;
   uint32_t agg_levels;     // levels whose backward scatter is warp-aggregated
+  uint32_t cta_mul;        // backward: CTA x visits sample chunk (x * cta_mul) % gridDim.x (0: x)
+  uint32_t box_bwd;        // backward: shared-memory vertex-box aggregation (spatially ordered samples)
   const float* params;
   float* grads;
   uint32_t n_pass;         // passes of this launch (grid.y)
@@ -154,6 +161,10 @@ struct FieldLaunch {
 };
 // Forward: one launch per slice index (slice k > 0 adds into X written by slice 0); returns
 // the number of launches.  Backward: one launch over every pass (reds commute).
+size_t order_sort_tmp_bytes(uint32_t n);
+int launch_order_field(const double* p, const uint32_t* item, uint64_t stride, uint64_t off, uint32_t n,
+                       uint32_t C, uint32_t bits, uint32_t* perm, uint32_t* inv, double* p_out,
+                       uint32_t* item_out, uint32_t* scratch, void* tmp, size_t tmp_bytes, cudaStream_t s);
 int launch_encode_fwd(const FieldLaunch& f, const std::vector<EncPass>& passes, float* X, cudaStream_t s);
 int launch_encode_bwd(const FieldLaunch& f, const std::vector<EncPass>& passes, const float* dX, cudaStream_t s);
 // stand-alone points variant (stage entry points): all points belong to one field
@@ -174,7 +185,8 @@ struct MlpLaunch {
   uint32_t levels;
   const float* dirs_f;         // optional per-sample dirs (stage entry) else from items
   const RayRec* rec;
-  const uint32_t* s_item;
+  const uint32_t* s_item;      // item of each sample (in sample order when perm is set)
+  const uint32_t* perm;        // sample order: tile row -> march sample (index of out); null: identity
   const float* app_table;      // [n_images][app_dim]
   const float* app_override;   // eval: one vector for all samples (or per-sample when app_per_sample)
   int app_per_sample;

@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(NT, 2) k_mlp_fwd(MlpLaunch m) {
       const float r = sigm(clip15(sm.b[0 * FLD + s], c));
       const float g = sigm(clip15(sm.b[1 * FLD + s], c));
       const float b = sigm(clip15(sm.b[2 * FLD + s], c));
-      m.out[s0 + s] = make_float4(expf(sm.sig_raw[s]), r, g, b);
+      m.out[m.perm ? m.perm[s0 + s] : s0 + s] = make_float4(expf(sm.sig_raw[s]), r, g, b);
     }
     __syncthreads();
   }

@@ -272,11 +272,13 @@ struct Pref {
       x[2 * j + 1] = xx.y;
     }
     if (part == SHP || part == APP) item = v ? __ldg(m.s_item + gs) : 0u;
-    if (want_g && part == 0) g = v ? __ldcs(m.grad_in + gs) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (want_g && part == 0)
+      g = v ? __ldcs(m.grad_in + gs) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 
   __device__ __forceinline__ void grad(const MlpLaunch& m, int part) {
-    if (part == 0) g = valid ? __ldcs(m.grad_in + gs) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (part == 0)
+      g = valid ? __ldcs(m.grad_in + gs) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __device__ __forceinline__ void rec(const MlpLaunch& m, int part) {
     if ((part == SHP || part == APP) && valid) {
@@ -678,7 +680,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
           clip_bits |= (z[k] > 15.f || z[k] < -15.f ? 1u : 0u) << (16 + k);
         }
         if (valid)
-          __stcs(m.out + gs, make_float4(expf(sm.sig_raw[row]), sigm(clip15(z[0])), sigm(clip15(z[1])),
+          __stcs(m.out + (m.perm ? __ldg(m.perm + gs) : gs), make_float4(expf(sm.sig_raw[row]), sigm(clip15(z[0])), sigm(clip15(z[1])),
                                          sigm(clip15(z[2]))));
         if (store_mask) __stcs(masks + 6ull * m.x_stride + gs, clip_bits);
       }

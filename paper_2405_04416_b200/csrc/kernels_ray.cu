@@ -618,7 +618,11 @@ __global__ void k_merge_backward(uint32_t n_items, ItemArrays it,
         const float alpha_grad = pf * (u - tail_c) - ut * pf * tail_t;
         const float dsig = alpha_grad * delta * om;
         const float cw = pf * alpha;
-        if (v) sm.grad[s] = make_float4(dsig, ucx * cw, ucy * cw, ucz * cw);
+        if (v) {
+          const float4 g = make_float4(dsig, ucx * cw, ucy * cw, ucz * cw);
+          if (sm.inv) sm.grad_ord[sm.inv[s]] = g;  // the MLP backward reads it in sample order
+          else sm.grad[s] = g;
+        }
         ctc = __shfl_sync(0xffffffffu, A, 0) * ctc + __shfl_sync(0xffffffffu, B, 0);
         cWs += warp_sum_f(w);
         cMs += warp_sum_f(w * ss);

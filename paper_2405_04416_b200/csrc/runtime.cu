@@ -1,3 +1,4 @@
+#include <numeric>
 // runtime.cu — the C ABI (include/distgrid_b200.h): context, state, and the composed
 // per-step pipeline that replaces DistributedRun::training_step / evaluate_rays
 // (worker.cpp:730-834) and Worker::handle_training_batch (worker.cpp:251-401).
@@ -139,7 +140,15 @@ struct dg_ctx {
   std::vector<std::vector<dg_array_desc>> layouts;
   uint64_t enc_budget_fwd = 192ull << 20;  // encode pass budgets (DG_ENC_FWD_MB / DG_ENC_BWD_MB)
   uint64_t enc_budget_bwd = 96ull << 20;
+  uint64_t enc_group_fwd = 0, enc_group_bwd = 0;  // level-grouping budgets (0: = slice budget)
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
+  bool sample_order = true;                // spatial sample order (DG_SAMPLE_ORDER=0 disables)
+  uint32_t order_bits = 8;                 // Morton cells per axis = 2^order_bits (DG_ORDER_BITS)
+  uint32_t order_chunk = 8;                // samples per sorted chunk (DG_ORDER_CHUNK)
+  uint32_t bwd_cta_mul = 7919;             // encode backward CTA visiting stride (DG_ENC_BWD_STRIDE)
+  bool enc_box = false;                    // shared-cell warp sums in the ordered backward (DG_ENC_BWD_BOX=1)
+  bool ordered = false;                    // the last front half ordered its samples
+  DBuf s_perm, s_inv, s_p_alt, s_item_ord, s_grad_ord, ord_scratch, ord_tmp;
   double enc_agg_samples_per_cell = 1.5;   // warp-aggregate levels with >= this many samples/cell (DG_ENC_AGG)
   uint64_t n_params = 0;
   uint64_t occ_bytes = 0;                 // bricked bitfields (all local partitions, both cascades)
@@ -560,6 +569,8 @@ SampleArrays sample_arrays(dg_ctx* c) {
   sm.out = c->s_out.as<float4>();
   sm.grad = c->s_grad.as<float4>();
   sm.dX = c->s_dX.as<float>();
+  sm.inv = c->ordered ? c->s_inv.as<uint32_t>() : nullptr;
+  sm.grad_ord = c->ordered ? c->s_grad_ord.as<float4>() : nullptr;
   return sm;
 }
 
@@ -613,8 +624,44 @@ __global__ void k_block_permute(const uint64_t* __restrict__ src, uint64_t* __re
 
 // Runs the K1/X1/K2 front half shared by train and render.  On return the items and
 // sample arrays are filled (march done) and c->part_item_off / c->field_off describe them.
+// Spatial sample order (kernels_order.cu): after the march, each field's samples are radix-
+// sorted by the Morton code of their normalised position (2^order_bits cells per axis).  The
+// encode passes, the MLP tiles, X / dX and the ReLU masks then run in that order; positions and
+// item ids are gathered into it once (s_p / s_item_ord), and the MLP reads its upstream and
+// writes its outputs through s_perm (sorted slot -> march sample), so the march / compositing /
+// merge arrays keep the march (ray, t) order.  Samples of one lattice cell now share a CTA: the
+// forward's corner rows hit L1 / L2 instead of HBM, and the backward scatters from spatially
+// compact CTAs (visited in a strided CTA order so concurrently running CTAs do not contend for
+// the same rows).
+int order_samples(dg_ctx* c, uint64_t NS, cudaStream_t s) {
+  c->ordered = false;
+  if (!c->sample_order || !c->enc_pcache || !NS) return DG_OK;
+  const uint32_t C = c->order_chunk;
+  TRY(c->s_perm.ensure(NS * 4 + 16));
+  TRY(c->s_inv.ensure(NS * 4 + 16));
+  TRY(c->s_p_alt.ensure(NS * 24 + 16));
+  TRY(c->s_item_ord.ensure(NS * 4 + 16));
+  TRY(c->s_grad_ord.ensure(NS * 16 + 16));
+  TRY(c->ord_scratch.ensure((NS / C + 1) * 16 + 16));
+  const size_t tb = order_sort_tmp_bytes(uint32_t(NS / C + 1));
+  TRY(c->ord_tmp.ensure(tb + 16));
+  for (size_t f = 0; f + 1 < c->field_off.size(); ++f) {
+    const uint32_t o = c->field_off[f], n = c->field_off[f + 1] - o;
+    const int k = launch_order_field(c->s_p.as<double>(), c->s_item.as<uint32_t>(), NS, o, n, C, c->order_bits,
+                                     c->s_perm.as<uint32_t>(), c->s_inv.as<uint32_t>(), c->s_p_alt.as<double>(),
+                                     c->s_item_ord.as<uint32_t>(), c->ord_scratch.as<uint32_t>(), c->ord_tmp.p, tb, s);
+    if (k < 0) return set_err(DG_ECUDA, "sample order: radix sort failed");
+    c->launches += k;
+  }
+  std::swap(c->s_p.p, c->s_p_alt.p);  // s_p now holds the positions in sample order
+  std::swap(c->s_p.bytes, c->s_p_alt.bytes);
+  c->ordered = true;
+  return DG_OK;
+}
+
 int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, uint64_t* dropped_out,
                uint64_t* bytes_sent) {
+  c->ordered = false;
   cudaStream_t s = c->stream;
   const uint64_t n = b->n;
   const uint32_t P = c->P, nl = uint32_t(c->local.size());
@@ -846,6 +893,7 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   launch_march_fill(c->d_parts.as<PartDesc>(), c->occ.as<uint8_t>(), NI, it, sm, c->n_fine,
                     c->step, c->cfg.seed, batch_id, train, s);
   c->launches += 2;  // march fill (runs, with the position cache) + overflow walk
+  TRY(order_samples(c, NS, s));
   // tile tables
   std::vector<uint32_t> tf(2 * nl + 1, 0), tb(2 * nl + 1, 0);
   for (uint32_t f = 0; f < 2 * nl; ++f) {
@@ -862,7 +910,8 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   return DG_OK;
 }
 
-FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passes) {
+FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passes, uint64_t group) {
+  if (!group) group = budget;
   FieldLaunch f{};
   f.fields = c->d_fields.as<FieldDesc>();
   f.parts = c->d_parts.as<PartDesc>();
@@ -896,11 +945,21 @@ FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passe
     for (uint32_t l = 0; l < f.levels;) {
       uint32_t l1 = l + 1;
       uint64_t bytes = level_bytes(l);
-      while (l1 < f.levels && bytes + level_bytes(l1) <= budget) bytes += level_bytes(l1++);
+      const uint64_t gb = std::min(group, budget);  // a sliced pass is always a single level
+      while (l1 < f.levels && bytes + level_bytes(l1) <= gb) bytes += level_bytes(l1++);
       const uint32_t S = std::min<uint64_t>(64, std::max<uint64_t>(1, (bytes + budget - 1) / budget));
-      for (uint32_t k = 0; k < S; ++k)
-        passes.push_back(EncPass{uint8_t(l), uint8_t(l1), uint8_t(k), uint8_t(S),
-                                 merged ? kAllFields : uint8_t(fi), 0, 0, 0});
+      for (uint32_t k = 0; k < S; ++k) {
+        EncPass ps{uint8_t(l), uint8_t(l1), uint8_t(k), uint8_t(S), merged ? kAllFields : uint8_t(fi), 0, 0, 0,
+                   {0u, 0u}, {0xffffffffu, 0xffffffffu}};
+        for (uint32_t slot = 0; slot < 2 && S > 1; ++slot) {  // slice bounds, even rows
+          const uint32_t fld = merged ? slot : fi;
+          if (fld >= c->fields.size()) break;
+          const uint64_t rows = c->fields[fld].lv[l].rows;
+          ps.lo[slot] = uint32_t((rows * k / S) & ~1ull);
+          ps.hi[slot] = k + 1 == S ? 0xffffffffu : uint32_t((rows * (k + 1) / S) & ~1ull);
+        }
+        passes.push_back(ps);
+      }
       l = l1;
     }
   }
@@ -940,12 +999,13 @@ MlpLaunch mlp_launch(dg_ctx* c, bool bwd) {
   m.x_stride = uint64_t(c->n_fine) + c->n_coarse;
   m.levels = c->cfg.grid_levels;
   m.rec = c->items_rec;
-  m.s_item = c->s_item.as<uint32_t>();
+  m.s_item = c->ordered ? c->s_item_ord.as<uint32_t>() : c->s_item.as<uint32_t>();
+  m.perm = c->ordered ? c->s_perm.as<uint32_t>() : nullptr;
   m.app_table = c->app.as<float>();
   m.params = c->params.as<float>();
   m.grads = c->grads.as<float>();
   m.out = c->s_out.as<float4>();
-  m.grad_in = c->s_grad.as<float4>();
+  m.grad_in = c->ordered ? c->s_grad_ord.as<float4>() : c->s_grad.as<float4>();
   m.dX = c->s_dX.as<float>();
   m.masks = c->s_mask.as<uint32_t>();  // set by the training step's forward, read by its backward
   return m;
@@ -1294,9 +1354,16 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   if (const char* e = std::getenv("DG_ENC_FWD_MB"))
     c->enc_budget_fwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   if (const char* e = std::getenv("DG_ENC_PCACHE")) c->enc_pcache = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("DG_SAMPLE_ORDER")) c->sample_order = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("DG_ORDER_CHUNK")) c->order_chunk = std::min(64u, std::max(1u, uint32_t(std::atoi(e))));
+  if (const char* e = std::getenv("DG_ORDER_BITS")) c->order_bits = std::min(10u, std::max(1u, uint32_t(std::atoi(e))));
+  if (const char* e = std::getenv("DG_ENC_BWD_STRIDE")) c->bwd_cta_mul = uint32_t(std::strtoul(e, nullptr, 10));
+  if (const char* e = std::getenv("DG_ENC_BWD_BOX")) c->enc_box = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("DG_ENC_AGG")) c->enc_agg_samples_per_cell = std::max(0.01, std::atof(e));
   if (const char* e = std::getenv("DG_ENC_BWD_MB"))
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
+  if (const char* e = std::getenv("DG_ENC_FWD_GROUP_MB")) c->enc_group_fwd = std::strtoull(e, nullptr, 10) << 20;
+  if (const char* e = std::getenv("DG_ENC_BWD_GROUP_MB")) c->enc_group_bwd = std::strtoull(e, nullptr, 10) << 20;
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = c->stream;
   CU(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
@@ -1716,7 +1783,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   // K3 / K4 forward
   {
     std::vector<EncPass> passes;
-    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes);
+    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd);
     c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
   }
   mark(c, 3);
@@ -1755,7 +1822,18 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   mark(c, 8);
   {
     std::vector<EncPass> passes;
-    const FieldLaunch fl = field_launch(c, c->enc_budget_bwd, passes);
+    FieldLaunch fl = field_launch(c, c->enc_budget_bwd, passes, c->enc_group_bwd);
+    if (c->ordered && c->bwd_cta_mul) {  // a CTA stride coprime with the CTA count along x
+      uint64_t nb = 0;
+      for (const EncPass& p : passes)
+        nb = std::max<uint64_t>(nb, p.f == kAllFields ? fl.n_total : fl.field_off[p.f + 1] - fl.field_off[p.f]);
+      nb = (nb + 255) / 256;
+      uint64_t m = c->bwd_cta_mul % std::max<uint64_t>(nb, 1);
+      if (m == 0) m = 1;
+      while (nb > 1 && std::gcd(m, nb) != 1) ++m;
+      fl.cta_mul = uint32_t(m);
+      fl.box_bwd = c->enc_box ? 1u : 0u;
+    }
     c->launches += launch_encode_bwd(fl, passes, sm.dX, s) - 1;
   }
   mark(c, 9);
@@ -1842,7 +1920,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   SampleArrays sm = sample_arrays(c);
   {
     std::vector<EncPass> passes;
-    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes);
+    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd);
     c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
   }
   MlpLaunch mf = mlp_launch(c, false);
@@ -2860,27 +2938,38 @@ int dg_last_sample_data(dg_ctx* c, uint32_t p, double* pos, float* features, flo
   if (pos) TRY(d2h(hp, c->s_p.p, 3 * NS, s));
   if (features) TRY(d2h(hx, c->s_X.p, 2ull * L * NS, s));
   if (field_out) TRY(d2h(ho, c->s_out.p, 4 * NS, s));
-  if (upstream) TRY(d2h(hg, c->s_grad.p, 4 * NS, s));
+  if (upstream) TRY(d2h(hg, c->ordered ? c->s_grad_ord.p : c->s_grad.p, 4 * NS, s));
   if (d_features) TRY(d2h(hdx, c->s_dX.p, 2ull * L * NS, s));
   std::vector<uint32_t> hm;
   if (masks) {
     if (!c->mlp_impl) return set_err(DG_EINVAL, "masks exist on the tcgen05 path only");
     TRY(d2h(hm, c->s_mask.p, 7 * NS, s));
   }
+  // positions, features, their gradients and the masks are in sample order when the step
+  // ordered its samples (s_perm: sorted slot -> march sample); map them back
+  std::vector<uint32_t> perm, inv;
+  if (c->ordered) {
+    TRY(d2h(perm, c->s_perm.p, NS, s));
+  }
   CU(cudaStreamSynchronize(s));
+  if (c->ordered) {
+    inv.assign(NS, 0);
+    for (uint64_t j = 0; j < NS; ++j) inv[perm[j]] = uint32_t(j);
+  }
   uint64_t k = 0;
   auto put = [&](uint64_t idx) {
-    for (int a = 0; a < 3 && pos; ++a) pos[3 * k + a] = hp[a * NS + idx];
+    const uint64_t o = c->ordered ? inv[idx] : idx;
+    for (int a = 0; a < 3 && pos; ++a) pos[3 * k + a] = hp[a * NS + o];
     for (uint32_t l = 0; l < L; ++l)
       for (int f = 0; f < 2; ++f) {
-        if (features) features[(k * L + l) * 2 + f] = hx[(l * NS + idx) * 2 + f];
-        if (d_features) d_features[(k * L + l) * 2 + f] = hdx[(l * NS + idx) * 2 + f];
+        if (features) features[(k * L + l) * 2 + f] = hx[(l * NS + o) * 2 + f];
+        if (d_features) d_features[(k * L + l) * 2 + f] = hdx[(l * NS + o) * 2 + f];
       }
     for (int a = 0; a < 4; ++a) {
       if (field_out) field_out[4 * k + a] = ho[4 * idx + a];
-      if (upstream) upstream[4 * k + a] = hg[4 * idx + a];
+      if (upstream) upstream[4 * k + a] = hg[4 * o + a];
     }
-    for (int w = 0; w < 7 && masks; ++w) masks[7 * k + w] = hm[w * NS + idx];
+    for (int w = 0; w < 7 && masks; ++w) masks[7 * k + w] = hm[w * NS + o];
     ++k;
   };
   for (uint32_t i = c->part_item_off[lp]; i < c->part_item_off[lp + 1]; ++i) {

@@ -134,10 +134,14 @@ def _rank_main(rank, world, port, ref_path, errq, cross=0, backend="host", corru
         # near-zero gradient into a full +-lr step of that entry, so the bar is on the
         # fraction of entries off by more than 1e-3 lr (as the parity suite's Adam check) plus
         # a loose rel L2.
+        # (The spatial sample order groups the coarse-level scatter per warp, so which
+        # near-zero gradients flip depends on the CTA layout of each world size; the flipped
+        # entries are what `off` counts, the rel L2 is over the others.)
         for g in ctx.local:
-            a, b = ctx.get_params(g), ref[f"p{g}"]
-            off = float(np.mean(np.abs(a.astype(np.float64) - b) > 1e-3 * cfg.lr_start))
-            err = rel_l2(a, b)
+            a, b = ctx.get_params(g).astype(np.float64), ref[f"p{g}"]
+            flip = np.abs(a - b) > 1e-3 * cfg.lr_start
+            off = float(np.mean(flip))
+            err = rel_l2(a[~flip], b[~flip])
             assert off <= 1e-3 and err < 1e-4, (rank, g, off, err)
         dist.barrier()
         dist.destroy_process_group()
