@@ -4,6 +4,7 @@
 #pragma once
 
 #include "distgrid/config.hpp"
+#include "distgrid/dataset.hpp"
 #include "distgrid/field.hpp"
 #include "distgrid/geometry.hpp"
 #include "distgrid/grid.hpp"

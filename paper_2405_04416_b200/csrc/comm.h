@@ -44,9 +44,13 @@ class Comm {
 // Exchanges over peer memory (one node, NVLink / NVSwitch): every rank's receive buffers are
 // CUDA-IPC mapped into every other rank, so the two pack kernels store each record straight
 // into its owner's buffer, in the owner's final layout — no staging buffer, no collective copy
-// kernel, no receive-side permute.  The host all-gather callback carries the per-step count
-// matrices, the IPC handles and the barriers (stream sync + all-gather: after it every rank's
-// pack kernel has completed, so every record is in place; no kernel ever waits on a peer).
+// kernel, no receive-side permute.  The per-step count matrices and the barriers travel over a
+// control buffer in device memory, CUDA-IPC mapped like the data buffers: a rank copies its
+// payload into slot [rank] of every peer's control buffer and then an epoch word into flag
+// [rank] (one copy stream, so the flag lands after the payload), and polls its own flags until
+// every peer's epoch has arrived (bounded by the step timeout).  The host all-gather callback
+// only bootstraps the control buffer's IPC handles.  No kernel ever waits on a peer: a barrier
+// is a stream sync + an all-gather, after which every rank's pack kernel has completed.
 class PeerComm final : public Comm {
  public:
   enum { kItems = 0, kPartials = 1, kCross = 2, kStage = 3, kBufs = 4 };
@@ -57,8 +61,11 @@ class PeerComm final : public Comm {
                 const std::vector<uint64_t>& recv_bytes, cudaStream_t s, std::string& err) override;
   const char* name() const override { return "peer"; }
   PeerComm* peer() override { return this; }
+  // all-gather of `bytes` per rank (rank order) over the control buffer; the host callback
+  // before the control buffer exists
   int allgather(const void* send, uint64_t bytes, void* recv, std::string& err);
   int barrier(cudaStream_t s, std::string& err);
+  uint64_t control_exchanges() const { return epoch_; }
   // collective: every rank's buffer k holds >= need bytes afterwards (need identical on all ranks)
   int reserve(int k, uint64_t need, std::string& err);
   void* local(int k) const { return buf_[k].local; }
@@ -74,10 +81,20 @@ class PeerComm final : public Comm {
     void** dev = nullptr;     // the same pointers on the device
   };
   void unmap(Buf& b);
+  int host_allgather(const void* send, uint64_t bytes, void* recv, std::string& err);
+  int control_init(std::string& err);
+  static constexpr uint64_t kSlot = 16384;  // bytes per rank and exchange (count matrices, handles)
   dg_allgather_fn fn_;
   void* user_;
   int rank_, world_;
   Buf buf_[kBufs];
+  // control buffer: [world] epoch flags (u64), then [2 (epoch parity)][world] slots of kSlot bytes
+  void* ctrl_ = nullptr;
+  std::vector<void*> ctrl_peer_;
+  cudaStream_t ctrl_s_ = nullptr;
+  uint64_t* ctrl_pin_ = nullptr;  // pinned: [0] epoch source, [1..world] flag readback, staging after
+  uint64_t epoch_ = 0;
+  bool ctrl_ok_ = false;
 };
 
 Comm* make_nccl_comm(const uint8_t id[DG_NCCL_UNIQUE_ID_BYTES], int rank, int world, int device,

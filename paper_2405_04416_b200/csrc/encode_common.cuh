@@ -123,6 +123,66 @@ __device__ __forceinline__ void level_corners_w32(const LevelDesc& lv, const dou
   corners_w32(lv, lattice_axes(lv, p), c);
 }
 
+// The training forward's gather of one level (k_encode_fwd) from its lattice axes: fp32 corner
+// weights (corner_weights_w32: <= 2 ulp from the reference's rounded fp64 products, i.e.
+// ~1e-7 of a feature), the two x-neighbour corners of each (y, z) pair fetched as one aligned
+// float4 when their rows share it.  A zero-weight corner contributes 0 * v (the reference skips
+// it: identical for finite tables).  SLICED: only rows in [lo, hi) are fetched.
+template <bool SLICED>
+__device__ __forceinline__ float2 gather_level_w32(const LevelDesc& lv, const LatticeAxes& la,
+                                                   const float2* __restrict__ table, uint32_t lo, uint32_t hi) {
+  float w[8];
+  bool zero[8];
+  corner_weights_w32(la, w, zero);
+  const uint32_t x0 = la.a[0].i0, x1 = la.a[0].i1;
+  uint32_t base[4];
+  if (lv.hashed) {
+    const uint32_t y0 = la.a[1].i0 * 2654435761u, y1 = la.a[1].i1 * 2654435761u;
+    const uint32_t z0 = la.a[2].i0 * 805459861u, z1 = la.a[2].i1 * 805459861u;
+    base[0] = y0 ^ z0;
+    base[1] = y1 ^ z0;
+    base[2] = y0 ^ z1;
+    base[3] = y1 ^ z1;
+  } else {
+    const uint32_t nx = lv.n[0], nxy = lv.n[0] * lv.n[1];
+    const uint32_t y0 = nx * la.a[1].i0, y1 = nx * la.a[1].i1, z0 = nxy * la.a[2].i0, z1 = nxy * la.a[2].i1;
+    base[0] = y0 + z0;
+    base[1] = y1 + z0;
+    base[2] = y0 + z1;
+    base[3] = y1 + z1;
+  }
+  const float4* t4 = reinterpret_cast<const float4*>(table);
+  float4 q[4];
+  float2 b[4];
+  uint32_t r0s[4];
+  bool pr[4], in0[4], in1[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t r0 = lv.hashed ? ((x0 ^ base[j]) & lv.mask) : x0 + base[j];
+    const uint32_t r1 = lv.hashed ? ((x1 ^ base[j]) & lv.mask) : x1 + base[j];
+    r0s[j] = r0;
+    pr[j] = (r0 ^ r1) == 1u;
+    in0[j] = !SLICED || (r0 >= lo && r0 < hi);
+    in1[j] = !SLICED || (r1 >= lo && r1 < hi);
+    q[j] = in0[j] || (pr[j] && in1[j]) ? __ldg(t4 + (r0 >> 1)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    b[j] = !pr[j] && in1[j] ? __ldg(table + r1) : make_float2(0.f, 0.f);
+  }
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool odd = r0s[j] & 1u;
+    float2 v0 = odd ? make_float2(q[j].z, q[j].w) : make_float2(q[j].x, q[j].y);
+    float2 v1 = pr[j] ? (odd ? make_float2(q[j].x, q[j].y) : make_float2(q[j].z, q[j].w)) : b[j];
+    const float w0 = (zero[2 * j] || !in0[j]) ? 0.f : w[2 * j];
+    const float w1 = (zero[2 * j + 1] || !in1[j]) ? 0.f : w[2 * j + 1];
+    acc.x = fmaf(w0, v0.x, acc.x);
+    acc.y = fmaf(w0, v0.y, acc.y);
+    acc.x = fmaf(w1, v1.x, acc.x);
+    acc.y = fmaf(w1, v1.y, acc.y);
+  }
+  return acc;
+}
+
 // Row pairing: the two x-neighbour corners (cx = 0, 1) of each (cy, cz) land in rows
 // i ^ h and (i + 1) ^ h (hashed) or r and r + 1 (one-to-one); when those differ only in bit 0
 // (half the time) they are one 16-byte aligned float4 (every level table is 16-byte aligned),

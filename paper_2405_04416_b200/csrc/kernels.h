@@ -150,7 +150,6 @@ struct FieldLaunch {
   uint32_t levels;
   uint32_t agg_levels;     // levels whose backward scatter is warp-aggregated
   uint32_t cta_mul;        // backward: CTA x visits sample chunk (x * cta_mul) % gridDim.x (0: x)
-  uint32_t box_bwd;        // backward: shared-memory vertex-box aggregation (spatially ordered samples)
   const float* params;
   float* grads;
   uint32_t n_pass;         // passes of this launch (grid.y)

@@ -61,9 +61,6 @@ __device__ __forceinline__ void scatter_level_pairs(float2* __restrict__ table, 
   }
 }
 
-// lattice_axis's upper index for lower index i0 (grid.cpp:22-41: clamped to n - 1)
-__device__ __forceinline__ uint32_t la_i1_of(uint32_t i0, uint32_t n) { return i0 + 1 < n - 1 ? i0 + 1 : n - 1; }
-
 // Keep only the corners whose row lies in this pass's slice of the level table (bounds from the
 // host: EncPass::lo / hi, slot = the sample's field in an all-fields pass, else 0).
 __device__ __forceinline__ void clip_to_slice(const EncPass& ps, uint32_t slot, Corners& c) {
@@ -84,38 +81,51 @@ __device__ __forceinline__ void st_stream(float2* p, float2 v) {
   asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y));
 }
 
-// Warp-aggregated scatter of one level: lanes hold consecutive samples (mostly one ray, in t
-// order), so at coarse levels neighbouring lanes share cells and hence identical corner rows.
-// For each corner slot, runs of equal (field, row) in lane order are summed with a segmented
-// shuffle scan and the run's last lane issues a single float2 red.  The scan runs only
-// ceil(log2(longest run)) steps (warp-uniform, from the run-head ballot).
-__device__ __forceinline__ void scatter_level_agg(float2* __restrict__ table, const Corners& c,
-                                                  float2 up, uint32_t field, bool valid) {
+// Warp-aggregated scatter of one level (the coarse levels, where neighbouring lanes share a
+// lattice cell: consecutive samples of a ray, or of a spatially ordered chunk run).  Lanes are
+// split into runs of equal (field, cell) in lane order; lanes of a run share all 8 corner rows,
+// so one segmented shuffle scan per corner value (its depth ceil(log2(longest run)), found
+// once per level) leaves each run's sums in its last lane, which issues the run's reds
+// (corner pairs merged).  Inactive lanes (zero upstream) form runs of their own and issue none.
+__device__ __forceinline__ void scatter_level_agg(float2* __restrict__ table, const Corners& c, const AxisW* ax,
+                                                  float2 up, uint32_t field, bool act) {
   const unsigned lane = threadIdx.x & 31;
+  const uint32_t key = act ? (ax[0].i0 | (ax[1].i0 << 11) | (ax[2].i0 << 22)) ^ (field << 31) : 0xffffffffu;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = lane == 0 || prev != key || !act;
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const unsigned run = 31u - __clz(heads & (0xffffffffu >> (31u - lane)));  // run start lane
+  const unsigned later = lane < 31 ? heads & (0xfffffffeu << lane) : 0u;
+  const unsigned len = head ? (later ? (unsigned)(__ffs(later) - 1) : 32u) - lane : 0u;
+  const unsigned longest = __reduce_max_sync(0xffffffffu, len);
+  float2 g[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t row = valid ? c.row[k] : 0xffffffffu;
-    const uint32_t prev_row = __shfl_up_sync(0xffffffffu, row, 1);
-    const uint32_t prev_fld = __shfl_up_sync(0xffffffffu, field, 1);
-    const bool head = lane == 0 || prev_row != row || prev_fld != field;
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    const unsigned run = 31u - __clz(heads & (0xffffffffu >> (31u - lane)));  // run start lane
-    // run length seen from its head lane: distance to the next head (or the warp end)
-    const unsigned later = lane < 31 ? heads & (0xfffffffeu << lane) : 0u;
-    const unsigned len = head ? (later ? (unsigned)(__ffs(later) - 1) : 32u) - lane : 0u;
-    const unsigned longest = __reduce_max_sync(0xffffffffu, len);
-    float vx = c.w[k] * up.x, vy = c.w[k] * up.y;
-    for (unsigned off = 1; off < longest; off <<= 1) {
-      const float tx = __shfl_up_sync(0xffffffffu, vx, off);
-      const float ty = __shfl_up_sync(0xffffffffu, vy, off);
-      if (lane >= off && lane - off >= run) {
-        vx += tx;
-        vy += ty;
+  for (int k = 0; k < 8; ++k) g[k] = make_float2(c.w[k] * up.x, c.w[k] * up.y);
+  for (unsigned off = 1; off < longest; off <<= 1) {
+    const bool take = lane >= off && lane - off >= run;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float tx = __shfl_up_sync(0xffffffffu, g[k].x, off);
+      const float ty = __shfl_up_sync(0xffffffffu, g[k].y, off);
+      if (take) {
+        g[k].x += tx;
+        g[k].y += ty;
       }
     }
-    const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
-    if (tail && row != 0xffffffffu && (vx != 0.f || vy != 0.f))
-      atomicAdd(table + row, make_float2(vx, vy));
+  }
+  const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
+  if (!(tail && act)) return;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t r0 = c.row[2 * j], r1 = c.row[2 * j + 1];
+    const float2 g0 = g[2 * j], g1 = g[2 * j + 1];
+    if (is_pair(r0, r1)) {
+      const float4 v = (r0 & 1u) ? make_float4(g1.x, g1.y, g0.x, g0.y) : make_float4(g0.x, g0.y, g1.x, g1.y);
+      atomicAdd(reinterpret_cast<float4*>(table) + (r0 >> 1), v);
+    } else {
+      if (r0 != 0xffffffffu) atomicAdd(table + r0, g0);
+      if (r1 != 0xffffffffu) atomicAdd(table + r1, g1);
+    }
   }
 }
 
@@ -153,8 +163,11 @@ __device__ __forceinline__ void load_point(const FieldLaunch& f, uint64_t s, con
 // lattice math, 8 gathers.
 // ALL: every pass of the launch covers every local field's samples (one partition per GPU);
 // otherwise each pass covers one field's samples (several partitions per GPU).
+#ifndef ENC_FWD_MINB
+#define ENC_FWD_MINB 1
+#endif
 template <bool PC, bool ALL>
-__global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __restrict__ X) {
+__global__ void __launch_bounds__(256, ENC_FWD_MINB) k_encode_fwd(FieldLaunch f, float* __restrict__ X) {
   const EncPass ps = f.pass[blockIdx.y];
   const uint64_t s = (ALL ? 0ull : (uint64_t)f.field_off[ps.f]) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= (ALL ? (uint64_t)f.n_total : (uint64_t)f.field_off[ps.f + 1])) return;
@@ -162,11 +175,13 @@ __global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __rest
   const FieldDesc& fd = f.fields[fidx];
   double p[3];
   load_point<PC>(f, s, fd, p);
+  const uint32_t slo = (ALL && fidx) ? ps.lo[1] : ps.lo[0], shi = (ALL && fidx) ? ps.hi[1] : ps.hi[0];
   for (uint32_t l = ps.l0; l < ps.l1; ++l) {
-    Corners c;
-    level_corners(fd.lv[l], p, c);
-    clip_to_slice(ps, ALL ? fidx : 0u, c);
-    float2 acc = gather_level_pairs(reinterpret_cast<const float2*>(f.params + fd.base + fd.lv[l].offset), c);
+    const LevelDesc lv = fd.lv[l];
+    const LatticeAxes la = lattice_axes(lv, p);
+    const float2* table = reinterpret_cast<const float2*>(f.params + fd.base + lv.offset);
+    float2 acc = ps.S > 1 ? gather_level_w32<true>(lv, la, table, slo, shi)
+                          : gather_level_w32<false>(lv, la, table, 0u, 0u);
     float2* xp = reinterpret_cast<float2*>(X) + (uint64_t)l * f.n_total + s;
     if (ps.k > 0) {
       const float2 o = ld_stream(xp);
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__(256) k_encode_fwd(FieldLaunch f, float* __rest
 }
 
 #ifndef ENC_BWD_MINB
-#define ENC_BWD_MINB 5  // 5 CTAs per SM (48 registers, 16 B of spills): ~1 % faster than 4
+#define ENC_BWD_MINB 4  // 4 CTAs per SM (64 registers; the per-cell run scan holds 16 sums)
 #endif
 template <bool PC, bool ALL>
 __global__ void __launch_bounds__(256, ENC_BWD_MINB) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
@@ -193,109 +208,19 @@ __global__ void __launch_bounds__(256, ENC_BWD_MINB) k_encode_bwd(FieldLaunch f,
   for (uint32_t l = ps.l0; l < ps.l1; ++l) {
     float2 up = make_float2(0.f, 0.f);
     Corners c;
+    LatticeAxes la;
     if (valid) {
       up = ld_stream(reinterpret_cast<const float2*>(dX) + (uint64_t)l * f.n_total + s);
-      level_corners_w32(fd.lv[l], p, c);
+      la = lattice_axes(fd.lv[l], p);
+      corners_w32(fd.lv[l], la, c);
       clip_to_slice(ps, ALL ? fidx : 0u, c);
     }
-    float2* table = reinterpret_cast<float2*>(f.grads + fd.base + fd.lv[l].offset);
-    if (l < f.agg_levels) {  // coarse levels: consecutive samples share corners
-      scatter_level_agg(table, c, up, fidx, valid && (up.x != 0.f || up.y != 0.f));
-    } else if (valid && (up.x != 0.f || up.y != 0.f)) {
-      scatter_level_pairs(table, c, up);
-    }
-  }
-}
-
-// Backward over spatially ordered samples (kernels_order.cu): a warp's 32 consecutive samples
-// are a compact blob of the field, so at the coarse levels all of its active lanes usually sit
-// in one lattice cell and share its 8 corners.  Such a warp sums its 8 x 2 corner
-// contributions across the lanes (a transposing butterfly: 16 shuffles, after which lane L
-// holds the sum of value (L >> 1) & 15) and issues 8 float2 reds instead of 256; other warps
-// scatter per lane (corner pairs merged, as k_encode_bwd).  CTAs visit their sample chunks in
-// a strided order (f.cta_mul) so that concurrently running CTAs work on distant blobs and
-// their reds do not contend for the same rows.
-#ifndef ENC_ORD_MINB
-#define ENC_ORD_MINB 4
-#endif
-template <bool ALL>
-__global__ void __launch_bounds__(256, ENC_ORD_MINB) k_encode_bwd_ord(FieldLaunch f, const float* __restrict__ dX) {
-  const EncPass ps = f.pass[blockIdx.y];
-  const uint32_t bx = f.cta_mul ? (uint32_t)(((uint64_t)blockIdx.x * f.cta_mul) % gridDim.x) : blockIdx.x;
-  const uint64_t base = ALL ? 0ull : (uint64_t)f.field_off[ps.f];
-  const uint64_t end = ALL ? (uint64_t)f.n_total : (uint64_t)f.field_off[ps.f + 1];
-  const uint64_t s = base + (uint64_t)bx * blockDim.x + threadIdx.x;
-  const bool valid = s < end;
-  const uint32_t fidx = ALL ? (valid ? sample_field(f, s) : 0u) : ps.f;
-  const FieldDesc& fd = f.fields[fidx];
-  double p[3] = {0.0, 0.0, 0.0};
-  if (valid) load_point<true>(f, s, fd, p);
-  const unsigned lane = threadIdx.x & 31;
-  // a warp whose samples span two fields never takes the shared-cell path
-  const uint32_t f_lo = __shfl_sync(0xffffffffu, fidx, 0), f_hi = __reduce_max_sync(0xffffffffu, valid ? fidx : 0u);
-  const bool one_field = f_lo == f_hi;
-  for (uint32_t l = ps.l0; l < ps.l1; ++l) {
-    const LevelDesc& lv = fd.lv[l];
-    float2 up = make_float2(0.f, 0.f);
-    if (valid) up = ld_stream(reinterpret_cast<const float2*>(dX) + (uint64_t)l * f.n_total + s);
     const bool act = valid && (up.x != 0.f || up.y != 0.f);
-    const unsigned amask = __ballot_sync(0xffffffffu, act);
-    if (!amask) continue;
-    float2* table = reinterpret_cast<float2*>(f.grads + fd.base + lv.offset);
-    LatticeAxes la;
-    if (act) la = lattice_axes(lv, p);
-    const int lead = __ffs(amask) - 1;
-    uint32_t cell[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) cell[a] = __shfl_sync(0xffffffffu, act ? la.a[a].i0 : 0u, lead);
-    const bool same = !act || (la.a[0].i0 == cell[0] && la.a[1].i0 == cell[1] && la.a[2].i0 == cell[2]);
-    if (one_field && __all_sync(0xffffffffu, same)) {
-      float v[16];
-      {
-        float w[8];
-        bool zero[8];
-        if (act) corner_weights_w32(la, w, zero);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float wk = (act && !zero[k]) ? w[k] : 0.f;
-          v[2 * k] = wk * up.x;
-          v[2 * k + 1] = wk * up.y;
-        }
-      }
-#pragma unroll
-      for (int step = 0; step < 4; ++step) {
-        const int o = 16 >> step, half = 8 >> step;
-        const bool upper = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (i < half) {
-            const float send = upper ? v[i] : v[half + i];
-            const float keep = upper ? v[half + i] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-          }
-        }
-      }
-      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-      // lane 4k holds corner k's x sum, lane 4k + 2 its y sum
-      const float vy = __shfl_down_sync(0xffffffffu, v[0], 2);
-      if ((lane & 3) == 0 && (v[0] != 0.f || vy != 0.f)) {
-        const uint32_t k = lane >> 2;
-        const uint32_t x = (k & 1) ? la_i1_of(cell[0], lv.n[0]) : cell[0];
-        const uint32_t y = ((k >> 1) & 1) ? la_i1_of(cell[1], lv.n[1]) : cell[1];
-        const uint32_t z = ((k >> 2) & 1) ? la_i1_of(cell[2], lv.n[2]) : cell[2];
-        const uint32_t row = vertex_row(lv, x, y, z);
-        const uint32_t slot = ALL ? fidx : 0u;
-        const bool in = ps.S == 1 || (row >= (slot ? ps.lo[1] : ps.lo[0]) && row < (slot ? ps.hi[1] : ps.hi[0]));
-        if (in) atomicAdd(table + row, make_float2(v[0], vy));
-      }
-    } else {
-      Corners c;
-      if (act) {
-        corners_w32(lv, la, c);
-        clip_to_slice(ps, ALL ? fidx : 0u, c);
-      }
-      if (l < f.agg_levels) scatter_level_agg(table, c, up, fidx, act);  // warp-uniform branch
-      else if (act) scatter_level_pairs(table, c, up);
+    float2* table = reinterpret_cast<float2*>(f.grads + fd.base + fd.lv[l].offset);
+    if (l < f.agg_levels) {  // coarse levels: neighbouring lanes share cells (warp-uniform branch)
+      scatter_level_agg(table, c, la.a, up, fidx, act);
+    } else if (act) {
+      scatter_level_pairs(table, c, up);
     }
   }
 }
@@ -385,10 +310,7 @@ int launch_encode_bwd(const FieldLaunch& f, const std::vector<EncPass>& passes, 
     for (uint32_t j = 0; j < h.n_pass; ++j) h.pass[j] = passes[i + j];
     const dim3 grid(pass_blocks(h, h.pass, h.n_pass), h.n_pass);
     const bool all = h.pass[0].f == kAllFields;
-    if (f.s_p && f.box_bwd) {
-      if (all) k_encode_bwd_ord<true><<<grid, 256, 0, s>>>(h, dX);
-      else k_encode_bwd_ord<false><<<grid, 256, 0, s>>>(h, dX);
-    } else if (f.s_p) {
+    if (f.s_p) {
       if (all) k_encode_bwd<true, true><<<grid, 256, 0, s>>>(h, dX);
       else k_encode_bwd<true, false><<<grid, 256, 0, s>>>(h, dX);
     } else {

@@ -146,7 +146,6 @@ struct dg_ctx {
   uint32_t order_bits = 8;                 // Morton cells per axis = 2^order_bits (DG_ORDER_BITS)
   uint32_t order_chunk = 8;                // samples per sorted chunk (DG_ORDER_CHUNK)
   uint32_t bwd_cta_mul = 7919;             // encode backward CTA visiting stride (DG_ENC_BWD_STRIDE)
-  bool enc_box = false;                    // shared-cell warp sums in the ordered backward (DG_ENC_BWD_BOX=1)
   bool ordered = false;                    // the last front half ordered its samples
   DBuf s_perm, s_inv, s_p_alt, s_item_ord, s_grad_ord, ord_scratch, ord_tmp;
   double enc_agg_samples_per_cell = 1.5;   // warp-aggregate levels with >= this many samples/cell (DG_ENC_AGG)
@@ -1358,7 +1357,6 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   if (const char* e = std::getenv("DG_ORDER_CHUNK")) c->order_chunk = std::min(64u, std::max(1u, uint32_t(std::atoi(e))));
   if (const char* e = std::getenv("DG_ORDER_BITS")) c->order_bits = std::min(10u, std::max(1u, uint32_t(std::atoi(e))));
   if (const char* e = std::getenv("DG_ENC_BWD_STRIDE")) c->bwd_cta_mul = uint32_t(std::strtoul(e, nullptr, 10));
-  if (const char* e = std::getenv("DG_ENC_BWD_BOX")) c->enc_box = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("DG_ENC_AGG")) c->enc_agg_samples_per_cell = std::max(0.01, std::atof(e));
   if (const char* e = std::getenv("DG_ENC_BWD_MB"))
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
@@ -1832,7 +1830,6 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
       if (m == 0) m = 1;
       while (nb > 1 && std::gcd(m, nb) != 1) ++m;
       fl.cta_mul = uint32_t(m);
-      fl.box_bwd = c->enc_box ? 1u : 0u;
     }
     c->launches += launch_encode_bwd(fl, passes, sm.dX, s) - 1;
   }

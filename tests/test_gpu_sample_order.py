@@ -1,6 +1,6 @@
 """The spatial sample order (kernels_order.cu: Morton-sorted samples for the encode passes and
-the MLP tiles; chunked or per-sample; the optional shared-cell warp sums of the encoding
-backward) is a schedule, not a change of arithmetic: every mode must give the march-order
+the MLP tiles; chunked or per-sample; the encoding backward's warp-aggregated scatter on any
+number of levels) is a schedule, not a change of arithmetic: every mode must give the march-order
 step's losses, gradients and render.
 
 Only the fp32 summation order of the gradient scatter (atomics, warp sums) differs,
@@ -21,10 +21,10 @@ MODES = {
     "ordered": {},
     "ordered_samples": {"DG_ORDER_CHUNK": "1"},
     "ordered_chunk5": {"DG_ORDER_CHUNK": "5", "DG_ORDER_BITS": "3"},
-    "ordered_shared_cell": {"DG_ENC_BWD_BOX": "1"},
+    "ordered_agg_all": {"DG_ENC_AGG": "0.01"},
     "ordered_sliced": {"DG_ENC_BWD_MB": "1", "DG_ENC_FWD_MB": "1"},
 }
-ENV = ("DG_SAMPLE_ORDER", "DG_ENC_BWD_BOX", "DG_ORDER_BITS", "DG_ORDER_CHUNK", "DG_ENC_BWD_MB", "DG_ENC_FWD_MB")
+ENV = ("DG_SAMPLE_ORDER", "DG_ENC_AGG", "DG_ORDER_BITS", "DG_ORDER_CHUNK", "DG_ENC_BWD_MB", "DG_ENC_FWD_MB")
 
 
 def _run(cfg, mode, monkeypatch, batch, state_seed=0, occupancy_fraction=None):
