@@ -142,7 +142,8 @@ struct dg_ctx {
   uint64_t enc_budget_bwd = 96ull << 20;
   uint64_t enc_group_fwd = 0, enc_group_bwd = 0;  // level-grouping budgets (0: = slice budget)
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
-  bool sample_order = true;                // spatial sample order (DG_SAMPLE_ORDER=0 disables)
+  int sample_order = 1;                    // spatial sample order: 1 when a level table > 64 MB,
+                                           // 0 never, 2 always (DG_SAMPLE_ORDER)
   uint32_t order_bits = 8;                 // Morton cells per axis = 2^order_bits (DG_ORDER_BITS)
   uint32_t order_chunk = 8;                // samples per sorted chunk (DG_ORDER_CHUNK)
   uint32_t bwd_cta_mul = 7919;             // encode backward CTA visiting stride (DG_ENC_BWD_STRIDE)
@@ -635,6 +636,15 @@ __global__ void k_block_permute(const uint64_t* __restrict__ src, uint64_t* __re
 int order_samples(dg_ctx* c, uint64_t NS, cudaStream_t s) {
   c->ordered = false;
   if (!c->sample_order || !c->enc_pcache || !NS) return DG_OK;
+  // Only when a level table outgrows what random accesses keep L2-resident (~75 MB on this
+  // B200, tools/ubench/l2_curve.cu): with small tables (C1: 4 MB per level) every gather hits
+  // L2 in march order already and the sort would be pure overhead.  DG_SAMPLE_ORDER=2 forces it.
+  if (c->sample_order == 1) {
+    uint64_t big = 0;
+    for (const FieldDesc& fd : c->fields)
+      for (uint32_t l = 0; l < fd.L; ++l) big = std::max<uint64_t>(big, uint64_t(fd.lv[l].rows) * 8);
+    if (big < (64ull << 20)) return DG_OK;
+  }
   const uint32_t C = c->order_chunk;
   TRY(c->s_perm.ensure(NS * 4 + 16));
   TRY(c->s_inv.ensure(NS * 4 + 16));
@@ -1353,7 +1363,7 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   if (const char* e = std::getenv("DG_ENC_FWD_MB"))
     c->enc_budget_fwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   if (const char* e = std::getenv("DG_ENC_PCACHE")) c->enc_pcache = std::strcmp(e, "0") != 0;
-  if (const char* e = std::getenv("DG_SAMPLE_ORDER")) c->sample_order = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("DG_SAMPLE_ORDER")) c->sample_order = std::atoi(e);
   if (const char* e = std::getenv("DG_ORDER_CHUNK")) c->order_chunk = std::min(64u, std::max(1u, uint32_t(std::atoi(e))));
   if (const char* e = std::getenv("DG_ORDER_BITS")) c->order_bits = std::min(10u, std::max(1u, uint32_t(std::atoi(e))));
   if (const char* e = std::getenv("DG_ENC_BWD_STRIDE")) c->bwd_cta_mul = uint32_t(std::strtoul(e, nullptr, 10));

@@ -18,11 +18,11 @@ pytestmark = pytest.mark.gpu
 
 MODES = {
     "march": {"DG_SAMPLE_ORDER": "0"},
-    "ordered": {},
-    "ordered_samples": {"DG_ORDER_CHUNK": "1"},
-    "ordered_chunk5": {"DG_ORDER_CHUNK": "5", "DG_ORDER_BITS": "3"},
-    "ordered_agg_all": {"DG_ENC_AGG": "0.01"},
-    "ordered_sliced": {"DG_ENC_BWD_MB": "1", "DG_ENC_FWD_MB": "1"},
+    "ordered": {"DG_SAMPLE_ORDER": "2"},
+    "ordered_samples": {"DG_SAMPLE_ORDER": "2", "DG_ORDER_CHUNK": "1"},
+    "ordered_chunk5": {"DG_SAMPLE_ORDER": "2", "DG_ORDER_CHUNK": "5", "DG_ORDER_BITS": "3"},
+    "ordered_agg_all": {"DG_SAMPLE_ORDER": "2", "DG_ENC_AGG": "0.01"},
+    "ordered_sliced": {"DG_SAMPLE_ORDER": "2", "DG_ENC_BWD_MB": "1", "DG_ENC_FWD_MB": "1"},
 }
 ENV = ("DG_SAMPLE_ORDER", "DG_ENC_AGG", "DG_ORDER_BITS", "DG_ORDER_CHUNK", "DG_ENC_BWD_MB", "DG_ENC_FWD_MB")
 
