@@ -192,6 +192,8 @@ struct MlpLaunch {
   const float* params;
   float* grads;
   float4* out;                 // fwd: sigma, rgb
+  float4* out_tile;            // train: the forward's (sigma, rgb) by tile row as well (written by
+                               // the forward when perm is set, else = out), read by the backward
   const float4* grad_in;       // bwd: dsigma, drgb
   float* dX;                   // bwd, level-major like X
   uint32_t* masks;             // tc path: [7][x_stride] ReLU / clip masks, written by the forward,

@@ -679,9 +679,12 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
           z[k] = v[k] + sm.w.bc2[k];
           clip_bits |= (z[k] > 15.f || z[k] < -15.f ? 1u : 0u) << (16 + k);
         }
-        if (valid)
-          __stcs(m.out + (m.perm ? __ldg(m.perm + gs) : gs), make_float4(expf(sm.sig_raw[row]), sigm(clip15(z[0])), sigm(clip15(z[1])),
-                                         sigm(clip15(z[2]))));
+        if (valid) {
+          const float4 o = make_float4(expf(sm.sig_raw[row]), sigm(clip15(z[0])), sigm(clip15(z[1])),
+                                       sigm(clip15(z[2])));
+          __stcs(m.out + (m.perm ? __ldg(m.perm + gs) : gs), o);
+          if (m.perm && m.out_tile) __stcs(m.out_tile + gs, o);
+        }
         if (store_mask) __stcs(masks + 6ull * m.x_stride + gs, clip_bits);
       }
       if (!has_next) break;
@@ -702,7 +705,9 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
 }
 
 // ============================================================================ backward
-// Per tile of 128 samples: recompute the forward (keeping every layer input in smem), then
+// Per tile of 128 samples: recompute the forward's hidden layers (keeping every layer input in
+// smem; the output layer is not recomputed: the colour-head adjoint and the sigma path take
+// the forward's stored sigma / rgb, MlpLaunch::out_tile, with its clip flags), then
 //   B1  G5  = d raw_rgb (clip/sigmoid adjoint)            dWc2 += G5^T C2 ; dC2 = G5 Wc2
 //   B2  G4  = dC2 * act'(C2)                              dWc1 += G4^T C1 ; dC1 = G4 Wc1
 //   B3  G3  = dC1 * act'(C1)                              dWc0 += G3^T Cin; dCin = G3 Wc0[:, :16]
@@ -976,10 +981,14 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       // loads are issued here rather than held in prefetch registers through the previous tile
       // (this part's 16 columns: h1 bits 0-15 | c1 bits 16-31, the c2 word; part 0: clip word)
       uint32_t mk_relu = 0u, mk_c2 = 0u, mk_clip = 0u;
+      float4 o_fwd = make_float4(0.f, 0.f, 0.f, 0.f);  // the forward's (sigma, rgb), part 0
       if (valid) {
         mk_relu = __ldcs(m.masks + (uint64_t)part * m.x_stride + gs);
         mk_c2 = __ldcs(m.masks + (uint64_t)(4 + (part >> 1)) * m.x_stride + gs);
-        if (part == 0) mk_clip = __ldcs(m.masks + 6ull * m.x_stride + gs);
+        if (part == 0) {
+          mk_clip = __ldcs(m.masks + 6ull * m.x_stride + gs);
+          o_fwd = __ldcs(m.out_tile + gs);
+        }
       }
       sync_mma();
       // ---------------- forward recompute (A operands from TMEM) ----------------
@@ -1041,34 +1050,31 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
           const float z = v[i] + sm.w.bc1[c16 + i];
           v[i] = act_c == 2 ? sigm(z) : fmaxf(z, 0.f);
         }
-        put8(sc2, row, c16, v);
-        put8(sc2, row, c16 + 8, v + 8);
+        // C2 feeds only dWc2 here (its smem tile): the output layer is not recomputed
+        put8s(sm.c2[0], sm.c2[1], row, c16, v);
+        put8s(sm.c2[0], sm.c2[1], row, c16 + 8, v + 8);
       }
-      sync_mma();
-      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
-      mma_done();
       mk_c2 = (mk_c2 >> (((uint32_t)part & 1u) * 16u)) & 0xffffu;
       // ---------------- B1: colour head adjoint (field.cpp:298-306) ----------------
+      // from the forward's outputs (sigma = exp(clip(raw0)), rgb = sigmoid(clip(z))) and its
+      // clip flags, so the output-layer GEMM is not recomputed
       if (part == 0) {
         sm.dmask[row] = mk_clip & 0xffffu;  // the forward's clip flags
-        float v[16];
-        ld16(my_lanes, v);
         const float ug[3] = {up.y, up.z, up.w};
+        const float sgs[3] = {o_fwd.y, o_fwd.z, o_fwd.w};
         float g[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) g[k] = 0.f;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          const float z = v[k] + sm.w.bc2[k];
           const bool clipped = (mk_clip >> (16 + k)) & 1u;
-          const float sg = sigm(clip15(z));
-          g[k] = clipped ? 0.f : ug[k] * sg * (1.f - sg);
+          g[k] = clipped ? 0.f : ug[k] * sgs[k] * (1.f - sgs[k]);
         }
         // columns 8-15 of G5 are always 0: zeroed once in shared memory; in the TMEM A region
         // they keep the previous operand's finite values, which meet zero-padded Wc2 rows
         put8(sg5, row, 0, g);
-        // sigma path of the density raw gradient (field.cpp:313)
-        sm.gsig[row] = (sm.dmask[row] & 1u) ? 0.f : up.x * expf(sm.sig_raw[row]);
+        // sigma path of the density raw gradient (field.cpp:313): up.sigma * exp(raw0)
+        sm.gsig[row] = (sm.dmask[row] & 1u) ? 0.f : up.x * o_fwd.x;
       }
       pf.grad(m, part);  // next tile's upstream gradient
       sync_mma();
@@ -1208,8 +1214,10 @@ void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
   k_mlp_fwd_tc<<<grid, NTF, smem, s>>>(m);
 }
 
-void launch_mlp_bwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
-  if (!m.n_tiles) return;
+void launch_mlp_bwd_tc(const MlpLaunch& m0, int num_sms, cudaStream_t s) {
+  if (!m0.n_tiles) return;
+  MlpLaunch m = m0;
+  if (!m.out_tile) m.out_tile = m.out;  // the forward's outputs by tile row
   static bool attr = false;
   const int smem = (int)sizeof(BwdTcSmem);  // no-swizzle operands need 16-byte alignment only
   if (!attr) {

@@ -148,7 +148,7 @@ struct dg_ctx {
   uint32_t order_chunk = 8;                // samples per sorted chunk (DG_ORDER_CHUNK)
   uint32_t bwd_cta_mul = 7919;             // encode backward CTA visiting stride (DG_ENC_BWD_STRIDE)
   bool ordered = false;                    // the last front half ordered its samples
-  DBuf s_perm, s_inv, s_p_alt, s_item_ord, s_grad_ord, ord_scratch, ord_tmp;
+  DBuf s_perm, s_inv, s_p_alt, s_item_ord, s_grad_ord, s_out_ord, ord_scratch, ord_tmp;
   double enc_agg_samples_per_cell = 1.5;   // warp-aggregate levels with >= this many samples/cell (DG_ENC_AGG)
   uint64_t n_params = 0;
   uint64_t occ_bytes = 0;                 // bricked bitfields (all local partitions, both cascades)
@@ -1795,8 +1795,13 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
     c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
   }
   mark(c, 3);
-  const MlpLaunch mf = mlp_launch(c, false);
-  if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);
+  MlpLaunch mf = mlp_launch(c, false);
+  if (c->mlp_impl) {
+    // the backward reads the forward's outputs by tile row (colour-head adjoint, sigma path)
+    if (c->ordered) TRY(c->s_out_ord.ensure((uint64_t(c->n_fine) + c->n_coarse) * 16 + 16));
+    mf.out_tile = c->ordered ? c->s_out_ord.as<float4>() : mf.out;
+    launch_mlp_fwd_tc(mf, c->num_sms, s);
+  }
   else launch_mlp_fwd(mf, s);
   mark(c, 4);
   launch_composite(NI, it, sm, c->n_fine, 0, s);
@@ -1823,7 +1828,9 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   mark(c, 7);
   // K4b / K3b backward
   if (c->mlp_impl) {
-    launch_mlp_bwd_tc(mlp_launch(c, false), c->num_sms, s);  // 128-sample tiles
+    MlpLaunch mb = mlp_launch(c, false);  // 128-sample tiles
+    mb.out_tile = c->ordered ? c->s_out_ord.as<float4>() : mb.out;
+    launch_mlp_bwd_tc(mb, c->num_sms, s);
   } else {
     launch_mlp_bwd(mlp_launch(c, true), c->num_sms, s);
   }
@@ -2293,6 +2300,7 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
   m.grads = c->grads.as<float>();
   TRY(out.ensure(n * 16 + 16));
   m.out = out.as<float4>();
+  m.out_tile = m.out;  // no sample permutation here: tile rows are the caller's points
   DBuf masks;
   if (!sig_grad) {
     TRY(upload(toff, tf.data(), tf.size() * 4, s));
