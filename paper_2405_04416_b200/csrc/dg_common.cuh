@@ -60,7 +60,10 @@ struct LevelDesc {
   uint32_t mask;     // rows - 1 when hashed
   uint32_t rows;     // table rows (2^T when hashed, n0 n1 n2 when one-to-one)
   uint64_t offset;   // floats from the field base to this level's table (rows x 2)
+  uint64_t poff;     // paired copy (one-to-one levels): float4 index of row 0 in the context's
+                     // pair buffers (pairs[r] = rows r, r + 1 of the table; kNoPair: none)
 };
+constexpr uint64_t kNoPair = ~0ull;
 
 struct FieldDesc {   // one (partition, cascade) sub-field: FieldParams + its box
   double box_lo[3], box_hi[3];

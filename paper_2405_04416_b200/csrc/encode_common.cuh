@@ -183,6 +183,49 @@ __device__ __forceinline__ float2 gather_level_w32(const LevelDesc& lv, const La
   return acc;
 }
 
+// One-to-one levels through their paired copy (kernels_pairs.cu: pairs[r] = rows r, r + 1):
+// corner pair (x0, x0 + 1) of (y, z) combo j is pairs[x0 + base_j], always one aligned 16-byte
+// access.  r0[j] = that pair row (kNoRow when outside the pass's slice [lo, hi)); w[k] = the
+// corner weights (0 for a zero-weight corner, as the reference skips it; a clamped x1 == x0
+// has weight 0).
+constexpr uint32_t kNoRow = 0xffffffffu;
+template <bool SLICED>
+__device__ __forceinline__ void paired_corners(const LevelDesc& lv, const LatticeAxes& la, uint32_t lo, uint32_t hi,
+                                               uint32_t r0[4], float w[8]) {
+  bool zero[8];
+  corner_weights_w32(la, w, zero);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w[k] = zero[k] ? 0.f : w[k];
+  const uint32_t nx = lv.n[0], nxy = lv.n[0] * lv.n[1];
+  const uint32_t y0 = nx * la.a[1].i0, y1 = nx * la.a[1].i1, z0 = nxy * la.a[2].i0, z1 = nxy * la.a[2].i1;
+  const uint32_t base[4] = {y0 + z0, y1 + z0, y0 + z1, y1 + z1};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t r = la.a[0].i0 + base[j];
+    r0[j] = (!SLICED || (r >= lo && r < hi)) ? r : kNoRow;
+  }
+}
+
+template <bool SLICED>
+__device__ __forceinline__ float2 gather_level_paired(const LevelDesc& lv, const LatticeAxes& la,
+                                                      const float4* __restrict__ pairs, uint32_t lo, uint32_t hi) {
+  uint32_t r0[4];
+  float w[8];
+  paired_corners<SLICED>(lv, la, lo, hi, r0, w);
+  float4 q[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) q[j] = r0[j] != kNoRow ? __ldg(pairs + r0[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    acc.x = fmaf(w[2 * j], q[j].x, acc.x);
+    acc.y = fmaf(w[2 * j], q[j].y, acc.y);
+    acc.x = fmaf(w[2 * j + 1], q[j].z, acc.x);
+    acc.y = fmaf(w[2 * j + 1], q[j].w, acc.y);
+  }
+  return acc;
+}
+
 // Row pairing: the two x-neighbour corners (cx = 0, 1) of each (cy, cz) land in rows
 // i ^ h and (i + 1) ^ h (hashed) or r and r + 1 (one-to-one); when those differ only in bit 0
 // (half the time) they are one 16-byte aligned float4 (every level table is 16-byte aligned),

@@ -128,13 +128,25 @@ void launch_items_to_records(uint32_t n, const float4* partial, const float* dep
 // pass's L2 budget); the pass covers only field f's samples.
 struct EncPass {
   uint8_t l0, l1, k, S;
-  uint8_t f, pad0, pad1, pad2;
+  uint8_t f, paired, pad1, pad2;  // paired: a level of the pass has a paired copy (kernels_pairs.cu)
   // S > 1 (a single level l0): table rows [lo, hi) of slice k, per field (f == kAllFields:
   // fields 0 and 1 of the single local partition; otherwise slot 0 is field f)
   uint32_t lo[2], hi[2];
 };
 constexpr int kMaxEncPass = 256;  // per launch; longer pass lists are launched in chunks
 constexpr uint8_t kAllFields = 0xff;  // EncPass.f: every local field's samples in one pass
+
+// Paired copy of one one-to-one level table (kernels_pairs.cu): pairs[pair0 + i] = rows i and
+// i + 1 of the table at params[table], as one float4 (row `rows` reads as 0).
+struct PairSeg {
+  uint64_t pair0;   // float4 index in the pair buffers
+  uint64_t table;   // float offset of the table in the parameter / gradient buffers
+  uint64_t rows;
+};
+void launch_pairs_expand(const PairSeg* segs, uint32_t nseg, uint64_t total, const float* params, float4* pairs,
+                         cudaStream_t s);
+void launch_pairs_fold(const PairSeg* segs, uint32_t nseg, uint64_t total, float4* pgrads, float* grads,
+                       cudaStream_t s);
 
 struct FieldLaunch {
   const FieldDesc* fields;     // [2][n_local] (cascade-major)
@@ -150,6 +162,8 @@ struct FieldLaunch {
   uint32_t levels;
   uint32_t agg_levels;     // levels whose backward scatter is warp-aggregated
   uint32_t cta_mul;        // backward: CTA x visits sample chunk (x * cta_mul) % gridDim.x (0: x)
+  const float4* pairs;     // paired one-to-one level tables (LevelDesc::poff), forward
+  float4* pgrads;          // their gradients, backward (folded into grads by launch_pairs_fold)
   const float* params;
   float* grads;
   uint32_t n_pass;         // passes of this launch (grid.y)

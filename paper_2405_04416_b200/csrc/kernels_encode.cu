@@ -87,7 +87,11 @@ __device__ __forceinline__ void st_stream(float2* p, float2 v) {
 // so one segmented shuffle scan per corner value (its depth ceil(log2(longest run)), found
 // once per level) leaves each run's sums in its last lane, which issues the run's reds
 // (corner pairs merged).  Inactive lanes (zero upstream) form runs of their own and issue none.
-__device__ __forceinline__ void scatter_level_agg(float2* __restrict__ table, const Corners& c, const AxisW* ax,
+// PAIRED: a paired one-to-one level (kernels_pairs.cu): c.row[2j] is combo j's pair row (kNoRow
+// outside the slice), and the run tail issues one float4 red per combo into the paired
+// gradient copy.
+template <bool PAIRED = false>
+__device__ __forceinline__ void scatter_level_agg(void* __restrict__ dst, const Corners& c, const AxisW* ax,
                                                   float2 up, uint32_t field, bool act) {
   const unsigned lane = threadIdx.x & 31;
   const uint32_t key = act ? (ax[0].i0 | (ax[1].i0 << 11) | (ax[2].i0 << 22)) ^ (field << 31) : 0xffffffffu;
@@ -115,6 +119,17 @@ __device__ __forceinline__ void scatter_level_agg(float2* __restrict__ table, co
   }
   const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
   if (!(tail && act)) return;
+  if (PAIRED) {
+    float4* pg = static_cast<float4*>(dst);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 g0 = g[2 * j], g1 = g[2 * j + 1];
+      if (c.row[2 * j] != kNoRow && (g0.x != 0.f || g0.y != 0.f || g1.x != 0.f || g1.y != 0.f))
+        atomicAdd(pg + c.row[2 * j], make_float4(g0.x, g0.y, g1.x, g1.y));
+    }
+    return;
+  }
+  float2* table = static_cast<float2*>(dst);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t r0 = c.row[2 * j], r1 = c.row[2 * j + 1];
@@ -182,9 +197,15 @@ __global__ void ENC_FWD_BOUNDS k_encode_fwd(FieldLaunch f, float* __restrict__ X
   for (uint32_t l = ps.l0; l < ps.l1; ++l) {
     const LevelDesc lv = fd.lv[l];
     const LatticeAxes la = lattice_axes(lv, p);
-    const float2* table = reinterpret_cast<const float2*>(f.params + fd.base + lv.offset);
-    float2 acc = ps.S > 1 ? gather_level_w32<true>(lv, la, table, slo, shi)
-                          : gather_level_w32<false>(lv, la, table, 0u, 0u);
+    float2 acc;
+    if (lv.poff != kNoPair && f.pairs) {  // one-to-one level through its paired copy (uniform)
+      acc = ps.S > 1 ? gather_level_paired<true>(lv, la, f.pairs + lv.poff, slo, shi)
+                     : gather_level_paired<false>(lv, la, f.pairs + lv.poff, 0u, 0u);
+    } else {
+      const float2* table = reinterpret_cast<const float2*>(f.params + fd.base + lv.offset);
+      acc = ps.S > 1 ? gather_level_w32<true>(lv, la, table, slo, shi)
+                     : gather_level_w32<false>(lv, la, table, 0u, 0u);
+    }
     float2* xp = reinterpret_cast<float2*>(X) + (uint64_t)l * f.n_total + s;
     if (ps.k > 0) {
       const float2 o = ld_stream(xp);
@@ -198,7 +219,9 @@ __global__ void ENC_FWD_BOUNDS k_encode_fwd(FieldLaunch f, float* __restrict__ X
 #ifndef ENC_BWD_MINB
 #define ENC_BWD_MINB 4  // 4 CTAs per SM (64 registers; the per-cell run scan holds 16 sums)
 #endif
-template <bool PC, bool ALL>
+// PAIRED: the launch's passes contain paired one-to-one levels (kernels_pairs.cu); the hashed
+// level passes run the variant without that code path (register allocation).
+template <bool PC, bool ALL, bool PAIRED>
 __global__ void __launch_bounds__(256, ENC_BWD_MINB) k_encode_bwd(FieldLaunch f, const float* __restrict__ dX) {
   const EncPass ps = f.pass[blockIdx.y];
   const uint32_t bx = f.cta_mul ? (uint32_t)(((uint64_t)blockIdx.x * f.cta_mul) % gridDim.x) : blockIdx.x;
@@ -208,17 +231,41 @@ __global__ void __launch_bounds__(256, ENC_BWD_MINB) k_encode_bwd(FieldLaunch f,
   double p[3] = {0.0, 0.0, 0.0};
   const FieldDesc& fd = f.fields[fidx];
   if (valid) load_point<PC>(f, s, fd, p);
+  const uint32_t slot = (ALL && fidx) ? 1u : 0u;
   for (uint32_t l = ps.l0; l < ps.l1; ++l) {
     float2 up = make_float2(0.f, 0.f);
     Corners c;
     LatticeAxes la;
+    const bool paired = PAIRED && fd.lv[l].poff != kNoPair;  // uniform per (field, level)
     if (valid) {
       up = ld_stream(reinterpret_cast<const float2*>(dX) + (uint64_t)l * f.n_total + s);
       la = lattice_axes(fd.lv[l], p);
-      corners_w32(fd.lv[l], la, c);
-      clip_to_slice(ps, ALL ? fidx : 0u, c);
+      if (paired) {
+        uint32_t r0[4];
+        if (ps.S > 1) paired_corners<true>(fd.lv[l], la, slot ? ps.lo[1] : ps.lo[0], slot ? ps.hi[1] : ps.hi[0], r0, c.w);
+        else paired_corners<false>(fd.lv[l], la, 0u, 0u, r0, c.w);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c.row[2 * j] = r0[j];
+      } else {
+        corners_w32(fd.lv[l], la, c);
+        clip_to_slice(ps, slot, c);
+      }
     }
     const bool act = valid && (up.x != 0.f || up.y != 0.f);
+    if (paired) {
+      float4* pg = f.pgrads + fd.lv[l].poff;
+      if (l < f.agg_levels) {
+        scatter_level_agg<true>(pg, c, la.a, up, fidx, act);
+      } else if (act) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float w0 = c.w[2 * j], w1 = c.w[2 * j + 1];
+          if (c.row[2 * j] != kNoRow && (w0 != 0.f || w1 != 0.f))
+            atomicAdd(pg + c.row[2 * j], make_float4(w0 * up.x, w0 * up.y, w1 * up.x, w1 * up.y));
+        }
+      }
+      continue;
+    }
     float2* table = reinterpret_cast<float2*>(f.grads + fd.base + fd.lv[l].offset);
     if (l < f.agg_levels) {  // coarse levels: neighbouring lanes share cells (warp-uniform branch)
       scatter_level_agg(table, c, la.a, up, fidx, act);
@@ -307,20 +354,28 @@ int launch_encode_bwd(const FieldLaunch& f, const std::vector<EncPass>& passes, 
   static const bool split = std::getenv("DG_ENC_SPLIT_LAUNCH") != nullptr;  // per-pass timing
   const uint32_t chunk = split ? 1u : (uint32_t)kMaxEncPass;
   int launches = 0;
-  for (uint32_t i = 0; i < passes.size(); i += chunk) {  // reds commute: any grouping
-    FieldLaunch h = f;
-    h.n_pass = std::min<uint32_t>(chunk, (uint32_t)passes.size() - i);
-    for (uint32_t j = 0; j < h.n_pass; ++j) h.pass[j] = passes[i + j];
-    const dim3 grid(pass_blocks(h, h.pass, h.n_pass), h.n_pass);
-    const bool all = h.pass[0].f == kAllFields;
-    if (f.s_p) {
-      if (all) k_encode_bwd<true, true><<<grid, 256, 0, s>>>(h, dX);
-      else k_encode_bwd<true, false><<<grid, 256, 0, s>>>(h, dX);
-    } else {
-      if (all) k_encode_bwd<false, true><<<grid, 256, 0, s>>>(h, dX);
-      else k_encode_bwd<false, false><<<grid, 256, 0, s>>>(h, dX);
+  for (int paired = 1; paired >= 0; --paired) {  // passes with paired levels first (reds commute)
+    std::vector<EncPass> pk;
+    for (const EncPass& p : passes)
+      if ((f.pgrads != nullptr && p.paired != 0) == (paired != 0)) pk.push_back(p);
+    for (uint32_t i = 0; i < pk.size(); i += chunk) {
+      FieldLaunch h = f;
+      h.n_pass = std::min<uint32_t>(chunk, (uint32_t)pk.size() - i);
+      for (uint32_t j = 0; j < h.n_pass; ++j) h.pass[j] = pk[i + j];
+      const dim3 grid(pass_blocks(h, h.pass, h.n_pass), h.n_pass);
+      const bool all = h.pass[0].f == kAllFields;
+      if (f.s_p && paired) {
+        if (all) k_encode_bwd<true, true, true><<<grid, 256, 0, s>>>(h, dX);
+        else k_encode_bwd<true, false, true><<<grid, 256, 0, s>>>(h, dX);
+      } else if (f.s_p) {
+        if (all) k_encode_bwd<true, true, false><<<grid, 256, 0, s>>>(h, dX);
+        else k_encode_bwd<true, false, false><<<grid, 256, 0, s>>>(h, dX);
+      } else {
+        if (all) k_encode_bwd<false, true, false><<<grid, 256, 0, s>>>(h, dX);
+        else k_encode_bwd<false, false, false><<<grid, 256, 0, s>>>(h, dX);
+      }
+      ++launches;
     }
-    ++launches;
   }
   return launches;
 }

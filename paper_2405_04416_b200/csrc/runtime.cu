@@ -137,6 +137,11 @@ struct dg_ctx {
     uint64_t dev, flat, count;  // relative to the field's device base / flat start
   };
   std::vector<std::vector<Seg>> field_segs;  // [2][n_local]
+  // paired copies of the one-to-one level tables (kernels_pairs.cu)
+  bool enc_paired = true;          // DG_ENC_PAIRED=0 disables
+  uint64_t pair_rows = 0;
+  std::vector<PairSeg> pair_segs;  // one per (field, one-to-one level)
+  DBuf pairs, pgrads, pair_segs_d;
   std::vector<std::vector<dg_array_desc>> layouts;
   uint64_t enc_budget_fwd = 192ull << 20;  // encode pass budgets (DG_ENC_FWD_MB / DG_ENC_BWD_MB)
   uint64_t enc_budget_bwd = 96ull << 20;
@@ -292,6 +297,9 @@ int ctx_setup(dg_ctx* c) {
   c->field_dev_off.assign(2 * nl, 0);
   c->field_size.assign(2 * nl, 0);
   c->field_segs.assign(2 * nl, {});
+  if (const char* e = std::getenv("DG_ENC_PAIRED")) c->enc_paired = std::strcmp(e, "0") != 0;
+  c->pair_rows = 0;
+  c->pair_segs.clear();
   uint64_t poff = 0, ooff = 0, doff = 0;
   for (uint32_t lp = 0; lp < nl; ++lp) {
     const uint32_t gid = c->local[lp];
@@ -362,6 +370,14 @@ int ctx_setup(dg_ctx* c) {
         lv.rows = uint32_t(rows);
         o = (o + 3) & ~uint64_t(3);  // 16-byte aligned table: row pairs (2m, 2m+1) are float4s
         lv.offset = o;
+        lv.poff = kNoPair;
+        // one-to-one level: x-neighbour pairs as one float4, when the paired copy (16 B per row)
+        // still fits L2 next to the rest of its pass (the backward's float4 reds RMW it)
+        if (!lv.hashed && c->enc_paired && rows * 16 <= (64ull << 20)) {
+          lv.poff = c->pair_rows;
+          c->pair_segs.push_back({c->pair_rows, poff + o, rows});
+          c->pair_rows += rows;
+        }
         c->layouts[lp].push_back({flat + of, rows * 2, uint32_t(casc), 0u, l, 0u});
         seg(rows * 2);
         o += rows * 2;
@@ -479,6 +495,12 @@ int ctx_alloc(dg_ctx* c) {
   for (DBuf* b : {&c->params, &c->grads, &c->adam_m, &c->adam_v}) {
     TRY(b->ensure(pb));
     CU(cudaMemsetAsync(b->p, 0, pb, s));
+  }
+  if (c->pair_rows) {
+    TRY(c->pairs.ensure(c->pair_rows * 16 + 16));
+    TRY(c->pgrads.ensure(c->pair_rows * 16 + 16));
+    CU(cudaMemsetAsync(c->pgrads.p, 0, c->pair_rows * 16, s));
+    TRY(upload(c->pair_segs_d, c->pair_segs.data(), c->pair_segs.size() * sizeof(PairSeg), s));
   }
   TRY(c->occ.ensure(c->occ_bytes));
   CU(cudaMemsetAsync(c->occ.p, 1, c->occ_bytes, s));  // fill_occupied (worker.cpp:199-200)
@@ -919,6 +941,16 @@ int front_half(dg_ctx* c, const dg_ray_batch* b, int train, uint64_t batch_id, u
   return DG_OK;
 }
 
+// The paired copies of the one-to-one level tables (kernels_pairs.cu), from the current
+// parameters (after the last Adam step or dg_set_params).
+int pairs_expand(dg_ctx* c, cudaStream_t s) {
+  if (!c->pair_rows) return DG_OK;
+  launch_pairs_expand(c->pair_segs_d.as<PairSeg>(), uint32_t(c->pair_segs.size()), c->pair_rows,
+                      c->params.as<float>(), c->pairs.as<float4>(), s);
+  ++c->launches;
+  return DG_OK;
+}
+
 FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passes, uint64_t group) {
   if (!group) group = budget;
   FieldLaunch f{};
@@ -960,6 +992,9 @@ FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passe
       for (uint32_t k = 0; k < S; ++k) {
         EncPass ps{uint8_t(l), uint8_t(l1), uint8_t(k), uint8_t(S), merged ? kAllFields : uint8_t(fi), 0, 0, 0,
                    {0u, 0u}, {0xffffffffu, 0xffffffffu}};
+        for (uint32_t ll = l; ll < l1; ++ll)  // the pass holds paired one-to-one levels
+          for (uint32_t fj = 0; fj < nf; ++fj)
+            if ((merged || fj == fi) && c->fields[fj].lv[ll].poff != kNoPair) ps.paired = 1;
         for (uint32_t slot = 0; slot < 2 && S > 1; ++slot) {  // slice bounds, even rows
           const uint32_t fld = merged ? slot : fi;
           if (fld >= c->fields.size()) break;
@@ -984,6 +1019,8 @@ FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passe
   f.agg_levels = agg;
   f.params = c->params.as<float>();
   f.grads = c->grads.as<float>();
+  f.pairs = c->pair_rows ? c->pairs.as<float4>() : nullptr;
+  f.pgrads = c->pair_rows ? c->pgrads.as<float4>() : nullptr;
   f.s_p = c->enc_pcache ? c->s_p.as<double>() : nullptr;
   f.n_fields = uint32_t(c->field_off.size() - 1);
   for (size_t i = 0; i < c->field_off.size(); ++i) f.field_off[i] = c->field_off[i];
@@ -1790,6 +1827,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   CU(cudaMemsetAsync(c->loss.p, 0, sizeof(LossAccum), s));
   // K3 / K4 forward
   {
+    TRY(pairs_expand(c, s));
     std::vector<EncPass> passes;
     const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd);
     c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
@@ -1849,6 +1887,11 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
       fl.cta_mul = uint32_t(m);
     }
     c->launches += launch_encode_bwd(fl, passes, sm.dX, s) - 1;
+    if (c->pair_rows) {  // the paired one-to-one levels' gradients into the tables
+      launch_pairs_fold(c->pair_segs_d.as<PairSeg>(), uint32_t(c->pair_segs.size()), c->pair_rows,
+                        c->pgrads.as<float4>(), c->grads.as<float>(), s);
+      ++c->launches;
+    }
   }
   mark(c, 9);
   c->launches += 3;
@@ -1933,6 +1976,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   ItemArrays it = item_arrays(c);
   SampleArrays sm = sample_arrays(c);
   {
+    TRY(pairs_expand(c, s));
     std::vector<EncPass> passes;
     const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd);
     c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;

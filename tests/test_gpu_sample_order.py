@@ -1,11 +1,12 @@
 """The spatial sample order (kernels_order.cu: Morton-sorted samples for the encode passes and
 the MLP tiles; chunked or per-sample; the encoding backward's warp-aggregated scatter on any
-number of levels) is a schedule, not a change of arithmetic: every mode must give the march-order
-step's losses, gradients and render.
+number of levels) and the paired copies of the one-to-one level tables (kernels_pairs.cu) are
+schedules / layouts, not changes of arithmetic: every mode must give the march-order step's
+losses, gradients and render.
 
-Only the fp32 summation order of the gradient scatter (atomics, warp sums) differs,
-so losses and renders agree to fp32 rounding and gradients to 1e-5 relative L2 per array.
-The oracle parity of the default (ordered) path is the rest of the GPU suite.
+Only the fp32 summation order of the gradient scatter (atomics, warp sums) differs, so losses
+and renders agree to fp32 rounding and gradients to 1e-5 relative L2 per array.  The oracle
+parity of the default path (ordered, paired) is the rest of the GPU suite.
 """
 import numpy as np
 import pytest
@@ -23,8 +24,10 @@ MODES = {
     "ordered_chunk5": {"DG_SAMPLE_ORDER": "2", "DG_ORDER_CHUNK": "5", "DG_ORDER_BITS": "3"},
     "ordered_agg_all": {"DG_SAMPLE_ORDER": "2", "DG_ENC_AGG": "0.01"},
     "ordered_sliced": {"DG_SAMPLE_ORDER": "2", "DG_ENC_BWD_MB": "1", "DG_ENC_FWD_MB": "1"},
+    "march_unpaired": {"DG_SAMPLE_ORDER": "0", "DG_ENC_PAIRED": "0"},
+    "ordered_unpaired": {"DG_SAMPLE_ORDER": "2", "DG_ENC_PAIRED": "0"},
 }
-ENV = ("DG_SAMPLE_ORDER", "DG_ENC_AGG", "DG_ORDER_BITS", "DG_ORDER_CHUNK", "DG_ENC_BWD_MB", "DG_ENC_FWD_MB")
+ENV = ("DG_SAMPLE_ORDER", "DG_ENC_PAIRED", "DG_ENC_AGG", "DG_ORDER_BITS", "DG_ORDER_CHUNK", "DG_ENC_BWD_MB", "DG_ENC_FWD_MB")
 
 
 def _run(cfg, mode, monkeypatch, batch, state_seed=0, occupancy_fraction=None):
