@@ -12,6 +12,6 @@ if [ "${MODE:-full}" = list ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_list.log 2>&1
 else
   K=${KERNELS:-k_mlp_bwd_tc|k_encode_fwd|k_encode_bwd}
-  N=$(echo "$K" | tr '|' '\n' | wc -l)
+  N=${COUNT:-$(( $(echo "$K" | tr "|" "\n" | wc -l) + 1 ))}
   ncu --set full --clock-control none --import-source on -k "regex:$K" -s 3 -c $N -o $OUT/$TAG $CMD > $OUT/ncu_$TAG.log 2>&1
 fi
