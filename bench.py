@@ -498,8 +498,9 @@ def main():
     ap.add_argument("--workload", default="weak", choices=["weak", "C1", "C2", "C3", "C4", "C5"],
                     help="weak: the C4 weak-scaling point (default); C1..C4: a BASELINE config whole "
                          "(training); C5: the render-only worst case")
-    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
-                    help="exchange backend for N > 1: NCCL all-to-all-v, or peer-memory pack kernels")
+    ap.add_argument("--comm", default="peer", choices=["nccl", "peer"],
+                    help="exchange backend for N > 1: peer-memory pack kernels (the transfer fused "
+                         "into the pack kernels over CUDA-IPC / NVLink, default) or NCCL all-to-all-v")
     ap.add_argument("--no-cpu-stages", action="store_true", help="skip the all-core stage baseline")
     ap.add_argument("--ref-rays", type=int, default=4096,
                     help="rays per partition per step of each reference replica (SURVEY 8d (i): 4,096)")

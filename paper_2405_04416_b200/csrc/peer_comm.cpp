@@ -106,13 +106,13 @@ int PeerComm::allgather(const void* send, uint64_t bytes, void* recv, std::strin
   const uint64_t slots = 8 * uint64_t(world_) + kSlot * uint64_t(world_) * (epoch & 1);
   for (int q = 0; q < world_; ++q) {
     uint8_t* base = static_cast<uint8_t*>(ctrl_peer_[q]);
-    if (!cu_ok(cudaMemcpyAsync(base + slots + kSlot * rank_, stage, bytes, cudaMemcpyHostToDevice, ctrl_s_),
+    if (!cu_ok(cudaMemcpyAsync(base + slots + kSlot * rank_, stage, bytes, cudaMemcpyDefault, ctrl_s_),
                "control payload copy", err))
       return DG_ECUDA;
   }
   for (int q = 0; q < world_; ++q) {
     uint8_t* base = static_cast<uint8_t*>(ctrl_peer_[q]);
-    if (!cu_ok(cudaMemcpyAsync(base + 8 * rank_, src_epoch, 8, cudaMemcpyHostToDevice, ctrl_s_),
+    if (!cu_ok(cudaMemcpyAsync(base + 8 * rank_, src_epoch, 8, cudaMemcpyDefault, ctrl_s_),
                "control flag copy", err))
       return DG_ECUDA;
   }
