@@ -65,6 +65,15 @@ int main() {
   m.grad_in = (const float4*)up(gin.data(), n * 16);
   void* dx; cudaMalloc(&dx, n * 32 * 4);
   m.dX = (float*)dx;
+  // the forward's ReLU / clip masks (every ReLU unit on, nothing clipped) and outputs
+  std::vector<uint32_t> masks(n * 7, 0xffffffffu);
+  for (uint64_t i = 0; i < n; ++i) masks[6 * n + i] = 0u;
+  m.masks = (uint32_t*)up(masks.data(), masks.size() * 4);
+  std::vector<float4> outs(n);
+  std::uniform_real_distribution<float> U01(0.05f, 0.95f);
+  for (auto& v : outs) v = make_float4(U01(rng), U01(rng), U01(rng), U01(rng));
+  m.out = (float4*)up(outs.data(), n * 16);
+  m.out_tile = m.out;
   void* tr; cudaMalloc(&tr, 64 * 2 * 32 * 8); cudaMemset(tr, 0, 64 * 2 * 32 * 8);
   m.trace = (unsigned long long*)tr;
   cudaEvent_t a, b;
@@ -80,18 +89,20 @@ int main() {
   }
   std::vector<unsigned long long> t(64 * 2 * 32);
   cudaMemcpy(t.data(), tr, t.size() * 8, cudaMemcpyDeviceToHost);
-  // points per tile: [sync_in, sync_out, mma_done] x 10 stages
-  const char* names[10] = {"F1 x.Wd0", "F2 h1.Wd1", "F3 cin.Wc0", "F4 c1.Wc1", "F5 c2.Wc2",
-                           "B1 g5", "B2 G4", "B3 G3", "B4 G2", "B5 G1"};
+  // points per tile: [sync_in, sync_out, mma_done] x 9 stages (the output layer is not
+  // recomputed: B1's colour-head adjoint runs in the F4 epilogue)
+  constexpr int NST = 9;
+  const char* names[NST] = {"F1 x.Wd0", "F2 h1.Wd1", "F3 cin.Wc0", "F4 c1.Wc1",
+                            "B1 g5", "B2 G4", "B3 G3", "B4 G2", "B5 G1"};
   for (int who = 0; who < 2; ++who) {
     printf("thread %d: stage  epi_before  barrier+issue  mma_wait   (cycles, mean over tiles 2..30)\n", who ? 480 : 0);
     double tot = 0;
-    for (int st = 0; st < 10; ++st) {
+    for (int st = 0; st < NST; ++st) {
       double e = 0, bi = 0, w = 0;
       int cnt = 0;
       for (int tile = 2; tile < 31; ++tile) {
         const unsigned long long* p = &t[(tile * 2 + who) * 32];
-        const unsigned long long prev_done = st == 0 ? t[((tile - 1) * 2 + who) * 32 + 29] : p[3 * st - 1];
+        const unsigned long long prev_done = st == 0 ? t[((tile - 1) * 2 + who) * 32 + 3 * NST - 1] : p[3 * st - 1];
         e += double(p[3 * st] - prev_done);
         bi += double(p[3 * st + 1] - p[3 * st]);
         w += double(p[3 * st + 2] - p[3 * st + 1]);
