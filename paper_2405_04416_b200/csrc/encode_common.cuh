@@ -119,10 +119,6 @@ __device__ __forceinline__ void corners_w32(const LevelDesc& lv, const LatticeAx
   }
 }
 
-__device__ __forceinline__ void level_corners_w32(const LevelDesc& lv, const double p[3], Corners& c) {
-  corners_w32(lv, lattice_axes(lv, p), c);
-}
-
 // The training forward's gather of one level (k_encode_fwd) from its lattice axes: fp32 corner
 // weights (corner_weights_w32: <= 2 ulp from the reference's rounded fp64 products, i.e.
 // ~1e-7 of a feature), the two x-neighbour corners of each (y, z) pair fetched as one aligned
