@@ -219,6 +219,8 @@ void launch_mlp_bwd(const MlpLaunch& m, int num_sms, cudaStream_t s);
 // tcgen05 (split-bf16) variants (kernels_mlp_tc.cu); tiles of 128 samples
 void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);
 void launch_mlp_bwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);  // tile_off at 128
+// evaluation forward (no masks, no backward): split-bf16
+void launch_mlp_eval_tc(const MlpLaunch& m, int num_sms, cudaStream_t s);
 
 // ---- compositing stage entry points (kernels_render_api.cu), fp64 like the reference ----
 // fp64 arithmetic in the reference's order; R = float (the C ABI's fp32 stage I/O) or double

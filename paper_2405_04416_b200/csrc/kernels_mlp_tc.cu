@@ -704,6 +704,157 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
   if (warp == 0) tc::tmem_free(tmem, 256);
 }
 
+// Evaluation forward (dg_render / evaluate_rays): split-bf16 (3 MMAs per 16-wide K step, 2^-17
+// operand error, inside the render's 1e-4 bar) — there is no backward, so no ReLU decision
+// needs the training forward's split-tf32 precision, and bf16 operands pack two per TMEM column
+// (half the epilogue stores, full-rate MMAs).  TMEM: [0, 64) the accumulator, [64, 128) A.
+struct EvalTcSmem {
+  TcWeights w;
+  float sig_raw[TM];
+  uint64_t mbar;
+  uint32_t tslot;
+};
+
+// 2 column parts (warps 0-3 / 4-7) x 4 lane quadrants; each thread owns one sample row and 32 of
+// the 64 hidden columns; tiles strided over the grid (as k_mlp_fwd_tc).
+__global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_eval_tc(MlpLaunch m) {
+  constexpr int NP = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  EvalTcSmem& sm = *reinterpret_cast<EvalTcSmem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quad = warp & 3, part = warp >> 2;
+  const int row = quad * 32 + lane;  // TMEM lane == sample row of the tile
+  if (warp == 0) tc::tmem_alloc(&sm.tslot, 128);
+  if (tid == 0) {
+    tc::mbar_init(&sm.mbar, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = sm.tslot;
+  const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
+  const Sink act{nullptr, nullptr, my_lanes + A_HI};
+  const uint32_t a_op = tmem + A_HI;
+  uint32_t phase = 0;
+  auto mma_done = [&]() {
+    tc::mbar_wait(&sm.mbar, phase);
+    phase ^= 1u;
+    tc::fence_after();
+  };
+  uint32_t tile = blockIdx.x;
+  if (tile < m.n_tiles) {
+    TileGeo cur = tile_geo(m, tile);
+    Pref<NP> pf;
+    pf.start(m, row < cur.count, cur.s0 + row, part, false);
+    pf.rec(m, part);
+    pf.appearance(m, m.fields[cur.f], part);
+    stage_weights_tc(m.fields[cur.f], m.params, sm.w);
+    int loaded = cur.f;
+    int act_c = m.fields[cur.f].coarse ? 2 : 1;  // colour activation of the loaded field
+    pf.put_x(act, row, part);
+    for (;;) {
+      const bool valid = row < cur.count;
+      const uint64_t gs = cur.s0 + row;
+      const uint32_t next = tile + gridDim.x;
+      const bool has_next = next < m.n_tiles;
+      const TileGeo nx = has_next ? tile_geo_at(m, cur, next) : cur;
+      to_mma();
+      // ---- L1: H1 = relu(X Wd0^T + b) ----
+      ISSUE(gemm_ts<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
+      float cin_app[17];
+#pragma unroll
+      for (int i = 0; i < 17; ++i) cin_app[i] = pf.app[i];
+      const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
+      pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next tile: X, item
+      mma_done();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        float v[16];
+        ld16(my_lanes + part * 32 + 16 * q, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[part * 32 + 16 * q + i], 0.f);
+        put8(act, row, part * 32 + 16 * q, v);
+        put8(act, row, part * 32 + 16 * q + 8, v + 8);
+      }
+      to_mma();
+      // ---- L2: raw16 = H1 Wd1^T + b ; Cin = [clip(raw1..15) | SH16 | app | 0] ----
+      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]));
+      mma_done();
+      {
+        float raw[16];
+        if (part == 0) {
+          ld16(my_lanes, raw);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) raw[i] = clip15(raw[i] + sm.w.bd1[i]);
+          sm.sig_raw[row] = raw[0];
+        }
+        // this tile's dir / app were prefetched into the (now next-tile) registers: restore
+        Pref<NP> cp;
+        cp.valid = valid;
+        cp.dir[0] = d0;
+        cp.dir[1] = d1;
+        cp.dir[2] = d2;
+#pragma unroll
+        for (int i = 0; i < 17; ++i) cp.app[i] = cin_app[i];
+        cp.put_cin(act, row, part, raw);
+      }
+      pf.rec(m, part);  // next tile's RayRec (item arrived during L1/L2)
+      to_mma();
+      // ---- L3: C1 = act(Cin Wc0^T + b) ----
+      ISSUE(gemm_ts<64, 48>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]));
+      mma_done();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        float v[16];
+        ld16(my_lanes + part * 32 + 16 * q, v);
+        act16(v, sm.w.bc0 + part * 32 + 16 * q, act_c);
+        put8(act, row, part * 32 + 16 * q, v);
+        put8(act, row, part * 32 + 16 * q + 8, v + 8);
+      }
+      to_mma();
+      // ---- L4: C2 = act(C1 Wc1^T + b) ----
+      ISSUE(gemm_ts<64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]));
+      mma_done();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        float v[16];
+        ld16(my_lanes + part * 32 + 16 * q, v);
+        act16(v, sm.w.bc1 + part * 32 + 16 * q, act_c);
+        put8(act, row, part * 32 + 16 * q, v);
+        put8(act, row, part * 32 + 16 * q + 8, v + 8);
+      }
+      pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
+      to_mma();
+      // ---- L5: rgb = sigmoid(clip(C2 Wc2^T + b)) ----
+      ISSUE(gemm_ts<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
+      mma_done();
+      if (part == 0) {
+        float v[16];
+        ld16(my_lanes, v);
+        if (valid)
+          __stcs(m.out + (m.perm ? __ldg(m.perm + gs) : gs),
+                 make_float4(expf(sm.sig_raw[row]), sigm(clip15(v[0] + sm.w.bc2[0])),
+                             sigm(clip15(v[1] + sm.w.bc2[1])), sigm(clip15(v[2] + sm.w.bc2[2]))));
+      }
+      if (!has_next) break;
+      if (nx.f != loaded) {
+        __syncthreads();  // every thread is done with the old biases
+        stage_weights_tc(m.fields[nx.f], m.params, sm.w);
+        loaded = nx.f;
+        act_c = m.fields[nx.f].coarse ? 2 : 1;
+      }
+      pf.put_x(act, row, part);  // the A region is free: every MMA has completed
+      tile = next;
+      cur = nx;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tmem, 128);
+}
+
+
 // ============================================================================ backward
 // Per tile of 128 samples: recompute the forward's hidden layers (keeping every layer input in
 // smem; the output layer is not recomputed: the colour-head adjoint and the sigma path take
@@ -1212,6 +1363,19 @@ void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
   const uint32_t want = (uint32_t)num_sms * MLP_FWD_MINB;
   const unsigned grid = m.n_tiles < want ? m.n_tiles : want;
   k_mlp_fwd_tc<<<grid, NTF, smem, s>>>(m);
+}
+
+void launch_mlp_eval_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
+  if (!m.n_tiles) return;
+  static bool attr = false;
+  const int smem = (int)sizeof(EvalTcSmem) + 1024;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mlp_eval_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const uint32_t want = (uint32_t)num_sms * MLP_FWD_MINB;
+  const unsigned grid = m.n_tiles < want ? m.n_tiles : want;
+  k_mlp_eval_tc<<<grid, NTF, smem, s>>>(m);
 }
 
 void launch_mlp_bwd_tc(const MlpLaunch& m0, int num_sms, cudaStream_t s) {

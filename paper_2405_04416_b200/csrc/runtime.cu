@@ -1984,7 +1984,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   MlpLaunch mf = mlp_launch(c, false);
   mf.masks = nullptr;  // evaluation has no backward
   mf.app_override = c->eval_app.as<float>();
-  if (c->mlp_impl) launch_mlp_fwd_tc(mf, c->num_sms, s);
+  if (c->mlp_impl) launch_mlp_eval_tc(mf, c->num_sms, s);  // split-bf16: no ReLU decision kept
   else launch_mlp_fwd(mf, s);
   launch_composite(NI, it, sm, c->n_fine, 1, s);
   c->launches += 3;
