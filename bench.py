@@ -388,6 +388,7 @@ class Runner:
         self.stream = torch.cuda.ExternalStream(sptr.value)
         self.stats = abi.StepStats()
         self.samples = 0
+        self.h2d = self.d2h = 0  # host <-> device bytes of the steps run (copies through the ABI)
         self.shard = wl.n_rays // world
         self.lo = rank * self.shard
 
@@ -396,6 +397,8 @@ class Runner:
         if rc != 0:
             raise self.dg.DGError(rc, self.dg.lib().dg_last_error().decode())
         self.samples += int(self.stats.samples)
+        self.h2d += int(self.stats.h2d_bytes)
+        self.d2h += int(self.stats.d2h_bytes)
 
     def barrier(self):
         if self.world > 1:
@@ -590,9 +593,13 @@ def main():
         r.step(args.warmup, pinned)  # first host-batch step allocates the staging buffers
         ctx.snapshot(restore=True)
         r.samples = 0
+        r.h2d = r.d2h = 0
         ems = r.timed(lambda i: r.step(i, pinned), args.steps, args.warmup)
+        # mean over the window: the ray batch every step, plus the occupancy update's sample
+        # stream (uploaded once per update, ahead of it) in the window's update step
         e2e = {"value": B / (ems / args.steps / 1000.0), "unit": "rays/s",
-               "h2d_bytes_per_step": int(r.stats.h2d_bytes), "d2h_bytes_per_step": int(r.stats.d2h_bytes),
+               "h2d_bytes_per_step": r.h2d // args.steps, "d2h_bytes_per_step": r.d2h // args.steps,
+               "batch_h2d_bytes_per_step": int(B // world * (48 + 12 + 4)),
                "ms_per_step": ems / args.steps, "same_steps_and_state_as_value": True,
                "samples_per_step": r.sum_over_ranks(r.samples) / args.steps}
 
