@@ -888,7 +888,7 @@ constexpr int XW = 32, HW = 64, CW = 48;  // activation tile widths
 // gradients are warp-reduced in the B1 epilogue instead.
 struct BwdTcSmem {
   TcWeights w;
-  uint8_t g5[2][TM * 16 * 2];  // followed by >= 12 KB of valid smem (M=64 MN-major reads 64 cols)
+  uint8_t g5[2][TM * 16 * 2];  // G5 hi / lo (the N = 16 operand of dWc2^T)
   uint8_t x_hi[TM * XW * 2];
   uint8_t ones_a[TM * 8 * 2];  // [x | 1] and [1 | h1]
   uint8_t h1_hi[TM * HW * 2];
@@ -914,7 +914,7 @@ static_assert(sizeof(BwdTcSmem) <= 232448, "backward tile set exceeds 227 KB of 
 // TMEM columns: [0,64) accumulator, [64,128) A operand; dW accumulators (M = 64 rows = out
 // features, row o at lane (o % 16) + 32 (o / 16)) with the bias column folded in: appended
 // after dW (C0: [cin | 1], D0: [x | 1]) or prepended (C1: [1 | c1], D1: [1 | h1]).
-constexpr uint32_t TD_C2 = 128;                    // 64 (bias: epilogue)
+constexpr uint32_t TD_C2 = 128;                    // dWc2^T: 16 of 64 (bias: epilogue)
 constexpr uint32_t TB_C1 = 192, TD_C1 = 200;       // 8 + 64
 constexpr uint32_t TD_C0 = 264, TB_C0 = 312;       // 48 + 8
 constexpr uint32_t TB_D1 = 320, TD_D1 = 328;       // 8 + 64
@@ -1019,7 +1019,21 @@ __device__ void flush_all(uint32_t tmem, const FieldDesc& fd, float* __restrict_
     if (bias_c2[threadIdx.x] != 0.f) atomicAdd(base + fd.cb2 + threadIdx.x, bias_c2[threadIdx.x]);
     bias_c2[threadIdx.x] = 0.f;
   }
-  flush_dw(tmem, TD_C2, HW, 3, 64, kNoBias, base + fd.cw2, base + fd.cb2);
+  {  // dWc2^T: row i (C2 feature) in lane (i % 16) + 32 (i / 16), column o (output, < 3)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, quad = warp & 3;
+    if ((warp >> 2) == 0) {
+      float v[8];
+      tc::tmem_ld8(tmem + ((uint32_t)(quad * 32) << 16) + TD_C2, v);
+      tc::tmem_wait_ld();
+      const int i = quad * 16 + lane;
+      if (lane < 16) {
+        float* gW = base + fd.cw2;
+#pragma unroll
+        for (int o = 0; o < 3; ++o)
+          if (v[o] != 0.f) atomicAdd(gW + o * 64 + i, v[o]);
+      }
+    }
+  }
   flush_dw(tmem, TD_C1, HW, 64, 64, TB_C1, base + fd.cw1, base + fd.cb1);
   flush_dw(tmem, TD_C0, CW, 64, cin, TB_C0, base + fd.cw0, base + fd.cb0);
   flush_dw(tmem, TD_D1, HW, 16, 64, TB_D1, base + fd.dw1, base + fd.db1);
@@ -1233,7 +1247,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
       pf.grad(m, part);  // next tile's upstream gradient
       sync_mma();
       issue2(warp, &sm.mbar, [&] { gemm_igrad<16, 64, 16>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]); },
-             [&] { gemm_wgrad<HW>(tmem + TD_C2, sm.g5[0], sm.g5[1], sm.c2[0], sm.c2[1], !fresh); });
+             // dWc2 transposed: D[64 C2 features x 16] = C2^T G5 (the c2 tile as the M = 64 operand,
+             // G5 as a 16-column B): a quarter of the B bytes of G5^T C2 at N = 64
+             [&] { gemm_wgrad<16>(tmem + TD_C2, sm.c2[0], sm.c2[1], sm.g5[0], sm.g5[1], !fresh); });
       mma_done();
       // ---------------- B2: G4 = dC2 * act'(C2) -> s ----------------
       {
