@@ -426,6 +426,7 @@ class Runner:
         e0.record(self.stream)
         for i in range(n):
             fn(first + i)
+        self.ctx.fence()  # the last step's Adam (side stream) inside the timed region
         e1.record(self.stream)
         e1.synchronize()
         self.barrier()

@@ -462,7 +462,13 @@ typedef struct dg_stage_times {
 } dg_stage_times;
 int dg_enable_stage_timing(dg_ctx* ctx, int enable);
 int dg_last_stage_times(dg_ctx* ctx, dg_stage_times* t);
+/* Waits (host) for every call's work, including the last training step's Adam update, which
+ * runs on a side stream so that the next step's segmentation / march overlaps it.  Every API
+ * call that reads or writes parameters, gradients or moments orders itself after that update;
+ * dg_fence does only that ordering (no host wait): work the caller queues afterwards on the
+ * context's stream (dg_set_stream) sees the updated parameters. */
 int dg_synchronize(dg_ctx* ctx);
+int dg_fence(dg_ctx* ctx);
 /* Diagnostics: runs the tcgen05 operand-layout self-test on the current device.
  * Host fp32 inputs A[128x64], B[64x64], X[128x32]; outputs Y0 = A B^T, Y1 = A B (128x64) and
  * Y2 = A^T X (64x32), each a split-bf16 (3-term) tcgen05.mma product accumulated in TMEM. */

@@ -269,7 +269,7 @@ void launch_adam_f64(double* p, const double* g, double* m, double* v, uint64_t 
 // ---- optimizer / init (kernels_adam.cu) ----
 void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, float b1, float b2,
                  float eps, float inv_bias1, float inv_bias2, cudaStream_t s,
-                 const uint32_t* abort_flag = nullptr, uint32_t abort_mask = 0);
+                 const uint32_t* abort_flag = nullptr, uint32_t abort_mask = 0, bool spread = false);
 void launch_fill_uniform(float* p, uint64_t n, float lo, float hi, uint64_t seed, cudaStream_t s);
 
 // ---- occupancy update (kernels_occ.cu) ----

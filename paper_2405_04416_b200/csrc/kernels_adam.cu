@@ -68,16 +68,19 @@ __global__ void k_fill_uniform(float* __restrict__ p, uint64_t n, float lo, floa
 
 }  // namespace
 
+// spread: one float4 per thread (many short CTAs) instead of a resident grid-stride grid, so
+// that kernels of a higher-priority stream (the next training step's front half) get SMs as
+// CTAs retire while this update runs on its side stream.
 void launch_adam(float* p, float* g, float* m, float* v, uint64_t n, float lr, float b1, float b2,
                  float eps, float inv_bias1, float inv_bias2, cudaStream_t s, const uint32_t* abort_flag,
-                 uint32_t abort_mask) {
+                 uint32_t abort_mask, bool spread) {
   const uint64_t n4 = n / 4;
   if (n4) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t want = (n4 + 255) / 256;
-    const unsigned grid = (unsigned)(want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8);
+    const unsigned grid = (unsigned)(spread || want < (uint64_t)sms * 8 ? want : (uint64_t)sms * 8);
     k_adam<<<grid, 256, 0, s>>>(reinterpret_cast<float4*>(p), reinterpret_cast<float4*>(g),
                                 reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, lr,
                                 b1, b2, eps, inv_bias1, inv_bias2, abort_flag, abort_mask);

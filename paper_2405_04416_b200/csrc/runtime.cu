@@ -174,6 +174,14 @@ struct dg_ctx {
   // ... and go up to the device on a copy stream as soon as they are drawn, so the 24 B/cell
   // transfer overlaps the training steps before the update instead of stalling it
   cudaStream_t stream_copy = nullptr;
+  // The training step's Adam runs on its own stream, so the next step's front half (which
+  // touches no parameter) overlaps it; every later use of the parameters / gradients / moments
+  // (the next step's encode, any API call) first orders the context stream after ev_adam.
+  cudaStream_t stream_adam = nullptr;
+  cudaEvent_t ev_grads = nullptr, ev_adam = nullptr;
+  bool adam_pending = false;
+  bool adam_spread = true;  // DG_ADAM_SPREAD=0: the resident grid-stride Adam grid
+  DBuf adam_flag;  // the step's error word as k_adam reads it
   // Pinned staging arena for the step's small host <-> device transfers.  A pageable source
   // makes cudaMemcpyAsync wait for the stream to drain and a pageable destination makes it
   // synchronous, so every plan upload / count readback would otherwise cost a full pipeline
@@ -1229,6 +1237,8 @@ int occ_try_upload(dg_ctx* c, bool block) {
 // Worker::update_occupancy (worker.cpp:549-562) + OccupancyGrid::decay_and_update
 // (grid.cpp:201-229).  The jitter points are the reference's mt19937_64 draws in its order
 // (fine grid, then coarse grid, same stream); sigma is evaluated on the device.
+int order_after_adam(dg_ctx* c);
+
 int occupancy_update(dg_ctx* c) {
   const dg_run_config& cfg = c->cfg;
   const uint64_t step = c->worker_step;
@@ -1236,6 +1246,7 @@ int occupancy_update(dg_ctx* c) {
       step % cfg.occ_update_interval != 0)
     return DG_OK;
   cudaStream_t s = c->stream;
+  TRY(order_after_adam(c));  // the density query reads the updated parameters
   const double threshold =
       (step < cfg.occ_threshold_switch_step ? cfg.occ_threshold_early : cfg.occ_threshold_late) *
       cfg.occ_threshold_scale;
@@ -1319,9 +1330,19 @@ int occupancy_update(dg_ctx* c) {
   return DG_OK;
 }
 
-int check_ctx(const dg_ctx* c) {
-  if (!c) return set_err(DG_EINVAL, "null context");
+// The context stream after the last step's asynchronous Adam update (no host wait).
+int order_after_adam(dg_ctx* c) {
+  if (!c->adam_pending) return DG_OK;
+  CU(cudaStreamWaitEvent(c->stream, c->ev_adam, 0));
+  c->adam_pending = false;
   return DG_OK;
+}
+
+// Every API entry but dg_train_step's front half: argument check + ordering after the last
+// step's Adam (parameters, gradients and moments are final for the caller).
+int check_ctx(const dg_ctx* cc) {
+  if (!cc) return set_err(DG_EINVAL, "null context");
+  return order_after_adam(const_cast<dg_ctx*>(cc));
 }
 
 int check_part(const dg_ctx* c, uint32_t partition, uint32_t* lp) {
@@ -1409,9 +1430,17 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   if (const char* e = std::getenv("DG_ENC_FWD_GROUP_MB")) c->enc_group_fwd = std::strtoull(e, nullptr, 10) << 20;
   if (const char* e = std::getenv("DG_ENC_BWD_GROUP_MB")) c->enc_group_bwd = std::strtoull(e, nullptr, 10) << 20;
-  CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  // the step stream at the highest priority, the side-stream Adam at the lowest: the next
+  // step's front half takes SMs ahead of the update's remaining CTAs
+  int prio_lo = 0, prio_hi = 0;
+  CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CU(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
   c->own_stream = c->stream;
   CU(cudaStreamCreateWithFlags(&c->stream_copy, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithPriority(&c->stream_adam, cudaStreamNonBlocking, prio_lo));
+  if (const char* e = std::getenv("DG_ADAM_SPREAD")) c->adam_spread = std::strcmp(e, "0") != 0;
+  CU(cudaEventCreateWithFlags(&c->ev_grads, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&c->ev_adam, cudaEventDisableTiming));
   c->pin_cap = 1 << 20;
   CU(cudaHostAlloc(reinterpret_cast<void**>(&c->pin), c->pin_cap, cudaHostAllocDefault));
   CU(cudaEventCreateWithFlags(&c->ev_occ_up, cudaEventDisableTiming));
@@ -1430,14 +1459,18 @@ int dg_ctx_destroy(dg_ctx* c) {
   if (c->pin) cudaFreeHost(c->pin);
   cudaStreamSynchronize(c->stream);
   if (c->stream_copy) cudaStreamSynchronize(c->stream_copy);
+  if (c->stream_adam) cudaStreamSynchronize(c->stream_adam);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->ev_occ_up) cudaEventDestroy(c->ev_occ_up);
   if (c->ev_occ_used) cudaEventDestroy(c->ev_occ_used);
-  cudaStream_t s = c->own_stream, sc = c->stream_copy;
+  if (c->ev_grads) cudaEventDestroy(c->ev_grads);
+  if (c->ev_adam) cudaEventDestroy(c->ev_adam);
+  cudaStream_t s = c->own_stream, sc = c->stream_copy, sa = c->stream_adam;
   delete c;
   if (s) cudaStreamDestroy(s);
   if (sc) cudaStreamDestroy(sc);
+  if (sa) cudaStreamDestroy(sa);
   return DG_OK;
 }
 
@@ -1792,7 +1825,8 @@ int dg_set_appearance(dg_ctx* c, const uint32_t* ids, const float* rows, uint32_
 }
 
 int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats* stats) {
-  TRY(check_ctx(c));
+  if (!c) return set_err(DG_EINVAL, "null context");  // no Adam ordering yet: the front half
+                                                      // overlaps the previous step's update
   if (!b) return set_err(DG_EINVAL, "null batch");
   if (b->n && (!b->origin || !b->dir || !b->color_gt)) return set_err(DG_EINVAL, "batch: missing arrays");
   if (b->n >= (1ull << 32) || b->first_ray_id + b->n > (1ull << 32))
@@ -1825,8 +1859,9 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
     c->d2h += pair_cnt.size() * 4;
   }
   CU(cudaMemsetAsync(c->loss.p, 0, sizeof(LossAccum), s));
-  // K3 / K4 forward
+  // K3 / K4 forward (from here on the parameters are read: after the previous step's Adam)
   {
+    TRY(order_after_adam(c));
     TRY(pairs_expand(c, s));
     std::vector<EncPass> passes;
     const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd);
@@ -1902,12 +1937,23 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   // k_adam skips the update (and discards the gradients) when the merge flagged a missing
   // partial, so an aborted step leaves params, moments, t and the step counter untouched
   // (the reference throws before apply_updates, worker.cpp:371-380)
+  // on the Adam stream: the call returns once the losses are read, and the next step's front
+  // half (no parameter access) runs under the update
+  // Adam reads its own copy of the error word: the next step clears the loss accumulator
+  // while this update may still be queued
+  TRY(c->adam_flag.ensure(16));
+  CU(cudaMemcpyAsync(c->adam_flag.p, &c->loss.as<LossAccum>()->error, sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                     s));
+  CU(cudaEventRecord(c->ev_grads, s));
+  CU(cudaStreamWaitEvent(c->stream_adam, c->ev_grads, 0));
   launch_adam(c->params.as<float>(), c->grads.as<float>(), c->adam_m.as<float>(), c->adam_v.as<float>(),
               c->n_params, float(lr), float(c->cfg.adam_beta1), float(c->cfg.adam_beta2),
-              float(c->cfg.adam_eps), float(1.0 / bias1), float(1.0 / bias2), s,
-              &c->loss.as<LossAccum>()->error, 2u);
+              float(c->cfg.adam_eps), float(1.0 / bias1), float(1.0 / bias2), c->stream_adam,
+              c->adam_flag.as<uint32_t>(), 2u, c->adam_spread);
   ++c->launches;
-  mark(c, 10);
+  if (c->timing) cudaEventRecord(c->ev[10], c->stream_adam);
+  CU(cudaEventRecord(c->ev_adam, c->stream_adam));
+  c->adam_pending = true;
   LossAccum la;
   LossAccum* la_pin = pin_slot<LossAccum>(c, 1);
   CU(cudaMemcpyAsync(la_pin ? la_pin : &la, c->loss.p, sizeof la, cudaMemcpyDeviceToHost, s));
@@ -1919,6 +1965,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   c->worker_step = step + 1;
   TRY(occupancy_update(c));
   if (c->timing) {
+    CU(cudaStreamSynchronize(c->stream_adam));  // stage timing (diagnostic) waits for Adam
     float* t = &c->times.segment;
     for (int k = 0; k < 10; ++k) cudaEventElapsedTime(&t[k], c->ev[k], c->ev[k + 1]);
     cudaEventElapsedTime(&c->times.total, c->ev[0], c->ev[10]);
@@ -3109,9 +3156,11 @@ int dg_set_stream(dg_ctx* c, void* stream) {
 }
 
 int dg_synchronize(dg_ctx* c) {
-  TRY(check_ctx(c));
+  TRY(check_ctx(c));  // orders the stream after the last step's Adam
   CU(cudaStreamSynchronize(c->stream));
   return DG_OK;
 }
+
+int dg_fence(dg_ctx* c) { return check_ctx(c); }
 
 }  // extern "C"

@@ -545,6 +545,10 @@ class Context:
     def synchronize(self):
         _check(lib().dg_synchronize(self.h))
 
+    def fence(self):
+        """Order the context stream after the last step's (side-stream) Adam update."""
+        _check(lib().dg_fence(self.h))
+
 
 def lr_at(cfg, step):
     return lib().dg_lr_at(C.byref(cfg), C.c_uint64(step))
