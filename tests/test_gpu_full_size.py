@@ -172,3 +172,30 @@ def test_value_parity_c1_grid(mb, monkeypatch):
     for k in ("loss_rgb", "loss_transmittance", "loss_distortion"):
         assert abs(sg[k] - so[k]) <= 1e-4 * abs(so[k]), (k, sg[k], so[k])
     _grad_parity(cfg, ctx, orc, p0, sg["lr"])
+
+
+@pytest.mark.slow
+def test_value_parity_c2_two_partitions_on_one_gpu():
+    """C2's configuration (2 x 1 partitions, T = 2^22 per partition, Nmax = 2048, divisor 193,
+    independent rays: ~50 % cross the plane) with both partitions on one GPU, on a 2,048-ray
+    subset: per-field encode passes over two fields' hashed and paired one-to-one tables, the
+    sample order per field, the aliased partial exchange and two-segment merges, against the
+    fp64 oracle from identical injected state (render, losses, per-array gradients, Adam)."""
+    from .helpers import params_for, tied_train_step
+    wl = workloads.c2()
+    cfg = wl.cfg
+    assert cfg.kx == 2 and cfg.fine_table_log2 == 22
+    ctx, orc = _full_pair(wl)
+    o, d, gt, img = workloads.make_rays(cfg, 2048, wl.generator, seed=11)
+    app = np.asarray(orc.app[0])
+    rgb, T, depth = ctx.render(o, d, app)
+    rgb_o, T_o, depth_o = orc.eval_rays(o, d, app)
+    assert np.allclose(rgb, rgb_o, rtol=1e-4, atol=1e-6), np.abs(rgb - rgb_o).max()
+    assert np.allclose(T, T_o, rtol=1e-4, atol=1e-6), np.abs(T - T_o).max()
+    p0 = [params_for(cfg, g, table_scale=0.5).astype(np.float64) for g in range(2)]
+    sg, so, (ties, zmax) = tied_train_step(ctx, orc, o, d, gt, img, 0)
+    assert ties <= 64 and zmax <= 4e-6, (ties, zmax)
+    assert sg["rays"] == so["rays"] == 2048
+    for k in ("loss_rgb", "loss_transmittance", "loss_distortion"):
+        assert abs(sg[k] - so[k]) <= 1e-4 * abs(so[k]), (k, sg[k], so[k])
+    _grad_parity(cfg, ctx, orc, p0, sg["lr"])
