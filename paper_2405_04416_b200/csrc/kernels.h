@@ -193,6 +193,8 @@ struct MlpLaunch {
   const uint32_t* field_off;   // device, n_fields + 1
   const uint32_t* tile_off;    // device, n_fields + 1 (prefix of tiles)
   uint32_t n_tiles;
+  uint32_t relu_tiles;         // bwd (tc): the leading tiles of ReLU (fine) fields, which take the
+                               // paired kernel k_mlp_bwd_tc_relu; 0: every tile the serial one
   const float* X;              // level-major [levels][x_stride] float2
   uint64_t x_stride;           // samples per level row of X / dX
   uint32_t levels;

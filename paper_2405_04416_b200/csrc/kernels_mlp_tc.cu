@@ -16,6 +16,9 @@
 //   -> C2 = act(C1 Wc1^T + b) [64] -> rgb = sigmoid(clip(C2 Wc2^T + b)) [3], sigma = exp(clip(raw0)).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "dg_common.cuh"
 #include "kernels.h"
 #include "tc.cuh"
@@ -914,11 +917,13 @@ static_assert(sizeof(BwdTcSmem) <= 232448, "backward tile set exceeds 227 KB of 
 // TMEM columns: [0,64) accumulator, [64,128) A operand; dW accumulators (M = 64 rows = out
 // features, row o at lane (o % 16) + 32 (o / 16)) with the bias column folded in: appended
 // after dW (C0: [cin | 1], D0: [x | 1]) or prepended (C1: [1 | c1], D1: [1 | h1]).
-constexpr uint32_t TD_C2 = 128;                    // dWc2^T: 16 of 64 (bias: epilogue)
-constexpr uint32_t TB_C1 = 192, TD_C1 = 200;       // 8 + 64
-constexpr uint32_t TD_C0 = 264, TB_C0 = 312;       // 48 + 8
-constexpr uint32_t TB_D1 = 320, TD_D1 = 328;       // 8 + 64
-constexpr uint32_t TD_D0 = 392, TB_D0 = 424;       // 32 + 8
+// The dW block fills columns [256, 512): the paired ReLU backward (k_mlp_bwd_tc_relu) keeps a
+// second accumulator and A region at [128, 256).
+constexpr uint32_t TD_C2 = 256;                    // dWc2^T: 16 of 64 (bias: epilogue)
+constexpr uint32_t TB_C1 = 272, TD_C1 = 280;       // 8 + 64
+constexpr uint32_t TD_C0 = 344, TB_C0 = 392;       // 48 + 8
+constexpr uint32_t TB_D1 = 400, TD_D1 = 408;       // 8 + 64
+constexpr uint32_t TD_D0 = 472, TB_D0 = 504;       // 32 + 8
 constexpr uint32_t kNoBias = 0xffffffffu;
 
 // D (M=64 x N) (+)= G^T A over K = TM samples; G tile (TM x >=64 cols span), A tile (TM x N);
@@ -1060,7 +1065,7 @@ __device__ __forceinline__ void grad_act16(const uint8_t* a_hi, const uint8_t* a
   put8(out, r, c0 + 8, v + 8);
 }
 
-__global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
+__global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m, uint32_t t_lo, uint32_t t_hi) {
   constexpr int NP = 4;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   BwdTcSmem& sm = *reinterpret_cast<BwdTcSmem*>(smem_raw);
@@ -1115,9 +1120,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
     to_mma();
     trace();
   };
-  // balanced contiguous tile range per CTA
-  const uint32_t t_begin = (uint32_t)(((uint64_t)blockIdx.x * m.n_tiles) / gridDim.x);
-  const uint32_t t_end = (uint32_t)(((uint64_t)(blockIdx.x + 1) * m.n_tiles) / gridDim.x);
+  // balanced contiguous tile range per CTA of [t_lo, t_hi)
+  const uint32_t t_begin = t_lo + (uint32_t)(((uint64_t)blockIdx.x * (t_hi - t_lo)) / gridDim.x);
+  const uint32_t t_end = t_lo + (uint32_t)(((uint64_t)(blockIdx.x + 1) * (t_hi - t_lo)) / gridDim.x);
   int loaded = -1;
   if (t_begin < t_end) {
     uint32_t tile = t_begin;
@@ -1369,6 +1374,350 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m) {
   if (warp == 0) tc::tmem_free(tmem, 512);
 }
 
+// ------------------------------------------------------------ backward, ReLU fields
+// In a ReLU field (the fine field, field.cpp:196-199) every activation derivative of the
+// backward comes from the forward's stored masks, so the input-gradient chain
+// G5 -> dC2 -> G4 -> dC1 -> G3 -> dCin -> G2 -> dH1 -> G1 -> dX never waits for the forward
+// recompute, which feeds only the weight gradients.  The two chains run as paired stages, each
+// with its own TMEM accumulator and A region, so a tile has 5 MMA waits instead of 9:
+//   S1  F1 = X Wd0^T      (-> H1 = relu)            | dC2 = G5 Wc2      (-> G4 = dC2 * c2 mask)
+//   S2  F2 = H1 Wd1^T     (-> raw -> Cin)           | dC1 = G4 Wc1      (-> G3 = dC1 * c1 mask)
+//   S3  F3 = Cin Wc0^T    (-> C1)                   | dCin = G3 Wc0     (-> G2)      + dWc0
+//   S4  F4 = C1 Wc1^T     (-> C2)                   | dH1 = G2 Wd1      (-> G1)      + dWc1
+//   S5                                              | dX = G1 Wd0                    + dWc2, dWd1
+//   tail: dWd0 (runs under the next tile's prologue)
+// G5 comes from the forward's stored outputs and clip flags (as in k_mlp_bwd_tc).  The
+// weight-gradient operand tiles rotate so that no in-flight GEMM's operand is overwritten:
+// G4 -> s, G3 -> c2, C2 -> c2 (after dWc0), G2 -> cin (after dWc0; copied out of the TMEM A
+// region at S4's epilogue), G1 -> s (after dWc1; copied out of TMEM at S5's epilogue).
+// Same arithmetic as k_mlp_bwd_tc (split-bf16 operands, fp32 TMEM accumulation, dW / db over
+// all of a CTA's tiles); only the issue order of the GEMMs differs.
+constexpr uint32_t TF_ACC = 0, TF_A = 64, TB_ACC = 128, TB_A = 192;
+
+// 16 columns [c0, c0 + 16) of this thread's row of a TMEM A region (packed bf16 pairs, hi at ta,
+// lo at ta + A_LO_OFF) -> the smem operand tile (hi / lo), bit for bit.
+__device__ __forceinline__ void a_to_smem16(uint32_t ta, int r, int c0, uint8_t* hi, uint8_t* lo) {
+  float h[8], l[8];
+  tc::tmem_ld8(ta + (uint32_t)(c0 >> 1), h);
+  tc::tmem_ld8(ta + A_LO_OFF + (uint32_t)(c0 >> 1), l);
+  tc::tmem_wait_ld();
+  const uint32_t o0 = tc::core_offset(r, c0, TM), o1 = tc::core_offset(r, c0 + 8, TM);
+  *reinterpret_cast<uint4*>(hi + o0) =
+      make_uint4(__float_as_uint(h[0]), __float_as_uint(h[1]), __float_as_uint(h[2]), __float_as_uint(h[3]));
+  *reinterpret_cast<uint4*>(hi + o1) =
+      make_uint4(__float_as_uint(h[4]), __float_as_uint(h[5]), __float_as_uint(h[6]), __float_as_uint(h[7]));
+  *reinterpret_cast<uint4*>(lo + o0) =
+      make_uint4(__float_as_uint(l[0]), __float_as_uint(l[1]), __float_as_uint(l[2]), __float_as_uint(l[3]));
+  *reinterpret_cast<uint4*>(lo + o1) =
+      make_uint4(__float_as_uint(l[4]), __float_as_uint(l[5]), __float_as_uint(l[6]), __float_as_uint(l[7]));
+}
+
+// v[i] kept where bit i of `bits` is set (ReLU derivative from the forward's mask)
+__device__ __forceinline__ void mask16(float* v, uint32_t bits) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = ((bits >> i) & 1u) ? v[i] : 0.f;
+}
+
+__global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_t t_lo, uint32_t t_hi) {
+  constexpr int NP = 4;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  BwdTcSmem& sm = *reinterpret_cast<BwdTcSmem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quad = warp & 3, part = warp >> 2;
+  const int row = quad * 32 + lane;
+  const int c16 = part * 16;  // this thread's 16 columns of a 64-wide layer
+  if (warp == 0) tc::tmem_alloc(&sm.tslot, 512);
+  if (tid == 0) {
+    tc::mbar_init(&sm.mbar, 1);
+    tc::fence_mbar_init();
+  }
+  for (int r = tid; r < TM; r += NTB) {
+    *reinterpret_cast<uint4*>(sm.ones_a + tc::core_offset(r, 0, TM)) = make_uint4(0x3f80u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sm.ones_b + tc::core_offset(r, 0, TM)) = make_uint4(0x3f80u, 0u, 0u, 0u);
+  }
+  if (tid < 4) sm.bias_c2[tid] = 0.f;
+  for (int i = tid; i < (int)(sizeof(sm.g5) / 16); i += NTB)  // G5 columns 3-15 stay 0
+    reinterpret_cast<uint4*>(sm.g5)[i] = make_uint4(0u, 0u, 0u, 0u);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = sm.tslot;
+  const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
+  const uint32_t aF = tmem + TF_A, aB = tmem + TB_A;            // A operands of the two chains
+  const uint32_t taF = my_lanes + TF_A, taB = my_lanes + TB_A;  // this thread's lane of them
+  const Sink fX{nullptr, nullptr, taF}, fH1{sm.h1_hi, sm.h1_lo, taF}, fCin{sm.cin_hi, sm.cin_lo, taF};
+  const Sink fC1{sm.c1_hi, sm.c1_lo, taF};
+  const Sink bT{nullptr, nullptr, taB}, bG4{sm.s[0], sm.s[1], taB}, bG3{sm.c2[0], sm.c2[1], taB};
+  if (part == 0) {  // G5's K columns 8-15 meet zero Wc2 rows: the region must start finite
+    const uint32_t z[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      tc::tmem_st4(taB + (uint32_t)c, z);
+      tc::tmem_st4(taB + A_LO_OFF + (uint32_t)c, z);
+    }
+  }
+  uint32_t phase = 0;
+  auto mma_done = [&]() {
+    tc::mbar_wait(&sm.mbar, phase);
+    phase ^= 1u;
+    tc::fence_after();
+  };
+  // the forward's masks / outputs of a tile row (see k_mlp_fwd_tc for the word layout)
+  auto load_fwd = [&](const TileGeo& g, bool ok, uint32_t& relu, uint32_t& c2, uint32_t& clip, float4& o) {
+    relu = c2 = clip = 0u;
+    o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok && row < g.count) {
+      const uint64_t s = (uint64_t)g.s0 + row;
+      relu = __ldcs(m.masks + (uint64_t)part * m.x_stride + s);
+      c2 = __ldcs(m.masks + (uint64_t)(4 + (part >> 1)) * m.x_stride + s);
+      if (part == 0) {
+        clip = __ldcs(m.masks + 6ull * m.x_stride + s);
+        o = __ldcs(m.out_tile + s);
+      }
+    }
+  };
+  const uint32_t t_begin = t_lo + (uint32_t)(((uint64_t)blockIdx.x * (t_hi - t_lo)) / gridDim.x);
+  const uint32_t t_end = t_lo + (uint32_t)(((uint64_t)(blockIdx.x + 1) * (t_hi - t_lo)) / gridDim.x);
+  int loaded = -1;
+  if (t_begin < t_end) {
+    uint32_t tile = t_begin;
+    TileGeo cur = tile_geo(m, tile);
+    Pref<NP> pf;
+    pf.start(m, row < cur.count, cur.s0 + row, part, true);
+    pf.rec(m, part);
+    pf.appearance(m, m.fields[cur.f], part);
+    uint32_t mk_relu, mk_c2, mk_clip;
+    float4 o_fwd;
+    load_fwd(cur, true, mk_relu, mk_c2, mk_clip, o_fwd);
+    if (m.fields[cur.f].coarse) __trap();  // sigmoid fields take k_mlp_bwd_tc
+    stage_weights_tc(m.fields[cur.f], m.params, sm.w);
+    loaded = cur.f;
+    bool fresh = true;  // next dW GEMMs start a new accumulation
+    for (;;) {
+      const bool valid = row < cur.count;
+      const uint64_t gs = cur.s0 + row;
+      const uint32_t next = tile + 1;
+      const bool has_next = next < t_end;
+      const TileGeo nx = has_next ? tile_geo_next(m, cur, next) : cur;
+      float cur_app[17];
+#pragma unroll
+      for (int i = 0; i < 17; ++i) cur_app[i] = pf.app[i];
+      const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
+      const float4 up = pf.g;
+      // ---------------- prologue: X -> A_F; G5 (colour-head adjoint, field.cpp:298-306) -> A_B
+      pf.put_x(fX, row, part);
+      float xk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xk[i] = pf.x[i];
+      float g5v[3] = {0.f, 0.f, 0.f};
+      if (part == 0) {
+        const uint32_t dm = mk_clip & 0xffffu;  // the forward's clip flags
+        sm.dmask[row] = dm;
+        const float ug[3] = {up.y, up.z, up.w};
+        const float sgs[3] = {o_fwd.y, o_fwd.z, o_fwd.w};
+        float g[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) g[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const bool clipped = (mk_clip >> (16 + k)) & 1u;
+          g[k] = clipped ? 0.f : ug[k] * sgs[k] * (1.f - sgs[k]);
+          g5v[k] = g[k];
+        }
+        put8(bT, row, 0, g);
+        // sigma path of the density raw gradient (field.cpp:313): up.sigma * exp(raw0)
+        sm.gsig[row] = (dm & 1u) ? 0.f : up.x * o_fwd.x;
+      }
+      to_mma();
+      // ---------------- S1: F1 | dC2 ----------------
+      ISSUE(gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]);
+            gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]));
+      pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next: X, item
+      mma_done();
+      {
+        put8s(sm.x_hi, sm.x_lo, row, part * 8, xk);  // the previous tile's dWd0 is done
+        if (part == 0) {  // G5 for dWc2 (the previous tile's dWc2 is done)
+          float g[8] = {g5v[0], g5v[1], g5v[2], 0.f, 0.f, 0.f, 0.f, 0.f};
+          put8s(sm.g5[0], sm.g5[1], row, 0, g);
+        }
+        float v[16];
+        ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[c16 + i], 0.f);
+        put8(fH1, row, c16, v);
+        put8(fH1, row, c16 + 8, v + 8);
+        ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
+        mask16(v, (mk_c2 >> (((uint32_t)part & 1u) * 16u)) & 0xffffu);
+        put8(bG4, row, c16, v);
+        put8(bG4, row, c16 + 8, v + 8);
+      }
+      to_mma();
+      // ---------------- S2: F2 | dC1 ----------------
+      ISSUE(gemm_ts<16, 64>(tmem + TF_ACC, aF, sm.w.d1[0], sm.w.d1[1]);
+            gemm_igrad<64, 64, 64>(tmem + TB_ACC, aB, sm.w.c1[0], sm.w.c1[1]));
+      pf.rec(m, part);  // next tile's RayRec
+      mma_done();
+      {
+        float raw[16];
+        if (part == 0) {
+          ld16(my_lanes + TF_ACC, raw);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) raw[i] = clip15(raw[i] + sm.w.bd1[i]);
+          sm.sig_raw[row] = raw[0];
+        }
+        Pref<NP> cp;
+        cp.valid = valid;
+        cp.dir[0] = d0;
+        cp.dir[1] = d1;
+        cp.dir[2] = d2;
+#pragma unroll
+        for (int i = 0; i < 17; ++i) cp.app[i] = cur_app[i];
+        cp.put_cin(fCin, row, part, raw);
+      }
+      {
+        float v[16];
+        ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
+        mask16(v, mk_relu >> 16);  // c1 bits of this part's columns
+        put8(bG3, row, c16, v);
+        put8(bG3, row, c16 + 8, v + 8);
+      }
+      to_mma();
+      // ---------------- S3: F3 | dCin, + dWc0 ----------------
+      issue2(warp, &sm.mbar,
+             [&] {
+               gemm_ts<64, 48>(tmem + TF_ACC, aF, sm.w.c0[0], sm.w.c0[1]);
+               gemm_igrad<64, 16, 64>(tmem + TB_ACC, aB, sm.w.c0[0], sm.w.c0[1]);
+             },
+             [&] { gemm_wgrad_bias<CW, false>(tmem + TD_C0, sm.c2[0], sm.c2[1], sm.cin_hi, sm.cin_lo, !fresh); });
+      pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
+      mma_done();
+      {
+        float v[16];
+        ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bc0[c16 + i], 0.f);
+        put8(fC1, row, c16, v);
+        put8(fC1, row, c16 + 8, v + 8);
+      }
+      if (part == 0) {  // G2 = [sigma path, clip-masked dCin[0..14]] -> A_B (smem copy at S4)
+        float v[16];
+        ld16(my_lanes + TB_ACC, v);
+        const uint32_t mask = sm.dmask[row];
+        float g[16];
+        g[0] = sm.gsig[row];
+#pragma unroll
+        for (int k = 1; k < 16; ++k) g[k] = ((mask >> k) & 1u) ? 0.f : v[k - 1];
+        put8(bT, row, 0, g);
+        put8(bT, row, 8, g + 8);
+      } else if (part == 1) {  // output-layer bias gradient db = G5^T . 1
+        float g5[8];
+        get8(sm.g5[0], sm.g5[1], row, 0, g5);
+        float b0 = g5[0], b1 = g5[1], b2 = g5[2];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          b0 += __shfl_xor_sync(0xffffffffu, b0, o);
+          b1 += __shfl_xor_sync(0xffffffffu, b1, o);
+          b2 += __shfl_xor_sync(0xffffffffu, b2, o);
+        }
+        if (lane == 0) {
+          atomicAdd(&sm.bias_c2[0], b0);
+          atomicAdd(&sm.bias_c2[1], b1);
+          atomicAdd(&sm.bias_c2[2], b2);
+        }
+      }
+      to_mma();
+      // ---------------- S4: F4 | dH1, + dWc1 ----------------
+      issue2(warp, &sm.mbar,
+             [&] {
+               gemm_ts<64, 64>(tmem + TF_ACC, aF, sm.w.c1[0], sm.w.c1[1]);
+               gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.d1[0], sm.w.d1[1]);
+             },
+             [&] { gemm_wgrad_bias<HW, true>(tmem + TB_C1, sm.s[0], sm.s[1], sm.ones_b, sm.c1_lo, !fresh); });
+      pf.grad(m, part);  // next tile's upstream gradient
+      uint32_t n_relu, n_c2, n_clip;
+      float4 n_o;
+      load_fwd(nx, has_next, n_relu, n_c2, n_clip, n_o);
+      mma_done();
+      // G2 -> cin tile for dWd1 (dWc0 has read cin), before G1 overwrites its A_B columns
+      if (part == 0) a_to_smem16(taB, row, 0, sm.cin_hi, sm.cin_lo);
+      {
+        float v[16];
+        ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bc1[c16 + i], 0.f);
+        // C2 feeds only dWc2 (its smem tile; dWc0 has read G3 from it)
+        put8s(sm.c2[0], sm.c2[1], row, c16, v);
+        put8s(sm.c2[0], sm.c2[1], row, c16 + 8, v + 8);
+        ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
+        mask16(v, mk_relu & 0xffffu);  // h1 bits
+        put8(bT, row, c16, v);
+        put8(bT, row, c16 + 8, v + 8);
+      }
+      to_mma();
+      // ---------------- S5: dX, + dWc2, dWd1 ----------------
+      issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 32, 64>(tmem + TB_ACC, aB, sm.w.d0[0], sm.w.d0[1]); },
+             [&] {
+               // dWc2 transposed: D[64 C2 features x 16] = C2^T G5
+               gemm_wgrad<16>(tmem + TD_C2, sm.c2[0], sm.c2[1], sm.g5[0], sm.g5[1], !fresh);
+               // G2's 16 columns from the cin tile (the M = 64 operand's rows 16-63 are unused)
+               gemm_wgrad_bias<HW, true>(tmem + TB_D1, sm.cin_hi, sm.cin_lo, sm.ones_a, sm.h1_lo, !fresh);
+             });
+      mma_done();
+      {  // dX -> global, level-major
+        float v[8];
+        tc::tmem_ld8(my_lanes + TB_ACC + (uint32_t)(part * 8), v);
+        tc::tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int l = part * 4 + j;
+            if (l < (int)m.levels)
+              __stcs(reinterpret_cast<float2*>(m.dX) + (uint64_t)l * m.x_stride + gs,
+                     make_float2(v[2 * j], v[2 * j + 1]));
+          }
+        }
+      }
+      a_to_smem16(taB, row, c16, sm.s[0], sm.s[1]);  // G1 -> s for dWd0 (dWc1 has read G4)
+      to_mma();
+      // tail: dWd0 without a commit of its own: the next stage's commit (or the flush's) covers it
+      if (warp == 0) {
+        if (tc::elect_one())
+          gemm_wgrad_bias<XW, false>(tmem + TD_D0, sm.s[0], sm.s[1], sm.x_hi, sm.x_lo, !fresh);
+        __syncwarp();
+      }
+      fresh = false;
+      if (!has_next || nx.f != loaded) {  // the weight-gradient GEMMs must land before a flush
+        issue2(warp, &sm.mbar, [] {}, [] {});
+        mma_done();
+      }
+      if (!has_next) break;
+      if (nx.f != loaded) {
+        flush_all(tmem, m.fields[loaded], m.grads, sm.bias_c2);
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (m.fields[nx.f].coarse) __trap();
+        stage_weights_tc(m.fields[nx.f], m.params, sm.w);
+        loaded = nx.f;
+        fresh = true;
+      }
+      mk_relu = n_relu;
+      mk_c2 = n_c2;
+      mk_clip = n_clip;
+      o_fwd = n_o;
+      tile = next;
+      cur = nx;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (loaded >= 0) flush_all(tmem, m.fields[loaded], m.grads, sm.bias_c2);
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tmem, 512);
+}
+
 }  // namespace
 
 void launch_mlp_fwd_tc(const MlpLaunch& m, int num_sms, cudaStream_t s) {
@@ -1405,10 +1754,15 @@ void launch_mlp_bwd_tc(const MlpLaunch& m0, int num_sms, cudaStream_t s) {
   const int smem = (int)sizeof(BwdTcSmem);  // no-swizzle operands need 16-byte alignment only
   if (!attr) {
     cudaFuncSetAttribute(k_mlp_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_mlp_bwd_tc_relu, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  const unsigned grid = m.n_tiles < (uint32_t)num_sms ? m.n_tiles : (uint32_t)num_sms;
-  k_mlp_bwd_tc<<<grid, NTB, smem, s>>>(m);
+  // the leading ReLU-field tiles take the paired kernel (DG_MLP_BWD_SERIAL=1: all serial)
+  static const bool serial = std::getenv("DG_MLP_BWD_SERIAL") != nullptr;
+  const uint32_t split = serial ? 0u : std::min(m.relu_tiles, m.n_tiles);
+  auto grid_of = [&](uint32_t n) { return (unsigned)std::min<uint32_t>(n, (uint32_t)num_sms); };
+  if (split) k_mlp_bwd_tc_relu<<<grid_of(split), NTB, smem, s>>>(m, 0u, split);
+  if (split < m.n_tiles) k_mlp_bwd_tc<<<grid_of(m.n_tiles - split), NTB, smem, s>>>(m, split, m.n_tiles);
 }
 
 }  // namespace dg

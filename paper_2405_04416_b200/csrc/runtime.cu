@@ -1046,6 +1046,7 @@ MlpLaunch mlp_launch(dg_ctx* c, bool bwd) {
   for (uint32_t f = 0; f < 2 * nl; ++f) {
     const uint32_t cnt = c->field_off[f + 1] - c->field_off[f];
     tiles += bwd ? (cnt + 63) / 64 : (cnt + 127) / 128;
+    if (f + 1 == nl && !bwd) m.relu_tiles = tiles;  // fields 0..nl-1: fine (ReLU colour units)
   }
   m.tile_off = bwd ? c->tile_off_b.as<uint32_t>() : c->tile_off_f.as<uint32_t>();
   m.n_tiles = tiles;
@@ -2431,6 +2432,7 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
   m.n_tiles = tt[2 * nl];
   m.grad_in = gin.as<float4>();
   m.dX = dX.as<float>();
+  m.relu_tiles = cascade == 0 ? m.n_tiles : 0u;  // the fine field's colour units are ReLU
   if (c->mlp_impl) launch_mlp_bwd_tc(m, c->num_sms, s);
   else launch_mlp_bwd(m, c->num_sms, s);
   launch_encode_points_bwd(fd, c->grads.as<float>(), pts.as<double>(), dX.as<float>(), n, c->cfg.grid_levels, s);

@@ -1,0 +1,6 @@
+O=gpurun_out/pair1
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sample_parity.py -x -q > $O/t1.log 2>&1; echo rc=$? >> $O/t1.log
+timeout 300 python bench.py --steps 10 --warmup 3 > $O/bench_pair.log 2>&1; echo rc=$? >> $O/bench_pair.log
+DG_MLP_BWD_SERIAL=1 timeout 300 python bench.py --steps 10 --warmup 3 > $O/bench_serial.log 2>&1; echo rc=$? >> $O/bench_serial.log
