@@ -1381,15 +1381,19 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m, uint32_t t_l
 // recompute, which feeds only the weight gradients.  The two chains run as paired stages, each
 // with its own TMEM accumulator and A region, so a tile has 5 MMA waits instead of 9:
 //   S1  F1 = X Wd0^T      (-> H1 = relu)            | dC2 = G5 Wc2      (-> G4 = dC2 * c2 mask)
+//       + the previous tile's dWd0, dWd1
 //   S2  F2 = H1 Wd1^T     (-> raw -> Cin)           | dC1 = G4 Wc1      (-> G3 = dC1 * c1 mask)
 //   S3  F3 = Cin Wc0^T    (-> C1)                   | dCin = G3 Wc0     (-> G2)      + dWc0
 //   S4  F4 = C1 Wc1^T     (-> C2)                   | dH1 = G2 Wd1      (-> G1)      + dWc1
-//   S5                                              | dX = G1 Wd0                    + dWc2, dWd1
-//   tail: dWd0 (runs under the next tile's prologue)
-// G5 comes from the forward's stored outputs and clip flags (as in k_mlp_bwd_tc).  The
-// weight-gradient operand tiles rotate so that no in-flight GEMM's operand is overwritten:
-// G4 -> s, G3 -> c2, C2 -> c2 (after dWc0), G2 -> cin (after dWc0; copied out of the TMEM A
-// region at S4's epilogue), G1 -> s (after dWc1; copied out of TMEM at S5's epilogue).
+//   S5                                              | dX = G1 Wd0                    + dWc2
+// Every weight-gradient GEMM is issued behind a stage's critical GEMMs and runs under the
+// next epilogue.  G5 comes from the forward's stored outputs and clip flags (as in
+// k_mlp_bwd_tc).  Operand tiles are placed so that no in-flight GEMM's operand is
+// overwritten: two 64-column buffers (s, c2) swap roles every tile — A holds G4 then G1
+// (copied out of the TMEM A region at S5's epilogue), B holds G3 then C2 — and H1 / X reach
+// their smem tiles at S2's epilogue (H1 copied out of the TMEM A region before Cin replaces
+// it), G2 reaches the cin tile at S4's epilogue, after the previous tile's dWd0 / dWd1 and
+// this tile's dWc0 have read them.
 // Same arithmetic as k_mlp_bwd_tc (split-bf16 operands, fp32 TMEM accumulation, dW / db over
 // all of a CTA's tiles); only the issue order of the GEMMs differs.
 constexpr uint32_t TF_ACC = 0, TF_A = 64, TB_ACC = 128, TB_A = 192;
@@ -1445,9 +1449,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t aF = tmem + TF_A, aB = tmem + TB_A;            // A operands of the two chains
   const uint32_t taF = my_lanes + TF_A, taB = my_lanes + TB_A;  // this thread's lane of them
-  const Sink fX{nullptr, nullptr, taF}, fH1{sm.h1_hi, sm.h1_lo, taF}, fCin{sm.cin_hi, sm.cin_lo, taF};
-  const Sink fC1{sm.c1_hi, sm.c1_lo, taF};
-  const Sink bT{nullptr, nullptr, taB}, bG4{sm.s[0], sm.s[1], taB}, bG3{sm.c2[0], sm.c2[1], taB};
+  const Sink fT{nullptr, nullptr, taF}, fCin{sm.cin_hi, sm.cin_lo, taF}, fC1{sm.c1_hi, sm.c1_lo, taF};
+  const Sink bT{nullptr, nullptr, taB};
   if (part == 0) {  // G5's K columns 8-15 meet zero Wc2 rows: the region must start finite
     const uint32_t z[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -1492,8 +1495,22 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
     if (m.fields[cur.f].coarse) __trap();  // sigmoid fields take k_mlp_bwd_tc
     stage_weights_tc(m.fields[cur.f], m.params, sm.w);
     loaded = cur.f;
-    bool fresh = true;  // next dW GEMMs start a new accumulation
+    bool fresh = true;        // next dW GEMMs start a new accumulation
+    bool pend = false;        // the previous tile's dWd0 / dWd1 are still to be issued
+    bool pend_fresh = false;  // ... and start their accumulations
+    int par = 0;              // tile parity: which of s / c2 is buffer A (G4, G1) and B (G3, C2)
+    // the previous tile's dWd0 (G1 in its buffer A = this tile's B) and dWd1 (G2 in the cin tile)
+    auto issue_pending = [&](int p_prev) {
+      if (!pend) return;
+      auto g1 = p_prev ? sm.c2 : sm.s;
+      gemm_wgrad_bias<XW, false>(tmem + TD_D0, g1[0], g1[1], sm.x_hi, sm.x_lo, !pend_fresh);
+      // G2's 16 columns from the cin tile (the M = 64 operand's rows 16-63 are unused)
+      gemm_wgrad_bias<HW, true>(tmem + TB_D1, sm.cin_hi, sm.cin_lo, sm.ones_a, sm.h1_lo, !pend_fresh);
+    };
     for (;;) {
+      auto bufA = par ? sm.c2 : sm.s;
+      auto bufB = par ? sm.s : sm.c2;
+      const Sink bA{bufA[0], bufA[1], taB}, bB{bufB[0], bufB[1], taB};
       const bool valid = row < cur.count;
       const uint64_t gs = cur.s0 + row;
       const uint32_t next = tile + 1;
@@ -1505,7 +1522,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       const double d0 = pf.dir[0], d1 = pf.dir[1], d2 = pf.dir[2];
       const float4 up = pf.g;
       // ---------------- prologue: X -> A_F; G5 (colour-head adjoint, field.cpp:298-306) -> A_B
-      pf.put_x(fX, row, part);
+      pf.put_x(fT, row, part);
       float xk[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) xk[i] = pf.x[i];
@@ -1529,13 +1546,17 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         sm.gsig[row] = (dm & 1u) ? 0.f : up.x * o_fwd.x;
       }
       to_mma();
-      // ---------------- S1: F1 | dC2 ----------------
-      ISSUE(gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]);
-            gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]));
+      // ---------------- S1: F1 | dC2, + the previous tile's dWd0, dWd1 ----------------
+      issue2(warp, &sm.mbar,
+             [&] {
+               gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]);
+               gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]);
+             },
+             [&] { issue_pending(par ^ 1); });
+      pend = false;
       pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next: X, item
       mma_done();
       {
-        put8s(sm.x_hi, sm.x_lo, row, part * 8, xk);  // the previous tile's dWd0 is done
         if (part == 0) {  // G5 for dWc2 (the previous tile's dWc2 is done)
           float g[8] = {g5v[0], g5v[1], g5v[2], 0.f, 0.f, 0.f, 0.f, 0.f};
           put8s(sm.g5[0], sm.g5[1], row, 0, g);
@@ -1544,12 +1565,12 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[c16 + i], 0.f);
-        put8(fH1, row, c16, v);
-        put8(fH1, row, c16 + 8, v + 8);
+        put8(fT, row, c16, v);  // H1 -> A_F; its smem tile at S2 (the previous dWd1 reads h1)
+        put8(fT, row, c16 + 8, v + 8);
         ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
         mask16(v, (mk_c2 >> (((uint32_t)part & 1u) * 16u)) & 0xffffu);
-        put8(bG4, row, c16, v);
-        put8(bG4, row, c16 + 8, v + 8);
+        put8(bA, row, c16, v);  // G4 (buffer A held the previous tile's C2: dWc2 is done)
+        put8(bA, row, c16 + 8, v + 8);
       }
       to_mma();
       // ---------------- S2: F2 | dC1 ----------------
@@ -1557,6 +1578,10 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
             gemm_igrad<64, 64, 64>(tmem + TB_ACC, aB, sm.w.c1[0], sm.w.c1[1]));
       pf.rec(m, part);  // next tile's RayRec
       mma_done();
+      // the previous tile's dWd0 / dWd1 are done: X and H1 to their smem tiles (H1 out of A_F
+      // before Cin replaces it: this thread's Cin columns are its H1 columns)
+      put8s(sm.x_hi, sm.x_lo, row, part * 8, xk);
+      a_to_smem16(taF, row, c16, sm.h1_hi, sm.h1_lo);
       {
         float raw[16];
         if (part == 0) {
@@ -1578,8 +1603,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         float v[16];
         ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
         mask16(v, mk_relu >> 16);  // c1 bits of this part's columns
-        put8(bG3, row, c16, v);
-        put8(bG3, row, c16 + 8, v + 8);
+        put8(bB, row, c16, v);  // G3 (buffer B held the previous tile's G1: dWd0 is done)
+        put8(bB, row, c16 + 8, v + 8);
       }
       to_mma();
       // ---------------- S3: F3 | dCin, + dWc0 ----------------
@@ -1588,7 +1613,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
                gemm_ts<64, 48>(tmem + TF_ACC, aF, sm.w.c0[0], sm.w.c0[1]);
                gemm_igrad<64, 16, 64>(tmem + TB_ACC, aB, sm.w.c0[0], sm.w.c0[1]);
              },
-             [&] { gemm_wgrad_bias<CW, false>(tmem + TD_C0, sm.c2[0], sm.c2[1], sm.cin_hi, sm.cin_lo, !fresh); });
+             [&] { gemm_wgrad_bias<CW, false>(tmem + TD_C0, bufB[0], bufB[1], sm.cin_hi, sm.cin_lo, !fresh); });
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
       mma_done();
       {
@@ -1632,7 +1657,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
                gemm_ts<64, 64>(tmem + TF_ACC, aF, sm.w.c1[0], sm.w.c1[1]);
                gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.d1[0], sm.w.d1[1]);
              },
-             [&] { gemm_wgrad_bias<HW, true>(tmem + TB_C1, sm.s[0], sm.s[1], sm.ones_b, sm.c1_lo, !fresh); });
+             [&] { gemm_wgrad_bias<HW, true>(tmem + TB_C1, bufA[0], bufA[1], sm.ones_b, sm.c1_lo, !fresh); });
       pf.grad(m, part);  // next tile's upstream gradient
       uint32_t n_relu, n_c2, n_clip;
       float4 n_o;
@@ -1645,23 +1670,19 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bc1[c16 + i], 0.f);
-        // C2 feeds only dWc2 (its smem tile; dWc0 has read G3 from it)
-        put8s(sm.c2[0], sm.c2[1], row, c16, v);
-        put8s(sm.c2[0], sm.c2[1], row, c16 + 8, v + 8);
+        // C2 feeds only dWc2 (its smem tile in buffer B: dWc0 has read G3 from it)
+        put8s(bufB[0], bufB[1], row, c16, v);
+        put8s(bufB[0], bufB[1], row, c16 + 8, v + 8);
         ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
         mask16(v, mk_relu & 0xffffu);  // h1 bits
         put8(bT, row, c16, v);
         put8(bT, row, c16 + 8, v + 8);
       }
       to_mma();
-      // ---------------- S5: dX, + dWc2, dWd1 ----------------
+      // ---------------- S5: dX, + dWc2 ----------------
       issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 32, 64>(tmem + TB_ACC, aB, sm.w.d0[0], sm.w.d0[1]); },
-             [&] {
-               // dWc2 transposed: D[64 C2 features x 16] = C2^T G5
-               gemm_wgrad<16>(tmem + TD_C2, sm.c2[0], sm.c2[1], sm.g5[0], sm.g5[1], !fresh);
-               // G2's 16 columns from the cin tile (the M = 64 operand's rows 16-63 are unused)
-               gemm_wgrad_bias<HW, true>(tmem + TB_D1, sm.cin_hi, sm.cin_lo, sm.ones_a, sm.h1_lo, !fresh);
-             });
+             // dWc2 transposed: D[64 C2 features x 16] = C2^T G5
+             [&] { gemm_wgrad<16>(tmem + TD_C2, bufB[0], bufB[1], sm.g5[0], sm.g5[1], !fresh); });
       mma_done();
       {  // dX -> global, level-major
         float v[8];
@@ -1677,17 +1698,15 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
           }
         }
       }
-      a_to_smem16(taB, row, c16, sm.s[0], sm.s[1]);  // G1 -> s for dWd0 (dWc1 has read G4)
-      to_mma();
-      // tail: dWd0 without a commit of its own: the next stage's commit (or the flush's) covers it
-      if (warp == 0) {
-        if (tc::elect_one())
-          gemm_wgrad_bias<XW, false>(tmem + TD_D0, sm.s[0], sm.s[1], sm.x_hi, sm.x_lo, !fresh);
-        __syncwarp();
-      }
+      a_to_smem16(taB, row, c16, bufA[0], bufA[1]);  // G1 -> buffer A (dWc1 has read G4)
+      pend = true;  // dWd0 / dWd1 go behind the next tile's first critical GEMMs
+      pend_fresh = fresh;
       fresh = false;
-      if (!has_next || nx.f != loaded) {  // the weight-gradient GEMMs must land before a flush
-        issue2(warp, &sm.mbar, [] {}, [] {});
+      par ^= 1;
+      if (!has_next || nx.f != loaded) {  // every weight-gradient GEMM must land before a flush
+        to_mma();
+        issue2(warp, &sm.mbar, [&] { issue_pending(par ^ 1); }, [] {});  // the commit covers all
+        pend = false;
         mma_done();
       }
       if (!has_next) break;
