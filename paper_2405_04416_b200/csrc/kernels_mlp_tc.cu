@@ -1430,6 +1430,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
   const int quad = warp & 3, part = warp >> 2;
   const int row = quad * 32 + lane;
   const int c16 = part * 16;  // this thread's 16 columns of a 64-wide layer
+  // MMAs are issued from warp 12 (part 3)
+  const int iw = warp == 12 ? 0 : 1;
   if (warp == 0) tc::tmem_alloc(&sm.tslot, 512);
   if (tid == 0) {
     tc::mbar_init(&sm.mbar, 1);
@@ -1547,7 +1549,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S1: F1 | dC2, + the previous tile's dWd0, dWd1 ----------------
-      issue2(warp, &sm.mbar,
+      issue2(iw, &sm.mbar,
              [&] {
                gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]);
                gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]);
@@ -1574,17 +1576,24 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S2: F2 | dC1 ----------------
-      ISSUE(gemm_ts<16, 64>(tmem + TF_ACC, aF, sm.w.d1[0], sm.w.d1[1]);
-            gemm_igrad<64, 64, 64>(tmem + TB_ACC, aB, sm.w.c1[0], sm.w.c1[1]));
+      issue2(iw, &sm.mbar,
+             [&] {
+               gemm_ts<16, 64>(tmem + TF_ACC, aF, sm.w.d1[0], sm.w.d1[1]);
+               gemm_igrad<64, 64, 64>(tmem + TB_ACC, aB, sm.w.c1[0], sm.w.c1[1]);
+             },
+             [] {});
       pf.rec(m, part);  // next tile's RayRec
       mma_done();
-      // the previous tile's dWd0 / dWd1 are done: X and H1 to their smem tiles (H1 out of A_F
-      // before Cin replaces it: this thread's Cin columns are its H1 columns)
+      // the previous tile's dWd0 / dWd1 are done: X and H1 to their smem tiles.  Cin column
+      // parts: part 3 the density outputs (cols 0-15), parts 1 / 2 SH / appearance (16-47),
+      // part 0 none (it builds G5 and copies G2 in other epilogues); each thread first copies
+      // the H1 columns (out of A_F) that its Cin columns replace
+      const int cpart = part == 3 ? 0 : (part == 0 ? 3 : part);
       put8s(sm.x_hi, sm.x_lo, row, part * 8, xk);
-      a_to_smem16(taF, row, c16, sm.h1_hi, sm.h1_lo);
+      a_to_smem16(taF, row, cpart * 16, sm.h1_hi, sm.h1_lo);
       {
         float raw[16];
-        if (part == 0) {
+        if (cpart == 0) {
           ld16(my_lanes + TF_ACC, raw);
 #pragma unroll
           for (int i = 0; i < 16; ++i) raw[i] = clip15(raw[i] + sm.w.bd1[i]);
@@ -1597,7 +1606,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         cp.dir[2] = d2;
 #pragma unroll
         for (int i = 0; i < 17; ++i) cp.app[i] = cur_app[i];
-        cp.put_cin(fCin, row, part, raw);
+        cp.put_cin(fCin, row, cpart, raw);
       }
       {
         float v[16];
@@ -1608,7 +1617,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S3: F3 | dCin, + dWc0 ----------------
-      issue2(warp, &sm.mbar,
+      issue2(iw, &sm.mbar,
              [&] {
                gemm_ts<64, 48>(tmem + TF_ACC, aF, sm.w.c0[0], sm.w.c0[1]);
                gemm_igrad<64, 16, 64>(tmem + TB_ACC, aB, sm.w.c0[0], sm.w.c0[1]);
@@ -1624,7 +1633,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         put8(fC1, row, c16, v);
         put8(fC1, row, c16 + 8, v + 8);
       }
-      if (part == 0) {  // G2 = [sigma path, clip-masked dCin[0..14]] -> A_B (smem copy at S4)
+      if (part == 3) {  // G2 = [sigma path, clip-masked dCin[0..14]] -> A_B (smem copy at S4)
         float v[16];
         ld16(my_lanes + TB_ACC, v);
         const uint32_t mask = sm.dmask[row];
@@ -1652,7 +1661,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S4: F4 | dH1, + dWc1 ----------------
-      issue2(warp, &sm.mbar,
+      issue2(iw, &sm.mbar,
              [&] {
                gemm_ts<64, 64>(tmem + TF_ACC, aF, sm.w.c1[0], sm.w.c1[1]);
                gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.d1[0], sm.w.d1[1]);
@@ -1680,7 +1689,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S5: dX, + dWc2 ----------------
-      issue2(warp, &sm.mbar, [&] { gemm_igrad<64, 32, 64>(tmem + TB_ACC, aB, sm.w.d0[0], sm.w.d0[1]); },
+      issue2(iw, &sm.mbar, [&] { gemm_igrad<64, 32, 64>(tmem + TB_ACC, aB, sm.w.d0[0], sm.w.d0[1]); },
              // dWc2 transposed: D[64 C2 features x 16] = C2^T G5
              [&] { gemm_wgrad<16>(tmem + TD_C2, bufB[0], bufB[1], sm.g5[0], sm.g5[1], !fresh); });
       mma_done();
@@ -1705,7 +1714,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       par ^= 1;
       if (!has_next || nx.f != loaded) {  // every weight-gradient GEMM must land before a flush
         to_mma();
-        issue2(warp, &sm.mbar, [&] { issue_pending(par ^ 1); }, [] {});  // the commit covers all
+        issue2(iw, &sm.mbar, [&] { issue_pending(par ^ 1); }, [] {});  // the commit covers all
         pend = false;
         mma_done();
       }
