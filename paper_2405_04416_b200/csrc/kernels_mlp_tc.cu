@@ -909,6 +909,7 @@ struct BwdTcSmem {
   float gsig[TM];
   uint32_t dmask[TM];
   uint64_t mbar;
+  uint64_t mbar_b;  // k_mlp_bwd_tc_relu: completion of the input-gradient chain's GEMMs
   uint32_t tslot;
 };
 
@@ -1435,6 +1436,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
   if (warp == 0) tc::tmem_alloc(&sm.tslot, 512);
   if (tid == 0) {
     tc::mbar_init(&sm.mbar, 1);
+    tc::mbar_init(&sm.mbar_b, 1);
     tc::fence_mbar_init();
   }
   for (int r = tid; r < TM; r += NTB) {
@@ -1461,11 +1463,42 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       tc::tmem_st4(taB + A_LO_OFF + (uint32_t)c, z);
     }
   }
-  uint32_t phase = 0;
-  auto mma_done = [&]() {
+  // Each stage commits its forward-recompute GEMM and its input-gradient GEMM to separate
+  // mbarriers (sm.mbar, sm.mbar_b): the recompute's epilogue starts while the input-gradient
+  // GEMM still runs.  A commit covers every earlier tcgen05 op of the issuing thread.
+  uint32_t phase = 0, phase_b = 0;
+  auto done_f = [&]() {
     tc::mbar_wait(&sm.mbar, phase);
     phase ^= 1u;
     tc::fence_after();
+  };
+  auto done_b = [&]() {
+    tc::mbar_wait(&sm.mbar_b, phase_b);
+    phase_b ^= 1u;
+    tc::fence_after();
+  };
+  // stage issue from warp 12: recompute GEMM, commit, input-gradient GEMM, commit, background
+  auto issue3 = [&](auto fwd, auto bwd, auto back) {
+    if (iw == 0) {
+      if (tc::elect_one()) {
+        fwd();
+        tc::commit(&sm.mbar);
+        bwd();
+        tc::commit(&sm.mbar_b);
+        back();
+      }
+      __syncwarp();
+    }
+  };
+  auto issue_b = [&](auto bwd, auto back) {
+    if (iw == 0) {
+      if (tc::elect_one()) {
+        bwd();
+        tc::commit(&sm.mbar_b);
+        back();
+      }
+      __syncwarp();
+    }
   };
   // the forward's masks / outputs of a tile row (see k_mlp_fwd_tc for the word layout)
   auto load_fwd = [&](const TileGeo& g, bool ok, uint32_t& relu, uint32_t& c2, uint32_t& clip, float4& o) {
@@ -1549,15 +1582,12 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S1: F1 | dC2, + the previous tile's dWd0, dWd1 ----------------
-      issue2(iw, &sm.mbar,
-             [&] {
-               gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]);
-               gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]);
-             },
+      issue3([&] { gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]); },
+             [&] { gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]); },
              [&] { issue_pending(par ^ 1); });
       pend = false;
       pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next: X, item
-      mma_done();
+      done_f();
       {
         if (part == 0) {  // G5 for dWc2 (the previous tile's dWc2 is done)
           float g[8] = {g5v[0], g5v[1], g5v[2], 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -1569,6 +1599,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[c16 + i], 0.f);
         put8(fT, row, c16, v);  // H1 -> A_F; its smem tile at S2 (the previous dWd1 reads h1)
         put8(fT, row, c16 + 8, v + 8);
+        done_b();
         ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
         mask16(v, (mk_c2 >> (((uint32_t)part & 1u) * 16u)) & 0xffffu);
         put8(bA, row, c16, v);  // G4 (buffer A held the previous tile's C2: dWc2 is done)
@@ -1576,14 +1607,10 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S2: F2 | dC1 ----------------
-      issue2(iw, &sm.mbar,
-             [&] {
-               gemm_ts<16, 64>(tmem + TF_ACC, aF, sm.w.d1[0], sm.w.d1[1]);
-               gemm_igrad<64, 64, 64>(tmem + TB_ACC, aB, sm.w.c1[0], sm.w.c1[1]);
-             },
-             [] {});
+      issue3([&] { gemm_ts<16, 64>(tmem + TF_ACC, aF, sm.w.d1[0], sm.w.d1[1]); },
+             [&] { gemm_igrad<64, 64, 64>(tmem + TB_ACC, aB, sm.w.c1[0], sm.w.c1[1]); }, [] {});
       pf.rec(m, part);  // next tile's RayRec
-      mma_done();
+      done_f();
       // the previous tile's dWd0 / dWd1 are done: X and H1 to their smem tiles.  Cin column
       // parts: part 3 the density outputs (cols 0-15), parts 1 / 2 SH / appearance (16-47),
       // part 0 none (it builds G5 and copies G2 in other epilogues); each thread first copies
@@ -1608,6 +1635,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         for (int i = 0; i < 17; ++i) cp.app[i] = cur_app[i];
         cp.put_cin(fCin, row, cpart, raw);
       }
+      done_b();
       {
         float v[16];
         ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
@@ -1617,14 +1645,11 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S3: F3 | dCin, + dWc0 ----------------
-      issue2(iw, &sm.mbar,
-             [&] {
-               gemm_ts<64, 48>(tmem + TF_ACC, aF, sm.w.c0[0], sm.w.c0[1]);
-               gemm_igrad<64, 16, 64>(tmem + TB_ACC, aB, sm.w.c0[0], sm.w.c0[1]);
-             },
+      issue3([&] { gemm_ts<64, 48>(tmem + TF_ACC, aF, sm.w.c0[0], sm.w.c0[1]); },
+             [&] { gemm_igrad<64, 16, 64>(tmem + TB_ACC, aB, sm.w.c0[0], sm.w.c0[1]); },
              [&] { gemm_wgrad_bias<CW, false>(tmem + TD_C0, bufB[0], bufB[1], sm.cin_hi, sm.cin_lo, !fresh); });
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
-      mma_done();
+      done_f();
       {
         float v[16];
         ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
@@ -1633,6 +1658,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         put8(fC1, row, c16, v);
         put8(fC1, row, c16 + 8, v + 8);
       }
+      done_b();
       if (part == 3) {  // G2 = [sigma path, clip-masked dCin[0..14]] -> A_B (smem copy at S4)
         float v[16];
         ld16(my_lanes + TB_ACC, v);
@@ -1661,17 +1687,14 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S4: F4 | dH1, + dWc1 ----------------
-      issue2(iw, &sm.mbar,
-             [&] {
-               gemm_ts<64, 64>(tmem + TF_ACC, aF, sm.w.c1[0], sm.w.c1[1]);
-               gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.d1[0], sm.w.d1[1]);
-             },
+      issue3([&] { gemm_ts<64, 64>(tmem + TF_ACC, aF, sm.w.c1[0], sm.w.c1[1]); },
+             [&] { gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.d1[0], sm.w.d1[1]); },
              [&] { gemm_wgrad_bias<HW, true>(tmem + TB_C1, bufA[0], bufA[1], sm.ones_b, sm.c1_lo, !fresh); });
       pf.grad(m, part);  // next tile's upstream gradient
       uint32_t n_relu, n_c2, n_clip;
       float4 n_o;
       load_fwd(nx, has_next, n_relu, n_c2, n_clip, n_o);
-      mma_done();
+      done_f();
       // G2 -> cin tile for dWd1 (dWc0 has read cin), before G1 overwrites its A_B columns
       if (part == 0) a_to_smem16(taB, row, 0, sm.cin_hi, sm.cin_lo);
       {
@@ -1682,6 +1705,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         // C2 feeds only dWc2 (its smem tile in buffer B: dWc0 has read G3 from it)
         put8s(bufB[0], bufB[1], row, c16, v);
         put8s(bufB[0], bufB[1], row, c16 + 8, v + 8);
+        done_b();
         ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
         mask16(v, mk_relu & 0xffffu);  // h1 bits
         put8(bT, row, c16, v);
@@ -1689,10 +1713,10 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S5: dX, + dWc2 ----------------
-      issue2(iw, &sm.mbar, [&] { gemm_igrad<64, 32, 64>(tmem + TB_ACC, aB, sm.w.d0[0], sm.w.d0[1]); },
+      issue_b([&] { gemm_igrad<64, 32, 64>(tmem + TB_ACC, aB, sm.w.d0[0], sm.w.d0[1]); },
              // dWc2 transposed: D[64 C2 features x 16] = C2^T G5
              [&] { gemm_wgrad<16>(tmem + TD_C2, bufB[0], bufB[1], sm.g5[0], sm.g5[1], !fresh); });
-      mma_done();
+      done_b();
       {  // dX -> global, level-major
         float v[8];
         tc::tmem_ld8(my_lanes + TB_ACC + (uint32_t)(part * 8), v);
@@ -1714,9 +1738,9 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       par ^= 1;
       if (!has_next || nx.f != loaded) {  // every weight-gradient GEMM must land before a flush
         to_mma();
-        issue2(iw, &sm.mbar, [&] { issue_pending(par ^ 1); }, [] {});  // the commit covers all
+        issue_b([&] { issue_pending(par ^ 1); }, [] {});  // the commit covers all
         pend = false;
-        mma_done();
+        done_b();
       }
       if (!has_next) break;
       if (nx.f != loaded) {
