@@ -17,7 +17,6 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "dg_common.cuh"
 #include "kernels.h"
@@ -1382,19 +1381,18 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc(MlpLaunch m, uint32_t t_l
 // recompute, which feeds only the weight gradients.  The two chains run as paired stages, each
 // with its own TMEM accumulator and A region, so a tile has 5 MMA waits instead of 9:
 //   S1  F1 = X Wd0^T      (-> H1 = relu)            | dC2 = G5 Wc2      (-> G4 = dC2 * c2 mask)
-//       + the previous tile's dWd0, dWd1
+//       + the previous tile's dWd0
 //   S2  F2 = H1 Wd1^T     (-> raw -> Cin)           | dC1 = G4 Wc1      (-> G3 = dC1 * c1 mask)
 //   S3  F3 = Cin Wc0^T    (-> C1)                   | dCin = G3 Wc0     (-> G2)      + dWc0
 //   S4  F4 = C1 Wc1^T     (-> C2)                   | dH1 = G2 Wd1      (-> G1)      + dWc1
-//   S5                                              | dX = G1 Wd0                    + dWc2
+//   S5                                              | dX = G1 Wd0                    + dWc2, dWd1
 // Every weight-gradient GEMM is issued behind a stage's critical GEMMs and runs under the
 // next epilogue.  G5 comes from the forward's stored outputs and clip flags (as in
 // k_mlp_bwd_tc).  Operand tiles are placed so that no in-flight GEMM's operand is
 // overwritten: two 64-column buffers (s, c2) swap roles every tile — A holds G4 then G1
-// (copied out of the TMEM A region at S5's epilogue), B holds G3 then C2 — and H1 / X reach
-// their smem tiles at S2's epilogue (H1 copied out of the TMEM A region before Cin replaces
-// it), G2 reaches the cin tile at S4's epilogue, after the previous tile's dWd0 / dWd1 and
-// this tile's dWc0 have read them.
+// (copied out of the TMEM A region at S5's epilogue), B holds G3 then C2 — X reaches its smem
+// tile at S2's epilogue (after the previous tile's dWd0), and G2 the cin tile at S4's
+// epilogue (copied out of the TMEM A region, after dWc0 has read Cin).
 // Same arithmetic as k_mlp_bwd_tc (split-bf16 operands, fp32 TMEM accumulation, dW / db over
 // all of a CTA's tiles); only the issue order of the GEMMs differs.
 constexpr uint32_t TF_ACC = 0, TF_A = 64, TB_ACC = 128, TB_A = 192;
@@ -1453,7 +1451,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
   const uint32_t my_lanes = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t aF = tmem + TF_A, aB = tmem + TB_A;            // A operands of the two chains
   const uint32_t taF = my_lanes + TF_A, taB = my_lanes + TB_A;  // this thread's lane of them
-  const Sink fT{nullptr, nullptr, taF}, fCin{sm.cin_hi, sm.cin_lo, taF}, fC1{sm.c1_hi, sm.c1_lo, taF};
+  const Sink fT{nullptr, nullptr, taF}, fH1{sm.h1_hi, sm.h1_lo, taF}, fCin{sm.cin_hi, sm.cin_lo, taF};
+  const Sink fC1{sm.c1_hi, sm.c1_lo, taF};
   const Sink bT{nullptr, nullptr, taB};
   if (part == 0) {  // G5's K columns 8-15 meet zero Wc2 rows: the region must start finite
     const uint32_t z[4] = {0u, 0u, 0u, 0u};
@@ -1531,16 +1530,14 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
     stage_weights_tc(m.fields[cur.f], m.params, sm.w);
     loaded = cur.f;
     bool fresh = true;        // next dW GEMMs start a new accumulation
-    bool pend = false;        // the previous tile's dWd0 / dWd1 are still to be issued
-    bool pend_fresh = false;  // ... and start their accumulations
+    bool pend = false;        // the previous tile's dWd0 is still to be issued
+    bool pend_fresh = false;  // ... and starts its accumulation
     int par = 0;              // tile parity: which of s / c2 is buffer A (G4, G1) and B (G3, C2)
-    // the previous tile's dWd0 (G1 in its buffer A = this tile's B) and dWd1 (G2 in the cin tile)
+    // the previous tile's dWd0 (G1 in its buffer A = this tile's B)
     auto issue_pending = [&](int p_prev) {
       if (!pend) return;
       auto g1 = p_prev ? sm.c2 : sm.s;
       gemm_wgrad_bias<XW, false>(tmem + TD_D0, g1[0], g1[1], sm.x_hi, sm.x_lo, !pend_fresh);
-      // G2's 16 columns from the cin tile (the M = 64 operand's rows 16-63 are unused)
-      gemm_wgrad_bias<HW, true>(tmem + TB_D1, sm.cin_hi, sm.cin_lo, sm.ones_a, sm.h1_lo, !pend_fresh);
     };
     for (;;) {
       auto bufA = par ? sm.c2 : sm.s;
@@ -1581,7 +1578,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         sm.gsig[row] = (dm & 1u) ? 0.f : up.x * o_fwd.x;
       }
       to_mma();
-      // ---------------- S1: F1 | dC2, + the previous tile's dWd0, dWd1 ----------------
+      // ---------------- S1: F1 | dC2, + the previous tile's dWd0 ----------------
       issue3([&] { gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]); },
              [&] { gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]); },
              [&] { issue_pending(par ^ 1); });
@@ -1597,8 +1594,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[c16 + i], 0.f);
-        put8(fT, row, c16, v);  // H1 -> A_F; its smem tile at S2 (the previous dWd1 reads h1)
-        put8(fT, row, c16 + 8, v + 8);
+        put8(fH1, row, c16, v);  // the previous tile's dWd1 is done
+        put8(fH1, row, c16 + 8, v + 8);
         done_b();
         ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
         mask16(v, (mk_c2 >> (((uint32_t)part & 1u) * 16u)) & 0xffffu);
@@ -1611,13 +1608,11 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
              [&] { gemm_igrad<64, 64, 64>(tmem + TB_ACC, aB, sm.w.c1[0], sm.w.c1[1]); }, [] {});
       pf.rec(m, part);  // next tile's RayRec
       done_f();
-      // the previous tile's dWd0 / dWd1 are done: X and H1 to their smem tiles.  Cin column
-      // parts: part 3 the density outputs (cols 0-15), parts 1 / 2 SH / appearance (16-47),
-      // part 0 none (it builds G5 and copies G2 in other epilogues); each thread first copies
-      // the H1 columns (out of A_F) that its Cin columns replace
+      // the previous tile's dWd0 is done: X to its smem tile.  Cin column parts: part 3 the
+      // density outputs (cols 0-15), parts 1 / 2 SH / appearance (16-47), part 0 none (it
+      // builds G5 and copies G2 in other epilogues)
       const int cpart = part == 3 ? 0 : (part == 0 ? 3 : part);
       put8s(sm.x_hi, sm.x_lo, row, part * 8, xk);
-      a_to_smem16(taF, row, cpart * 16, sm.h1_hi, sm.h1_lo);
       {
         float raw[16];
         if (cpart == 0) {
@@ -1712,10 +1707,14 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         put8(bT, row, c16 + 8, v + 8);
       }
       to_mma();
-      // ---------------- S5: dX, + dWc2 ----------------
+      // ---------------- S5: dX, + dWc2, dWd1 ----------------
       issue_b([&] { gemm_igrad<64, 32, 64>(tmem + TB_ACC, aB, sm.w.d0[0], sm.w.d0[1]); },
-             // dWc2 transposed: D[64 C2 features x 16] = C2^T G5
-             [&] { gemm_wgrad<16>(tmem + TD_C2, bufB[0], bufB[1], sm.g5[0], sm.g5[1], !fresh); });
+              [&] {
+                // dWc2 transposed: D[64 C2 features x 16] = C2^T G5
+                gemm_wgrad<16>(tmem + TD_C2, bufB[0], bufB[1], sm.g5[0], sm.g5[1], !fresh);
+                // G2's 16 columns from the cin tile (the M = 64 operand's rows 16-63 are unused)
+                gemm_wgrad_bias<HW, true>(tmem + TB_D1, sm.cin_hi, sm.cin_lo, sm.ones_a, sm.h1_lo, !fresh);
+              });
       done_b();
       {  // dX -> global, level-major
         float v[8];
@@ -1732,7 +1731,7 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
         }
       }
       a_to_smem16(taB, row, c16, bufA[0], bufA[1]);  // G1 -> buffer A (dWc1 has read G4)
-      pend = true;  // dWd0 / dWd1 go behind the next tile's first critical GEMMs
+      pend = true;  // dWd0 goes behind the next tile's first critical GEMMs
       pend_fresh = fresh;
       fresh = false;
       par ^= 1;
@@ -1809,9 +1808,9 @@ void launch_mlp_bwd_tc(const MlpLaunch& m0, int num_sms, cudaStream_t s) {
     cudaFuncSetAttribute(k_mlp_bwd_tc_relu, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  // the leading ReLU-field tiles take the paired kernel (DG_MLP_BWD_SERIAL=1: all serial)
-  static const bool serial = std::getenv("DG_MLP_BWD_SERIAL") != nullptr;
-  const uint32_t split = serial ? 0u : std::min(m.relu_tiles, m.n_tiles);
+  // the leading ReLU-field tiles take the paired kernel (the context's DG_MLP_BWD_SERIAL=1
+  // leaves relu_tiles at 0: every tile the serial kernel)
+  const uint32_t split = std::min(m.relu_tiles, m.n_tiles);
   auto grid_of = [&](uint32_t n) { return (unsigned)std::min<uint32_t>(n, (uint32_t)num_sms); };
   if (split) k_mlp_bwd_tc_relu<<<grid_of(split), NTB, smem, s>>>(m, 0u, split);
   if (split < m.n_tiles) k_mlp_bwd_tc<<<grid_of(m.n_tiles - split), NTB, smem, s>>>(m, split, m.n_tiles);
