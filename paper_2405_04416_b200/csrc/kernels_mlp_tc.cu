@@ -1429,8 +1429,8 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
   const int quad = warp & 3, part = warp >> 2;
   const int row = quad * 32 + lane;
   const int c16 = part * 16;  // this thread's 16 columns of a 64-wide layer
-  // MMAs are issued from warp 12 (part 3)
-  const int iw = warp == 12 ? 0 : 1;
+  // MMAs are issued from warp m.issue_warp (default 8: part 2, the lightest epilogues)
+  const int iw = warp == (int)m.issue_warp ? 0 : 1;
   if (warp == 0) tc::tmem_alloc(&sm.tslot, 512);
   if (tid == 0) {
     tc::mbar_init(&sm.mbar, 1);
