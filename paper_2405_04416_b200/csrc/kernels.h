@@ -196,6 +196,7 @@ struct MlpLaunch {
   uint32_t relu_tiles;         // bwd (tc): the leading tiles of ReLU (fine) fields, which take the
                                // paired kernel k_mlp_bwd_tc_relu; 0: every tile the serial one
   uint32_t issue_warp;         // k_mlp_bwd_tc_relu: the warp whose elected lane issues the MMAs
+  uint32_t issue_warp_fwd;     // k_mlp_fwd_tc: the same (0-7)
   const float* X;              // level-major [levels][x_stride] float2
   uint64_t x_stride;           // samples per level row of X / dX
   uint32_t levels;

@@ -366,6 +366,18 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
     }                                   \
   } while (0)
 
+// The same from warp `w`.
+#define ISSUE_W(w, ...)                 \
+  do {                                  \
+    if (warp == (w)) {                  \
+      if (tc::elect_one()) {            \
+        __VA_ARGS__;                    \
+        tc::commit(&sm.mbar);           \
+      }                                 \
+      __syncwarp();                     \
+    }                                   \
+  } while (0)
+
 // Critical MMAs, their commit (the next epilogue waits for it), then background MMAs whose
 // completion a later commit covers (commit tracks every earlier tcgen05 op of the thread).
 template <class Crit, class Back>
@@ -494,6 +506,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quad = warp & 3, part = warp >> 2;
   const int row = quad * 32 + lane;  // TMEM lane == sample row of the tile
+  const int fiw = (int)m.issue_warp_fwd;  // the MMA-issuing warp
   if (warp == 0) tc::tmem_alloc(&sm.tslot, 256);
   if (tid == 0) {
     tc::mbar_init(&sm.mbar, 1);
@@ -536,7 +549,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
       const bool store_mask = masks != nullptr && valid;
       to_mma();
       // ---- L1: H1 = relu(X Wd0^T + b) ----
-      ISSUE(gemm_ts32<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
+      ISSUE_W(fiw, gemm_ts32<64, 32>(tmem, a_op, sm.w.d0[0], sm.w.d0[1]));
       if (part == 1) {  // Cin columns 16-47 (SH1..15, appearance) of this tile's row -> smem
         float* cs = sm.cin_s + row * kCinS;
         float c[16];
@@ -586,7 +599,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
       }
       to_mma();
       // ---- L2: raw16 = H1 Wd1^T + b ; Cin = [clip(raw1..15) | SH16 | app | 0] ----
-      ISSUE(gemm_ts32<16, 64>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]));
+      ISSUE_W(fiw, gemm_ts32<16, 64>(tmem, a_op, sm.w.d1[0], sm.w.d1[1]));
       mma_done();
       uint32_t clip_bits = 0;
       {
@@ -628,7 +641,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
       pf.rec(m, part);  // next tile's RayRec (item arrived during L1/L2)
       to_mma();
       // ---- L3: C1 = act(Cin Wc0^T + b) ----
-      ISSUE(gemm_ts32<64, 48>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]));
+      ISSUE_W(fiw, gemm_ts32<64, 48>(tmem, a_op, sm.w.c0[0], sm.w.c0[1]));
       mma_done();
       {
         uint32_t bits = 0;
@@ -651,7 +664,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
       }
       to_mma();
       // ---- L4: C2 = act(C1 Wc1^T + b) ----
-      ISSUE(gemm_ts32<64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]));
+      ISSUE_W(fiw, gemm_ts32<64, 64>(tmem, a_op, sm.w.c1[0], sm.w.c1[1]));
       mma_done();
       {
         uint32_t bits = 0;
@@ -670,7 +683,7 @@ __global__ void __launch_bounds__(NTF, MLP_FWD_MINB) k_mlp_fwd_tc(MlpLaunch m) {
       }
       to_mma();
       // ---- L5: rgb = sigmoid(clip(C2 Wc2^T + b)) ----
-      ISSUE(gemm_ts32<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
+      ISSUE_W(fiw, gemm_ts32<16, 64>(tmem, a_op, sm.w.c2[0], sm.w.c2[1]));
       mma_done();
       if (part == 0) {
         float v[16];

@@ -154,6 +154,7 @@ struct dg_ctx {
   uint32_t bwd_cta_mul = 7919;             // encode backward CTA visiting stride (DG_ENC_BWD_STRIDE)
   bool mlp_bwd_paired = true;              // ReLU fields take k_mlp_bwd_tc_relu (DG_MLP_BWD_SERIAL=1: off)
   uint32_t mlp_issue_warp = 8;             // k_mlp_bwd_tc_relu's MMA-issuing warp (DG_MLP_ISSUE_WARP)
+  uint32_t mlp_issue_warp_fwd = 0;         // k_mlp_fwd_tc's (DG_MLP_FWD_ISSUE_WARP)
   bool ordered = false;                    // the last front half ordered its samples
   DBuf s_perm, s_inv, s_p_alt, s_item_ord, s_grad_ord, s_out_ord, ord_scratch, ord_tmp;
   double enc_agg_samples_per_cell = 1.5;   // warp-aggregate levels with >= this many samples/cell (DG_ENC_AGG)
@@ -1051,6 +1052,7 @@ MlpLaunch mlp_launch(dg_ctx* c, bool bwd) {
     if (f + 1 == nl && !bwd && c->mlp_bwd_paired) m.relu_tiles = tiles;  // fields 0..nl-1: fine (ReLU)
   }
   m.issue_warp = c->mlp_issue_warp;
+  m.issue_warp_fwd = c->mlp_issue_warp_fwd;
   m.tile_off = bwd ? c->tile_off_b.as<uint32_t>() : c->tile_off_f.as<uint32_t>();
   m.n_tiles = tiles;
   m.X = c->s_X.as<float>();
@@ -1431,6 +1433,7 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   if (const char* e = std::getenv("DG_ENC_BWD_STRIDE")) c->bwd_cta_mul = uint32_t(std::strtoul(e, nullptr, 10));
   if (const char* e = std::getenv("DG_MLP_BWD_SERIAL")) c->mlp_bwd_paired = std::strcmp(e, "0") == 0;
   if (const char* e = std::getenv("DG_MLP_ISSUE_WARP")) c->mlp_issue_warp = uint32_t(std::strtoul(e, nullptr, 10)) % 16u;
+  if (const char* e = std::getenv("DG_MLP_FWD_ISSUE_WARP")) c->mlp_issue_warp_fwd = uint32_t(std::strtoul(e, nullptr, 10)) % 8u;
   if (const char* e = std::getenv("DG_ENC_AGG")) c->enc_agg_samples_per_cell = std::max(0.01, std::atof(e));
   if (const char* e = std::getenv("DG_ENC_BWD_MB"))
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
@@ -2439,6 +2442,7 @@ static int field_stage(dg_ctx* c, uint32_t p, uint32_t cascade, const double* po
   m.dX = dX.as<float>();
   m.relu_tiles = cascade == 0 && c->mlp_bwd_paired ? m.n_tiles : 0u;  // the fine field: ReLU units
   m.issue_warp = c->mlp_issue_warp;
+  m.issue_warp_fwd = c->mlp_issue_warp_fwd;
   if (c->mlp_impl) launch_mlp_bwd_tc(m, c->num_sms, s);
   else launch_mlp_bwd(m, c->num_sms, s);
   launch_encode_points_bwd(fd, c->grads.as<float>(), pts.as<double>(), dX.as<float>(), n, c->cfg.grid_levels, s);
