@@ -147,7 +147,7 @@ struct dg_ctx {
   uint64_t enc_budget_bwd = 96ull << 20;
   uint64_t enc_group_fwd = 0, enc_group_bwd = 0;  // level-grouping budgets (0: = slice budget)
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
-  int sample_order = 1;                    // spatial sample order: 1 when a level table > 64 MB,
+  int sample_order = 1;                    // spatial sample order: 1 when a field's tables > 64 MB,
                                            // 0 never, 2 always (DG_SAMPLE_ORDER)
   uint32_t order_bits = 8;                 // Morton cells per axis = 2^order_bits (DG_ORDER_BITS)
   uint32_t order_chunk = 8;                // samples per sorted chunk (DG_ORDER_CHUNK)
@@ -669,13 +669,18 @@ __global__ void k_block_permute(const uint64_t* __restrict__ src, uint64_t* __re
 int order_samples(dg_ctx* c, uint64_t NS, cudaStream_t s) {
   c->ordered = false;
   if (!c->sample_order || !c->enc_pcache || !NS) return DG_OK;
-  // Only when a level table outgrows what random accesses keep L2-resident (~75 MB on this
-  // B200, tools/ubench/l2_curve.cu): with small tables (C1: 4 MB per level) every gather hits
-  // L2 in march order already and the sort would be pure overhead.  DG_SAMPLE_ORDER=2 forces it.
+  // Only when a field's level tables outgrow what random accesses keep L2-resident (~75 MB on
+  // this B200, tools/ubench/l2_curve.cu; the encode passes group levels up to 192 / 96 MB): with
+  // small tables (C1: 4 MB per level, ~40 MB per field) every gather hits L2 in march order
+  // already and the sort would be pure overhead; C2 (32 MB per level, ~0.3 GB per field) gains
+  // 4.56 -> 5.31 M training and 12.3 -> 17.2 M render rays/s.  DG_SAMPLE_ORDER=2 forces it.
   if (c->sample_order == 1) {
     uint64_t big = 0;
-    for (const FieldDesc& fd : c->fields)
-      for (uint32_t l = 0; l < fd.L; ++l) big = std::max<uint64_t>(big, uint64_t(fd.lv[l].rows) * 8);
+    for (const FieldDesc& fd : c->fields) {
+      uint64_t field_bytes = 0;
+      for (uint32_t l = 0; l < fd.L; ++l) field_bytes += uint64_t(fd.lv[l].rows) * 8;
+      big = std::max(big, field_bytes);
+    }
     if (big < (64ull << 20)) return DG_OK;
   }
   const uint32_t C = c->order_chunk;
