@@ -146,6 +146,8 @@ struct dg_ctx {
   uint64_t enc_budget_fwd = 192ull << 20;  // encode pass budgets (DG_ENC_FWD_MB / DG_ENC_BWD_MB)
   uint64_t enc_budget_bwd = 96ull << 20;
   uint64_t enc_group_fwd = 0, enc_group_bwd = 0;  // level-grouping budgets (0: = slice budget)
+  uint64_t enc_hgroup_fwd = 64ull << 20;   // forward grouping budget of passes with a hashed level
+                                           // (DG_ENC_FWD_HGROUP_MB; 0: the grouping budget)
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
   int sample_order = 1;                    // spatial sample order: 1 when a field's tables > 64 MB,
                                            // 0 never, 2 always (DG_SAMPLE_ORDER)
@@ -967,7 +969,8 @@ int pairs_expand(dg_ctx* c, cudaStream_t s) {
   return DG_OK;
 }
 
-FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passes, uint64_t group) {
+FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passes, uint64_t group,
+                         uint64_t hgroup) {
   if (!group) group = budget;
   FieldLaunch f{};
   f.fields = c->d_fields.as<FieldDesc>();
@@ -999,11 +1002,30 @@ FieldLaunch field_launch(dg_ctx* c, uint64_t budget, std::vector<EncPass>& passe
       for (const FieldDesc& fd : c->fields) b += uint64_t(fd.lv[l].rows) * 8;
       return b;
     };
+    // a pass holding a hashed level groups up to hgroup bytes (if set): a hashed level's
+    // gathers are random over its whole table, so several of them in one pass thrash L2 (C2:
+    // 32 MB levels, six to a 192 MB pass), while the one-to-one levels' gathers follow the
+    // sample order and group well up to the budget (C4: levels 0-8, 118 MB, in one pass)
+    // (hashed tables of a few MB, e.g. the coarse field's, stay L2-resident and do not count)
+    auto big_hashed = [](const LevelDesc& lv) { return lv.hashed && uint64_t(lv.rows) * 8 >= (8ull << 20); };
+    auto level_hashed = [&](uint32_t l) {
+      if (!merged) return big_hashed(c->fields[fi].lv[l]);
+      for (const FieldDesc& fd : c->fields)
+        if (big_hashed(fd.lv[l])) return true;
+      return false;
+    };
     for (uint32_t l = 0; l < f.levels;) {
       uint32_t l1 = l + 1;
       uint64_t bytes = level_bytes(l);
       const uint64_t gb = std::min(group, budget);  // a sliced pass is always a single level
-      while (l1 < f.levels && bytes + level_bytes(l1) <= gb) bytes += level_bytes(l1++);
+      bool any_hashed = level_hashed(l);
+      while (l1 < f.levels) {
+        const bool h = any_hashed || level_hashed(l1);
+        const uint64_t lim = h && hgroup ? std::min(gb, hgroup) : gb;
+        if (bytes + level_bytes(l1) > lim) break;
+        any_hashed = h;
+        bytes += level_bytes(l1++);
+      }
       const uint32_t S = std::min<uint64_t>(64, std::max<uint64_t>(1, (bytes + budget - 1) / budget));
       for (uint32_t k = 0; k < S; ++k) {
         EncPass ps{uint8_t(l), uint8_t(l1), uint8_t(k), uint8_t(S), merged ? kAllFields : uint8_t(fi), 0, 0, 0,
@@ -1443,6 +1465,7 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
   if (const char* e = std::getenv("DG_ENC_BWD_MB"))
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   if (const char* e = std::getenv("DG_ENC_FWD_GROUP_MB")) c->enc_group_fwd = std::strtoull(e, nullptr, 10) << 20;
+  if (const char* e = std::getenv("DG_ENC_FWD_HGROUP_MB")) c->enc_hgroup_fwd = std::strtoull(e, nullptr, 10) << 20;
   if (const char* e = std::getenv("DG_ENC_BWD_GROUP_MB")) c->enc_group_bwd = std::strtoull(e, nullptr, 10) << 20;
   // the step stream at the highest priority, the side-stream Adam at the lowest: the next
   // step's front half takes SMs ahead of the update's remaining CTAs
@@ -1878,7 +1901,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
     TRY(order_after_adam(c));
     TRY(pairs_expand(c, s));
     std::vector<EncPass> passes;
-    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd);
+    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd, c->enc_hgroup_fwd);
     c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
   }
   mark(c, 3);
@@ -1924,7 +1947,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   mark(c, 8);
   {
     std::vector<EncPass> passes;
-    FieldLaunch fl = field_launch(c, c->enc_budget_bwd, passes, c->enc_group_bwd);
+    FieldLaunch fl = field_launch(c, c->enc_budget_bwd, passes, c->enc_group_bwd, 0);
     if (c->ordered && c->bwd_cta_mul) {  // a CTA stride coprime with the CTA count along x
       uint64_t nb = 0;
       for (const EncPass& p : passes)
@@ -2039,7 +2062,7 @@ int dg_render(dg_ctx* c, const dg_ray_batch* b, const float* appearance, dg_merg
   {
     TRY(pairs_expand(c, s));
     std::vector<EncPass> passes;
-    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd);
+    const FieldLaunch fl = field_launch(c, c->enc_budget_fwd, passes, c->enc_group_fwd, c->enc_hgroup_fwd);
     c->launches += launch_encode_fwd(fl, passes, sm.X, s) - 1;
   }
   MlpLaunch mf = mlp_launch(c, false);
