@@ -148,6 +148,7 @@ struct dg_ctx {
   uint64_t enc_group_fwd = 0, enc_group_bwd = 0;  // level-grouping budgets (0: = slice budget)
   uint64_t enc_hgroup_fwd = 64ull << 20;   // forward grouping budget of passes with a hashed level
                                            // (DG_ENC_FWD_HGROUP_MB; 0: the grouping budget)
+  uint64_t enc_hgroup_bwd = 32ull << 20;   // the backward's (DG_ENC_BWD_HGROUP_MB)
   bool enc_pcache = true;                  // per-sample position cache (DG_ENC_PCACHE)
   int sample_order = 1;                    // spatial sample order: 1 when a field's tables > 64 MB,
                                            // 0 never, 2 always (DG_SAMPLE_ORDER)
@@ -1466,6 +1467,7 @@ int dg_ctx_create(const dg_run_config* cfg, int device, int rank, int world, dg_
     c->enc_budget_bwd = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) << 20;
   if (const char* e = std::getenv("DG_ENC_FWD_GROUP_MB")) c->enc_group_fwd = std::strtoull(e, nullptr, 10) << 20;
   if (const char* e = std::getenv("DG_ENC_FWD_HGROUP_MB")) c->enc_hgroup_fwd = std::strtoull(e, nullptr, 10) << 20;
+  if (const char* e = std::getenv("DG_ENC_BWD_HGROUP_MB")) c->enc_hgroup_bwd = std::strtoull(e, nullptr, 10) << 20;
   if (const char* e = std::getenv("DG_ENC_BWD_GROUP_MB")) c->enc_group_bwd = std::strtoull(e, nullptr, 10) << 20;
   // the step stream at the highest priority, the side-stream Adam at the lowest: the next
   // step's front half takes SMs ahead of the update's remaining CTAs
@@ -1947,7 +1949,7 @@ int dg_train_step(dg_ctx* c, const dg_ray_batch* b, uint64_t step, dg_step_stats
   mark(c, 8);
   {
     std::vector<EncPass> passes;
-    FieldLaunch fl = field_launch(c, c->enc_budget_bwd, passes, c->enc_group_bwd, 0);
+    FieldLaunch fl = field_launch(c, c->enc_budget_bwd, passes, c->enc_group_bwd, c->enc_hgroup_bwd);
     if (c->ordered && c->bwd_cta_mul) {  // a CTA stride coprime with the CTA count along x
       uint64_t nb = 0;
       for (const EncPass& p : passes)
