@@ -432,7 +432,7 @@ class Runner:
         self.barrier()
         return self.max_over_ranks(e0.elapsed_time(e1))
 
-    def render_rate(self, batches, steps):
+    def render_rate(self, batches, steps, warmup=3):
         torch, abi = self.torch, self.abi
         m = abi.Merged()
         out = [torch.empty(x, device="cuda") for x in ((self.shard, 3), (self.shard,), (self.shard,))]
@@ -446,7 +446,8 @@ class Runner:
             if rc != 0:
                 raise self.dg.DGError(rc, self.dg.lib().dg_last_error().decode())
 
-        render(0)
+        for i in range(max(warmup, 1)):
+            render(i)
         l0 = self.ctx.kernel_launches()
         rms = self.timed(render, steps, 0) / steps
         return self.wl.n_rays / (rms / 1000.0), rms, self.ctx.kernel_launches() - l0
@@ -546,10 +547,12 @@ def main():
     config = workload_config(wl, world, cfg.fine_table_log2, "render" if render_only else "train")
 
     if render_only:
-        rv, rms, launches = r.render_rate(dev, max(args.steps, 1))
+        with ClockSampler(local) as clk:
+            rv, rms, launches = r.render_rate(dev, max(args.steps, 1), max(args.warmup, 1))
         if rank == 0:
             print(json.dumps({"metric": METRIC, "value": rv, "unit": "rays/s", "n_gpus": world,
-                              "steps": max(args.steps, 1), "warmup": 1, "ms_per_step": rms,
+                              "steps": max(args.steps, 1), "warmup": max(args.warmup, 1),
+                              "clocks": clk.summary(), "ms_per_step": rms,
                               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                               "dtype": "fp32", "data": "synthetic (random-init grids, corner rays)",
                               "config": config, "gpu_launches": int(launches), "e2e": None,
