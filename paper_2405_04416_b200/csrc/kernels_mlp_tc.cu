@@ -1502,6 +1502,20 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       __syncwarp();
     }
   };
+  // the same with the input-gradient GEMM first (where it is the shorter of the two, so its
+  // epilogue starts while the recompute GEMM runs)
+  auto issue3b = [&](auto fwd, auto bwd, auto back) {
+    if (iw == 0) {
+      if (tc::elect_one()) {
+        bwd();
+        tc::commit(&sm.mbar_b);
+        fwd();
+        tc::commit(&sm.mbar);
+        back();
+      }
+      __syncwarp();
+    }
+  };
   auto issue_b = [&](auto bwd, auto back) {
     if (iw == 0) {
       if (tc::elect_one()) {
@@ -1592,28 +1606,28 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S1: F1 | dC2, + the previous tile's dWd0 ----------------
-      issue3([&] { gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]); },
-             [&] { gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]); },
-             [&] { issue_pending(par ^ 1); });
+      issue3b([&] { gemm_ts<64, 32>(tmem + TF_ACC, aF, sm.w.d0[0], sm.w.d0[1]); },
+              [&] { gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.c2[0], sm.w.c2[1]); },
+              [&] { issue_pending(par ^ 1); });
       pend = false;
       pf.start(m, has_next && row < nx.count, nx.s0 + row, part, false);  // next: X, item
-      done_f();
+      done_b();
       {
         if (part == 0) {  // G5 for dWc2 (the previous tile's dWc2 is done)
           float g[8] = {g5v[0], g5v[1], g5v[2], 0.f, 0.f, 0.f, 0.f, 0.f};
           put8s(sm.g5[0], sm.g5[1], row, 0, g);
         }
         float v[16];
+        ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
+        mask16(v, (mk_c2 >> (((uint32_t)part & 1u) * 16u)) & 0xffffu);
+        put8(bA, row, c16, v);  // G4 (buffer A held the previous tile's C2: dWc2 is done)
+        put8(bA, row, c16 + 8, v + 8);
+        done_f();
         ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bd0[c16 + i], 0.f);
         put8(fH1, row, c16, v);  // the previous tile's dWd1 is done
         put8(fH1, row, c16 + 8, v + 8);
-        done_b();
-        ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
-        mask16(v, (mk_c2 >> (((uint32_t)part & 1u) * 16u)) & 0xffffu);
-        put8(bA, row, c16, v);  // G4 (buffer A held the previous tile's C2: dWc2 is done)
-        put8(bA, row, c16 + 8, v + 8);
       }
       to_mma();
       // ---------------- S2: F2 | dC1 ----------------
@@ -1653,19 +1667,10 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
       }
       to_mma();
       // ---------------- S3: F3 | dCin, + dWc0 ----------------
-      issue3([&] { gemm_ts<64, 48>(tmem + TF_ACC, aF, sm.w.c0[0], sm.w.c0[1]); },
-             [&] { gemm_igrad<64, 16, 64>(tmem + TB_ACC, aB, sm.w.c0[0], sm.w.c0[1]); },
-             [&] { gemm_wgrad_bias<CW, false>(tmem + TD_C0, bufB[0], bufB[1], sm.cin_hi, sm.cin_lo, !fresh); });
+      issue3b([&] { gemm_ts<64, 48>(tmem + TF_ACC, aF, sm.w.c0[0], sm.w.c0[1]); },
+              [&] { gemm_igrad<64, 16, 64>(tmem + TB_ACC, aB, sm.w.c0[0], sm.w.c0[1]); },
+              [&] { gemm_wgrad_bias<CW, false>(tmem + TD_C0, bufB[0], bufB[1], sm.cin_hi, sm.cin_lo, !fresh); });
       pf.appearance(m, m.fields[nx.f], part);  // next tile's appearance rows
-      done_f();
-      {
-        float v[16];
-        ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bc0[c16 + i], 0.f);
-        put8(fC1, row, c16, v);
-        put8(fC1, row, c16 + 8, v + 8);
-      }
       done_b();
       if (part == 3) {  // G2 = [sigma path, clip-masked dCin[0..14]] -> A_B (smem copy at S4)
         float v[16];
@@ -1693,31 +1698,40 @@ __global__ void __launch_bounds__(NTB, 1) k_mlp_bwd_tc_relu(MlpLaunch m, uint32_
           atomicAdd(&sm.bias_c2[2], b2);
         }
       }
+      done_f();
+      {
+        float v[16];
+        ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bc0[c16 + i], 0.f);
+        put8(fC1, row, c16, v);
+        put8(fC1, row, c16 + 8, v + 8);
+      }
       to_mma();
       // ---------------- S4: F4 | dH1, + dWc1 ----------------
-      issue3([&] { gemm_ts<64, 64>(tmem + TF_ACC, aF, sm.w.c1[0], sm.w.c1[1]); },
-             [&] { gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.d1[0], sm.w.d1[1]); },
+      issue3b([&] { gemm_ts<64, 64>(tmem + TF_ACC, aF, sm.w.c1[0], sm.w.c1[1]); },
+              [&] { gemm_igrad<16, 64, 16>(tmem + TB_ACC, aB, sm.w.d1[0], sm.w.d1[1]); },
              [&] { gemm_wgrad_bias<HW, true>(tmem + TB_C1, bufA[0], bufA[1], sm.ones_b, sm.c1_lo, !fresh); });
       pf.grad(m, part);  // next tile's upstream gradient
       uint32_t n_relu, n_c2, n_clip;
       float4 n_o;
       load_fwd(nx, has_next, n_relu, n_c2, n_clip, n_o);
-      done_f();
+      done_b();
       // G2 -> cin tile for dWd1 (dWc0 has read cin), before G1 overwrites its A_B columns
       if (part == 0) a_to_smem16(taB, row, 0, sm.cin_hi, sm.cin_lo);
       {
         float v[16];
+        ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
+        mask16(v, mk_relu & 0xffffu);  // h1 bits
+        put8(bT, row, c16, v);
+        put8(bT, row, c16 + 8, v + 8);
+        done_f();
         ld16(my_lanes + TF_ACC + (uint32_t)c16, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + sm.w.bc1[c16 + i], 0.f);
         // C2 feeds only dWc2 (its smem tile in buffer B: dWc0 has read G3 from it)
         put8s(bufB[0], bufB[1], row, c16, v);
         put8s(bufB[0], bufB[1], row, c16 + 8, v + 8);
-        done_b();
-        ld16(my_lanes + TB_ACC + (uint32_t)c16, v);
-        mask16(v, mk_relu & 0xffffu);  // h1 bits
-        put8(bT, row, c16, v);
-        put8(bT, row, c16 + 8, v + 8);
       }
       to_mma();
       // ---------------- S5: dX, + dWc2, dWd1 ----------------
